@@ -1,0 +1,206 @@
+"""RaDe-GS CPU oracle (fp64) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference`
+legs may import this package. The product path (paper_2406_01467_b200/) never imports
+it and shares no code with it. See oracle/rade_oracle.cpp for what is computed and the
+PAPER.md lines each step follows.
+
+Parity status of each oracle function:
+  project      pinned (tests/test_oracle_pins.py: Σ examples + scipy rotation, Jacobian vs
+               finite differences, Σ′/t* vs brute-force 1D maximisation, isotropic and
+               flattened closed forms, q̂·v′ = 1, centre identity, planarity)
+  sh_basis     pinned (scipy real spherical harmonics with Condon-Shortley phase)
+  splat_eval   pinned (brute-force 1D search; perspective Eq.7 vs isotropic closed form)
+  render       pinned (two opaque layers, single splat, empty scene, Σω + T = 1, median
+               property, tile-free brute force by construction)
+  grad         pinned (central finite differences of render)
+  Constants chosen by convention (readings S1, S5, S6, S8, S14) are parity unpinned
+  against the paper: the paper fixes none of them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "rade_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+PG_STRIDE = 96
+PG = dict(valid=0, zkey=1, x=slice(2, 5), z=5, tc=6, u=7, v=8, Sigma=slice(9, 18), Sc=slice(18, 27),
+          J=slice(27, 36), Sp=slice(36, 45), Spi=slice(45, 54), A2=slice(54, 57), conic=slice(57, 60),
+          qhat=slice(60, 63), q=slice(63, 65), p=slice(65, 67), n=slice(67, 70), rgb=slice(70, 73),
+          rgb_clamped=slice(73, 76), o=76, ndotx=77)
+NPARAM = 59
+
+# default ambiguity bands: F1 α-cutoff, F2 α-clamp (|Δ ln α|),
+# F3 T-stop (relative), F4 median crossing (|T′ − median_T|), F5 grazing |n·x̂_c|
+DEFAULT_EPS = (1e-4, 1e-4, 1e-4, 1e-5, 0.05)
+
+
+def build(force=False):
+    """Compile the oracle (g++ -O2 -fopenmp, no fast-math, no FP contraction)."""
+    if not force and os.path.exists(_LIB) and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC):
+        return _LIB
+    tmp = _LIB + f".tmp{os.getpid()}"
+    cmd = ["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=off",
+           "-fno-fast-math", _SRC, "-o", tmp]
+    subprocess.check_call(cmd)
+    os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            dp = ctypes.POINTER(ctypes.c_double)
+            i64 = ctypes.c_int64
+            common = [i64, dp, dp, dp, dp, dp, ctypes.c_int, dp, dp]
+            L.or_project.argtypes = common + [dp]
+            L.or_splat_eval.argtypes = common + [i64, i64, dp, dp]
+            L.or_render.argtypes = common + [i64, ctypes.c_void_p, dp, dp, dp, dp, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p]
+            L.or_grad.argtypes = common + [dp, i64, ctypes.c_void_p, dp]
+            L.or_sh_basis.argtypes = [dp, dp]
+            L.or_sh_basis.restype = None
+            L.or_num_threads.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _scene_args(scene):
+    means = np.ascontiguousarray(scene.means, np.float64)
+    scales = np.ascontiguousarray(scene.scales, np.float64)
+    rot = np.ascontiguousarray(scene.rotations, np.float64)
+    opac = np.ascontiguousarray(scene.opacities, np.float64)
+    sh = np.ascontiguousarray(scene.sh, np.float64).reshape(scene.sh.shape[0] * 3, scene.n)
+    keep = (means, scales, rot, opac, sh)
+    return keep, [ctypes.c_int64(scene.n), _dp(means), _dp(scales), _dp(rot), _dp(opac), _dp(sh),
+                  ctypes.c_int(int(scene.sh.shape[0]))]
+
+
+def _cam_vec(cam):
+    v = np.zeros(19, np.float64)
+    v[0:6] = [cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height]
+    v[6:15] = np.asarray(cam.R, np.float64).reshape(9)
+    v[15:18] = np.asarray(cam.t, np.float64).reshape(3)
+    v[18] = cam.znear
+    return v
+
+
+def _opt_vec(opt, eps=DEFAULT_EPS):
+    """Options are taken at their fp32 values: both sides see the same float inputs."""
+    f = lambda x: float(np.float32(x))
+    v = np.zeros(14, np.float64)
+    v[0:5] = [f(opt.alpha_min), f(opt.alpha_max), f(opt.T_min), f(opt.median_T), f(opt.dilation)]
+    v[5:8] = [f(b) for b in opt.bg]
+    v[8] = opt.sh_degree
+    v[9:14] = eps
+    return v
+
+
+def _cam_f32(cam):
+    """Camera values as the fp32 numbers the GPU receives."""
+    import copy
+    c = copy.copy(cam)
+    c.fx, c.fy, c.cx, c.cy, c.znear = (float(np.float32(x)) for x in (cam.fx, cam.fy, cam.cx, cam.cy, cam.znear))
+    c.R = np.asarray(cam.R, np.float32)
+    c.t = np.asarray(cam.t, np.float32)
+    return c
+
+
+def project(scene, cam, opt):
+    """Per-Gaussian projection, array [N, 96] indexed by oracle.PG."""
+    keep, sargs = _scene_args(scene)
+    cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt)
+    out = np.zeros((scene.n, PG_STRIDE), np.float64)
+    lib().or_project(*sargs, _dp(cv), _dp(ov), _dp(out))
+    return out
+
+
+def splat_eval(scene, cam, opt, gid, uv):
+    """Per (Gaussian gid, point uv[k]) -> [k, 6]: α_raw, t*_ray, d, t*_persp, depth_persp, power."""
+    keep, sargs = _scene_args(scene)
+    cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt)
+    uv = np.ascontiguousarray(uv, np.float64).reshape(-1, 2)
+    out = np.zeros((uv.shape[0], 6), np.float64)
+    rc = lib().or_splat_eval(*sargs, _dp(cv), _dp(ov), ctypes.c_int64(gid), ctypes.c_int64(uv.shape[0]),
+                             _dp(uv), _dp(out))
+    if rc != 0:
+        raise ValueError(f"splat {gid} culled (rc={rc})")
+    return out
+
+
+def render(scene, cam, opt, pixels=None, eps=DEFAULT_EPS):
+    """Brute-force render. pixels=None: full frame, outputs shaped [C][H][W] / [H][W];
+    else a 1-D array of linear pixel indices, outputs shaped [C][k] / [k]."""
+    keep, sargs = _scene_args(scene)
+    cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt, eps)
+    W, H = cam.width, cam.height
+    if pixels is None:
+        npix, pix = W * H, None
+    else:
+        pix = np.ascontiguousarray(pixels, np.int64)
+        npix = pix.shape[0]
+    color = np.zeros(3 * npix)
+    depth = np.zeros(npix)
+    normal = np.zeros(3 * npix)
+    alpha = np.zeros(npix)
+    flags = np.zeros(npix, np.uint8)
+    nblend = np.zeros(npix, np.int32)
+    mid = np.zeros(npix, np.int64)
+    lib().or_render(*sargs, _dp(cv), _dp(ov), ctypes.c_int64(npix),
+                    None if pix is None else pix.ctypes.data, _dp(color), _dp(depth), _dp(normal),
+                    _dp(alpha), flags.ctypes.data, nblend.ctypes.data, mid.ctypes.data)
+    shape = (H, W) if pixels is None else (npix,)
+    return dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), normal=normal.reshape((3,) + shape),
+                alpha=alpha.reshape(shape), flags=flags.reshape(shape), nblend=nblend.reshape(shape),
+                median_id=mid.reshape(shape))
+
+
+def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS):
+    """Exact dL/dθ for the listed Gaussians, L = Σ_px cot·(C, D, N, A). Returns [len(gids), 59]
+    (μ 0..2, s 3..5, q 6..9, o 10, sh 11 + coeff*3 + ch)."""
+    keep, sargs = _scene_args(scene)
+    cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt, eps)
+    W, H = cam.width, cam.height
+    c = np.zeros((8, H, W), np.float64)
+    c[0:3] = cot["color"]
+    c[3] = cot["depth"]
+    c[4:7] = cot["normal"]
+    c[7] = cot["alpha"]
+    c = np.ascontiguousarray(c)
+    gids = np.ascontiguousarray(gids, np.int64)
+    out = np.zeros((gids.shape[0], NPARAM), np.float64)
+    lib().or_grad(*sargs, _dp(cv), _dp(ov), _dp(c), ctypes.c_int64(gids.shape[0]), gids.ctypes.data, _dp(out))
+    return out
+
+
+def sh_basis(direction):
+    d = np.ascontiguousarray(direction, np.float64)
+    out = np.zeros(16)
+    lib().or_sh_basis(_dp(d), _dp(out))
+    return out
+
+
+def loss(outputs, cot, bg=None):
+    """L = Σ_px cot·(C, D, N, A) from a render() result (fp64)."""
+    return float(np.sum(outputs["color"] * cot["color"]) + np.sum(outputs["depth"] * cot["depth"])
+                 + np.sum(outputs["normal"] * cot["normal"]) + np.sum(outputs["alpha"] * cot["alpha"]))
+
+
+def num_threads():
+    return int(lib().or_num_threads())

@@ -1,0 +1,485 @@
+"""Pins of the fp64 oracle against things other than itself (closed forms, textbook
+identities, library routines for sub-steps, brute force on tiny inputs, SPEC examples).
+
+Each test names the PAPER.md lines of the step it pins. None of these call the CUDA path.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import scenegen as sg
+from helpers import concat, dense_scene, one_gaussian, quat_to_rot_scipy, random_cam
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+OPT = sg.Options()
+
+
+@pytest.fixture(scope="module")
+def O(oracle_lib):
+    return oracle_lib
+
+
+def _pg(O, scene, cam, opt=OPT):
+    return O.project(scene, cam, opt)
+
+
+def _f32cam(cam):
+    return O_cam(cam)
+
+
+def O_cam(cam):
+    import oracle
+    return oracle._cam_f32(cam)
+
+
+# ----------------------------------------------------------------------------- Σ
+
+@pytest.mark.parametrize("case", GOLD["covariance"])
+def test_covariance_golden(O, case):
+    sc = one_gaussian([0, 0, 3], case["scales"], case["quat_wxyz"])
+    pg = _pg(O, sc, sg.camera_identity(32, 32, 32))[0]
+    assert pg[O.PG["valid"]] == 1
+    np.testing.assert_allclose(pg[O.PG["Sigma"]].reshape(3, 3), case["sigma"], atol=1e-7)
+
+
+def test_covariance_vs_scipy_rotation(O):
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        q = rng.normal(size=4) * rng.uniform(0.2, 3.0)  # raw, unnormalised (reading S15)
+        s = np.exp(rng.uniform(-4, 0, 3))
+        sc = one_gaussian([0.1, -0.2, 4.0], s, q)
+        pg = _pg(O, sc, sg.camera_identity(32, 32, 32))[0]
+        qf = sc.rotations[:, 0].astype(np.float64)
+        sf = sc.scales[:, 0].astype(np.float64)
+        R = quat_to_rot_scipy(qf)
+        ref = R @ np.diag(sf ** 2) @ R.T
+        np.testing.assert_allclose(pg[O.PG["Sigma"]].reshape(3, 3), ref, rtol=1e-12, atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- J
+
+def _uvt(cam, x):
+    return np.array([cam.fx * x[0] / x[2] + cam.cx, cam.fy * x[1] / x[2] + cam.cy, np.linalg.norm(x)])
+
+
+def _fd_jac(cam, x, h=1e-6):
+    J = np.zeros((3, 3))
+    for k in range(3):
+        e = np.zeros(3)
+        e[k] = h * max(1.0, abs(x[k]))
+        J[:, k] = (_uvt(cam, x + e) - _uvt(cam, x - e)) / (2 * e[k])
+    return J
+
+
+def test_jacobian_vs_finite_differences(O):
+    rng = np.random.default_rng(1)
+    for _ in range(10):
+        cam = O_cam(random_cam(rng))
+        sc = one_gaussian(rng.normal(scale=0.3, size=3), [0.1, 0.1, 0.1])
+        pg = _pg(O, sc, cam)[0]
+        assert pg[0] == 1
+        x = pg[O.PG["x"]]
+        np.testing.assert_allclose(pg[O.PG["J"]].reshape(3, 3), _fd_jac(cam, x), rtol=1e-7, atol=1e-9)
+        # the pinhole projection itself: (u_c, v_c, t_c) equal the (u, v, t) map at x_c
+        np.testing.assert_allclose([pg[O.PG["u"]], pg[O.PG["v"]], pg[O.PG["tc"]]], _uvt(cam, x), rtol=1e-13)
+
+
+# ----------------------------------------------------------------------------- Σ′, q̂, t*
+
+def _independent_sigma_prime(cam, sc):
+    """Σ′ = J W Σ Wᵀ Jᵀ built from scipy's rotation and a finite-difference J."""
+    q = sc.rotations[:, 0].astype(float)
+    s = sc.scales[:, 0].astype(float)
+    R = quat_to_rot_scipy(q)
+    Sig = R @ np.diag(s ** 2) @ R.T
+    W = np.asarray(cam.R, float)
+    x = W @ sc.means[:, 0].astype(float) + np.asarray(cam.t, float)
+    Sc = W @ Sig @ W.T
+    J = _fd_jac(cam, x)
+    return J @ Sc @ J.T, x, Sc
+
+
+def _argmax_1d(f, lo, hi):
+    """Brute-force maximiser of a 1-D function: dense grid, then golden section."""
+    ts = np.linspace(lo, hi, 20001)
+    vals = f(ts)
+    k = int(np.argmax(vals))
+    a, b = ts[max(k - 1, 0)], ts[min(k + 1, len(ts) - 1)]
+    g = (np.sqrt(5) - 1) / 2
+    for _ in range(200):
+        c, d = b - g * (b - a), a + g * (b - a)
+        if f(np.array([c]))[0] > f(np.array([d]))[0]:
+            b = d
+        else:
+            a = c
+    return 0.5 * (a + b)
+
+
+def test_sigma_prime_and_ray_space_maximum_bruteforce(O):
+    """PAPER:413-416 (Eq.2) and PAPER:497-522 (Eq.9-13): the closed-form t* is the maximiser
+    of the ray-space 1D Gaussian G′¹(t) (Eq.10), checked by brute-force search."""
+    rng = np.random.default_rng(2)
+    for trial in range(6):
+        cam = O_cam(random_cam(rng))
+        flat = [1.0, 0.3, 0.05][trial % 3]
+        sc = one_gaussian(rng.normal(scale=0.3, size=3), np.array([0.2, 0.1, 0.2 * flat]), rng.normal(size=4))
+        pg = _pg(O, sc, cam)[0]
+        assert pg[0] == 1
+        Sp, x, _ = _independent_sigma_prime(cam, sc)
+        np.testing.assert_allclose(pg[O.PG["Sp"]].reshape(3, 3), Sp, rtol=2e-6, atol=1e-9 * np.abs(Sp).max())
+        Spi = np.linalg.inv(Sp)
+        uc = np.array([pg[O.PG["u"]], pg[O.PG["v"]], pg[O.PG["tc"]]])
+        sd = np.sqrt(Sp[2, 2])
+        pts = uc[:2] + rng.normal(scale=2.0, size=(8, 2)) * np.sqrt(np.diag(Sp)[:2])
+        ev = O.splat_eval(sc, cam, OPT, 0, pts)
+        # α = o·exp(−½ Δᵀ (Σ′[0:2,0:2] + hI)⁻¹ Δ) (readings S1, S5)
+        A2 = Sp[:2, :2] + float(np.float32(0.3)) * np.eye(2)
+        dl = uc[:2][None, :] - pts
+        a_ref = float(sc.opacities[0]) * np.exp(-0.5 * np.einsum("ni,ij,nj->n", dl, np.linalg.inv(A2), dl))
+        np.testing.assert_allclose(ev[:, 0], a_ref, rtol=1e-5)
+        for k, (u, v) in enumerate(pts):
+            def G(t):
+                w = np.stack([np.full_like(t, u - uc[0]), np.full_like(t, v - uc[1]), t - uc[2]], 0)
+                return np.exp(-np.einsum("in,ij,jn->n", w, Spi, w))
+            tb = _argmax_1d(G, uc[2] - 30 * sd, uc[2] + 30 * sd)
+            assert abs(ev[k, 1] - tb) <= 1e-6 * uc[2], (ev[k, 1], tb)
+            # Eq.15: d = (z_c/t_c) t*
+            assert abs(ev[k, 2] - pg[O.PG["z"]] / uc[2] * ev[k, 1]) <= 1e-12 * uc[2]
+
+
+def test_conditional_mean_identity(O):
+    """The maximum of a Gaussian along t at fixed (u, v) is the conditional mean
+    t_c + Σ′_{t,uv} Σ′_{uv,uv}⁻¹ (uv − uv_c) (textbook), i.e. q = −Σ′_{uv,uv}⁻¹ Σ′_{uv,t}."""
+    rng = np.random.default_rng(3)
+    for _ in range(10):
+        cam = O_cam(random_cam(rng))
+        sc = one_gaussian(rng.normal(scale=0.3, size=3), np.exp(rng.uniform(-3, -1, 3)), rng.normal(size=4))
+        pg = _pg(O, sc, cam)[0]
+        Sp, _, _ = _independent_sigma_prime(cam, sc)
+        A = Sp[:2, :2]
+        q_ref = -np.linalg.solve(A, Sp[:2, 2])
+        np.testing.assert_allclose(pg[O.PG["q"]], q_ref, rtol=1e-5, atol=1e-9)
+
+
+def test_qhat_normalisation_and_q_p_relation(O):
+    """q̂·v′ = 1, p = (z_c/t_c) q."""
+    rng = np.random.default_rng(4)
+    cam = O_cam(random_cam(rng))
+    sc = dense_scene(4, 50)
+    pg = _pg(O, sc, sg.camera_identity(64, 64, 64))
+    v = pg[:, 0] == 1
+    np.testing.assert_allclose(pg[v, 62], 1.0, rtol=0, atol=1e-15)
+    zt = (pg[v, O.PG["z"]] / pg[v, O.PG["tc"]])[:, None]
+    np.testing.assert_allclose(pg[v][:, O.PG["p"]], zt * pg[v][:, O.PG["q"]], rtol=1e-15)
+
+
+def test_centre_identity_and_planarity(O):
+    """d(u_c, v_c) = z_c (PAPER:535-550 and appendix); the ray-space
+    intersection points lie on the plane (q, 1)·(𝐮 − 𝐮_c) = 0."""
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        cam = O_cam(random_cam(rng))
+        sc = one_gaussian(rng.normal(scale=0.3, size=3), np.exp(rng.uniform(-4, -1, 3)), rng.normal(size=4))
+        pg = _pg(O, sc, cam)[0]
+        uc, vc, tc, z = pg[O.PG["u"]], pg[O.PG["v"]], pg[O.PG["tc"]], pg[O.PG["z"]]
+        ev = O.splat_eval(sc, cam, OPT, 0, [[uc, vc]])
+        assert abs(ev[0, 1] - tc) <= 1e-13 * tc
+        assert abs(ev[0, 2] - z) <= 1e-13 * tc
+        pts = np.array([uc, vc]) + rng.normal(scale=5.0, size=(50, 2))
+        ev = O.splat_eval(sc, cam, OPT, 0, pts)
+        q = pg[O.PG["q"]]
+        res = q[0] * (pts[:, 0] - uc) + q[1] * (pts[:, 1] - vc) + (ev[:, 1] - tc)
+        assert np.abs(res).max() <= 1e-9 * tc
+
+
+# ----------------------------------------------------------------------------- normal
+
+def test_normal_is_conjugate_direction(O):
+    """n = Jᵀ n′ normalised equals −Σ_c⁻¹x_c/‖·‖ (derived: q̂ J ∝ x_cᵀΣ_c⁻¹),
+    computed here from scipy's rotation, independent of J and the intrinsics."""
+    rng = np.random.default_rng(6)
+    for _ in range(20):
+        cam = O_cam(random_cam(rng))
+        sc = one_gaussian(rng.normal(scale=0.3, size=3), np.exp(rng.uniform(-4, -1, 3)), rng.normal(size=4))
+        pg = _pg(O, sc, cam)[0]
+        _, x, Sc = _independent_sigma_prime(cam, sc)
+        m = -np.linalg.solve(Sc, x)
+        m /= np.linalg.norm(m)
+        n = pg[O.PG["n"]]
+        assert np.linalg.norm(n - m) < 1e-8
+        assert np.dot(n, x) < 0  # toward the image plane
+
+
+def test_isotropic_gaussian(O):
+    """Isotropic: Σ′ has v′ as eigenvector ⇒ q = p = 0, d ≡ z_c, n = −x̂_c; at the centre
+    pixel the rasterized depth equals the perspective ray maximum of Eq.7."""
+    g = GOLD["isotropic_on_axis"]
+    sc = one_gaussian(g["mean"], g["scales"])
+    pg = _pg(O, sc, sg.camera_identity(64, 64, 64))[0]
+    np.testing.assert_allclose(pg[O.PG["q"]], g["q"], atol=1e-15)
+    np.testing.assert_allclose(pg[O.PG["p"]], g["p"], atol=1e-15)
+    np.testing.assert_allclose(pg[O.PG["n"]], g["n"], atol=1e-15)
+    rng = np.random.default_rng(7)
+    for _ in range(10):
+        # W = I exactly (an fp32 look-at rotation is orthonormal only to 1e-7, which would
+        # make W Σ Wᵀ slightly anisotropic)
+        cam = sg.Camera(rng.uniform(40, 80), rng.uniform(40, 80), rng.uniform(20, 40), rng.uniform(20, 30), 64, 48,
+                        np.eye(3, dtype=np.float32), np.zeros(3, np.float32), 0.2)
+        s = np.exp(rng.uniform(-4, -1))
+        z = rng.uniform(2, 6)
+        sc = one_gaussian([rng.uniform(-0.4, 0.4) * z, rng.uniform(-0.3, 0.3) * z, z], [s, s, s], rng.normal(size=4))
+        pg = _pg(O, sc, cam)[0]
+        x = pg[O.PG["x"]]
+        assert np.abs(pg[O.PG["q"]]).max() < 1e-12 * pg[O.PG["tc"]]
+        np.testing.assert_allclose(pg[O.PG["n"]], -x / np.linalg.norm(x), atol=1e-12)
+        uc, vc = pg[O.PG["u"]], pg[O.PG["v"]]
+        ev = O.splat_eval(sc, cam, OPT, 0, [[uc, vc], [uc + 3.0, vc - 2.0]])
+        assert abs(ev[0, 4] - pg[O.PG["z"]]) < 1e-12 * pg[O.PG["tc"]]  # perspective depth at centre
+        assert abs(ev[0, 2] - pg[O.PG["z"]]) < 1e-12 * pg[O.PG["tc"]]  # rasterized depth at centre
+        assert abs(ev[1, 2] - pg[O.PG["z"]]) < 1e-12 * pg[O.PG["tc"]]  # d ≡ z_c off-centre too
+
+
+def test_flattened_gaussian_normal_converges_to_splat_normal(O):
+    """As s_min/s_max → 0 the rasterized normal → ±R_c e_min: the angle
+    decreases quadratically with the flatness."""
+    rng = np.random.default_rng(8)
+    for _ in range(5):
+        cam = O_cam(random_cam(rng))
+        q = rng.normal(size=4)
+        mean = rng.normal(scale=0.3, size=3)
+        q32 = q.astype(np.float32).astype(float)  # the value the scene stores
+        Rc = np.asarray(cam.R, float) @ quat_to_rot_scipy(q32 / np.linalg.norm(q32))
+        e = Rc[:, 2]
+        x = np.asarray(cam.R, float) @ mean + np.asarray(cam.t, float)
+        if abs(np.dot(e, x / np.linalg.norm(x))) < 0.3:  # avoid near-grazing splats
+            continue
+        angs = []
+        for eps in (1e-1, 1e-2, 1e-3):
+            sc = one_gaussian(mean, [0.2, 0.15, 0.2 * eps], q)
+            n = _pg(O, sc, cam)[0][O.PG["n"]]
+            angs.append(np.degrees(np.arctan2(np.linalg.norm(np.cross(n, e)), abs(np.dot(n, e)))))
+        assert angs[0] < 5.0 and angs[2] < 1e-3
+        # quadratic convergence: each 10x flatter splat cuts the angle ~100x
+        assert angs[1] < 0.02 * angs[0] and angs[2] < 0.02 * angs[1]
+
+
+# ----------------------------------------------------------------------------- SH
+
+def _real_sh_scipy(l, m, d):
+    from scipy.special import sph_harm_y
+    x, y, z = d
+    theta = np.arccos(np.clip(z, -1, 1))
+    phi = np.arctan2(y, x)
+    Y = sph_harm_y(l, abs(m), theta, phi)  # includes the Condon-Shortley phase
+    if m < 0:
+        return np.sqrt(2) * (-1) ** m * Y.imag
+    if m > 0:
+        return np.sqrt(2) * (-1) ** m * Y.real
+    return Y.real
+
+
+def test_sh_basis_vs_scipy(O):
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        B = O.sh_basis(d)
+        for l in range(4):
+            for m in range(-l, l + 1):
+                # reading S14: 3DGS basis = (−1)^m × standard real SH
+                ref = (-1) ** m * _real_sh_scipy(l, m, d)
+                assert abs(B[l * l + l + m] - ref) < 1e-12, (l, m)
+
+
+def test_sh_degree0_and_zero_dc(O):
+    cam = sg.camera_identity(32, 32, 32)
+    sc0 = one_gaussian([0, 0, 3], [0.1] * 3, dc=(0, 0, 0))
+    np.testing.assert_allclose(_pg(O, sc0, cam)[0][O.PG["rgb"]], GOLD["sh_zero_dc"]["rgb"], atol=0)
+    rgbs = []
+    for mean in ([0, 0, 3], [1, 0.5, 3], [-1, -1, 4]):
+        sc = one_gaussian(mean, [0.1] * 3, dc=(0.7, -0.3, 0.2))
+        rgbs.append(_pg(O, sc, cam, sg.Options(sh_degree=0))[0][O.PG["rgb"]])
+    np.testing.assert_allclose(rgbs[0], rgbs[1], atol=1e-15)
+    np.testing.assert_allclose(rgbs[0], rgbs[2], atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- blending / median
+
+def _empty_scene():
+    return sg.make_scene(np.zeros((3, 0)), np.zeros((3, 0)), np.zeros((4, 0)), np.zeros(0), np.zeros((16, 3, 0)))
+
+
+def test_empty_scene_renders_zeros(O):
+    r = O.render(_empty_scene(), sg.camera_identity(16, 8, 16), OPT)
+    for k in ("color", "depth", "normal", "alpha"):
+        assert np.all(r[k] == 0)
+
+
+@pytest.mark.parametrize("case", GOLD["alpha_at_centre"]["cases"])
+def test_single_splat_at_centre(O, case):
+    """Pixel whose centre is the splat centre: C = c·min(o, α_max)."""
+    cam = sg.camera_identity(64, 64, 64)
+    z = 3.0
+    # u_c = fx x/z + cx = 20.5 (centre of pixel 20), v_c = 40.5
+    mean = [(20.5 - 32) * z / 64, (40.5 - 32) * z / 64, z]
+    sc = one_gaussian(mean, [0.1, 0.08, 0.12], [0.9, 0.1, -0.2, 0.3], opacity=case["opacity"])
+    pg = _pg(O, sc, cam)[0]
+    r = O.render(sc, cam, OPT)
+    a = case["alpha"]
+    np.testing.assert_allclose(r["alpha"][40, 20], a, rtol=1e-7)
+    np.testing.assert_allclose(r["color"][:, 40, 20], a * pg[O.PG["rgb"]], rtol=1e-7)
+    np.testing.assert_allclose(r["normal"][:, 40, 20], a * pg[O.PG["n"]], rtol=1e-7, atol=1e-12)
+    if a > 0.5:
+        np.testing.assert_allclose(r["depth"][40, 20], pg[O.PG["z"]], rtol=1e-12)
+
+
+def test_two_opaque_layers_median(O):
+    """Median depth (reading S9) selects, not averages: with fronto-parallel flat
+    splats on the principal axis (q = 0 ⇒ d = z_c), D = 2.0 where α₁ > 0.5 and 3.0 where
+    only the two together cross 0.5."""
+    g = GOLD["two_opaque_layers"]
+    cam = sg.camera_identity(64, 64, 64)
+    o = g["opacity"]
+    front = one_gaussian([0, 0, g["front_depth"]], [0.15, 0.15, 1e-3], opacity=o)
+    back = one_gaussian([0, 0, g["back_depth"]], [0.6, 0.6, 1e-3], opacity=o)
+    sc = concat(front, back)
+    pg = _pg(O, sc, cam)
+    np.testing.assert_allclose(pg[:, 63:67], 0.0, atol=1e-15)  # q = p = 0
+    r = O.render(sc, cam, OPT)
+    D = r["depth"]
+    assert abs(D[32, 32] - g["median_at_centre"]) < 1e-12
+    # analytic α of an isotropic screen Gaussian: σ² = (f s / z)² + h
+    ii, jj = np.meshgrid(np.arange(64) + 0.5, np.arange(64) + 0.5)
+    r2 = (ii - 32) ** 2 + (jj - 32) ** 2
+    s1, s2 = float(front.scales[0, 0]), float(back.scales[0, 0])
+    h = float(np.float32(0.3))
+    a1 = np.minimum(0.99, o * np.exp(-0.5 * r2 / ((64 * s1 / 2.0) ** 2 + h)))
+    a2 = np.minimum(0.99, o * np.exp(-0.5 * r2 / ((64 * s2 / 3.0) ** 2 + h)))
+    a1 = np.where(a1 >= 1 / 255, a1, 0.0)
+    a2 = np.where(a2 >= 1 / 255, a2, 0.0)
+    T1 = 1 - a1
+    T2 = T1 * (1 - a2)
+    expect = np.where(T1 <= 0.5, 2.0, np.where(T2 <= 0.5, 3.0, 0.0))
+    ok = (np.abs(T1 - 0.5) > 1e-6) & (np.abs(T2 - 0.5) > 1e-6)
+    np.testing.assert_allclose(D[ok], expect[ok], rtol=0, atol=1e-12)
+    assert (expect == 3.0).sum() > 20 and (expect == 2.0).sum() > 20
+    mean_depth = (2.0 * 0.99 + 3.0 * 0.01 * 0.99) / (0.99 + 0.0099)
+    assert abs(mean_depth - g["expected_depth_at_centre_if_mean"]) < 1e-4
+
+
+def test_weights_sum_identity_and_median_property(O):
+    """Σω + T_final = 1 (telescoping Eq.3): with every colour = 1 and bg = 0
+    the colour channel equals α = 1 − T. When D ≠ 0 it equals d (Eq.15) of exactly the
+    median splat at that pixel."""
+    sc = dense_scene(10, 300)
+    sc.sh[:] = 0
+    sc.sh[0] = 0.5 / 0.28209479177387814  # rgb = 1
+    cam = sg.camera_identity(64, 64, 64)
+    r = O.render(sc, cam, OPT)
+    for c in range(3):
+        np.testing.assert_allclose(r["color"][c], r["alpha"], atol=1e-12)
+    assert r["nblend"].mean() > 3
+    ys, xs = np.nonzero(r["depth"])
+    assert len(ys) > 100
+    rng = np.random.default_rng(0)
+    for k in rng.choice(len(ys), 40, replace=False):
+        y, x = ys[k], xs[k]
+        gid = int(r["median_id"][y, x])
+        ev = O.splat_eval(sc, cam, OPT, gid, [[x + 0.5, y + 0.5]])
+        assert ev[0, 2] == pytest.approx(r["depth"][y, x], rel=1e-13)
+
+
+def test_tile_free_subset_render_matches_full(O):
+    """Rendering a pixel subset gives the same values as the full frame (pure per-pixel
+    definition; no tiling anywhere in the oracle)."""
+    sc = dense_scene(11, 120)
+    cam = sg.camera_identity(64, 64, 64)
+    full = O.render(sc, cam, OPT)
+    pix = np.array([0, 5, 64 * 10 + 3, 64 * 63 + 63, 2000])
+    sub = O.render(sc, cam, OPT, pixels=pix)
+    for k in ("color", "normal"):
+        np.testing.assert_array_equal(sub[k], full[k].reshape(3, -1)[:, pix])
+    for k in ("depth", "alpha", "flags", "nblend"):
+        np.testing.assert_array_equal(sub[k], full[k].reshape(-1)[pix])
+
+
+# ----------------------------------------------------------------------------- gradients
+
+def _loss(O, sc, cam, cot, opt=OPT):
+    return O.loss(O.render(sc, cam, opt), cot)
+
+
+def _set_param(sc, j, gid, value):
+    if j < 3:
+        sc.means[j, gid] = value
+    elif j < 6:
+        sc.scales[j - 3, gid] = value
+    elif j < 10:
+        sc.rotations[j - 6, gid] = value
+    elif j == 10:
+        sc.opacities[gid] = value
+    else:
+        k = j - 11
+        sc.sh[k // 3, k % 3, gid] = value
+
+
+def _get_param(sc, j, gid):
+    if j < 3:
+        return sc.means[j, gid]
+    if j < 6:
+        return sc.scales[j - 3, gid]
+    if j < 10:
+        return sc.rotations[j - 6, gid]
+    if j == 10:
+        return sc.opacities[gid]
+    k = j - 11
+    return sc.sh[k // 3, k % 3, gid]
+
+
+def _double_scene(sc):
+    d = sc.copy()
+    for k in ("means", "scales", "rotations", "opacities", "sh"):
+        setattr(d, k, getattr(d, k).astype(np.float64))
+    return d
+
+
+def test_dual_gradient_vs_central_fd(O):
+    """The oracle's forward-mode dual gradient equals central finite differences of its own
+    render, away from the flagged kinks."""
+    sc = _double_scene(dense_scene(12, 40, smin=0.05))
+    cam = sg.camera_identity(48, 48, 48)
+    cot = sg.cotangents(3, 48, 48)
+    r = O.render(sc, cam, OPT)
+    m = r["flags"] == 0
+    for k in cot:
+        cot[k] = cot[k] * m
+    pg = _pg(O, sc, cam)
+    cand = [i for i in range(sc.n) if pg[i, 0] == 1 and not pg[i, 73:76].any()]
+    gids = np.array(cand[:4])
+    G = O.grad(sc, cam, OPT, cot, gids)
+    params = list(range(11)) + [11, 13, 14, 16, 30, 58]
+    checked = 0
+    for gk, gid in enumerate(gids):
+        for j in params:
+            x0 = _get_param(sc, j, gid)
+            h = 1e-6 * max(abs(x0), 0.05)
+            _set_param(sc, j, gid, x0 + h)
+            Lp = _loss(O, sc, cam, cot)
+            _set_param(sc, j, gid, x0 - h)
+            Lm = _loss(O, sc, cam, cot)
+            _set_param(sc, j, gid, x0)
+            fd = (Lp - Lm) / (2 * h)
+            scale = max(abs(G[gk, j]), 1e-3 * np.abs(G[gk]).max(), 1e-6)
+            assert abs(fd - G[gk, j]) <= 2e-5 * scale + 1e-7, (gid, j, fd, G[gk, j])
+            checked += 1
+    assert checked > 50
+
+
+def test_zero_cotangent_gives_zero_gradient(O):
+    sc = dense_scene(13, 30)
+    cam = sg.camera_identity(32, 32, 32)
+    z = {k: np.zeros_like(v) for k, v in sg.cotangents(0, 32, 32).items()}
+    G = O.grad(sc, cam, OPT, z, np.arange(30))
+    assert np.all(G == 0)
