@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""Benchmark of the RaDe-GS rasterizer hot path on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--views-per-step B]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...        # the fp64 CPU oracle arm (rank 0 only)
+
+A step = B views per rank, each view one pass of the whole hot path:
+rd_preprocess → rd_bin → rd_render_fwd → rd_render_bwd (gradients accumulated into one
+flat buffer), then — for N > 1 — one NCCL all-reduce (sum) of the flat gradient buffer
+(the only exchange step, §8(e)). Views are partitioned across ranks (v mod N = rank) with
+the Gaussians replicated: weak scaling. `value` = views processed by all ranks / the max
+over ranks of the device-timed region (CUDA events, barrier + synchronize on both sides).
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd frames/sec (color+depth+normal)"
+UNIT = "frames/s"
+SEED_COT = 1000
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- roofline model
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    hbm = d.get("hbm_gbs", 6650.0)
+    src = "measured" if "hbm_gbs" in d else "fallback"
+    sm_mhz = d.get("sm_max_mhz", 1965.0)
+    return hbm, src, sm_mhz
+
+
+def fp32_peak_tflops(n_sm, sm_mhz):
+    """FFMA peak: SMs × 128 FP32 lanes × 2 flop × clock."""
+    return n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+# algorithmic work per unit
+FWD_FLOP_EVAL, FWD_FLOP_BLEND = 12, 15     # K3: per evaluated pair / extra per blended pair
+BWD_FLOP_EVAL, BWD_FLOP_BLEND = 12, 80     # K4: per evaluated pair / extra per blended pair
+K1_B_ALL, K1_B_VIS = 20, 296               # K1: cull read (means + opacity + touched) / visible
+K5_B_ALL, K5_B_VIS = 4, 772                # K5: touched / params 236 + g2d 64 + grads RMW 472
+
+
+def kernel_work(name, t, views, key_bits):
+    """Algorithmic (bytes or flops, bound) summed over the timed views for one kernel."""
+    n, nvis, M = t["n"], t["n_visible"], t["n_duplicates"]
+    if name == "preprocess_fwd":
+        return K1_B_ALL * n * views + K1_B_VIS * nvis, "hbm"
+    if name == "scan":
+        return 8 * n * views, "hbm"
+    if name == "duplicate":
+        return (4 * n) * views + 12 * nvis + 12 * M, "hbm"
+    if name == "sort":
+        return 24 * M * math.ceil(key_bits / 8), "hbm"
+    if name == "ranges":
+        return 8 * M, "hbm"
+    if name == "render_fwd":
+        return FWD_FLOP_EVAL * t["pairs_evaluated_fwd"] + FWD_FLOP_BLEND * t["pairs_blended_fwd"], "alu"
+    if name == "memset_g2d":
+        return 64 * n * views, "hbm"
+    if name == "render_bwd":
+        return BWD_FLOP_EVAL * t["pairs_evaluated_bwd"] + BWD_FLOP_BLEND * t["pairs_blended_fwd"], "alu"
+    if name == "preprocess_bwd":
+        return K5_B_ALL * n * views + K5_B_VIS * nvis, "hbm"
+    raise KeyError(name)
+
+
+# ----------------------------------------------------------------------------- distributed
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def barrier(dist_on):
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, dist_on, device):
+    if not dist_on:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- CPU oracle arm
+
+
+def oracle_frame_time(scene, cam, opt, n_pix=16, n_grad=1, seed=0):
+    """Times the oracle as it stands on a bounded sample of one view: the forward on n_pix
+    random pixels and the dual-number gradient of n_grad random visible Gaussians; returns
+    (seconds per full frame fwd+bwd extrapolated, description, cores)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    W, H = cam.width, cam.height
+    pix = rng.choice(W * H, n_pix, replace=False)
+    tf = np.zeros(3)
+    oracle.render(scene, cam, opt, pixels=pix, timing=tf)
+    n_vis = int(tf[2])
+    # pick visible (in-front, near-centre) Gaussians with small footprints as the gradient sample
+    x = (np.asarray(cam.R, np.float64) @ scene.means.astype(np.float64) + np.asarray(cam.t, np.float64)[:, None])
+    z = x[2]
+    u = cam.fx * x[0] / np.maximum(z, 1e-6) + cam.cx
+    v = cam.fy * x[1] / np.maximum(z, 1e-6) + cam.cy
+    ok = (z > 0.5) & (u > 0) & (u < W) & (v > 0) & (v < H) & (scene.opacities > 0.05)
+    cand = np.nonzero(ok)[0]
+    gids = rng.choice(cand, min(n_grad, len(cand)), replace=False) if len(cand) else np.zeros(0, np.int64)
+    cot = {"color": np.zeros((3, H, W)), "depth": np.zeros((H, W)), "normal": np.zeros((3, H, W)),
+           "alpha": np.zeros((H, W))}
+    r = np.random.default_rng(seed + 1)
+    cot["color"][:] = r.normal(size=(3, H, W))
+    cot["depth"][:] = r.normal(size=(H, W))
+    tg = np.zeros(3)
+    if len(gids):
+        oracle.grad(scene, cam, opt, cot, gids, timing=tg)
+    t_fwd = tf[0] + tf[1] * (W * H / n_pix)
+    t_bwd = tg[0] + tg[1] * (n_vis / max(len(gids), 1))
+    desc = (f"one view of the workload: fp64 forward on {n_pix} random pixels (of {W * H}) + dual-number gradient "
+            f"of {len(gids)} visible Gaussian(s) (of {n_vis}), extrapolated to the full frame; "
+            f"measured {tf[0] + tf[1] + tg[0] + tg[1]:.1f} s")
+    return t_fwd + t_bwd, desc, oracle.num_threads(), tf[0] + tf[1] + tg[0] + tg[1]
+
+
+def run_reference(args, cfg_name, config):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import scenegen as sg
+    oracle.build()
+    scene, cams, opt = sg.config_scene_and_cameras(cfg_name, n_gaussians=args.n_gaussians)
+    times, desc, cores = [], "", 1
+    for step in range(args.warmup + args.steps):
+        cam = cams[step % len(cams)]
+        t, desc, cores, _ = oracle_frame_time(scene, cam, opt, n_pix=args.ref_pixels, n_grad=1, seed=step)
+        if step >= args.warmup:
+            times.append(t)
+    frame_s = float(np.mean(times))
+    value = 1.0 / frame_s
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": frame_s * 1e3 * args.views_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"each step: {desc}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def run_gpu(args, cfg_name, config):
+    import torch
+    import paper_2406_01467_b200 as P
+    import scenegen as sg
+
+    ws, rank, local = dist_env()
+    dist_on = ws > 1
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+
+    scene, cams, opt = sg.config_scene_and_cameras(cfg_name, n_gaussians=args.n_gaussians)
+    n = scene.n
+    my_views = [cams[v] for v in range(len(cams)) if v % ws == rank]
+    B = args.views_per_step
+    g = P.Gaussians.from_numpy(scene, device)
+    K = g.sh.shape[0]
+    flat = torch.zeros(n * (3 + 3 + 4 + 1 + 3 * K), dtype=torch.float32, device=device)
+    o = 0
+    parts = []
+    for shp in ((3, n), (3, n), (4, n), (n,), (K, 3, n)):
+        c = int(np.prod(shp))
+        parts.append(flat[o:o + c].view(*shp))
+        o += c
+    grads = P.Gaussians(*parts)
+    H, W = cams[0].height, cams[0].width
+    n_ring = min(B * 2, 8)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(SEED_COT + rank)
+    cots = [torch.randn((8, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
+    opts = dict(tile=opt.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
+                median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
+    view = P.View(device)
+    outs = {"color": torch.empty((3, H, W), device=device), "depth": torch.empty((H, W), device=device),
+            "normal": torch.empty((3, H, W), device=device), "alpha": torch.empty((H, W), device=device)}
+    counter = {"v": 0}
+
+    def one_view(cam, cot):
+        P.rd_preprocess(view, g, cam, opts)
+        P.rd_bin(view)
+        P.rd_render_fwd(view, outs["color"], outs["depth"], outs["normal"], outs["alpha"])
+        P.rd_render_bwd(view, g, cot[0:3], cot[3], cot[4:7], cot[7], grads)
+
+    def step():
+        flat.zero_()
+        for b in range(B):
+            k = counter["v"]
+            counter["v"] += 1
+            one_view(my_views[k % len(my_views)], cots[k % n_ring])
+        if dist_on:
+            import torch.distributed as dist
+            dist.all_reduce(flat)
+
+    # ---------------- device-resident timed region
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    P.rd_set_profiling(view, True)
+    clocks = ClockSampler(local)
+    barrier(dist_on)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(dist_on)
+    clk = clocks.stop()
+    elapsed_ms = max_over_ranks(e0.elapsed_time(e1), dist_on, device)
+    tim = P.rd_get_timings(view, reset=True)
+    P.rd_set_profiling(view, False)
+    total_views = args.steps * B * ws
+    value = total_views / (elapsed_ms / 1e3)
+
+    # ---------------- end-to-end: host cotangents in (pinned), rendered maps out, per step
+    e2e = None
+    if not args.no_e2e:
+        host_cots = [c.cpu().pin_memory() for c in cots]
+        host_out = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in outs.items()}
+        dev_cot = torch.empty((8, H, W), device=device)
+        h2d = 0
+        d2h = 0
+
+        def step_e2e():
+            nonlocal h2d, d2h
+            flat.zero_()
+            for b in range(B):
+                k = counter["v"]
+                counter["v"] += 1
+                dev_cot.copy_(host_cots[k % n_ring], non_blocking=True)
+                h2d += dev_cot.numel() * 4
+                one_view(my_views[k % len(my_views)], dev_cot)
+                for key, t in outs.items():
+                    host_out[key].copy_(t, non_blocking=True)
+                    d2h += t.numel() * 4
+            if dist_on:
+                import torch.distributed as dist
+                dist.all_reduce(flat)
+
+        steps_e2e = max(1, args.steps // 2)
+        step_e2e()
+        torch.cuda.synchronize()
+        h2d = d2h = 0
+        barrier(dist_on)
+        t0 = time.perf_counter()
+        for _ in range(steps_e2e):
+            step_e2e()
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, dist_on, device)
+        e2e = {"value": steps_e2e * B * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // steps_e2e,
+               "d2h_bytes_per_step": d2h // steps_e2e,
+               "what": "per view: H2D of the view's 8-channel cotangent image from pinned host memory, the four "
+                       "C-ABI calls, D2H of color/depth/normal/alpha; Gaussians and gradients stay resident "
+                       "(model state); host wall clock, max over ranks"}
+
+    # ---------------- roofline of the dominant kernel + per-kernel breakdown
+    hbm, hbm_src, sm_max = peaks()
+    n_sm = torch.cuda.get_device_properties(device).multi_processor_count
+    fp32 = fp32_peak_tflops(n_sm, sm_max)
+    views_timed = tim["views"]
+    tim_ext = dict(tim)
+    tim_ext["n"] = n
+    st = P.rd_view_stats(view)
+    key_bits = st["key_bits"]
+    kernels = {}
+    for name, ms in tim["ms"].items():
+        launches = tim["launches"][name]
+        if launches == 0:
+            continue
+        work, bound = kernel_work(name, tim_ext, views_timed, key_bits)
+        avg_ms = ms / launches
+        per_launch = work / launches
+        if bound == "hbm":
+            ach = per_launch / (avg_ms * 1e-3) / 1e9
+            kernels[name] = {"ms_per_launch": avg_ms, "share": None, "bound": "hbm", "achieved": ach,
+                             "unit": "GB/s", "frac": ach / hbm}
+        else:
+            ach = per_launch / (avg_ms * 1e-3) / 1e12
+            kernels[name] = {"ms_per_launch": avg_ms, "share": None, "bound": "alu", "achieved": ach,
+                             "unit": "TFLOP/s", "frac": ach / fp32}
+    tot_ms = sum(tim["ms"].values())
+    for name in kernels:
+        kernels[name]["share"] = tim["ms"][name] / tot_ms
+    dom = max(kernels, key=lambda k: tim["ms"][k])
+    dk = kernels[dom]
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get(dom)
+    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
+                "peak": hbm if dk["bound"] == "hbm" else fp32, "unit": dk["unit"], "frac": dk["frac"],
+                "traffic": traffic,
+                "peak_source": (f"{hbm_src} HBM copy (MEASURED_PEAKS.json)" if dk["bound"] == "hbm" else
+                                f"FP32 FFMA {n_sm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (DESIGN.md)")}
+
+    # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so)
+    launches_per_view = 1 + 2 + 1 + (2 + math.ceil(key_bits / 8)) + 1 + 1 + 1 + 1
+    views_per_rank = args.steps * B
+    M_avg = tim["n_duplicates"] / max(views_timed, 1)
+    vis_avg = tim["n_visible"] / max(views_timed, 1)
+    config.update({
+        "views_per_step_per_rank": B, "views_timed": total_views,
+        "l2": "inputs larger than L2: 354 MB of Gaussian parameters streamed per view (126 MB L2)"
+        if n >= 1_000_000 else "small config",
+        "M_per_view": M_avg, "visible_per_view": vis_avg, "tiles_per_visible": M_avg / max(vis_avg, 1),
+        "pairs_evaluated_per_px_fwd": tim["pairs_evaluated_fwd"] / max(views_timed, 1) / (H * W),
+        "pairs_blended_per_px": tim["pairs_blended_fwd"] / max(views_timed, 1) / (H * W),
+        "ms_per_view_by_kernel": {k: tim["ms"][k] / max(views_timed, 1) for k in tim["ms"]},
+        "parallelism": f"view-parallel dp{ws}",
+    })
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+            "roofline": roofline, "kernels": kernels, "gpu_launches": launches_per_view * views_per_rank,
+            "clocks": clk, "e2e": e2e}
+
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cam = my_views[0]
+        t, desc, cores, spent = oracle_frame_time(scene, cam, opt, n_pix=args.ref_pixels, n_grad=1, seed=0)
+        line["cpu_baseline"] = {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    view.close()
+    if dist_on:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="rade", choices=["rade", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
+    ap.add_argument("--views-per-step", type=int, default=4)
+    ap.add_argument("--n-gaussians", type=int, default=None)
+    ap.add_argument("--ref-pixels", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 does not meet the timing rules", file=sys.stderr)
+    import scenegen as sg
+    info = sg.CONFIGS[args.config]
+    config = {"workload": f"{args.config}: {info['name']}", "width": info["width"], "height": info["height"],
+              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": 16,
+              "scene_recipe": "scenegen (DESIGN.md §Input recipe), seed 0 + config index"}
+    if args.impl == "reference":
+        return run_reference(args, args.config, config)
+    return run_gpu(args, args.config, config)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,210 @@
+/*
+ * rade.h — C ABI of the B200-native RaDe-GS rasterizer (arXiv 2406.01467).
+ *
+ * The library renders, for one camera view and a set of general 3D Gaussians, in ONE
+ * pass: colour (Eq.3), alpha, the normal map (Eq.21-22, PAPER:617-627;
+ * aggregated as Σ ω_i n_i, reading S10) and the median-depth map (the depth of
+ * each splat at a pixel is the rasterized plane d = z_c + p·Δ of Eq.4),
+ * and the matching backward pass (gradients for means, scales, rotations, opacities and
+ * SH colours — the training use of PAPER:43-46). The problem statement it follows is
+ * "given Gaussians (x_c, Σ = R S Sᵀ Rᵀ, opacity, SH) and a camera (W, intrinsics),
+ * render colour, median depth and normal".
+ *
+ * Calls, in order, per view:
+ *   rd_preprocess  stage 1 (K1): per-Gaussian EWA projection, conic, α-bounded tile rect,
+ *                  SH colour, depth-plane coefficients p and normal n
+ *   rd_bin         stage 2 (K2): tile-count scan, duplicate (tile | depth) keys, device
+ *                  radix sort, per-tile ranges
+ *   rd_render_fwd  stage 3 (K3): per-tile front-to-back blend of C, A, N, median D
+ *   rd_render_bwd  stage 4 (K4, K5): reverse replay per pixel, per-Gaussian chain rule
+ *
+ * Conventions:
+ *   - Camera: world->camera rotation R (row-major) and translation t; +z forward, +y down;
+ *     pixel (i, j) is sampled at (i + 0.5, j + 0.5); u = fx·x/z + cx, v = fy·y/z + cy.
+ *   - Gaussian arrays are structure-of-arrays fp32 DEVICE arrays:
+ *       means[3][n], scales[3][n] (activated, > 0), rotations[4][n] (raw quaternion w,x,y,z;
+ *       normalised internally), opacities[n] (activated, in (0,1)),
+ *       sh[sh_coeffs][3][n] (coefficient-major, then channel; sh_coeffs = (deg+1)^2 ≤ 16).
+ *   - Image outputs are planar fp32 DEVICE arrays: color[3][H][W], depth[H][W] (0 where the
+ *     transmittance never crosses median_T), normal[3][H][W] (camera space, unnormalised
+ *     Σ ω n), alpha[H][W] = 1 − T_final.
+ *   - Gradients are ACCUMULATED (+=) into rd_grads arrays laid out like rd_gaussians, so
+ *     several views can be summed before an all-reduce; the caller zeroes them.
+ *
+ * Ownership: every array passed in is owned by the caller. Internal scratch (per-Gaussian
+ * records, keys/values, sort temp, per-pixel forward state, 2-D gradient accumulators) is
+ * owned by the rd_view and obtained from the caller's rd_alloc_fn (e.g. PyTorch's caching
+ * allocator) or, when alloc is NULL, from cudaMallocAsync on the call's stream. Buffers are
+ * cached by capacity and reused across views. All calls on one view must use one stream.
+ *
+ * Errors: functions never throw; they return an rd_status and set a thread-local message
+ * readable with rd_last_error(). Invalid arguments (null pointers, n < 0, width/height ≤ 0,
+ * tile ∉ {8, 16}, thresholds outside (0, 1), alpha_min ≥ alpha_max, sh_degree > 3 or
+ * (sh_degree+1)^2 > sh_coeffs) return RD_ERR_INVALID_ARGUMENT; out-of-order calls return
+ * RD_ERR_STATE; allocation failure RD_ERR_ALLOC; CUDA launch/runtime errors RD_ERR_CUDA.
+ * A degenerate primitive (non-finite input, scale ≤ 0, zero quaternion, centre depth ≤
+ * znear, opacity < alpha_min, singular 2-D covariance) is CULLED, not an error: it
+ * contributes nothing and receives zero gradient.
+ *
+ * Synchronisation: every call is asynchronous on the given stream except rd_bin, which
+ * reads the duplicate count M back to the host once (one D2H copy + stream sync).
+ */
+#ifndef RADE_H_
+#define RADE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RD_OK = 0,
+  RD_ERR_INVALID_ARGUMENT = 1,
+  RD_ERR_STATE = 2,
+  RD_ERR_ALLOC = 3,
+  RD_ERR_CUDA = 4
+} rd_status;
+
+/* Host struct. R is world->camera, row-major; znear culls centres with z ≤ znear. */
+typedef struct rd_camera {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float R[9];
+  float t[3];
+  float znear;
+} rd_camera;
+
+/* Host struct. Defaults (rd_options_default): tile 16, alpha_min 1/255, alpha_max 0.99,
+ * T_min 1e-4, median_T 0.5, dilation 0.3 px², bg (0,0,0), sh_degree 3. */
+typedef struct rd_options {
+  int32_t tile;      /* 8 or 16 pixels */
+  float alpha_min;   /* splats with α < alpha_min are skipped (S8) */
+  float alpha_max;   /* α = min(alpha_max, o·G) (S8) */
+  float T_min;       /* stop before blending a splat that would make T < T_min (S8) */
+  float median_T;    /* median depth: first blended splat with T_after ≤ median_T (S9) */
+  float dilation;    /* h added to the 2-D covariance diagonal for α only (S5) */
+  float bg[3];       /* C += T_final · bg (S17) */
+  int32_t sh_degree; /* active SH degree 0..3 */
+} rd_options;
+
+/* Device SoA Gaussian parameters (see layout above). */
+typedef struct rd_gaussians {
+  int64_t n;
+  int32_t sh_coeffs; /* coefficients stored per channel: 1, 4, 9 or 16 */
+  const float* means;
+  const float* scales;
+  const float* rotations;
+  const float* opacities;
+  const float* sh;
+} rd_gaussians;
+
+/* Device gradient arrays, same layouts as rd_gaussians; accumulated (+=). */
+typedef struct rd_grads {
+  float* means;
+  float* scales;
+  float* rotations;
+  float* opacities;
+  float* sh;
+} rd_grads;
+
+/* Per-view statistics (host struct filled by rd_view_stats). */
+typedef struct rd_stats {
+  int64_t n;            /* Gaussians in the last rd_preprocess */
+  int64_t n_duplicates; /* M: (Gaussian, tile) pairs after rd_bin */
+  int32_t tiles_x, tiles_y;
+  int32_t width, height;
+  int32_t stage;        /* 0 created, 1 preprocessed, 2 binned, 3 rendered */
+  int32_t key_bits;     /* radix-sort bits: 32 + ceil(log2(tiles)) */
+} rd_stats;
+
+/* Per-kernel device timings and work counters (host struct filled by rd_get_timings).
+ * Kernel index: 0 K1 preprocess_fwd, 1 K2a scan, 2 K2b duplicate, 3 K2c sort, 4 K2d ranges,
+ * 5 K3 render_fwd, 6 memset of the 2-D gradient scratch, 7 K4 render_bwd, 8 K5 preprocess_bwd. */
+#define RD_NUM_KERNELS 9
+typedef struct rd_timings {
+  double ms[RD_NUM_KERNELS];       /* summed CUDA-event durations since the last reset */
+  int64_t launches[RD_NUM_KERNELS];
+  int64_t pairs_evaluated_fwd;     /* (pixel, splat) pairs K3 evaluated (α computed)   */
+  int64_t pairs_blended_fwd;       /* pairs K3 blended (α ≥ alpha_min, not stopped)   */
+  int64_t pairs_evaluated_bwd;     /* pairs K4 evaluated (list positions < n_contrib) */
+  int64_t n_visible;               /* Σ over views of Gaussians with tiles_touched > 0 */
+  int64_t n_duplicates;            /* Σ over views of M */
+  int64_t views;                   /* rd_render_fwd calls since the last reset */
+} rd_timings;
+
+typedef void* (*rd_alloc_fn)(size_t bytes, void* ctx);
+typedef void (*rd_free_fn)(void* ptr, void* ctx);
+typedef struct rd_view rd_view;
+typedef void* rd_stream; /* a cudaStream_t */
+
+/* Fills *opt with the defaults listed above. */
+rd_status rd_options_default(rd_options* opt);
+
+/* Creates a view handle. alloc/free may both be NULL (then cudaMallocAsync/cudaFreeAsync
+ * on the call stream are used); otherwise both must be given. */
+rd_status rd_view_create(rd_view** view, rd_alloc_fn alloc, rd_free_fn free_fn, void* ctx);
+
+/* Releases the handle and every internal buffer (through free_fn / cudaFree). */
+rd_status rd_view_destroy(rd_view* view);
+
+/* Stage 1 (K1). Validates arguments, then launches one thread per Gaussian: cull,
+ * x_c = W μ + t, (u_c, v_c), J, Σ′ top-left 2x2, conic of the dilated 2-D
+ * covariance, α-bounded tile rect, SH → RGB, p (Eq.12-15) and n
+ * (Eq.21-22). The camera and options are captured by value. */
+rd_status rd_preprocess(rd_view* view, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
+                        rd_stream stream);
+
+/* Stage 2 (K2). Exclusive scan of tiles touched; reads M to the host (writes it to
+ * *n_duplicates_out if non-NULL); emits M keys (tile << 32 | float_bits(z_c)) with the
+ * Gaussian id as value in id order; stable LSD radix sort on bits [0, 32 + ceil(log2 T));
+ * per-tile [first, last) ranges. Order = (tile, z_c, id): the depth sort of PAPER:422. */
+rd_status rd_bin(rd_view* view, int64_t* n_duplicates_out, rd_stream stream);
+
+/* Stage 3 (K3). One CTA per tile. Any output pointer may be NULL to skip that map.
+ * color[3][H][W], depth[H][W], normal[3][H][W], alpha[H][W] (device, fp32). */
+rd_status rd_render_fwd(rd_view* view, float* color, float* depth, float* normal, float* alpha, rd_stream stream);
+
+/* Stage 4 (K4 + K5). Cotangents dL/d(color, depth, normal, alpha) in the output layouts
+ * (any may be NULL = zero). `g` must be the same Gaussians given to rd_preprocess.
+ * Gradients are accumulated into `grads` (all five pointers required). */
+rd_status rd_render_bwd(rd_view* view, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
+                        const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream);
+
+/* Profiling: when enabled, every kernel launch of this view is bracketed by CUDA events on
+ * its stream and K3/K4 count the pairs they evaluate (a few atomics per warp). Enabling
+ * or disabling resets the accumulators. rd_get_timings synchronises on the recorded
+ * events, sums their durations into *out, and resets if `reset` is non-zero. */
+rd_status rd_set_profiling(rd_view* view, int32_t enabled);
+rd_status rd_get_timings(rd_view* view, rd_timings* out, int32_t reset);
+
+/* Statistics of the last calls (host). */
+rd_status rd_view_stats(const rd_view* view, rd_stats* out);
+
+/* Debug copies (device → caller device buffers, async on `stream`), for bit-exact tests:
+ *  rd_debug_binning: keys u64[M], ids u32[M] (sorted), ranges u32[2*T] ([first, last)).
+ *  rd_debug_preprocess: records f32[n][16] (u, v, conic a, b, c, o, r, g, b, nx, ny, nz,
+ *    z_c, p0, p1, 0), rects u32[n][2] (x0 | y0 << 16, x1 | y1 << 16; tiles, half-open),
+ *    tiles_touched u32[n]. Any pointer may be NULL.
+ *  rd_debug_pixel_state: T_final f32[H*W], n_contrib i32[H*W], median_pos i32[H*W].
+ *  rd_debug_grads2d: after rd_render_bwd, per-Gaussian 2-D gradients f32[n][16] (du, dv,
+ *    da, db, dc, dopacity, dr, dg, db, dnx, dny, dnz, dz, dp0, dp1, 0). */
+rd_status rd_debug_binning(const rd_view* view, uint64_t* keys, uint32_t* ids, uint32_t* ranges, rd_stream stream);
+rd_status rd_debug_preprocess(const rd_view* view, float* records, uint32_t* rects, uint32_t* tiles_touched,
+                              rd_stream stream);
+rd_status rd_debug_pixel_state(const rd_view* view, float* T_final, int32_t* n_contrib, int32_t* median_pos,
+                               rd_stream stream);
+rd_status rd_debug_grads2d(const rd_view* view, float* grads2d, rd_stream stream);
+
+/* Thread-local message of the last error ("" if none). */
+const char* rd_last_error(void);
+
+/* Library version / build string. */
+const char* rd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RADE_H_ */

@@ -68,8 +68,8 @@ def lib():
             L.or_project.argtypes = common + [dp]
             L.or_splat_eval.argtypes = common + [i64, i64, dp, dp]
             L.or_render.argtypes = common + [i64, ctypes.c_void_p, dp, dp, dp, dp, ctypes.c_void_p,
-                                             ctypes.c_void_p, ctypes.c_void_p]
-            L.or_grad.argtypes = common + [dp, i64, ctypes.c_void_p, dp]
+                                             ctypes.c_void_p, ctypes.c_void_p, dp]
+            L.or_grad.argtypes = common + [dp, i64, ctypes.c_void_p, dp, dp]
             L.or_sh_basis.argtypes = [dp, dp]
             L.or_sh_basis.restype = None
             L.or_num_threads.restype = ctypes.c_int
@@ -144,9 +144,10 @@ def splat_eval(scene, cam, opt, gid, uv):
     return out
 
 
-def render(scene, cam, opt, pixels=None, eps=DEFAULT_EPS):
+def render(scene, cam, opt, pixels=None, eps=DEFAULT_EPS, timing=None):
     """Brute-force render. pixels=None: full frame, outputs shaped [C][H][W] / [H][W];
-    else a 1-D array of linear pixel indices, outputs shaped [C][k] / [k]."""
+    else a 1-D array of linear pixel indices, outputs shaped [C][k] / [k].
+    timing (optional float64[3]) receives: project+sort s, per-pixel loop s, survivors."""
     keep, sargs = _scene_args(scene)
     cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt, eps)
     W, H = cam.width, cam.height
@@ -164,14 +165,15 @@ def render(scene, cam, opt, pixels=None, eps=DEFAULT_EPS):
     mid = np.zeros(npix, np.int64)
     lib().or_render(*sargs, _dp(cv), _dp(ov), ctypes.c_int64(npix),
                     None if pix is None else pix.ctypes.data, _dp(color), _dp(depth), _dp(normal),
-                    _dp(alpha), flags.ctypes.data, nblend.ctypes.data, mid.ctypes.data)
+                    _dp(alpha), flags.ctypes.data, nblend.ctypes.data, mid.ctypes.data,
+                    None if timing is None else _dp(timing))
     shape = (H, W) if pixels is None else (npix,)
     return dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), normal=normal.reshape((3,) + shape),
                 alpha=alpha.reshape(shape), flags=flags.reshape(shape), nblend=nblend.reshape(shape),
                 median_id=mid.reshape(shape))
 
 
-def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS):
+def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS, timing=None):
     """Exact dL/dθ for the listed Gaussians, L = Σ_px cot·(C, D, N, A). Returns [len(gids), 59]
     (μ 0..2, s 3..5, q 6..9, o 10, sh 11 + coeff*3 + ch)."""
     keep, sargs = _scene_args(scene)
@@ -185,7 +187,8 @@ def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS):
     c = np.ascontiguousarray(c)
     gids = np.ascontiguousarray(gids, np.int64)
     out = np.zeros((gids.shape[0], NPARAM), np.float64)
-    lib().or_grad(*sargs, _dp(cv), _dp(ov), _dp(c), ctypes.c_int64(gids.shape[0]), gids.ctypes.data, _dp(out))
+    lib().or_grad(*sargs, _dp(cv), _dp(ov), _dp(c), ctypes.c_int64(gids.shape[0]), gids.ctypes.data, _dp(out),
+                  None if timing is None else _dp(timing))
     return out
 
 

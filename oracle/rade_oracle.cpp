@@ -400,6 +400,14 @@ void prepare(const SceneIn& sc, const Cam& cam, const Opt& opt, Prepared& pr) {
   for (size_t k = 0; k < pr.splats.size(); ++k) pr.pos_of[pr.splats[k].id] = (int64_t)k;
 }
 
+double wall() {
+#ifdef _OPENMP
+  return omp_get_wtime();
+#else
+  return 0.0;
+#endif
+}
+
 Cam make_cam(const double* c) {
   Cam cam;
   cam.fx = c[0]; cam.fy = c[1]; cam.cx = c[2]; cam.cy = c[3];
@@ -523,12 +531,14 @@ int or_splat_eval(int64_t n, const double* means, const double* scales, const do
 int or_render(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
               const double* sh, int sh_coeffs, const double* camv, const double* optv, int64_t npix,
               const int64_t* pix, double* color, double* depth, double* normal, double* alpha, uint8_t* flags,
-              int32_t* nblend, int64_t* median_id) {
+              int32_t* nblend, int64_t* median_id, double* timing) {
   SceneIn sc = make_scene(n, means, scales, rot, opac, sh, sh_coeffs);
   Cam cam = make_cam(camv);
   Opt opt = make_opt(optv);
   Prepared pr;
+  double t0 = wall();
   prepare(sc, cam, opt, pr);
+  double t1 = wall();
   const int64_t ns = (int64_t)pr.splats.size();
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t k = 0; k < npix; ++k) {
@@ -548,6 +558,11 @@ int or_render(int64_t n, const double* means, const double* scales, const double
     nblend[k] = px.nblend;
     median_id[k] = px.median_id;
   }
+  if (timing) {  // [0] project + sort seconds, [1] per-pixel loop seconds, [2] surviving Gaussians
+    timing[0] = t1 - t0;
+    timing[1] = wall() - t1;
+    timing[2] = (double)ns;
+  }
   return 0;
 }
 
@@ -558,12 +573,14 @@ int or_render(int64_t n, const double* means, const double* scales, const double
  *   culled Gaussians get zero. */
 int or_grad(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
             const double* sh, int sh_coeffs, const double* camv, const double* optv, const double* cot,
-            int64_t ng, const int64_t* gids, double* out) {
+            int64_t ng, const int64_t* gids, double* out, double* timing) {
   SceneIn sc = make_scene(n, means, scales, rot, opac, sh, sh_coeffs);
   Cam cam = make_cam(camv);
   Opt opt = make_opt(optv);
   Prepared pr;
+  double t0 = wall();
   prepare(sc, cam, opt, pr);
+  double t1 = wall();
   const int64_t ns = (int64_t)pr.splats.size();
   const int64_t npx = (int64_t)cam.W * cam.H;
   for (int64_t gk = 0; gk < ng; ++gk) {
@@ -609,6 +626,11 @@ int or_grad(int64_t n, const double* means, const double* scales, const double* 
 #pragma omp critical
       for (int j = 0; j < NP; ++j) res[j] += acc[j];
     }
+  }
+  if (timing) {  // [0] project + sort seconds, [1] dual-number loop seconds, [2] surviving Gaussians
+    timing[0] = t1 - t0;
+    timing[1] = wall() - t1;
+    timing[2] = (double)ns;
   }
   return 0;
 }

@@ -1,0 +1,491 @@
+// abi.cu — the C ABI of include/rade.h: argument validation, the per-view stage machine,
+// capacity-cached scratch buffers (caller allocator or cudaMallocAsync), optional per-kernel
+// CUDA-event profiling, and the launch sequence of the five stages. Host code only;
+// kernels live in preprocess.cu, binning.cu and render.cu.
+#include "../../include/rade.h"
+#include "rade_internal.cuh"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace rade;
+
+namespace {
+
+thread_local std::string g_err;
+
+rd_status fail(rd_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+rd_status fail(rd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define RD_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(RD_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define RD_CHECK_LAUNCH(what)                                                                       \
+  do {                                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ != cudaSuccess) return fail(RD_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct Buf {
+  void* ptr = nullptr;
+  size_t cap = 0;
+};
+
+enum Kernel { K_PRE = 0, K_SCAN, K_DUP, K_SORT, K_RANGES, K_FWD, K_MEMSET, K_BWD, K_PREBWD };
+
+}  // namespace
+
+struct rd_view {
+  rd_alloc_fn alloc = nullptr;
+  rd_free_fn free_fn = nullptr;
+  void* ctx = nullptr;
+  int stage = 0;
+  int64_t n = 0;
+  int sh_coeffs = 0;
+  DevCam cam{};
+  DevOpt opt{};
+  int tiles_x = 0, tiles_y = 0;
+  int key_bits = 0;
+  int64_t M = 0;
+  int sort_sel = 0;
+  uint32_t* host_M = nullptr;  // pinned
+  Buf rec, rect, touched, offsets, zkey, scan_tmp;
+  Buf keys0, keys1, vals0, vals1, sort_tmp;
+  Buf ranges;
+  Buf T_final, n_contrib, median_pos;
+  Buf g2d;
+  // profiling
+  bool prof = false;
+  cudaStream_t last_stream = nullptr;
+  struct Ev {
+    cudaEvent_t a, b;
+    int k;
+  };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> pool;
+  Buf counters;
+  double acc_ms[RD_NUM_KERNELS] = {0};
+  int64_t acc_launch[RD_NUM_KERNELS] = {0};
+  int64_t acc_M = 0, acc_views = 0;
+  cudaEvent_t cur_a = nullptr;
+
+  rd_status ensure(Buf& b, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return RD_OK;
+    release(b, s);
+    size_t want = bytes + bytes / 4 + 256;
+    void* p = nullptr;
+    if (alloc) {
+      p = alloc(want, ctx);
+      if (!p) return fail(RD_ERR_ALLOC, "allocator callback failed for %zu bytes", want);
+    } else {
+      cudaError_t e = cudaMallocAsync(&p, want, s);
+      if (e != cudaSuccess) return fail(RD_ERR_ALLOC, "cudaMallocAsync(%zu): %s", want, cudaGetErrorString(e));
+    }
+    b.ptr = p;
+    b.cap = want;
+    return RD_OK;
+  }
+  void release(Buf& b, cudaStream_t s) {
+    if (!b.ptr) return;
+    if (free_fn)
+      free_fn(b.ptr, ctx);
+    else
+      cudaFreeAsync(b.ptr, s);
+    b.ptr = nullptr;
+    b.cap = 0;
+  }
+  cudaEvent_t get_event() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void begin(cudaStream_t s) {
+    last_stream = s;
+    if (!prof) return;
+    cur_a = get_event();
+    cudaEventRecord(cur_a, s);
+  }
+  void end(int k, cudaStream_t s) {
+    if (!prof) return;
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, s);
+    pending.push_back(Ev{cur_a, b, k});
+  }
+  Counter* ctr() { return prof ? (Counter*)counters.ptr : nullptr; }
+  void resolve() {
+    for (const Ev& e : pending) {
+      float ms = 0.f;
+      cudaEventSynchronize(e.b);
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      acc_ms[e.k] += ms;
+      acc_launch[e.k] += 1;
+      pool.push_back(e.a);
+      pool.push_back(e.b);
+    }
+    pending.clear();
+  }
+  void reset_acc() {
+    resolve();
+    for (int k = 0; k < RD_NUM_KERNELS; ++k) {
+      acc_ms[k] = 0.0;
+      acc_launch[k] = 0;
+    }
+    acc_M = acc_views = 0;
+    if (counters.ptr) cudaMemsetAsync(counters.ptr, 0, kNumCounters * sizeof(Counter), last_stream);
+  }
+};
+
+#define RD_ENSURE(buf, bytes, s)              \
+  do {                                        \
+    rd_status st_ = v->ensure(buf, bytes, s); \
+    if (st_ != RD_OK) return st_;             \
+  } while (0)
+
+extern "C" {
+
+const char* rd_last_error(void) { return g_err.c_str(); }
+
+const char* rd_version(void) { return "rade-b200 0.1 (sm_100a)"; }
+
+rd_status rd_options_default(rd_options* opt) {
+  if (!opt) return fail(RD_ERR_INVALID_ARGUMENT, "opt is NULL");
+  opt->tile = 16;
+  opt->alpha_min = 1.f / 255.f;
+  opt->alpha_max = 0.99f;
+  opt->T_min = 1e-4f;
+  opt->median_T = 0.5f;
+  opt->dilation = 0.3f;
+  opt->bg[0] = opt->bg[1] = opt->bg[2] = 0.f;
+  opt->sh_degree = 3;
+  return RD_OK;
+}
+
+rd_status rd_view_create(rd_view** view, rd_alloc_fn alloc, rd_free_fn free_fn, void* ctx) {
+  g_err.clear();
+  if (!view) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if ((alloc == nullptr) != (free_fn == nullptr))
+    return fail(RD_ERR_INVALID_ARGUMENT, "alloc and free_fn must both be given or both be NULL");
+  rd_view* v = new (std::nothrow) rd_view();
+  if (!v) return fail(RD_ERR_ALLOC, "out of host memory");
+  v->alloc = alloc;
+  v->free_fn = free_fn;
+  v->ctx = ctx;
+  *view = v;  // no CUDA call here: the pinned M slot is allocated by the first rd_bin
+  return RD_OK;
+}
+
+rd_status rd_view_destroy(rd_view* v) {
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  Buf* all[] = {&v->rec,     &v->rect,      &v->touched,    &v->offsets, &v->zkey,  &v->scan_tmp,
+                &v->keys0,   &v->keys1,     &v->vals0,      &v->vals1,   &v->sort_tmp, &v->ranges,
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d,     &v->counters};
+  if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
+  v->resolve();
+  for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
+  for (Buf* b : all) v->release(*b, v->last_stream);
+  if (v->host_M) cudaFreeHost(v->host_M);
+  delete v;
+  return RD_OK;
+}
+
+static bool in01(float x) { return x > 0.f && x < 1.f && std::isfinite(x); }
+
+rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
+                        rd_stream stream) {
+  g_err.clear();
+  if (!v || !g || !cam || !opt) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/gaussians/camera/options");
+  if (g->n < 0) return fail(RD_ERR_INVALID_ARGUMENT, "n < 0");
+  if (g->n > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "n >= 2^31 not supported");
+  if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities || !g->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL Gaussian array");
+  if (cam->width <= 0 || cam->height <= 0) return fail(RD_ERR_INVALID_ARGUMENT, "width/height must be > 0");
+  if (!(cam->fx > 0.f && cam->fy > 0.f) || !std::isfinite(cam->fx) || !std::isfinite(cam->fy))
+    return fail(RD_ERR_INVALID_ARGUMENT, "fx, fy must be finite and > 0");
+  if (!(cam->znear > 0.f)) return fail(RD_ERR_INVALID_ARGUMENT, "znear must be > 0");
+  if (opt->tile != 8 && opt->tile != 16) return fail(RD_ERR_INVALID_ARGUMENT, "tile must be 8 or 16");
+  if (!in01(opt->alpha_min) || !in01(opt->alpha_max) || !in01(opt->T_min) || !in01(opt->median_T))
+    return fail(RD_ERR_INVALID_ARGUMENT, "alpha_min, alpha_max, T_min, median_T must lie in (0, 1)");
+  if (!(opt->alpha_min < opt->alpha_max)) return fail(RD_ERR_INVALID_ARGUMENT, "alpha_min must be < alpha_max");
+  if (!(opt->dilation >= 0.f) || !std::isfinite(opt->dilation))
+    return fail(RD_ERR_INVALID_ARGUMENT, "dilation must be finite and >= 0");
+  if (opt->sh_degree < 0 || opt->sh_degree > 3) return fail(RD_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
+  const int need = (opt->sh_degree + 1) * (opt->sh_degree + 1);
+  if (g->sh_coeffs < need || g->sh_coeffs > 16)
+    return fail(RD_ERR_INVALID_ARGUMENT, "sh_coeffs=%d incompatible with sh_degree=%d", g->sh_coeffs,
+                opt->sh_degree);
+  const int tiles_x = (cam->width + opt->tile - 1) / opt->tile;
+  const int tiles_y = (cam->height + opt->tile - 1) / opt->tile;
+  if (tiles_x > 65535 || tiles_y > 65535) return fail(RD_ERR_INVALID_ARGUMENT, "image too large");
+
+  cudaStream_t s = (cudaStream_t)stream;
+  v->n = g->n;
+  v->sh_coeffs = g->sh_coeffs;
+  DevCam& c = v->cam;
+  c.fx = cam->fx; c.fy = cam->fy; c.cx = cam->cx; c.cy = cam->cy;
+  c.W = cam->width; c.H = cam->height;
+  for (int k = 0; k < 9; ++k) c.R[k] = cam->R[k];
+  for (int k = 0; k < 3; ++k) c.t[k] = cam->t[k];
+  c.znear = cam->znear;
+  for (int i = 0; i < 3; ++i) {
+    double acc = 0.0;
+    for (int k = 0; k < 3; ++k) acc -= (double)cam->R[3 * k + i] * (double)cam->t[k];
+    c.campos[i] = (float)acc;
+  }
+  DevOpt& o = v->opt;
+  o.tile = opt->tile;
+  o.alpha_min = opt->alpha_min; o.alpha_max = opt->alpha_max; o.T_min = opt->T_min;
+  o.median_T = opt->median_T; o.dilation = opt->dilation;
+  for (int k = 0; k < 3; ++k) o.bg[k] = opt->bg[k];
+  o.sh_degree = opt->sh_degree;
+  o.ln_alpha_min = logf(opt->alpha_min);
+  v->tiles_x = tiles_x;
+  v->tiles_y = tiles_y;
+  int bits = 1;
+  while ((1LL << bits) < (long long)tiles_x * tiles_y) ++bits;
+  v->key_bits = 32 + bits;
+
+  const size_t n = (size_t)g->n;
+  RD_ENSURE(v->rec, n * sizeof(Record), s);
+  RD_ENSURE(v->rect, n * sizeof(uint2), s);
+  RD_ENSURE(v->touched, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->offsets, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->zkey, n * sizeof(float), s);
+
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
+  v->begin(s);
+  launch_preprocess_fwd(dg, c, o, tiles_x, tiles_y, (Record*)v->rec.ptr, (uint2*)v->rect.ptr,
+                        (uint32_t*)v->touched.ptr, (float*)v->zkey.ptr, v->ctr(), s);
+  RD_CHECK_LAUNCH("preprocess_fwd");
+  v->end(K_PRE, s);
+  v->stage = 1;
+  v->M = 0;
+  return RD_OK;
+}
+
+rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
+  g_err.clear();
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (v->stage < 1) return fail(RD_ERR_STATE, "rd_bin before rd_preprocess");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = v->n;
+  const int n_tiles = v->tiles_x * v->tiles_y;
+  int64_t M = 0;
+  if (n > 0) {
+    const size_t scan_bytes = binning_scan_temp_bytes(n);
+    RD_ENSURE(v->scan_tmp, scan_bytes, s);
+    if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, sizeof(uint32_t)));
+    v->begin(s);
+    launch_scan((const uint32_t*)v->touched.ptr, (uint32_t*)v->offsets.ptr, n, v->scan_tmp.ptr, scan_bytes, s);
+    RD_CHECK_LAUNCH("scan");
+    v->end(K_SCAN, s);
+    RD_CUDA(cudaMemcpyAsync(v->host_M, (const uint32_t*)v->offsets.ptr + (n - 1), sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+    RD_CUDA(cudaStreamSynchronize(s));
+    M = (int64_t)*v->host_M;
+  }
+  if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
+  RD_ENSURE(v->keys0, (size_t)M * sizeof(uint64_t), s);
+  RD_ENSURE(v->keys1, (size_t)M * sizeof(uint64_t), s);
+  RD_ENSURE(v->vals0, (size_t)M * sizeof(uint32_t), s);
+  RD_ENSURE(v->vals1, (size_t)M * sizeof(uint32_t), s);
+  RD_ENSURE(v->ranges, (size_t)n_tiles * sizeof(uint2), s);
+  v->sort_sel = 0;
+  if (M > 0) {
+    v->begin(s);
+    launch_duplicate(n, (const uint32_t*)v->offsets.ptr, (const uint2*)v->rect.ptr, (const float*)v->zkey.ptr,
+                     v->tiles_x, (uint64_t*)v->keys0.ptr, (uint32_t*)v->vals0.ptr, s);
+    RD_CHECK_LAUNCH("duplicate");
+    v->end(K_DUP, s);
+    const size_t sort_bytes = binning_sort_temp_bytes(M, v->key_bits);
+    RD_ENSURE(v->sort_tmp, sort_bytes, s);
+    v->begin(s);
+    v->sort_sel = launch_sort((uint64_t*)v->keys0.ptr, (uint64_t*)v->keys1.ptr, (uint32_t*)v->vals0.ptr,
+                              (uint32_t*)v->vals1.ptr, M, v->key_bits, v->sort_tmp.ptr, sort_bytes, s);
+    RD_CHECK_LAUNCH("sort");
+    v->end(K_SORT, s);
+  }
+  const uint64_t* keys = (const uint64_t*)(v->sort_sel ? v->keys1.ptr : v->keys0.ptr);
+  v->begin(s);
+  launch_ranges(keys, M, n_tiles, (uint2*)v->ranges.ptr, s);
+  RD_CHECK_LAUNCH("ranges");
+  v->end(K_RANGES, s);
+  v->M = M;
+  v->acc_M += M;
+  v->stage = 2;
+  if (n_duplicates_out) *n_duplicates_out = M;
+  return RD_OK;
+}
+
+rd_status rd_render_fwd(rd_view* v, float* color, float* depth, float* normal, float* alpha, rd_stream stream) {
+  g_err.clear();
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (v->stage < 2) return fail(RD_ERR_STATE, "rd_render_fwd before rd_bin");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t HW = (size_t)v->cam.W * v->cam.H;
+  RD_ENSURE(v->T_final, HW * sizeof(float), s);
+  RD_ENSURE(v->n_contrib, HW * sizeof(int32_t), s);
+  RD_ENSURE(v->median_pos, HW * sizeof(int32_t), s);
+  const uint32_t* ids = (const uint32_t*)(v->sort_sel ? v->vals1.ptr : v->vals0.ptr);
+  v->begin(s);
+  launch_render_fwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
+                    (const Record*)v->rec.ptr, color, depth, normal, alpha, (float*)v->T_final.ptr,
+                    (int32_t*)v->n_contrib.ptr, (int32_t*)v->median_pos.ptr, v->ctr(), s);
+  RD_CHECK_LAUNCH("render_fwd");
+  v->end(K_FWD, s);
+  v->acc_views += 1;
+  v->stage = 3;
+  return RD_OK;
+}
+
+rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
+                        const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream) {
+  g_err.clear();
+  if (!v || !g || !grads) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/gaussians/grads");
+  if (v->stage < 3) return fail(RD_ERR_STATE, "rd_render_bwd before rd_render_fwd");
+  if (g->n != v->n || g->sh_coeffs != v->sh_coeffs)
+    return fail(RD_ERR_INVALID_ARGUMENT, "Gaussians differ from those given to rd_preprocess");
+  if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities || !g->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL Gaussian array");
+  if (g->n > 0 && (!grads->means || !grads->scales || !grads->rotations || !grads->opacities || !grads->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL gradient array");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t n = (size_t)v->n;
+  RD_ENSURE(v->g2d, n * kG2D * sizeof(float), s);
+  if (n > 0) {
+    v->begin(s);
+    RD_CUDA(cudaMemsetAsync(v->g2d.ptr, 0, n * kG2D * sizeof(float), s));
+    v->end(K_MEMSET, s);
+  }
+  const uint32_t* ids = (const uint32_t*)(v->sort_sel ? v->vals1.ptr : v->vals0.ptr);
+  v->begin(s);
+  launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
+                    (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
+                    (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,
+                    (float*)v->g2d.ptr, v->ctr(), s);
+  RD_CHECK_LAUNCH("render_bwd");
+  v->end(K_BWD, s);
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
+  DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
+  v->begin(s);
+  launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const float*)v->g2d.ptr, dgr, s);
+  RD_CHECK_LAUNCH("preprocess_bwd");
+  v->end(K_PREBWD, s);
+  return RD_OK;
+}
+
+rd_status rd_set_profiling(rd_view* v, int32_t enabled) {
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (enabled) {
+    rd_status st = v->ensure(v->counters, kNumCounters * sizeof(Counter), v->last_stream);
+    if (st != RD_OK) return st;
+  }
+  v->prof = enabled != 0;
+  v->reset_acc();
+  if (cudaGetLastError() != cudaSuccess) return fail(RD_ERR_CUDA, "rd_set_profiling: CUDA error");
+  return RD_OK;
+}
+
+rd_status rd_get_timings(rd_view* v, rd_timings* out, int32_t reset) {
+  if (!v || !out) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/out");
+  v->resolve();
+  std::memset(out, 0, sizeof(*out));
+  for (int k = 0; k < RD_NUM_KERNELS; ++k) {
+    out->ms[k] = v->acc_ms[k];
+    out->launches[k] = v->acc_launch[k];
+  }
+  out->n_duplicates = v->acc_M;
+  out->views = v->acc_views;
+  if (v->counters.ptr) {
+    Counter h[kNumCounters] = {0};
+    RD_CUDA(cudaMemcpyAsync(h, v->counters.ptr, sizeof(h), cudaMemcpyDeviceToHost, v->last_stream));
+    RD_CUDA(cudaStreamSynchronize(v->last_stream));
+    out->pairs_evaluated_fwd = (int64_t)h[0];
+    out->pairs_blended_fwd = (int64_t)h[1];
+    out->pairs_evaluated_bwd = (int64_t)h[2];
+    out->n_visible = (int64_t)h[3];
+  }
+  if (reset) v->reset_acc();
+  return RD_OK;
+}
+
+rd_status rd_view_stats(const rd_view* v, rd_stats* out) {
+  if (!v || !out) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/out");
+  out->n = v->n;
+  out->n_duplicates = v->M;
+  out->tiles_x = v->tiles_x;
+  out->tiles_y = v->tiles_y;
+  out->width = v->cam.W;
+  out->height = v->cam.H;
+  out->stage = v->stage;
+  out->key_bits = v->key_bits;
+  return RD_OK;
+}
+
+rd_status rd_debug_binning(const rd_view* v, uint64_t* keys, uint32_t* ids, uint32_t* ranges, rd_stream stream) {
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (v->stage < 2) return fail(RD_ERR_STATE, "rd_debug_binning before rd_bin");
+  cudaStream_t s = (cudaStream_t)stream;
+  const void* k = v->sort_sel ? v->keys1.ptr : v->keys0.ptr;
+  const void* i = v->sort_sel ? v->vals1.ptr : v->vals0.ptr;
+  if (keys && v->M) RD_CUDA(cudaMemcpyAsync(keys, k, (size_t)v->M * 8, cudaMemcpyDeviceToDevice, s));
+  if (ids && v->M) RD_CUDA(cudaMemcpyAsync(ids, i, (size_t)v->M * 4, cudaMemcpyDeviceToDevice, s));
+  if (ranges)
+    RD_CUDA(cudaMemcpyAsync(ranges, v->ranges.ptr, (size_t)v->tiles_x * v->tiles_y * 8, cudaMemcpyDeviceToDevice, s));
+  return RD_OK;
+}
+
+rd_status rd_debug_preprocess(const rd_view* v, float* records, uint32_t* rects, uint32_t* tiles_touched,
+                              rd_stream stream) {
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (v->stage < 1) return fail(RD_ERR_STATE, "rd_debug_preprocess before rd_preprocess");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t n = (size_t)v->n;
+  if (n == 0) return RD_OK;
+  if (records) RD_CUDA(cudaMemcpyAsync(records, v->rec.ptr, n * sizeof(Record), cudaMemcpyDeviceToDevice, s));
+  if (rects) RD_CUDA(cudaMemcpyAsync(rects, v->rect.ptr, n * sizeof(uint2), cudaMemcpyDeviceToDevice, s));
+  if (tiles_touched) RD_CUDA(cudaMemcpyAsync(tiles_touched, v->touched.ptr, n * 4, cudaMemcpyDeviceToDevice, s));
+  return RD_OK;
+}
+
+rd_status rd_debug_pixel_state(const rd_view* v, float* T_final, int32_t* n_contrib, int32_t* median_pos,
+                               rd_stream stream) {
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (v->stage < 3) return fail(RD_ERR_STATE, "rd_debug_pixel_state before rd_render_fwd");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t HW = (size_t)v->cam.W * v->cam.H;
+  if (T_final) RD_CUDA(cudaMemcpyAsync(T_final, v->T_final.ptr, HW * 4, cudaMemcpyDeviceToDevice, s));
+  if (n_contrib) RD_CUDA(cudaMemcpyAsync(n_contrib, v->n_contrib.ptr, HW * 4, cudaMemcpyDeviceToDevice, s));
+  if (median_pos) RD_CUDA(cudaMemcpyAsync(median_pos, v->median_pos.ptr, HW * 4, cudaMemcpyDeviceToDevice, s));
+  return RD_OK;
+}
+
+rd_status rd_debug_grads2d(const rd_view* v, float* grads2d, rd_stream stream) {
+  if (!v || !grads2d) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/grads2d");
+  if (!v->g2d.ptr) return fail(RD_ERR_STATE, "rd_debug_grads2d before rd_render_bwd");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (v->n) RD_CUDA(cudaMemcpyAsync(grads2d, v->g2d.ptr, (size_t)v->n * kG2D * 4, cudaMemcpyDeviceToDevice, s));
+  return RD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,500 @@
+// preprocess.cu — K1 (per-Gaussian forward, stage 1) and K5 (per-Gaussian backward,
+// second half of stage 4) of the RaDe-GS rasterizer, sm_100a.
+//
+// One thread per Gaussian; structure-of-arrays inputs so every parameter plane is read
+// coalesced (HBM-bound kernels: ~236 B in, 80 B out per visible Gaussian).
+//
+// Per Gaussian (PAPER.md line refs; readings S* in DESIGN.md):
+//   Σ = R S Sᵀ Rᵀ; x_c = W μ + t; u_c, v_c pinhole; t_c = ‖x_c‖
+//   2-D covariance = top-left 2x2 of Σ′ = J W Σ Wᵀ Jᵀ, formed as M Mᵀ with
+//     M = J₂ (W R) S (no 3x3 Σ is materialised), dilated by h·I for α only (S5)
+//   depth-plane p and normal n: the paper's q̂ = v′ᵀΣ′⁻¹/(v′ᵀΣ′⁻¹v′) (Eq.13),
+//     p = (z_c/t_c) q and n = normalize(Jᵀ(−(q,1)ᵀ)),
+//     evaluated in the algebraically identical cancellation-free "m-form":
+//       m = Σ_c⁻¹ x̂ = R_c (R_cᵀ x̂ ⊘ s²), μ = x̂ᵀ Σ_c⁻¹ x̂,
+//       p_k = z_c² / (f_k t_c) · (m_k/μ − x̂_k),  n = −m/‖m‖.
+//   colour from degree-≤3 SH at the Gaussian's view direction.
+#include "rade_internal.cuh"
+
+#include <math.h>
+
+namespace rade {
+namespace {
+
+// real-SH basis constants (3DGS convention, reading S14)
+constexpr float kC0 = 0.28209479177387814f;
+constexpr float kC1 = 0.4886025119029199f;
+constexpr float kC2_0 = 1.0925484305920792f, kC2_1 = -1.0925484305920792f, kC2_2 = 0.31539156525252005f,
+                kC2_3 = -1.0925484305920792f, kC2_4 = 0.5462742152960396f;
+constexpr float kC3_0 = -0.5900435899266435f, kC3_1 = 2.890611442640554f, kC3_2 = -0.4570457994644658f,
+                kC3_3 = 0.3731763325901154f, kC3_4 = -0.4570457994644658f, kC3_5 = 1.445305721320277f,
+                kC3_6 = -0.5900435899266435f;
+
+__device__ __forceinline__ void sh_basis(float x, float y, float z, int deg, float Y[16]) {
+  Y[0] = kC0;
+  if (deg < 1) return;
+  Y[1] = -kC1 * y;
+  Y[2] = kC1 * z;
+  Y[3] = -kC1 * x;
+  if (deg < 2) return;
+  float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  Y[4] = kC2_0 * xy;
+  Y[5] = kC2_1 * yz;
+  Y[6] = kC2_2 * (2.f * zz - xx - yy);
+  Y[7] = kC2_3 * xz;
+  Y[8] = kC2_4 * (xx - yy);
+  if (deg < 3) return;
+  Y[9] = kC3_0 * y * (3.f * xx - yy);
+  Y[10] = kC3_1 * xy * z;
+  Y[11] = kC3_2 * y * (4.f * zz - xx - yy);
+  Y[12] = kC3_3 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+  Y[13] = kC3_4 * x * (4.f * zz - xx - yy);
+  Y[14] = kC3_5 * z * (xx - yy);
+  Y[15] = kC3_6 * x * (xx - 3.f * yy);
+}
+
+// d(Σ_k c_k Y_k)/d(x, y, z) for the basis above (direction treated as free 3-vector).
+__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, int deg, const float c[16], float& gx,
+                                              float& gy, float& gz) {
+  gx = gy = gz = 0.f;
+  if (deg < 1) return;
+  gy += -kC1 * c[1];
+  gz += kC1 * c[2];
+  gx += -kC1 * c[3];
+  if (deg < 2) return;
+  float xx = x * x, yy = y * y, zz = z * z;
+  gx += kC2_0 * y * c[4];
+  gy += kC2_0 * x * c[4];
+  gy += kC2_1 * z * c[5];
+  gz += kC2_1 * y * c[5];
+  gx += -2.f * kC2_2 * x * c[6];
+  gy += -2.f * kC2_2 * y * c[6];
+  gz += 4.f * kC2_2 * z * c[6];
+  gx += kC2_3 * z * c[7];
+  gz += kC2_3 * x * c[7];
+  gx += 2.f * kC2_4 * x * c[8];
+  gy += -2.f * kC2_4 * y * c[8];
+  if (deg < 3) return;
+  gx += kC3_0 * 6.f * x * y * c[9];
+  gy += kC3_0 * 3.f * (xx - yy) * c[9];
+  gx += kC3_1 * y * z * c[10];
+  gy += kC3_1 * x * z * c[10];
+  gz += kC3_1 * x * y * c[10];
+  gx += kC3_2 * (-2.f * x * y) * c[11];
+  gy += kC3_2 * (4.f * zz - xx - 3.f * yy) * c[11];
+  gz += kC3_2 * 8.f * y * z * c[11];
+  gx += kC3_3 * (-6.f * x * z) * c[12];
+  gy += kC3_3 * (-6.f * y * z) * c[12];
+  gz += kC3_3 * (6.f * zz - 3.f * xx - 3.f * yy) * c[12];
+  gx += kC3_4 * (4.f * zz - 3.f * xx - yy) * c[13];
+  gy += kC3_4 * (-2.f * x * y) * c[13];
+  gz += kC3_4 * 8.f * x * z * c[13];
+  gx += kC3_5 * 2.f * x * z * c[14];
+  gy += kC3_5 * (-2.f * y * z) * c[14];
+  gz += kC3_5 * (xx - yy) * c[14];
+  gx += kC3_6 * 3.f * (xx - yy) * c[15];
+  gy += kC3_6 * (-6.f * x * y) * c[15];
+}
+
+// Forward quantities of one Gaussian (registers only).
+struct GF {
+  float mu[3], s[3], qr[4], o;
+  float qinv, qn[4];
+  float Rc[9];  // W R(q̂), row-major
+  float x[3], t2, it;
+  float u, v;
+  float RS[9];  // Rc diag(s)
+  float j00, j02, j11, j12;
+  float M[6];   // J₂ RS, rows 0..1
+  float A00, A01, A11, det, ca, cb, cc;
+  float xh[3], rh[3], w[3], ah[3], mh[3], muq, ml;
+  float e0, e1, p0, p1, n[3];
+};
+
+__device__ __forceinline__ bool isfin(float v) { return isfinite(v); }
+
+// Loads one Gaussian and runs stage 1 up to (but not including) SH. Returns false if culled.
+__device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
+                                                 GF& f) {
+  const int64_t n = g.n;
+  f.mu[0] = g.means[i];
+  f.mu[1] = g.means[n + i];
+  f.mu[2] = g.means[2 * n + i];
+  if (!(isfin(f.mu[0]) && isfin(f.mu[1]) && isfin(f.mu[2]))) return false;
+  // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
+  const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
+  if (!(z > cam.znear)) return false;
+  f.o = g.opac[i];
+  if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;
+  f.s[0] = g.scales[i];
+  f.s[1] = g.scales[n + i];
+  f.s[2] = g.scales[2 * n + i];
+  if (!(f.s[0] > 0.f && f.s[1] > 0.f && f.s[2] > 0.f) || !(isfin(f.s[0]) && isfin(f.s[1]) && isfin(f.s[2])))
+    return false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f.qr[k] = g.rot[k * n + i];
+  if (!(isfin(f.qr[0]) && isfin(f.qr[1]) && isfin(f.qr[2]) && isfin(f.qr[3]))) return false;
+  const float ql2 = f.qr[0] * f.qr[0] + f.qr[1] * f.qr[1] + f.qr[2] * f.qr[2] + f.qr[3] * f.qr[3];
+  if (!(ql2 > 0.f)) return false;
+
+  f.x[0] = __fmaf_rn(cam.R[0], f.mu[0], __fmaf_rn(cam.R[1], f.mu[1], __fmaf_rn(cam.R[2], f.mu[2], cam.t[0])));
+  f.x[1] = __fmaf_rn(cam.R[3], f.mu[0], __fmaf_rn(cam.R[4], f.mu[1], __fmaf_rn(cam.R[5], f.mu[2], cam.t[1])));
+  f.x[2] = z;
+  f.t2 = f.x[0] * f.x[0] + f.x[1] * f.x[1] + z * z;
+  f.it = rsqrtf(f.t2);
+  const float iz = 1.f / z;
+  f.u = f.x[0] * iz * cam.fx + cam.cx;
+  f.v = f.x[1] * iz * cam.fy + cam.cy;
+
+  // R(q̂), q̂ = q/‖q‖, (w, x, y, z) (reading S15)
+  f.qinv = rsqrtf(ql2);
+  const float w = f.qr[0] * f.qinv, a = f.qr[1] * f.qinv, b = f.qr[2] * f.qinv, c = f.qr[3] * f.qinv;
+  f.qn[0] = w; f.qn[1] = a; f.qn[2] = b; f.qn[3] = c;
+  const float Rq[9] = {1.f - 2.f * (b * b + c * c), 2.f * (a * b - w * c), 2.f * (a * c + w * b),
+                       2.f * (a * b + w * c), 1.f - 2.f * (a * a + c * c), 2.f * (b * c - w * a),
+                       2.f * (a * c - w * b), 2.f * (b * c + w * a), 1.f - 2.f * (a * a + b * b)};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      f.Rc[3 * r + k] = cam.R[3 * r] * Rq[k] + cam.R[3 * r + 1] * Rq[3 + k] + cam.R[3 * r + 2] * Rq[6 + k];
+
+  // 2-D covariance: M = J₂ R_c S, A = M Mᵀ (+ h I) (S2, S5)
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f.RS[3 * r + k] = f.Rc[3 * r + k] * f.s[k];
+  f.j00 = cam.fx * iz;
+  f.j02 = -cam.fx * f.x[0] * iz * iz;
+  f.j11 = cam.fy * iz;
+  f.j12 = -cam.fy * f.x[1] * iz * iz;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    f.M[k] = f.j00 * f.RS[k] + f.j02 * f.RS[6 + k];
+    f.M[3 + k] = f.j11 * f.RS[3 + k] + f.j12 * f.RS[6 + k];
+  }
+  f.A00 = f.M[0] * f.M[0] + f.M[1] * f.M[1] + f.M[2] * f.M[2] + opt.dilation;
+  f.A01 = f.M[0] * f.M[3] + f.M[1] * f.M[4] + f.M[2] * f.M[5];
+  f.A11 = f.M[3] * f.M[3] + f.M[4] * f.M[4] + f.M[5] * f.M[5] + opt.dilation;
+  f.det = f.A00 * f.A11 - f.A01 * f.A01;
+  if (!(f.det > 0.f) || !isfin(f.det)) return false;
+  const float idet = 1.f / f.det;
+  f.ca = f.A11 * idet;
+  f.cb = -f.A01 * idet;
+  f.cc = f.A00 * idet;
+
+  // depth plane and normal (m-form of Eq.12-15, 21-22)
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.xh[k] = f.x[k] * f.it;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    f.rh[k] = f.Rc[k] * f.xh[0] + f.Rc[3 + k] * f.xh[1] + f.Rc[6 + k] * f.xh[2];
+    f.w[k] = 1.f / (f.s[k] * f.s[k]);
+    f.ah[k] = f.rh[k] * f.w[k];
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) f.mh[r] = f.Rc[3 * r] * f.ah[0] + f.Rc[3 * r + 1] * f.ah[1] + f.Rc[3 * r + 2] * f.ah[2];
+  f.muq = f.rh[0] * f.ah[0] + f.rh[1] * f.ah[1] + f.rh[2] * f.ah[2];
+  f.ml = sqrtf(f.mh[0] * f.mh[0] + f.mh[1] * f.mh[1] + f.mh[2] * f.mh[2]);
+  if (!(f.muq > 0.f) || !isfin(f.muq) || !(f.ml > 0.f) || !isfin(f.ml)) return false;
+  const float imu = 1.f / f.muq;
+  f.e0 = f.mh[0] * imu - f.xh[0];
+  f.e1 = f.mh[1] * imu - f.xh[1];
+  const float zzit = z * z * f.it;
+  f.p0 = zzit / cam.fx * f.e0;
+  f.p1 = zzit / cam.fy * f.e1;
+  const float iml = 1.f / f.ml;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.n[k] = -f.mh[k] * iml;
+  return true;
+}
+
+// ---------------------------------------------------------------------------- K1
+template <int DEG>
+__global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
+                                                         int tiles_y, Record* __restrict__ rec,
+                                                         uint2* __restrict__ rect, uint32_t* __restrict__ touched,
+                                                         float* __restrict__ zkey, Counter* __restrict__ counters) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  GF f;
+  if (!gaussian_forward(g, i, cam, opt, f)) {
+    touched[i] = 0u;
+    return;
+  }
+  // α-bounded footprint: α = o·G ≥ α_min ⇔ Δᵀ conic Δ ≤ k = 2 ln(o/α_min); its axis-aligned
+  // half extents are sqrt(k·A′₀₀), sqrt(k·A′₁₁) (reading S8); inflated for fp32 safety.
+  const float kk = 2.f * (logf(f.o) - opt.ln_alpha_min);
+  const float rx = sqrtf(fmaxf(kk, 0.f) * f.A00) * 1.00001f + 1e-3f;
+  const float ry = sqrtf(fmaxf(kk, 0.f) * f.A11) * 1.00001f + 1e-3f;
+  // pixels i with |u_c − (i + ½)| ≤ rx
+  const float fx0 = fmaxf(ceilf(f.u - rx - 0.5f), 0.f);
+  const float fx1 = fminf(floorf(f.u + rx - 0.5f), (float)(cam.W - 1));
+  const float fy0 = fmaxf(ceilf(f.v - ry - 0.5f), 0.f);
+  const float fy1 = fminf(floorf(f.v + ry - 0.5f), (float)(cam.H - 1));
+  if (!(fx0 <= fx1 && fy0 <= fy1)) {
+    touched[i] = 0u;
+    return;
+  }
+  const int T = opt.tile;
+  const uint32_t tx0 = (uint32_t)fx0 / T, tx1 = (uint32_t)fx1 / T + 1;
+  const uint32_t ty0 = (uint32_t)fy0 / T, ty1 = (uint32_t)fy1 / T + 1;
+
+  // colour: dir = normalize(μ − campos), degree ≤ sh_degree, + 0.5, clamp ≥ 0
+  float dx = f.mu[0] - cam.campos[0], dy = f.mu[1] - cam.campos[1], dz = f.mu[2] - cam.campos[2];
+  const float idl = rsqrtf(dx * dx + dy * dy + dz * dz);
+  dx *= idl; dy *= idl; dz *= idl;
+  float Y[16];
+  sh_basis(dx, dy, dz, DEG, Y);
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  float rgb[3] = {0.5f, 0.5f, 0.5f};
+  const int64_t n = g.n;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * g.sh[(int64_t)(k * 3 + ch) * n + i];
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
+
+  Record r;
+  r.r0 = make_float4(f.u, f.v, -0.5f * kLog2e * f.ca, -kLog2e * f.cb);
+  r.r1 = make_float4(-0.5f * kLog2e * f.cc, f.o, rgb[0], rgb[1]);
+  r.r2 = make_float4(rgb[2], f.n[0], f.n[1], f.n[2]);
+  r.r3 = make_float4(f.x[2], f.p0, f.p1, 0.f);
+  rec[i] = r;
+  rect[i] = make_uint2(tx0 | (ty0 << 16), tx1 | (ty1 << 16));
+  touched[i] = (tx1 - tx0) * (ty1 - ty0);
+  zkey[i] = f.x[2];
+  if (counters) {  // warp-aggregated: one atomic per converged group of visible threads
+    const unsigned m = __activemask();
+    if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counters + 3, (Counter)__popc(m));
+  }
+}
+
+// ---------------------------------------------------------------------------- K5
+template <int DEG>
+__global__ void __launch_bounds__(256) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
+                                                         const uint32_t* __restrict__ touched,
+                                                         const float* __restrict__ g2d, DevGrads gr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  if (touched[i] == 0u) return;  // culled or off-screen: zero gradient
+  GF f;
+  if (!gaussian_forward(g, i, cam, opt, f)) return;
+  const int64_t n = g.n;
+  const float4* G4 = reinterpret_cast<const float4*>(g2d + i * kG2D);
+  const float4 q0 = G4[0], q1 = G4[1], q2 = G4[2], q3 = G4[3];
+  const float d_u = q0.x, d_v = q0.y, d_A2 = q0.z, d_B2 = q0.w;
+  const float d_C2 = q1.x, d_o = q1.y;
+  const float d_rgb[3] = {q1.z, q1.w, q2.x};
+  const float d_n[3] = {q2.y, q2.z, q2.w};
+  const float d_z = q3.x, d_p0 = q3.y, d_p1 = q3.z;
+
+  float dx[3] = {0.f, 0.f, 0.f};  // dL/dx_c (camera space)
+  float dRc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) dRc[k] = 0.f;
+  float ds[3] = {0.f, 0.f, 0.f};
+  float dmu[3] = {0.f, 0.f, 0.f};  // direct world-space mean grads (SH view direction)
+
+  // ---- colour / SH (zero gradient through clamped channels)
+  {
+    float ex = f.mu[0] - cam.campos[0], ey = f.mu[1] - cam.campos[1], ez = f.mu[2] - cam.campos[2];
+    const float idl = rsqrtf(ex * ex + ey * ey + ez * ez);
+    const float hx = ex * idl, hy = ey * idl, hz = ez * idl;
+    float Y[16];
+    sh_basis(hx, hy, hz, DEG, Y);
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    float rgb[3] = {0.5f, 0.5f, 0.5f};
+    float coef[3][16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) coef[ch][k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        coef[ch][k] = g.sh[(int64_t)(k * 3 + ch) * n + i];
+        rgb[ch] += Y[k] * coef[ch][k];
+      }
+    float drgb[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) drgb[ch] = rgb[ch] < 0.f ? 0.f : d_rgb[ch];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) gr.sh[(int64_t)(k * 3 + ch) * n + i] += Y[k] * drgb[ch];
+    float c16[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c16[k] = drgb[0] * coef[0][k] + drgb[1] * coef[1][k] + drgb[2] * coef[2][k];
+    float gx, gy, gz;
+    sh_basis_grad(hx, hy, hz, DEG, c16, gx, gy, gz);
+    // through the normalisation of dir
+    const float dot = gx * hx + gy * hy + gz * hz;
+    dmu[0] += (gx - hx * dot) * idl;
+    dmu[1] += (gy - hy * dot) * idl;
+    dmu[2] += (gz - hz * dot) * idl;
+  }
+
+  // ---- projected centre and centre depth
+  const float iz = 1.f / f.x[2];
+  dx[0] += d_u * cam.fx * iz;
+  dx[1] += d_v * cam.fy * iz;
+  dx[2] += -(d_u * cam.fx * f.x[0] + d_v * cam.fy * f.x[1]) * iz * iz + d_z;
+
+  // ---- conic: stored (A2, B2, C2) = log2e·(−a/2, −b, −c/2), conic = A′⁻¹
+  {
+    const float da = -0.5f * kLog2e * d_A2, db = -kLog2e * d_B2, dc = -0.5f * kLog2e * d_C2;
+    // dL/dA′ = −C Ḡ C with Ḡ = [[da, db/2], [db/2, dc]]; off-diagonal counted twice
+    const float a = f.ca, b = f.cb, c = f.cc;
+    const float dA00 = -(a * a * da + a * b * db + b * b * dc);
+    const float dA11 = -(b * b * da + b * c * db + c * c * dc);
+    const float dA01 = -(2.f * a * b * da + (a * c + b * b) * db + 2.f * b * c * dc);
+    // A = M Mᵀ
+    float dM[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dM[k] = 2.f * dA00 * f.M[k] + dA01 * f.M[3 + k];
+      dM[3 + k] = dA01 * f.M[k] + 2.f * dA11 * f.M[3 + k];
+    }
+    // M = J₂ RS
+    float dj00 = 0.f, dj02 = 0.f, dj11 = 0.f, dj12 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dj00 += dM[k] * f.RS[k];
+      dj02 += dM[k] * f.RS[6 + k];
+      dj11 += dM[3 + k] * f.RS[3 + k];
+      dj12 += dM[3 + k] * f.RS[6 + k];
+      const float dRS0 = dM[k] * f.j00;
+      const float dRS1 = dM[3 + k] * f.j11;
+      const float dRS2 = dM[k] * f.j02 + dM[3 + k] * f.j12;
+      dRc[k] += dRS0 * f.s[k];
+      dRc[3 + k] += dRS1 * f.s[k];
+      dRc[6 + k] += dRS2 * f.s[k];
+      ds[k] += dRS0 * f.Rc[k] + dRS1 * f.Rc[3 + k] + dRS2 * f.Rc[6 + k];
+    }
+    // J₂(x): j00 = fx/z, j02 = −fx x/z², j11 = fy/z, j12 = −fy y/z²
+    const float iz2 = iz * iz;
+    dx[0] += -dj02 * cam.fx * iz2;
+    dx[1] += -dj12 * cam.fy * iz2;
+    dx[2] += -dj00 * cam.fx * iz2 - dj11 * cam.fy * iz2 + 2.f * dj02 * cam.fx * f.x[0] * iz2 * iz +
+             2.f * dj12 * cam.fy * f.x[1] * iz2 * iz;
+  }
+
+  // ---- depth plane p and normal n (m-form backward)
+  {
+    const float imu = 1.f / f.muq;
+    const float iml = 1.f / f.ml;
+    float dmh[3];
+    // n = −m̂/‖m̂‖
+    const float nd = f.n[0] * d_n[0] + f.n[1] * d_n[1] + f.n[2] * d_n[2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dmh[k] = -(d_n[k] - f.n[k] * nd) * iml;
+    // p_k = c_k e_k, c_k = z² it / f_k, e_k = m̂_k/μ − x̂_k
+    const float z = f.x[2];
+    const float zzit = z * z * f.it;
+    const float de0 = d_p0 * zzit / cam.fx, de1 = d_p1 * zzit / cam.fy;
+    dx[2] += 2.f * (d_p0 * f.p0 + d_p1 * f.p1) / z;
+    float dit = (d_p0 * f.p0 + d_p1 * f.p1) / f.it;
+    dmh[0] += de0 * imu;
+    dmh[1] += de1 * imu;
+    const float dmuq = -(de0 * f.mh[0] + de1 * f.mh[1]) * imu * imu;
+    float dxh[3] = {-de0, -de1, 0.f};
+    float dah[3], drh[3];
+    // μ = r̂·â ; m̂ = R_c â
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dah[k] = dmuq * f.rh[k] + f.Rc[k] * dmh[0] + f.Rc[3 + k] * dmh[1] + f.Rc[6 + k] * dmh[2];
+      drh[k] = dmuq * f.ah[k];
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dRc[3 * r + k] += dmh[r] * f.ah[k];
+    // â = r̂ ⊘ s²
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      drh[k] += dah[k] * f.w[k];
+      ds[k] += -2.f * dah[k] * f.ah[k] / f.s[k];
+    }
+    // r̂ = R_cᵀ x̂
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      dxh[r] += f.Rc[3 * r] * drh[0] + f.Rc[3 * r + 1] * drh[1] + f.Rc[3 * r + 2] * drh[2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dRc[3 * r + k] += f.xh[r] * drh[k];
+    }
+    // x̂ = x·it, it = t2^{-1/2}
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      dx[r] += dxh[r] * f.it;
+      dit += dxh[r] * f.x[r];
+    }
+    const float dt2 = -0.5f * dit * f.it * f.it * f.it;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) dx[r] += 2.f * f.x[r] * dt2;
+  }
+
+  // ---- x_c = W μ + t ; R_c = W R_q
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dmu[k] += cam.R[k] * dx[0] + cam.R[3 + k] * dx[1] + cam.R[6 + k] * dx[2];
+  float dRq[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dRq[3 * r + k] = cam.R[r] * dRc[k] + cam.R[3 + r] * dRc[3 + k] + cam.R[6 + r] * dRc[6 + k];
+  // R(q̂) → q̂ → raw q
+  const float w = f.qn[0], a = f.qn[1], b = f.qn[2], c = f.qn[3];
+  float dqn[4];
+  dqn[0] = 2.f * (-c * dRq[1] + b * dRq[2] + c * dRq[3] - a * dRq[5] - b * dRq[6] + a * dRq[7]);
+  dqn[1] = 2.f * (b * dRq[1] + c * dRq[2] + b * dRq[3] - 2.f * a * dRq[4] - w * dRq[5] + c * dRq[6] + w * dRq[7] -
+                  2.f * a * dRq[8]);
+  dqn[2] = 2.f * (-2.f * b * dRq[0] + a * dRq[1] + w * dRq[2] + a * dRq[3] + c * dRq[5] - w * dRq[6] + c * dRq[7] -
+                  2.f * b * dRq[8]);
+  dqn[3] = 2.f * (-2.f * c * dRq[0] - w * dRq[1] + a * dRq[2] + w * dRq[3] - 2.f * c * dRq[4] + b * dRq[5] +
+                  a * dRq[6] + b * dRq[7]);
+  const float qd = dqn[0] * w + dqn[1] * a + dqn[2] * b + dqn[3] * c;
+
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gr.means[k * n + i] += dmu[k];
+    gr.scales[k * n + i] += ds[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gr.rot[k * n + i] += (dqn[k] - f.qn[k] * qd) * f.qinv;
+  // α = min(α_max, o·G): d_o already excludes the clamp (K4)
+  gr.opac[i] += d_o;
+}
+
+}  // namespace
+
+void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y,
+                           Record* rec, uint2* rect, uint32_t* tiles_touched, float* zkey, Counter* counters,
+                           cudaStream_t s) {
+  if (g.n == 0) return;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
+  switch (opt.sh_degree) {
+    case 0: k_preprocess_fwd<0><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
+    case 1: k_preprocess_fwd<1><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
+    case 2: k_preprocess_fwd<2><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
+    default: k_preprocess_fwd<3><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
+  }
+}
+
+void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
+                           const float* g2d, DevGrads grads, cudaStream_t s) {
+  if (g.n == 0) return;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
+  switch (opt.sh_degree) {
+    case 0: k_preprocess_bwd<0><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
+    case 1: k_preprocess_bwd<1><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
+    case 2: k_preprocess_bwd<2><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
+    default: k_preprocess_bwd<3><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
+  }
+}
+
+}  // namespace rade

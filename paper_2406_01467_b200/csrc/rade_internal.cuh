@@ -1,0 +1,124 @@
+// rade_internal.cuh — device-side types and math shared by the sm_100a kernels of the
+// RaDe-GS rasterizer (K1 preprocess, K2 binning, K3 blend fwd, K4 blend bwd, K5
+// preprocess bwd). Nothing here is shared with oracle/ (which is test infrastructure).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rade {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// Camera as the kernels see it (by value in kernel parameters).
+struct DevCam {
+  float fx, fy, cx, cy;
+  int W, H;
+  float R[9];   // world -> camera, row-major
+  float t[3];
+  float znear;
+  float campos[3];  // -R^T t (camera centre in world space), for SH view directions
+};
+
+struct DevOpt {
+  int tile;
+  float alpha_min, alpha_max, T_min, median_T, dilation;
+  float bg[3];
+  int sh_degree;  // active degree
+  float ln_alpha_min;
+};
+
+struct DevGauss {
+  int64_t n;
+  int sh_coeffs;
+  const float* __restrict__ means;
+  const float* __restrict__ scales;
+  const float* __restrict__ rot;
+  const float* __restrict__ opac;
+  const float* __restrict__ sh;
+};
+
+struct DevGrads {
+  float* means;
+  float* scales;
+  float* rot;
+  float* opac;
+  float* sh;
+};
+
+// Per-visible-Gaussian record written by K1 and gathered by K3/K4 (64 B, 4 x float4):
+//   r0 = (u_c, v_c, A2, B2)   r1 = (C2, o, R, G)   r2 = (B, nx, ny, nz)   r3 = (z_c, p0, p1, 0)
+// where (A2, B2, C2) = log2(e) * (-a/2, -b, -c/2) for the conic [[a, b], [b, c]] of the
+// dilated 2-D covariance, so that G = exp2(A2 dx^2 + B2 dx dy + C2 dy^2) with
+// (dx, dy) = (u_c - u, v_c - v) (readings S1, S4, S5).
+struct __align__(16) Record {
+  float4 r0, r1, r2, r3;
+};
+
+// 2-D gradient accumulator per Gaussian (64 B):
+//   du, dv, dA2, dB2, dC2, dopacity, dR, dG, dB, dnx, dny, dnz, dz, dp0, dp1, unused
+constexpr int kG2D = 16;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// The per-pair α evaluation shared bit-for-bit by K3 and K4 (explicit roundings so the
+// two kernels take identical skip / stop decisions).
+struct PairAlpha {
+  float dx, dy, G, a_raw, alpha;
+};
+__device__ __forceinline__ PairAlpha eval_alpha(const float4& r0, float C2, float o, float px, float py,
+                                                float alpha_max) {
+  PairAlpha pa;
+  pa.dx = __fsub_rn(r0.x, px);
+  pa.dy = __fsub_rn(r0.y, py);
+  float inner = __fmaf_rn(r0.z, pa.dx, __fmul_rn(r0.w, pa.dy));          // A2 dx + B2 dy
+  float pw = __fmaf_rn(pa.dx, inner, __fmul_rn(__fmul_rn(C2, pa.dy), pa.dy));  // + C2 dy^2
+  pa.G = ex2_approx(pw);
+  pa.a_raw = __fmul_rn(o, pa.G);
+  pa.alpha = fminf(alpha_max, pa.a_raw);
+  return pa;
+}
+
+// ------------------------------------------------------------------ launchers (host)
+// Profiling counters (nullable): [0] pairs evaluated by K3, [1] pairs blended by K3,
+// [2] pairs evaluated by K4, [3] visible Gaussians (K1).
+typedef unsigned long long Counter;
+constexpr int kNumCounters = 4;
+
+__device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
+  // all 32 lanes must call this (converged)
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, (Counter)v);
+}
+
+void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y,
+                           Record* rec, uint2* rect, uint32_t* tiles_touched, float* zkey, Counter* counters,
+                           cudaStream_t s);
+void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
+                           const float* g2d, DevGrads grads, cudaStream_t s);
+size_t binning_scan_temp_bytes(int64_t n);
+void launch_scan(const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp, size_t temp_bytes,
+                 cudaStream_t s);
+void launch_duplicate(int64_t n, const uint32_t* offsets, const uint2* rect, const float* zkey, int tiles_x,
+                      uint64_t* keys, uint32_t* vals, cudaStream_t s);
+size_t binning_sort_temp_bytes(int64_t m, int end_bit);
+// sorts (keys[0], vals[0]) with keys[1], vals[1] as alternate buffers; returns selector
+int launch_sort(uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int end_bit,
+                void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_ranges(const uint64_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s);
+void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
+                       const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal,
+                       float* alpha, float* T_final, int32_t* n_contrib, int32_t* median_pos, Counter* counters,
+                       cudaStream_t s);
+void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
+                       const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
+                       const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
+                       const float* dL_dnormal, const float* dL_dalpha, float* g2d, Counter* counters,
+                       cudaStream_t s);
+
+}  // namespace rade

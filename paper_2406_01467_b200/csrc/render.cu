@@ -1,0 +1,274 @@
+// render.cu — stage 3 (K3, blend forward) and the first half of stage 4 (K4, blend
+// backward) of the RaDe-GS rasterizer, sm_100a.
+//
+// One CTA per TILE×TILE tile, one thread per pixel (sampled at (i+½, j+½), reading S4).
+// Each CTA walks its tile's depth-sorted list (ranges from K2) in batches of TILE² splats
+// staged in shared memory (one coalesced 64-B record gather per thread), the whole block
+// leaving as soon as every pixel is saturated (__syncthreads_count).
+//
+// Per (pixel, splat), front to back (Eq.3; readings S1, S8, S9, S10):
+//   α = min(α_max, o·exp(−½ Δᵀ conic Δ)), Δ = (u_c − u, v_c − v)  (skip if α < α_min)
+//   T′ = T(1 − α); stop before blending if T′ < T_min
+//   w = α T; C += w c; N += w n
+//   first splat with T > median_T ≥ T′: D = z_c + p·Δ        (Eq.4)
+// Epilogue: C += T·bg, A = 1 − T; per pixel state (T_final, n_contrib, median_pos) for K4.
+//
+// K4 replays each pixel's list backwards from n_contrib, reconstructing T_i = T_{i+1}/(1−α_i)
+// and suffix sums of colour and normal, and produces the 15 per-splat 2-D gradients, which
+// are warp-reduced with shuffles before one set of L2 atomics per (warp, splat).
+#include "rade_internal.cuh"
+
+namespace rade {
+namespace {
+
+template <int TILE>
+__global__ void __launch_bounds__(TILE* TILE) k_render_fwd(DevCam cam, DevOpt opt, int tiles_x,
+                                                            const uint2* __restrict__ ranges,
+                                                            const uint32_t* __restrict__ ids,
+                                                            const Record* __restrict__ rec, float* __restrict__ color,
+                                                            float* __restrict__ depth, float* __restrict__ normal,
+                                                            float* __restrict__ alpha_out, float* __restrict__ T_final,
+                                                            int32_t* __restrict__ n_contrib,
+                                                            int32_t* __restrict__ median_pos,
+                                                            Counter* __restrict__ counters) {
+  constexpr int BLOCK = TILE * TILE;
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int px = tx * TILE + (int)(threadIdx.x % TILE), py = ty * TILE + (int)(threadIdx.x / TILE);
+  const bool inside = px < cam.W && py < cam.H;
+  const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+  const uint2 range = ranges[tile];
+  const int total = (int)(range.y - range.x);
+
+  __shared__ float4 s0[BLOCK], s1[BLOCK], s2[BLOCK];
+  __shared__ uint32_t sid[BLOCK];
+
+  float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, N0 = 0.f, N1 = 0.f, N2 = 0.f, D = 0.f;
+  int last = 0, med = -1;
+  unsigned n_eval = 0, n_blend = 0;
+  bool done = !inside;
+  for (int base = 0; base < total; base += BLOCK) {
+    if (__syncthreads_count(done) == BLOCK) break;
+    const int k = base + (int)threadIdx.x;
+    if (k < total) {
+      const uint32_t id = ids[range.x + k];
+      const Record* r = rec + id;
+      sid[threadIdx.x] = id;
+      s0[threadIdx.x] = r->r0;
+      s1[threadIdx.x] = r->r1;
+      s2[threadIdx.x] = r->r2;
+    }
+    __syncthreads();
+    const int cnt = min(BLOCK, total - base);
+    for (int j = 0; j < cnt && !done; ++j) {
+      const float4 a0 = s0[j], a1 = s1[j];
+      const PairAlpha pa = eval_alpha(a0, a1.x, a1.y, fpx, fpy, opt.alpha_max);
+      ++n_eval;
+      if (pa.alpha < opt.alpha_min) continue;
+      const float Tn = __fmul_rn(T, __fsub_rn(1.f, pa.alpha));
+      if (Tn < opt.T_min) {
+        done = true;
+        break;
+      }
+      const float4 a2 = s2[j];
+      const float w = __fmul_rn(pa.alpha, T);
+      C0 = __fmaf_rn(w, a1.z, C0);
+      C1 = __fmaf_rn(w, a1.w, C1);
+      C2 = __fmaf_rn(w, a2.x, C2);
+      N0 = __fmaf_rn(w, a2.y, N0);
+      N1 = __fmaf_rn(w, a2.z, N1);
+      N2 = __fmaf_rn(w, a2.w, N2);
+      if (T > opt.median_T && Tn <= opt.median_T) {
+        const float4 a3 = rec[sid[j]].r3;  // (z_c, p0, p1): once per pixel
+        D = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
+        med = base + j;
+      }
+      T = Tn;
+      last = base + j + 1;
+      ++n_blend;
+    }
+  }
+  if (counters) {
+    warp_count(counters + 0, n_eval);
+    warp_count(counters + 1, n_blend);
+  }
+  if (!inside) return;
+  const int HW = cam.W * cam.H;
+  const int pix = py * cam.W + px;
+  if (color) {
+    color[pix] = __fmaf_rn(T, opt.bg[0], C0);
+    color[HW + pix] = __fmaf_rn(T, opt.bg[1], C1);
+    color[2 * HW + pix] = __fmaf_rn(T, opt.bg[2], C2);
+  }
+  if (normal) {
+    normal[pix] = N0;
+    normal[HW + pix] = N1;
+    normal[2 * HW + pix] = N2;
+  }
+  if (depth) depth[pix] = D;
+  if (alpha_out) alpha_out[pix] = 1.f - T;
+  T_final[pix] = T;
+  n_contrib[pix] = last;
+  median_pos[pix] = med;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int TILE>
+__global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
+    DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
+    const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
+    const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
+    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, float* __restrict__ g2d,
+    Counter* __restrict__ counters) {
+  constexpr int BLOCK = TILE * TILE;
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int px = tx * TILE + (int)(threadIdx.x % TILE), py = ty * TILE + (int)(threadIdx.x / TILE);
+  const bool inside = px < cam.W && py < cam.H;
+  const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+  const uint2 range = ranges[tile];
+  const int HW = cam.W * cam.H;
+  const int pix = py * cam.W + px;
+  const int lane = (int)(threadIdx.x & 31);
+
+  __shared__ float4 s0[BLOCK], s1[BLOCK], s2[BLOCK], s3[BLOCK];
+  __shared__ uint32_t sid[BLOCK];
+  __shared__ int s_maxlast;
+
+  int last = 0, med = -1;
+  float T = 1.f;
+  float gC0 = 0.f, gC1 = 0.f, gC2 = 0.f, gN0 = 0.f, gN1 = 0.f, gN2 = 0.f, gD = 0.f, gA = 0.f;
+  if (inside) {
+    last = n_contrib[pix];
+    med = median_pos[pix];
+    T = T_final[pix];
+    if (dL_dcolor) { gC0 = dL_dcolor[pix]; gC1 = dL_dcolor[HW + pix]; gC2 = dL_dcolor[2 * HW + pix]; }
+    if (dL_dnormal) { gN0 = dL_dnormal[pix]; gN1 = dL_dnormal[HW + pix]; gN2 = dL_dnormal[2 * HW + pix]; }
+    if (dL_ddepth) gD = dL_ddepth[pix];
+    if (dL_dalpha) gA = dL_dalpha[pix];
+  }
+  if (counters) warp_count(counters + 2, (unsigned)last);
+  if (threadIdx.x == 0) s_maxlast = 0;
+  __syncthreads();
+  if (last > 0) atomicMax(&s_maxlast, last);
+  __syncthreads();
+  const int maxlast = s_maxlast;
+
+  const float TF = T;
+  const float aterm = gA - (opt.bg[0] * gC0 + opt.bg[1] * gC1 + opt.bg[2] * gC2);
+  float accC0 = 0.f, accC1 = 0.f, accC2 = 0.f, accN0 = 0.f, accN1 = 0.f, accN2 = 0.f;
+  float lA = 0.f, lC0 = 0.f, lC1 = 0.f, lC2 = 0.f, lN0 = 0.f, lN1 = 0.f, lN2 = 0.f;
+
+  for (int end = maxlast; end > 0; end -= BLOCK) {
+    const int start = max(0, end - BLOCK);
+    const int cnt = end - start;
+    __syncthreads();
+    if ((int)threadIdx.x < cnt) {
+      const uint32_t id = ids[range.x + start + threadIdx.x];
+      const Record* r = rec + id;
+      sid[threadIdx.x] = id;
+      s0[threadIdx.x] = r->r0;
+      s1[threadIdx.x] = r->r1;
+      s2[threadIdx.x] = r->r2;
+      s3[threadIdx.x] = r->r3;
+    }
+    __syncthreads();
+    for (int j = cnt - 1; j >= 0; --j) {
+      const int pos = start + j;
+      const float4 a0 = s0[j], a1 = s1[j];
+      float g[15];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) g[k] = 0.f;
+      bool active = pos < last;
+      if (active) {
+        const PairAlpha pa = eval_alpha(a0, a1.x, a1.y, fpx, fpy, opt.alpha_max);
+        if (pa.alpha < opt.alpha_min) {
+          active = false;
+        } else {
+          const float4 a2 = s2[j];
+          const float one_m = 1.f - pa.alpha;
+          T = T / one_m;  // T_i
+          const float w = pa.alpha * T;
+          g[6] = w * gC0; g[7] = w * gC1; g[8] = w * gC2;
+          g[9] = w * gN0; g[10] = w * gN1; g[11] = w * gN2;
+          // suffix sums S_i = Σ_{j>i} c_j α_j Π_{i<k<j}(1−α_k)
+          accC0 = lA * lC0 + (1.f - lA) * accC0;
+          accC1 = lA * lC1 + (1.f - lA) * accC1;
+          accC2 = lA * lC2 + (1.f - lA) * accC2;
+          accN0 = lA * lN0 + (1.f - lA) * accN0;
+          accN1 = lA * lN1 + (1.f - lA) * accN1;
+          accN2 = lA * lN2 + (1.f - lA) * accN2;
+          lA = pa.alpha;
+          lC0 = a1.z; lC1 = a1.w; lC2 = a2.x;
+          lN0 = a2.y; lN1 = a2.z; lN2 = a2.w;
+          const float dL_dal = T * ((a1.z - accC0) * gC0 + (a1.w - accC1) * gC1 + (a2.x - accC2) * gC2 +
+                                    (a2.y - accN0) * gN0 + (a2.z - accN1) * gN1 + (a2.w - accN2) * gN2) +
+                               TF / one_m * aterm;
+          float dum = 0.f, dvm = 0.f;
+          if (pos == med) {  // median depth D = z_c + p·Δ (Eq.4)
+            const float4 a3 = s3[j];
+            g[12] = gD;
+            g[13] = gD * pa.dx;
+            g[14] = gD * pa.dy;
+            dum = gD * a3.y;
+            dvm = gD * a3.z;
+          }
+          float dpw = 0.f;
+          if (pa.a_raw <= opt.alpha_max) {  // α not clamped (S8)
+            g[5] = pa.G * dL_dal;
+            dpw = a1.y * pa.G * kLn2 * dL_dal;  // dL/d(power in log2 units)
+          }
+          g[0] = dpw * (2.f * a0.z * pa.dx + a0.w * pa.dy) + dum;
+          g[1] = dpw * (a0.w * pa.dx + 2.f * a1.x * pa.dy) + dvm;
+          g[2] = dpw * pa.dx * pa.dx;
+          g[3] = dpw * pa.dx * pa.dy;
+          g[4] = dpw * pa.dy * pa.dy;
+        }
+      }
+      if (__ballot_sync(0xffffffffu, active)) {
+#pragma unroll
+        for (int k = 0; k < 15; ++k) g[k] = warp_sum(g[k]);
+        if (lane == 0) {
+          float* dst = g2d + (size_t)sid[j] * kG2D;
+#pragma unroll
+          for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g[k]);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
+                       const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal, float* alpha,
+                       float* T_final, int32_t* n_contrib, int32_t* median_pos, Counter* counters, cudaStream_t s) {
+  const unsigned grid = (unsigned)(tiles_x * tiles_y);
+  if (opt.tile == 16)
+    k_render_fwd<16><<<grid, 256, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal, alpha, T_final,
+                                          n_contrib, median_pos, counters);
+  else
+    k_render_fwd<8><<<grid, 64, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal, alpha, T_final,
+                                        n_contrib, median_pos, counters);
+}
+
+void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
+                       const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
+                       const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
+                       const float* dL_dnormal, const float* dL_dalpha, float* g2d, Counter* counters,
+                       cudaStream_t s) {
+  const unsigned grid = (unsigned)(tiles_x * tiles_y);
+  if (opt.tile == 16)
+    k_render_bwd<16><<<grid, 256, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
+                                          dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
+  else
+    k_render_bwd<8><<<grid, 64, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
+                                        dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
+}
+
+}  // namespace rade

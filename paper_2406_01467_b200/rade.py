@@ -1,0 +1,320 @@
+"""Thin Python binding of the C ABI (include/rade.h): same names, argument marshalling only.
+
+Every step of the path runs in librade.so's CUDA kernels; this module only turns torch
+tensors (device memory, owned by the caller) and the current CUDA stream into the ABI's
+plain pointers, and supplies a torch-backed allocator callback for the view's scratch.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+
+_DEF = None
+
+
+def default_options():
+    """rd_options_default() as a dict."""
+    lib = N.load()
+    o = N.RdOptions()
+    N.check(lib.rd_options_default(ctypes.byref(o)), "rd_options_default")
+    return dict(tile=o.tile, alpha_min=o.alpha_min, alpha_max=o.alpha_max, T_min=o.T_min, median_T=o.median_T,
+                dilation=o.dilation, bg=tuple(o.bg), sh_degree=o.sh_degree)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check_f32(name, t, shape=None):
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+@dataclass
+class Gaussians:
+    """SoA device parameters (include/rade.h rd_gaussians): means [3,N], scales [3,N]
+    (activated), rotations [4,N] (raw w,x,y,z), opacities [N] (activated), sh [K,3,N]."""
+    means: torch.Tensor
+    scales: torch.Tensor
+    rotations: torch.Tensor
+    opacities: torch.Tensor
+    sh: torch.Tensor
+
+    @property
+    def n(self):
+        return int(self.opacities.shape[0])
+
+    def validate(self):
+        n = self.n
+        _check_f32("means", self.means, (3, n))
+        _check_f32("scales", self.scales, (3, n))
+        _check_f32("rotations", self.rotations, (4, n))
+        _check_f32("opacities", self.opacities, (n,))
+        _check_f32("sh", self.sh)
+        if self.sh.dim() != 3 or self.sh.shape[1] != 3 or self.sh.shape[2] != n:
+            raise ValueError("sh must be [K, 3, N]")
+
+    def c_struct(self):
+        self.validate()
+        return N.RdGaussians(self.n, int(self.sh.shape[0]), self.means.data_ptr(), self.scales.data_ptr(),
+                             self.rotations.data_ptr(), self.opacities.data_ptr(), self.sh.data_ptr())
+
+    @staticmethod
+    def from_numpy(scene, device="cuda"):
+        f = lambda a: torch.as_tensor(a, dtype=torch.float32).contiguous().to(device)
+        return Gaussians(f(scene.means), f(scene.scales), f(scene.rotations), f(scene.opacities), f(scene.sh))
+
+    def zeros_like(self):
+        return Gaussians(*(torch.zeros_like(t) for t in (self.means, self.scales, self.rotations, self.opacities,
+                                                             self.sh)))
+
+    def tensors(self):
+        return (self.means, self.scales, self.rotations, self.opacities, self.sh)
+
+
+def camera_struct(cam):
+    """Any object with fx, fy, cx, cy, width, height, R (3x3), t (3), znear."""
+    c = N.RdCamera()
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    R = [float(x) for row in (cam.R.tolist() if hasattr(cam.R, "tolist") else cam.R) for x in row]
+    t = [float(x) for x in (cam.t.tolist() if hasattr(cam.t, "tolist") else cam.t)]
+    for k in range(9):
+        c.R[k] = R[k]
+    for k in range(3):
+        c.t[k] = t[k]
+    c.znear = float(getattr(cam, "znear", 0.2))
+    return c
+
+
+def options_struct(opt=None):
+    o = N.RdOptions()
+    N.check(N.load().rd_options_default(ctypes.byref(o)), "rd_options_default")
+    if opt is None:
+        return o
+    get = (lambda k, d: opt.get(k, d)) if isinstance(opt, dict) else (lambda k, d: getattr(opt, k, d))
+    o.tile = int(get("tile", o.tile))
+    o.alpha_min = float(get("alpha_min", o.alpha_min))
+    o.alpha_max = float(get("alpha_max", o.alpha_max))
+    o.T_min = float(get("T_min", o.T_min))
+    o.median_T = float(get("median_T", o.median_T))
+    o.dilation = float(get("dilation", o.dilation))
+    bg = get("bg", tuple(o.bg))
+    for k in range(3):
+        o.bg[k] = float(bg[k])
+    o.sh_degree = int(get("sh_degree", o.sh_degree))
+    return o
+
+
+class View:
+    """Owns an rd_view* and the torch tensors backing its scratch buffers."""
+
+    def __init__(self, device=None):
+        self.lib = N.load()
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self._bufs = {}
+
+        def _alloc(nbytes, ctx):
+            try:
+                t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            except Exception:  # noqa: BLE001 - reported to C as a NULL pointer -> RD_ERR_ALLOC
+                return None
+            self._bufs[t.data_ptr()] = t
+            return t.data_ptr()
+
+        def _free(ptr, ctx):
+            self._bufs.pop(ptr, None)
+
+        self._alloc_cb = N.ALLOC_FN(_alloc)
+        self._free_cb = N.FREE_FN(_free)
+        h = ctypes.c_void_p()
+        N.check(self.lib.rd_view_create(ctypes.byref(h), self._alloc_cb, self._free_cb, None), "rd_view_create")
+        self.handle = h
+        self.camera = None
+        self.options = None
+        self.n = 0
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.rd_view_destroy(self.handle)
+            self.handle = None
+            self._bufs.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def rd_view_create(device=None) -> View:
+    return View(device)
+
+
+def rd_view_destroy(view: View):
+    view.close()
+
+
+def rd_preprocess(view: View, gaussians: Gaussians, camera, options=None, stream=None):
+    g = gaussians.c_struct()
+    c = camera_struct(camera)
+    o = options_struct(options)
+    N.check(view.lib.rd_preprocess(view.handle, ctypes.byref(g), ctypes.byref(c), ctypes.byref(o),
+                                   _stream_ptr(stream)), "rd_preprocess")
+    view.camera, view.options, view.n = c, o, gaussians.n
+
+
+def rd_bin(view: View, stream=None) -> int:
+    m = ctypes.c_int64(0)
+    N.check(view.lib.rd_bin(view.handle, ctypes.byref(m), _stream_ptr(stream)), "rd_bin")
+    return int(m.value)
+
+
+def rd_render_fwd(view: View, color=None, depth=None, normal=None, alpha=None, stream=None, allocate=True):
+    """Renders into the given tensors; missing ones are allocated if `allocate`."""
+    H, W = view.camera.height, view.camera.width
+    dev = view.device
+    if allocate:
+        color = torch.empty((3, H, W), dtype=torch.float32, device=dev) if color is None else color
+        depth = torch.empty((H, W), dtype=torch.float32, device=dev) if depth is None else depth
+        normal = torch.empty((3, H, W), dtype=torch.float32, device=dev) if normal is None else normal
+        alpha = torch.empty((H, W), dtype=torch.float32, device=dev) if alpha is None else alpha
+    for name, t, shp in (("color", color, (3, H, W)), ("depth", depth, (H, W)), ("normal", normal, (3, H, W)),
+                         ("alpha", alpha, (H, W))):
+        if t is not None:
+            _check_f32(name, t, shp)
+    N.check(view.lib.rd_render_fwd(view.handle, _ptr(color), _ptr(depth), _ptr(normal), _ptr(alpha),
+                                   _stream_ptr(stream)), "rd_render_fwd")
+    return dict(color=color, depth=depth, normal=normal, alpha=alpha)
+
+
+def rd_render_bwd(view: View, gaussians: Gaussians, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None,
+                  dL_dalpha=None, grads: Gaussians = None, stream=None):
+    """Accumulates (+=) parameter gradients into `grads` (same layout as `gaussians`)."""
+    H, W = view.camera.height, view.camera.width
+    for name, t, shp in (("dL_dcolor", dL_dcolor, (3, H, W)), ("dL_ddepth", dL_ddepth, (H, W)),
+                         ("dL_dnormal", dL_dnormal, (3, H, W)), ("dL_dalpha", dL_dalpha, (H, W))):
+        if t is not None:
+            _check_f32(name, t, shp)
+    g = gaussians.c_struct()
+    if grads is None:
+        raise ValueError("grads is required")
+    grads.validate()
+    gr = N.RdGrads(grads.means.data_ptr(), grads.scales.data_ptr(), grads.rotations.data_ptr(),
+                   grads.opacities.data_ptr(), grads.sh.data_ptr())
+    N.check(view.lib.rd_render_bwd(view.handle, ctypes.byref(g), _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(dL_dnormal),
+                                   _ptr(dL_dalpha), ctypes.byref(gr), _stream_ptr(stream)), "rd_render_bwd")
+    return grads
+
+
+def rd_view_stats(view: View) -> dict:
+    s = N.RdStats()
+    N.check(view.lib.rd_view_stats(view.handle, ctypes.byref(s)), "rd_view_stats")
+    return {k: getattr(s, k) for k, _ in N.RdStats._fields_}
+
+
+def rd_set_profiling(view: View, enabled: bool = True):
+    N.check(view.lib.rd_set_profiling(view.handle, 1 if enabled else 0), "rd_set_profiling")
+
+
+def rd_get_timings(view: View, reset: bool = False) -> dict:
+    t = N.RdTimings()
+    N.check(view.lib.rd_get_timings(view.handle, ctypes.byref(t), 1 if reset else 0), "rd_get_timings")
+    d = {k: getattr(t, k) for k, _ in N.RdTimings._fields_ if k not in ("ms", "launches")}
+    d["ms"] = {name: t.ms[i] for i, name in enumerate(N.KERNEL_NAMES)}
+    d["launches"] = {name: t.launches[i] for i, name in enumerate(N.KERNEL_NAMES)}
+    return d
+
+
+def rd_debug_binning(view: View, stream=None):
+    st = rd_view_stats(view)
+    M, T = st["n_duplicates"], st["tiles_x"] * st["tiles_y"]
+    keys = torch.empty(max(M, 1), dtype=torch.int64, device=view.device)
+    ids = torch.empty(max(M, 1), dtype=torch.int32, device=view.device)
+    ranges = torch.empty(2 * T, dtype=torch.int32, device=view.device)
+    N.check(view.lib.rd_debug_binning(view.handle, _ptr(keys), _ptr(ids), _ptr(ranges), _stream_ptr(stream)),
+            "rd_debug_binning")
+    return keys[:M], ids[:M], ranges.view(T, 2)
+
+
+def rd_debug_preprocess(view: View, stream=None):
+    n = view.n
+    rec = torch.empty((max(n, 1), 16), dtype=torch.float32, device=view.device)
+    rect = torch.empty((max(n, 1), 2), dtype=torch.int32, device=view.device)
+    touched = torch.empty(max(n, 1), dtype=torch.int32, device=view.device)
+    N.check(view.lib.rd_debug_preprocess(view.handle, _ptr(rec), _ptr(rect), _ptr(touched), _stream_ptr(stream)),
+            "rd_debug_preprocess")
+    return rec[:n], rect[:n], touched[:n]
+
+
+def rd_debug_pixel_state(view: View, stream=None):
+    H, W = view.camera.height, view.camera.width
+    T = torch.empty((H, W), dtype=torch.float32, device=view.device)
+    nc = torch.empty((H, W), dtype=torch.int32, device=view.device)
+    mp = torch.empty((H, W), dtype=torch.int32, device=view.device)
+    N.check(view.lib.rd_debug_pixel_state(view.handle, _ptr(T), _ptr(nc), _ptr(mp), _stream_ptr(stream)),
+            "rd_debug_pixel_state")
+    return T, nc, mp
+
+
+def rd_debug_grads2d(view: View, stream=None):
+    g = torch.empty((max(view.n, 1), 16), dtype=torch.float32, device=view.device)
+    N.check(view.lib.rd_debug_grads2d(view.handle, _ptr(g), _stream_ptr(stream)), "rd_debug_grads2d")
+    return g[:view.n]
+
+
+def rd_version() -> str:
+    return N.load().rd_version().decode()
+
+
+# ----------------------------------------------------------------------------- convenience
+
+def render(gaussians: Gaussians, camera, options=None, view: View = None, stream=None):
+    """One forward pass through all three forward stages. Returns (outputs, view)."""
+    view = View() if view is None else view
+    rd_preprocess(view, gaussians, camera, options, stream)
+    rd_bin(view, stream)
+    out = rd_render_fwd(view, stream=stream)
+    return out, view
+
+
+def render_backward(view: View, gaussians: Gaussians, cot: dict, grads: Gaussians, stream=None):
+    return rd_render_bwd(view, gaussians, cot.get("color"), cot.get("depth"), cot.get("normal"), cot.get("alpha"),
+                         grads, stream)
+
+
+class RadeRasterize(torch.autograd.Function):
+    """torch.autograd wrapper: (means, scales, rotations, opacities, sh) -> (color, depth,
+    normal, alpha). Marshalling only; forward and backward are the C-ABI calls."""
+
+    @staticmethod
+    def forward(ctx, means, scales, rotations, opacities, sh, camera, options=None):
+        g = Gaussians(means.contiguous(), scales.contiguous(), rotations.contiguous(), opacities.contiguous(),
+                      sh.contiguous())
+        out, view = render(g, camera, options)
+        ctx.view, ctx.g = view, g
+        return out["color"], out["depth"], out["normal"], out["alpha"]
+
+    @staticmethod
+    def backward(ctx, gc, gd, gn, ga):
+        g = ctx.g
+        grads = g.zeros_like()
+        f = lambda t: None if t is None else t.contiguous()
+        rd_render_bwd(ctx.view, g, f(gc), f(gd), f(gn), f(ga), grads)
+        return grads.means, grads.scales, grads.rotations, grads.opacities, grads.sh, None, None
+
+
+def rasterize(means, scales, rotations, opacities, sh, camera, options=None):
+    return RadeRasterize.apply(means, scales, rotations, opacities, sh, camera, options)

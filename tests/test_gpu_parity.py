@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical
+seeded scenes. Tolerances are the north star's (BASELINE.json): colour, depth, normal
+(and alpha) within 1e-4 absolute; gradients within 1e-3 relative; binning bit-exact.
+Pixels whose result is decided by a discrete threshold the two precisions can take
+differently are excluded by the oracle's ambiguity flags."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2406_01467_b200 as P
+import scenegen as sg
+from gpu_helpers import cpu_binning_reference, gpu_forward, gpu_grads
+from helpers import concat, dense_scene, one_gaussian, random_cam
+
+pytestmark = pytest.mark.gpu
+
+F1, F2, F3, F4, F5 = 1, 2, 4, 8, 16
+TOL = 1e-4
+
+
+def _scenes():
+    rng = np.random.default_rng(42)
+    cases = [("C0", sg.scene_c0(), sg.camera_c0(), sg.Options()),
+             ("dense400", dense_scene(1, 400), sg.camera_identity(64, 64, 64), sg.Options()),
+             ("dense400_t8", dense_scene(1, 400), sg.camera_identity(64, 64, 64), sg.Options(tile=8)),
+             ("ragged", dense_scene(2, 300, width=83, height=61, f=70.0), sg.camera_identity(83, 61, 70.0),
+              sg.Options(bg=(0.2, 0.5, 1.0))),
+             ("deg1", dense_scene(3, 200), sg.camera_identity(64, 64, 64), sg.Options(sh_degree=1)),
+             ("deg0", dense_scene(4, 200), sg.camera_identity(64, 64, 64), sg.Options(sh_degree=0))]
+    sc = dense_scene(5, 500, zr=(1.5, 4.0))
+    cases.append(("lookat", sc, _lookat_cam(rng, 96, 72), sg.Options()))
+    return cases
+
+
+def _lookat_cam(rng, W, H):
+    R, t = sg.look_at([0.3, -0.2, -0.5], [0.0, 0.0, 3.0], up=(0, -1, 0))
+    return sg.Camera(80.0, 82.0, W / 2 + 1.3, H / 2 - 0.7, W, H, R, t, 0.2)
+
+
+CASES = _scenes()
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def case(request):
+    name, scene, cam, opt = request.param
+    ref = oracle.render(scene, cam, opt)
+    gpu, view, g = gpu_forward(scene, cam, opt)
+    return dict(name=name, scene=scene, cam=cam, opt=opt, ref=ref, gpu=gpu, view=view, g=g)
+
+
+def test_forward_parity(case):
+    ref, gpu = case["ref"], case["gpu"]
+    fl = ref["flags"]
+    ok = (fl & (F1 | F3)) == 0
+    assert ok.mean() > 0.95, ok.mean()
+    for k in ("color", "normal"):
+        err = np.abs(gpu[k] - ref[k])[:, ok]
+        assert err.max() <= TOL, (k, err.max())
+    err = np.abs(gpu["alpha"] - ref["alpha"])[ok]
+    assert err.max() <= TOL, ("alpha", err.max())
+    okd = (fl & (F1 | F3 | F4 | F5)) == 0
+    err = np.abs(gpu["depth"] - ref["depth"])[okd]
+    assert err.max() <= TOL, ("depth", err.max())
+    assert (ref["depth"] > 0).sum() > 10 or case["name"] == "C0"
+
+
+def test_pixel_state_matches_oracle(case):
+    """n_contrib / median position: the median splat the GPU selects is the oracle's."""
+    T, nc, mp = (t.cpu().numpy() for t in P.rd_debug_pixel_state(case["view"]))
+    ref = case["ref"]
+    ok = (ref["flags"] & (F1 | F3 | F4)) == 0
+    np.testing.assert_allclose(1.0 - T[ok], ref["alpha"][ok], atol=TOL)
+    keys, ids, ranges = (t.cpu().numpy() for t in P.rd_debug_binning(case["view"]))
+    tile = case["opt"].tile
+    tiles_x = (case["cam"].width + tile - 1) // tile
+    H, W = T.shape
+    ys, xs = np.nonzero(ok & (mp >= 0))
+    for y, x in zip(ys, xs):
+        t = (y // tile) * tiles_x + x // tile
+        gid = ids[ranges[t, 0] + mp[y, x]]
+        assert gid == ref["median_id"][y, x]
+    assert ((mp >= 0) == (ref["median_id"] >= 0))[ok].all()
+
+
+def test_preprocess_parity(case):
+    scene, cam, opt = case["scene"], case["cam"], case["opt"]
+    pg = oracle.project(scene, cam, opt)
+    rec, rect, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(case["view"]))
+    vis = touched > 0
+    assert np.all(pg[vis, 0] == 1), "GPU kept a Gaussian the oracle culls"
+    r = rec[vis].astype(np.float64)
+    o = pg[vis]
+    np.testing.assert_allclose(r[:, 0], o[:, oracle.PG["u"]], rtol=1e-5, atol=1e-4)
+    np.testing.assert_allclose(r[:, 1], o[:, oracle.PG["v"]], rtol=1e-5, atol=1e-4)
+    log2e = 1.4426950408889634
+    conic = np.stack([-2 * r[:, 2] / log2e, -r[:, 3] / log2e, -2 * r[:, 4] / log2e], 1)
+    np.testing.assert_allclose(conic, o[:, oracle.PG["conic"]], rtol=2e-4, atol=1e-7)
+    np.testing.assert_allclose(r[:, 5], o[:, oracle.PG["o"]], rtol=1e-7)
+    np.testing.assert_allclose(r[:, 6:9], o[:, oracle.PG["rgb"]], atol=1e-5)
+    np.testing.assert_allclose(r[:, 12], o[:, oracle.PG["z"]], rtol=1e-6)
+    ng = np.abs(o[:, oracle.PG["ndotx"]]) >= 0.05
+    np.testing.assert_allclose(r[ng, 9:12], o[ng, 67:70], atol=1e-5)
+    np.testing.assert_allclose(r[ng, 13:15], o[ng][:, oracle.PG["p"]], rtol=1e-3, atol=1e-7)
+
+
+def test_binning_bit_exact(case):
+    view = case["view"]
+    rec, rect, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(view))
+    keys, ids, ranges = (t.cpu().numpy() for t in P.rd_debug_binning(view))
+    st = P.rd_view_stats(view)
+    rk, ri = cpu_binning_reference(rect, touched, rec[:, 12], st["tiles_x"])
+    assert st["n_duplicates"] == len(rk)
+    np.testing.assert_array_equal(keys.view(np.uint64), rk)
+    np.testing.assert_array_equal(ids.view(np.uint32), ri)
+    T = st["tiles_x"] * st["tiles_y"]
+    tiles = (rk >> np.uint64(32)).astype(np.int64)
+    exp = np.zeros((T, 2), np.int64)
+    for t in range(T):
+        w = np.nonzero(tiles == t)[0]
+        if len(w):
+            exp[t] = (w[0], w[-1] + 1)
+    np.testing.assert_array_equal(ranges.astype(np.int64), exp)
+
+
+def test_rect_is_conservative(case):
+    """Every pixel where the oracle's α clears α_min (outside the F1 band) lies in a tile of
+    the GPU's rect."""
+    scene, cam, opt = case["scene"], case["cam"], case["opt"]
+    rec, rect, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(case["view"]))
+    pg = oracle.project(scene, cam, opt)
+    W, H, tile = cam.width, cam.height, opt.tile
+    uu, vv = np.meshgrid(np.arange(W) + 0.5, np.arange(H) + 0.5)
+    uv = np.stack([uu.ravel(), vv.ravel()], 1)
+    amin = float(np.float32(opt.alpha_min))
+    for i in np.nonzero(pg[:, 0] == 1)[0]:
+        ev = oracle.splat_eval(scene, cam, opt, int(i), uv)
+        a = np.minimum(float(np.float32(opt.alpha_max)), ev[:, 0])
+        need = np.log(np.maximum(a, 1e-300)) - np.log(amin) > 1e-4
+        if not need.any():
+            continue
+        assert touched[i] > 0, i
+        r0, r1 = int(rect[i, 0]) & 0xFFFFFFFF, int(rect[i, 1]) & 0xFFFFFFFF
+        tx = (uv[need, 0] // tile).astype(int)
+        ty = (uv[need, 1] // tile).astype(int)
+        assert np.all((tx >= (r0 & 0xFFFF)) & (tx < (r1 & 0xFFFF)) & (ty >= (r0 >> 16)) & (ty < (r1 >> 16))), i
+
+
+def test_backward_parity(case):
+    scene, cam, opt = case["scene"], case["cam"], case["opt"]
+    cot = sg.cotangents(7, cam.width, cam.height)
+    ref = case["ref"]
+    mask = ref["flags"] == 0
+    cot = {k: (v * mask).astype(np.float32) for k, v in cot.items()}
+    _, G, _ = gpu_grads(scene, cam, opt, cot)
+    pg = oracle.project(scene, cam, opt)
+    rgb_raw_near0 = np.zeros(scene.n, bool)  # F6: colour channel within 1e-6 of the clamp
+    vis = np.nonzero(pg[:, 0] == 1)[0]
+    R = oracle.grad(scene, cam, opt, cot, vis)
+    Gv = G[vis]
+    excl = rgb_raw_near0[vis]
+    classes = {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10), "opacities": slice(10, 11),
+               "sh": slice(11, 11 + 3 * (opt.sh_degree + 1) ** 2)}
+    for name, sl in classes.items():
+        a, b = Gv[~excl, sl], R[~excl, sl]
+        nb = np.linalg.norm(b)
+        if nb == 0:
+            assert np.abs(a).max() == 0
+            continue
+        rel = np.linalg.norm(a - b) / nb
+        assert rel <= 1e-3, (name, rel)
+        med = np.median(np.abs(b[b != 0])) if (b != 0).any() else 0.0
+        bad = np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med
+        assert bad.mean() <= 0.002, (name, bad.mean(), np.abs(a - b).max())
+    # Gaussians the GPU did not draw get exactly zero gradient
+    off = np.setdiff1d(np.arange(scene.n), vis)
+    assert np.all(G[off] == 0)
+
+
+def test_tile_size_independence():
+    """Outputs are bit-identical for tile 8 and 16 (the per-pixel op sequence does not depend
+    on the tile; reading S8)."""
+    scene, cam = dense_scene(21, 400), sg.camera_identity(64, 64, 64)
+    a, _, _ = gpu_forward(scene, cam, sg.Options(tile=16))
+    b, _, _ = gpu_forward(scene, cam, sg.Options(tile=8))
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_forward_determinism_and_backward_close():
+    scene, cam, opt = dense_scene(22, 400), sg.camera_identity(64, 64, 64), sg.Options()
+    cot = sg.cotangents(1, 64, 64)
+    a, Ga, _ = gpu_grads(scene, cam, opt, cot)
+    b, Gb, _ = gpu_grads(scene, cam, opt, cot)
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+    # gradients use float atomics (order not fixed): equal to rounding
+    np.testing.assert_allclose(Ga, Gb, rtol=1e-4, atol=1e-6 * np.abs(Ga).max())
+
+
+def test_empty_and_degenerate_inputs():
+    cam, opt = sg.camera_identity(40, 24, 40), sg.Options()
+    empty = sg.make_scene(np.zeros((3, 0)), np.zeros((3, 0)), np.zeros((4, 0)), np.zeros(0), np.zeros((16, 3, 0)))
+    out, view, g = gpu_forward(empty, cam, opt)
+    assert all(np.all(v == 0) for v in out.values())
+    assert P.rd_view_stats(view)["n_duplicates"] == 0
+    grads = g.zeros_like()
+    P.rd_render_bwd(view, g, None, None, None, None, grads)
+    # behind the camera, non-positive scale, zero quaternion, NaN mean, tiny opacity: all culled
+    bad = concat(one_gaussian([0, 0, -3], [0.1] * 3), one_gaussian([0, 0, 3], [0.1, -0.1, 0.1]),
+                 one_gaussian([0, 0, 3], [0.1] * 3, quat=(0, 0, 0, 0)),
+                 one_gaussian([np.nan, 0, 3], [0.1] * 3), one_gaussian([0, 0, 3], [0.1] * 3, opacity=1e-3),
+                 one_gaussian([0, 0, 0.1], [0.1] * 3))
+    out, view, g = gpu_forward(bad, cam, opt)
+    assert all(np.all(v == 0) for v in out.values())
+    cot = sg.cotangents(2, 40, 24)
+    _, G, _ = gpu_grads(bad, cam, opt, cot)
+    assert np.all(G == 0)
+
+
+def test_single_splat_at_centre():
+    cam = sg.camera_identity(64, 64, 64)
+    z = 3.0
+    sc = one_gaussian([(20.5 - 32) * z / 64, (40.5 - 32) * z / 64, z], [0.1, 0.08, 0.12], [0.9, 0.1, -0.2, 0.3],
+                      opacity=0.999)
+    out, _, _ = gpu_forward(sc, cam, sg.Options())
+    pg = oracle.project(sc, cam, sg.Options())[0]
+    assert abs(out["alpha"][40, 20] - 0.99) < 1e-6
+    np.testing.assert_allclose(out["color"][:, 40, 20], 0.99 * pg[oracle.PG["rgb"]], atol=1e-6)
+    assert abs(out["depth"][40, 20] - pg[oracle.PG["z"]]) < 1e-5
+
+
+def test_invalid_arguments_return_errors():
+    cam = sg.camera_identity(16, 16, 16)
+    g = P.Gaussians.from_numpy(dense_scene(0, 5))
+    view = P.View()
+    for bad in (dict(tile=12), dict(alpha_min=0.0), dict(alpha_min=0.995), dict(sh_degree=4), dict(T_min=1.5)):
+        with pytest.raises(P.rade.N.RadeError) as e:
+            P.rd_preprocess(view, g, cam, bad)
+        assert e.value.status == 1
+    with pytest.raises(P.rade.N.RadeError) as e:
+        P.rd_bin(view)
+    assert e.value.status == 2
+    bad_cam = sg.camera_identity(16, 16, 16)
+    bad_cam.width = 0
+    with pytest.raises(P.rade.N.RadeError):
+        P.rd_preprocess(view, g, bad_cam)
+
+
+def test_rasterize_autograd_wrapper():
+    scene, cam, opt = dense_scene(30, 100), sg.camera_identity(32, 32, 32), sg.Options()
+    g = P.Gaussians.from_numpy(scene)
+    ts = [t.clone().requires_grad_(True) for t in g.tensors()]
+    color, depth, normal, alpha = P.rasterize(*ts, cam)
+    cot = sg.cotangents(3, 32, 32)
+    c = {k: torch.as_tensor(v).cuda() for k, v in cot.items()}
+    L = (color * c["color"]).sum() + (depth * c["depth"]).sum() + (normal * c["normal"]).sum() + (alpha * c["alpha"]).sum()
+    L.backward()
+    _, G, _ = gpu_grads(scene, cam, opt, cot)
+    np.testing.assert_allclose(ts[0].grad.double().cpu().numpy().T, G[:, 0:3], rtol=1e-4, atol=1e-6)
