@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,9 +36,20 @@ rd_status fail(rd_status s, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(RD_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
 
+// RADE_SYNC_CHECK=1 in the environment synchronises after every launch so a device fault
+// is attributed to the kernel that raised it (debugging only).
+bool sync_check() {
+  static const bool on = [] {
+    const char* e = getenv("RADE_SYNC_CHECK");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 #define RD_CHECK_LAUNCH(what)                                                                       \
   do {                                                                                              \
     cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ == cudaSuccess && sync_check()) e_ = cudaDeviceSynchronize();                            \
     if (e_ != cudaSuccess) return fail(RD_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e_)); \
   } while (0)
 

@@ -17,26 +17,68 @@
 namespace rade {
 namespace {
 
+// Warp-cooperative emission: a warp owns 32 consecutive Gaussians, whose outputs are
+// contiguous in [start(first), end(last)). The warp walks that span 32 outputs at a time;
+// output t belongs to the first lane whose inclusive warp-prefix exceeds t (a 5-step binary
+// search over shuffled prefixes),
+// whose rect / key are fetched by shuffle. Stores are fully coalesced and a large splat no
+// longer serialises one thread. Per-Gaussian output order is row-major over its rect.
 __global__ void __launch_bounds__(256) k_duplicate(int64_t n, const uint32_t* __restrict__ offsets,
                                                     const uint2* __restrict__ rect, const float* __restrict__ zkey,
                                                     int tiles_x, uint64_t* __restrict__ keys,
                                                     uint32_t* __restrict__ vals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t end = offsets[i];
-  const uint32_t start = i == 0 ? 0u : offsets[i - 1];
-  if (start == end) return;
-  const uint2 r = rect[i];
-  const uint32_t x0 = r.x & 0xffffu, y0 = r.x >> 16, x1 = r.y & 0xffffu, y1 = r.y >> 16;
-  const uint64_t zb = (uint64_t)__float_as_uint(zkey[i]);
-  uint32_t o = start;
-  for (uint32_t ty = y0; ty < y1; ++ty)
-    for (uint32_t tx = x0; tx < x1; ++tx) {
-      const uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + tx;
-      keys[o] = (tile << 32) | zb;
-      vals[o] = (uint32_t)i;
-      ++o;
+  const int lane = (int)(threadIdx.x & 31);
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  if (base >= n) return;  // whole warp out of range
+  const int64_t i = base + lane;
+  uint32_t start = 0, end = 0;
+  if (i < n) {
+    end = offsets[i];
+    start = i == 0 ? 0u : offsets[i - 1];
+  } else {
+    end = start = offsets[n - 1];
+  }
+  const uint32_t cnt = end - start;
+  uint32_t x0 = 0, y0 = 0, w = 1, zb = 0;
+  if (cnt) {
+    const uint2 r = rect[i];
+    x0 = r.x & 0xffffu;
+    y0 = r.x >> 16;
+    w = (r.y & 0xffffu) - x0;
+    zb = __float_as_uint(zkey[i]);
+  }
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t excl = incl - cnt;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t wstart = __shfl_sync(0xffffffffu, start, 0);
+  for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+    const uint32_t t = t0 + lane;
+    // owner = first lane whose inclusive prefix exceeds t (binary search over shuffled prefixes)
+    int owner = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + s - 1);
+      if (v <= t) owner += s;
     }
+    owner &= 31;
+    const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, owner);
+    const uint32_t o_x0 = __shfl_sync(0xffffffffu, x0, owner);
+    const uint32_t o_y0 = __shfl_sync(0xffffffffu, y0, owner);
+    const uint32_t o_w = __shfl_sync(0xffffffffu, w, owner);
+    const uint32_t o_zb = __shfl_sync(0xffffffffu, zb, owner);
+    if (t < total) {
+      const uint32_t li = t - o_excl;
+      const uint32_t ty = o_y0 + li / o_w, tx = o_x0 + li % o_w;
+      const uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + tx;
+      keys[wstart + t] = (tile << 32) | (uint64_t)o_zb;
+      vals[wstart + t] = (uint32_t)(base + owner);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys, int64_t m,

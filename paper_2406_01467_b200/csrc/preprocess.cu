@@ -96,26 +96,36 @@ __device__ __forceinline__ void sh_basis_grad(float x, float y, float z, int deg
   gy += kC3_6 * (-6.f * x * y) * c[15];
 }
 
-// Forward quantities of one Gaussian (registers only).
+// Forward quantities of one Gaussian (registers only). S = double in K1 (HBM-bound, and
+// B200's FP64 pipe is fast: the geometry — conic, plane p, normal n — is then accurate to
+// fp32 rounding of the stored results even for flat, near-grazing splats), S = float in K5.
+template <typename S>
 struct GF {
   float mu[3], s[3], qr[4], o;
-  float qinv, qn[4];
-  float Rc[9];  // W R(q̂), row-major
-  float x[3], t2, it;
-  float u, v;
-  float RS[9];  // Rc diag(s)
-  float j00, j02, j11, j12;
-  float M[6];   // J₂ RS, rows 0..1
-  float A00, A01, A11, det, ca, cb, cc;
-  float xh[3], rh[3], w[3], ah[3], mh[3], muq, ml;
-  float e0, e1, p0, p1, n[3];
+  float zkey;   // the fp32 sort key of reading S7 (also the stored z_c)
+  S qinv, qn[4];
+  S Rc[9];  // W R(q̂), row-major
+  S x[3], t2, it;
+  S u, v;
+  S RS[9];  // Rc diag(s)
+  S j00, j02, j11, j12;
+  S M[6];   // J₂ RS, rows 0..1
+  S A00, A01, A11, det, ca, cb, cc;
+  S xh[3], rh[3], w[3], ah[3], mh[3], muq, ml;
+  S e0, e1, p0, p1, n[3];
 };
 
 __device__ __forceinline__ bool isfin(float v) { return isfinite(v); }
+__device__ __forceinline__ bool isfin(double v) { return isfinite(v); }
+__device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
+__device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
+__device__ __forceinline__ float sq_root(float v) { return sqrtf(v); }
+__device__ __forceinline__ double sq_root(double v) { return sqrt(v); }
 
 // Loads one Gaussian and runs stage 1 up to (but not including) SH. Returns false if culled.
+template <typename S>
 __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
-                                                 GF& f) {
+                                                 GF<S>& f) {
   const int64_t n = g.n;
   f.mu[0] = g.means[i];
   f.mu[1] = g.means[n + i];
@@ -124,6 +134,7 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
   // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
   const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
   if (!(z > cam.znear)) return false;
+  f.zkey = z;
   f.o = g.opac[i];
   if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;
   f.s[0] = g.scales[i];
@@ -134,51 +145,52 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
 #pragma unroll
   for (int k = 0; k < 4; ++k) f.qr[k] = g.rot[k * n + i];
   if (!(isfin(f.qr[0]) && isfin(f.qr[1]) && isfin(f.qr[2]) && isfin(f.qr[3]))) return false;
-  const float ql2 = f.qr[0] * f.qr[0] + f.qr[1] * f.qr[1] + f.qr[2] * f.qr[2] + f.qr[3] * f.qr[3];
-  if (!(ql2 > 0.f)) return false;
+  const S ql2 = (S)f.qr[0] * f.qr[0] + (S)f.qr[1] * f.qr[1] + (S)f.qr[2] * f.qr[2] + (S)f.qr[3] * f.qr[3];
+  if (!(ql2 > S(0))) return false;
 
-  f.x[0] = __fmaf_rn(cam.R[0], f.mu[0], __fmaf_rn(cam.R[1], f.mu[1], __fmaf_rn(cam.R[2], f.mu[2], cam.t[0])));
-  f.x[1] = __fmaf_rn(cam.R[3], f.mu[0], __fmaf_rn(cam.R[4], f.mu[1], __fmaf_rn(cam.R[5], f.mu[2], cam.t[1])));
-  f.x[2] = z;
-  f.t2 = f.x[0] * f.x[0] + f.x[1] * f.x[1] + z * z;
-  f.it = rsqrtf(f.t2);
-  const float iz = 1.f / z;
-  f.u = f.x[0] * iz * cam.fx + cam.cx;
-  f.v = f.x[1] * iz * cam.fy + cam.cy;
+  const S R[9] = {cam.R[0], cam.R[1], cam.R[2], cam.R[3], cam.R[4], cam.R[5], cam.R[6], cam.R[7], cam.R[8]};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    f.x[r] = R[3 * r] * f.mu[0] + R[3 * r + 1] * f.mu[1] + R[3 * r + 2] * f.mu[2] + (S)cam.t[r];
+  f.t2 = f.x[0] * f.x[0] + f.x[1] * f.x[1] + f.x[2] * f.x[2];
+  f.it = rsq(f.t2);
+  const S iz = S(1) / f.x[2];
+  f.u = f.x[0] * iz * (S)cam.fx + (S)cam.cx;
+  f.v = f.x[1] * iz * (S)cam.fy + (S)cam.cy;
 
   // R(q̂), q̂ = q/‖q‖, (w, x, y, z) (reading S15)
-  f.qinv = rsqrtf(ql2);
-  const float w = f.qr[0] * f.qinv, a = f.qr[1] * f.qinv, b = f.qr[2] * f.qinv, c = f.qr[3] * f.qinv;
+  f.qinv = rsq(ql2);
+  const S w = f.qr[0] * f.qinv, a = f.qr[1] * f.qinv, b = f.qr[2] * f.qinv, c = f.qr[3] * f.qinv;
   f.qn[0] = w; f.qn[1] = a; f.qn[2] = b; f.qn[3] = c;
-  const float Rq[9] = {1.f - 2.f * (b * b + c * c), 2.f * (a * b - w * c), 2.f * (a * c + w * b),
-                       2.f * (a * b + w * c), 1.f - 2.f * (a * a + c * c), 2.f * (b * c - w * a),
-                       2.f * (a * c - w * b), 2.f * (b * c + w * a), 1.f - 2.f * (a * a + b * b)};
+  const S one(1), two(2);
+  const S Rq[9] = {one - two * (b * b + c * c), two * (a * b - w * c), two * (a * c + w * b),
+                   two * (a * b + w * c), one - two * (a * a + c * c), two * (b * c - w * a),
+                   two * (a * c - w * b), two * (b * c + w * a), one - two * (a * a + b * b)};
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      f.Rc[3 * r + k] = cam.R[3 * r] * Rq[k] + cam.R[3 * r + 1] * Rq[3 + k] + cam.R[3 * r + 2] * Rq[6 + k];
+    for (int k = 0; k < 3; ++k) f.Rc[3 * r + k] = R[3 * r] * Rq[k] + R[3 * r + 1] * Rq[3 + k] + R[3 * r + 2] * Rq[6 + k];
 
   // 2-D covariance: M = J₂ R_c S, A = M Mᵀ (+ h I) (S2, S5)
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int k = 0; k < 3; ++k) f.RS[3 * r + k] = f.Rc[3 * r + k] * f.s[k];
-  f.j00 = cam.fx * iz;
-  f.j02 = -cam.fx * f.x[0] * iz * iz;
-  f.j11 = cam.fy * iz;
-  f.j12 = -cam.fy * f.x[1] * iz * iz;
+  f.j00 = (S)cam.fx * iz;
+  f.j02 = -(S)cam.fx * f.x[0] * iz * iz;
+  f.j11 = (S)cam.fy * iz;
+  f.j12 = -(S)cam.fy * f.x[1] * iz * iz;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     f.M[k] = f.j00 * f.RS[k] + f.j02 * f.RS[6 + k];
     f.M[3 + k] = f.j11 * f.RS[3 + k] + f.j12 * f.RS[6 + k];
   }
-  f.A00 = f.M[0] * f.M[0] + f.M[1] * f.M[1] + f.M[2] * f.M[2] + opt.dilation;
+  f.A00 = f.M[0] * f.M[0] + f.M[1] * f.M[1] + f.M[2] * f.M[2] + (S)opt.dilation;
   f.A01 = f.M[0] * f.M[3] + f.M[1] * f.M[4] + f.M[2] * f.M[5];
-  f.A11 = f.M[3] * f.M[3] + f.M[4] * f.M[4] + f.M[5] * f.M[5] + opt.dilation;
+  f.A11 = f.M[3] * f.M[3] + f.M[4] * f.M[4] + f.M[5] * f.M[5] + (S)opt.dilation;
   f.det = f.A00 * f.A11 - f.A01 * f.A01;
-  if (!(f.det > 0.f) || !isfin(f.det)) return false;
-  const float idet = 1.f / f.det;
+  if (!(f.det > S(0)) || !isfin(f.det)) return false;
+  const S idet = S(1) / f.det;
   f.ca = f.A11 * idet;
   f.cb = -f.A01 * idet;
   f.cc = f.A00 * idet;
@@ -189,21 +201,21 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     f.rh[k] = f.Rc[k] * f.xh[0] + f.Rc[3 + k] * f.xh[1] + f.Rc[6 + k] * f.xh[2];
-    f.w[k] = 1.f / (f.s[k] * f.s[k]);
+    f.w[k] = S(1) / ((S)f.s[k] * f.s[k]);
     f.ah[k] = f.rh[k] * f.w[k];
   }
 #pragma unroll
   for (int r = 0; r < 3; ++r) f.mh[r] = f.Rc[3 * r] * f.ah[0] + f.Rc[3 * r + 1] * f.ah[1] + f.Rc[3 * r + 2] * f.ah[2];
   f.muq = f.rh[0] * f.ah[0] + f.rh[1] * f.ah[1] + f.rh[2] * f.ah[2];
-  f.ml = sqrtf(f.mh[0] * f.mh[0] + f.mh[1] * f.mh[1] + f.mh[2] * f.mh[2]);
-  if (!(f.muq > 0.f) || !isfin(f.muq) || !(f.ml > 0.f) || !isfin(f.ml)) return false;
-  const float imu = 1.f / f.muq;
+  f.ml = sq_root(f.mh[0] * f.mh[0] + f.mh[1] * f.mh[1] + f.mh[2] * f.mh[2]);
+  if (!(f.muq > S(0)) || !isfin(f.muq) || !(f.ml > S(0)) || !isfin(f.ml)) return false;
+  const S imu = S(1) / f.muq;
   f.e0 = f.mh[0] * imu - f.xh[0];
   f.e1 = f.mh[1] * imu - f.xh[1];
-  const float zzit = z * z * f.it;
-  f.p0 = zzit / cam.fx * f.e0;
-  f.p1 = zzit / cam.fy * f.e1;
-  const float iml = 1.f / f.ml;
+  const S zzit = f.x[2] * f.x[2] * f.it;
+  f.p0 = zzit / (S)cam.fx * f.e0;
+  f.p1 = zzit / (S)cam.fy * f.e1;
+  const S iml = S(1) / f.ml;
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.n[k] = -f.mh[k] * iml;
   return true;
@@ -217,21 +229,22 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
                                                          float* __restrict__ zkey, Counter* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
-  GF f;
-  if (!gaussian_forward(g, i, cam, opt, f)) {
+  GF<double> f;
+  if (!gaussian_forward<double>(g, i, cam, opt, f)) {
     touched[i] = 0u;
     return;
   }
   // α-bounded footprint: α = o·G ≥ α_min ⇔ Δᵀ conic Δ ≤ k = 2 ln(o/α_min); its axis-aligned
   // half extents are sqrt(k·A′₀₀), sqrt(k·A′₁₁) (reading S8); inflated for fp32 safety.
+  const float uc = (float)f.u, vc = (float)f.v;
   const float kk = 2.f * (logf(f.o) - opt.ln_alpha_min);
-  const float rx = sqrtf(fmaxf(kk, 0.f) * f.A00) * 1.00001f + 1e-3f;
-  const float ry = sqrtf(fmaxf(kk, 0.f) * f.A11) * 1.00001f + 1e-3f;
-  // pixels i with |u_c − (i + ½)| ≤ rx
-  const float fx0 = fmaxf(ceilf(f.u - rx - 0.5f), 0.f);
-  const float fx1 = fminf(floorf(f.u + rx - 0.5f), (float)(cam.W - 1));
-  const float fy0 = fmaxf(ceilf(f.v - ry - 0.5f), 0.f);
-  const float fy1 = fminf(floorf(f.v + ry - 0.5f), (float)(cam.H - 1));
+  const float rx = sqrtf(fmaxf(kk, 0.f) * (float)f.A00) * 1.00001f + 1e-3f;
+  const float ry = sqrtf(fmaxf(kk, 0.f) * (float)f.A11) * 1.00001f + 1e-3f;
+  // pixels i with |u_c − (i + ½)| ≤ rx (evaluated on the stored fp32 u_c the blend uses)
+  const float fx0 = fmaxf(ceilf(uc - rx - 0.5f), 0.f);
+  const float fx1 = fminf(floorf(uc + rx - 0.5f), (float)(cam.W - 1));
+  const float fy0 = fmaxf(ceilf(vc - ry - 0.5f), 0.f);
+  const float fy1 = fminf(floorf(vc + ry - 0.5f), (float)(cam.H - 1));
   if (!(fx0 <= fx1 && fy0 <= fy1)) {
     touched[i] = 0u;
     return;
@@ -258,14 +271,15 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
 
   Record r;
-  r.r0 = make_float4(f.u, f.v, -0.5f * kLog2e * f.ca, -kLog2e * f.cb);
-  r.r1 = make_float4(-0.5f * kLog2e * f.cc, f.o, rgb[0], rgb[1]);
-  r.r2 = make_float4(rgb[2], f.n[0], f.n[1], f.n[2]);
-  r.r3 = make_float4(f.x[2], f.p0, f.p1, 0.f);
+  const double L2E = 1.4426950408889634;
+  r.r0 = make_float4(uc, vc, (float)(-0.5 * L2E * f.ca), (float)(-L2E * f.cb));
+  r.r1 = make_float4((float)(-0.5 * L2E * f.cc), f.o, rgb[0], rgb[1]);
+  r.r2 = make_float4(rgb[2], (float)f.n[0], (float)f.n[1], (float)f.n[2]);
+  r.r3 = make_float4(f.zkey, (float)f.p0, (float)f.p1, 0.f);
   rec[i] = r;
   rect[i] = make_uint2(tx0 | (ty0 << 16), tx1 | (ty1 << 16));
   touched[i] = (tx1 - tx0) * (ty1 - ty0);
-  zkey[i] = f.x[2];
+  zkey[i] = f.zkey;
   if (counters) {  // warp-aggregated: one atomic per converged group of visible threads
     const unsigned m = __activemask();
     if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counters + 3, (Counter)__popc(m));
@@ -274,14 +288,14 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
 
 // ---------------------------------------------------------------------------- K5
 template <int DEG>
-__global__ void __launch_bounds__(256) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
+__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
                                                          const uint32_t* __restrict__ touched,
                                                          const float* __restrict__ g2d, DevGrads gr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   if (touched[i] == 0u) return;  // culled or off-screen: zero gradient
-  GF f;
-  if (!gaussian_forward(g, i, cam, opt, f)) return;
+  GF<float> f;
+  if (!gaussian_forward<float>(g, i, cam, opt, f)) return;
   const int64_t n = g.n;
   const float4* G4 = reinterpret_cast<const float4*>(g2d + i * kG2D);
   const float4 q0 = G4[0], q1 = G4[1], q2 = G4[2], q3 = G4[3];
@@ -322,10 +336,18 @@ __global__ void __launch_bounds__(256) k_preprocess_bwd(DevGauss g, DevCam cam, 
     float drgb[3];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) drgb[ch] = rgb[ch] < 0.f ? 0.f : d_rgb[ch];
+    // += into the SH gradient planes: loads batched per chunk so the read-modify-writes
+    // overlap instead of serialising one HBM round trip per coefficient
+    constexpr int NV = 3 * K;
+    constexpr int CH = NV < 16 ? NV : 16;
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int c0 = 0; c0 < NV; c0 += CH) {
+      float old[CH];
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) gr.sh[(int64_t)(k * 3 + ch) * n + i] += Y[k] * drgb[ch];
+      for (int j = 0; j < CH; ++j) old[j] = gr.sh[(int64_t)(c0 + j) * n + i];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) gr.sh[(int64_t)(c0 + j) * n + i] = old[j] + Y[(c0 + j) / 3] * drgb[(c0 + j) % 3];
+    }
     float c16[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) c16[k] = drgb[0] * coef[0][k] + drgb[1] * coef[1][k] + drgb[2] * coef[2][k];
@@ -457,15 +479,25 @@ __global__ void __launch_bounds__(256) k_preprocess_bwd(DevGauss g, DevCam cam, 
                   a * dRq[6] + b * dRq[7]);
   const float qd = dqn[0] * w + dqn[1] * a + dqn[2] * b + dqn[3] * c;
 
+  // read-modify-write of the 11 non-SH gradient planes, loads batched first
+  float om[3], os[3], oq[4];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    gr.means[k * n + i] += dmu[k];
-    gr.scales[k * n + i] += ds[k];
+    om[k] = gr.means[k * n + i];
+    os[k] = gr.scales[k * n + i];
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) gr.rot[k * n + i] += (dqn[k] - f.qn[k] * qd) * f.qinv;
+  for (int k = 0; k < 4; ++k) oq[k] = gr.rot[k * n + i];
+  const float oo = gr.opac[i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gr.means[k * n + i] = om[k] + dmu[k];
+    gr.scales[k * n + i] = os[k] + ds[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gr.rot[k * n + i] = oq[k] + (dqn[k] - f.qn[k] * qd) * f.qinv;
   // α = min(α_max, o·G): d_o already excludes the clamp (K4)
-  gr.opac[i] += d_o;
+  gr.opac[i] = oo + d_o;
 }
 
 }  // namespace
@@ -487,7 +519,7 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const float* g2d, DevGrads grads, cudaStream_t s) {
   if (g.n == 0) return;
-  const int threads = 256;
+  const int threads = 128;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
   switch (opt.sh_degree) {
     case 0: k_preprocess_bwd<0><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;

@@ -40,11 +40,11 @@ struct DevGauss {
 };
 
 struct DevGrads {
-  float* means;
-  float* scales;
-  float* rot;
-  float* opac;
-  float* sh;
+  float* __restrict__ means;
+  float* __restrict__ scales;
+  float* __restrict__ rot;
+  float* __restrict__ opac;
+  float* __restrict__ sh;
 };
 
 // Per-visible-Gaussian record written by K1 and gathered by K3/K4 (64 B, 4 x float4):

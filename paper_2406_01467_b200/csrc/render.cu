@@ -112,10 +112,21 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_fwd(DevCam cam, DevOpt op
   median_pos[pix] = med;
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Reduce-scatter of v[0..15] across the warp: level s (offsets 16, 8, 4, 2) halves the set
+// of values each lane keeps (the half selected by lane bit s) and adds the partner's copy
+// of it; a final xor-1 exchange completes the sum. Returns Σ_lanes v[lane >> 1].
+__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < half; ++k) {
+      const float send = up ? v[k] : v[k + half];
+      const float keep = up ? v[k + half] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
 template <int TILE>
@@ -181,9 +192,9 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
     for (int j = cnt - 1; j >= 0; --j) {
       const int pos = start + j;
       const float4 a0 = s0[j], a1 = s1[j];
-      float g[15];
+      float g[16];
 #pragma unroll
-      for (int k = 0; k < 15; ++k) g[k] = 0.f;
+      for (int k = 0; k < 16; ++k) g[k] = 0.f;
       bool active = pos < last;
       if (active) {
         const PairAlpha pa = eval_alpha(a0, a1.x, a1.y, fpx, fpy, opt.alpha_max);
@@ -192,7 +203,8 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
         } else {
           const float4 a2 = s2[j];
           const float one_m = 1.f - pa.alpha;
-          T = T / one_m;  // T_i
+          const float rinv = __fdividef(1.f, one_m);  // α ≤ α_max < 1: well conditioned
+          T = T * rinv;  // T_i = T_{i+1} / (1 − α_i)
           const float w = pa.alpha * T;
           g[6] = w * gC0; g[7] = w * gC1; g[8] = w * gC2;
           g[9] = w * gN0; g[10] = w * gN1; g[11] = w * gN2;
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
           lN0 = a2.y; lN1 = a2.z; lN2 = a2.w;
           const float dL_dal = T * ((a1.z - accC0) * gC0 + (a1.w - accC1) * gC1 + (a2.x - accC2) * gC2 +
                                     (a2.y - accN0) * gN0 + (a2.z - accN1) * gN1 + (a2.w - accN2) * gN2) +
-                               TF / one_m * aterm;
+                               TF * rinv * aterm;
           float dum = 0.f, dvm = 0.f;
           if (pos == med) {  // median depth D = z_c + p·Δ (Eq.4)
             const float4 a3 = s3[j];
@@ -230,13 +242,20 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
           g[4] = dpw * pa.dy * pa.dy;
         }
       }
-      if (__ballot_sync(0xffffffffu, active)) {
+      const unsigned act = __ballot_sync(0xffffffffu, active);
+      if (act) {
+        float* dst = g2d + (size_t)sid[j] * kG2D;
+        if (__popc(act) == 1) {  // one contributing pixel in this warp: no reduction needed
+          if (active) {
 #pragma unroll
-        for (int k = 0; k < 15; ++k) g[k] = warp_sum(g[k]);
-        if (lane == 0) {
-          float* dst = g2d + (size_t)sid[j] * kG2D;
-#pragma unroll
-          for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g[k]);
+            for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g[k]);
+          }
+        } else {
+          // butterfly reduce-scatter of 16 values over 32 lanes: 16 shuffles instead of 75;
+          // afterwards lanes 2k and 2k+1 both hold the warp sum of value k
+          const float v = reduce_scatter16(g, lane);
+          const int k = lane >> 1;
+          if ((lane & 1) == 0 && k < 15) atomicAdd(dst + k, v);
         }
       }
     }

@@ -100,7 +100,7 @@ def test_preprocess_parity(case):
     np.testing.assert_allclose(r[:, 6:9], o[:, oracle.PG["rgb"]], atol=1e-5)
     np.testing.assert_allclose(r[:, 12], o[:, oracle.PG["z"]], rtol=1e-6)
     ng = np.abs(o[:, oracle.PG["ndotx"]]) >= 0.05
-    np.testing.assert_allclose(r[ng, 9:12], o[ng, 67:70], atol=1e-5)
+    np.testing.assert_allclose(r[ng, 9:12], o[ng, 67:70], atol=2e-6)
     np.testing.assert_allclose(r[ng, 13:15], o[ng][:, oracle.PG["p"]], rtol=1e-3, atol=1e-7)
 
 
