@@ -112,9 +112,10 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_fwd(DevCam cam, DevOpt op
   median_pos[pix] = med;
 }
 
-// Reduce-scatter of v[0..15] across the warp: level s (offsets 16, 8, 4, 2) halves the set
-// of values each lane keeps (the half selected by lane bit s) and adds the partner's copy
-// of it; a final xor-1 exchange completes the sum. Returns Σ_lanes v[lane >> 1].
+// Reduce-scatter of v[0..15] across the warp (16 shuffles instead of 75 for a plain
+// all-reduce of 15 values): level off=16,8,4,2 halves the set of values a lane keeps (the
+// half selected by that lane bit) and adds the partner's copy of it; a final xor-1 exchange
+// completes the sum. Returns Σ_lanes v[lane >> 1] (lanes l and l^1 hold the same value).
 __device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
 #pragma unroll
   for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
@@ -129,6 +130,13 @@ __device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// K4. Per pixel, reverse replay of its blended splats. With the per-pixel scalar
+//   D_i = Σ_{j>i} w_j (c_j·g_C + n_j·g_N)   (suffix sum, w_j = α_j T_j)
+// the α gradient of Eq.3's colour and of the normal map is
+//   ∂L/∂α_i = T_i (c_i·g_C + n_i·g_N) − D_i / (1 − α_i) + T_final/(1 − α_i) (g_A − bg·g_C),
+// (3DGS-style derivation collapsed to one scalar: gC, gN are per-pixel constants). The 15
+// per-splat values (du, dv, dA2, dB2, dC2, do, dRGB, dN, and at the pixel's median splat
+// dz, dp of Eq.4) are warp-reduced and added with one L2 atomic per value per warp.
 template <int TILE>
 __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
@@ -147,7 +155,8 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
   const int pix = py * cam.W + px;
   const int lane = (int)(threadIdx.x & 31);
 
-  __shared__ float4 s0[BLOCK], s1[BLOCK], s2[BLOCK], s3[BLOCK];
+  __shared__ float4 s0[BLOCK], s1[BLOCK], s2[BLOCK];
+  __shared__ float2 s3[BLOCK];  // (p0, p1) for the median-depth gradient
   __shared__ uint32_t sid[BLOCK];
   __shared__ int s_maxlast;
 
@@ -170,10 +179,8 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
   __syncthreads();
   const int maxlast = s_maxlast;
 
-  const float TF = T;
-  const float aterm = gA - (opt.bg[0] * gC0 + opt.bg[1] * gC1 + opt.bg[2] * gC2);
-  float accC0 = 0.f, accC1 = 0.f, accC2 = 0.f, accN0 = 0.f, accN1 = 0.f, accN2 = 0.f;
-  float lA = 0.f, lC0 = 0.f, lC1 = 0.f, lC2 = 0.f, lN0 = 0.f, lN1 = 0.f, lN2 = 0.f;
+  const float TFa = T * (gA - (opt.bg[0] * gC0 + opt.bg[1] * gC1 + opt.bg[2] * gC2));
+  float Dsuf = 0.f;
 
   for (int end = maxlast; end > 0; end -= BLOCK) {
     const int start = max(0, end - BLOCK);
@@ -186,7 +193,8 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
       s0[threadIdx.x] = r->r0;
       s1[threadIdx.x] = r->r1;
       s2[threadIdx.x] = r->r2;
-      s3[threadIdx.x] = r->r3;
+      const float4 r3 = r->r3;
+      s3[threadIdx.x] = make_float2(r3.y, r3.z);
     }
     __syncthreads();
     for (int j = cnt - 1; j >= 0; --j) {
@@ -202,44 +210,32 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
           active = false;
         } else {
           const float4 a2 = s2[j];
-          const float one_m = 1.f - pa.alpha;
-          const float rinv = __fdividef(1.f, one_m);  // α ≤ α_max < 1: well conditioned
+          const float rinv = __fdividef(1.f, 1.f - pa.alpha);  // α ≤ α_max < 1
           T = T * rinv;  // T_i = T_{i+1} / (1 − α_i)
           const float w = pa.alpha * T;
+          const float dot = a1.z * gC0 + a1.w * gC1 + a2.x * gC2 + a2.y * gN0 + a2.z * gN1 + a2.w * gN2;
+          const float dL_dal = T * dot - rinv * (Dsuf - TFa);
+          Dsuf = fmaf(w, dot, Dsuf);
           g[6] = w * gC0; g[7] = w * gC1; g[8] = w * gC2;
           g[9] = w * gN0; g[10] = w * gN1; g[11] = w * gN2;
-          // suffix sums S_i = Σ_{j>i} c_j α_j Π_{i<k<j}(1−α_k)
-          accC0 = lA * lC0 + (1.f - lA) * accC0;
-          accC1 = lA * lC1 + (1.f - lA) * accC1;
-          accC2 = lA * lC2 + (1.f - lA) * accC2;
-          accN0 = lA * lN0 + (1.f - lA) * accN0;
-          accN1 = lA * lN1 + (1.f - lA) * accN1;
-          accN2 = lA * lN2 + (1.f - lA) * accN2;
-          lA = pa.alpha;
-          lC0 = a1.z; lC1 = a1.w; lC2 = a2.x;
-          lN0 = a2.y; lN1 = a2.z; lN2 = a2.w;
-          const float dL_dal = T * ((a1.z - accC0) * gC0 + (a1.w - accC1) * gC1 + (a2.x - accC2) * gC2 +
-                                    (a2.y - accN0) * gN0 + (a2.z - accN1) * gN1 + (a2.w - accN2) * gN2) +
-                               TF * rinv * aterm;
-          float dum = 0.f, dvm = 0.f;
-          if (pos == med) {  // median depth D = z_c + p·Δ (Eq.4)
-            const float4 a3 = s3[j];
+          if (pa.a_raw <= opt.alpha_max) {  // α not clamped (S8)
+            g[5] = pa.G * dL_dal;
+            const float dpw = a1.y * g[5] * kLn2;  // dL/d(power in log2 units)
+            const float hx = dpw * pa.dx, hy = dpw * pa.dy;
+            g[0] = 2.f * a0.z * hx + a0.w * hy;
+            g[1] = a0.w * hx + 2.f * a1.x * hy;
+            g[2] = hx * pa.dx;
+            g[3] = hx * pa.dy;
+            g[4] = hy * pa.dy;
+          }
+          if (pos == med) {  // median depth D = z_c + p·Δ (Eq.4, PAPER:443-450)
+            const float2 p = s3[j];
+            g[0] += gD * p.x;
+            g[1] += gD * p.y;
             g[12] = gD;
             g[13] = gD * pa.dx;
             g[14] = gD * pa.dy;
-            dum = gD * a3.y;
-            dvm = gD * a3.z;
           }
-          float dpw = 0.f;
-          if (pa.a_raw <= opt.alpha_max) {  // α not clamped (S8)
-            g[5] = pa.G * dL_dal;
-            dpw = a1.y * pa.G * kLn2 * dL_dal;  // dL/d(power in log2 units)
-          }
-          g[0] = dpw * (2.f * a0.z * pa.dx + a0.w * pa.dy) + dum;
-          g[1] = dpw * (a0.w * pa.dx + 2.f * a1.x * pa.dy) + dvm;
-          g[2] = dpw * pa.dx * pa.dx;
-          g[3] = dpw * pa.dx * pa.dy;
-          g[4] = dpw * pa.dy * pa.dy;
         }
       }
       const unsigned act = __ballot_sync(0xffffffffu, active);
@@ -251,8 +247,6 @@ __global__ void __launch_bounds__(TILE* TILE) k_render_bwd(
             for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g[k]);
           }
         } else {
-          // butterfly reduce-scatter of 16 values over 32 lanes: 16 shuffles instead of 75;
-          // afterwards lanes 2k and 2k+1 both hold the warp sum of value k
           const float v = reduce_scatter16(g, lane);
           const int k = lane >> 1;
           if ((lane & 1) == 0 && k < 15) atomicAdd(dst + k, v);

@@ -194,8 +194,10 @@ def test_forward_determinism_and_backward_close():
     b, Gb, _ = gpu_grads(scene, cam, opt, cot)
     for k in a:
         np.testing.assert_array_equal(a[k], b[k])
-    # gradients use float atomics (order not fixed): equal to rounding
-    np.testing.assert_allclose(Ga, Gb, rtol=1e-4, atol=1e-6 * np.abs(Ga).max())
+    # gradients use float atomics (order not fixed): equal to rounding, per parameter class
+    for sl in (slice(0, 3), slice(3, 6), slice(6, 10), slice(10, 11), slice(11, 59)):
+        na = np.linalg.norm(Ga[:, sl])
+        assert np.linalg.norm(Ga[:, sl] - Gb[:, sl]) <= 1e-5 * max(na, 1e-30), sl
 
 
 def test_empty_and_degenerate_inputs():
