@@ -117,23 +117,23 @@ K1_B_ALL, K1_B_VIS = 20, 296               # K1: cull read (means + opacity + to
 K5_B_ALL, K5_B_VIS = 4, 772                # K5: touched / params 236 + g2d 64 + grads RMW 472
 
 
-def kernel_work(name, t, views, key_bits):
+def kernel_work(name, t, views, tile_bits):
     """Algorithmic (bytes or flops, bound) summed over the timed views for one kernel."""
     n, nvis, M = t["n"], t["n_visible"], t["n_duplicates"]
     if name == "preprocess_fwd":
         return K1_B_ALL * n * views + K1_B_VIS * nvis, "hbm"
-    if name == "scan":
-        return 8 * n * views, "hbm"
-    if name == "duplicate":
-        return (4 * n) * views + 12 * nvis + 12 * M, "hbm"
-    if name == "sort":
-        return 24 * M * math.ceil(key_bits / 8), "hbm"
+    if name == "depth_sort":   # (key, id) 8 B read + 8 B write per radix pass, 4 passes
+        return 16 * 4 * n * views, "hbm"
+    if name == "scan":         # sorted id + gathered count read, offset write
+        return 12 * n * views, "hbm"
+    if name == "duplicate":    # offsets + sorted ids + rects of visible, 8 B (tile, id) per duplicate
+        return 8 * n * views + 8 * nvis + 8 * M, "hbm"
+    if name == "tile_sort":    # (tile, id) 8 B read + 8 B write per pass
+        return 16 * M * math.ceil(tile_bits / 8), "hbm"
     if name == "ranges":
-        return 8 * M, "hbm"
+        return 4 * M, "hbm"
     if name == "render_fwd":
         return FWD_FLOP_EVAL * t["pairs_evaluated_fwd"] + FWD_FLOP_BLEND * t["pairs_blended_fwd"], "alu"
-    if name == "memset_g2d":
-        return 64 * n * views, "hbm"
     if name == "render_bwd":
         return BWD_FLOP_EVAL * t["pairs_evaluated_bwd"] + BWD_FLOP_BLEND * t["pairs_blended_fwd"], "alu"
     if name == "preprocess_bwd":
@@ -362,13 +362,13 @@ def run_gpu(args, cfg_name, config):
     tim_ext = dict(tim)
     tim_ext["n"] = n
     st = P.rd_view_stats(view)
-    key_bits = st["key_bits"]
+    tile_bits = st["key_bits"] - 32
     kernels = {}
     for name, ms in tim["ms"].items():
         launches = tim["launches"][name]
         if launches == 0:
             continue
-        work, bound = kernel_work(name, tim_ext, views_timed, key_bits)
+        work, bound = kernel_work(name, tim_ext, views_timed, tile_bits)
         avg_ms = ms / launches
         per_launch = work / launches
         if bound == "hbm":
@@ -394,8 +394,10 @@ def run_gpu(args, cfg_name, config):
                 "peak_source": (f"{hbm_src} HBM copy (MEASURED_PEAKS.json)" if dk["bound"] == "hbm" else
                                 f"FP32 FFMA {n_sm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (DESIGN.md)")}
 
-    # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so)
-    launches_per_view = 1 + 2 + 1 + (2 + math.ceil(key_bits / 8)) + 1 + 1 + 1 + 1
+    # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so):
+    # K1, depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan),
+    # duplicate, tile sort (histogram + exclusive-sum + passes), ranges, K3, K4, K5
+    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 1
     views_per_rank = args.steps * B
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)

@@ -120,8 +120,9 @@ typedef struct rd_stats {
 } rd_stats;
 
 /* Per-kernel device timings and work counters (host struct filled by rd_get_timings).
- * Kernel index: 0 K1 preprocess_fwd, 1 K2a scan, 2 K2b duplicate, 3 K2c sort, 4 K2d ranges,
- * 5 K3 render_fwd, 6 memset of the 2-D gradient scratch, 7 K4 render_bwd, 8 K5 preprocess_bwd. */
+ * Kernel index: 0 K1 preprocess_fwd, 1 K2a depth_sort, 2 K2b scan, 3 K2c duplicate,
+ * 4 K2d tile_sort, 5 K2e ranges, 6 K3 render_fwd, 7 K4 render_bwd (including the zeroing of
+ * the 2-D gradient scratch), 8 K5 preprocess_bwd. */
 #define RD_NUM_KERNELS 9
 typedef struct rd_timings {
   double ms[RD_NUM_KERNELS];       /* summed CUDA-event durations since the last reset */

@@ -51,7 +51,7 @@ class RdStats(ctypes.Structure):
 
 
 RD_NUM_KERNELS = 9
-KERNEL_NAMES = ["preprocess_fwd", "scan", "duplicate", "sort", "ranges", "render_fwd", "memset_g2d", "render_bwd",
+KERNEL_NAMES = ["preprocess_fwd", "depth_sort", "scan", "duplicate", "tile_sort", "ranges", "render_fwd", "render_bwd",
                 "preprocess_bwd"]
 
 

@@ -58,7 +58,7 @@ struct Buf {
   size_t cap = 0;
 };
 
-enum Kernel { K_PRE = 0, K_SCAN, K_DUP, K_SORT, K_RANGES, K_FWD, K_MEMSET, K_BWD, K_PREBWD };
+enum Kernel { K_PRE = 0, K_DSORT, K_SCAN, K_DUP, K_TSORT, K_RANGES, K_FWD, K_BWD, K_PREBWD };
 
 }  // namespace
 
@@ -72,12 +72,13 @@ struct rd_view {
   DevCam cam{};
   DevOpt opt{};
   int tiles_x = 0, tiles_y = 0;
-  int key_bits = 0;
+  int key_bits = 0;   // 32 + tile_bits: the equivalent one-pass 64-bit key width
+  int tile_bits = 0;
   int64_t M = 0;
-  int sort_sel = 0;
+  int dsel = 0, tsel = 0;  // CUB DoubleBuffer selectors of the depth and tile sorts
   uint32_t* host_M = nullptr;  // pinned
-  Buf rec, rect, touched, offsets, zkey, scan_tmp;
-  Buf keys0, keys1, vals0, vals1, sort_tmp;
+  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp;
+  Buf tkeys0, tkeys1, vals0, vals1;
   Buf ranges;
   Buf T_final, n_contrib, median_pos;
   Buf g2d;
@@ -209,9 +210,9 @@ rd_status rd_view_create(rd_view** view, rd_alloc_fn alloc, rd_free_fn free_fn, 
 
 rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
-  Buf* all[] = {&v->rec,     &v->rect,      &v->touched,    &v->offsets, &v->zkey,  &v->scan_tmp,
-                &v->keys0,   &v->keys1,     &v->vals0,      &v->vals1,   &v->sort_tmp, &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d,     &v->counters};
+  Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
+                &v->didx1,  &v->tmp,    &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
@@ -275,6 +276,7 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   v->tiles_y = tiles_y;
   int bits = 1;
   while ((1LL << bits) < (long long)tiles_x * tiles_y) ++bits;
+  v->tile_bits = bits;
   v->key_bits = 32 + bits;
 
   const size_t n = (size_t)g->n;
@@ -282,12 +284,15 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   RD_ENSURE(v->rect, n * sizeof(uint2), s);
   RD_ENSURE(v->touched, n * sizeof(uint32_t), s);
   RD_ENSURE(v->offsets, n * sizeof(uint32_t), s);
-  RD_ENSURE(v->zkey, n * sizeof(float), s);
+  RD_ENSURE(v->dkey0, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->dkey1, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->didx0, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->didx1, n * sizeof(uint32_t), s);
 
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
   v->begin(s);
   launch_preprocess_fwd(dg, c, o, tiles_x, tiles_y, (Record*)v->rec.ptr, (uint2*)v->rect.ptr,
-                        (uint32_t*)v->touched.ptr, (float*)v->zkey.ptr, v->ctr(), s);
+                        (uint32_t*)v->touched.ptr, (uint32_t*)v->dkey0.ptr, (uint32_t*)v->didx0.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("preprocess_fwd");
   v->end(K_PRE, s);
   v->stage = 1;
@@ -303,12 +308,20 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   const int64_t n = v->n;
   const int n_tiles = v->tiles_x * v->tiles_y;
   int64_t M = 0;
+  v->dsel = v->tsel = 0;
+  const uint32_t* sorted_ids = (const uint32_t*)v->didx0.ptr;
   if (n > 0) {
-    const size_t scan_bytes = binning_scan_temp_bytes(n);
-    RD_ENSURE(v->scan_tmp, scan_bytes, s);
+    const size_t tb = binning_temp_bytes(n, 0, v->tile_bits);
+    RD_ENSURE(v->tmp, tb, s);
     if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, sizeof(uint32_t)));
     v->begin(s);
-    launch_scan((const uint32_t*)v->touched.ptr, (uint32_t*)v->offsets.ptr, n, v->scan_tmp.ptr, scan_bytes, s);
+    v->dsel = launch_depth_sort((uint32_t*)v->dkey0.ptr, (uint32_t*)v->dkey1.ptr, (uint32_t*)v->didx0.ptr,
+                                (uint32_t*)v->didx1.ptr, n, v->tmp.ptr, v->tmp.cap, s);
+    RD_CHECK_LAUNCH("depth_sort");
+    v->end(K_DSORT, s);
+    sorted_ids = (const uint32_t*)(v->dsel ? v->didx1.ptr : v->didx0.ptr);
+    v->begin(s);
+    launch_scan(sorted_ids, (const uint32_t*)v->touched.ptr, (uint32_t*)v->offsets.ptr, n, v->tmp.ptr, v->tmp.cap, s);
     RD_CHECK_LAUNCH("scan");
     v->end(K_SCAN, s);
     RD_CUDA(cudaMemcpyAsync(v->host_M, (const uint32_t*)v->offsets.ptr + (n - 1), sizeof(uint32_t),
@@ -317,27 +330,26 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
     M = (int64_t)*v->host_M;
   }
   if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
-  RD_ENSURE(v->keys0, (size_t)M * sizeof(uint64_t), s);
-  RD_ENSURE(v->keys1, (size_t)M * sizeof(uint64_t), s);
+  RD_ENSURE(v->tkeys0, (size_t)M * sizeof(uint32_t), s);
+  RD_ENSURE(v->tkeys1, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->vals0, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->vals1, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->ranges, (size_t)n_tiles * sizeof(uint2), s);
-  v->sort_sel = 0;
   if (M > 0) {
     v->begin(s);
-    launch_duplicate(n, (const uint32_t*)v->offsets.ptr, (const uint2*)v->rect.ptr, (const float*)v->zkey.ptr,
-                     v->tiles_x, (uint64_t*)v->keys0.ptr, (uint32_t*)v->vals0.ptr, s);
+    launch_duplicate(n, M, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect.ptr, v->tiles_x,
+                     (uint32_t*)v->tkeys0.ptr, (uint32_t*)v->vals0.ptr, s);
     RD_CHECK_LAUNCH("duplicate");
     v->end(K_DUP, s);
-    const size_t sort_bytes = binning_sort_temp_bytes(M, v->key_bits);
-    RD_ENSURE(v->sort_tmp, sort_bytes, s);
+    const size_t tb = binning_temp_bytes(0, M, v->tile_bits);
+    RD_ENSURE(v->tmp, tb, s);
     v->begin(s);
-    v->sort_sel = launch_sort((uint64_t*)v->keys0.ptr, (uint64_t*)v->keys1.ptr, (uint32_t*)v->vals0.ptr,
-                              (uint32_t*)v->vals1.ptr, M, v->key_bits, v->sort_tmp.ptr, sort_bytes, s);
-    RD_CHECK_LAUNCH("sort");
-    v->end(K_SORT, s);
+    v->tsel = launch_tile_sort((uint32_t*)v->tkeys0.ptr, (uint32_t*)v->tkeys1.ptr, (uint32_t*)v->vals0.ptr,
+                               (uint32_t*)v->vals1.ptr, M, v->tile_bits, v->tmp.ptr, v->tmp.cap, s);
+    RD_CHECK_LAUNCH("tile_sort");
+    v->end(K_TSORT, s);
   }
-  const uint64_t* keys = (const uint64_t*)(v->sort_sel ? v->keys1.ptr : v->keys0.ptr);
+  const uint32_t* keys = (const uint32_t*)(v->tsel ? v->tkeys1.ptr : v->tkeys0.ptr);
   v->begin(s);
   launch_ranges(keys, M, n_tiles, (uint2*)v->ranges.ptr, s);
   RD_CHECK_LAUNCH("ranges");
@@ -358,7 +370,7 @@ rd_status rd_render_fwd(rd_view* v, float* color, float* depth, float* normal, f
   RD_ENSURE(v->T_final, HW * sizeof(float), s);
   RD_ENSURE(v->n_contrib, HW * sizeof(int32_t), s);
   RD_ENSURE(v->median_pos, HW * sizeof(int32_t), s);
-  const uint32_t* ids = (const uint32_t*)(v->sort_sel ? v->vals1.ptr : v->vals0.ptr);
+  const uint32_t* ids = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
   v->begin(s);
   launch_render_fwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, color, depth, normal, alpha, (float*)v->T_final.ptr,
@@ -384,13 +396,9 @@ rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolo
   cudaStream_t s = (cudaStream_t)stream;
   const size_t n = (size_t)v->n;
   RD_ENSURE(v->g2d, n * kG2D * sizeof(float), s);
-  if (n > 0) {
-    v->begin(s);
-    RD_CUDA(cudaMemsetAsync(v->g2d.ptr, 0, n * kG2D * sizeof(float), s));
-    v->end(K_MEMSET, s);
-  }
-  const uint32_t* ids = (const uint32_t*)(v->sort_sel ? v->vals1.ptr : v->vals0.ptr);
-  v->begin(s);
+  const uint32_t* ids = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
+  v->begin(s);  // K4 timing includes the zeroing of the 2-D gradient scratch
+  if (n > 0) RD_CUDA(cudaMemsetAsync(v->g2d.ptr, 0, n * kG2D * sizeof(float), s));
   launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
                     (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,
@@ -458,10 +466,13 @@ rd_status rd_debug_binning(const rd_view* v, uint64_t* keys, uint32_t* ids, uint
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   if (v->stage < 2) return fail(RD_ERR_STATE, "rd_debug_binning before rd_bin");
   cudaStream_t s = (cudaStream_t)stream;
-  const void* k = v->sort_sel ? v->keys1.ptr : v->keys0.ptr;
-  const void* i = v->sort_sel ? v->vals1.ptr : v->vals0.ptr;
-  if (keys && v->M) RD_CUDA(cudaMemcpyAsync(keys, k, (size_t)v->M * 8, cudaMemcpyDeviceToDevice, s));
-  if (ids && v->M) RD_CUDA(cudaMemcpyAsync(ids, i, (size_t)v->M * 4, cudaMemcpyDeviceToDevice, s));
+  const uint32_t* tk = (const uint32_t*)(v->tsel ? v->tkeys1.ptr : v->tkeys0.ptr);
+  const uint32_t* iv = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
+  if (keys && v->M) {
+    launch_keys64(tk, iv, (const Record*)v->rec.ptr, v->M, keys, s);
+    RD_CHECK_LAUNCH("keys64");
+  }
+  if (ids && v->M) RD_CUDA(cudaMemcpyAsync(ids, iv, (size_t)v->M * 4, cudaMemcpyDeviceToDevice, s));
   if (ranges)
     RD_CUDA(cudaMemcpyAsync(ranges, v->ranges.ptr, (size_t)v->tiles_x * v->tiles_y * 8, cudaMemcpyDeviceToDevice, s));
   return RD_OK;

@@ -1,138 +1,190 @@
 // binning.cu — stage 2 (K2) of the RaDe-GS rasterizer, sm_100a.
 //
-//   K2a  inclusive scan of tiles_touched → offsets; M = offsets[n−1]
-//   K2b  duplicate: for each Gaussian (id order) and each tile of its rect, emit
-//        key = (tile << 32) | float_bits(z_c), value = id         (PAPER:422 depth sort)
-//   K2c  stable LSD radix sort of (key, id) on bits [0, 32 + ceil(log2 T))
-//   K2d  ranges[tile] = [first, last) in the sorted list
+// The depth sort of PAPER:422 per tile, as a two-stage stable sort whose result is
+// bit-identical to one LSD radix sort of 64-bit keys (tile << 32 | float_bits(z_c)) over
+// (Gaussian, tile) pairs emitted in id order (reading S7):
 //
-// z_c > znear > 0, so the IEEE bit pattern of z_c orders like its value; with the stable
-// sort over input in id order the final order is (tile, z_c, id) — reading S7.
-// Integer work: the result is checked bit-exactly against a CPU std::stable_sort.
+//   K2a  depth sort: stable radix sort of the N pairs (float_bits(z_c), id) — culled or
+//        off-screen Gaussians carry key 0xFFFFFFFF and sink to the end. Order (z_c, id).
+//   K2b  inclusive scan of tiles_touched gathered in that order → offsets; M = offsets[N−1]
+//   K2c  duplicate: each Gaussian, in depth order, emits (tile, id) for every tile of its
+//        rect (warp-cooperative, coalesced stores)
+//   K2d  stable radix sort of the M pairs by tile on ceil(log2 T) bits (2 passes at 4096
+//        tiles instead of 6 passes over 12-byte pairs): within a tile the (z_c, id) order
+//        of K2a is preserved
+//   K2e  ranges[tile] = [first, last) in the sorted list
+//
+// z_c > znear > 0, so the IEEE bit pattern orders like the value. Integer work: checked
+// bit-exactly against a CPU std::stable_sort of the 64-bit keys.
 #include "rade_internal.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 
 namespace rade {
 namespace {
 
-// Warp-cooperative emission: a warp owns 32 consecutive Gaussians, whose outputs are
-// contiguous in [start(first), end(last)). The warp walks that span 32 outputs at a time;
-// output t belongs to the first lane whose inclusive warp-prefix exceeds t (a 5-step binary
-// search over shuffled prefixes),
-// whose rect / key are fetched by shuffle. Stores are fully coalesced and a large splat no
-// longer serialises one thread. Per-Gaussian output order is row-major over its rect.
-__global__ void __launch_bounds__(256) k_duplicate(int64_t n, const uint32_t* __restrict__ offsets,
-                                                    const uint2* __restrict__ rect, const float* __restrict__ zkey,
-                                                    int tiles_x, uint64_t* __restrict__ keys,
-                                                    uint32_t* __restrict__ vals) {
-  const int lane = (int)(threadIdx.x & 31);
-  const int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-  if (base >= n) return;  // whole warp out of range
-  const int64_t i = base + lane;
-  uint32_t start = 0, end = 0;
-  if (i < n) {
-    end = offsets[i];
-    start = i == 0 ? 0u : offsets[i - 1];
-  } else {
-    end = start = offsets[n - 1];
-  }
-  const uint32_t cnt = end - start;
-  uint32_t x0 = 0, y0 = 0, w = 1, zb = 0;
-  if (cnt) {
-    const uint2 r = rect[i];
-    x0 = r.x & 0xffffu;
-    y0 = r.x >> 16;
-    w = (r.y & 0xffffu) - x0;
-    zb = __float_as_uint(zkey[i]);
-  }
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const uint32_t excl = incl - cnt;
-  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  const uint32_t wstart = __shfl_sync(0xffffffffu, start, 0);
-  for (uint32_t t0 = 0; t0 < total; t0 += 32) {
-    const uint32_t t = t0 + lane;
-    // owner = first lane whose inclusive prefix exceeds t (binary search over shuffled prefixes)
-    int owner = 0;
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + s - 1);
-      if (v <= t) owner += s;
+struct CountOf {
+  const uint32_t* __restrict__ touched;
+  __host__ __device__ __forceinline__ uint32_t operator()(const uint32_t id) const { return touched[id]; }
+};
+
+// First index p in [0, n) with a[p] > target (n if none), searched by a whole warp: each
+// round probes 32 evenly spaced positions and keeps the bracket (4 rounds for n = 1.5M).
+__device__ __forceinline__ uint32_t warp_upper_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t target,
+                                                     int lane) {
+  uint32_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t probe = lo + (uint32_t)lane * step;
+    const bool gt = probe < hi ? (a[probe] > target) : true;
+    const unsigned m = __ballot_sync(0xffffffffu, gt);
+    if (m == 0) {
+      lo = lo + 31 * step + 1;
+    } else {
+      const int f = __ffs(m) - 1;
+      if (f == 0) return lo;
+      const uint32_t nlo = lo + (uint32_t)(f - 1) * step + 1;
+      hi = min(hi, lo + (uint32_t)f * step);
+      lo = nlo;
     }
-    owner &= 31;
-    const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, owner);
-    const uint32_t o_x0 = __shfl_sync(0xffffffffu, x0, owner);
-    const uint32_t o_y0 = __shfl_sync(0xffffffffu, y0, owner);
-    const uint32_t o_w = __shfl_sync(0xffffffffu, w, owner);
-    const uint32_t o_zb = __shfl_sync(0xffffffffu, zb, owner);
-    if (t < total) {
-      const uint32_t li = t - o_excl;
-      const uint32_t ty = o_y0 + li / o_w, tx = o_x0 + li % o_w;
-      const uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + tx;
-      keys[wstart + t] = (tile << 32) | (uint64_t)o_zb;
-      vals[wstart + t] = (uint32_t)(base + owner);
+  }
+  const uint32_t probe = lo + (uint32_t)lane;
+  const bool gt = probe < hi ? (a[probe] > target) : true;
+  const unsigned m = __ballot_sync(0xffffffffu, gt);
+  return m ? min(hi, lo + (uint32_t)(__ffs(m) - 1)) : hi;
+}
+
+constexpr int kDupThreads = 256;
+constexpr int kDupOut = 2048;  // outputs per block
+
+// Load-balanced emission over OUTPUTS: block b writes duplicates [b·2048, (b+1)·2048). In
+// depth order every visible Gaussian touches ≥ 1 tile, so the block's outputs come from at
+// most 2048 consecutive positions [g0, g1], found by one warp-wide search of the inclusive
+// offsets. Their offsets, ids and rects are staged in shared memory; each output finds its
+// owner by binary search there. Stores are coalesced and a huge near-camera splat is spread
+// over as many blocks as its tiles need (no per-thread or per-warp serialisation). Per
+// Gaussian the tiles are emitted row-major over its rect.
+__global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, int64_t m, const uint32_t* __restrict__ offsets,
+                                                            const uint32_t* __restrict__ sorted_ids,
+                                                            const uint2* __restrict__ rect, int tiles_x,
+                                                            uint32_t* __restrict__ tile_keys,
+                                                            uint32_t* __restrict__ vals) {
+  __shared__ uint32_t s_end[kDupOut + 1];
+  __shared__ uint32_t s_id[kDupOut];
+  __shared__ uint2 s_rect[kDupOut];
+  __shared__ uint32_t s_g[2];
+  const uint32_t o0 = blockIdx.x * (uint32_t)kDupOut;
+  const uint32_t o1 = min((uint32_t)m, o0 + (uint32_t)kDupOut);
+  if (threadIdx.x < 32) {
+    const uint32_t g0 = warp_upper_bound(offsets, (uint32_t)n, o0, (int)threadIdx.x);
+    const uint32_t g1 = warp_upper_bound(offsets, (uint32_t)n, o1 - 1, (int)threadIdx.x);
+    if (threadIdx.x == 0) {
+      s_g[0] = g0;
+      s_g[1] = g1;
     }
+  }
+  __syncthreads();
+  const uint32_t g0 = s_g[0];
+  const int ng = (int)(s_g[1] - g0) + 1;  // ≤ kDupOut
+  // s_end[0] = start of g0; s_end[k + 1] = end of g0 + k
+  if (threadIdx.x == 0) s_end[0] = g0 == 0 ? 0u : offsets[g0 - 1];
+  for (int k = threadIdx.x; k < ng; k += kDupThreads) {
+    s_end[k + 1] = offsets[g0 + k];
+    const uint32_t id = sorted_ids[g0 + k];
+    s_id[k] = id;
+    s_rect[k] = rect[id];
+  }
+  __syncthreads();
+  for (uint32_t o = o0 + threadIdx.x; o < o1; o += kDupThreads) {
+    // owner k: s_end[k] <= o < s_end[k + 1]
+    int lo = 0, hi = ng - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_end[mid] <= o) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t li = o - s_end[lo];
+    const uint2 r = s_rect[lo];
+    const uint32_t x0 = r.x & 0xffffu, y0 = r.x >> 16, w = (r.y & 0xffffu) - x0;
+    const uint32_t ty = y0 + li / w, tx = x0 + li % w;
+    tile_keys[o] = ty * (uint32_t)tiles_x + tx;
+    vals[o] = s_id[lo];
   }
 }
 
-__global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys, int64_t m,
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int64_t m,
                                                  uint2* __restrict__ ranges) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
-  const uint32_t tile = (uint32_t)(keys[k] >> 32);
-  if (k == 0 || (uint32_t)(keys[k - 1] >> 32) != tile) ranges[tile].x = (uint32_t)k;
-  if (k == m - 1 || (uint32_t)(keys[k + 1] >> 32) != tile) ranges[tile].y = (uint32_t)(k + 1);
+  const uint32_t tile = keys[k];
+  if (k == 0 || keys[k - 1] != tile) ranges[tile].x = (uint32_t)k;
+  if (k == m - 1 || keys[k + 1] != tile) ranges[tile].y = (uint32_t)(k + 1);
+}
+
+__global__ void __launch_bounds__(256) k_keys64(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ ids,
+                                                 const Record* __restrict__ rec, int64_t m,
+                                                 uint64_t* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  out[k] = ((uint64_t)tiles[k] << 32) | (uint64_t)__float_as_uint(rec[ids[k]].r3.x);
 }
 
 }  // namespace
 
-size_t binning_scan_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
-  return bytes;
+size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, k, v, (int)n, 0, 32);
+  cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it(nullptr, CountOf{nullptr});
+  cub::DeviceScan::InclusiveSum(nullptr, b, it, (uint32_t*)nullptr, (int)n);
+  if (m > 0) cub::DeviceRadixSort::SortPairs(nullptr, c, k, v, (int)m, 0, tile_bits);
+  size_t r = a > b ? a : b;
+  return r > c ? r : c;
 }
 
-void launch_scan(const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp, size_t temp_bytes,
-                 cudaStream_t s) {
-  if (n == 0) return;
-  cub::DeviceScan::InclusiveSum(temp, temp_bytes, tiles_touched, offsets, (int)n, s);
-}
-
-void launch_duplicate(int64_t n, const uint32_t* offsets, const uint2* rect, const float* zkey, int tiles_x,
-                      uint64_t* keys, uint32_t* vals, cudaStream_t s) {
-  if (n == 0) return;
-  const int threads = 256;
-  k_duplicate<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(n, offsets, rect, zkey, tiles_x, keys, vals);
-}
-
-size_t binning_sort_temp_bytes(int64_t m, int end_bit) {
-  size_t bytes = 0;
-  cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
-  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v, (int)m, 0, end_bit);
-  return bytes;
-}
-
-int launch_sort(uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int end_bit, void* temp,
-                size_t temp_bytes, cudaStream_t s) {
-  if (m == 0) return 0;
-  cub::DoubleBuffer<uint64_t> k(keys0, keys1);
-  cub::DoubleBuffer<uint32_t> v(vals0, vals1);
-  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)m, 0, end_bit, s);
+int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t* idx1, int64_t n, void* temp,
+                      size_t temp_bytes, cudaStream_t s) {
+  if (n == 0) return 0;
+  cub::DoubleBuffer<uint32_t> k(dkey0, dkey1), v(idx0, idx1);
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, 32, s);
   return k.selector;
 }
 
-void launch_ranges(const uint64_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s) {
+void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp,
+                 size_t temp_bytes, cudaStream_t s) {
+  if (n == 0) return;
+  cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it(sorted_ids, CountOf{tiles_touched});
+  cub::DeviceScan::InclusiveSum(temp, temp_bytes, it, offsets, (int)n, s);
+}
+
+void launch_duplicate(int64_t n, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
+                      int tiles_x, uint32_t* tile_keys, uint32_t* vals, cudaStream_t s) {
+  if (n == 0 || m == 0) return;
+  k_duplicate<<<(unsigned)((m + kDupOut - 1) / kDupOut), kDupThreads, 0, s>>>(n, m, offsets, sorted_ids, rect, tiles_x,
+                                                                            tile_keys, vals);
+}
+
+int launch_tile_sort(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int tile_bits,
+                     void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (m == 0) return 0;
+  cub::DoubleBuffer<uint32_t> k(keys0, keys1), v(vals0, vals1);
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)m, 0, tile_bits, s);
+  return k.selector;
+}
+
+void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s) {
   cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
   if (m == 0) return;
   const int threads = 256;
   k_ranges<<<(unsigned)((m + threads - 1) / threads), threads, 0, s>>>(keys, m, ranges);
+}
+
+void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,
+                   cudaStream_t s) {
+  if (m == 0) return;
+  const int threads = 256;
+  k_keys64<<<(unsigned)((m + threads - 1) / threads), threads, 0, s>>>(tiles, ids, rec, m, out);
 }
 
 }  // namespace rade

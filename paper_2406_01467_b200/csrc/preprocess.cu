@@ -226,12 +226,15 @@ template <int DEG>
 __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
                                                          int tiles_y, Record* __restrict__ rec,
                                                          uint2* __restrict__ rect, uint32_t* __restrict__ touched,
-                                                         float* __restrict__ zkey, Counter* __restrict__ counters) {
+                                                         uint32_t* __restrict__ dkey, uint32_t* __restrict__ didx,
+                                                         Counter* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
+  didx[i] = (uint32_t)i;
   GF<double> f;
   if (!gaussian_forward<double>(g, i, cam, opt, f)) {
     touched[i] = 0u;
+    dkey[i] = 0xffffffffu;
     return;
   }
   // α-bounded footprint: α = o·G ≥ α_min ⇔ Δᵀ conic Δ ≤ k = 2 ln(o/α_min); its axis-aligned
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   const float fy1 = fminf(floorf(vc + ry - 0.5f), (float)(cam.H - 1));
   if (!(fx0 <= fx1 && fy0 <= fy1)) {
     touched[i] = 0u;
+    dkey[i] = 0xffffffffu;
     return;
   }
   const int T = opt.tile;
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   rec[i] = r;
   rect[i] = make_uint2(tx0 | (ty0 << 16), tx1 | (ty1 << 16));
   touched[i] = (tx1 - tx0) * (ty1 - ty0);
-  zkey[i] = f.zkey;
+  dkey[i] = __float_as_uint(f.zkey);
   if (counters) {  // warp-aggregated: one atomic per converged group of visible threads
     const unsigned m = __activemask();
     if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counters + 3, (Counter)__popc(m));
@@ -503,17 +507,20 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(DevGauss g, DevCam ca
 }  // namespace
 
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y,
-                           Record* rec, uint2* rect, uint32_t* tiles_touched, float* zkey, Counter* counters,
-                           cudaStream_t s) {
+                           Record* rec, uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx,
+                           Counter* counters, cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = 256;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
+#define RD_K1(D) \
+  k_preprocess_fwd<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, dkey, didx, counters)
   switch (opt.sh_degree) {
-    case 0: k_preprocess_fwd<0><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
-    case 1: k_preprocess_fwd<1><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
-    case 2: k_preprocess_fwd<2><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
-    default: k_preprocess_fwd<3><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, zkey, counters); break;
+    case 0: RD_K1(0); break;
+    case 1: RD_K1(1); break;
+    case 2: RD_K1(2); break;
+    default: RD_K1(3); break;
   }
+#undef RD_K1
 }
 
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,

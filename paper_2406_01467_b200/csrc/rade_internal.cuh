@@ -96,21 +96,27 @@ __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, (Counter)v);
 }
 
+// K1 also writes the depth-sort input: dkey[i] = float_bits(z_c) (0xFFFFFFFF if the
+// Gaussian touches no tile) and didx[i] = i.
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y,
-                           Record* rec, uint2* rect, uint32_t* tiles_touched, float* zkey, Counter* counters,
-                           cudaStream_t s);
+                           Record* rec, uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx,
+                           Counter* counters, cudaStream_t s);
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const float* g2d, DevGrads grads, cudaStream_t s);
-size_t binning_scan_temp_bytes(int64_t n);
-void launch_scan(const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp, size_t temp_bytes,
-                 cudaStream_t s);
-void launch_duplicate(int64_t n, const uint32_t* offsets, const uint2* rect, const float* zkey, int tiles_x,
-                      uint64_t* keys, uint32_t* vals, cudaStream_t s);
-size_t binning_sort_temp_bytes(int64_t m, int end_bit);
-// sorts (keys[0], vals[0]) with keys[1], vals[1] as alternate buffers; returns selector
-int launch_sort(uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int end_bit,
-                void* temp, size_t temp_bytes, cudaStream_t s);
-void launch_ranges(const uint64_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s);
+// K2 (binning.cu). Sorts return the CUB DoubleBuffer selector (1: result in the *1 buffers).
+size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits);
+int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t* idx1, int64_t n, void* temp,
+                      size_t temp_bytes, cudaStream_t s);
+void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp,
+                 size_t temp_bytes, cudaStream_t s);
+void launch_duplicate(int64_t n, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
+                      int tiles_x, uint32_t* tile_keys, uint32_t* vals, cudaStream_t s);
+int launch_tile_sort(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int tile_bits,
+                     void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s);
+// debug: 64-bit keys (tile << 32 | float_bits(z_c)) of the sorted list
+void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,
+                   cudaStream_t s);
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal,
                        float* alpha, float* T_final, int32_t* n_contrib, int32_t* median_pos, Counter* counters,
