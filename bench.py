@@ -216,7 +216,8 @@ def run_reference(args, cfg_name, config):
     times, desc, cores = [], "", 1
     for step in range(args.warmup + args.steps):
         cam = cams[step % len(cams)]
-        t, desc, cores, _ = oracle_frame_time(scene, cam, opt, n_pix=args.ref_pixels, n_grad=1, seed=step)
+        t, desc, cores, _ = oracle_frame_time(scene, cam, opt, n_pix=args.ref_pixels, n_grad=args.ref_grads,
+                                              seed=step)
         if step >= args.warmup:
             times.append(t)
     frame_s = float(np.mean(times))
@@ -248,20 +249,16 @@ def run_gpu(args, cfg_name, config):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
 
+    from paper_2406_01467_b200.parallel import FlatGrads, views_for_rank
+
     scene, cams, opt = sg.config_scene_and_cameras(cfg_name, n_gaussians=args.n_gaussians)
     n = scene.n
-    my_views = [cams[v] for v in range(len(cams)) if v % ws == rank]
+    my_views = [cams[v] for v in views_for_rank(len(cams), ws, rank)]
     B = args.views_per_step
     g = P.Gaussians.from_numpy(scene, device)
     K = g.sh.shape[0]
-    flat = torch.zeros(n * (3 + 3 + 4 + 1 + 3 * K), dtype=torch.float32, device=device)
-    o = 0
-    parts = []
-    for shp in ((3, n), (3, n), (4, n), (n,), (K, 3, n)):
-        c = int(np.prod(shp))
-        parts.append(flat[o:o + c].view(*shp))
-        o += c
-    grads = P.Gaussians(*parts)
+    fg = FlatGrads.allocate(n, K, device)  # one flat buffer: the all-reduce operand
+    grads = fg.as_gaussians()
     H, W = cams[0].height, cams[0].width
     n_ring = min(B * 2, 8)
     gen = torch.Generator(device=device)
@@ -281,14 +278,12 @@ def run_gpu(args, cfg_name, config):
         P.rd_render_bwd(view, g, cot[0:3], cot[3], cot[4:7], cot[7], grads)
 
     def step():
-        flat.zero_()
+        fg.zero_()
         for b in range(B):
             k = counter["v"]
             counter["v"] += 1
             one_view(my_views[k % len(my_views)], cots[k % n_ring])
-        if dist_on:
-            import torch.distributed as dist
-            dist.all_reduce(flat)
+        fg.allreduce()  # NCCL sum over ranks (no-op at N = 1)
 
     # ---------------- device-resident timed region
     for _ in range(args.warmup):
@@ -324,7 +319,7 @@ def run_gpu(args, cfg_name, config):
 
         def step_e2e():
             nonlocal h2d, d2h
-            flat.zero_()
+            fg.zero_()
             for b in range(B):
                 k = counter["v"]
                 counter["v"] += 1
@@ -334,9 +329,7 @@ def run_gpu(args, cfg_name, config):
                 for key, t in outs.items():
                     host_out[key].copy_(t, non_blocking=True)
                     d2h += t.numel() * 4
-            if dist_on:
-                import torch.distributed as dist
-                dist.all_reduce(flat)
+            fg.allreduce()
 
         steps_e2e = max(1, args.steps // 2)
         step_e2e()
@@ -419,7 +412,8 @@ def run_gpu(args, cfg_name, config):
 
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cam = my_views[0]
-        t, desc, cores, spent = oracle_frame_time(scene, cam, opt, n_pix=args.ref_pixels, n_grad=1, seed=0)
+        t, desc, cores, spent = oracle_frame_time(scene, cam, opt, n_pix=args.cpu_pixels, n_grad=args.cpu_grads,
+                                                  seed=0)
         line["cpu_baseline"] = {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -439,7 +433,10 @@ def main():
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--views-per-step", type=int, default=4)
     ap.add_argument("--n-gaussians", type=int, default=None)
-    ap.add_argument("--ref-pixels", type=int, default=16)
+    ap.add_argument("--ref-pixels", type=int, default=32, help="oracle arm: forward pixels sampled per step")
+    ap.add_argument("--ref-grads", type=int, default=2, help="oracle arm: Gaussians differentiated per step")
+    ap.add_argument("--cpu-pixels", type=int, default=256, help="cpu_baseline: forward pixels sampled")
+    ap.add_argument("--cpu-grads", type=int, default=8, help="cpu_baseline: Gaussians differentiated")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
