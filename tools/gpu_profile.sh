@@ -14,5 +14,5 @@ echo "bench rc=$?" >> gpurun_out/bench_$TAG.log
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline $*"
 $B > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/ncu_list_$TAG.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$KREGEX" -s 12 -c 4 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$KREGEX" -s 10 -c 10 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full_$TAG.log
