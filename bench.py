@@ -256,7 +256,7 @@ def run_gpu(args, cfg_name, config):
     my_views = [cams[v] for v in views_for_rank(len(cams), ws, rank)]
     B = args.views_per_step
     g = P.Gaussians.from_numpy(scene, device)
-    K = g.sh.shape[0]
+    K = g.sh.shape[1]
     fg = FlatGrads.allocate(n, K, device)  # one flat buffer: the all-reduce operand
     grads = fg.as_gaussians()
     H, W = cams[0].height, cams[0].width

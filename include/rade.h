@@ -21,10 +21,12 @@
  * Conventions:
  *   - Camera: world->camera rotation R (row-major) and translation t; +z forward, +y down;
  *     pixel (i, j) is sampled at (i + 0.5, j + 0.5); u = fx·x/z + cx, v = fy·y/z + cy.
- *   - Gaussian arrays are structure-of-arrays fp32 DEVICE arrays:
- *       means[3][n], scales[3][n] (activated, > 0), rotations[4][n] (raw quaternion w,x,y,z;
- *       normalised internally), opacities[n] (activated, in (0,1)),
- *       sh[sh_coeffs][3][n] (coefficient-major, then channel; sh_coeffs = (deg+1)^2 ≤ 16).
+ *   - Gaussian arrays are row-major fp32 DEVICE arrays, one row per Gaussian (the layout of
+ *     the (N,3)/(N,4)/(N,16,3) tensors of a 3DGS trainer; a view touches ~half of the
+ *     Gaussians, and per-Gaussian rows keep the untouched half out of the traffic):
+ *       means[n][3], scales[n][3] (activated, > 0), rotations[n][4] (raw quaternion w,x,y,z,
+ *       normalised internally; the base pointer must be 16-byte aligned),
+ *       opacities[n] (activated, in (0,1)), sh[n][sh_coeffs][3] (sh_coeffs = (deg+1)^2 ≤ 16).
  *   - Image outputs are planar fp32 DEVICE arrays: color[3][H][W], depth[H][W] (0 where the
  *     transmittance never crosses median_T), normal[3][H][W] (camera space, unnormalised
  *     Σ ω n), alpha[H][W] = 1 − T_final.
@@ -39,7 +41,8 @@
  *
  * Errors: functions never throw; they return an rd_status and set a thread-local message
  * readable with rd_last_error(). Invalid arguments (null pointers, n < 0, width/height ≤ 0,
- * tile ∉ {8, 16}, thresholds outside (0, 1), alpha_min ≥ alpha_max, sh_degree > 3 or
+ * rotations not 16-byte aligned, tile ∉ {8, 16}, thresholds outside (0, 1),
+ * alpha_min ≥ alpha_max, sh_degree > 3 or
  * (sh_degree+1)^2 > sh_coeffs) return RD_ERR_INVALID_ARGUMENT; out-of-order calls return
  * RD_ERR_STATE; allocation failure RD_ERR_ALLOC; CUDA launch/runtime errors RD_ERR_CUDA.
  * A degenerate primitive (non-finite input, scale ≤ 0, zero quaternion, centre depth ≤
@@ -89,7 +92,7 @@ typedef struct rd_options {
   int32_t sh_degree; /* active SH degree 0..3 */
 } rd_options;
 
-/* Device SoA Gaussian parameters (see layout above). */
+/* Device Gaussian parameters, one row per Gaussian (see layout above). */
 typedef struct rd_gaussians {
   int64_t n;
   int32_t sh_coeffs; /* coefficients stored per channel: 1, 4, 9 or 16 */

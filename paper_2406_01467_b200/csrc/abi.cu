@@ -232,6 +232,9 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   if (g->n > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "n >= 2^31 not supported");
   if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities || !g->sh))
     return fail(RD_ERR_INVALID_ARGUMENT, "NULL Gaussian array");
+  if (((uintptr_t)g->rotations & 15u) != 0) return fail(RD_ERR_INVALID_ARGUMENT, "rotations not 16-byte aligned");
+  if ((g->sh_coeffs * 3) % 4 == 0 && ((uintptr_t)g->sh & 15u) != 0)
+    return fail(RD_ERR_INVALID_ARGUMENT, "sh not 16-byte aligned");
   if (cam->width <= 0 || cam->height <= 0) return fail(RD_ERR_INVALID_ARGUMENT, "width/height must be > 0");
   if (!(cam->fx > 0.f && cam->fy > 0.f) || !std::isfinite(cam->fx) || !std::isfinite(cam->fy))
     return fail(RD_ERR_INVALID_ARGUMENT, "fx, fy must be finite and > 0");
@@ -393,6 +396,10 @@ rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolo
     return fail(RD_ERR_INVALID_ARGUMENT, "NULL Gaussian array");
   if (g->n > 0 && (!grads->means || !grads->scales || !grads->rotations || !grads->opacities || !grads->sh))
     return fail(RD_ERR_INVALID_ARGUMENT, "NULL gradient array");
+  if ((((uintptr_t)g->rotations | (uintptr_t)grads->rotations) & 15u) != 0)
+    return fail(RD_ERR_INVALID_ARGUMENT, "rotations / their gradients not 16-byte aligned");
+  if ((g->sh_coeffs * 3) % 4 == 0 && (((uintptr_t)g->sh | (uintptr_t)grads->sh) & 15u) != 0)
+    return fail(RD_ERR_INVALID_ARGUMENT, "sh / its gradient not 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t n = (size_t)v->n;
   RD_ENSURE(v->g2d, n * kG2D * sizeof(float), s);
@@ -408,7 +415,9 @@ rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolo
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
   DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
   v->begin(s);
-  launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const float*)v->g2d.ptr, dgr, s);
+  launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr,
+                        (const uint32_t*)(v->dsel ? v->didx1.ptr : v->didx0.ptr),
+                        (const uint32_t*)(v->dsel ? v->dkey1.ptr : v->dkey0.ptr), (const float*)v->g2d.ptr, dgr, s);
   RD_CHECK_LAUNCH("preprocess_bwd");
   v->end(K_PREBWD, s);
   return RD_OK;

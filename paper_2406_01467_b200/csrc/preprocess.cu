@@ -115,6 +115,27 @@ struct GF {
   S e0, e1, p0, p1, n[3];
 };
 
+// First NV floats of one Gaussian's SH row (row-major [n][sh_coeffs][3]) into registers:
+// 16-byte vector loads when the row length is a multiple of 4 floats (rows then stay
+// 16-B aligned), scalar loads otherwise. out[NV..] is zero-filled in the scalar case.
+template <int NV>
+__device__ __forceinline__ void load_sh_row(const float* __restrict__ row, bool vec, float (&out)[(NV + 3) / 4 * 4]) {
+  constexpr int NV4 = (NV + 3) / 4;
+  if (vec) {
+#pragma unroll
+    for (int q = 0; q < NV4; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(row)[q];
+      out[4 * q] = v.x;
+      out[4 * q + 1] = v.y;
+      out[4 * q + 2] = v.z;
+      out[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NV4 * 4; ++j) out[j] = j < NV ? row[j] : 0.f;
+  }
+}
+
 __device__ __forceinline__ bool isfin(float v) { return isfinite(v); }
 __device__ __forceinline__ bool isfin(double v) { return isfinite(v); }
 __device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
@@ -126,10 +147,9 @@ __device__ __forceinline__ double sq_root(double v) { return sqrt(v); }
 template <typename S>
 __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
                                                  GF<S>& f) {
-  const int64_t n = g.n;
-  f.mu[0] = g.means[i];
-  f.mu[1] = g.means[n + i];
-  f.mu[2] = g.means[2 * n + i];
+  f.mu[0] = g.means[3 * i];
+  f.mu[1] = g.means[3 * i + 1];
+  f.mu[2] = g.means[3 * i + 2];
   if (!(isfin(f.mu[0]) && isfin(f.mu[1]) && isfin(f.mu[2]))) return false;
   // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
   const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
@@ -137,13 +157,18 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
   f.zkey = z;
   f.o = g.opac[i];
   if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;
-  f.s[0] = g.scales[i];
-  f.s[1] = g.scales[n + i];
-  f.s[2] = g.scales[2 * n + i];
+  f.s[0] = g.scales[3 * i];
+  f.s[1] = g.scales[3 * i + 1];
+  f.s[2] = g.scales[3 * i + 2];
   if (!(f.s[0] > 0.f && f.s[1] > 0.f && f.s[2] > 0.f) || !(isfin(f.s[0]) && isfin(f.s[1]) && isfin(f.s[2])))
     return false;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) f.qr[k] = g.rot[k * n + i];
+  {
+    const float4 q4 = reinterpret_cast<const float4*>(g.rot)[i];  // [n][4], 16-B aligned rows
+    f.qr[0] = q4.x;
+    f.qr[1] = q4.y;
+    f.qr[2] = q4.z;
+    f.qr[3] = q4.w;
+  }
   if (!(isfin(f.qr[0]) && isfin(f.qr[1]) && isfin(f.qr[2]) && isfin(f.qr[3]))) return false;
   const S ql2 = (S)f.qr[0] * f.qr[0] + (S)f.qr[1] * f.qr[1] + (S)f.qr[2] * f.qr[2] + (S)f.qr[3] * f.qr[3];
   if (!(ql2 > S(0))) return false;
@@ -265,11 +290,14 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   sh_basis(dx, dy, dz, DEG, Y);
   constexpr int K = (DEG + 1) * (DEG + 1);
   float rgb[3] = {0.5f, 0.5f, 0.5f};
-  const int64_t n = g.n;
+  {
+    float c[(3 * K + 3) / 4 * 4];
+    load_sh_row<3 * K>(g.sh + (int64_t)i * g.sh_coeffs * 3, (g.sh_coeffs * 3) % 4 == 0, c);
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < K; ++k) {
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * g.sh[(int64_t)(k * 3 + ch) * n + i];
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * c[k * 3 + ch];
+    }
   }
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
@@ -291,70 +319,71 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
 }
 
 // ---------------------------------------------------------------------------- K5
+// Two kernels, one thread per Gaussian in id order; only visible Gaussians (tiles_touched >
+// 0, ≈ half at C3) read and write their rows, so with row-major parameters the invisible
+// half stays out of the DRAM traffic. K5a (SH colour) and K5b (geometry) are split so each
+// issues its independent loads in one round trip at a register count that keeps enough
+// warps in flight to cover HBM latency. K5a runs first and leaves the view-direction part
+// of dL/dμ in the mean gradient; K5b adds the projection part.
+
+// K5a (per-thread fallback for SH rows that are not a multiple of 4 floats).
 template <int DEG>
-__global__ void __launch_bounds__(128, 4) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
-                                                         const uint32_t* __restrict__ touched,
-                                                         const float* __restrict__ g2d, DevGrads gr) {
+__global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam cam, DevOpt opt,
+                                                           const uint32_t* __restrict__ touched,
+                                                           const float* __restrict__ g2d, DevGrads gr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   if (touched[i] == 0u) return;  // culled or off-screen: zero gradient
-  GF<float> f;
-  if (!gaussian_forward<float>(g, i, cam, opt, f)) return;
-  const int64_t n = g.n;
   const float4* G4 = reinterpret_cast<const float4*>(g2d + i * kG2D);
-  const float4 q0 = G4[0], q1 = G4[1], q2 = G4[2], q3 = G4[3];
-  const float d_u = q0.x, d_v = q0.y, d_A2 = q0.z, d_B2 = q0.w;
-  const float d_C2 = q1.x, d_o = q1.y;
+  const float4 q1 = G4[1], q2 = G4[2];
   const float d_rgb[3] = {q1.z, q1.w, q2.x};
-  const float d_n[3] = {q2.y, q2.z, q2.w};
-  const float d_z = q3.x, d_p0 = q3.y, d_p1 = q3.z;
-
-  float dx[3] = {0.f, 0.f, 0.f};  // dL/dx_c (camera space)
-  float dRc[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) dRc[k] = 0.f;
-  float ds[3] = {0.f, 0.f, 0.f};
-  float dmu[3] = {0.f, 0.f, 0.f};  // direct world-space mean grads (SH view direction)
-
-  // ---- colour / SH (zero gradient through clamped channels)
+  const float mu0 = g.means[3 * i], mu1 = g.means[3 * i + 1], mu2 = g.means[3 * i + 2];
+  float dmu[3] = {0.f, 0.f, 0.f};
   {
-    float ex = f.mu[0] - cam.campos[0], ey = f.mu[1] - cam.campos[1], ez = f.mu[2] - cam.campos[2];
+    float ex = mu0 - cam.campos[0], ey = mu1 - cam.campos[1], ez = mu2 - cam.campos[2];
     const float idl = rsqrtf(ex * ex + ey * ey + ez * ez);
     const float hx = ex * idl, hy = ey * idl, hz = ez * idl;
     float Y[16];
     sh_basis(hx, hy, hz, DEG, Y);
     constexpr int K = (DEG + 1) * (DEG + 1);
     float rgb[3] = {0.5f, 0.5f, 0.5f};
-    float coef[3][16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) coef[ch][k] = 0.f;
+    constexpr int NV = 3 * K, NV4 = (NV + 3) / 4;
+    const bool vec = (g.sh_coeffs * 3) % 4 == 0;
+    float coef[NV4 * 4];
+    load_sh_row<NV>(g.sh + (int64_t)i * g.sh_coeffs * 3, vec, coef);
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        coef[ch][k] = g.sh[(int64_t)(k * 3 + ch) * n + i];
-        rgb[ch] += Y[k] * coef[ch][k];
-      }
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * coef[k * 3 + ch];
     float drgb[3];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) drgb[ch] = rgb[ch] < 0.f ? 0.f : d_rgb[ch];
-    // += into the SH gradient planes: loads batched per chunk so the read-modify-writes
-    // overlap instead of serialising one HBM round trip per coefficient
-    constexpr int NV = 3 * K;
-    constexpr int CH = NV < 16 ? NV : 16;
+    // += into this Gaussian's contiguous SH gradient row (16-B vector RMW when aligned;
+    // entries past the active degree are rewritten unchanged)
+    float* gsh = gr.sh + (int64_t)i * g.sh_coeffs * 3;
+    if (vec) {
+      float4* g4 = reinterpret_cast<float4*>(gsh);
+      float4 old[NV4];
 #pragma unroll
-    for (int c0 = 0; c0 < NV; c0 += CH) {
-      float old[CH];
+      for (int q = 0; q < NV4; ++q) old[q] = g4[q];
 #pragma unroll
-      for (int j = 0; j < CH; ++j) old[j] = gr.sh[(int64_t)(c0 + j) * n + i];
+      for (int q = 0; q < NV4; ++q) {
+        float d[4];
 #pragma unroll
-      for (int j = 0; j < CH; ++j) gr.sh[(int64_t)(c0 + j) * n + i] = old[j] + Y[(c0 + j) / 3] * drgb[(c0 + j) % 3];
+        for (int e = 0; e < 4; ++e) d[e] = (4 * q + e) < NV ? Y[(4 * q + e) / 3] * drgb[(4 * q + e) % 3] : 0.f;
+        g4[q] = make_float4(old[q].x + d[0], old[q].y + d[1], old[q].z + d[2], old[q].w + d[3]);
+      }
+    } else {
+      float old[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) old[j] = gsh[j];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) gsh[j] = old[j] + Y[j / 3] * drgb[j % 3];
     }
     float c16[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) c16[k] = drgb[0] * coef[0][k] + drgb[1] * coef[1][k] + drgb[2] * coef[2][k];
+    for (int k = 0; k < 16; ++k)
+      c16[k] = k < K ? drgb[0] * coef[3 * k] + drgb[1] * coef[3 * k + 1] + drgb[2] * coef[3 * k + 2] : 0.f;
     float gx, gy, gz;
     sh_basis_grad(hx, hy, hz, DEG, c16, gx, gy, gz);
     // through the normalisation of dir
@@ -363,6 +392,30 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(DevGauss g, DevCam ca
     dmu[1] += (gy - hy * dot) * idl;
     dmu[2] += (gz - hz * dot) * idl;
   }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gr.means[3 * i + k] += dmu[k];
+}
+
+// K5b: geometry — centre, conic, depth plane and normal back to μ, s, q, o (dmu_extra: the
+// view-direction part of dL/dμ from K5a when fused).
+__device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
+                                                  const float* __restrict__ g2d, DevGrads& gr,
+                                                  const float (&dmu_extra)[3]) {
+  GF<float> f;
+  if (!gaussian_forward<float>(g, i, cam, opt, f)) return;
+  const float4* G4 = reinterpret_cast<const float4*>(g2d + i * kG2D);
+  const float4 q0 = G4[0], q1 = G4[1], q2 = G4[2], q3 = G4[3];
+  const float d_u = q0.x, d_v = q0.y, d_A2 = q0.z, d_B2 = q0.w;
+  const float d_C2 = q1.x, d_o = q1.y;
+  const float d_n[3] = {q2.y, q2.z, q2.w};
+  const float d_z = q3.x, d_p0 = q3.y, d_p1 = q3.z;
+
+  float dx[3] = {0.f, 0.f, 0.f};  // dL/dx_c (camera space)
+  float dRc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) dRc[k] = 0.f;
+  float ds[3] = {0.f, 0.f, 0.f};
+  float dmu[3] = {0.f, 0.f, 0.f};
 
   // ---- projected centre and centre depth
   const float iz = 1.f / f.x[2];
@@ -483,26 +536,136 @@ __global__ void __launch_bounds__(128, 4) k_preprocess_bwd(DevGauss g, DevCam ca
                   a * dRq[6] + b * dRq[7]);
   const float qd = dqn[0] * w + dqn[1] * a + dqn[2] * b + dqn[3] * c;
 
-  // read-modify-write of the 11 non-SH gradient planes, loads batched first
-  float om[3], os[3], oq[4];
+  // read-modify-write of the non-SH gradient rows, loads batched first
+  float om[3], os[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    om[k] = gr.means[k * n + i];
-    os[k] = gr.scales[k * n + i];
+    om[k] = gr.means[3 * i + k];
+    os[k] = gr.scales[3 * i + k];
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) oq[k] = gr.rot[k * n + i];
+  float4* grot = reinterpret_cast<float4*>(gr.rot) + i;
+  const float4 oq = *grot;
   const float oo = gr.opac[i];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    gr.means[k * n + i] = om[k] + dmu[k];
-    gr.scales[k * n + i] = os[k] + ds[k];
+    gr.means[3 * i + k] = om[k] + dmu[k] + dmu_extra[k];
+    gr.scales[3 * i + k] = os[k] + ds[k];
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) gr.rot[k * n + i] = oq[k] + (dqn[k] - f.qn[k] * qd) * f.qinv;
+  *grot = make_float4(oq.x + (dqn[0] - f.qn[0] * qd) * f.qinv, oq.y + (dqn[1] - f.qn[1] * qd) * f.qinv,
+                      oq.z + (dqn[2] - f.qn[2] * qd) * f.qinv, oq.w + (dqn[3] - f.qn[3] * qd) * f.qinv);
   // α = min(α_max, o·G): d_o already excludes the clamp (K4)
   gr.opac[i] = oo + d_o;
 }
+
+__global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
+                                                        const uint32_t* __restrict__ touched,
+                                                        const float* __restrict__ g2d, DevGrads gr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  if (touched[i] == 0u) return;  // culled or off-screen: zero gradient
+  const float zero[3] = {0.f, 0.f, 0.f};
+  geometry_backward(g, i, cam, opt, g2d, gr, zero);
+}
+
+// K5a (cooperative, rows of a multiple of 4 floats): each warp owns 32 VISIBLE Gaussians —
+// 32 consecutive positions of the depth order (K2a), whose prefix is exactly the visible
+// set — and moves their SH coefficient rows and SH gradient rows between HBM and shared
+// memory cooperatively: each warp-wide 16-B load covers ~3 whole 192-B rows (full sectors,
+// vs 32 scattered half-sectors for per-thread row loads), 2·NV4 loads per lane are in
+// flight at once, and only visible rows are touched. Lane l then works on row l (pitch
+// NV4+1 float4: conflict-free), and the updated gradient rows are stored back the same way.
+template <int DEG>
+__global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCam cam, DevOpt opt,
+                                                               const uint32_t* __restrict__ order,
+                                                               const uint32_t* __restrict__ sorted_keys,
+                                                               const float* __restrict__ g2d, DevGrads gr) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int NV = 3 * K, NV4 = (NV + 3) / 4, P = NV4 + 1;
+  __shared__ float4 s_coef[2][32 * P];
+  __shared__ float4 s_grad[2][32 * P];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = p < g.n && sorted_keys[p] != 0xffffffffu;
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  if (vmask == 0) return;  // warp-uniform: the invisible tail of the depth order
+  const uint32_t id = valid ? order[p] : 0u;
+  const int64_t L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
+  float mu0 = 0.f, mu1 = 0.f, mu2 = 0.f, d_rgb[3] = {0.f, 0.f, 0.f};
+  if (valid) {
+    const float4* G4 = reinterpret_cast<const float4*>(g2d + (size_t)id * kG2D);
+    const float4 q1 = G4[1], q2 = G4[2];
+    d_rgb[0] = q1.z;
+    d_rgb[1] = q1.w;
+    d_rgb[2] = q2.x;
+    mu0 = g.means[3 * (size_t)id];
+    mu1 = g.means[3 * (size_t)id + 1];
+    mu2 = g.means[3 * (size_t)id + 2];
+  }
+  float4* sc = s_coef[warp];
+  float4* sg = s_grad[warp];
+  const float4* sh4 = reinterpret_cast<const float4*>(g.sh);
+  float4* gsh4 = reinterpret_cast<float4*>(gr.sh);
+#pragma unroll
+  for (int it = 0; it < NV4; ++it) {
+    const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
+    const uint32_t rid = __shfl_sync(0xffffffffu, id, row);
+    if ((vmask >> row) & 1u) {
+      sc[row * P + c] = sh4[(int64_t)rid * L4 + c];
+      sg[row * P + c] = gsh4[(int64_t)rid * L4 + c];
+    }
+  }
+  __syncwarp();
+  if (valid) {
+    float ex = mu0 - cam.campos[0], ey = mu1 - cam.campos[1], ez = mu2 - cam.campos[2];
+    const float idl = rsqrtf(ex * ex + ey * ey + ez * ez);
+    const float hx = ex * idl, hy = ey * idl, hz = ez * idl;
+    float Y[16];
+    sh_basis(hx, hy, hz, DEG, Y);
+    float coef[NV4 * 4];
+#pragma unroll
+    for (int q = 0; q < NV4; ++q) {
+      const float4 v = sc[lane * P + q];
+      coef[4 * q] = v.x;
+      coef[4 * q + 1] = v.y;
+      coef[4 * q + 2] = v.z;
+      coef[4 * q + 3] = v.w;
+    }
+    float rgb[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * coef[k * 3 + ch];
+    float drgb[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) drgb[ch] = rgb[ch] < 0.f ? 0.f : d_rgb[ch];  // clamp: zero grad
+#pragma unroll
+    for (int q = 0; q < NV4; ++q) {
+      float d[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) d[e] = (4 * q + e) < NV ? Y[(4 * q + e) / 3] * drgb[(4 * q + e) % 3] : 0.f;
+      const float4 o = sg[lane * P + q];
+      sg[lane * P + q] = make_float4(o.x + d[0], o.y + d[1], o.z + d[2], o.w + d[3]);
+    }
+    float c16[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      c16[k] = k < K ? drgb[0] * coef[3 * k] + drgb[1] * coef[3 * k + 1] + drgb[2] * coef[3 * k + 2] : 0.f;
+    float gx, gy, gz;
+    sh_basis_grad(hx, hy, hz, DEG, c16, gx, gy, gz);
+    const float dot = gx * hx + gy * hy + gz * hz;  // through the normalisation of dir
+    gr.means[3 * (size_t)id] += (gx - hx * dot) * idl;
+    gr.means[3 * (size_t)id + 1] += (gy - hy * dot) * idl;
+    gr.means[3 * (size_t)id + 2] += (gz - hz * dot) * idl;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < NV4; ++it) {
+    const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
+    const uint32_t rid = __shfl_sync(0xffffffffu, id, row);
+    if ((vmask >> row) & 1u) gsh4[(int64_t)rid * L4 + c] = sg[row * P + c];
+  }
+}
+
 
 }  // namespace
 
@@ -524,16 +687,32 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 }
 
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
-                           const float* g2d, DevGrads grads, cudaStream_t s) {
+                           const uint32_t* order, const uint32_t* sorted_keys, const float* g2d, DevGrads grads,
+                           cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = 128;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
-  switch (opt.sh_degree) {
-    case 0: k_preprocess_bwd<0><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
-    case 1: k_preprocess_bwd<1><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
-    case 2: k_preprocess_bwd<2><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
-    default: k_preprocess_bwd<3><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads); break;
+  if ((g.sh_coeffs * 3) % 4 == 0) {
+    const unsigned cblocks = (unsigned)((g.n + 63) / 64);
+#define RD_K5A(D) k_preprocess_bwd_sh_coop<D><<<cblocks, 64, 0, s>>>(g, cam, opt, order, sorted_keys, g2d, grads)
+    switch (opt.sh_degree) {
+      case 0: RD_K5A(0); break;
+      case 1: RD_K5A(1); break;
+      case 2: RD_K5A(2); break;
+      default: RD_K5A(3); break;
+    }
+#undef RD_K5A
+  } else {
+#define RD_K5A(D) k_preprocess_bwd_sh<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads)
+    switch (opt.sh_degree) {
+      case 0: RD_K5A(0); break;
+      case 1: RD_K5A(1); break;
+      case 2: RD_K5A(2); break;
+      default: RD_K5A(3); break;
+    }
+#undef RD_K5A
   }
+  k_preprocess_bwd<<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads);
 }
 
 }  // namespace rade

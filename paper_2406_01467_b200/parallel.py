@@ -36,7 +36,7 @@ class FlatGrads:
 
     @staticmethod
     def allocate(n: int, sh_coeffs: int = 16, device="cuda") -> "FlatGrads":
-        shapes = ((3, n), (3, n), (4, n), (n,), (sh_coeffs, 3, n))
+        shapes = ((n, 3), (n, 3), (n, 4), (n,), (n, sh_coeffs, 3))
         total = sum(int(torch.Size(s).numel()) for s in shapes)
         flat = torch.zeros(total, dtype=torch.float32, device=device)
         parts, o = [], 0

@@ -44,8 +44,9 @@ def _check_f32(name, t, shape=None):
 
 @dataclass
 class Gaussians:
-    """SoA device parameters (include/rade.h rd_gaussians): means [3,N], scales [3,N]
-    (activated), rotations [4,N] (raw w,x,y,z), opacities [N] (activated), sh [K,3,N]."""
+    """Device parameters, one row per Gaussian (include/rade.h rd_gaussians): means [N,3],
+    scales [N,3] (activated), rotations [N,4] (raw w,x,y,z), opacities [N] (activated),
+    sh [N,K,3] — the tensor layout of a 3DGS trainer."""
     means: torch.Tensor
     scales: torch.Tensor
     rotations: torch.Tensor
@@ -58,23 +59,25 @@ class Gaussians:
 
     def validate(self):
         n = self.n
-        _check_f32("means", self.means, (3, n))
-        _check_f32("scales", self.scales, (3, n))
-        _check_f32("rotations", self.rotations, (4, n))
+        _check_f32("means", self.means, (n, 3))
+        _check_f32("scales", self.scales, (n, 3))
+        _check_f32("rotations", self.rotations, (n, 4))
         _check_f32("opacities", self.opacities, (n,))
         _check_f32("sh", self.sh)
-        if self.sh.dim() != 3 or self.sh.shape[1] != 3 or self.sh.shape[2] != n:
-            raise ValueError("sh must be [K, 3, N]")
+        if self.sh.dim() != 3 or self.sh.shape[0] != n or self.sh.shape[2] != 3:
+            raise ValueError("sh must be [N, K, 3]")
 
     def c_struct(self):
         self.validate()
-        return N.RdGaussians(self.n, int(self.sh.shape[0]), self.means.data_ptr(), self.scales.data_ptr(),
+        return N.RdGaussians(self.n, int(self.sh.shape[1]), self.means.data_ptr(), self.scales.data_ptr(),
                              self.rotations.data_ptr(), self.opacities.data_ptr(), self.sh.data_ptr())
 
     @staticmethod
     def from_numpy(scene, device="cuda"):
+        """From a scenegen.Scene (whose arrays are [3][N], [4][N], [K][3][N])."""
         f = lambda a: torch.as_tensor(a, dtype=torch.float32).contiguous().to(device)
-        return Gaussians(f(scene.means), f(scene.scales), f(scene.rotations), f(scene.opacities), f(scene.sh))
+        return Gaussians(f(scene.means.T), f(scene.scales.T), f(scene.rotations.T), f(scene.opacities),
+                         f(scene.sh.transpose(2, 0, 1)))
 
     def zeros_like(self):
         return Gaussians(*(torch.zeros_like(t) for t in (self.means, self.scales, self.rotations, self.opacities,

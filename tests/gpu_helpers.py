@@ -32,13 +32,13 @@ def gpu_grads(scene, cam, opt, cot):
 
 def grads_to_rows(grads, n):
     G = np.zeros((n, 59))
-    G[:, 0:3] = grads.means.double().cpu().numpy().T
-    G[:, 3:6] = grads.scales.double().cpu().numpy().T
-    G[:, 6:10] = grads.rotations.double().cpu().numpy().T
+    G[:, 0:3] = grads.means.double().cpu().numpy()
+    G[:, 3:6] = grads.scales.double().cpu().numpy()
+    G[:, 6:10] = grads.rotations.double().cpu().numpy()
     G[:, 10] = grads.opacities.double().cpu().numpy()
-    sh = grads.sh.double().cpu().numpy()  # [K, 3, N]
-    K = sh.shape[0]
-    G[:, 11:11 + 3 * K] = sh.reshape(3 * K, n).T
+    sh = grads.sh.double().cpu().numpy()  # [N, K, 3]
+    K = sh.shape[1]
+    G[:, 11:11 + 3 * K] = sh.reshape(n, 3 * K)
     return G
 
 

@@ -259,4 +259,4 @@ def test_rasterize_autograd_wrapper():
     L = (color * c["color"]).sum() + (depth * c["depth"]).sum() + (normal * c["normal"]).sum() + (alpha * c["alpha"]).sum()
     L.backward()
     _, G, _ = gpu_grads(scene, cam, opt, cot)
-    np.testing.assert_allclose(ts[0].grad.double().cpu().numpy().T, G[:, 0:3], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(ts[0].grad.double().cpu().numpy(), G[:, 0:3], rtol=1e-4, atol=1e-6)

@@ -33,10 +33,10 @@ def test_views_for_rank_partition():
 def test_flat_grads_layout():
     g = FlatGrads.allocate(5, 16, "cpu")
     assert g.flat.numel() == 59 * 5
-    g.sh[3, 2, 4] = 7.0
-    g.means[1, 0] = 3.0
-    assert g.flat[1 * 5 + 0].item() == 3.0  # means[1][0] of means[3][n]
-    off = (3 + 3 + 4 + 1) * 5 + (3 * 3 + 2) * 5 + 4
+    g.sh[4, 3, 2] = 7.0   # Gaussian 4, coefficient 3, channel 2 of sh[n][K][3]
+    g.means[1, 0] = 3.0   # Gaussian 1, x of means[n][3]
+    assert g.flat[1 * 3 + 0].item() == 3.0
+    off = (3 + 3 + 4 + 1) * 5 + 4 * 48 + 3 * 3 + 2
     assert g.flat[off].item() == 7.0
     g.zero_()
     assert g.flat.abs().sum().item() == 0
