@@ -188,12 +188,13 @@ rd_status rd_view_stats(const rd_view* view, rd_stats* out);
 
 /* Debug copies (device → caller device buffers, async on `stream`), for bit-exact tests:
  *  rd_debug_binning: keys u64[M], ids u32[M] (sorted), ranges u32[2*T] ([first, last)).
- *  rd_debug_preprocess: records f32[n][16] (u, v, conic a, b, c, o, r, g, b, nx, ny, nz,
- *    z_c, p0, p1, 0), rects u32[n][2] (x0 | y0 << 16, x1 | y1 << 16; tiles, half-open),
- *    tiles_touched u32[n]. Any pointer may be NULL.
+ *  rd_debug_preprocess: records f32[n][16] (u, v, A2, B2, C2, log2 o, r, g, b, nx, ny, nz,
+ *    z_c, p0, p1, 1/o) with (A2, B2, C2) = log2(e)·(−a/2, −b, −c/2) for the conic [[a,b],[b,c]]
+ *    of the dilated 2-D covariance; rects u32[n][2] (x0 | y0 << 16, x1 | y1 << 16; tiles,
+ *    half-open), tiles_touched u32[n]. Any pointer may be NULL. Valid for visible Gaussians.
  *  rd_debug_pixel_state: T_final f32[H*W], n_contrib i32[H*W], median_pos i32[H*W].
  *  rd_debug_grads2d: after rd_render_bwd, per-Gaussian 2-D gradients f32[n][16] (du, dv,
- *    da, db, dc, dopacity, dr, dg, db, dnx, dny, dnz, dz, dp0, dp1, 0). */
+ *    dA2, dB2, dC2, dopacity, dr, dg, db, dnx, dny, dnz, dz, dp0, dp1, 0). */
 rd_status rd_debug_binning(const rd_view* view, uint64_t* keys, uint32_t* ids, uint32_t* ranges, rd_stream stream);
 rd_status rd_debug_preprocess(const rd_view* view, float* records, uint32_t* rects, uint32_t* tiles_touched,
                               rd_stream stream);

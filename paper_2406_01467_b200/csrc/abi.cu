@@ -275,6 +275,7 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   for (int k = 0; k < 3; ++k) o.bg[k] = opt->bg[k];
   o.sh_degree = opt->sh_degree;
   o.ln_alpha_min = logf(opt->alpha_min);
+  o.log2_alpha_min = log2f(opt->alpha_min);
   v->tiles_x = tiles_x;
   v->tiles_y = tiles_y;
   int bits = 1;

@@ -305,9 +305,9 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   Record r;
   const double L2E = 1.4426950408889634;
   r.r0 = make_float4(uc, vc, (float)(-0.5 * L2E * f.ca), (float)(-L2E * f.cb));
-  r.r1 = make_float4((float)(-0.5 * L2E * f.cc), f.o, rgb[0], rgb[1]);
+  r.r1 = make_float4((float)(-0.5 * L2E * f.cc), (float)log2((double)f.o), rgb[0], rgb[1]);
   r.r2 = make_float4(rgb[2], (float)f.n[0], (float)f.n[1], (float)f.n[2]);
-  r.r3 = make_float4(f.zkey, (float)f.p0, (float)f.p1, 0.f);
+  r.r3 = make_float4(f.zkey, (float)f.p0, (float)f.p1, 1.f / f.o);
   rec[i] = r;
   rect[i] = make_uint2(tx0 | (ty0 << 16), tx1 | (ty1 << 16));
   touched[i] = (tx1 - tx0) * (ty1 - ty0);

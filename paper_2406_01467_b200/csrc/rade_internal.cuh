@@ -27,6 +27,7 @@ struct DevOpt {
   float bg[3];
   int sh_degree;  // active degree
   float ln_alpha_min;
+  float log2_alpha_min;
 };
 
 struct DevGauss {
@@ -48,7 +49,7 @@ struct DevGrads {
 };
 
 // Per-visible-Gaussian record written by K1 and gathered by K3/K4 (64 B, 4 x float4):
-//   r0 = (u_c, v_c, A2, B2)   r1 = (C2, o, R, G)   r2 = (B, nx, ny, nz)   r3 = (z_c, p0, p1, 0)
+//   r0 = (u_c, v_c, A2, B2)   r1 = (C2, log2 o, R, G)   r2 = (B, nx, ny, nz)   r3 = (z_c, p0, p1, 1/o)
 // where (A2, B2, C2) = log2(e) * (-a/2, -b, -c/2) for the conic [[a, b], [b, c]] of the
 // dilated 2-D covariance, so that G = exp2(A2 dx^2 + B2 dx dy + C2 dy^2) with
 // (dx, dy) = (u_c - u, v_c - v) (readings S1, S4, S5).
@@ -67,20 +68,23 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // The per-pair α evaluation shared bit-for-bit by K3 and K4 (explicit roundings so the
-// two kernels take identical skip / stop decisions).
+// two kernels take identical skip / stop decisions). With lo = log2(o) stored in the record,
+//   e = A2 dx² + B2 dx dy + C2 dy² + lo,   α_raw = o·exp(−½ΔᵀCΔ) = 2^e,
+// so the α ≥ α_min test is e ≥ log2(α_min) — taken BEFORE the exp2, which rejected pairs
+// never evaluate — and α = min(α_max, 2^e) (readings S1, S8).
 struct PairAlpha {
-  float dx, dy, G, a_raw, alpha;
+  float dx, dy, e;
+  bool pass;
 };
-__device__ __forceinline__ PairAlpha eval_alpha(const float4& r0, float C2, float o, float px, float py,
-                                                float alpha_max) {
+__device__ __forceinline__ PairAlpha pair_power(const float4& r0, float C2, float lo, float px, float py,
+                                                float log2_alpha_min) {
   PairAlpha pa;
   pa.dx = __fsub_rn(r0.x, px);
   pa.dy = __fsub_rn(r0.y, py);
-  float inner = __fmaf_rn(r0.z, pa.dx, __fmul_rn(r0.w, pa.dy));          // A2 dx + B2 dy
-  float pw = __fmaf_rn(pa.dx, inner, __fmul_rn(__fmul_rn(C2, pa.dy), pa.dy));  // + C2 dy^2
-  pa.G = ex2_approx(pw);
-  pa.a_raw = __fmul_rn(o, pa.G);
-  pa.alpha = fminf(alpha_max, pa.a_raw);
+  const float inner = __fmaf_rn(r0.z, pa.dx, __fmul_rn(r0.w, pa.dy));                    // A2 dx + B2 dy
+  const float pw = __fmaf_rn(pa.dx, inner, __fmul_rn(__fmul_rn(C2, pa.dy), pa.dy));     // + C2 dy²
+  pa.e = __fadd_rn(pw, lo);
+  pa.pass = pa.e >= log2_alpha_min;
   return pa;
 }
 

@@ -47,16 +47,17 @@ __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool insi
 __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4* __restrict__ s2,
                                          const uint32_t* __restrict__ sid, const Record* __restrict__ rec, int j,
                                          int pos, const DevOpt& opt) {
-  const PairAlpha pa = eval_alpha(a0, a1.x, a1.y, s.px, s.py, opt.alpha_max);
+  const PairAlpha pa = pair_power(a0, a1.x, a1.y, s.px, s.py, opt.log2_alpha_min);
   ++s.n_eval;
-  if (pa.alpha < opt.alpha_min) return;
-  const float Tn = __fmul_rn(s.T, __fsub_rn(1.f, pa.alpha));
-  if (Tn < opt.T_min) {
+  if (!pa.pass) return;  // α < α_min: skipped (S8)
+  const float alpha = fminf(opt.alpha_max, ex2_approx(pa.e));
+  const float Tn = __fmul_rn(s.T, __fsub_rn(1.f, alpha));
+  if (Tn < opt.T_min) {  // stop before blending this splat (S8)
     s.done = true;
     return;
   }
   const float4 a2 = s2[j];
-  const float w = __fmul_rn(pa.alpha, s.T);
+  const float w = __fmul_rn(alpha, s.T);
   s.C0 = __fmaf_rn(w, a1.z, s.C0);
   s.C1 = __fmaf_rn(w, a1.w, s.C1);
   s.C2 = __fmaf_rn(w, a2.x, s.C2);
@@ -214,45 +215,43 @@ __device__ __forceinline__ void pixb_init(PixB& s, float px, float py, bool insi
 // α gradient of Eq.3's colour and of the normal map is
 //   ∂L/∂α_i = T_i (c_i·g_C + n_i·g_N) − D_i / (1 − α_i) + T_final/(1 − α_i) (g_A − bg·g_C)
 // (the 3DGS derivation collapsed to one scalar, since g_C, g_N are per-pixel constants).
-__device__ __forceinline__ bool bwd_step(PixB& s, float (&g)[16], const float4& a0, const float4& a1,
-                                         const float4* __restrict__ s2, const float2* __restrict__ s3, int j, int pos,
-                                         const DevOpt& opt) {
-  if (pos >= s.last) return false;
-  const PairAlpha pa = eval_alpha(a0, a1.x, a1.y, s.px, s.py, opt.alpha_max);
-  if (pa.alpha < opt.alpha_min) return false;
-  const float4 a2 = s2[j];
-  const float rinv = __fdividef(1.f, 1.f - pa.alpha);  // α ≤ α_max < 1
-  s.T = s.T * rinv;                                     // T_i = T_{i+1} / (1 − α_i)
-  const float w = pa.alpha * s.T;
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Branch-free: an inactive pair (past the pixel's list, or α < α_min) contributes exact
+// zeros (α masked to 0 ⇒ rinv = 1, w = 0, dL/dα = 0), so the warp runs one straight-line
+// sequence instead of divergent paths. FIRST writes g[0..11], otherwise adds.
+template <bool FIRST>
+__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[16], const PairAlpha& pa, bool act, const float4& a0,
+                                          const float4& a1, const float4& a2, float inv_o, const DevOpt& opt) {
+  const float a_raw = ex2_approx(pa.e);                  // o·exp(−½ΔᵀCΔ)
+  const float al = act ? fminf(opt.alpha_max, a_raw) : 0.f;
+  const float rinv = act ? rcp_approx(1.f - al) : 1.f;   // α ≤ α_max < 1
+  s.T = s.T * rinv;                                      // T_i = T_{i+1} / (1 − α_i)
+  const float w = al * s.T;
   const float dot = a1.z * s.gC0 + a1.w * s.gC1 + a2.x * s.gC2 + a2.y * s.gN0 + a2.z * s.gN1 + a2.w * s.gN2;
-  const float dL_dal = s.T * dot - rinv * (s.Dsuf - s.TFa);
+  const float dL_dal = act && a_raw <= opt.alpha_max ? s.T * dot - rinv * (s.Dsuf - s.TFa) : 0.f;  // clamp (S8)
   s.Dsuf = fmaf(w, dot, s.Dsuf);
-  g[6] += w * s.gC0;
-  g[7] += w * s.gC1;
-  g[8] += w * s.gC2;
-  g[9] += w * s.gN0;
-  g[10] += w * s.gN1;
-  g[11] += w * s.gN2;
-  if (pa.a_raw <= opt.alpha_max) {  // α not clamped (S8)
-    const float dG = pa.G * dL_dal;
-    g[5] += dG;
-    const float dpw = a1.y * dG * kLn2;  // dL/d(power in log2 units)
-    const float hx = dpw * pa.dx, hy = dpw * pa.dy;
-    g[0] += 2.f * a0.z * hx + a0.w * hy;
-    g[1] += a0.w * hx + 2.f * a1.x * hy;
-    g[2] += hx * pa.dx;
-    g[3] += hx * pa.dy;
-    g[4] += hy * pa.dy;
-  }
-  if (pos == s.med) {  // median depth D = z_c + p·Δ (Eq.4)
-    const float2 p = s3[j];
-    g[0] += s.gD * p.x;
-    g[1] += s.gD * p.y;
-    g[12] += s.gD;
-    g[13] += s.gD * pa.dx;
-    g[14] += s.gD * pa.dy;
-  }
-  return true;
+  const float dA = a_raw * dL_dal;                       // α_raw·∂L/∂α
+  const float dpw = dA * kLn2;                           // dL/d(power in log2 units)
+  const float hx = dpw * pa.dx, hy = dpw * pa.dy;
+  const float v[12] = {2.f * a0.z * hx + a0.w * hy, a0.w * hx + 2.f * a1.x * hy, hx * pa.dx, hx * pa.dy,
+                       hy * pa.dy, dA * inv_o,           // ∂α/∂o = α_raw/o
+                       w * s.gC0, w * s.gC1, w * s.gC2, w * s.gN0, w * s.gN1, w * s.gN2};
+#pragma unroll
+  for (int k = 0; k < 12; ++k) g[k] = FIRST ? v[k] : g[k] + v[k];
+}
+
+// Median-depth terms D = z_c + p·Δ (Eq.4), at the pixel's median splat only.
+__device__ __forceinline__ void bwd_median(const PixB& s, float (&g)[16], const PairAlpha& pa, const float4& p) {
+  g[0] += s.gD * p.y;
+  g[1] += s.gD * p.z;
+  g[12] += s.gD;
+  g[13] += s.gD * pa.dx;
+  g[14] += s.gD * pa.dy;
 }
 
 template <int TILE>
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
   const int lane = (int)(threadIdx.x & 31);
 
   __shared__ float4 s0[BATCH], s1[BATCH], s2[BATCH];
-  __shared__ float2 s3[BATCH];  // (p0, p1) for the median-depth gradient
+  __shared__ float4 s3[BATCH];  // (z_c, p0, p1, 1/o)
   __shared__ uint32_t sid[BATCH];
   __shared__ int s_maxlast;
 
@@ -305,8 +304,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
         s0[t] = r->r0;
         s1[t] = r->r1;
         s2[t] = r->r2;
-        const float4 r3 = r->r3;
-        s3[t] = make_float2(r3.y, r3.z);
+        s3[t] = r->r3;
       }
     }
     __syncthreads();
@@ -314,14 +312,20 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
       const int pos = start + j;
       if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
       const float4 a0 = s0[j], a1 = s1[j];
-      float g[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) g[k] = 0.f;
-      const bool actA = bwd_step(A, g, a0, a1, s2, s3, j, pos, opt);
-      const bool actB = bwd_step(B, g, a0, a1, s2, s3, j, pos, opt);
+      const PairAlpha pA = pair_power(a0, a1.x, a1.y, A.px, A.py, opt.log2_alpha_min);
+      const PairAlpha pB = pair_power(a0, a1.x, a1.y, B.px, B.py, opt.log2_alpha_min);
+      const bool actA = pos < A.last && pA.pass;
+      const bool actB = pos < B.last && pB.pass;
       const bool active = actA || actB;
       const unsigned act = __ballot_sync(0xffffffffu, active);
-      if (act) {
+      if (act) {  // warp-uniform: the splat contributes to some pixel of this warp
+        const float4 a2 = s2[j], a3 = s3[j];
+        float g[16];
+        bwd_accum<true>(A, g, pA, actA, a0, a1, a2, a3.w, opt);
+        bwd_accum<false>(B, g, pB, actB, a0, a1, a2, a3.w, opt);
+        g[12] = g[13] = g[14] = g[15] = 0.f;
+        if (actA && pos == A.med) bwd_median(A, g, pA, a3);
+        if (actB && pos == B.med) bwd_median(B, g, pB, a3);
         float* dst = g2d + (size_t)sid[j] * kG2D;
         if (__popc(act) == 1) {  // one contributing thread in this warp: no reduction needed
           if (active) {

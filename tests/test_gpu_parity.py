@@ -96,7 +96,8 @@ def test_preprocess_parity(case):
     log2e = 1.4426950408889634
     conic = np.stack([-2 * r[:, 2] / log2e, -r[:, 3] / log2e, -2 * r[:, 4] / log2e], 1)
     np.testing.assert_allclose(conic, o[:, oracle.PG["conic"]], rtol=2e-4, atol=1e-7)
-    np.testing.assert_allclose(r[:, 5], o[:, oracle.PG["o"]], rtol=1e-7)
+    np.testing.assert_allclose(np.exp2(r[:, 5]), o[:, oracle.PG["o"]], rtol=1e-6)  # log2 o
+    np.testing.assert_allclose(r[:, 15], 1.0 / o[:, oracle.PG["o"]], rtol=1e-6)   # 1/o
     np.testing.assert_allclose(r[:, 6:9], o[:, oracle.PG["rgb"]], atol=1e-5)
     np.testing.assert_allclose(r[:, 12], o[:, oracle.PG["z"]], rtol=1e-6)
     ng = np.abs(o[:, oracle.PG["ndotx"]]) >= 0.05
