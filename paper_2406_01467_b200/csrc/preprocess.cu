@@ -606,14 +606,16 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
   const float4* sh4 = reinterpret_cast<const float4*>(g.sh);
   float4* gsh4 = reinterpret_cast<float4*>(gr.sh);
 #pragma unroll
-  for (int it = 0; it < NV4; ++it) {
+  for (int it = 0; it < NV4; ++it) {  // all 2·NV4 copies per lane in flight at once
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
     const uint32_t rid = __shfl_sync(0xffffffffu, id, row);
     if ((vmask >> row) & 1u) {
-      sc[row * P + c] = sh4[(int64_t)rid * L4 + c];
-      sg[row * P + c] = gsh4[(int64_t)rid * L4 + c];
+      cp_async16(&sc[row * P + c], &sh4[(int64_t)rid * L4 + c]);
+      cp_async16(&sg[row * P + c], &gsh4[(int64_t)rid * L4 + c]);
     }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncwarp();
   if (valid) {
     float ex = mu0 - cam.campos[0], ey = mu1 - cam.campos[1], ez = mu2 - cam.campos[2];

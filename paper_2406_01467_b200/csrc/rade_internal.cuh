@@ -61,6 +61,17 @@ struct __align__(16) Record {
 //   du, dv, dA2, dB2, dC2, dopacity, dR, dG, dB, dnx, dny, dnz, dz, dp0, dp1, unused
 constexpr int kG2D = 16;
 
+// 16-byte global → shared copy without a register round trip (cp.async / LDGSTS, L2-only).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
