@@ -44,11 +44,11 @@ __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool insi
 }
 
 // One (pixel, splat) step of Eq.3 with the median-depth selection of reading S9.
-__device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4* __restrict__ s2,
-                                         const uint32_t* __restrict__ sid, const Record* __restrict__ rec, int j,
-                                         int pos, const DevOpt& opt) {
+template <bool PROF>
+__device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4& a2, uint32_t id,
+                                         const Record* __restrict__ rec, int pos, const DevOpt& opt) {
   const PairAlpha pa = pair_power(a0, a1.x, a1.y, s.px, s.py, opt.log2_alpha_min);
-  ++s.n_eval;
+  if (PROF) ++s.n_eval;
   if (!pa.pass) return;  // α < α_min: skipped (S8)
   const float alpha = fminf(opt.alpha_max, ex2_approx(pa.e));
   const float Tn = __fmul_rn(s.T, __fsub_rn(1.f, alpha));
@@ -56,7 +56,6 @@ __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4
     s.done = true;
     return;
   }
-  const float4 a2 = s2[j];
   const float w = __fmul_rn(alpha, s.T);
   s.C0 = __fmaf_rn(w, a1.z, s.C0);
   s.C1 = __fmaf_rn(w, a1.w, s.C1);
@@ -65,13 +64,13 @@ __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4
   s.N1 = __fmaf_rn(w, a2.z, s.N1);
   s.N2 = __fmaf_rn(w, a2.w, s.N2);
   if (s.T > opt.median_T && Tn <= opt.median_T) {
-    const float4 a3 = rec[sid[j]].r3;  // (z_c, p0, p1): once per pixel
+    const float4 a3 = rec[id].r3;  // (z_c, p0, p1): once per pixel
     s.D = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
     s.med = pos;
   }
   s.T = Tn;
   s.last = pos + 1;
-  ++s.n_blend;
+  if (PROF) ++s.n_blend;
 }
 
 __device__ __forceinline__ void fwd_store(const PixF& s, bool inside, int pix, int HW, const DevOpt& opt,
@@ -97,7 +96,7 @@ __device__ __forceinline__ void fwd_store(const PixF& s, bool inside, int pix, i
   median_pos[pix] = s.med;
 }
 
-template <int TILE>
+template <int TILE, bool PROF>
 __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOpt opt, int tiles_x,
                                                                 const uint2* __restrict__ ranges,
                                                                 const uint32_t* __restrict__ ids,
@@ -119,8 +118,11 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   const uint2 range = ranges[tile];
   const int total = (int)(range.y - range.x);
 
-  __shared__ float4 s0[BATCH], s1[BATCH], s2[BATCH];
+  __shared__ float4 sbuf[3][BATCH];  // record quarters r0, r1, r2 of the batch
   __shared__ uint32_t sid[BATCH];
+  float4* s0 = sbuf[0];
+  float4* s1 = sbuf[1];
+  float4* s2 = sbuf[2];
 
   PixF A, B;
   pixf_init(A, (float)px + 0.5f, (float)pyA + 0.5f, inA);
@@ -142,14 +144,17 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
     }
     __syncthreads();
     const int cnt = min(BATCH, total - base);
+    const unsigned a_s0 = smem_addr(s0), a_id = smem_addr(sid);  // s0, s1, s2 are contiguous
     for (int j = 0; j < cnt; ++j) {
       if (A.done && B.done) break;
-      const float4 a0 = s0[j], a1 = s1[j];
-      if (!A.done) fwd_step(A, a0, a1, s2, sid, rec, j, base + j, opt);
-      if (!B.done) fwd_step(B, a0, a1, s2, sid, rec, j, base + j, opt);
+      const unsigned a = a_s0 + 16u * j;
+      const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH), a2 = lds128(a + 32u * BATCH);
+      const uint32_t id = lds32(a_id + 4u * j);
+      if (!A.done) fwd_step<PROF>(A, a0, a1, a2, id, rec, base + j, opt);
+      if (!B.done) fwd_step<PROF>(B, a0, a1, a2, id, rec, base + j, opt);
     }
   }
-  if (counters) {
+  if (PROF) {
     warp_count(counters + 0, A.n_eval + B.n_eval);
     warp_count(counters + 1, A.n_blend + B.n_blend);
   }
@@ -272,10 +277,13 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
   const int HW = cam.W * cam.H;
   const int lane = (int)(threadIdx.x & 31);
 
-  __shared__ float4 s0[BATCH], s1[BATCH], s2[BATCH];
-  __shared__ float4 s3[BATCH];  // (z_c, p0, p1, 1/o)
+  __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch; r3 = (z_c, p0, p1, 1/o)
   __shared__ uint32_t sid[BATCH];
   __shared__ int s_maxlast;
+  float4* s0 = sbuf[0];
+  float4* s1 = sbuf[1];
+  float4* s2 = sbuf[2];
+  float4* s3 = sbuf[3];
 
   PixB A, B;
   pixb_init(A, (float)px + 0.5f, (float)pyA + 0.5f, inA, pyA * cam.W + px, HW, opt, T_final, n_contrib, median_pos,
@@ -308,10 +316,12 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
       }
     }
     __syncthreads();
+    const unsigned a_s0 = smem_addr(s0), a_id = smem_addr(sid);
     for (int j = cnt - 1; j >= 0; --j) {
       const int pos = start + j;
       if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
-      const float4 a0 = s0[j], a1 = s1[j];
+      const unsigned a = a_s0 + 16u * j;
+      const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const PairAlpha pA = pair_power(a0, a1.x, a1.y, A.px, A.py, opt.log2_alpha_min);
       const PairAlpha pB = pair_power(a0, a1.x, a1.y, B.px, B.py, opt.log2_alpha_min);
       const bool actA = pos < A.last && pA.pass;
@@ -319,14 +329,14 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
       const bool active = actA || actB;
       const unsigned act = __ballot_sync(0xffffffffu, active);
       if (act) {  // warp-uniform: the splat contributes to some pixel of this warp
-        const float4 a2 = s2[j], a3 = s3[j];
+        const float4 a2 = lds128(a + 32u * BATCH), a3 = lds128(a + 48u * BATCH);
         float g[16];
         bwd_accum<true>(A, g, pA, actA, a0, a1, a2, a3.w, opt);
         bwd_accum<false>(B, g, pB, actB, a0, a1, a2, a3.w, opt);
         g[12] = g[13] = g[14] = g[15] = 0.f;
         if (actA && pos == A.med) bwd_median(A, g, pA, a3);
         if (actB && pos == B.med) bwd_median(B, g, pB, a3);
-        float* dst = g2d + (size_t)sid[j] * kG2D;
+        float* dst = g2d + (size_t)lds32(a_id + 4u * j) * kG2D;
         if (__popc(act) == 1) {  // one contributing thread in this warp: no reduction needed
           if (active) {
 #pragma unroll
@@ -348,12 +358,15 @@ void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal, float* alpha,
                        float* T_final, int32_t* n_contrib, int32_t* median_pos, Counter* counters, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
-  if (opt.tile == 16)
-    k_render_fwd<16><<<grid, 128, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal, alpha, T_final,
-                                          n_contrib, median_pos, counters);
-  else
-    k_render_fwd<8><<<grid, 32, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal, alpha, T_final,
-                                        n_contrib, median_pos, counters);
+#define RD_K3(T, P)                                                                                              \
+  k_render_fwd<T, P><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal, alpha, \
+                                                T_final, n_contrib, median_pos, counters)
+  if (opt.tile == 16) {
+    if (counters) RD_K3(16, true); else RD_K3(16, false);
+  } else {
+    if (counters) RD_K3(8, true); else RD_K3(8, false);
+  }
+#undef RD_K3
 }
 
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
