@@ -143,9 +143,9 @@ __device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
 __device__ __forceinline__ float sq_root(float v) { return sqrtf(v); }
 __device__ __forceinline__ double sq_root(double v) { return sqrt(v); }
 
-// Loads one Gaussian and runs stage 1 up to (but not including) SH. Returns false if culled.
+// Loads one Gaussian and runs stage 1 up to the conic (no plane, no SH). False if culled.
 template <typename S>
-__device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
+__device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
                                                  GF<S>& f) {
   f.mu[0] = g.means[3 * i];
   f.mu[1] = g.means[3 * i + 1];
@@ -219,8 +219,12 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
   f.ca = f.A11 * idet;
   f.cb = -f.A01 * idet;
   f.cc = f.A00 * idet;
+  return true;
+}
 
-  // depth plane and normal (m-form of Eq.12-15, 21-22)
+// Depth plane and normal (m-form of Eq.12-15, 21-22). Returns false if degenerate.
+template <typename S>
+__device__ __forceinline__ bool gaussian_plane(const DevCam& cam, GF<S>& f) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) f.xh[k] = f.x[k] * f.it;
 #pragma unroll
@@ -246,6 +250,13 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
   return true;
 }
 
+// Stage 1 up to (but not including) SH. Returns false if culled.
+template <typename S>
+__device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
+                                                 GF<S>& f) {
+  return gaussian_project<S>(g, i, cam, opt, f) && gaussian_plane<S>(cam, f);
+}
+
 // ---------------------------------------------------------------------------- K1
 template <int DEG>
 __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
@@ -257,7 +268,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   if (i >= g.n) return;
   didx[i] = (uint32_t)i;
   GF<double> f;
-  if (!gaussian_forward<double>(g, i, cam, opt, f)) {
+  if (!gaussian_project<double>(g, i, cam, opt, f)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
     return;
@@ -282,22 +293,27 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   const uint32_t tx0 = (uint32_t)fx0 / T, tx1 = (uint32_t)fx1 / T + 1;
   const uint32_t ty0 = (uint32_t)fy0 / T, ty1 = (uint32_t)fy1 / T + 1;
 
+  // visible: issue the SH row loads now so their latency overlaps the plane math
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  float c[(3 * K + 3) / 4 * 4];
+  load_sh_row<3 * K>(g.sh + (int64_t)i * g.sh_coeffs * 3, (g.sh_coeffs * 3) % 4 == 0, c);
+  if (!gaussian_plane<double>(cam, f)) {
+    touched[i] = 0u;
+    dkey[i] = 0xffffffffu;
+    return;
+  }
+
   // colour: dir = normalize(μ − campos), degree ≤ sh_degree, + 0.5, clamp ≥ 0
   float dx = f.mu[0] - cam.campos[0], dy = f.mu[1] - cam.campos[1], dz = f.mu[2] - cam.campos[2];
   const float idl = rsqrtf(dx * dx + dy * dy + dz * dz);
   dx *= idl; dy *= idl; dz *= idl;
   float Y[16];
   sh_basis(dx, dy, dz, DEG, Y);
-  constexpr int K = (DEG + 1) * (DEG + 1);
   float rgb[3] = {0.5f, 0.5f, 0.5f};
-  {
-    float c[(3 * K + 3) / 4 * 4];
-    load_sh_row<3 * K>(g.sh + (int64_t)i * g.sh_coeffs * 3, (g.sh_coeffs * 3) % 4 == 0, c);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+  for (int k = 0; k < K; ++k) {
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * c[k * 3 + ch];
-    }
+    for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * c[k * 3 + ch];
   }
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(rgb[ch], 0.f);
