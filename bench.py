@@ -435,8 +435,8 @@ def main():
     ap.add_argument("--n-gaussians", type=int, default=None)
     ap.add_argument("--ref-pixels", type=int, default=32, help="oracle arm: forward pixels sampled per step")
     ap.add_argument("--ref-grads", type=int, default=2, help="oracle arm: Gaussians differentiated per step")
-    ap.add_argument("--cpu-pixels", type=int, default=256, help="cpu_baseline: forward pixels sampled")
-    ap.add_argument("--cpu-grads", type=int, default=8, help="cpu_baseline: Gaussians differentiated")
+    ap.add_argument("--cpu-pixels", type=int, default=2048, help="cpu_baseline: forward pixels sampled")
+    ap.add_argument("--cpu-grads", type=int, default=64, help="cpu_baseline: Gaussians differentiated")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
