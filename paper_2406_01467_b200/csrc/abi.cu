@@ -76,8 +76,9 @@ struct rd_view {
   int tile_bits = 0;
   int64_t M = 0;
   int dsel = 0, tsel = 0;  // CUB DoubleBuffer selectors of the depth and tile sorts
-  uint32_t* host_M = nullptr;  // pinned
-  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp;
+  int64_t n_vis = 0;
+  uint32_t* host_M = nullptr;  // pinned: [0] M, [1] visible Gaussians
+  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp, vis, nvis;
   Buf tkeys0, tkeys1, vals0, vals1;
   Buf ranges;
   Buf T_final, n_contrib, median_pos;
@@ -212,7 +213,7 @@ rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
                 &v->didx1,  &v->tmp,    &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters};
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->vis, &v->nvis};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
@@ -292,15 +293,20 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   RD_ENSURE(v->dkey1, n * sizeof(uint32_t), s);
   RD_ENSURE(v->didx0, n * sizeof(uint32_t), s);
   RD_ENSURE(v->didx1, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->vis, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->nvis, sizeof(uint32_t), s);
 
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
-  v->begin(s);
-  launch_preprocess_fwd(dg, c, o, tiles_x, tiles_y, (Record*)v->rec.ptr, (uint2*)v->rect.ptr,
-                        (uint32_t*)v->touched.ptr, (uint32_t*)v->dkey0.ptr, (uint32_t*)v->didx0.ptr, v->ctr(), s);
+  v->begin(s);  // K1 timing includes the zeroing of the visible counter
+  RD_CUDA(cudaMemsetAsync(v->nvis.ptr, 0, sizeof(uint32_t), s));
+  launch_preprocess_fwd(dg, c, o, tiles_x, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
+                        (uint32_t*)v->dkey0.ptr, (uint32_t*)v->didx0.ptr, (uint32_t*)v->nvis.ptr,
+                        (uint32_t*)v->vis.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("preprocess_fwd");
   v->end(K_PRE, s);
   v->stage = 1;
   v->M = 0;
+  v->n_vis = 0;
   return RD_OK;
 }
 
@@ -317,7 +323,7 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   if (n > 0) {
     const size_t tb = binning_temp_bytes(n, 0, v->tile_bits);
     RD_ENSURE(v->tmp, tb, s);
-    if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, sizeof(uint32_t)));
+    if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, 2 * sizeof(uint32_t)));
     v->begin(s);
     v->dsel = launch_depth_sort((uint32_t*)v->dkey0.ptr, (uint32_t*)v->dkey1.ptr, (uint32_t*)v->didx0.ptr,
                                 (uint32_t*)v->didx1.ptr, n, v->tmp.ptr, v->tmp.cap, s);
@@ -330,8 +336,10 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
     v->end(K_SCAN, s);
     RD_CUDA(cudaMemcpyAsync(v->host_M, (const uint32_t*)v->offsets.ptr + (n - 1), sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, s));
+    RD_CUDA(cudaMemcpyAsync(v->host_M + 1, v->nvis.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     RD_CUDA(cudaStreamSynchronize(s));
-    M = (int64_t)*v->host_M;
+    M = (int64_t)v->host_M[0];
+    v->n_vis = (int64_t)v->host_M[1];
   }
   if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
   RD_ENSURE(v->tkeys0, (size_t)M * sizeof(uint32_t), s);
@@ -416,9 +424,8 @@ rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolo
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
   DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
   v->begin(s);
-  launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr,
-                        (const uint32_t*)(v->dsel ? v->didx1.ptr : v->didx0.ptr),
-                        (const uint32_t*)(v->dsel ? v->dkey1.ptr : v->dkey0.ptr), (const float*)v->g2d.ptr, dgr, s);
+  launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const uint32_t*)v->vis.ptr, v->n_vis,
+                        (const float*)v->g2d.ptr, dgr, s);
   RD_CHECK_LAUNCH("preprocess_bwd");
   v->end(K_PREBWD, s);
   return RD_OK;

@@ -113,13 +113,32 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, int64_t m,
   }
 }
 
+// 8 consecutive sorted keys per thread (two 16-B loads) + the next one; a boundary between
+// positions k and k+1 closes tile keys[k] and opens tile keys[k+1].
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int64_t m,
                                                  uint2* __restrict__ ranges) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  const uint32_t tile = keys[k];
-  if (k == 0 || keys[k - 1] != tile) ranges[tile].x = (uint32_t)k;
-  if (k == m - 1 || keys[k + 1] != tile) ranges[tile].y = (uint32_t)(k + 1);
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (b >= m) return;
+  uint32_t k[9];
+  if (b + 8 <= m) {
+    const uint4 q0 = *reinterpret_cast<const uint4*>(keys + b);
+    const uint4 q1 = *reinterpret_cast<const uint4*>(keys + b + 4);
+    k[0] = q0.x; k[1] = q0.y; k[2] = q0.z; k[3] = q0.w;
+    k[4] = q1.x; k[5] = q1.y; k[6] = q1.z; k[7] = q1.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) k[j] = b + j < m ? keys[b + j] : 0xffffffffu;
+  }
+  k[8] = b + 8 < m ? keys[b + 8] : 0xffffffffu;
+  if (b == 0) ranges[k[0]].x = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t p = b + j;
+    if (p < m && k[j] != k[j + 1]) {
+      ranges[k[j]].y = (uint32_t)(p + 1);
+      if (p + 1 < m) ranges[k[j + 1]].x = (uint32_t)(p + 1);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_keys64(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ ids,
@@ -177,7 +196,8 @@ void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, 
   cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
   if (m == 0) return;
   const int threads = 256;
-  k_ranges<<<(unsigned)((m + threads - 1) / threads), threads, 0, s>>>(keys, m, ranges);
+  const int64_t items = (m + 7) / 8;
+  k_ranges<<<(unsigned)((items + threads - 1) / threads), threads, 0, s>>>(keys, m, ranges);
 }
 
 void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,

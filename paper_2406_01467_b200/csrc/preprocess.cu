@@ -1,8 +1,10 @@
 // preprocess.cu — K1 (per-Gaussian forward, stage 1) and K5 (per-Gaussian backward,
 // second half of stage 4) of the RaDe-GS rasterizer, sm_100a.
 //
-// One thread per Gaussian; structure-of-arrays inputs so every parameter plane is read
-// coalesced (HBM-bound kernels: ~236 B in, 80 B out per visible Gaussian).
+// One thread per Gaussian over row-major parameters (means[N][3], scales[N][3],
+// rotations[N][4], opacities[N], sh[N][K][3]); only visible Gaussians move their SH rows
+// (memory-bound kernels: ~236 B in, 80 B out per visible Gaussian). K1 also feeds the
+// backward: it appends the visible ids to a compact list that K5a walks.
 //
 // Per Gaussian (PAPER.md line refs; readings S* in DESIGN.md):
 //   Σ = R S Sᵀ Rᵀ; x_c = W μ + t; u_c, v_c pinhole; t_c = ‖x_c‖
@@ -258,20 +260,19 @@ __device__ __forceinline__ bool gaussian_forward(const DevGauss& g, int64_t i, c
 }
 
 // ---------------------------------------------------------------------------- K1
+// One Gaussian: writes its record, rect, tiles_touched and depth key; returns the rect
+// (tile x0, y0, width) and the number of tiles it touches (0: culled / off-screen).
 template <int DEG>
-__global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
-                                                         int tiles_y, Record* __restrict__ rec,
-                                                         uint2* __restrict__ rect, uint32_t* __restrict__ touched,
-                                                         uint32_t* __restrict__ dkey, uint32_t* __restrict__ didx,
-                                                         Counter* __restrict__ counters) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n) return;
-  didx[i] = (uint32_t)i;
+__device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i, const DevCam& cam,
+                                                   const DevOpt& opt, Record* __restrict__ rec,
+                                                   uint2* __restrict__ rect, uint32_t* __restrict__ touched,
+                                                   uint32_t* __restrict__ dkey, uint32_t& rx0, uint32_t& ry0,
+                                                   uint32_t& rw) {
   GF<double> f;
   if (!gaussian_project<double>(g, i, cam, opt, f)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
-    return;
+    return 0u;
   }
   // α-bounded footprint: α = o·G ≥ α_min ⇔ Δᵀ conic Δ ≤ k = 2 ln(o/α_min); its axis-aligned
   // half extents are sqrt(k·A′₀₀), sqrt(k·A′₁₁) (reading S8); inflated for fp32 safety.
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   if (!(fx0 <= fx1 && fy0 <= fy1)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
-    return;
+    return 0u;
   }
   const int T = opt.tile;
   const uint32_t tx0 = (uint32_t)fx0 / T, tx1 = (uint32_t)fx1 / T + 1;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   if (!gaussian_plane<double>(cam, f)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
-    return;
+    return 0u;
   }
 
   // colour: dir = normalize(μ − campos), degree ≤ sh_degree, + 0.5, clamp ≥ 0
@@ -326,12 +327,41 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   r.r3 = make_float4(f.zkey, (float)f.p0, (float)f.p1, 1.f / f.o);
   rec[i] = r;
   rect[i] = make_uint2(tx0 | (ty0 << 16), tx1 | (ty1 << 16));
-  touched[i] = (tx1 - tx0) * (ty1 - ty0);
+  const uint32_t nt = (tx1 - tx0) * (ty1 - ty0);
+  touched[i] = nt;
   dkey[i] = __float_as_uint(f.zkey);
-  if (counters) {  // warp-aggregated: one atomic per converged group of visible threads
-    const unsigned m = __activemask();
-    if ((int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counters + 3, (Counter)__popc(m));
+  rx0 = tx0;
+  ry0 = ty0;
+  rw = tx1 - tx0;
+  return nt;
+}
+
+// K1 kernel: per-Gaussian forward (plus the depth-sort input dkey[i], didx[i] = i), then
+// the warp-aggregated append of the visible ids to the visible list (one atomic per warp;
+// list order is arbitrary — K5a, its only user, is order-independent).
+template <int DEG>
+__global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
+                                                         Record* __restrict__ rec, uint2* __restrict__ rect,
+                                                         uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
+                                                         uint32_t* __restrict__ didx,
+                                                         uint32_t* __restrict__ n_visible,
+                                                         uint32_t* __restrict__ vis, Counter* __restrict__ counters) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(threadIdx.x & 31);
+  uint32_t x0 = 0, y0 = 0, w = 1, nt = 0;
+  if (i < g.n) {
+    didx[i] = (uint32_t)i;
+    nt = preprocess_one<DEG>(g, i, cam, opt, rec, rect, touched, dkey, x0, y0, w);
   }
+  const unsigned vmask = __ballot_sync(0xffffffffu, nt > 0u);
+  if (vmask == 0u) return;  // warp-uniform
+  uint32_t base = 0;
+  if (lane == 0) {
+    base = atomicAdd(n_visible, (uint32_t)__popc(vmask));
+    if (counters) atomicAdd(counters + 3, (Counter)__popc(vmask));
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (nt > 0u) vis[base + __popc(vmask & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
 // ---------------------------------------------------------------------------- K5
@@ -584,16 +614,15 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, 
 }
 
 // K5a (cooperative, rows of a multiple of 4 floats): each warp owns 32 VISIBLE Gaussians —
-// 32 consecutive positions of the depth order (K2a), whose prefix is exactly the visible
-// set — and moves their SH coefficient rows and SH gradient rows between HBM and shared
+// 32 consecutive entries of K1's visible list — and moves their SH coefficient rows and
+// SH gradient rows between HBM and shared
 // memory cooperatively: each warp-wide 16-B load covers ~3 whole 192-B rows (full sectors,
 // vs 32 scattered half-sectors for per-thread row loads), 2·NV4 loads per lane are in
 // flight at once, and only visible rows are touched. Lane l then works on row l (pitch
 // NV4+1 float4: conflict-free), and the updated gradient rows are stored back the same way.
 template <int DEG>
 __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCam cam, DevOpt opt,
-                                                               const uint32_t* __restrict__ order,
-                                                               const uint32_t* __restrict__ sorted_keys,
+                                                               const uint32_t* __restrict__ vis, int64_t n_vis,
                                                                const float* __restrict__ g2d, DevGrads gr) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int NV = 3 * K, NV4 = (NV + 3) / 4, P = NV4 + 1;
@@ -601,10 +630,10 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
   __shared__ float4 s_grad[2][32 * P];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = p < g.n && sorted_keys[p] != 0xffffffffu;
+  const bool valid = p < n_vis;
   const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-  if (vmask == 0) return;  // warp-uniform: the invisible tail of the depth order
-  const uint32_t id = valid ? order[p] : 0u;
+  if (vmask == 0) return;  // warp-uniform: past the end of the list
+  const uint32_t id = valid ? vis[p] : 0u;
   const int64_t L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
   float mu0 = 0.f, mu1 = 0.f, mu2 = 0.f, d_rgb[3] = {0.f, 0.f, 0.f};
   if (valid) {
@@ -687,14 +716,15 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
 
 }  // namespace
 
-void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y,
-                           Record* rec, uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx,
-                           Counter* counters, cudaStream_t s) {
+void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
+                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* n_visible,
+                           uint32_t* vis, Counter* counters, cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = 256;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
-#define RD_K1(D) \
-  k_preprocess_fwd<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, tiles_y, rec, rect, tiles_touched, dkey, didx, counters)
+#define RD_K1(D)                                                                                                 \
+  k_preprocess_fwd<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, rec, rect, tiles_touched, dkey, didx, \
+                                                 n_visible, vis, counters)
   switch (opt.sh_degree) {
     case 0: RD_K1(0); break;
     case 1: RD_K1(1); break;
@@ -705,14 +735,14 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 }
 
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
-                           const uint32_t* order, const uint32_t* sorted_keys, const float* g2d, DevGrads grads,
-                           cudaStream_t s) {
+                           const uint32_t* vis, int64_t n_vis, const float* g2d, DevGrads grads, cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = 128;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
   if ((g.sh_coeffs * 3) % 4 == 0) {
-    const unsigned cblocks = (unsigned)((g.n + 63) / 64);
-#define RD_K5A(D) k_preprocess_bwd_sh_coop<D><<<cblocks, 64, 0, s>>>(g, cam, opt, order, sorted_keys, g2d, grads)
+    const unsigned cblocks = (unsigned)((n_vis + 63) / 64);
+#define RD_K5A(D) \
+  if (cblocks) k_preprocess_bwd_sh_coop<D><<<cblocks, 64, 0, s>>>(g, cam, opt, vis, n_vis, g2d, grads)
     switch (opt.sh_degree) {
       case 0: RD_K5A(0); break;
       case 1: RD_K5A(1); break;

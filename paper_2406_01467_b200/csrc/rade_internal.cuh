@@ -130,15 +130,14 @@ __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
 }
 
 // K1 also writes the depth-sort input: dkey[i] = float_bits(z_c) (0xFFFFFFFF if the
-// Gaussian touches no tile) and didx[i] = i.
-void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y,
-                           Record* rec, uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx,
-                           Counter* counters, cudaStream_t s);
-// K5 = K5a (SH; walks the depth order of K2a: order = sorted ids, sorted_keys = their keys,
-// 0xFFFFFFFF marking the invisible tail) then K5b (geometry, id order).
+// Gaussian touches no tile) and didx[i] = i, and appends the visible ids to vis
+// (*n_visible, zeroed beforehand).
+void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
+                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* n_visible,
+                           uint32_t* vis, Counter* counters, cudaStream_t s);
+// K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry, id order).
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
-                           const uint32_t* order, const uint32_t* sorted_keys, const float* g2d, DevGrads grads,
-                           cudaStream_t s);
+                           const uint32_t* vis, int64_t n_vis, const float* g2d, DevGrads grads, cudaStream_t s);
 // K2 (binning.cu). Sorts return the CUB DoubleBuffer selector (1: result in the *1 buffers).
 size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits);
 int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t* idx1, int64_t n, void* temp,
