@@ -1,8 +1,9 @@
 // render.cu — stage 3 (K3, blend forward) and the first half of stage 4 (K4, blend
 // backward) of the RaDe-GS rasterizer, sm_100a.
 //
-// One CTA per TILE×TILE tile, TILE²/2 threads, each owning two pixels (rows r and
-// r + TILE/2 of the tile; pixels sampled at (i+½, j+½), reading S4). Each CTA walks its
+// One CTA per TILE×TILE tile, TILE²/2 threads, each owning two pixels; each warp owns a
+// compact band of rows (16×4 pixels at TILE 16), which keeps its ballot-based skipping
+// tight (pixels sampled at (i+½, j+½), reading S4). Each CTA walks its
 // tile's depth-sorted list (ranges from K2) in batches of TILE² splats staged in shared
 // memory (two coalesced 64-B record gathers per thread); every shared-memory broadcast,
 // loop step and — in K4 — every warp reduction then serves two pixels. The block leaves
@@ -112,8 +113,12 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   constexpr int BATCH = TILE * TILE;   // splats staged per round
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int lx = (int)(threadIdx.x % TILE), ly = (int)(threadIdx.x / TILE);
-  const int px = tx * TILE + lx, pyA = ty * TILE + ly, pyB = pyA + TILE / 2;
+  // warp w owns the compact 2W-row band [2W·w, 2W·w + 2W) of the tile (W = 32 / TILE lane
+  // rows): lane row r holds pixel rows 2W·w + r (A) and + W (B)
+  constexpr int W = 32 / TILE;
+  const int lane_ = (int)(threadIdx.x & 31), warp_ = (int)(threadIdx.x >> 5);
+  const int lx = lane_ % TILE, ly = 2 * W * warp_ + lane_ / TILE;
+  const int px = tx * TILE + lx, pyA = ty * TILE + ly, pyB = pyA + W;
   const bool inA = px < cam.W && pyA < cam.H, inB = px < cam.W && pyB < cam.H;
   const uint2 range = ranges[tile];
   const int total = (int)(range.y - range.x);
@@ -215,85 +220,112 @@ __device__ __forceinline__ void pixb_init(PixB& s, float px, float py, bool insi
   s.Dsuf = 0.f;
 }
 
-// One (pixel, splat) step of K4; adds this pixel's contribution to g[0..14]. With the
-// per-pixel scalar D_i = Σ_{j>i} w_j (c_j·g_C + n_j·g_N) (suffix sum, w_j = α_j T_j) the
-// α gradient of Eq.3's colour and of the normal map is
-//   ∂L/∂α_i = T_i (c_i·g_C + n_i·g_N) − D_i / (1 − α_i) + T_final/(1 − α_i) (g_A − bg·g_C)
-// (the 3DGS derivation collapsed to one scalar, since g_C, g_N are per-pixel constants).
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
+// One (pixel, splat) step of K4: adds this pixel's contribution to the 12 per-splat sums
+//   g0 = Σ dA·dx, g1 = Σ dA·dy, g2 = Σ dA·dx², g3 = Σ dA·dx·dy, g4 = Σ dA·dy², g5 = Σ dA,
+//   g6..8 = Σ w·g_C, g9..11 = Σ w·g_N        (dA = α_raw·∂L/∂α)
+// from which the 2-D gradients follow per splat after the warp reduction (k_render_bwd).
+// With the per-pixel scalar D_i = Σ_{j>i} w_j (c_j·g_C + n_j·g_N) (suffix sum, w_j = α_j T_j)
+// the α gradient of Eq.3's colour and of the normal map is
+//   ∂L/∂α_i = T_i (c_i·g_C + n_i·g_N) − D_i / (1 − α_i) + T_final/(1 − α_i) (g_A − bg·g_C)
+// (the 3DGS derivation collapsed to one scalar, since g_C, g_N are per-pixel constants).
 // Branch-free: an inactive pair (past the pixel's list, or α < α_min) contributes exact
-// zeros (α masked to 0 ⇒ rinv = 1, w = 0, dL/dα = 0), so the warp runs one straight-line
-// sequence instead of divergent paths. FIRST writes g[0..11], otherwise adds.
-template <bool FIRST>
-__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[16], const PairAlpha& pa, bool act, const float4& a0,
-                                          const float4& a1, const float4& a2, float inv_o, const DevOpt& opt) {
+// zeros (α masked to 0 ⇒ rinv = rcp(1) = 1, w = 0, dA = 0).
+__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[16], const PairAlpha& pa, bool act, const float4& a1,
+                                          const float4& a2, const DevOpt& opt) {
   const float a_raw = ex2_approx(pa.e);                  // o·exp(−½ΔᵀCΔ)
   const float al = act ? fminf(opt.alpha_max, a_raw) : 0.f;
-  const float rinv = act ? rcp_approx(1.f - al) : 1.f;   // α ≤ α_max < 1
+  const float rinv = rcp_approx(1.f - al);               // α ≤ α_max < 1; exact 1 when masked
   s.T = s.T * rinv;                                      // T_i = T_{i+1} / (1 − α_i)
   const float w = al * s.T;
   const float dot = a1.z * s.gC0 + a1.w * s.gC1 + a2.x * s.gC2 + a2.y * s.gN0 + a2.z * s.gN1 + a2.w * s.gN2;
   const float dL_dal = act && a_raw <= opt.alpha_max ? s.T * dot - rinv * (s.Dsuf - s.TFa) : 0.f;  // clamp (S8)
   s.Dsuf = fmaf(w, dot, s.Dsuf);
-  const float dA = a_raw * dL_dal;                       // α_raw·∂L/∂α
-  const float dpw = dA * kLn2;                           // dL/d(power in log2 units)
-  const float hx = dpw * pa.dx, hy = dpw * pa.dy;
-  const float v[12] = {2.f * a0.z * hx + a0.w * hy, a0.w * hx + 2.f * a1.x * hy, hx * pa.dx, hx * pa.dy,
-                       hy * pa.dy, dA * inv_o,           // ∂α/∂o = α_raw/o
-                       w * s.gC0, w * s.gC1, w * s.gC2, w * s.gN0, w * s.gN1, w * s.gN2};
-#pragma unroll
-  for (int k = 0; k < 12; ++k) g[k] = FIRST ? v[k] : g[k] + v[k];
+  const float dA = a_raw * dL_dal;
+  const float hx = dA * pa.dx, hy = dA * pa.dy;
+  g[0] += hx;
+  g[1] += hy;
+  g[2] = fmaf(hx, pa.dx, g[2]);
+  g[3] = fmaf(hx, pa.dy, g[3]);
+  g[4] = fmaf(hy, pa.dy, g[4]);
+  g[5] += dA;
+  g[6] = fmaf(w, s.gC0, g[6]);
+  g[7] = fmaf(w, s.gC1, g[7]);
+  g[8] = fmaf(w, s.gC2, g[8]);
+  g[9] = fmaf(w, s.gN0, g[9]);
+  g[10] = fmaf(w, s.gN1, g[10]);
+  g[11] = fmaf(w, s.gN2, g[11]);
 }
 
-// Median-depth terms D = z_c + p·Δ (Eq.4), at the pixel's median splat only.
-__device__ __forceinline__ void bwd_median(const PixB& s, float (&g)[16], const PairAlpha& pa, const float4& p) {
-  g[0] += s.gD * p.y;
-  g[1] += s.gD * p.z;
+// Median-depth sums g12 = Σ g_D, g13 = Σ g_D·dx, g14 = Σ g_D·dy for D = z_c + p·Δ (Eq.4,
+// PAPER:443-450), at the pixel's median splat only.
+__device__ __forceinline__ void bwd_median(const PixB& s, float (&g)[16], const PairAlpha& pa) {
   g[12] += s.gD;
-  g[13] += s.gD * pa.dx;
-  g[14] += s.gD * pa.dy;
+  g[13] = fmaf(s.gD, pa.dx, g[13]);
+  g[14] = fmaf(s.gD, pa.dy, g[14]);
 }
 
-template <int TILE>
-__global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
+// The 2-D gradient slot k (rade_internal.cuh order) of one splat from the reduced sums S:
+//   du = ln2(2A2·S0 + B2·S1) + p0·S12, dv = ln2(B2·S0 + 2C2·S1) + p1·S12 (e = A2dx² + B2dxdy
+//   + C2dy² + log2 o in log2 units, D = z_c + p·Δ), dA2 = ln2·S2, dB2 = ln2·S3, dC2 = ln2·S4,
+//   do = S5/o (∂α_raw/∂o = α_raw/o), the rest as summed.
+__device__ __forceinline__ float g2d_slot(int k, float sk, float s0, float s1, float s12, const float4& a0,
+                                          const float4& a1, const float4& a3) {
+  if (k == 0) return kLn2 * (2.f * a0.z * s0 + a0.w * s1) + a3.y * s12;
+  if (k == 1) return kLn2 * (a0.w * s0 + 2.f * a1.x * s1) + a3.z * s12;
+  if (k >= 2 && k <= 4) return kLn2 * sk;
+  if (k == 5) return sk * a3.w;
+  return sk;
+}
+
+// K4: one CTA per tile, TILE²/PPT threads, PPT pixels per thread. Warp w owns the compact
+// band of LR·PPT rows starting at LR·PPT·w (LR = 32/TILE lane rows); lane row r holds pixel
+// rows band + r + LR·k, k < PPT. Per splat the warp evaluates α for its pixels, skips the
+// splat if none uses it (ballot), otherwise accumulates the 15 sums over the thread's PPT
+// pixels, reduces them across the warp and issues one L2 atomic per value.
+template <int TILE, int PPT>
+__global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
     const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
     const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, float* __restrict__ g2d,
     Counter* __restrict__ counters) {
-  constexpr int NT = TILE * TILE / 2;
+  constexpr int NT = TILE * TILE / PPT;
   constexpr int BATCH = TILE * TILE;
+  constexpr int LR = 32 / TILE;
+  static_assert(NT % 32 == 0, "whole warps");
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int lx = (int)(threadIdx.x % TILE), ly = (int)(threadIdx.x / TILE);
-  const int px = tx * TILE + lx, pyA = ty * TILE + ly, pyB = pyA + TILE / 2;
-  const bool inA = px < cam.W && pyA < cam.H, inB = px < cam.W && pyB < cam.H;
+  const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+  const int px = tx * TILE + lane % TILE;
+  const int py0 = ty * TILE + LR * PPT * warp + lane / TILE;
   const uint2 range = ranges[tile];
   const int HW = cam.W * cam.H;
-  const int lane = (int)(threadIdx.x & 31);
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch; r3 = (z_c, p0, p1, 1/o)
   __shared__ uint32_t sid[BATCH];
   __shared__ int s_maxlast;
-  float4* s0 = sbuf[0];
-  float4* s1 = sbuf[1];
-  float4* s2 = sbuf[2];
-  float4* s3 = sbuf[3];
 
-  PixB A, B;
-  pixb_init(A, (float)px + 0.5f, (float)pyA + 0.5f, inA, pyA * cam.W + px, HW, opt, T_final, n_contrib, median_pos,
-            dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha);
-  pixb_init(B, (float)px + 0.5f, (float)pyB + 0.5f, inB, pyB * cam.W + px, HW, opt, T_final, n_contrib, median_pos,
-            dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha);
-  if (counters) warp_count(counters + 2, (unsigned)(A.last + B.last));
+  PixB s[PPT];
+  int mylast = 0;
+  unsigned evals = 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int py = py0 + LR * k;
+    const bool in = px < cam.W && py < cam.H;
+    pixb_init(s[k], (float)px + 0.5f, (float)py + 0.5f, in, py * cam.W + px, HW, opt, T_final, n_contrib, median_pos,
+              dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha);
+    mylast = max(mylast, s[k].last);
+    evals += (unsigned)s[k].last;
+  }
+  if (counters) warp_count(counters + 2, evals);
   if (threadIdx.x == 0) s_maxlast = 0;
   __syncthreads();
-  const int mylast = max(A.last, B.last);
   if (mylast > 0) atomicMax(&s_maxlast, mylast);
   __syncthreads();
   const int maxlast = s_maxlast;
@@ -303,50 +335,58 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_bwd(
     const int cnt = end - start;
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < BATCH / NT; ++h) {
       const int t = (int)threadIdx.x + h * NT;
       if (t < cnt) {
         const uint32_t id = ids[range.x + start + t];
         const Record* r = rec + id;
         sid[t] = id;
-        s0[t] = r->r0;
-        s1[t] = r->r1;
-        s2[t] = r->r2;
-        s3[t] = r->r3;
+        sbuf[0][t] = r->r0;
+        sbuf[1][t] = r->r1;
+        sbuf[2][t] = r->r2;
+        sbuf[3][t] = r->r3;
       }
     }
     __syncthreads();
-    const unsigned a_s0 = smem_addr(s0), a_id = smem_addr(sid);
+    const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid);
     for (int j = cnt - 1; j >= 0; --j) {
       const int pos = start + j;
       if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
-      const PairAlpha pA = pair_power(a0, a1.x, a1.y, A.px, A.py, opt.log2_alpha_min);
-      const PairAlpha pB = pair_power(a0, a1.x, a1.y, B.px, B.py, opt.log2_alpha_min);
-      const bool actA = pos < A.last && pA.pass;
-      const bool actB = pos < B.last && pB.pass;
-      const bool active = actA || actB;
-      const unsigned act = __ballot_sync(0xffffffffu, active);
-      if (act) {  // warp-uniform: the splat contributes to some pixel of this warp
-        const float4 a2 = lds128(a + 32u * BATCH), a3 = lds128(a + 48u * BATCH);
-        float g[16];
-        bwd_accum<true>(A, g, pA, actA, a0, a1, a2, a3.w, opt);
-        bwd_accum<false>(B, g, pB, actB, a0, a1, a2, a3.w, opt);
-        g[12] = g[13] = g[14] = g[15] = 0.f;
-        if (actA && pos == A.med) bwd_median(A, g, pA, a3);
-        if (actB && pos == B.med) bwd_median(B, g, pB, a3);
-        float* dst = g2d + (size_t)lds32(a_id + 4u * j) * kG2D;
-        if (__popc(act) == 1) {  // one contributing thread in this warp: no reduction needed
-          if (active) {
+      PairAlpha pa[PPT];
+      bool act[PPT];
+      bool any = false;
 #pragma unroll
-            for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g[k]);
-          }
-        } else {
-          const float v = reduce_scatter16(g, lane);
-          const int k = lane >> 1;
-          if ((lane & 1) == 0 && k < 15) atomicAdd(dst + k, v);
+      for (int k = 0; k < PPT; ++k) {
+        pa[k] = pair_power(a0, a1.x, a1.y, s[k].px, s[k].py, opt.log2_alpha_min);
+        act[k] = pos < s[k].last && pa[k].pass;
+        any = any || act[k];
+      }
+      const unsigned am = __ballot_sync(0xffffffffu, any);
+      if (am == 0u) continue;  // warp-uniform: no pixel of this warp uses the splat
+      const float4 a2 = lds128(a + 32u * BATCH), a3 = lds128(a + 48u * BATCH);
+      float g[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) g[k] = 0.f;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) bwd_accum(s[k], g, pa[k], act[k], a1, a2, opt);
+#pragma unroll
+      for (int k = 0; k < PPT; ++k)
+        if (act[k] && pos == s[k].med) bwd_median(s[k], g, pa[k]);
+      float* dst = g2d + (size_t)lds32(a_id + 4u * j) * kG2D;
+      if (__popc(am) == 1) {  // one contributing thread in this warp: no reduction needed
+        if (any) {
+#pragma unroll
+          for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g2d_slot(k, g[k], g[0], g[1], g[12], a0, a1, a3));
         }
+      } else {
+        const float v = reduce_scatter16(g, lane);
+        const float s0 = __shfl_sync(0xffffffffu, v, 0);
+        const float s1 = __shfl_sync(0xffffffffu, v, 2);
+        const float s12 = __shfl_sync(0xffffffffu, v, 24);
+        const int k = lane >> 1;
+        if ((lane & 1) == 0 && k < 15) atomicAdd(dst + k, g2d_slot(k, v, s0, s1, s12, a0, a1, a3));
       }
     }
   }
@@ -376,11 +416,11 @@ void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
                        cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
   if (opt.tile == 16)
-    k_render_bwd<16><<<grid, 128, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
-                                          dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
+    k_render_bwd<16, 4><<<grid, 64, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
+                                            dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
   else
-    k_render_bwd<8><<<grid, 32, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
-                                        dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
+    k_render_bwd<8, 2><<<grid, 32, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
+                                           dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
 }
 
 }  // namespace rade
