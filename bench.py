@@ -266,30 +266,61 @@ def run_gpu(args, cfg_name, config):
     cots = [torch.randn((8, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
     opts = dict(tile=opt.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
                 median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
-    view = P.View(device)
-    outs = {"color": torch.empty((3, H, W), device=device), "depth": torch.empty((H, W), device=device),
-            "normal": torch.empty((3, H, W), device=device), "alpha": torch.empty((H, W), device=device)}
+    # Views are pipelined over `args.pipeline` CUDA streams, each with its own rd_view and
+    # output maps: view v+1's preprocess/binning/forward overlap view v's backward. The
+    # gradient accumulation (K5's read-modify-write of the shared gradient rows) stays in
+    # view order: each rd_render_bwd waits for the previous view's (event chain).
+    P_ = max(1, args.pipeline)
+    slots = []
+    for _ in range(P_):
+        st = torch.cuda.Stream(device)
+        with torch.cuda.stream(st):  # the view's scratch is allocated on its own stream
+            slot = {"stream": st, "view": P.View(device),
+                    "outs": {"color": torch.empty((3, H, W), device=device),
+                             "depth": torch.empty((H, W), device=device),
+                             "normal": torch.empty((3, H, W), device=device),
+                             "alpha": torch.empty((H, W), device=device)},
+                    "done": torch.cuda.Event()}
+        slots.append(slot)
+    view = slots[0]["view"]
+    outs = slots[0]["outs"]
     counter = {"v": 0}
+    main_stream = torch.cuda.current_stream(device)
 
-    def one_view(cam, cot):
-        P.rd_preprocess(view, g, cam, opts)
-        P.rd_bin(view)
-        P.rd_render_fwd(view, outs["color"], outs["depth"], outs["normal"], outs["alpha"])
-        P.rd_render_bwd(view, g, cot[0:3], cot[3], cot[4:7], cot[7], grads)
+    def one_view(slot, cam, cot, after):
+        st, vw, o = slot["stream"], slot["view"], slot["outs"]
+        with torch.cuda.stream(st):
+            P.rd_preprocess(vw, g, cam, opts, stream=st)
+            P.rd_bin(vw, stream=st)
+            P.rd_render_fwd(vw, o["color"], o["depth"], o["normal"], o["alpha"], stream=st)
+            st.wait_event(after)  # gradient rows: the previous view's K5 first
+            P.rd_render_bwd(vw, g, cot[0:3], cot[3], cot[4:7], cot[7], grads, stream=st)
+            slot["done"].record(st)
+        return slot["done"]
 
-    def step():
+    def run_views(per_view):
+        """Zero the gradients, run B views through the slots, join, all-reduce."""
         fg.zero_()
+        start = torch.cuda.Event()
+        start.record(main_stream)
+        for sl in slots:
+            sl["stream"].wait_event(start)
+        prev = start
         for b in range(B):
             k = counter["v"]
             counter["v"] += 1
-            one_view(my_views[k % len(my_views)], cots[k % n_ring])
+            prev = per_view(slots[k % P_], k, prev)
+        for sl in slots:
+            main_stream.wait_event(sl["done"])
         fg.allreduce()  # NCCL sum over ranks (no-op at N = 1)
 
-    # ---------------- device-resident timed region
+    def step():
+        run_views(lambda sl, k, prev: one_view(sl, my_views[k % len(my_views)], cots[k % n_ring], prev))
+
+    # ---------------- device-resident timed region (no per-kernel events: pipelined streams)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    P.rd_set_profiling(view, True)
     clocks = ClockSampler(local)
     barrier(dist_on)
     torch.cuda.synchronize()
@@ -303,33 +334,51 @@ def run_gpu(args, cfg_name, config):
     barrier(dist_on)
     clk = clocks.stop()
     elapsed_ms = max_over_ranks(e0.elapsed_time(e1), dist_on, device)
-    tim = P.rd_get_timings(view, reset=True)
-    P.rd_set_profiling(view, False)
     total_views = args.steps * B * ws
     value = total_views / (elapsed_ms / 1e3)
+
+    # ---------------- per-kernel timings: the same steps again, serialised on one stream with
+    # the ABI's CUDA-event hooks around every kernel (rd_set_profiling)
+    slots_all = slots
+    slots = slots_all[:1]
+    P_ = 1
+    P.rd_set_profiling(view, True)
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    tim = P.rd_get_timings(view, reset=True)
+    P.rd_set_profiling(view, False)
+    slots = slots_all
+    P_ = len(slots_all)
 
     # ---------------- end-to-end: host cotangents in (pinned), rendered maps out, per step
     e2e = None
     if not args.no_e2e:
         host_cots = [c.cpu().pin_memory() for c in cots]
-        host_out = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in outs.items()}
-        dev_cot = torch.empty((8, H, W), device=device)
         h2d = 0
         d2h = 0
 
-        def step_e2e():
+        host_outs = [{k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in outs.items()}
+                     for _ in slots]
+        dev_cots = [torch.empty((8, H, W), device=device) for _ in slots]
+
+        def per_view_e2e(sl, k, prev):
             nonlocal h2d, d2h
-            fg.zero_()
-            for b in range(B):
-                k = counter["v"]
-                counter["v"] += 1
-                dev_cot.copy_(host_cots[k % n_ring], non_blocking=True)
-                h2d += dev_cot.numel() * 4
-                one_view(my_views[k % len(my_views)], dev_cot)
-                for key, t in outs.items():
-                    host_out[key].copy_(t, non_blocking=True)
+            i = slots.index(sl)
+            with torch.cuda.stream(sl["stream"]):
+                dev_cots[i].copy_(host_cots[k % n_ring], non_blocking=True)
+            h2d += dev_cots[i].numel() * 4
+            done = one_view(sl, my_views[k % len(my_views)], dev_cots[i], prev)
+            with torch.cuda.stream(sl["stream"]):
+                for key, t in sl["outs"].items():
+                    host_outs[i][key].copy_(t, non_blocking=True)
                     d2h += t.numel() * 4
-            fg.allreduce()
+                sl["done"].record(sl["stream"])
+            return sl["done"]
+
+        def step_e2e():
+            run_views(per_view_e2e)
 
         steps_e2e = max(1, args.steps // 2)
         step_e2e()
@@ -389,8 +438,8 @@ def run_gpu(args, cfg_name, config):
 
     # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so):
     # K1, depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan),
-    # duplicate, tile sort (histogram + exclusive-sum + passes), ranges, K3, K4, K5
-    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 1
+    # duplicate, tile sort (histogram + exclusive-sum + passes), ranges, K3, K4, K5a + K5b
+    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 2
     views_per_rank = args.steps * B
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)
@@ -417,7 +466,8 @@ def run_gpu(args, cfg_name, config):
         line["cpu_baseline"] = {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    view.close()
+    for sl in slots:
+        sl["view"].close()
     if dist_on:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -437,6 +487,7 @@ def main():
     ap.add_argument("--ref-grads", type=int, default=2, help="oracle arm: Gaussians differentiated per step")
     ap.add_argument("--cpu-pixels", type=int, default=2048, help="cpu_baseline: forward pixels sampled")
     ap.add_argument("--cpu-grads", type=int, default=64, help="cpu_baseline: Gaussians differentiated")
+    ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the views are pipelined over")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -1,0 +1,119 @@
+// Stand-alone timing of the binning sorts' CUB onesweep policies on the C3 sizes
+// (N = 1.5M 32-bit depth keys; M = 5.6M 12-bit tile keys; 32-bit values).
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a tools/sort_bench.cu -o /tmp/sort_bench
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/dispatch/dispatch_radix_sort.cuh>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+template <int THREADS, int ITEMS>
+struct Hub {
+  using Base = cub::detail::radix::policy_hub<uint32_t, uint32_t, uint32_t>;
+  struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, Policy1000> {
+    using B = typename Base::Policy1000;
+    static constexpr bool ONESWEEP = true;
+    static constexpr int ONESWEEP_RADIX_BITS = 8;
+    using HistogramPolicy = typename B::HistogramPolicy;
+    using ExclusiveSumPolicy = typename B::ExclusiveSumPolicy;
+    using OnesweepPolicy =
+        cub::AgentRadixSortOnesweepPolicy<THREADS, ITEMS, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
+                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+    using ScanPolicy = typename B::ScanPolicy;
+    using DownsweepPolicy = typename B::DownsweepPolicy;
+    using AltDownsweepPolicy = typename B::AltDownsweepPolicy;
+    using UpsweepPolicy = typename B::UpsweepPolicy;
+    using AltUpsweepPolicy = typename B::AltUpsweepPolicy;
+    using SingleTilePolicy = typename B::SingleTilePolicy;
+    using SegmentedPolicy = typename B::SegmentedPolicy;
+    using AltSegmentedPolicy = typename B::AltSegmentedPolicy;
+  };
+  using MaxPolicy = Policy1000;
+};
+
+template <typename H>
+float run(uint32_t* k0, uint32_t* k1, uint32_t* v0, uint32_t* v1, const uint32_t* kin, const uint32_t* vin, uint32_t n,
+          int bits, void* tmp, size_t tb, int reps) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9f;
+  for (int r = 0; r < reps; ++r) {
+    cudaMemcpy(k0, kin, n * 4, cudaMemcpyDeviceToDevice);
+    cudaMemcpy(v0, vin, n * 4, cudaMemcpyDeviceToDevice);
+    cub::DoubleBuffer<uint32_t> K(k0, k1), V(v0, v1);
+    cudaEventRecord(a);
+    cub::DispatchRadixSort<false, uint32_t, uint32_t, uint32_t, H>::Dispatch(tmp, tb, K, V, n, 0, bits, true, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+template <int T, int I>
+void one(const char* name, uint32_t* k0, uint32_t* k1, uint32_t* v0, uint32_t* v1, const uint32_t* kin,
+         const uint32_t* vin, uint32_t n, int bits) {
+  size_t tb = 0;
+  cub::DoubleBuffer<uint32_t> K(k0, k1), V(v0, v1);
+  cub::DispatchRadixSort<false, uint32_t, uint32_t, uint32_t, Hub<T, I>>::Dispatch(nullptr, tb, K, V, n, 0, bits, true,
+                                                                                 0);
+  void* tmp;
+  cudaMalloc(&tmp, tb);
+  float ms = run<Hub<T, I>>(k0, k1, v0, v1, kin, vin, n, bits, tmp, tb, 20);
+  printf("%-10s n=%u bits=%d  %d x %d : %.1f us\n", name, n, bits, T, I, ms * 1e3);
+  cudaFree(tmp);
+}
+
+int main() {
+  const uint32_t N = 1500000, M = 5600000;
+  std::vector<uint32_t> hk(M), hv(M), ht(M);
+  srand(1);
+  for (uint32_t i = 0; i < M; ++i) {
+    float z = 0.5f + 50.f * (float)rand() / RAND_MAX;
+    uint32_t b;
+    memcpy(&b, &z, 4);
+    hk[i] = (i % 2 == 0 && i < N) ? 0xffffffffu : b;  // half of the depth keys culled
+    hv[i] = i;
+    ht[i] = rand() % 4056;
+  }
+  uint32_t *kin, *vin, *tin, *k0, *k1, *v0, *v1;
+  cudaMalloc(&kin, M * 4); cudaMalloc(&vin, M * 4); cudaMalloc(&tin, M * 4);
+  cudaMalloc(&k0, M * 4); cudaMalloc(&k1, M * 4); cudaMalloc(&v0, M * 4); cudaMalloc(&v1, M * 4);
+  cudaMemcpy(kin, hk.data(), M * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(vin, hv.data(), M * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(tin, ht.data(), M * 4, cudaMemcpyHostToDevice);
+  {  // CUB default
+    for (int which = 0; which < 3; ++which) {
+      const uint32_t n = which == 0 ? N : which == 1 ? N / 2 : M;
+      const int bits = which == 2 ? 12 : 32;
+      const uint32_t* ki = which == 2 ? tin : kin;
+      size_t tb = 0;
+      cub::DoubleBuffer<uint32_t> K(k0, k1), V(v0, v1);
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, K, V, (int)n, 0, bits);
+      void* tmp;
+      cudaMalloc(&tmp, tb);
+      float ms = run<cub::detail::radix::policy_hub<uint32_t, uint32_t, uint32_t>>(k0, k1, v0, v1, ki, vin, n, bits,
+                                                                                    tmp, tb, 20);
+      printf("default    n=%u bits=%d : %.1f us\n", n, bits, ms * 1e3);
+      cudaFree(tmp);
+    }
+  }
+#define CFG(T, I)                                          \
+  one<T, I>("depth", k0, k1, v0, v1, kin, vin, N, 32);      \
+  one<T, I>("depth/2", k0, k1, v0, v1, kin, vin, N / 2, 32); \
+  one<T, I>("tile", k0, k1, v0, v1, tin, vin, M, 12);
+  CFG(384, 23)
+  CFG(256, 16)
+  CFG(256, 12)
+  CFG(256, 8)
+  CFG(512, 8)
+  CFG(512, 12)
+  CFG(128, 16)
+  CFG(384, 12)
+  printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
