@@ -264,12 +264,12 @@ def run_gpu(args, cfg_name, config):
     gen = torch.Generator(device=device)
     gen.manual_seed(SEED_COT + rank)
     cots = [torch.randn((8, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
-    opts = dict(tile=opt.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
+    opts = dict(tile=args.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
                 median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
     # Views are pipelined over `args.pipeline` CUDA streams, each with its own rd_view and
-    # output maps: view v+1's preprocess/binning/forward overlap view v's backward. The
-    # gradient accumulation (K5's read-modify-write of the shared gradient rows) stays in
-    # view order: each rd_render_bwd waits for the previous view's (event chain).
+    # output maps: view v+1's preprocess/binning/blending overlap view v's. The gradient
+    # accumulation (K5's read-modify-write of the shared gradient rows, rd_preprocess_bwd)
+    # stays in view order: each waits for the previous view's (event chain).
     P_ = max(1, args.pipeline)
     slots = []
     for _ in range(P_):
@@ -293,8 +293,9 @@ def run_gpu(args, cfg_name, config):
             P.rd_preprocess(vw, g, cam, opts, stream=st)
             P.rd_bin(vw, stream=st)
             P.rd_render_fwd(vw, o["color"], o["depth"], o["normal"], o["alpha"], stream=st)
+            P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)  # K4: view-private output
             st.wait_event(after)  # gradient rows: the previous view's K5 first
-            P.rd_render_bwd(vw, g, cot[0:3], cot[3], cot[4:7], cot[7], grads, stream=st)
+            P.rd_preprocess_bwd(vw, g, grads, stream=st)
             slot["done"].record(st)
         return slot["done"]
 
@@ -438,8 +439,8 @@ def run_gpu(args, cfg_name, config):
 
     # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so):
     # K1, depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan),
-    # duplicate, tile sort (histogram + exclusive-sum + passes), ranges, K3, K4, K5a + K5b
-    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 2
+    # duplicate, tile sort (histogram + exclusive-sum + passes), ranges, K3, K4, K5a + K5b + K5b64
+    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 3
     views_per_rank = args.steps * B
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)
@@ -487,6 +488,7 @@ def main():
     ap.add_argument("--ref-grads", type=int, default=2, help="oracle arm: Gaussians differentiated per step")
     ap.add_argument("--cpu-pixels", type=int, default=2048, help="cpu_baseline: forward pixels sampled")
     ap.add_argument("--cpu-grads", type=int, default=64, help="cpu_baseline: Gaussians differentiated")
+    ap.add_argument("--tile", type=int, default=8, choices=[8, 16], help="blend tile edge (outputs are tile-size independent)")
     ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the views are pipelined over")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -496,7 +498,7 @@ def main():
     import scenegen as sg
     info = sg.CONFIGS[args.config]
     config = {"workload": f"{args.config}: {info['name']}", "width": info["width"], "height": info["height"],
-              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": 16,
+              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": args.tile,
               "scene_recipe": "scenegen (DESIGN.md §Input recipe), seed 0 + config index"}
     if args.impl == "reference":
         return run_reference(args, args.config, config)

@@ -17,6 +17,7 @@
  *                  radix sort, per-tile ranges
  *   rd_render_fwd  stage 3 (K3): per-tile front-to-back blend of C, A, N, median D
  *   rd_render_bwd  stage 4 (K4, K5): reverse replay per pixel, per-Gaussian chain rule
+ *                  (also as its two halves rd_blend_bwd (K4) and rd_preprocess_bwd (K5))
  *
  * Conventions:
  *   - Camera: world->camera rotation R (row-major) and translation t; +z forward, +y down;
@@ -118,7 +119,7 @@ typedef struct rd_stats {
   int64_t n_duplicates; /* M: (Gaussian, tile) pairs after rd_bin */
   int32_t tiles_x, tiles_y;
   int32_t width, height;
-  int32_t stage;        /* 0 created, 1 preprocessed, 2 binned, 3 rendered */
+  int32_t stage;        /* 0 created, 1 preprocessed, 2 binned, 3 rendered, 4 blend-backward done */
   int32_t key_bits;     /* radix-sort bits: 32 + ceil(log2(tiles)) */
 } rd_stats;
 
@@ -172,9 +173,23 @@ rd_status rd_render_fwd(rd_view* view, float* color, float* depth, float* normal
 
 /* Stage 4 (K4 + K5). Cotangents dL/d(color, depth, normal, alpha) in the output layouts
  * (any may be NULL = zero). `g` must be the same Gaussians given to rd_preprocess.
- * Gradients are accumulated into `grads` (all five pointers required). */
+ * Gradients are accumulated into `grads` (all five pointers required).
+ * = rd_blend_bwd followed by rd_preprocess_bwd on the same stream. */
 rd_status rd_render_bwd(rd_view* view, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
                         const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream);
+
+/* Stage 4, first half (K4): the reverse per-pixel replay of Eq.3/Eq.4 into
+ * the view's per-Gaussian 2-D gradients (see rd_debug_grads2d); touches no user gradient.
+ * Cotangents as in rd_render_bwd. Requires rd_render_fwd on this view. */
+rd_status rd_blend_bwd(rd_view* view, const float* dL_dcolor, const float* dL_ddepth, const float* dL_dnormal,
+                       const float* dL_dalpha, rd_stream stream);
+
+/* Stage 4, second half (K5): the per-Gaussian chain rule from the 2-D gradients of the last
+ * rd_blend_bwd to means, scales, rotations, opacities and SH, ACCUMULATED (+=, plain
+ * read-modify-write of each visible Gaussian's rows) into `grads`. Two calls that target
+ * the same `grads` must not run concurrently (order them on one stream or with events);
+ * rd_blend_bwd of another view may overlap this call. */
+rd_status rd_preprocess_bwd(rd_view* view, const rd_gaussians* g, const rd_grads* grads, rd_stream stream);
 
 /* Profiling: when enabled, every kernel launch of this view is bracketed by CUDA events on
  * its stream and K3/K4 count the pairs they evaluate (a few atomics per warp). Enabling
@@ -188,13 +203,18 @@ rd_status rd_view_stats(const rd_view* view, rd_stats* out);
 
 /* Debug copies (device → caller device buffers, async on `stream`), for bit-exact tests:
  *  rd_debug_binning: keys u64[M], ids u32[M] (sorted), ranges u32[2*T] ([first, last)).
- *  rd_debug_preprocess: records f32[n][16] (u, v, A2, B2, C2, log2 o, r, g, b, nx, ny, nz,
- *    z_c, p0, p1, 1/o) with (A2, B2, C2) = log2(e)·(−a/2, −b, −c/2) for the conic [[a,b],[b,c]]
- *    of the dilated 2-D covariance; rects u32[n][2] (x0 | y0 << 16, x1 | y1 << 16; tiles,
+ *  rd_debug_preprocess: records f32[n][16] (u_hi, v_hi, g11, g21, g22, log2 o, r, g, b, nx,
+ *    ny, nz, z_c, p0, p1, uv_lo) with [[g11, g21], [0, g22]] the Cholesky factor U of
+ *    (log2 e / 2)·[[a,b],[b,c]] (UᵀU), [[a,b],[b,c]] the conic of the dilated 2-D
+ *    covariance, and uv_lo the bits of two fp16 remainders: u_c = u_hi + u_lo,
+ *    v_c = v_hi + v_lo; rects u32[n][2] (x0 | y0 << 16, x1 | y1 << 16; tiles,
  *    half-open), tiles_touched u32[n]. Any pointer may be NULL. Valid for visible Gaussians.
  *  rd_debug_pixel_state: T_final f32[H*W], n_contrib i32[H*W], median_pos i32[H*W].
- *  rd_debug_grads2d: after rd_render_bwd, per-Gaussian 2-D gradients f32[n][16] (du, dv,
- *    dA2, dB2, dC2, dopacity, dr, dg, db, dnx, dny, dnz, dz, dp0, dp1, 0). */
+ *  rd_debug_grads2d: after rd_blend_bwd / rd_render_bwd, the per-Gaussian sums K4
+ *    accumulated, as f32[n][16] (valid for visible Gaussians): Σ dA·dx, Σ dA·dy, Σ dA·dx²,
+ *    Σ dA·dx·dy, Σ dA·dy² (accumulated in fp64), Σ dA, Σ w·g_C (3), Σ w·g_N (3), and over
+ *    the pixels whose median splat it is Σ g_D, Σ g_D·dx, Σ g_D·dy; then 0. Here
+ *    dA = α_raw·∂L/∂α, (dx, dy) = centre − pixel, w = α·T. */
 rd_status rd_debug_binning(const rd_view* view, uint64_t* keys, uint32_t* ids, uint32_t* ranges, rd_stream stream);
 rd_status rd_debug_preprocess(const rd_view* view, float* records, uint32_t* rects, uint32_t* tiles_touched,
                               rd_stream stream);

@@ -200,6 +200,19 @@ float zkey_of(const Cam& cam, float mx, float my, float mz) {
   return std::fmaf((float)cam.R[6], mx, std::fmaf((float)cam.R[7], my, std::fmaf((float)cam.R[8], mz, (float)cam.t[2])));
 }
 
+// Contract S6b: the centre must project into the 1.3x guard band of the image,
+// u_c ∈ [−0.15 W, 1.15 W] and v_c ∈ [−0.15 H, 1.15 H] (the 3DGS in_frustum NDC test), decided
+// in fp32 as fx·x_k ∈ [g_u0·z_k, g_u1·z_k] (and likewise for y) with x_k, y_k formed like z_k
+// and g_u0 = float(−0.15 W − cx), g_u1 = float(1.15 W − cx), ... rounded once from double.
+bool in_guard_band(const Cam& cam, float mx, float my, float mz, float zk) {
+  const float xk = std::fmaf((float)cam.R[0], mx, std::fmaf((float)cam.R[1], my, std::fmaf((float)cam.R[2], mz, (float)cam.t[0])));
+  const float yk = std::fmaf((float)cam.R[3], mx, std::fmaf((float)cam.R[4], my, std::fmaf((float)cam.R[5], mz, (float)cam.t[1])));
+  const float gu0 = (float)(-0.15 * cam.W - cam.cx), gu1 = (float)(1.15 * cam.W - cam.cx);
+  const float gv0 = (float)(-0.15 * cam.H - cam.cy), gv1 = (float)(1.15 * cam.H - cam.cy);
+  const float fu = (float)cam.fx * xk, fv = (float)cam.fy * yk;
+  return fu >= gu0 * zk && fu <= gu1 * zk && fv >= gv0 * zk && fv <= gv1 * zk;
+}
+
 template <class S>
 bool project(const S P[NP], const double raw[11], const Cam& cam, const Opt& opt, PG<S>& g) {
   g.valid = false;
@@ -211,6 +224,7 @@ bool project(const S P[NP], const double raw[11], const Cam& cam, const Opt& opt
   if (!(qn2 > 0.0)) return false;
   g.zkey = zkey_of(cam, (float)raw[0], (float)raw[1], (float)raw[2]);
   if (!(g.zkey > (float)cam.znear)) return false;
+  if (!in_guard_band(cam, (float)raw[0], (float)raw[1], (float)raw[2], g.zkey)) return false;
   if (!(raw[10] >= opt.alpha_min)) return false;
   g.o = P[10];
 

@@ -77,6 +77,8 @@ SIGNATURES = {
     "rd_render_fwd": ([_VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_render_bwd": ([_VP, ctypes.POINTER(RdGaussians), _VP, _VP, _VP, _VP, ctypes.POINTER(RdGrads), _VP],
                       ctypes.c_int),
+    "rd_blend_bwd": ([_VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
+    "rd_preprocess_bwd": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
     "rd_view_stats": ([_VP, ctypes.POINTER(RdStats)], ctypes.c_int),
     "rd_set_profiling": ([_VP, ctypes.c_int32], ctypes.c_int),
     "rd_get_timings": ([_VP, ctypes.POINTER(RdTimings), ctypes.c_int32], ctypes.c_int),

@@ -76,9 +76,10 @@ struct rd_view {
   int tile_bits = 0;
   int64_t M = 0;
   int dsel = 0, tsel = 0;  // CUB DoubleBuffer selectors of the depth and tile sorts
-  int64_t n_vis = 0;
-  uint32_t* host_M = nullptr;  // pinned: [0] M, [1] visible Gaussians
-  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp, vis, nvis;
+  int64_t n_vis = 0, n_big = 0;
+  bool g2d_dirty = false;  // the G2D rows hold a previous rd_blend_bwd's sums (K1 zeroes them)
+  uint32_t* host_M = nullptr;  // pinned: [0] M, [1] visible Gaussians, [2] big ones
+  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp, vis, big, nvis;
   Buf tkeys0, tkeys1, vals0, vals1;
   Buf ranges;
   Buf T_final, n_contrib, median_pos;
@@ -213,7 +214,7 @@ rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
                 &v->didx1,  &v->tmp,    &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->vis, &v->nvis};
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->vis, &v->big, &v->nvis};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
@@ -264,6 +265,10 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   for (int k = 0; k < 9; ++k) c.R[k] = cam->R[k];
   for (int k = 0; k < 3; ++k) c.t[k] = cam->t[k];
   c.znear = cam->znear;
+  c.gu0 = (float)(-0.15 * cam->width - (double)cam->cx);
+  c.gu1 = (float)(1.15 * cam->width - (double)cam->cx);
+  c.gv0 = (float)(-0.15 * cam->height - (double)cam->cy);
+  c.gv1 = (float)(1.15 * cam->height - (double)cam->cy);
   for (int i = 0; i < 3; ++i) {
     double acc = 0.0;
     for (int k = 0; k < 3; ++k) acc -= (double)cam->R[3 * k + i] * (double)cam->t[k];
@@ -294,19 +299,22 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   RD_ENSURE(v->didx0, n * sizeof(uint32_t), s);
   RD_ENSURE(v->didx1, n * sizeof(uint32_t), s);
   RD_ENSURE(v->vis, n * sizeof(uint32_t), s);
-  RD_ENSURE(v->nvis, sizeof(uint32_t), s);
+  RD_ENSURE(v->big, n * sizeof(uint32_t), s);
+  RD_ENSURE(v->nvis, 2 * sizeof(uint32_t), s);
+  RD_ENSURE(v->g2d, n * sizeof(G2D), s);
 
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
-  v->begin(s);  // K1 timing includes the zeroing of the visible counter
-  RD_CUDA(cudaMemsetAsync(v->nvis.ptr, 0, sizeof(uint32_t), s));
+  v->begin(s);  // K1 timing includes the zeroing of the list counters
+  RD_CUDA(cudaMemsetAsync(v->nvis.ptr, 0, 2 * sizeof(uint32_t), s));
   launch_preprocess_fwd(dg, c, o, tiles_x, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
                         (uint32_t*)v->dkey0.ptr, (uint32_t*)v->didx0.ptr, (uint32_t*)v->nvis.ptr,
-                        (uint32_t*)v->vis.ptr, v->ctr(), s);
+                        (uint32_t*)v->vis.ptr, (uint32_t*)v->big.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("preprocess_fwd");
   v->end(K_PRE, s);
   v->stage = 1;
   v->M = 0;
-  v->n_vis = 0;
+  v->n_vis = v->n_big = 0;
+  v->g2d_dirty = false;
   return RD_OK;
 }
 
@@ -323,7 +331,7 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   if (n > 0) {
     const size_t tb = binning_temp_bytes(n, 0, v->tile_bits);
     RD_ENSURE(v->tmp, tb, s);
-    if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, 2 * sizeof(uint32_t)));
+    if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, 3 * sizeof(uint32_t)));
     v->begin(s);
     v->dsel = launch_depth_sort((uint32_t*)v->dkey0.ptr, (uint32_t*)v->dkey1.ptr, (uint32_t*)v->didx0.ptr,
                                 (uint32_t*)v->didx1.ptr, n, v->tmp.ptr, v->tmp.cap, s);
@@ -336,10 +344,11 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
     v->end(K_SCAN, s);
     RD_CUDA(cudaMemcpyAsync(v->host_M, (const uint32_t*)v->offsets.ptr + (n - 1), sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, s));
-    RD_CUDA(cudaMemcpyAsync(v->host_M + 1, v->nvis.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    RD_CUDA(cudaMemcpyAsync(v->host_M + 1, v->nvis.ptr, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     RD_CUDA(cudaStreamSynchronize(s));
     M = (int64_t)v->host_M[0];
     v->n_vis = (int64_t)v->host_M[1];
+    v->n_big = (int64_t)v->host_M[2];
   }
   if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
   RD_ENSURE(v->tkeys0, (size_t)M * sizeof(uint32_t), s);
@@ -394,11 +403,31 @@ rd_status rd_render_fwd(rd_view* v, float* color, float* depth, float* normal, f
   return RD_OK;
 }
 
-rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
-                        const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream) {
+rd_status rd_blend_bwd(rd_view* v, const float* dL_dcolor, const float* dL_ddepth, const float* dL_dnormal,
+                       const float* dL_dalpha, rd_stream stream) {
+  g_err.clear();
+  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (v->stage < 3) return fail(RD_ERR_STATE, "rd_blend_bwd before rd_render_fwd");
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t* ids = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
+  v->begin(s);
+  if (v->g2d_dirty && v->n > 0)  // another backward after the same rd_preprocess: re-zero the rows
+    RD_CUDA(cudaMemsetAsync(v->g2d.ptr, 0, (size_t)v->n * sizeof(G2D), s));
+  v->g2d_dirty = true;
+  launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
+                    (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
+                    (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,
+                    (G2D*)v->g2d.ptr, v->ctr(), s);
+  RD_CHECK_LAUNCH("render_bwd");
+  v->end(K_BWD, s);
+  v->stage = 4;
+  return RD_OK;
+}
+
+rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* grads, rd_stream stream) {
   g_err.clear();
   if (!v || !g || !grads) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/gaussians/grads");
-  if (v->stage < 3) return fail(RD_ERR_STATE, "rd_render_bwd before rd_render_fwd");
+  if (v->stage < 4) return fail(RD_ERR_STATE, "rd_preprocess_bwd before rd_blend_bwd");
   if (g->n != v->n || g->sh_coeffs != v->sh_coeffs)
     return fail(RD_ERR_INVALID_ARGUMENT, "Gaussians differ from those given to rd_preprocess");
   if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities || !g->sh))
@@ -410,25 +439,30 @@ rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolo
   if ((g->sh_coeffs * 3) % 4 == 0 && (((uintptr_t)g->sh | (uintptr_t)grads->sh) & 15u) != 0)
     return fail(RD_ERR_INVALID_ARGUMENT, "sh / its gradient not 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t n = (size_t)v->n;
-  RD_ENSURE(v->g2d, n * kG2D * sizeof(float), s);
-  const uint32_t* ids = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
-  v->begin(s);  // K4 timing includes the zeroing of the 2-D gradient scratch
-  if (n > 0) RD_CUDA(cudaMemsetAsync(v->g2d.ptr, 0, n * kG2D * sizeof(float), s));
-  launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
-                    (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
-                    (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,
-                    (float*)v->g2d.ptr, v->ctr(), s);
-  RD_CHECK_LAUNCH("render_bwd");
-  v->end(K_BWD, s);
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
   DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
   v->begin(s);
   launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const uint32_t*)v->vis.ptr, v->n_vis,
-                        (const float*)v->g2d.ptr, dgr, s);
+                        (const uint32_t*)v->big.ptr, v->n_big, (const G2D*)v->g2d.ptr, dgr, s);
   RD_CHECK_LAUNCH("preprocess_bwd");
   v->end(K_PREBWD, s);
   return RD_OK;
+}
+
+rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
+                        const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream) {
+  g_err.clear();
+  if (!v || !g || !grads) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/gaussians/grads");
+  if (v->stage < 3) return fail(RD_ERR_STATE, "rd_render_bwd before rd_render_fwd");
+  if (g->n != v->n || g->sh_coeffs != v->sh_coeffs)
+    return fail(RD_ERR_INVALID_ARGUMENT, "Gaussians differ from those given to rd_preprocess");
+  if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities || !g->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL Gaussian array");
+  if (g->n > 0 && (!grads->means || !grads->scales || !grads->rotations || !grads->opacities || !grads->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL gradient array");
+  rd_status st = rd_blend_bwd(v, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, stream);
+  if (st != RD_OK) return st;
+  return rd_preprocess_bwd(v, g, grads, stream);
 }
 
 rd_status rd_set_profiling(rd_view* v, int32_t enabled) {
@@ -524,7 +558,8 @@ rd_status rd_debug_grads2d(const rd_view* v, float* grads2d, rd_stream stream) {
   if (!v || !grads2d) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/grads2d");
   if (!v->g2d.ptr) return fail(RD_ERR_STATE, "rd_debug_grads2d before rd_render_bwd");
   cudaStream_t s = (cudaStream_t)stream;
-  if (v->n) RD_CUDA(cudaMemcpyAsync(grads2d, v->g2d.ptr, (size_t)v->n * kG2D * 4, cudaMemcpyDeviceToDevice, s));
+  launch_g2d_to_f32((const G2D*)v->g2d.ptr, v->n, grads2d, s);
+  RD_CHECK_LAUNCH("g2d_to_f32");
   return RD_OK;
 }
 

@@ -156,6 +156,14 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
   const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
   if (!(z > cam.znear)) return false;
+  {  // guard band (reading S6b), decided in fp32 with the same op order as the oracle
+    const float xk = __fmaf_rn(cam.R[0], f.mu[0], __fmaf_rn(cam.R[1], f.mu[1], __fmaf_rn(cam.R[2], f.mu[2], cam.t[0])));
+    const float yk = __fmaf_rn(cam.R[3], f.mu[0], __fmaf_rn(cam.R[4], f.mu[1], __fmaf_rn(cam.R[5], f.mu[2], cam.t[1])));
+    const float fu = __fmul_rn(cam.fx, xk), fv = __fmul_rn(cam.fy, yk);
+    if (!(fu >= __fmul_rn(cam.gu0, z) && fu <= __fmul_rn(cam.gu1, z) && fv >= __fmul_rn(cam.gv0, z) &&
+          fv <= __fmul_rn(cam.gv1, z)))
+      return false;
+  }
   f.zkey = z;
   f.o = g.opac[i];
   if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;
@@ -321,10 +329,17 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
 
   Record r;
   const double L2E = 1.4426950408889634;
-  r.r0 = make_float4(uc, vc, (float)(-0.5 * L2E * f.ca), (float)(-L2E * f.cb));
-  r.r1 = make_float4((float)(-0.5 * L2E * f.cc), (float)log2((double)f.o), rgb[0], rgb[1]);
+  // centre as fp32 + half remainder (rade_internal.cuh: Record)
+  const __half2 uvlo = __floats2half2_rn((float)(f.u - (double)uc), (float)(f.v - (double)vc));
+  // (log2e/2)·conic = UᵀU, U = [[g11, g21], [0, g22]] (Cholesky, from the covariance side:
+  // g22² = (log2e/2)/A′11 needs no difference of products)
+  const double Lh = 0.5 * L2E;
+  const double g11 = sqrt(Lh * (double)f.ca), g21 = (double)f.cb * sqrt(Lh / (double)f.ca);
+  const double g22 = sqrt(Lh / (double)f.A11);
+  r.r0 = make_float4(uc, vc, (float)g11, (float)g21);
+  r.r1 = make_float4((float)g22, (float)log2((double)f.o), rgb[0], rgb[1]);
   r.r2 = make_float4(rgb[2], (float)f.n[0], (float)f.n[1], (float)f.n[2]);
-  r.r3 = make_float4(f.zkey, (float)f.p0, (float)f.p1, 1.f / f.o);
+  r.r3 = make_float4(f.zkey, (float)f.p0, (float)f.p1, *reinterpret_cast<const float*>(&uvlo));
   rec[i] = r;
   rect[i] = make_uint2(tx0 | (ty0 << 16), tx1 | (ty1 << 16));
   const uint32_t nt = (tx1 - tx0) * (ty1 - ty0);
@@ -344,8 +359,9 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
                                                          Record* __restrict__ rec, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
                                                          uint32_t* __restrict__ didx,
-                                                         uint32_t* __restrict__ n_visible,
-                                                         uint32_t* __restrict__ vis, Counter* __restrict__ counters) {
+                                                         uint32_t* __restrict__ count, uint32_t* __restrict__ vis,
+                                                         uint32_t* __restrict__ big, G2D* __restrict__ g2d,
+                                                         Counter* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(threadIdx.x & 31);
   uint32_t x0 = 0, y0 = 0, w = 1, nt = 0;
@@ -355,13 +371,23 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, nt > 0u);
   if (vmask == 0u) return;  // warp-uniform
-  uint32_t base = 0;
+  const unsigned bmask = __ballot_sync(0xffffffffu, nt > kBigTiles);
+  uint32_t base = 0, bbase = 0;
   if (lane == 0) {
-    base = atomicAdd(n_visible, (uint32_t)__popc(vmask));
+    base = atomicAdd(count, (uint32_t)__popc(vmask));
+    if (bmask) bbase = atomicAdd(count + 1, (uint32_t)__popc(bmask));
     if (counters) atomicAdd(counters + 3, (Counter)__popc(vmask));
   }
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (nt > 0u) vis[base + __popc(vmask & ((1u << lane) - 1u))] = (uint32_t)i;
+  bbase = __shfl_sync(0xffffffffu, bbase, 0);
+  const unsigned below = (1u << lane) - 1u;
+  if (nt > 0u) {
+    vis[base + __popc(vmask & below)] = (uint32_t)i;
+    float4* row = reinterpret_cast<float4*>(g2d + i);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (nt > kBigTiles) big[bbase + __popc(bmask & below)] = (uint32_t)i;
 }
 
 // ---------------------------------------------------------------------------- K5
@@ -376,13 +402,11 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
 template <int DEG>
 __global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam cam, DevOpt opt,
                                                            const uint32_t* __restrict__ touched,
-                                                           const float* __restrict__ g2d, DevGrads gr) {
+                                                           const G2D* __restrict__ g2d, DevGrads gr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   if (touched[i] == 0u) return;  // culled or off-screen: zero gradient
-  const float4* G4 = reinterpret_cast<const float4*>(g2d + i * kG2D);
-  const float4 q1 = G4[1], q2 = G4[2];
-  const float d_rgb[3] = {q1.z, q1.w, q2.x};
+  const float d_rgb[3] = {g2d[i].f[1], g2d[i].f[2], g2d[i].f[3]};
   const float mu0 = g.means[3 * i], mu1 = g.means[3 * i + 1], mu2 = g.means[3 * i + 2];
   float dmu[3] = {0.f, 0.f, 0.f};
   {
@@ -444,90 +468,97 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam ca
 
 // K5b: geometry — centre, conic, depth plane and normal back to μ, s, q, o (dmu_extra: the
 // view-direction part of dL/dμ from K5a when fused).
+template <typename S>
 __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
-                                                  const float* __restrict__ g2d, DevGrads& gr,
+                                                  const G2D* __restrict__ g2d, DevGrads& gr,
                                                   const float (&dmu_extra)[3]) {
-  GF<float> f;
-  if (!gaussian_forward<float>(g, i, cam, opt, f)) return;
-  const float4* G4 = reinterpret_cast<const float4*>(g2d + i * kG2D);
-  const float4 q0 = G4[0], q1 = G4[1], q2 = G4[2], q3 = G4[3];
-  const float d_u = q0.x, d_v = q0.y, d_A2 = q0.z, d_B2 = q0.w;
-  const float d_C2 = q1.x, d_o = q1.y;
-  const float d_n[3] = {q2.y, q2.z, q2.w};
-  const float d_z = q3.x, d_p0 = q3.y, d_p1 = q3.z;
+  GF<S> f;
+  if (!gaussian_forward<S>(g, i, cam, opt, f)) return;
+  // the G2D sums of K4 → 2-D gradients (log2 e · ln 2 = 1 cancels between the stored
+  // (A2, B2, C2) = log2e·(−a/2, −b, −c/2) and α = 2^e):
+  //   dL/du = −(a S0 + b S1) + p0 S12, dL/dv = −(b S0 + c S1) + p1 S12,
+  //   dL/da = −S2/2, dL/db = −S3, dL/dc = −S4/2, dL/do = S5/o (∂α_raw/∂o = α_raw/o)
+  const G2D& q = g2d[i];
+  const S S0 = (S)q.m[0], S1 = (S)q.m[1], S2 = (S)q.m[2], S3 = (S)q.m[3], S4 = (S)q.m[4];
+  const S S12 = q.f[7];
+  const S d_u = -(f.ca * S0 + f.cb * S1) + f.p0 * S12;
+  const S d_v = -(f.cb * S0 + f.cc * S1) + f.p1 * S12;
+  const float d_o = q.f[0] / f.o;
+  const S d_n[3] = {q.f[4], q.f[5], q.f[6]};
+  const S d_z = S12, d_p0 = q.f[8], d_p1 = q.f[9];
 
-  float dx[3] = {0.f, 0.f, 0.f};  // dL/dx_c (camera space)
-  float dRc[9];
+  S dx[3] = {0, 0, 0};  // dL/dx_c (camera space)
+  S dRc[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) dRc[k] = 0.f;
-  float ds[3] = {0.f, 0.f, 0.f};
-  float dmu[3] = {0.f, 0.f, 0.f};
+  for (int k = 0; k < 9; ++k) dRc[k] = 0;
+  S ds[3] = {0, 0, 0};
+  S dmu[3] = {0, 0, 0};
 
   // ---- projected centre and centre depth
-  const float iz = 1.f / f.x[2];
+  const S iz = S(1) / f.x[2];
   dx[0] += d_u * cam.fx * iz;
   dx[1] += d_v * cam.fy * iz;
   dx[2] += -(d_u * cam.fx * f.x[0] + d_v * cam.fy * f.x[1]) * iz * iz + d_z;
 
   // ---- conic: stored (A2, B2, C2) = log2e·(−a/2, −b, −c/2), conic = A′⁻¹
   {
-    const float da = -0.5f * kLog2e * d_A2, db = -kLog2e * d_B2, dc = -0.5f * kLog2e * d_C2;
+    const S da = S(-0.5) * S2, db = -S3, dc = S(-0.5) * S4;
     // dL/dA′ = −C Ḡ C with Ḡ = [[da, db/2], [db/2, dc]]; off-diagonal counted twice
-    const float a = f.ca, b = f.cb, c = f.cc;
-    const float dA00 = -(a * a * da + a * b * db + b * b * dc);
-    const float dA11 = -(b * b * da + b * c * db + c * c * dc);
-    const float dA01 = -(2.f * a * b * da + (a * c + b * b) * db + 2.f * b * c * dc);
+    const S a = f.ca, b = f.cb, c = f.cc;
+    const S dA00 = -(a * a * da + a * b * db + b * b * dc);
+    const S dA11 = -(b * b * da + b * c * db + c * c * dc);
+    const S dA01 = -(S(2) * a * b * da + (a * c + b * b) * db + S(2) * b * c * dc);
     // A = M Mᵀ
-    float dM[6];
+    S dM[6];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      dM[k] = 2.f * dA00 * f.M[k] + dA01 * f.M[3 + k];
-      dM[3 + k] = dA01 * f.M[k] + 2.f * dA11 * f.M[3 + k];
+      dM[k] = S(2) * dA00 * f.M[k] + dA01 * f.M[3 + k];
+      dM[3 + k] = dA01 * f.M[k] + S(2) * dA11 * f.M[3 + k];
     }
     // M = J₂ RS
-    float dj00 = 0.f, dj02 = 0.f, dj11 = 0.f, dj12 = 0.f;
+    S dj00 = 0, dj02 = 0, dj11 = 0, dj12 = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       dj00 += dM[k] * f.RS[k];
       dj02 += dM[k] * f.RS[6 + k];
       dj11 += dM[3 + k] * f.RS[3 + k];
       dj12 += dM[3 + k] * f.RS[6 + k];
-      const float dRS0 = dM[k] * f.j00;
-      const float dRS1 = dM[3 + k] * f.j11;
-      const float dRS2 = dM[k] * f.j02 + dM[3 + k] * f.j12;
+      const S dRS0 = dM[k] * f.j00;
+      const S dRS1 = dM[3 + k] * f.j11;
+      const S dRS2 = dM[k] * f.j02 + dM[3 + k] * f.j12;
       dRc[k] += dRS0 * f.s[k];
       dRc[3 + k] += dRS1 * f.s[k];
       dRc[6 + k] += dRS2 * f.s[k];
       ds[k] += dRS0 * f.Rc[k] + dRS1 * f.Rc[3 + k] + dRS2 * f.Rc[6 + k];
     }
     // J₂(x): j00 = fx/z, j02 = −fx x/z², j11 = fy/z, j12 = −fy y/z²
-    const float iz2 = iz * iz;
+    const S iz2 = iz * iz;
     dx[0] += -dj02 * cam.fx * iz2;
     dx[1] += -dj12 * cam.fy * iz2;
-    dx[2] += -dj00 * cam.fx * iz2 - dj11 * cam.fy * iz2 + 2.f * dj02 * cam.fx * f.x[0] * iz2 * iz +
-             2.f * dj12 * cam.fy * f.x[1] * iz2 * iz;
+    dx[2] += -dj00 * cam.fx * iz2 - dj11 * cam.fy * iz2 + S(2) * dj02 * cam.fx * f.x[0] * iz2 * iz +
+             S(2) * dj12 * cam.fy * f.x[1] * iz2 * iz;
   }
 
   // ---- depth plane p and normal n (m-form backward)
   {
-    const float imu = 1.f / f.muq;
-    const float iml = 1.f / f.ml;
-    float dmh[3];
+    const S imu = S(1) / f.muq;
+    const S iml = S(1) / f.ml;
+    S dmh[3];
     // n = −m̂/‖m̂‖
-    const float nd = f.n[0] * d_n[0] + f.n[1] * d_n[1] + f.n[2] * d_n[2];
+    const S nd = f.n[0] * d_n[0] + f.n[1] * d_n[1] + f.n[2] * d_n[2];
 #pragma unroll
     for (int k = 0; k < 3; ++k) dmh[k] = -(d_n[k] - f.n[k] * nd) * iml;
     // p_k = c_k e_k, c_k = z² it / f_k, e_k = m̂_k/μ − x̂_k
-    const float z = f.x[2];
-    const float zzit = z * z * f.it;
-    const float de0 = d_p0 * zzit / cam.fx, de1 = d_p1 * zzit / cam.fy;
-    dx[2] += 2.f * (d_p0 * f.p0 + d_p1 * f.p1) / z;
-    float dit = (d_p0 * f.p0 + d_p1 * f.p1) / f.it;
+    const S z = f.x[2];
+    const S zzit = z * z * f.it;
+    const S de0 = d_p0 * zzit / cam.fx, de1 = d_p1 * zzit / cam.fy;
+    dx[2] += S(2) * (d_p0 * f.p0 + d_p1 * f.p1) / z;
+    S dit = (d_p0 * f.p0 + d_p1 * f.p1) / f.it;
     dmh[0] += de0 * imu;
     dmh[1] += de1 * imu;
-    const float dmuq = -(de0 * f.mh[0] + de1 * f.mh[1]) * imu * imu;
-    float dxh[3] = {-de0, -de1, 0.f};
-    float dah[3], drh[3];
+    const S dmuq = -(de0 * f.mh[0] + de1 * f.mh[1]) * imu * imu;
+    S dxh[3] = {-de0, -de1, 0};
+    S dah[3], drh[3];
     // μ = r̂·â ; m̂ = R_c â
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -542,7 +573,7 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       drh[k] += dah[k] * f.w[k];
-      ds[k] += -2.f * dah[k] * f.ah[k] / f.s[k];
+      ds[k] += -S(2) * dah[k] * f.ah[k] / f.s[k];
     }
     // r̂ = R_cᵀ x̂
 #pragma unroll
@@ -557,30 +588,30 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
       dx[r] += dxh[r] * f.it;
       dit += dxh[r] * f.x[r];
     }
-    const float dt2 = -0.5f * dit * f.it * f.it * f.it;
+    const S dt2 = S(-0.5) * dit * f.it * f.it * f.it;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) dx[r] += 2.f * f.x[r] * dt2;
+    for (int r = 0; r < 3; ++r) dx[r] += S(2) * f.x[r] * dt2;
   }
 
   // ---- x_c = W μ + t ; R_c = W R_q
 #pragma unroll
   for (int k = 0; k < 3; ++k) dmu[k] += cam.R[k] * dx[0] + cam.R[3 + k] * dx[1] + cam.R[6 + k] * dx[2];
-  float dRq[9];
+  S dRq[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int k = 0; k < 3; ++k) dRq[3 * r + k] = cam.R[r] * dRc[k] + cam.R[3 + r] * dRc[3 + k] + cam.R[6 + r] * dRc[6 + k];
   // R(q̂) → q̂ → raw q
-  const float w = f.qn[0], a = f.qn[1], b = f.qn[2], c = f.qn[3];
-  float dqn[4];
-  dqn[0] = 2.f * (-c * dRq[1] + b * dRq[2] + c * dRq[3] - a * dRq[5] - b * dRq[6] + a * dRq[7]);
-  dqn[1] = 2.f * (b * dRq[1] + c * dRq[2] + b * dRq[3] - 2.f * a * dRq[4] - w * dRq[5] + c * dRq[6] + w * dRq[7] -
-                  2.f * a * dRq[8]);
-  dqn[2] = 2.f * (-2.f * b * dRq[0] + a * dRq[1] + w * dRq[2] + a * dRq[3] + c * dRq[5] - w * dRq[6] + c * dRq[7] -
-                  2.f * b * dRq[8]);
-  dqn[3] = 2.f * (-2.f * c * dRq[0] - w * dRq[1] + a * dRq[2] + w * dRq[3] - 2.f * c * dRq[4] + b * dRq[5] +
+  const S w = f.qn[0], a = f.qn[1], b = f.qn[2], c = f.qn[3];
+  S dqn[4];
+  dqn[0] = S(2) * (-c * dRq[1] + b * dRq[2] + c * dRq[3] - a * dRq[5] - b * dRq[6] + a * dRq[7]);
+  dqn[1] = S(2) * (b * dRq[1] + c * dRq[2] + b * dRq[3] - S(2) * a * dRq[4] - w * dRq[5] + c * dRq[6] + w * dRq[7] -
+                  S(2) * a * dRq[8]);
+  dqn[2] = S(2) * (-S(2) * b * dRq[0] + a * dRq[1] + w * dRq[2] + a * dRq[3] + c * dRq[5] - w * dRq[6] + c * dRq[7] -
+                  S(2) * b * dRq[8]);
+  dqn[3] = S(2) * (-S(2) * c * dRq[0] - w * dRq[1] + a * dRq[2] + w * dRq[3] - S(2) * c * dRq[4] + b * dRq[5] +
                   a * dRq[6] + b * dRq[7]);
-  const float qd = dqn[0] * w + dqn[1] * a + dqn[2] * b + dqn[3] * c;
+  const S qd = dqn[0] * w + dqn[1] * a + dqn[2] * b + dqn[3] * c;
 
   // read-modify-write of the non-SH gradient rows, loads batched first
   float om[3], os[3];
@@ -594,23 +625,47 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   const float oo = gr.opac[i];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    gr.means[3 * i + k] = om[k] + dmu[k] + dmu_extra[k];
-    gr.scales[3 * i + k] = os[k] + ds[k];
+    gr.means[3 * i + k] = om[k] + (float)dmu[k] + dmu_extra[k];
+    gr.scales[3 * i + k] = os[k] + (float)ds[k];
   }
-  *grot = make_float4(oq.x + (dqn[0] - f.qn[0] * qd) * f.qinv, oq.y + (dqn[1] - f.qn[1] * qd) * f.qinv,
-                      oq.z + (dqn[2] - f.qn[2] * qd) * f.qinv, oq.w + (dqn[3] - f.qn[3] * qd) * f.qinv);
+  *grot = make_float4(oq.x + (float)((dqn[0] - f.qn[0] * qd) * f.qinv), oq.y + (float)((dqn[1] - f.qn[1] * qd) * f.qinv),
+                      oq.z + (float)((dqn[2] - f.qn[2] * qd) * f.qinv), oq.w + (float)((dqn[3] - f.qn[3] * qd) * f.qinv));
   // α = min(α_max, o·G): d_o already excludes the clamp (K4)
   gr.opac[i] = oo + d_o;
 }
 
+// K5b, fp32, one thread per Gaussian in id order: the visible ones touching ≤ kBigTiles
+// tiles (the others are K5b64's).
 __global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
                                                         const uint32_t* __restrict__ touched,
-                                                        const float* __restrict__ g2d, DevGrads gr) {
+                                                        const G2D* __restrict__ g2d, DevGrads gr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
-  if (touched[i] == 0u) return;  // culled or off-screen: zero gradient
+  const uint32_t nt = touched[i];
+  if (nt == 0u || nt > kBigTiles) return;  // culled / off-screen (zero gradient), or big
   const float zero[3] = {0.f, 0.f, 0.f};
-  geometry_backward(g, i, cam, opt, g2d, gr, zero);
+  geometry_backward<float>(g, i, cam, opt, g2d, gr, zero);
+}
+
+// K5b64: the same chain rule in fp64 for the Gaussians of K1's big list.
+__global__ void __launch_bounds__(128) k_preprocess_bwd64(DevGauss g, DevCam cam, DevOpt opt,
+                                                          const uint32_t* __restrict__ big, int64_t n_big,
+                                                          const G2D* __restrict__ g2d, DevGrads gr) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_big) return;
+  const float zero[3] = {0.f, 0.f, 0.f};
+  geometry_backward<double>(g, big[p], cam, opt, g2d, gr, zero);
+}
+
+__global__ void __launch_bounds__(256) k_g2d_to_f32(const G2D* __restrict__ g2d, int64_t n, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float* o = out + 16 * i;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = (float)g2d[i].m[k];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) o[5 + k] = g2d[i].f[k];
+  o[15] = 0.f;
 }
 
 // K5a (cooperative, rows of a multiple of 4 floats): each warp owns 32 VISIBLE Gaussians —
@@ -623,7 +678,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, 
 template <int DEG>
 __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCam cam, DevOpt opt,
                                                                const uint32_t* __restrict__ vis, int64_t n_vis,
-                                                               const float* __restrict__ g2d, DevGrads gr) {
+                                                               const G2D* __restrict__ g2d, DevGrads gr) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int NV = 3 * K, NV4 = (NV + 3) / 4, P = NV4 + 1;
   __shared__ float4 s_coef[2][32 * P];
@@ -637,11 +692,9 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
   const int64_t L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
   float mu0 = 0.f, mu1 = 0.f, mu2 = 0.f, d_rgb[3] = {0.f, 0.f, 0.f};
   if (valid) {
-    const float4* G4 = reinterpret_cast<const float4*>(g2d + (size_t)id * kG2D);
-    const float4 q1 = G4[1], q2 = G4[2];
-    d_rgb[0] = q1.z;
-    d_rgb[1] = q1.w;
-    d_rgb[2] = q2.x;
+    d_rgb[0] = g2d[id].f[1];
+    d_rgb[1] = g2d[id].f[2];
+    d_rgb[2] = g2d[id].f[3];
     mu0 = g.means[3 * (size_t)id];
     mu1 = g.means[3 * (size_t)id + 1];
     mu2 = g.means[3 * (size_t)id + 2];
@@ -717,14 +770,14 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
 }  // namespace
 
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
-                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* n_visible,
-                           uint32_t* vis, Counter* counters, cudaStream_t s) {
+                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* count,
+                           uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = 256;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
 #define RD_K1(D)                                                                                                 \
   k_preprocess_fwd<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, rec, rect, tiles_touched, dkey, didx, \
-                                                 n_visible, vis, counters)
+                                                 count, vis, big, g2d, counters)
   switch (opt.sh_degree) {
     case 0: RD_K1(0); break;
     case 1: RD_K1(1); break;
@@ -735,7 +788,8 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 }
 
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
-                           const uint32_t* vis, int64_t n_vis, const float* g2d, DevGrads grads, cudaStream_t s) {
+                           const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
+                           DevGrads grads, cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = 128;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
@@ -761,6 +815,13 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 #undef RD_K5A
   }
   k_preprocess_bwd<<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads);
+  if (n_big > 0)
+    k_preprocess_bwd64<<<(unsigned)((n_big + 127) / 128), 128, 0, s>>>(g, cam, opt, big, n_big, g2d, grads);
+}
+
+void launch_g2d_to_f32(const G2D* g2d, int64_t n, float* out, cudaStream_t s) {
+  if (n == 0) return;
+  k_g2d_to_f32<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g2d, n, out);
 }
 
 }  // namespace rade

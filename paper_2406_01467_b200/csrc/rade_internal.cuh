@@ -3,6 +3,7 @@
 // preprocess bwd). Nothing here is shared with oracle/ (which is test infrastructure).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -19,6 +20,8 @@ struct DevCam {
   float t[3];
   float znear;
   float campos[3];  // -R^T t (camera centre in world space), for SH view directions
+  // guard band (reading S6b): float(−0.15 W − cx), float(1.15 W − cx), same for v
+  float gu0, gu1, gv0, gv1;
 };
 
 struct DevOpt {
@@ -49,17 +52,37 @@ struct DevGrads {
 };
 
 // Per-visible-Gaussian record written by K1 and gathered by K3/K4 (64 B, 4 x float4):
-//   r0 = (u_c, v_c, A2, B2)   r1 = (C2, log2 o, R, G)   r2 = (B, nx, ny, nz)   r3 = (z_c, p0, p1, 1/o)
-// where (A2, B2, C2) = log2(e) * (-a/2, -b, -c/2) for the conic [[a, b], [b, c]] of the
-// dilated 2-D covariance, so that G = exp2(A2 dx^2 + B2 dx dy + C2 dy^2) with
-// (dx, dy) = (u_c - u, v_c - v) (readings S1, S4, S5).
+//   r0 = (u_hi, v_hi, g11, g21)   r1 = (g22, log2 o, R, G)   r2 = (B, nx, ny, nz)
+//   r3 = (z_c, p0, p1, half2(u_lo, v_lo))
+// where UᵀU = (log2 e / 2)·[[a, b], [b, c]], U = [[g11, g21], [0, g22]], is the Cholesky
+// factor of the conic of the dilated 2-D covariance, so that
+//   G = exp(−½ΔᵀCΔ) = 2^−((g11 dx + g21 dy)² + (g22 dy)²),  (dx, dy) = (u_c − u, v_c − v)
+// (readings S1, S4, S5). A sum of two squares has no cancellation: the
+// expanded a·dx² + 2b·dx·dy + c·dy² of a long thin splat is a difference of terms ~10⁵
+// times larger than the result, whose fp32 rounding would move α by percents. The centre
+// is a float + half pair, u_c = u_hi + u_lo: an fp32 pixel coordinate alone carries up to
+// 3e-5 px of rounding at u ~ 600, which moves α of a 1-px splat by ~6e-5 relative.
 struct __align__(16) Record {
   float4 r0, r1, r2, r3;
 };
 
-// 2-D gradient accumulator per Gaussian (64 B):
-//   du, dv, dA2, dB2, dC2, dopacity, dR, dG, dB, dnx, dny, dnz, dz, dp0, dp1, unused
-constexpr int kG2D = 16;
+// Per-Gaussian backward sums, accumulated by K4's atomics over (pixel, splat) pairs and
+// read by K5 (80 B row; zeroed by K1 for every visible Gaussian). dA = α_raw·∂L/∂α,
+// (dx, dy) = centre − pixel, w = α T, g_* the pixel cotangents:
+//   m[0..4] = Σ dA·dx, Σ dA·dy, Σ dA·dx², Σ dA·dx·dy, Σ dA·dy²   (fp64: for screen-sized
+//             splats these are sums of ~10⁶ terms of size ~10⁶ whose result is orders of
+//             magnitude smaller; fp32 atomics would leave ~1e-6 relative noise, which the
+//             chain rule through the conic amplifies ~10⁴-fold)
+//   f[0] = Σ dA, f[1..3] = Σ w·g_C, f[4..6] = Σ w·g_N,
+//   f[7..9] = Σ g_D, Σ g_D·dx, Σ g_D·dy over the pixels whose median splat this is.
+struct __align__(16) G2D {
+  double m[5];
+  float f[10];
+};
+static_assert(sizeof(G2D) == 80, "G2D row");
+// K5b runs in fp64 for splats touching more tiles than this (their conic gradient is the
+// small difference of large terms); in fp32 otherwise.
+constexpr uint32_t kBigTiles = 64;
 
 // 16-byte global → shared copy without a register round trip (cp.async / LDGSTS, L2-only).
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -98,21 +121,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 // The per-pair α evaluation shared bit-for-bit by K3 and K4 (explicit roundings so the
 // two kernels take identical skip / stop decisions). With lo = log2(o) stored in the record,
-//   e = A2 dx² + B2 dx dy + C2 dy² + lo,   α_raw = o·exp(−½ΔᵀCΔ) = 2^e,
+//   e = lo − (g11 dx + g21 dy)² − (g22 dy)²,   α_raw = o·exp(−½ΔᵀCΔ) = 2^e,
 // so the α ≥ α_min test is e ≥ log2(α_min) — taken BEFORE the exp2, which rejected pairs
 // never evaluate — and α = min(α_max, 2^e) (readings S1, S8).
 struct PairAlpha {
   float dx, dy, e;
   bool pass;
 };
-__device__ __forceinline__ PairAlpha pair_power(const float4& r0, float C2, float lo, float px, float py,
+// (u_lo, v_lo) of a record's r3.w
+__device__ __forceinline__ float2 uv_lo(float w) { return __half22float2(*reinterpret_cast<const __half2*>(&w)); }
+// dx = (u_hi − px) + u_lo: the first difference is exact or carries |dx|-relative rounding
+// only, so Δ is accurate to ~1e-7·|Δ| + the half rounding of u_lo (< 3e-8 px).
+__device__ __forceinline__ PairAlpha pair_power(const float4& r0, float g22, float lo, float2 ulo, float px, float py,
                                                 float log2_alpha_min) {
   PairAlpha pa;
-  pa.dx = __fsub_rn(r0.x, px);
-  pa.dy = __fsub_rn(r0.y, py);
-  const float inner = __fmaf_rn(r0.z, pa.dx, __fmul_rn(r0.w, pa.dy));                    // A2 dx + B2 dy
-  const float pw = __fmaf_rn(pa.dx, inner, __fmul_rn(__fmul_rn(C2, pa.dy), pa.dy));     // + C2 dy²
-  pa.e = __fadd_rn(pw, lo);
+  pa.dx = __fadd_rn(__fsub_rn(r0.x, px), ulo.x);
+  pa.dy = __fadd_rn(__fsub_rn(r0.y, py), ulo.y);
+  const float t1 = __fmaf_rn(r0.z, pa.dx, __fmul_rn(r0.w, pa.dy));  // g11 dx + g21 dy
+  const float t2 = __fmul_rn(g22, pa.dy);
+  const float pw = __fmaf_rn(t1, t1, __fmul_rn(t2, t2));
+  pa.e = __fsub_rn(lo, pw);
   pa.pass = pa.e >= log2_alpha_min;
   return pa;
 }
@@ -130,14 +158,19 @@ __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
 }
 
 // K1 also writes the depth-sort input: dkey[i] = float_bits(z_c) (0xFFFFFFFF if the
-// Gaussian touches no tile) and didx[i] = i, and appends the visible ids to vis
-// (*n_visible, zeroed beforehand).
+// Gaussian touches no tile) and didx[i] = i, zeroes the G2D row of every visible Gaussian,
+// and appends the visible ids to vis (count[0]) and those touching more than kBigTiles
+// tiles to big (count[1]); count is zeroed beforehand.
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
-                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* n_visible,
-                           uint32_t* vis, Counter* counters, cudaStream_t s);
-// K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry, id order).
+                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* count,
+                           uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s);
+// K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry: fp32 in id
+// order for the visible Gaussians touching ≤ kBigTiles tiles, fp64 over the big list).
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
-                           const uint32_t* vis, int64_t n_vis, const float* g2d, DevGrads grads, cudaStream_t s);
+                           const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
+                           DevGrads grads, cudaStream_t s);
+// debug: G2D rows → f32 [n][16] (m[0..4], f[0..9], 0)
+void launch_g2d_to_f32(const G2D* g2d, int64_t n, float* out, cudaStream_t s);
 // K2 (binning.cu). Sorts return the CUB DoubleBuffer selector (1: result in the *1 buffers).
 size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits);
 int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t* idx1, int64_t n, void* temp,
@@ -159,7 +192,7 @@ void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
-                       const float* dL_dnormal, const float* dL_dalpha, float* g2d, Counter* counters,
+                       const float* dL_dnormal, const float* dL_dalpha, G2D* g2d, Counter* counters,
                        cudaStream_t s);
 
 }  // namespace rade

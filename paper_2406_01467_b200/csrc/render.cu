@@ -46,9 +46,9 @@ __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool insi
 
 // One (pixel, splat) step of Eq.3 with the median-depth selection of reading S9.
 template <bool PROF>
-__device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4& a2, uint32_t id,
-                                         const Record* __restrict__ rec, int pos, const DevOpt& opt) {
-  const PairAlpha pa = pair_power(a0, a1.x, a1.y, s.px, s.py, opt.log2_alpha_min);
+__device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4& a2,
+                                         const float4& a3, float2 ulo, int pos, const DevOpt& opt) {
+  const PairAlpha pa = pair_power(a0, a1.x, a1.y, ulo, s.px, s.py, opt.log2_alpha_min);
   if (PROF) ++s.n_eval;
   if (!pa.pass) return;  // α < α_min: skipped (S8)
   const float alpha = fminf(opt.alpha_max, ex2_approx(pa.e));
@@ -64,8 +64,7 @@ __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4
   s.N0 = __fmaf_rn(w, a2.y, s.N0);
   s.N1 = __fmaf_rn(w, a2.z, s.N1);
   s.N2 = __fmaf_rn(w, a2.w, s.N2);
-  if (s.T > opt.median_T && Tn <= opt.median_T) {
-    const float4 a3 = rec[id].r3;  // (z_c, p0, p1): once per pixel
+  if (s.T > opt.median_T && Tn <= opt.median_T) {  // a3 = (z_c, p0, p1, ·)
     s.D = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
     s.med = pos;
   }
@@ -123,11 +122,11 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   const uint2 range = ranges[tile];
   const int total = (int)(range.y - range.x);
 
-  __shared__ float4 sbuf[3][BATCH];  // record quarters r0, r1, r2 of the batch
-  __shared__ uint32_t sid[BATCH];
+  __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   float4* s0 = sbuf[0];
   float4* s1 = sbuf[1];
   float4* s2 = sbuf[2];
+  float4* s3 = sbuf[3];
 
   PixF A, B;
   pixf_init(A, (float)px + 0.5f, (float)pyA + 0.5f, inA);
@@ -139,24 +138,24 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const int t = (int)threadIdx.x + h * NT;
       const int k = base + t;
       if (k < total) {
-        const uint32_t id = ids[range.x + k];
-        const Record* r = rec + id;
-        sid[t] = id;
+        const Record* r = rec + ids[range.x + k];
         s0[t] = r->r0;
         s1[t] = r->r1;
         s2[t] = r->r2;
+        s3[t] = r->r3;
       }
     }
     __syncthreads();
     const int cnt = min(BATCH, total - base);
-    const unsigned a_s0 = smem_addr(s0), a_id = smem_addr(sid);  // s0, s1, s2 are contiguous
+    const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
     for (int j = 0; j < cnt; ++j) {
       if (A.done && B.done) break;
       const unsigned a = a_s0 + 16u * j;
-      const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH), a2 = lds128(a + 32u * BATCH);
-      const uint32_t id = lds32(a_id + 4u * j);
-      if (!A.done) fwd_step<PROF>(A, a0, a1, a2, id, rec, base + j, opt);
-      if (!B.done) fwd_step<PROF>(B, a0, a1, a2, id, rec, base + j, opt);
+      const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH), a2 = lds128(a + 32u * BATCH),
+                   a3 = lds128(a + 48u * BATCH);
+      const float2 ulo = uv_lo(a3.w);
+      if (!A.done) fwd_step<PROF>(A, a0, a1, a2, a3, ulo, base + j, opt);
+      if (!B.done) fwd_step<PROF>(B, a0, a1, a2, a3, ulo, base + j, opt);
     }
   }
   if (PROF) {
@@ -270,17 +269,12 @@ __device__ __forceinline__ void bwd_median(const PixB& s, float (&g)[16], const 
   g[14] = fmaf(s.gD, pa.dy, g[14]);
 }
 
-// The 2-D gradient slot k (rade_internal.cuh order) of one splat from the reduced sums S:
-//   du = ln2(2A2·S0 + B2·S1) + p0·S12, dv = ln2(B2·S0 + 2C2·S1) + p1·S12 (e = A2dx² + B2dxdy
-//   + C2dy² + log2 o in log2 units, D = z_c + p·Δ), dA2 = ln2·S2, dB2 = ln2·S3, dC2 = ln2·S4,
-//   do = S5/o (∂α_raw/∂o = α_raw/o), the rest as summed.
-__device__ __forceinline__ float g2d_slot(int k, float sk, float s0, float s1, float s12, const float4& a0,
-                                          const float4& a1, const float4& a3) {
-  if (k == 0) return kLn2 * (2.f * a0.z * s0 + a0.w * s1) + a3.y * s12;
-  if (k == 1) return kLn2 * (a0.w * s0 + 2.f * a1.x * s1) + a3.z * s12;
-  if (k >= 2 && k <= 4) return kLn2 * sk;
-  if (k == 5) return sk * a3.w;
-  return sk;
+// Sum k of one splat into its G2D row (k < 5: fp64 moments, see rade_internal.cuh).
+__device__ __forceinline__ void g2d_add(G2D* row, int k, float v) {
+  if (k < 5)
+    atomicAdd(&row->m[k], (double)v);
+  else
+    atomicAdd(&row->f[k - 5], v);
 }
 
 // K4: one CTA per tile, TILE²/PPT threads, PPT pixels per thread. Warp w owns the compact
@@ -293,7 +287,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
     const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
-    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, float* __restrict__ g2d,
+    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, G2D* __restrict__ g2d,
     Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / PPT;
   constexpr int BATCH = TILE * TILE;
@@ -307,7 +301,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
   const uint2 range = ranges[tile];
   const int HW = cam.W * cam.H;
 
-  __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch; r3 = (z_c, p0, p1, 1/o)
+  __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   __shared__ uint32_t sid[BATCH];
   __shared__ int s_maxlast;
 
@@ -354,18 +348,19 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
+      const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
       PairAlpha pa[PPT];
       bool act[PPT];
       bool any = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        pa[k] = pair_power(a0, a1.x, a1.y, s[k].px, s[k].py, opt.log2_alpha_min);
+        pa[k] = pair_power(a0, a1.x, a1.y, ulo, s[k].px, s[k].py, opt.log2_alpha_min);
         act[k] = pos < s[k].last && pa[k].pass;
         any = any || act[k];
       }
       const unsigned am = __ballot_sync(0xffffffffu, any);
       if (am == 0u) continue;  // warp-uniform: no pixel of this warp uses the splat
-      const float4 a2 = lds128(a + 32u * BATCH), a3 = lds128(a + 48u * BATCH);
+      const float4 a2 = lds128(a + 32u * BATCH);
       float g[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) g[k] = 0.f;
@@ -374,19 +369,16 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
         if (act[k] && pos == s[k].med) bwd_median(s[k], g, pa[k]);
-      float* dst = g2d + (size_t)lds32(a_id + 4u * j) * kG2D;
+      G2D* dst = g2d + lds32(a_id + 4u * j);
       if (__popc(am) == 1) {  // one contributing thread in this warp: no reduction needed
         if (any) {
 #pragma unroll
-          for (int k = 0; k < 15; ++k) atomicAdd(dst + k, g2d_slot(k, g[k], g[0], g[1], g[12], a0, a1, a3));
+          for (int k = 0; k < 15; ++k) g2d_add(dst, k, g[k]);
         }
       } else {
         const float v = reduce_scatter16(g, lane);
-        const float s0 = __shfl_sync(0xffffffffu, v, 0);
-        const float s1 = __shfl_sync(0xffffffffu, v, 2);
-        const float s12 = __shfl_sync(0xffffffffu, v, 24);
         const int k = lane >> 1;
-        if ((lane & 1) == 0 && k < 15) atomicAdd(dst + k, g2d_slot(k, v, s0, s1, s12, a0, a1, a3));
+        if ((lane & 1) == 0 && k < 15) g2d_add(dst, k, v);
       }
     }
   }
@@ -412,7 +404,7 @@ void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
-                       const float* dL_dnormal, const float* dL_dalpha, float* g2d, Counter* counters,
+                       const float* dL_dnormal, const float* dL_dalpha, G2D* g2d, Counter* counters,
                        cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
   if (opt.tile == 16)

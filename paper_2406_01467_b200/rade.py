@@ -203,22 +203,46 @@ def rd_render_fwd(view: View, color=None, depth=None, normal=None, alpha=None, s
     return dict(color=color, depth=depth, normal=normal, alpha=alpha)
 
 
-def rd_render_bwd(view: View, gaussians: Gaussians, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None,
-                  dL_dalpha=None, grads: Gaussians = None, stream=None):
-    """Accumulates (+=) parameter gradients into `grads` (same layout as `gaussians`)."""
+def _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha):
     H, W = view.camera.height, view.camera.width
     for name, t, shp in (("dL_dcolor", dL_dcolor, (3, H, W)), ("dL_ddepth", dL_ddepth, (H, W)),
                          ("dL_dnormal", dL_dnormal, (3, H, W)), ("dL_dalpha", dL_dalpha, (H, W))):
         if t is not None:
             _check_f32(name, t, shp)
-    g = gaussians.c_struct()
+
+
+def _grads_struct(grads):
     if grads is None:
         raise ValueError("grads is required")
     grads.validate()
-    gr = N.RdGrads(grads.means.data_ptr(), grads.scales.data_ptr(), grads.rotations.data_ptr(),
-                   grads.opacities.data_ptr(), grads.sh.data_ptr())
+    return N.RdGrads(grads.means.data_ptr(), grads.scales.data_ptr(), grads.rotations.data_ptr(),
+                     grads.opacities.data_ptr(), grads.sh.data_ptr())
+
+
+def rd_render_bwd(view: View, gaussians: Gaussians, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None,
+                  dL_dalpha=None, grads: Gaussians = None, stream=None):
+    """Accumulates (+=) parameter gradients into `grads` (same layout as `gaussians`)."""
+    _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha)
+    g = gaussians.c_struct()
+    gr = _grads_struct(grads)
     N.check(view.lib.rd_render_bwd(view.handle, ctypes.byref(g), _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(dL_dnormal),
                                    _ptr(dL_dalpha), ctypes.byref(gr), _stream_ptr(stream)), "rd_render_bwd")
+    return grads
+
+
+def rd_blend_bwd(view: View, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None, dL_dalpha=None, stream=None):
+    """K4 only: the per-Gaussian 2-D gradients of the view (first half of rd_render_bwd)."""
+    _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha)
+    N.check(view.lib.rd_blend_bwd(view.handle, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(dL_dnormal), _ptr(dL_dalpha),
+                                  _stream_ptr(stream)), "rd_blend_bwd")
+
+
+def rd_preprocess_bwd(view: View, gaussians: Gaussians, grads: Gaussians, stream=None):
+    """K5 only: accumulates (+=) parameter gradients from the last rd_blend_bwd of the view."""
+    g = gaussians.c_struct()
+    gr = _grads_struct(grads)
+    N.check(view.lib.rd_preprocess_bwd(view.handle, ctypes.byref(g), ctypes.byref(gr), _stream_ptr(stream)),
+            "rd_preprocess_bwd")
     return grads
 
 

@@ -93,11 +93,15 @@ def test_preprocess_parity(case):
     o = pg[vis]
     np.testing.assert_allclose(r[:, 0], o[:, oracle.PG["u"]], rtol=1e-5, atol=1e-4)
     np.testing.assert_allclose(r[:, 1], o[:, oracle.PG["v"]], rtol=1e-5, atol=1e-4)
-    log2e = 1.4426950408889634
-    conic = np.stack([-2 * r[:, 2] / log2e, -r[:, 3] / log2e, -2 * r[:, 4] / log2e], 1)
+    # (log2e/2)·conic = UᵀU with U = [[g11, g21], [0, g22]] = (r2, r3, r4)
+    L = 1.4426950408889634 / 2
+    conic = np.stack([r[:, 2] ** 2, r[:, 2] * r[:, 3], r[:, 3] ** 2 + r[:, 4] ** 2], 1) / L
     np.testing.assert_allclose(conic, o[:, oracle.PG["conic"]], rtol=2e-4, atol=1e-7)
     np.testing.assert_allclose(np.exp2(r[:, 5]), o[:, oracle.PG["o"]], rtol=1e-6)  # log2 o
-    np.testing.assert_allclose(r[:, 15], 1.0 / o[:, oracle.PG["o"]], rtol=1e-6)   # 1/o
+    # centre = fp32 + half remainder (r3.w): accurate far below the fp32 ulp of u (~6e-5 px)
+    lo = rec[vis][:, 15].copy().view(np.float16).astype(np.float64).reshape(-1, 2)
+    np.testing.assert_allclose(r[:, 0] + lo[:, 0], o[:, oracle.PG["u"]], rtol=0, atol=2e-6)
+    np.testing.assert_allclose(r[:, 1] + lo[:, 1], o[:, oracle.PG["v"]], rtol=0, atol=2e-6)
     np.testing.assert_allclose(r[:, 6:9], o[:, oracle.PG["rgb"]], atol=1e-5)
     np.testing.assert_allclose(r[:, 12], o[:, oracle.PG["z"]], rtol=1e-6)
     ng = np.abs(o[:, oracle.PG["ndotx"]]) >= 0.05

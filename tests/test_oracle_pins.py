@@ -483,3 +483,31 @@ def test_zero_cotangent_gives_zero_gradient(O):
     z = {k: np.zeros_like(v) for k, v in sg.cotangents(0, 32, 32).items()}
     G = O.grad(sc, cam, OPT, z, np.arange(30))
     assert np.all(G == 0)
+
+
+# ----------------------------------------------------------------------------- guard band (S6b)
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_guard_band_cull(O, axis):
+    """Reading S6b: a centre projecting outside [−0.15, 1.15]× the image is culled (3DGS
+    in_frustum NDC test). Pinned by placing a wide splat just inside / just outside each
+    edge (closed-form pixel position u = fx·x/z + cx) and checking that it is kept and
+    reaches into the image, or culled and contributes nothing."""
+    cam = sg.camera_identity(64, 48, 60.0)
+    size = (cam.width, cam.height)[axis]
+    f = (cam.fx, cam.fy)[axis]
+    c = (cam.cx, cam.cy)[axis]
+    z = 3.0
+    lo, hi = -0.15 * size, 1.15 * size
+    for target in (hi - 0.5, hi + 0.5, lo + 0.5, lo - 0.5):
+        keep = lo <= target <= hi
+        pos = [0.0, 0.0, z]
+        pos[axis] = (target - c) * z / f
+        sc = one_gaussian(pos, [1.0, 1.0, 1.0], opacity=0.9)
+        pg = O.project(sc, cam, OPT)
+        assert (pg[0, 0] == 1) == keep, (axis, target)
+        out = O.render(sc, cam, OPT)
+        if keep:
+            assert out["alpha"].max() > 0.05  # σ ≈ 20 px: its footprint reaches into the image
+        else:
+            assert out["alpha"].max() == 0.0
