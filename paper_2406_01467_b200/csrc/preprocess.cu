@@ -371,7 +371,8 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, nt > 0u);
   if (vmask == 0u) return;  // warp-uniform
-  const unsigned bmask = __ballot_sync(0xffffffffu, nt > kBigTiles);
+  const bool bigg = is_big(nt, opt.tile);
+  const unsigned bmask = __ballot_sync(0xffffffffu, bigg);
   uint32_t base = 0, bbase = 0;
   if (lane == 0) {
     base = atomicAdd(count, (uint32_t)__popc(vmask));
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, 
 #pragma unroll
     for (int q = 0; q < 5; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  if (nt > kBigTiles) big[bbase + __popc(bmask & below)] = (uint32_t)i;
+  if (bigg) big[bbase + __popc(bmask & below)] = (uint32_t)i;
 }
 
 // ---------------------------------------------------------------------------- K5
@@ -634,7 +635,7 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   gr.opac[i] = oo + d_o;
 }
 
-// K5b, fp32, one thread per Gaussian in id order: the visible ones touching ≤ kBigTiles
+// K5b, fp32, one thread per Gaussian in id order: the visible ones that are not is_big
 // tiles (the others are K5b64's).
 __global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
                                                         const uint32_t* __restrict__ touched,
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, 
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   const uint32_t nt = touched[i];
-  if (nt == 0u || nt > kBigTiles) return;  // culled / off-screen (zero gradient), or big
+  if (nt == 0u || is_big(nt, opt.tile)) return;  // culled / off-screen (zero gradient), or big
   const float zero[3] = {0.f, 0.f, 0.f};
   geometry_backward<float>(g, i, cam, opt, g2d, gr, zero);
 }

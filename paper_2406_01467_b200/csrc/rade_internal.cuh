@@ -80,9 +80,12 @@ struct __align__(16) G2D {
   float f[10];
 };
 static_assert(sizeof(G2D) == 80, "G2D row");
-// K5b runs in fp64 for splats touching more tiles than this (their conic gradient is the
-// small difference of large terms); in fp32 otherwise.
-constexpr uint32_t kBigTiles = 64;
+// K5b runs in fp64 for splats whose tile rect covers more pixels than this (their conic
+// gradient is the small difference of large terms); in fp32 otherwise.
+constexpr uint32_t kBigPixels = 64 * 256;
+__device__ __forceinline__ bool is_big(uint32_t tiles_touched, int tile) {
+  return tiles_touched * (uint32_t)(tile * tile) > kBigPixels;
+}
 
 // 16-byte global → shared copy without a register round trip (cp.async / LDGSTS, L2-only).
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -159,13 +162,13 @@ __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
 
 // K1 also writes the depth-sort input: dkey[i] = float_bits(z_c) (0xFFFFFFFF if the
 // Gaussian touches no tile) and didx[i] = i, zeroes the G2D row of every visible Gaussian,
-// and appends the visible ids to vis (count[0]) and those touching more than kBigTiles
+// and appends the visible ids to vis (count[0]) and the big ones (is_big)
 // tiles to big (count[1]); count is zeroed beforehand.
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
                            uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* count,
                            uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s);
 // K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry: fp32 in id
-// order for the visible Gaussians touching ≤ kBigTiles tiles, fp64 over the big list).
+// order for the visible Gaussians that are not is_big, fp64 over the big list).
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
                            DevGrads grads, cudaStream_t s);

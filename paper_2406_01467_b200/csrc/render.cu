@@ -96,6 +96,65 @@ __device__ __forceinline__ void fwd_store(const PixF& s, bool inside, int pix, i
   median_pos[pix] = s.med;
 }
 
+// Can the splat reach α ≥ α_min at a pixel centre of [x0, x1] × [y0, y1]? It does where
+// q(Δ) = t1² + t2² ≤ K = log2 o − log2 α_min (t1 = g11 dx + g21 dy, t2 = g22 dy, Δ = centre −
+// pixel), so the exact test is min over the Δ-box of the convex q ≤ K. Its unconstrained
+// minimiser is Δ = 0; if that lies outside the box the minimum lies on a face whose side
+// excludes 0 (at most one per axis), where q is a 1-D quadratic minimised in closed form
+// and clamped to the face. Accepting with a 1e-5 relative margin keeps the test
+// conservative against pair_power's fp32 roundings (it never drops a pair pair_power
+// would accept).
+__device__ __forceinline__ bool splat_reaches(const float4& r0, const float4& r1, float2 c, float x0, float x1,
+                                              float y0, float y1, float log2_alpha_min) {
+  const float K = r1.y - log2_alpha_min;
+  if (!(K > 0.f)) return false;
+  const float g11 = r0.z, g21 = r0.w, g22 = r1.x;
+  const float dxa = c.x - x1, dxb = c.x - x0, dya = c.y - y1, dyb = c.y - y0;  // Δ-box
+  const bool in_x = dxa <= 0.f && dxb >= 0.f, in_y = dya <= 0.f && dyb >= 0.f;
+  if (in_x && in_y) return true;
+  float qmin = 3.4e38f;
+  if (!in_x) {  // face dx = cx, dy ∈ [dya, dyb]
+    const float cx = dxa > 0.f ? dxa : dxb;
+    const float a = fmaf(g21, g21, g22 * g22);
+    const float dy = fminf(fmaxf(-g11 * g21 * cx / a, dya), dyb);
+    const float t1 = fmaf(g11, cx, g21 * dy), t2 = g22 * dy;
+    qmin = fminf(qmin, fmaf(t1, t1, t2 * t2));
+  }
+  if (!in_y) {  // face dy = cy, dx ∈ [dxa, dxb]
+    const float cy = dya > 0.f ? dya : dyb;
+    const float dx = fminf(fmaxf(-g21 * cy / g11, dxa), dxb);
+    const float t1 = fmaf(g11, dx, g21 * cy), t2 = g22 * cy;
+    qmin = fminf(qmin, fmaf(t1, t1, t2 * t2));
+  }
+  return qmin <= K * 1.00001f + 1e-5f;
+}
+
+// Per-warp filter of a staged batch: the indices k < cnt (in order) of the splats that can
+// reach the warp's pixel rectangle, written to wl; returns their number. Lane-parallel (32
+// splats per pass), so a warp then steps only through splats that touch its pixels.
+__device__ __forceinline__ int warp_filter(const float4* s0, const float4* s1, const float4* s3, int cnt, int lane,
+                                           float x0, float x1, float y0, float y1, float log2_alpha_min,
+                                           uint16_t* wl) {
+  int nsel = 0;
+  for (int k0 = 0; k0 < cnt; k0 += 32) {
+    const int k = k0 + lane;
+    bool ok = false;
+    if (k < cnt) {
+      const float4 r0 = s0[k], r1 = s1[k];
+      const float2 lo = uv_lo(s3[k].w);
+      ok = splat_reaches(r0, r1, make_float2(r0.x + lo.x, r0.y + lo.y), x0, x1, y0, y1, log2_alpha_min);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (ok) wl[nsel + __popc(m & ((1u << lane) - 1u))] = (uint16_t)k;
+    nsel += __popc(m);
+  }
+  __syncwarp();
+  return nsel;
+}
+
+// K3: one CTA per TILE×TILE tile, TILE²/2 threads; warp w owns the 8×8 quadrant w of the
+// tile (lane l: column l % 8, rows l / 8 and l / 8 + 4). Per staged batch each warp first
+// filters the batch down to the splats that reach its quadrant, then blends those.
 template <int TILE, bool PROF>
 __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOpt opt, int tiles_x,
                                                                 const uint2* __restrict__ ranges,
@@ -109,20 +168,21 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                                                 int32_t* __restrict__ median_pos,
                                                                 Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / 2;  // threads
+  constexpr int NW = NT / 32;          // warps = 8×8 quadrants
   constexpr int BATCH = TILE * TILE;   // splats staged per round
+  constexpr bool kFilter = TILE > 8;
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  // warp w owns the compact 2W-row band [2W·w, 2W·w + 2W) of the tile (W = 32 / TILE lane
-  // rows): lane row r holds pixel rows 2W·w + r (A) and + W (B)
-  constexpr int W = 32 / TILE;
-  const int lane_ = (int)(threadIdx.x & 31), warp_ = (int)(threadIdx.x >> 5);
-  const int lx = lane_ % TILE, ly = 2 * W * warp_ + lane_ / TILE;
-  const int px = tx * TILE + lx, pyA = ty * TILE + ly, pyB = pyA + W;
+  const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+  const int qx = tx * TILE + (warp % (TILE / 8)) * 8, qy = ty * TILE + (warp / (TILE / 8)) * 8;
+  const int px = qx + lane % 8, pyA = qy + lane / 8, pyB = pyA + 4;
   const bool inA = px < cam.W && pyA < cam.H, inB = px < cam.W && pyB < cam.H;
+  const float fx0 = (float)qx + 0.5f, fy0 = (float)qy + 0.5f;  // pixel-centre rectangle of the quadrant
   const uint2 range = ranges[tile];
   const int total = (int)(range.y - range.x);
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
+  __shared__ uint16_t wlist[kFilter ? NW : 1][kFilter ? BATCH : 1];
   float4* s0 = sbuf[0];
   float4* s1 = sbuf[1];
   float4* s2 = sbuf[2];
@@ -146,10 +206,16 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       }
     }
     __syncthreads();
+    if (__all_sync(0xffffffffu, A.done && B.done)) continue;  // this warp is saturated
     const int cnt = min(BATCH, total - base);
+    // 8×8 tiles: the binning rect is already tight, filtering costs more than it saves
+    const int nsel = kFilter ? warp_filter(s0, s1, s3, cnt, lane, fx0, fx0 + 7.f, fy0, fy0 + 7.f,
+                                           opt.log2_alpha_min, wlist[warp])
+                             : cnt;
     const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
-    for (int j = 0; j < cnt; ++j) {
+    for (int i = 0; i < nsel; ++i) {
       if (A.done && B.done) break;
+      const int j = kFilter ? (int)wlist[warp][i] : i;
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH), a2 = lds128(a + 32u * BATCH),
                    a3 = lds128(a + 48u * BATCH);
@@ -277,11 +343,12 @@ __device__ __forceinline__ void g2d_add(G2D* row, int k, float v) {
     atomicAdd(&row->f[k - 5], v);
 }
 
-// K4: one CTA per tile, TILE²/PPT threads, PPT pixels per thread. Warp w owns the compact
-// band of LR·PPT rows starting at LR·PPT·w (LR = 32/TILE lane rows); lane row r holds pixel
-// rows band + r + LR·k, k < PPT. Per splat the warp evaluates α for its pixels, skips the
-// splat if none uses it (ballot), otherwise accumulates the 15 sums over the thread's PPT
-// pixels, reduces them across the warp and issues one L2 atomic per value.
+// K4: one CTA per tile, TILE²/PPT threads, PPT pixels per thread. Warp w owns an 8-wide,
+// 4·PPT-tall pixel rectangle of the tile (lane l: column l % 8, rows l / 8 + 4k, k < PPT).
+// Per staged batch the warp filters the splats that can reach its rectangle (warp_filter),
+// then, per such splat in reverse order, evaluates α for its pixels, skips the splat if none
+// uses it (ballot), otherwise accumulates the 15 sums over the thread's PPT pixels, reduces
+// them across the warp and issues one L2 atomic per value.
 template <int TILE, int PPT>
 __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
@@ -290,19 +357,24 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, G2D* __restrict__ g2d,
     Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / PPT;
+  constexpr int NW = NT / 32;
   constexpr int BATCH = TILE * TILE;
-  constexpr int LR = 32 / TILE;
-  static_assert(NT % 32 == 0, "whole warps");
+  constexpr int SH = 4 * PPT;  // each warp: an 8-wide, SH-tall pixel rectangle
+  constexpr bool kFilter = TILE > 8;
+  static_assert(NT % 32 == 0 && TILE % SH == 0, "whole warps tiling the tile");
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
-  const int px = tx * TILE + lane % TILE;
-  const int py0 = ty * TILE + LR * PPT * warp + lane / TILE;
+  const int qx = tx * TILE + (warp % (TILE / 8)) * 8, qy = ty * TILE + (warp / (TILE / 8)) * SH;
+  const int px = qx + lane % 8;
+  const int py0 = qy + lane / 8;  // pixel k at row py0 + 4k
+  const float fx0 = (float)qx + 0.5f, fy0 = (float)qy + 0.5f;
   const uint2 range = ranges[tile];
   const int HW = cam.W * cam.H;
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   __shared__ uint32_t sid[BATCH];
+  __shared__ uint16_t wlist[kFilter ? NW : 1][kFilter ? BATCH : 1];
   __shared__ int s_maxlast;
 
   PixB s[PPT];
@@ -310,7 +382,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
   unsigned evals = 0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    const int py = py0 + LR * k;
+    const int py = py0 + 4 * k;
     const bool in = px < cam.W && py < cam.H;
     pixb_init(s[k], (float)px + 0.5f, (float)py + 0.5f, in, py * cam.W + px, HW, opt, T_final, n_contrib, median_pos,
               dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha);
@@ -342,8 +414,13 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       }
     }
     __syncthreads();
+    if (!__any_sync(0xffffffffu, start < mylast)) continue;  // the whole warp is past its pixels' lists
+    const int nsel = kFilter ? warp_filter(sbuf[0], sbuf[1], sbuf[3], cnt, lane, fx0, fx0 + 7.f, fy0,
+                                           fy0 + (float)(SH - 1), opt.log2_alpha_min, wlist[warp])
+                             : cnt;
     const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid);
-    for (int j = cnt - 1; j >= 0; --j) {
+    for (int i = nsel - 1; i >= 0; --i) {
+      const int j = kFilter ? (int)wlist[warp][i] : i;
       const int pos = start + j;
       if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
       const unsigned a = a_s0 + 16u * j;
@@ -365,7 +442,8 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
 #pragma unroll
       for (int k = 0; k < 16; ++k) g[k] = 0.f;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) bwd_accum(s[k], g, pa[k], act[k], a1, a2, opt);
+      for (int k = 0; k < PPT; ++k)  // a pixel row no lane uses contributes exact zeros: skip it
+        if (__any_sync(0xffffffffu, act[k])) bwd_accum(s[k], g, pa[k], act[k], a1, a2, opt);
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
         if (act[k] && pos == s[k].med) bwd_median(s[k], g, pa[k]);
@@ -408,7 +486,7 @@ void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
                        cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
   if (opt.tile == 16)
-    k_render_bwd<16, 4><<<grid, 64, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
+    k_render_bwd<16, 2><<<grid, 128, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
                                             dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
   else
     k_render_bwd<8, 2><<<grid, 32, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
