@@ -635,15 +635,16 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   gr.opac[i] = oo + d_o;
 }
 
-// K5b, fp32, one thread per Gaussian in id order: the visible ones that are not is_big
+// K5b, fp32, one thread per entry of the visible list (the ones that are not is_big)
 // tiles (the others are K5b64's).
 __global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
                                                         const uint32_t* __restrict__ touched,
+                                                        const uint32_t* __restrict__ vis, int64_t n_vis,
                                                         const G2D* __restrict__ g2d, DevGrads gr) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n) return;
-  const uint32_t nt = touched[i];
-  if (nt == 0u || is_big(nt, opt.tile)) return;  // culled / off-screen (zero gradient), or big
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_vis) return;
+  const uint32_t i = vis[p];  // over K1's visible list: every thread has work
+  if (is_big(touched[i], opt.tile)) return;  // K5b64's
   const float zero[3] = {0.f, 0.f, 0.f};
   geometry_backward<float>(g, i, cam, opt, g2d, gr, zero);
 }
@@ -815,7 +816,9 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
     }
 #undef RD_K5A
   }
-  k_preprocess_bwd<<<blocks, threads, 0, s>>>(g, cam, opt, tiles_touched, g2d, grads);
+  if (n_vis > 0)
+    k_preprocess_bwd<<<(unsigned)((n_vis + threads - 1) / threads), threads, 0, s>>>(g, cam, opt, tiles_touched,
+                                                                                     vis, n_vis, g2d, grads);
   if (n_big > 0)
     k_preprocess_bwd64<<<(unsigned)((n_big + 127) / 128), 128, 0, s>>>(g, cam, opt, big, n_big, g2d, grads);
 }
