@@ -233,21 +233,33 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   fwd_store(B, inB, pyB * cam.W + px, HW, opt, color, depth, normal, alpha_out, T_final, n_contrib, median_pos);
 }
 
-// Reduce-scatter of v[0..15] across the warp (16 shuffles instead of 75 for a plain
-// all-reduce of 15 values): level off=16,8,4,2 halves the set of values a lane keeps (the
-// half selected by that lane bit) and adds the partner's copy of it; a final xor-1 exchange
-// completes the sum. Returns Σ_lanes v[lane >> 1] (lanes l and l^1 hold the same value).
-__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
+// One butterfly level: lanes with bit `off` set keep the upper `half` of v[0..2·half) and
+// send the lower, the others the reverse; the kept half gets the partner's copy added.
+template <int HALF>
+__device__ __forceinline__ void butterfly(float* v, int lane, int off) {
+  const bool up = (lane & off) != 0;
 #pragma unroll
-  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int k = 0; k < half; ++k) {
-      const float send = up ? v[k] : v[k + half];
-      const float keep = up ? v[k + half] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
+  for (int k = 0; k < HALF; ++k) {
+    const float send = up ? v[k] : v[k + HALF];
+    const float keep = up ? v[k + HALF] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
   }
+}
+
+// Reduce-scatter of v[0..11] across the warp (13 shuffles instead of 60 for a plain
+// all-reduce of 12 values): levels off = 16 (12 → 6), 8 (6 → 3), 4 (3 + a zero pad → 2),
+// 2 (→ 1), then an xor-1 exchange completes the sum. Lanes l and l^1 then hold the sum of
+// value slot12(l) (≥ 12: the pad, nothing).
+__device__ __forceinline__ int slot12(int lane) {
+  const int t = 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
+  return t == 3 ? 12 : ((lane & 16) ? 6 : 0) + ((lane & 8) ? 3 : 0) + t;
+}
+__device__ __forceinline__ float reduce_scatter12(float (&v)[12], int lane) {
+  butterfly<6>(v, lane, 16);
+  butterfly<3>(v, lane, 8);
+  v[3] = 0.f;
+  butterfly<2>(v, lane, 4);
+  butterfly<1>(v, lane, 2);
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
@@ -301,7 +313,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // (the 3DGS derivation collapsed to one scalar, since g_C, g_N are per-pixel constants).
 // Branch-free: an inactive pair (past the pixel's list, or α < α_min) contributes exact
 // zeros (α masked to 0 ⇒ rinv = rcp(1) = 1, w = 0, dA = 0).
-__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[16], const PairAlpha& pa, bool act, const float4& a1,
+__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[12], const PairAlpha& pa, bool act, const float4& a1,
                                           const float4& a2, const DevOpt& opt) {
   const float a_raw = ex2_approx(pa.e);                  // o·exp(−½ΔᵀCΔ)
   const float al = act ? fminf(opt.alpha_max, a_raw) : 0.f;
@@ -327,12 +339,13 @@ __device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[16], const PairAlp
   g[11] = fmaf(w, s.gN2, g[11]);
 }
 
-// Median-depth sums g12 = Σ g_D, g13 = Σ g_D·dx, g14 = Σ g_D·dy for D = z_c + p·Δ (Eq.4,
-// PAPER:443-450), at the pixel's median splat only.
-__device__ __forceinline__ void bwd_median(const PixB& s, float (&g)[16], const PairAlpha& pa) {
-  g[12] += s.gD;
-  g[13] = fmaf(s.gD, pa.dx, g[13]);
-  g[14] = fmaf(s.gD, pa.dy, g[14]);
+// Median-depth sums Σ g_D, Σ g_D·dx, Σ g_D·dy (G2D f[7..9]) for D = z_c + p·Δ (Eq.4,
+// PAPER:443-450): one pixel per splat at most, so added directly (no warp reduction).
+__device__ __forceinline__ void bwd_median(const PixB& s, G2D* row, const PairAlpha& pa) {
+  if (s.gD == 0.f) return;
+  atomicAdd(&row->f[7], s.gD);
+  atomicAdd(&row->f[8], s.gD * pa.dx);
+  atomicAdd(&row->f[9], s.gD * pa.dy);
 }
 
 // Sum k of one splat into its G2D row (k < 5: fp64 moments, see rade_internal.cuh).
@@ -438,25 +451,25 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       const unsigned am = __ballot_sync(0xffffffffu, any);
       if (am == 0u) continue;  // warp-uniform: no pixel of this warp uses the splat
       const float4 a2 = lds128(a + 32u * BATCH);
-      float g[16];
+      float g[12];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) g[k] = 0.f;
+      for (int k = 0; k < 12; ++k) g[k] = 0.f;
 #pragma unroll
       for (int k = 0; k < PPT; ++k)  // a pixel row no lane uses contributes exact zeros: skip it
         if (__any_sync(0xffffffffu, act[k])) bwd_accum(s[k], g, pa[k], act[k], a1, a2, opt);
+      G2D* dst = g2d + lds32(a_id + 4u * j);
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
-        if (act[k] && pos == s[k].med) bwd_median(s[k], g, pa[k]);
-      G2D* dst = g2d + lds32(a_id + 4u * j);
+        if (act[k] && pos == s[k].med) bwd_median(s[k], dst, pa[k]);
       if (__popc(am) == 1) {  // one contributing thread in this warp: no reduction needed
         if (any) {
 #pragma unroll
-          for (int k = 0; k < 15; ++k) g2d_add(dst, k, g[k]);
+          for (int k = 0; k < 12; ++k) g2d_add(dst, k, g[k]);
         }
       } else {
-        const float v = reduce_scatter16(g, lane);
-        const int k = lane >> 1;
-        if ((lane & 1) == 0 && k < 15) g2d_add(dst, k, v);
+        const float v = reduce_scatter12(g, lane);
+        const int k = slot12(lane);
+        if ((lane & 1) == 0 && k < 12) g2d_add(dst, k, v);
       }
     }
   }
