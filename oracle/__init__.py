@@ -163,27 +163,31 @@ def render(scene, cam, opt, pixels=None, eps=DEFAULT_EPS, timing=None):
     flags = np.zeros(npix, np.uint8)
     nblend = np.zeros(npix, np.int32)
     mid = np.zeros(npix, np.int64)
+    dist = np.zeros(npix)
     lib().or_render(*sargs, _dp(cv), _dp(ov), ctypes.c_int64(npix),
                     None if pix is None else pix.ctypes.data, _dp(color), _dp(depth), _dp(normal),
-                    _dp(alpha), flags.ctypes.data, nblend.ctypes.data, mid.ctypes.data,
+                    _dp(alpha), flags.ctypes.data, nblend.ctypes.data, mid.ctypes.data, _dp(dist),
                     None if timing is None else _dp(timing))
     shape = (H, W) if pixels is None else (npix,)
     return dict(color=color.reshape((3,) + shape), depth=depth.reshape(shape), normal=normal.reshape((3,) + shape),
                 alpha=alpha.reshape(shape), flags=flags.reshape(shape), nblend=nblend.reshape(shape),
-                median_id=mid.reshape(shape))
+                median_id=mid.reshape(shape), distortion=dist.reshape(shape))
 
 
 def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS, timing=None):
-    """Exact dL/dθ for the listed Gaussians, L = Σ_px cot·(C, D, N, A). Returns [len(gids), 59]
-    (μ 0..2, s 3..5, q 6..9, o 10, sh 11 + coeff*3 + ch)."""
+    """Exact dL/dθ for the listed Gaussians, L = Σ_px cot·(C, D, N, A[, L_d]) (cot["distortion"]
+    optional; ω detached in L_d, S21). Returns [len(gids), 59] (μ 0..2, s 3..5, q 6..9, o 10,
+    sh 11 + coeff*3 + ch)."""
     keep, sargs = _scene_args(scene)
     cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt, eps)
     W, H = cam.width, cam.height
-    c = np.zeros((8, H, W), np.float64)
+    c = np.zeros((9, H, W), np.float64)
     c[0:3] = cot["color"]
     c[3] = cot["depth"]
     c[4:7] = cot["normal"]
     c[7] = cot["alpha"]
+    if cot.get("distortion") is not None:
+        c[8] = cot["distortion"]
     c = np.ascontiguousarray(c)
     gids = np.ascontiguousarray(gids, np.int64)
     out = np.zeros((gids.shape[0], NPARAM), np.float64)

@@ -27,6 +27,8 @@
  *                  normal map N = Σ ω_i n_i (unnormalised)        PAPER:30 (S10)
  *                  median depth = d of the first blended splat at
  *                  which T crosses median_T                       PAPER:30 (S9)
+ *                  depth distortion L_d = Σ_i Σ_j ω_i ω_j (d_i − d_j)² over the
+ *                  blended splats, ω detached in the gradient     PAPER:635-639 (S21)
  *   gradients      forward-mode dual numbers through all of the above (exact derivative of
  *                  this definition; independent of the GPU's hand-derived backward).
  *
@@ -333,7 +335,21 @@ struct Pix {
   int64_t median_id = -1;
   uint8_t flags = 0;
   double median_ndotx = 1.0;
+  std::vector<double> wl;  // ω_i of the blended splats (values only: detached, S21)
+  std::vector<S> dl;       // their per-pixel depths d_i
 };
+
+// Depth distortion: the plain double sum over the blended splats.
+template <class S>
+S distortion(const Pix<S>& px) {
+  S L = S(0.0);
+  for (size_t i = 0; i < px.dl.size(); ++i)
+    for (size_t j = 0; j < px.dl.size(); ++j) {
+      S dd = px.dl[i] - px.dl[j];
+      L = L + (px.wl[i] * px.wl[j]) * (dd * dd);
+    }
+  return L;
+}
 template <class S>
 void pix_init(Pix<S>& px) {
   px.T = S(1.0);
@@ -347,6 +363,9 @@ void promote(const Pix<SG>& a, Pix<SS>& b) {
   b.D = SS(val(a.D));
   b.Dset = a.Dset; b.done = a.done; b.nblend = a.nblend; b.median_id = a.median_id; b.flags = a.flags;
   b.median_ndotx = a.median_ndotx;
+  b.wl = a.wl;
+  b.dl.clear();
+  for (const auto& d : a.dl) b.dl.push_back(SS(val(d)));
 }
 
 // One splat against one pixel, front to back (Eq.3; readings S1, S8, S9).
@@ -372,6 +391,8 @@ bool blend(Pix<SS>& px, const Splat<SG>& s, double u, double v, const Opt& opt) 
   SG d = (s.z / s.tc) * tstar;  // d = cosθ_c t* = (z_c/t_c) t*
   SS w = alpha * px.T;
   for (int k = 0; k < 3; ++k) { px.C[k] += w * s.rgb[k]; px.N[k] += w * s.n[k]; }
+  px.wl.push_back(val(w));
+  px.dl.push_back(SS(0.0) + d);
   if (!px.Dset && val(px.T) > opt.median_T && val(Tn) <= opt.median_T) {
     px.D = SS(0.0) + d;
     px.Dset = true;
@@ -541,11 +562,12 @@ int or_splat_eval(int64_t n, const double* means, const double* scales, const do
  *   color[3*npix] (color[c*npix+k]), depth[npix] (median, 0 = none), normal[3*npix],
  *   alpha[npix] = 1 − T_final, flags[npix] (bit0 F1 α-cutoff, bit1 F2 α-clamp, bit2 F3
  *   T-stop, bit3 F4 median crossing, bit4 F5 grazing median splat), nblend[npix] (number
- *   of blended splats), median_id[npix] (Gaussian id of the median splat or −1). */
+ *   of blended splats), median_id[npix] (Gaussian id of the median splat or −1),
+ *   distortion[npix] = L_d of the pixel (S21). */
 int or_render(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
               const double* sh, int sh_coeffs, const double* camv, const double* optv, int64_t npix,
               const int64_t* pix, double* color, double* depth, double* normal, double* alpha, uint8_t* flags,
-              int32_t* nblend, int64_t* median_id, double* timing) {
+              int32_t* nblend, int64_t* median_id, double* distortion_out, double* timing) {
   SceneIn sc = make_scene(n, means, scales, rot, opac, sh, sh_coeffs);
   Cam cam = make_cam(camv);
   Opt opt = make_opt(optv);
@@ -571,6 +593,7 @@ int or_render(int64_t n, const double* means, const double* scales, const double
     flags[k] = px.flags;
     nblend[k] = px.nblend;
     median_id[k] = px.median_id;
+    distortion_out[k] = distortion(px);
   }
   if (timing) {  // [0] project + sort seconds, [1] per-pixel loop seconds, [2] surviving Gaussians
     timing[0] = t1 - t0;
@@ -580,9 +603,10 @@ int or_render(int64_t n, const double* means, const double* scales, const double
   return 0;
 }
 
-/* or_grad: exact gradient of L = Σ_px g·(C, D, N, A) w.r.t. the 59 parameters of each
- * listed Gaussian, by forward-mode dual numbers through or_render's definition.
- *   cot[8][H][W] planar: dL/dC (3), dL/dD, dL/dN (3), dL/dA.
+/* or_grad: exact gradient of L = Σ_px g·(C, D, N, A, L_d) w.r.t. the 59 parameters of each
+ * listed Gaussian, by forward-mode dual numbers through or_render's definition (ω detached
+ * in L_d, S21).
+ *   cot[9][H][W] planar: dL/dC (3), dL/dD, dL/dN (3), dL/dA, dL/dL_d.
  *   out[k*59 + j]: j = μ 0..2, s 3..5, q(w,x,y,z) 6..9, o 10, sh 11 + coeff*3 + channel.
  *   culled Gaussians get zero. */
 int or_grad(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
@@ -633,6 +657,7 @@ int or_grad(int64_t n, const double* means, const double* scales, const double* 
           for (int64_t s = pos + 1; s < ns; ++s)
             if (!blend(px, pr.splats[s], u, v, opt)) break;
         Dual L = px.D * cot[3 * npx + lin] + (1.0 - px.T) * cot[7 * npx + lin];
+        if (cot[8 * npx + lin] != 0.0) L = L + distortion(px) * cot[8 * npx + lin];
         for (int c = 0; c < 3; ++c)
           L = L + (px.C[c] + px.T * opt.bg[c]) * cot[c * npx + lin] + px.N[c] * cot[(4 + c) * npx + lin];
         for (int j = 0; j < NP; ++j) acc[j] += L.d[j];

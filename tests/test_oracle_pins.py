@@ -511,3 +511,84 @@ def test_guard_band_cull(O, axis):
             assert out["alpha"].max() > 0.05  # σ ≈ 20 px: its footprint reaches into the image
         else:
             assert out["alpha"].max() == 0.0
+
+
+# ----------------------------------------------------------------------------- L_d
+
+def _two_layers(o=0.9):
+    """Fronto-parallel flat splats on the principal axis (q = p = 0 ⇒ d = z_c at every pixel),
+    depths 2 and 3; at the centre pixel α = o exactly for both."""
+    front = one_gaussian([0, 0, 2.0], [0.15, 0.15, 1e-3], opacity=o)
+    back = one_gaussian([0, 0, 3.0], [0.6, 0.6, 1e-3], opacity=o)
+    return concat(front, back)
+
+
+def _two_layer_alphas(r2):
+    """Analytic α of the two isotropic screen Gaussians: σ² = (f s / z)² + h (S5), with the
+    fp32 values the renderer receives."""
+    h = float(np.float32(0.3))
+    o, s1, s2 = (float(np.float32(x)) for x in (0.9, 0.15, 0.6))
+    a1 = o * np.exp(-0.5 * r2 / ((64 * s1 / 2.0) ** 2 + h))
+    a2 = o * np.exp(-0.5 * r2 / ((64 * s2 / 3.0) ** 2 + h))
+    return a1, a2
+
+
+def test_depth_distortion_two_layers_closed_form(O):
+    """L_d = Σ_i Σ_j ω_i ω_j (d_i − d_j)² with ω = (α₁, α₂(1 − α₁)) and
+    d = (2, 3): 2·ω₁·ω₂·1² (the double sum counts (i, j) and (j, i)) at every pixel, with
+    the α of the analytic isotropic screen Gaussians."""
+    cam = sg.camera_identity(64, 64, 64)
+    r = O.render(_two_layers(), cam, OPT)
+    ii, jj = np.meshgrid(np.arange(64) + 0.5, np.arange(64) + 0.5)
+    r2 = (ii - 32) ** 2 + (jj - 32) ** 2
+    a1, a2 = _two_layer_alphas(r2)
+    a1 = np.where(a1 >= 1 / 255, a1, 0.0)
+    a2 = np.where(a2 >= 1 / 255, a2, 0.0)
+    expect = 2 * a1 * (1 - a1) * a2 * 1.0
+    np.testing.assert_allclose(r["distortion"], expect, rtol=1e-9, atol=1e-14)
+    assert expect[32, 32] > 0.17
+
+
+def test_depth_distortion_gradient_detached_weights(O):
+    """Reading S21 (ω detached): dL_d/dμ_z of the back layer at a pixel is
+    ∂L_d/∂d₂ = 4 ω₂ (A d₂ − D₁) with A = Σω, D₁ = Σωd, since d₂ = z_c moves one-for-one
+    with μ_z (q = p = 0, centre on the axis) and the weights carry no derivative."""
+    cam = sg.camera_identity(64, 64, 64)
+    sc = _two_layers()
+    zero = {"color": np.zeros((3, 64, 64)), "depth": np.zeros((64, 64)), "normal": np.zeros((3, 64, 64)),
+            "alpha": np.zeros((64, 64)), "distortion": np.zeros((64, 64))}
+    zero["distortion"][32, 32] = 1.0
+    G = O.grad(sc, cam, OPT, zero, [0, 1])
+    a1, a2 = _two_layer_alphas(0.5)
+    w1, w2, d1, d2 = a1, a2 * (1 - a1), 2.0, 3.0
+    A, D1 = w1 + w2, w1 * d1 + w2 * d2
+    assert G[1, 2] == pytest.approx(4 * w2 * (A * d2 - D1), rel=1e-9)
+    assert G[0, 2] == pytest.approx(4 * w1 * (A * d1 - D1), rel=1e-9)
+    assert abs(G[1, 10]) < 1e-12  # opacity enters only through ω: detached
+
+
+def test_depth_distortion_one_pass_identity(O):
+    """Σ_ij ω_i ω_j (d_i − d_j)² = 2 (A·D₂ − D₁²) (expansion of the square), and
+    L_d ≥ 0: checked on a dense random scene through per-pixel (ω, d) lists rebuilt from the
+    oracle's own per-splat evaluation."""
+    sc = dense_scene(12, 120)
+    cam = sg.camera_identity(32, 32, 32)
+    r = O.render(sc, cam, OPT)
+    assert (r["distortion"] >= -1e-12).all() and r["distortion"].max() > 1e-3
+    pg = O.project(sc, cam, OPT)
+    order = [i for i in np.lexsort((np.arange(sc.n), pg[:, 1])) if pg[i, 0] == 1]
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        y, x = rng.integers(0, 32, 2)
+        T, A, D1, D2 = 1.0, 0.0, 0.0, 0.0
+        for gid in order:
+            ev = O.splat_eval(sc, cam, OPT, int(gid), [[x + 0.5, y + 0.5]])
+            a = min(0.99, ev[0, 0])
+            if a < 1 / 255:
+                continue
+            if T * (1 - a) < 1e-4:
+                break
+            w = a * T
+            A, D1, D2 = A + w, D1 + w * ev[0, 2], D2 + w * ev[0, 2] ** 2
+            T *= 1 - a
+        assert r["distortion"][y, x] == pytest.approx(2 * (A * D2 - D1 * D1), rel=1e-7, abs=1e-10)
