@@ -171,6 +171,31 @@ rd_status rd_bin(rd_view* view, int64_t* n_duplicates_out, rd_stream stream);
  * color[3][H][W], depth[H][W], normal[3][H][W], alpha[H][W] (device, fp32). */
 rd_status rd_render_fwd(rd_view* view, float* color, float* depth, float* normal, float* alpha, rd_stream stream);
 
+/* Stage 3 with the optional depth-distortion map (NEXT-1, reading S21):
+ * distortion[H][W] = L_d = Σ_i Σ_j ω_i ω_j (d_i − d_j)² over the pixel's blended splats
+ * (ω = blend weights, d = the per-pixel depth of Eq.15). Any pointer may be NULL; when
+ * `distortion` is non-NULL the view also keeps the per-pixel state its backward needs. */
+typedef struct rd_fwd_maps {
+  float* color;       /* [3][H][W] */
+  float* depth;       /* [H][W] median depth */
+  float* normal;      /* [3][H][W] */
+  float* alpha;       /* [H][W] */
+  float* distortion;  /* [H][W] L_d, or NULL (then no distortion state is kept) */
+} rd_fwd_maps;
+rd_status rd_render_fwd_ex(rd_view* view, const rd_fwd_maps* maps, rd_stream stream);
+
+/* Cotangents of rd_fwd_maps (any may be NULL = zero). dL_ddistortion needs a forward that
+ * produced the distortion map (else RD_ERR_STATE); its gradient flows through d only — the
+ * weights ω are detached (S21): ∂L_d/∂d_k = 4 ω_k (A d_k − D₁), A = Σω, D₁ = Σωd. */
+typedef struct rd_bwd_cotangents {
+  const float* dL_dcolor;
+  const float* dL_ddepth;
+  const float* dL_dnormal;
+  const float* dL_dalpha;
+  const float* dL_ddistortion;
+} rd_bwd_cotangents;
+rd_status rd_blend_bwd_ex(rd_view* view, const rd_bwd_cotangents* cot, rd_stream stream);
+
 /* Stage 4 (K4 + K5). Cotangents dL/d(color, depth, normal, alpha) in the output layouts
  * (any may be NULL = zero). `g` must be the same Gaussians given to rd_preprocess.
  * Gradients are accumulated into `grads` (all five pointers required).

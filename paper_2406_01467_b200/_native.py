@@ -44,6 +44,16 @@ class RdGrads(ctypes.Structure):
                 ("opacities", ctypes.c_void_p), ("sh", ctypes.c_void_p)]
 
 
+class RdFwdMaps(ctypes.Structure):
+    _fields_ = [("color", ctypes.c_void_p), ("depth", ctypes.c_void_p), ("normal", ctypes.c_void_p),
+                ("alpha", ctypes.c_void_p), ("distortion", ctypes.c_void_p)]
+
+
+class RdBwdCotangents(ctypes.Structure):
+    _fields_ = [("dL_dcolor", ctypes.c_void_p), ("dL_ddepth", ctypes.c_void_p), ("dL_dnormal", ctypes.c_void_p),
+                ("dL_dalpha", ctypes.c_void_p), ("dL_ddistortion", ctypes.c_void_p)]
+
+
 class RdStats(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("n_duplicates", ctypes.c_int64), ("tiles_x", ctypes.c_int32),
                 ("tiles_y", ctypes.c_int32), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
@@ -78,6 +88,8 @@ SIGNATURES = {
     "rd_render_bwd": ([_VP, ctypes.POINTER(RdGaussians), _VP, _VP, _VP, _VP, ctypes.POINTER(RdGrads), _VP],
                       ctypes.c_int),
     "rd_blend_bwd": ([_VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
+    "rd_render_fwd_ex": ([_VP, ctypes.POINTER(RdFwdMaps), _VP], ctypes.c_int),
+    "rd_blend_bwd_ex": ([_VP, ctypes.POINTER(RdBwdCotangents), _VP], ctypes.c_int),
     "rd_preprocess_bwd": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
     "rd_view_stats": ([_VP, ctypes.POINTER(RdStats)], ctypes.c_int),
     "rd_set_profiling": ([_VP, ctypes.c_int32], ctypes.c_int),

@@ -78,6 +78,8 @@ struct rd_view {
   int dsel = 0, tsel = 0;  // CUB DoubleBuffer selectors of the depth and tile sorts
   int64_t n_vis = 0, n_big = 0;
   bool g2d_dirty = false;  // the G2D rows hold a previous rd_blend_bwd's sums (K1 zeroes them)
+  bool dist_fwd = false;   // the last forward produced the distortion map and its K4 state
+  Buf dist_d0, dist_D1;
   uint32_t* host_M = nullptr;  // pinned: [0] M, [1] visible Gaussians, [2] big ones
   Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp, vis, big, nvis;
   Buf tkeys0, tkeys1, vals0, vals1;
@@ -214,7 +216,7 @@ rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
                 &v->didx1,  &v->tmp,    &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->vis, &v->big, &v->nvis};
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->vis, &v->big, &v->nvis, &v->dist_d0, &v->dist_D1};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
@@ -382,20 +384,28 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   return RD_OK;
 }
 
-rd_status rd_render_fwd(rd_view* v, float* color, float* depth, float* normal, float* alpha, rd_stream stream) {
+rd_status rd_render_fwd_ex(rd_view* v, const rd_fwd_maps* maps, rd_stream stream) {
   g_err.clear();
-  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (!v || !maps) return fail(RD_ERR_INVALID_ARGUMENT, "view / maps is NULL");
   if (v->stage < 2) return fail(RD_ERR_STATE, "rd_render_fwd before rd_bin");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t HW = (size_t)v->cam.W * v->cam.H;
   RD_ENSURE(v->T_final, HW * sizeof(float), s);
   RD_ENSURE(v->n_contrib, HW * sizeof(int32_t), s);
   RD_ENSURE(v->median_pos, HW * sizeof(int32_t), s);
+  DistIO dio{nullptr, nullptr, nullptr, nullptr};
+  v->dist_fwd = maps->distortion != nullptr;
+  if (v->dist_fwd) {
+    RD_ENSURE(v->dist_d0, HW * sizeof(float), s);
+    RD_ENSURE(v->dist_D1, HW * sizeof(float), s);
+    dio = DistIO{maps->distortion, (float*)v->dist_d0.ptr, (float*)v->dist_D1.ptr, nullptr};
+  }
   const uint32_t* ids = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
   v->begin(s);
   launch_render_fwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
-                    (const Record*)v->rec.ptr, color, depth, normal, alpha, (float*)v->T_final.ptr,
-                    (int32_t*)v->n_contrib.ptr, (int32_t*)v->median_pos.ptr, v->ctr(), s);
+                    (const Record*)v->rec.ptr, maps->color, maps->depth, maps->normal, maps->alpha,
+                    (float*)v->T_final.ptr, (int32_t*)v->n_contrib.ptr, (int32_t*)v->median_pos.ptr, dio, v->ctr(),
+                    s);
   RD_CHECK_LAUNCH("render_fwd");
   v->end(K_FWD, s);
   v->acc_views += 1;
@@ -403,11 +413,29 @@ rd_status rd_render_fwd(rd_view* v, float* color, float* depth, float* normal, f
   return RD_OK;
 }
 
+rd_status rd_render_fwd(rd_view* v, float* color, float* depth, float* normal, float* alpha, rd_stream stream) {
+  const rd_fwd_maps maps{color, depth, normal, alpha, nullptr};
+  return rd_render_fwd_ex(v, &maps, stream);
+}
+
 rd_status rd_blend_bwd(rd_view* v, const float* dL_dcolor, const float* dL_ddepth, const float* dL_dnormal,
                        const float* dL_dalpha, rd_stream stream) {
+  const rd_bwd_cotangents cot{dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, nullptr};
+  return rd_blend_bwd_ex(v, &cot, stream);
+}
+
+rd_status rd_blend_bwd_ex(rd_view* v, const rd_bwd_cotangents* cot, rd_stream stream) {
   g_err.clear();
-  if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
+  if (!v || !cot) return fail(RD_ERR_INVALID_ARGUMENT, "view / cotangents is NULL");
   if (v->stage < 3) return fail(RD_ERR_STATE, "rd_blend_bwd before rd_render_fwd");
+  if (cot->dL_ddistortion && !v->dist_fwd)
+    return fail(RD_ERR_STATE, "distortion cotangent given, but the forward produced no distortion map");
+  const float* dL_dcolor = cot->dL_dcolor;
+  const float* dL_ddepth = cot->dL_ddepth;
+  const float* dL_dnormal = cot->dL_dnormal;
+  const float* dL_dalpha = cot->dL_dalpha;
+  DistIO dio{nullptr, nullptr, nullptr, nullptr};
+  if (cot->dL_ddistortion) dio = DistIO{nullptr, (float*)v->dist_d0.ptr, (float*)v->dist_D1.ptr, cot->dL_ddistortion};
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t* ids = (const uint32_t*)(v->tsel ? v->vals1.ptr : v->vals0.ptr);
   v->begin(s);
@@ -416,7 +444,7 @@ rd_status rd_blend_bwd(rd_view* v, const float* dL_dcolor, const float* dL_ddept
   v->g2d_dirty = true;
   launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
-                    (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,
+                    (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, dio,
                     (G2D*)v->g2d.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("render_bwd");
   v->end(K_BWD, s);

@@ -148,6 +148,16 @@ __device__ __forceinline__ PairAlpha pair_power(const float4& r0, float g22, flo
   return pa;
 }
 
+// Depth distortion (reading S21) plumbing: K3 writes the L_d map (dist, may be NULL) and the
+// per-pixel state d0 (first blended depth) and D1 = Σω(d − d0) when d0 != NULL; K4 adds the
+// L_d gradient when dL_ddist != NULL (then d0/D1 must hold K3's values).
+struct DistIO {
+  float* dist;
+  float* d0;
+  float* D1;
+  const float* dL_ddist;
+};
+
 // ------------------------------------------------------------------ launchers (host)
 // Profiling counters (nullable): [0] pairs evaluated by K3, [1] pairs blended by K3,
 // [2] pairs evaluated by K4, [3] visible Gaussians (K1).
@@ -190,12 +200,12 @@ void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec
                    cudaStream_t s);
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal,
-                       float* alpha, float* T_final, int32_t* n_contrib, int32_t* median_pos, Counter* counters,
-                       cudaStream_t s);
+                       float* alpha, float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
+                       Counter* counters, cudaStream_t s);
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
-                       const float* dL_dnormal, const float* dL_dalpha, G2D* g2d, Counter* counters,
-                       cudaStream_t s);
+                       const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio, G2D* g2d,
+                       Counter* counters, cudaStream_t s);
 
 }  // namespace rade

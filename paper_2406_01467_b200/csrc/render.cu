@@ -28,6 +28,7 @@ namespace {
 struct PixF {  // forward state of one pixel
   float px, py;
   float T, C0, C1, C2, N0, N1, N2, D;
+  float d0, D1, D2;  // depth distortion (S21): Σω(d − d0), Σω(d − d0)², d0 = first blended depth
   int last, med;
   unsigned n_eval, n_blend;
   bool done;
@@ -38,14 +39,17 @@ __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool insi
   s.py = py;
   s.T = 1.f;
   s.C0 = s.C1 = s.C2 = s.N0 = s.N1 = s.N2 = s.D = 0.f;
+  s.d0 = s.D1 = s.D2 = 0.f;
   s.last = 0;
   s.med = -1;
   s.n_eval = s.n_blend = 0;
   s.done = !inside;
 }
 
-// One (pixel, splat) step of Eq.3 with the median-depth selection of reading S9.
-template <bool PROF>
+// One (pixel, splat) step of Eq.3 with the median-depth selection of reading S9, and with
+// DIST the depth-distortion sums of reading S21 (centred on the first blended depth d0, so
+// L_d = 2(A·D2 − D1²) loses no digits to cancellation: it is shift invariant).
+template <bool PROF, bool DIST>
 __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4& a2,
                                          const float4& a3, float2 ulo, int pos, const DevOpt& opt) {
   const PairAlpha pa = pair_power(a0, a1.x, a1.y, ulo, s.px, s.py, opt.log2_alpha_min);
@@ -68,17 +72,31 @@ __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4
     s.D = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
     s.med = pos;
   }
+  if (DIST) {  // d of Eq.15 for this splat (the median channel's depth)
+    const float d = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
+    if (s.last == 0) s.d0 = d;
+    const float e = d - s.d0;
+    s.D1 = fmaf(w, e, s.D1);
+    s.D2 = fmaf(w * e, e, s.D2);
+  }
   s.T = Tn;
   s.last = pos + 1;
   if (PROF) ++s.n_blend;
 }
 
+template <bool DIST>
 __device__ __forceinline__ void fwd_store(const PixF& s, bool inside, int pix, int HW, const DevOpt& opt,
                                           float* __restrict__ color, float* __restrict__ depth,
                                           float* __restrict__ normal, float* __restrict__ alpha_out,
                                           float* __restrict__ T_final, int32_t* __restrict__ n_contrib,
-                                          int32_t* __restrict__ median_pos) {
+                                          int32_t* __restrict__ median_pos, const DistIO& dio) {
   if (!inside) return;
+  if (DIST) {  // L_d = Σ_ij ω_i ω_j (d_i − d_j)² = 2(A·D2 − D1²), A = Σω = 1 − T
+    const float A = 1.f - s.T;
+    if (dio.dist) dio.dist[pix] = fmaxf(2.f * fmaf(A, s.D2, -s.D1 * s.D1), 0.f);
+    dio.d0[pix] = s.d0;
+    dio.D1[pix] = s.D1;
+  }
   if (color) {
     color[pix] = __fmaf_rn(s.T, opt.bg[0], s.C0);
     color[HW + pix] = __fmaf_rn(s.T, opt.bg[1], s.C1);
@@ -155,7 +173,7 @@ __device__ __forceinline__ int warp_filter(const float4* s0, const float4* s1, c
 // K3: one CTA per TILE×TILE tile, TILE²/2 threads; warp w owns the 8×8 quadrant w of the
 // tile (lane l: column l % 8, rows l / 8 and l / 8 + 4). Per staged batch each warp first
 // filters the batch down to the splats that reach its quadrant, then blends those.
-template <int TILE, bool PROF>
+template <int TILE, bool PROF, bool DIST>
 __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOpt opt, int tiles_x,
                                                                 const uint2* __restrict__ ranges,
                                                                 const uint32_t* __restrict__ ids,
@@ -166,7 +184,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                                                 float* __restrict__ T_final,
                                                                 int32_t* __restrict__ n_contrib,
                                                                 int32_t* __restrict__ median_pos,
-                                                                Counter* __restrict__ counters) {
+                                                                DistIO dio, Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / 2;  // threads
   constexpr int NW = NT / 32;          // warps = 8×8 quadrants
   constexpr int BATCH = TILE * TILE;   // splats staged per round
@@ -220,8 +238,8 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH), a2 = lds128(a + 32u * BATCH),
                    a3 = lds128(a + 48u * BATCH);
       const float2 ulo = uv_lo(a3.w);
-      if (!A.done) fwd_step<PROF>(A, a0, a1, a2, a3, ulo, base + j, opt);
-      if (!B.done) fwd_step<PROF>(B, a0, a1, a2, a3, ulo, base + j, opt);
+      if (!A.done) fwd_step<PROF, DIST>(A, a0, a1, a2, a3, ulo, base + j, opt);
+      if (!B.done) fwd_step<PROF, DIST>(B, a0, a1, a2, a3, ulo, base + j, opt);
     }
   }
   if (PROF) {
@@ -229,8 +247,10 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
     warp_count(counters + 1, A.n_blend + B.n_blend);
   }
   const int HW = cam.W * cam.H;
-  fwd_store(A, inA, pyA * cam.W + px, HW, opt, color, depth, normal, alpha_out, T_final, n_contrib, median_pos);
-  fwd_store(B, inB, pyB * cam.W + px, HW, opt, color, depth, normal, alpha_out, T_final, n_contrib, median_pos);
+  fwd_store<DIST>(A, inA, pyA * cam.W + px, HW, opt, color, depth, normal, alpha_out, T_final, n_contrib,
+                  median_pos, dio);
+  fwd_store<DIST>(B, inB, pyB * cam.W + px, HW, opt, color, depth, normal, alpha_out, T_final, n_contrib,
+                  median_pos, dio);
 }
 
 // One butterfly level: lanes with bit `off` set keep the upper `half` of v[0..2·half) and
@@ -254,6 +274,14 @@ __device__ __forceinline__ int slot12(int lane) {
   const int t = 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
   return t == 3 ? 12 : ((lane & 16) ? 6 : 0) + ((lane & 8) ? 3 : 0) + t;
 }
+// Reduce-scatter of v[0..15] (16 shuffles): lanes l, l^1 end with Σ_lanes v[l >> 1].
+__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
+  butterfly<8>(v, lane, 16);
+  butterfly<4>(v, lane, 8);
+  butterfly<2>(v, lane, 4);
+  butterfly<1>(v, lane, 2);
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
 __device__ __forceinline__ float reduce_scatter12(float (&v)[12], int lane) {
   butterfly<6>(v, lane, 16);
   butterfly<3>(v, lane, 8);
@@ -267,6 +295,7 @@ struct PixB {  // backward state of one pixel
   float px, py;
   float T, TFa, Dsuf;
   float gC0, gC1, gC2, gN0, gN1, gN2, gD;
+  float gL, d0, D1, A;  // depth distortion (S21): 4·dL/dL_d, K3's d0 and D1, A = Σω
   int last, med;
 };
 
@@ -275,13 +304,15 @@ __device__ __forceinline__ void pixb_init(PixB& s, float px, float py, bool insi
                                           const int32_t* __restrict__ n_contrib,
                                           const int32_t* __restrict__ median_pos,
                                           const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
-                                          const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha) {
+                                          const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha,
+                                          const DistIO& dio) {
   s.px = px;
   s.py = py;
   s.T = 1.f;
   s.last = 0;
   s.med = -1;
   s.gC0 = s.gC1 = s.gC2 = s.gN0 = s.gN1 = s.gN2 = s.gD = 0.f;
+  s.gL = s.d0 = s.D1 = s.A = 0.f;
   float gA = 0.f;
   if (inside) {
     s.last = n_contrib[pix];
@@ -291,6 +322,12 @@ __device__ __forceinline__ void pixb_init(PixB& s, float px, float py, bool insi
     if (dL_dnormal) { s.gN0 = dL_dnormal[pix]; s.gN1 = dL_dnormal[HW + pix]; s.gN2 = dL_dnormal[2 * HW + pix]; }
     if (dL_ddepth) s.gD = dL_ddepth[pix];
     if (dL_dalpha) gA = dL_dalpha[pix];
+    if (dio.dL_ddist) {
+      s.gL = 4.f * dio.dL_ddist[pix];
+      s.d0 = dio.d0[pix];
+      s.D1 = dio.D1[pix];
+      s.A = 1.f - s.T;
+    }
   }
   // ∂L/∂α_i gets T_final/(1 − α_i)·(g_A − bg·g_C) from A = 1 − T_final and C += T_final·bg
   s.TFa = s.T * (gA - (opt.bg[0] * s.gC0 + opt.bg[1] * s.gC1 + opt.bg[2] * s.gC2));
@@ -313,8 +350,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // (the 3DGS derivation collapsed to one scalar, since g_C, g_N are per-pixel constants).
 // Branch-free: an inactive pair (past the pixel's list, or α < α_min) contributes exact
 // zeros (α masked to 0 ⇒ rinv = rcp(1) = 1, w = 0, dA = 0).
-__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[12], const PairAlpha& pa, bool act, const float4& a1,
-                                          const float4& a2, const DevOpt& opt) {
+template <bool DIST, int NG>
+__device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[NG], const PairAlpha& pa, bool act, const float4& a1,
+                                          const float4& a2, const float4& a3, const DevOpt& opt) {
   const float a_raw = ex2_approx(pa.e);                  // o·exp(−½ΔᵀCΔ)
   const float al = act ? fminf(opt.alpha_max, a_raw) : 0.f;
   const float rinv = rcp_approx(1.f - al);               // α ≤ α_max < 1; exact 1 when masked
@@ -337,6 +375,13 @@ __device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[12], const PairAlp
   g[9] = fmaf(w, s.gN0, g[9]);
   g[10] = fmaf(w, s.gN1, g[10]);
   g[11] = fmaf(w, s.gN2, g[11]);
+  if constexpr (DIST) {  // ∂L_d/∂d = 4 ω (A (d − d0) − D1), ω detached (S21); into the Eq.15 sums
+    const float d = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
+    const float gd = s.gL * w * fmaf(s.A, d - s.d0, -s.D1);
+    g[12] += gd;
+    g[13] = fmaf(gd, pa.dx, g[13]);
+    g[14] = fmaf(gd, pa.dy, g[14]);
+  }
 }
 
 // Median-depth sums Σ g_D, Σ g_D·dx, Σ g_D·dy (G2D f[7..9]) for D = z_c + p·Δ (Eq.4,
@@ -362,12 +407,12 @@ __device__ __forceinline__ void g2d_add(G2D* row, int k, float v) {
 // then, per such splat in reverse order, evaluates α for its pixels, skips the splat if none
 // uses it (ballot), otherwise accumulates the 15 sums over the thread's PPT pixels, reduces
 // them across the warp and issues one L2 atomic per value.
-template <int TILE, int PPT>
+template <int TILE, int PPT, bool DIST>
 __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
     const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
-    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, G2D* __restrict__ g2d,
+    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, DistIO dio, G2D* __restrict__ g2d,
     Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / PPT;
   constexpr int NW = NT / 32;
@@ -398,7 +443,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     const int py = py0 + 4 * k;
     const bool in = px < cam.W && py < cam.H;
     pixb_init(s[k], (float)px + 0.5f, (float)py + 0.5f, in, py * cam.W + px, HW, opt, T_final, n_contrib, median_pos,
-              dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha);
+              dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, dio);
     mylast = max(mylast, s[k].last);
     evals += (unsigned)s[k].last;
   }
@@ -451,12 +496,14 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       const unsigned am = __ballot_sync(0xffffffffu, any);
       if (am == 0u) continue;  // warp-uniform: no pixel of this warp uses the splat
       const float4 a2 = lds128(a + 32u * BATCH);
-      float g[12];
+      const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;  // (z_c, p0, p1, ·) for d of Eq.15
+      constexpr int NG = DIST ? 16 : 12;  // + Σ gd, Σ gd·dx, Σ gd·dy of the distortion
+      float g[NG];
 #pragma unroll
-      for (int k = 0; k < 12; ++k) g[k] = 0.f;
+      for (int k = 0; k < NG; ++k) g[k] = 0.f;
 #pragma unroll
       for (int k = 0; k < PPT; ++k)  // a pixel row no lane uses contributes exact zeros: skip it
-        if (__any_sync(0xffffffffu, act[k])) bwd_accum(s[k], g, pa[k], act[k], a1, a2, opt);
+        if (__any_sync(0xffffffffu, act[k])) bwd_accum<DIST>(s[k], g, pa[k], act[k], a1, a2, a3, opt);
       G2D* dst = g2d + lds32(a_id + 4u * j);
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
@@ -464,8 +511,12 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       if (__popc(am) == 1) {  // one contributing thread in this warp: no reduction needed
         if (any) {
 #pragma unroll
-          for (int k = 0; k < 12; ++k) g2d_add(dst, k, g[k]);
+          for (int k = 0; k < (DIST ? 15 : 12); ++k) g2d_add(dst, k, g[k]);
         }
+      } else if constexpr (DIST) {
+        const float v = reduce_scatter16(g, lane);
+        const int k = lane >> 1;
+        if ((lane & 1) == 0 && k < 15) g2d_add(dst, k, v);  // 12..14 → f[7..9] (Eq.15 sums)
       } else {
         const float v = reduce_scatter12(g, lane);
         const int k = slot12(lane);
@@ -479,31 +530,43 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
 
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal, float* alpha,
-                       float* T_final, int32_t* n_contrib, int32_t* median_pos, Counter* counters, cudaStream_t s) {
+                       float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
+                       Counter* counters, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
-#define RD_K3(T, P)                                                                                              \
-  k_render_fwd<T, P><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal, alpha, \
-                                                T_final, n_contrib, median_pos, counters)
-  if (opt.tile == 16) {
-    if (counters) RD_K3(16, true); else RD_K3(16, false);
-  } else {
-    if (counters) RD_K3(8, true); else RD_K3(8, false);
+#define RD_K3(T, P, D)                                                                                            \
+  k_render_fwd<T, P, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal,   \
+                                                   alpha, T_final, n_contrib, median_pos, dio, counters)
+#define RD_K3T(T)                                     \
+  if (dio.d0) {                                       \
+    if (counters) RD_K3(T, true, true); else RD_K3(T, false, true);   \
+  } else {                                            \
+    if (counters) RD_K3(T, true, false); else RD_K3(T, false, false); \
   }
+  if (opt.tile == 16) {
+    RD_K3T(16)
+  } else {
+    RD_K3T(8)
+  }
+#undef RD_K3T
 #undef RD_K3
 }
 
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
-                       const float* dL_dnormal, const float* dL_dalpha, G2D* g2d, Counter* counters,
-                       cudaStream_t s) {
+                       const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio, G2D* g2d,
+                       Counter* counters, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
-  if (opt.tile == 16)
-    k_render_bwd<16, 2><<<grid, 128, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
-                                            dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
-  else
-    k_render_bwd<8, 2><<<grid, 32, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, median_pos,
-                                           dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, g2d, counters);
+#define RD_K4(T, D)                                                                                        \
+  k_render_bwd<T, 2, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, \
+                                                   median_pos, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,  \
+                                                   dio, g2d, counters)
+  if (opt.tile == 16) {
+    if (dio.dL_ddist) RD_K4(16, true); else RD_K4(16, false);
+  } else {
+    if (dio.dL_ddist) RD_K4(8, true); else RD_K4(8, false);
+  }
+#undef RD_K4
 }
 
 }  // namespace rade

@@ -203,6 +203,32 @@ def rd_render_fwd(view: View, color=None, depth=None, normal=None, alpha=None, s
     return dict(color=color, depth=depth, normal=normal, alpha=alpha)
 
 
+def rd_render_fwd_ex(view: View, color=None, depth=None, normal=None, alpha=None, distortion=None, stream=None):
+    """rd_render_fwd plus the depth-distortion map L_d (reading S21) when `distortion` is a
+    [H, W] float32 tensor (or True: allocated). Returns the dict of the given maps."""
+    H, W = view.camera.height, view.camera.width
+    if distortion is True:
+        distortion = torch.empty((H, W), dtype=torch.float32, device=view.device)
+    for name, t, shp in (("color", color, (3, H, W)), ("depth", depth, (H, W)), ("normal", normal, (3, H, W)),
+                         ("alpha", alpha, (H, W)), ("distortion", distortion, (H, W))):
+        if t is not None:
+            _check_f32(name, t, shp)
+    m = N.RdFwdMaps(*(None if t is None else t.data_ptr() for t in (color, depth, normal, alpha, distortion)))
+    N.check(view.lib.rd_render_fwd_ex(view.handle, ctypes.byref(m), _stream_ptr(stream)), "rd_render_fwd_ex")
+    return dict(color=color, depth=depth, normal=normal, alpha=alpha, distortion=distortion)
+
+
+def rd_blend_bwd_ex(view: View, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None, dL_dalpha=None,
+                    dL_ddistortion=None, stream=None):
+    """rd_blend_bwd plus the cotangent of the distortion map (ω detached, S21)."""
+    _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha)
+    if dL_ddistortion is not None:
+        _check_f32("dL_ddistortion", dL_ddistortion, (view.camera.height, view.camera.width))
+    c = N.RdBwdCotangents(*(None if t is None else t.data_ptr()
+                            for t in (dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, dL_ddistortion)))
+    N.check(view.lib.rd_blend_bwd_ex(view.handle, ctypes.byref(c), _stream_ptr(stream)), "rd_blend_bwd_ex")
+
+
 def _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha):
     H, W = view.camera.height, view.camera.width
     for name, t, shp in (("dL_dcolor", dL_dcolor, (3, H, W)), ("dL_ddepth", dL_ddepth, (H, W)),

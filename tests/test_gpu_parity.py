@@ -10,7 +10,7 @@ import torch
 import oracle
 import paper_2406_01467_b200 as P
 import scenegen as sg
-from gpu_helpers import cpu_binning_reference, gpu_forward, gpu_grads
+from gpu_helpers import cpu_binning_reference, gpu_forward, gpu_grads, grads_to_rows, opts_dict
 from helpers import concat, dense_scene, one_gaussian, random_cam
 
 pytestmark = pytest.mark.gpu
@@ -265,3 +265,65 @@ def test_rasterize_autograd_wrapper():
     L.backward()
     _, G, _ = gpu_grads(scene, cam, opt, cot)
     np.testing.assert_allclose(ts[0].grad.double().cpu().numpy(), G[:, 0:3], rtol=1e-4, atol=1e-6)
+
+
+# ----------------------------------------------------------------------------- NEXT-1: L_d
+
+def _gpu_distortion(scene, cam, opt):
+    g = P.Gaussians.from_numpy(scene)
+    view = P.View()
+    P.rd_preprocess(view, g, cam, opts_dict(opt))
+    P.rd_bin(view)
+    out = P.rd_render_fwd_ex(view, distortion=True)
+    torch.cuda.synchronize()
+    return out["distortion"].double().cpu().numpy(), view, g
+
+
+def test_distortion_forward_parity(case):
+    """Depth-distortion map (reading S21) vs the oracle's double sum."""
+    ref = case["ref"]
+    L, _, _ = _gpu_distortion(case["scene"], case["cam"], case["opt"])
+    ok = (ref["flags"] & (F1 | F3)) == 0
+    err = np.abs(L - ref["distortion"])[ok]
+    assert err.max() <= TOL * np.maximum(1.0, np.abs(ref["distortion"][ok])).max(), err.max()
+    assert ref["distortion"].max() > 1e-3 or case["name"] == "C0"
+
+
+def test_distortion_backward_parity(case):
+    """Gradients of Σ g·L_d (ω detached, S21) — together with the four image cotangents —
+    vs the oracle's dual numbers; per parameter class ≤ 1e-3 relative."""
+    scene, cam, opt = case["scene"], case["cam"], case["opt"]
+    ref = case["ref"]
+    mask = ref["flags"] == 0
+    cot = sg.cotangents(8, cam.width, cam.height)
+    rng = np.random.default_rng(9)
+    cot["distortion"] = rng.normal(size=(cam.height, cam.width))
+    cot = {k: (v * mask).astype(np.float32) for k, v in cot.items()}
+    _, view, g = _gpu_distortion(scene, cam, opt)
+    dev = torch.device("cuda")
+    c = {k: torch.as_tensor(v).contiguous().to(dev) for k, v in cot.items()}
+    grads = g.zeros_like()
+    P.rd_blend_bwd_ex(view, c["color"], c["depth"], c["normal"], c["alpha"], c["distortion"])
+    P.rd_preprocess_bwd(view, g, grads)
+    torch.cuda.synchronize()
+    G = grads_to_rows(grads, scene.n)
+    pg = oracle.project(scene, cam, opt)
+    vis = np.nonzero(pg[:, 0] == 1)[0]
+    R = oracle.grad(scene, cam, opt, cot, vis)
+    for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
+                     "opacities": slice(10, 11), "sh": slice(11, 11 + 3 * (opt.sh_degree + 1) ** 2)}.items():
+        a, b = G[vis, sl], R[:, sl]
+        nb = np.linalg.norm(b)
+        if nb == 0:
+            assert np.abs(a).max() == 0
+            continue
+        assert np.linalg.norm(a - b) / nb <= 1e-3, name
+
+
+def test_distortion_cotangent_needs_distortion_forward():
+    scene, cam = dense_scene(3, 50), sg.camera_identity(32, 32, 32)
+    out, view, g = gpu_forward(scene, cam, sg.Options())
+    z = torch.zeros((32, 32), device="cuda")
+    with pytest.raises(P.rade.N.RadeError) as e:
+        P.rd_blend_bwd_ex(view, dL_ddistortion=z)
+    assert e.value.status == 2
