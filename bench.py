@@ -263,7 +263,7 @@ def run_gpu(args, cfg_name, config):
     n_ring = min(B * 2, 8)
     gen = torch.Generator(device=device)
     gen.manual_seed(SEED_COT + rank)
-    cots = [torch.randn((8, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
+    cots = [torch.randn((9, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
     opts = dict(tile=args.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
                 median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
     # Views are pipelined over `args.pipeline` CUDA streams, each with its own rd_view and
@@ -279,7 +279,8 @@ def run_gpu(args, cfg_name, config):
                     "outs": {"color": torch.empty((3, H, W), device=device),
                              "depth": torch.empty((H, W), device=device),
                              "normal": torch.empty((3, H, W), device=device),
-                             "alpha": torch.empty((H, W), device=device)},
+                             "alpha": torch.empty((H, W), device=device),
+                             "distortion": torch.empty((H, W), device=device)},
                     "done": torch.cuda.Event()}
         slots.append(slot)
     view = slots[0]["view"]
@@ -287,13 +288,29 @@ def run_gpu(args, cfg_name, config):
     counter = {"v": 0}
     main_stream = torch.cuda.current_stream(device)
 
-    def one_view(slot, cam, cot, after):
+    def one_view(slot, cam, cot, after, io=None):
+        """io (end-to-end pass): events that order the view's forward after the D2H of the
+        slot's previous maps, publish the forward for its D2H, hold K4 until the H2D of the
+        cotangents landed, and publish K4 (the cotangent buffer is free again)."""
         st, vw, o = slot["stream"], slot["view"], slot["outs"]
         with torch.cuda.stream(st):
             P.rd_preprocess(vw, g, cam, opts, stream=st)
             P.rd_bin(vw, stream=st)
-            P.rd_render_fwd(vw, o["color"], o["depth"], o["normal"], o["alpha"], stream=st)
-            P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)  # K4: view-private output
+            if io:
+                st.wait_event(io["outs_free"])
+            if args.distortion:  # NEXT-1: + the depth-distortion map and its gradient
+                P.rd_render_fwd_ex(vw, o["color"], o["depth"], o["normal"], o["alpha"], o["distortion"], stream=st)
+            else:
+                P.rd_render_fwd(vw, o["color"], o["depth"], o["normal"], o["alpha"], stream=st)
+            if io:
+                io["fwd_done"].record(st)
+                st.wait_event(io["cot_ready"])
+            if args.distortion:
+                P.rd_blend_bwd_ex(vw, cot[0:3], cot[3], cot[4:7], cot[7], cot[8], stream=st)
+            else:
+                P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)  # K4: view-private output
+            if io:
+                io["k4_done"].record(st)
             st.wait_event(after)  # gradient rows: the previous view's K5 first
             P.rd_preprocess_bwd(vw, g, grads, stream=st)
             slot["done"].record(st)
@@ -356,27 +373,39 @@ def run_gpu(args, cfg_name, config):
     # ---------------- end-to-end: host cotangents in (pinned), rendered maps out, per step
     e2e = None
     if not args.no_e2e:
-        host_cots = [c.cpu().pin_memory() for c in cots]
+        nch = 9 if args.distortion else 8  # cotangent channels the step consumes
+        host_cots = [c[:nch].cpu().pin_memory() for c in cots]
         h2d = 0
         d2h = 0
-
-        host_outs = [{k: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k, v in outs.items()}
+        out_keys = [k for k in outs if k != "distortion" or args.distortion]
+        host_outs = [{k: torch.empty(outs[k].shape, dtype=torch.float32).pin_memory() for k in out_keys}
                      for _ in slots]
-        dev_cots = [torch.empty((8, H, W), device=device) for _ in slots]
+        dev_cots = [torch.empty((nch, H, W), device=device) for _ in slots]
+
+        # transfers on their own copy streams, overlapped with the compute of other views:
+        # the H2D of a view's cotangents is only awaited by its K4, the D2H of its maps only
+        # by the next forward of the same slot
+        cin, cout = torch.cuda.Stream(device), torch.cuda.Stream(device)
+        ios = [{k: torch.cuda.Event() for k in ("cot_ready", "k4_done", "fwd_done", "outs_free")} for _ in slots]
 
         def per_view_e2e(sl, k, prev):
             nonlocal h2d, d2h
             i = slots.index(sl)
-            with torch.cuda.stream(sl["stream"]):
+            io = ios[i]
+            with torch.cuda.stream(cin):
+                cin.wait_event(io["k4_done"])  # the slot's previous K4 has read the buffer
                 dev_cots[i].copy_(host_cots[k % n_ring], non_blocking=True)
+                io["cot_ready"].record(cin)
             h2d += dev_cots[i].numel() * 4
-            done = one_view(sl, my_views[k % len(my_views)], dev_cots[i], prev)
-            with torch.cuda.stream(sl["stream"]):
-                for key, t in sl["outs"].items():
+            done = one_view(sl, my_views[k % len(my_views)], dev_cots[i], prev, io)
+            with torch.cuda.stream(cout):
+                cout.wait_event(io["fwd_done"])
+                for key in out_keys:
+                    t = sl["outs"][key]
                     host_outs[i][key].copy_(t, non_blocking=True)
                     d2h += t.numel() * 4
-                sl["done"].record(sl["stream"])
-            return sl["done"]
+                io["outs_free"].record(cout)
+            return done
 
         def step_e2e():
             run_views(per_view_e2e)
@@ -393,8 +422,9 @@ def run_gpu(args, cfg_name, config):
         t_e2e = max_over_ranks(time.perf_counter() - t0, dist_on, device)
         e2e = {"value": steps_e2e * B * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // steps_e2e,
                "d2h_bytes_per_step": d2h // steps_e2e,
-               "what": "per view: H2D of the view's 8-channel cotangent image from pinned host memory, the four "
-                       "C-ABI calls, D2H of color/depth/normal/alpha; Gaussians and gradients stay resident "
+               "what": "per view: H2D of the view's cotangent image (8 channels, 9 with --distortion) from "
+                       "pinned host memory, the five C-ABI calls, D2H of the rendered maps, on two copy streams "
+                       "overlapped with the compute of other views; Gaussians and gradients stay resident "
                        "(model state); host wall clock, max over ranks"}
 
     # ---------------- roofline of the dominant kernel + per-kernel breakdown
@@ -489,6 +519,7 @@ def main():
     ap.add_argument("--cpu-pixels", type=int, default=2048, help="cpu_baseline: forward pixels sampled")
     ap.add_argument("--cpu-grads", type=int, default=64, help="cpu_baseline: Gaussians differentiated")
     ap.add_argument("--tile", type=int, default=8, choices=[8, 16], help="blend tile edge (outputs are tile-size independent)")
+    ap.add_argument("--distortion", action="store_true", help="NEXT-1: also render L_d and back-propagate it")
     ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the views are pipelined over")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -498,7 +529,7 @@ def main():
     import scenegen as sg
     info = sg.CONFIGS[args.config]
     config = {"workload": f"{args.config}: {info['name']}", "width": info["width"], "height": info["height"],
-              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": args.tile,
+              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": args.tile, "depth_distortion": args.distortion,
               "scene_recipe": "scenegen (DESIGN.md §Input recipe), seed 0 + config index"}
     if args.impl == "reference":
         return run_reference(args, args.config, config)

@@ -183,3 +183,22 @@ def test_c3_sampled_gradients(c3):
         assert nb > 0, name
         rel = np.linalg.norm(A[:, sl] - R[:, sl]) / nb
         assert rel <= 1e-3, (name, rel)
+
+
+def test_c3_distortion_sampled_pixels(c3):
+    """NEXT-1 at full size: the depth-distortion map (S21) at 48 random pixels vs the oracle."""
+    cam, g = c3["cam"], c3["g"]
+    view = P.View()
+    P.rd_preprocess(view, g, cam, opts_dict(c3["opt"]))
+    P.rd_bin(view)
+    L = P.rd_render_fwd_ex(view, distortion=True)["distortion"]
+    torch.cuda.synchronize()
+    L = L.double().cpu().numpy()
+    rng = np.random.default_rng(12)
+    pix = rng.choice(cam.width * cam.height, 48, replace=False)
+    ref = oracle.render(c3["scene"], cam, c3["opt"], pixels=pix)
+    ys, xs = pix // cam.width, pix % cam.width
+    ok = (ref["flags"] & (F1 | F3)) == 0
+    assert ok.mean() > 0.8 and ref["distortion"].max() > 1e-3
+    err = np.abs(L[ys, xs] - ref["distortion"])[ok]
+    assert err.max() <= TOL * max(1.0, np.abs(ref["distortion"][ok]).max()), err.max()
