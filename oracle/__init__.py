@@ -14,6 +14,11 @@ Parity status of each oracle function:
   render       pinned (two opaque layers, single splat, empty scene, Σω + T = 1, median
                property, tile-free brute force by construction)
   grad         pinned (central finite differences of render)
+  distortion   pinned (two-layer closed form; detached-weight gradient closed form;
+               one-pass identity on per-splat evaluations)
+  depth_normal, normal_consistency (NEXT-2, image space, plain numpy fp64)
+               pinned (fronto-parallel and tilted planes: analytic normals; holes;
+               Σω(1 − n·ñ) = A − N·ñ on the oracle's own blend)
   Constants chosen by convention (readings S1, S5, S6, S8, S14) are parity unpinned
   against the paper: the paper fixes none of them.
 """
@@ -207,6 +212,47 @@ def loss(outputs, cot, bg=None):
     """L = Σ_px cot·(C, D, N, A) from a render() result (fp64)."""
     return float(np.sum(outputs["color"] * cot["color"]) + np.sum(outputs["depth"] * cot["depth"])
                  + np.sum(outputs["normal"] * cot["normal"]) + np.sum(outputs["alpha"] * cot["alpha"]))
+
+
+def depth_normal(depth, cam):
+    """Normal from the depth map by finite differences ("applying finite
+    difference on the depth map"; reading S22 = SPEC:309-316): back-project the pixel centre
+    and its right and lower neighbours, P = D·((x+½−cx)/fx, (y+½−cy)/fy, 1);
+    ñ = normalize((P_right − P) × (P_down − P)), flipped so that ñ·P < 0; 0 where the pixel
+    or either neighbour is a hole (D = 0) or missing (last column / row).
+    depth [H, W] → ñ [3, H, W] (fp64)."""
+    D = np.asarray(depth, np.float64)
+    H, W = D.shape
+    fx, fy, cx, cy = (float(np.float32(v)) for v in (cam.fx, cam.fy, cam.cx, cam.cy))
+    xs = (np.arange(W) + 0.5 - cx) / fx
+    ys = (np.arange(H) + 0.5 - cy) / fy
+    P = np.stack([D * xs[None, :], D * ys[:, None], D], 0)
+    out = np.zeros((3, H, W))
+    for y in range(H - 1):
+        for x in range(W - 1):
+            if D[y, x] == 0 or D[y, x + 1] == 0 or D[y + 1, x] == 0:
+                continue
+            a = P[:, y, x + 1] - P[:, y, x]
+            b = P[:, y + 1, x] - P[:, y, x]
+            m = np.cross(a, b)
+            nm = np.linalg.norm(m)
+            if nm == 0:
+                continue
+            n = m / nm
+            if n @ P[:, y, x] > 0:
+                n = -n
+            out[:, y, x] = n
+    return out
+
+
+def normal_consistency(depth, alpha, normal, cam):
+    """Per-pixel normal consistency (reading S22): L_n = Σ_i ω_i (1 − n_iᵀñ)
+    = A − Nᵀñ with A = Σω (alpha) and N = Σωn (the normal map), ñ = depth_normal; 0 where
+    ñ is undefined. Returns (L_n [H, W], ñ [3, H, W])."""
+    nt = depth_normal(depth, cam)
+    valid = np.any(nt != 0, axis=0)
+    L = np.where(valid, np.asarray(alpha, np.float64) - np.sum(np.asarray(normal, np.float64) * nt, 0), 0.0)
+    return L, nt
 
 
 def num_threads():

@@ -592,3 +592,59 @@ def test_depth_distortion_one_pass_identity(O):
             A, D1, D2 = A + w, D1 + w * ev[0, 2], D2 + w * ev[0, 2] ** 2
             T *= 1 - a
         assert r["distortion"][y, x] == pytest.approx(2 * (A * D2 - D1 * D1), rel=1e-7, abs=1e-10)
+
+
+# ----------------------------------------------------------------------------- L_n
+
+def test_depth_normal_planes(O):
+    """Reading S22: finite-difference normals of an analytically rendered
+    plane. Fronto-parallel → (0, 0, −1) everywhere interior; a tilted plane n·X = c →
+    ±n (oriented so ñ·P < 0) to rounding; the last row/column are 0."""
+    cam = sg.Camera(50.0, 55.0, 20.3, 14.7, 40, 30, np.eye(3), np.zeros(3), 0.2)
+    D = np.full((30, 40), 3.5)
+    nt = O.depth_normal(D, cam)
+    np.testing.assert_allclose(nt[:, :-1, :-1], np.broadcast_to(np.array([0, 0, -1.0])[:, None, None], (3, 29, 39)),
+                               atol=1e-12)
+    assert np.all(nt[:, -1, :] == 0) and np.all(nt[:, :, -1] == 0)
+    n = np.array([0.3, -0.2, -0.9])
+    n /= np.linalg.norm(n)
+    c = -4.0  # n·X = c, in front of the camera (X_z > 0)
+    fx, fy, cx, cy = 50.0, 55.0, 20.3, 14.7
+    xs = (np.arange(40) + 0.5 - cx) / fx
+    ys = (np.arange(30) + 0.5 - cy) / fy
+    r = np.stack([np.broadcast_to(xs[None, :], (30, 40)), np.broadcast_to(ys[:, None], (30, 40)),
+                  np.ones((30, 40))], 0)
+    D = c / np.einsum("k,kyx->yx", n, r)
+    assert (D > 0).all()
+    nt = O.depth_normal(D, cam)
+    expect = n if (n @ r[:, 5, 5]) * D[5, 5] < 0 else -n
+    np.testing.assert_allclose(nt[:, :-1, :-1], np.broadcast_to(expect[:, None, None], (3, 29, 39)), atol=1e-9)
+
+
+def test_depth_normal_holes(O):
+    """A hole (D = 0) removes the normals of the three stencils that use it."""
+    cam = sg.camera_identity(16, 12, 20.0)
+    D = np.full((12, 16), 2.0)
+    D[5, 7] = 0.0
+    nt = O.depth_normal(D, cam)
+    zero = np.all(nt == 0, 0)
+    assert zero[5, 7] and zero[5, 6] and zero[4, 7]
+    assert zero.sum() == 3 + 12 + 16 - 1
+
+
+def test_normal_consistency_flat_splat_is_zero(O):
+    """A fronto-parallel flat splat has n = (0, 0, −1) = ñ of its constant depth, so
+    L_n = A − N·ñ = A − A = 0 wherever it alone is blended; L_n ∈ [0, 2A] always."""
+    cam = sg.camera_identity(32, 32, 32)
+    sc = one_gaussian([0, 0, 2.0], [0.6, 0.6, 1e-4], opacity=0.8)
+    r = O.render(sc, cam, OPT)
+    L, nt = O.normal_consistency(r["depth"], r["alpha"], r["normal"], cam)
+    valid = np.any(nt != 0, 0)
+    assert valid.sum() > 200
+    np.testing.assert_allclose(L[valid], 0.0, atol=1e-9)
+    sc2 = dense_scene(14, 150, width=32, height=32, f=32.0)
+    r2 = O.render(sc2, cam, OPT)
+    L2, nt2 = O.normal_consistency(r2["depth"], r2["alpha"], r2["normal"], cam)
+    v2 = np.any(nt2 != 0, 0)
+    assert v2.sum() > 50
+    assert (L2[v2] >= -1e-12).all() and (L2[v2] <= 2 * r2["alpha"][v2] + 1e-12).all()
