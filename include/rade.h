@@ -216,6 +216,22 @@ rd_status rd_blend_bwd(rd_view* view, const float* dL_dcolor, const float* dL_dd
  * rd_blend_bwd of another view may overlap this call. */
 rd_status rd_preprocess_bwd(rd_view* view, const rd_gaussians* g, const rd_grads* grads, rd_stream stream);
 
+/* NEXT-2: normal consistency (reading S22) on rendered maps (device, fp32,
+ * the layouts of rd_render_fwd): ñ = the finite-difference normal of the median depth map
+ * (back-project the pixel and its right / lower neighbours with the camera intrinsics,
+ * ñ = normalize((P_r − P) × (P_d − P)) oriented so ñ·P < 0, 0 where a depth is 0 or the
+ * neighbour is outside the image), consistency[H][W] = Σ_i ω_i (1 − n_iᵀñ) = alpha − normal·ñ
+ * (0 where ñ is 0), depth_normal[3][H][W] = ñ. Either output may be NULL. Only fx, fy, cx, cy,
+ * width, height of `cam` are used. */
+rd_status rd_normal_consistency(const rd_camera* cam, const float* depth, const float* alpha, const float* normal,
+                                float* consistency, float* depth_normal, rd_stream stream);
+/* Backward of Σ_p dL_dconsistency[p]·consistency[p] into the map cotangents, ACCUMULATED
+ * (+=): dL_ddepth[H][W] (through ñ; neighbours by atomics), dL_dalpha[H][W],
+ * dL_dnormal[3][H][W]; any may be NULL. Pass the results to rd_blend_bwd / rd_render_bwd. */
+rd_status rd_normal_consistency_bwd(const rd_camera* cam, const float* depth, const float* normal,
+                                    const float* dL_dconsistency, float* dL_ddepth, float* dL_dalpha,
+                                    float* dL_dnormal, rd_stream stream);
+
 /* Profiling: when enabled, every kernel launch of this view is bracketed by CUDA events on
  * its stream and K3/K4 count the pairs they evaluate (a few atomics per warp). Enabling
  * or disabling resets the accumulators. rd_get_timings synchronises on the recorded

@@ -89,6 +89,8 @@ SIGNATURES = {
                       ctypes.c_int),
     "rd_blend_bwd": ([_VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_render_fwd_ex": ([_VP, ctypes.POINTER(RdFwdMaps), _VP], ctypes.c_int),
+    "rd_normal_consistency": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
+    "rd_normal_consistency_bwd": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_blend_bwd_ex": ([_VP, ctypes.POINTER(RdBwdCotangents), _VP], ctypes.c_int),
     "rd_preprocess_bwd": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
     "rd_view_stats": ([_VP, ctypes.POINTER(RdStats)], ctypes.c_int),

@@ -493,6 +493,33 @@ rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolo
   return rd_preprocess_bwd(v, g, grads, stream);
 }
 
+rd_status rd_normal_consistency(const rd_camera* cam, const float* depth, const float* alpha, const float* normal,
+                                float* consistency, float* depth_normal, rd_stream stream) {
+  g_err.clear();
+  if (!cam || !depth) return fail(RD_ERR_INVALID_ARGUMENT, "NULL camera / depth");
+  if (consistency && (!alpha || !normal)) return fail(RD_ERR_INVALID_ARGUMENT, "consistency needs alpha and normal");
+  if (cam->width < 0 || cam->height < 0) return fail(RD_ERR_INVALID_ARGUMENT, "negative image size");
+  if (!(cam->fx > 0.f && cam->fy > 0.f)) return fail(RD_ERR_INVALID_ARGUMENT, "fx, fy must be > 0");
+  launch_normal_consistency(cam->fx, cam->fy, cam->cx, cam->cy, cam->width, cam->height, depth, alpha, normal,
+                            consistency, depth_normal, (cudaStream_t)stream);
+  RD_CHECK_LAUNCH("normal_consistency");
+  return RD_OK;
+}
+
+rd_status rd_normal_consistency_bwd(const rd_camera* cam, const float* depth, const float* normal,
+                                    const float* dL_dconsistency, float* dL_ddepth, float* dL_dalpha,
+                                    float* dL_dnormal, rd_stream stream) {
+  g_err.clear();
+  if (!cam || !depth || !normal || !dL_dconsistency)
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL camera / depth / normal / dL_dconsistency");
+  if (cam->width < 0 || cam->height < 0) return fail(RD_ERR_INVALID_ARGUMENT, "negative image size");
+  if (!(cam->fx > 0.f && cam->fy > 0.f)) return fail(RD_ERR_INVALID_ARGUMENT, "fx, fy must be > 0");
+  launch_normal_consistency_bwd(cam->fx, cam->fy, cam->cx, cam->cy, cam->width, cam->height, depth, normal,
+                                dL_dconsistency, dL_ddepth, dL_dalpha, dL_dnormal, (cudaStream_t)stream);
+  RD_CHECK_LAUNCH("normal_consistency_bwd");
+  return RD_OK;
+}
+
 rd_status rd_set_profiling(rd_view* v, int32_t enabled) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   if (enabled) {

@@ -195,6 +195,13 @@ void launch_duplicate(int64_t n, int64_t m, const uint32_t* offsets, const uint3
 int launch_tile_sort(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int tile_bits,
                      void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s);
+// NEXT-2 (regularize.cu): L_n = A − Nᵀñ per pixel and ñ (either may be NULL); backward adds
+// into the map cotangents gD (atomics), gA, gN (any may be NULL).
+void launch_normal_consistency(float fx, float fy, float cx, float cy, int W, int H, const float* depth,
+                               const float* alpha, const float* normal, float* Ln, float* nt, cudaStream_t s);
+void launch_normal_consistency_bwd(float fx, float fy, float cx, float cy, int W, int H, const float* depth,
+                                   const float* normal, const float* gL, float* gD, float* gA, float* gN,
+                                   cudaStream_t s);
 // debug: 64-bit keys (tile << 32 | float_bits(z_c)) of the sorted list
 void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,
                    cudaStream_t s);

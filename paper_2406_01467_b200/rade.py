@@ -229,6 +229,44 @@ def rd_blend_bwd_ex(view: View, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None,
     N.check(view.lib.rd_blend_bwd_ex(view.handle, ctypes.byref(c), _stream_ptr(stream)), "rd_blend_bwd_ex")
 
 
+def rd_normal_consistency(camera, depth, alpha=None, normal=None, consistency=True, depth_normal=False,
+                          stream=None):
+    """NEXT-2 (reading S22): the normal-consistency map A − N·ñ and/or the depth normals ñ
+    from rendered maps. consistency / depth_normal: tensors, True (allocate) or None/False."""
+    depth = depth.contiguous()
+    H, W = depth.shape
+    dev = depth.device
+    if consistency is True:
+        consistency = torch.empty((H, W), dtype=torch.float32, device=dev)
+    if depth_normal is True:
+        depth_normal = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    consistency = consistency if isinstance(consistency, torch.Tensor) else None
+    depth_normal = depth_normal if isinstance(depth_normal, torch.Tensor) else None
+    for name, t, shp in (("depth", depth, (H, W)), ("alpha", alpha, (H, W)), ("normal", normal, (3, H, W)),
+                         ("consistency", consistency, (H, W)), ("depth_normal", depth_normal, (3, H, W))):
+        if t is not None:
+            _check_f32(name, t, shp)
+    c = camera_struct(camera)
+    N.check(N.load().rd_normal_consistency(ctypes.byref(c), _ptr(depth), _ptr(alpha), _ptr(normal), _ptr(consistency),
+                                           _ptr(depth_normal), _stream_ptr(stream)), "rd_normal_consistency")
+    return consistency, depth_normal
+
+
+def rd_normal_consistency_bwd(camera, depth, normal, dL_dconsistency, dL_ddepth=None, dL_dalpha=None,
+                              dL_dnormal=None, stream=None):
+    """Adds the backward of Σ dL_dconsistency·consistency into the given map cotangents."""
+    H, W = depth.shape
+    for name, t, shp in (("depth", depth, (H, W)), ("normal", normal, (3, H, W)),
+                         ("dL_dconsistency", dL_dconsistency, (H, W)), ("dL_ddepth", dL_ddepth, (H, W)),
+                         ("dL_dalpha", dL_dalpha, (H, W)), ("dL_dnormal", dL_dnormal, (3, H, W))):
+        if t is not None:
+            _check_f32(name, t, shp)
+    c = camera_struct(camera)
+    N.check(N.load().rd_normal_consistency_bwd(ctypes.byref(c), _ptr(depth), _ptr(normal), _ptr(dL_dconsistency),
+                                               _ptr(dL_ddepth), _ptr(dL_dalpha), _ptr(dL_dnormal),
+                                               _stream_ptr(stream)), "rd_normal_consistency_bwd")
+
+
 def _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha):
     H, W = view.camera.height, view.camera.width
     for name, t, shp in (("dL_dcolor", dL_dcolor, (3, H, W)), ("dL_ddepth", dL_ddepth, (H, W)),

@@ -327,3 +327,69 @@ def test_distortion_cotangent_needs_distortion_forward():
     with pytest.raises(P.rade.N.RadeError) as e:
         P.rd_blend_bwd_ex(view, dL_ddistortion=z)
     assert e.value.status == 2
+
+
+# ----------------------------------------------------------------------------- NEXT-2: L_n
+
+def test_normal_consistency_forward_parity(case):
+    """L_n = A − N·ñ and the depth normals ñ (reading S22): the GPU kernel on the GPU's maps vs
+    the oracle's numpy definition on the same maps (≤ 1e-4), excluding stencils whose
+    orientation is ambiguous (|ñ·P̂| < 1e-3)."""
+    cam, gpu = case["cam"], case["gpu"]
+    dev = torch.device("cuda")
+    t = {k: torch.as_tensor(np.asarray(gpu[k], np.float32)).contiguous().to(dev) for k in ("depth", "alpha", "normal")}
+    L, nt = P.rd_normal_consistency(cam, t["depth"], t["alpha"], t["normal"], consistency=True, depth_normal=True)
+    torch.cuda.synchronize()
+    Lr, ntr = oracle.normal_consistency(gpu["depth"].astype(np.float32).astype(np.float64),
+                                        gpu["alpha"].astype(np.float32).astype(np.float64),
+                                        gpu["normal"].astype(np.float32).astype(np.float64), cam)
+    H, W = gpu["depth"].shape
+    xs = (np.arange(W) + 0.5 - cam.cx) / cam.fx
+    ys = (np.arange(H) + 0.5 - cam.cy) / cam.fy
+    ray = np.stack([np.broadcast_to(xs[None, :], (H, W)), np.broadcast_to(ys[:, None], (H, W)), np.ones((H, W))], 0)
+    cosang = np.abs(np.sum(ntr * ray, 0)) / np.linalg.norm(ray, axis=0)
+    valid = np.any(ntr != 0, 0)
+    ok = ~valid | (cosang > 1e-3)
+    np.testing.assert_allclose(nt.cpu().numpy()[:, ok], ntr[:, ok], atol=1e-4)
+    np.testing.assert_allclose(L.cpu().numpy()[ok], Lr[ok], atol=1e-4)
+    assert valid.sum() > 20 or case["name"] == "C0"
+
+
+def test_normal_consistency_backward_vs_finite_differences():
+    """dL/dD, dL/dA, dL/dN of Σ g·L_n from the GPU kernel vs central finite differences of the
+    oracle's fp64 L_n on a small smooth depth map (plus the closed forms dL/dA = g on valid
+    pixels and dL/dN = −g ñ)."""
+    cam = sg.Camera(30.0, 32.0, 6.2, 4.9, 12, 10, np.eye(3), np.zeros(3), 0.2)
+    rng = np.random.default_rng(3)
+    H, W = 10, 12
+    yy, xx = np.mgrid[0:H, 0:W]
+    D = 3.0 + 0.3 * np.sin(0.5 * xx) + 0.2 * np.cos(0.4 * yy) + 0.05 * rng.random((H, W))
+    D[7, 3] = 0.0  # a hole
+    A = rng.uniform(0.2, 1.0, (H, W))
+    Nm = rng.normal(size=(3, H, W)) * 0.5
+    g = rng.normal(size=(H, W))
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    D, A, Nm, g = f32(D), f32(A), f32(Nm), f32(g)
+    dev = torch.device("cuda")
+    tD, tA, tN, tg = (torch.as_tensor(np.asarray(v, np.float32)).contiguous().to(dev) for v in (D, A, Nm, g))
+    gD, gA, gN = torch.zeros_like(tD), torch.zeros_like(tA), torch.zeros_like(tN)
+    P.rd_normal_consistency_bwd(cam, tD, tN, tg, gD, gA, gN)
+    torch.cuda.synchronize()
+    L0, nt = oracle.normal_consistency(D, A, Nm, cam)
+    valid = np.any(nt != 0, 0)
+    np.testing.assert_allclose(gA.cpu().numpy(), np.where(valid, g, 0.0), atol=1e-6)
+    np.testing.assert_allclose(gN.cpu().numpy(), -g[None] * nt, atol=1e-6)
+    fd = np.zeros((H, W))
+    h = 1e-6
+    for y in range(H):
+        for x in range(W):
+            if D[y, x] == 0:
+                continue
+            Dp, Dm = D.copy(), D.copy()
+            Dp[y, x] += h
+            Dm[y, x] -= h
+            fd[y, x] = (np.sum(g * oracle.normal_consistency(Dp, A, Nm, cam)[0])
+                        - np.sum(g * oracle.normal_consistency(Dm, A, Nm, cam)[0])) / (2 * h)
+    got = gD.cpu().numpy()
+    np.testing.assert_allclose(got, fd, rtol=1e-3, atol=1e-3 * np.abs(fd).max())
+    assert np.abs(fd).max() > 1e-2
