@@ -263,7 +263,7 @@ def run_gpu(args, cfg_name, config):
     n_ring = min(B * 2, 8)
     gen = torch.Generator(device=device)
     gen.manual_seed(SEED_COT + rank)
-    cots = [torch.randn((9, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
+    cots = [torch.randn((10, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
     opts = dict(tile=args.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
                 median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
     # Views are pipelined over `args.pipeline` CUDA streams, each with its own rd_view and
@@ -280,7 +280,9 @@ def run_gpu(args, cfg_name, config):
                              "depth": torch.empty((H, W), device=device),
                              "normal": torch.empty((3, H, W), device=device),
                              "alpha": torch.empty((H, W), device=device),
-                             "distortion": torch.empty((H, W), device=device)},
+                             "distortion": torch.empty((H, W), device=device),
+                             "consistency": torch.empty((H, W), device=device)},
+                    "cot": torch.empty((10, H, W), device=device),
                     "done": torch.cuda.Event()}
         slots.append(slot)
     view = slots[0]["view"]
@@ -305,6 +307,13 @@ def run_gpu(args, cfg_name, config):
             if io:
                 io["fwd_done"].record(st)
                 st.wait_event(io["cot_ready"])
+            if args.normal_consistency:  # NEXT-2: L_n on the maps; its cotangents join the maps'
+                ct = slot["cot"]
+                ct.copy_(cot)
+                P.rd_normal_consistency(cam, o["depth"], o["alpha"], o["normal"], consistency=o["consistency"],
+                                        stream=st)
+                P.rd_normal_consistency_bwd(cam, o["depth"], o["normal"], ct[9], ct[3], ct[7], ct[4:7], stream=st)
+                cot = ct
             if args.distortion:
                 P.rd_blend_bwd_ex(vw, cot[0:3], cot[3], cot[4:7], cot[7], cot[8], stream=st)
             else:
@@ -373,11 +382,12 @@ def run_gpu(args, cfg_name, config):
     # ---------------- end-to-end: host cotangents in (pinned), rendered maps out, per step
     e2e = None
     if not args.no_e2e:
-        nch = 9 if args.distortion else 8  # cotangent channels the step consumes
+        nch = 10 if args.normal_consistency else 9 if args.distortion else 8  # cotangent channels consumed
         host_cots = [c[:nch].cpu().pin_memory() for c in cots]
         h2d = 0
         d2h = 0
-        out_keys = [k for k in outs if k != "distortion" or args.distortion]
+        out_keys = [k for k in outs if (k != "distortion" or args.distortion)
+                    and (k != "consistency" or args.normal_consistency)]
         host_outs = [{k: torch.empty(outs[k].shape, dtype=torch.float32).pin_memory() for k in out_keys}
                      for _ in slots]
         dev_cots = [torch.empty((nch, H, W), device=device) for _ in slots]
@@ -520,6 +530,8 @@ def main():
     ap.add_argument("--cpu-grads", type=int, default=64, help="cpu_baseline: Gaussians differentiated")
     ap.add_argument("--tile", type=int, default=8, choices=[8, 16], help="blend tile edge (outputs are tile-size independent)")
     ap.add_argument("--distortion", action="store_true", help="NEXT-1: also render L_d and back-propagate it")
+    ap.add_argument("--normal-consistency", action="store_true",
+                    help="NEXT-2: also compute L_n on the maps and back-propagate it")
     ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the views are pipelined over")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -529,7 +541,9 @@ def main():
     import scenegen as sg
     info = sg.CONFIGS[args.config]
     config = {"workload": f"{args.config}: {info['name']}", "width": info["width"], "height": info["height"],
-              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": args.tile, "depth_distortion": args.distortion,
+              "n_gaussians": args.n_gaussians or info["n"], "sh_degree": 3, "tile": args.tile,
+              "depth_distortion": args.distortion,
+              "normal_consistency": args.normal_consistency,
               "scene_recipe": "scenegen (DESIGN.md §Input recipe), seed 0 + config index"}
     if args.impl == "reference":
         return run_reference(args, args.config, config)
