@@ -214,6 +214,34 @@ def loss(outputs, cot, bg=None):
                  + np.sum(outputs["normal"] * cot["normal"]) + np.sum(outputs["alpha"] * cot["alpha"]))
 
 
+def apply_filter3d(scene, filt):
+    """The Mip-Splatting 3D filter ("incorporate the 3D filter proposed in
+    Mip-Splatting"; reading S23): Σ ← Σ + f²I per Gaussian, which for Σ = R S²Rᵀ is the
+    Gaussian with scales s' = √(s² + f²) and the same rotation, and o ← o·√(det Σ / det Σ')
+    = o·Π_k s_k/s'_k. Returns (filtered scene, vjp) where vjp maps the gradient rows of the
+    filtered scene ([n, 59]) to the raw scales and opacities (f is a constant)."""
+    f = np.asarray(filt, np.float64)
+    s = np.asarray(scene.scales, np.float64)
+    sp = np.sqrt(s * s + f[None, :] ** 2)
+    ratio = np.prod(s / sp, axis=0)
+    out = scene.copy()
+    out.scales = sp
+    out.opacities = np.asarray(scene.opacities, np.float64) * ratio
+    op = out.opacities
+
+    def vjp(G, gids):
+        G = np.array(G, np.float64, copy=True)
+        gids = np.asarray(gids)
+        d_op = G[:, 10].copy()
+        for k in range(3):
+            sk, spk = s[k, gids], sp[k, gids]
+            G[:, 3 + k] = G[:, 3 + k] * sk / spk + d_op * op[gids] * (1.0 / sk - sk / spk ** 2)
+        G[:, 10] = d_op * op[gids] / np.asarray(scene.opacities, np.float64)[gids]
+        return G
+
+    return out, vjp
+
+
 def depth_normal(depth, cam):
     """Normal from the depth map by finite differences ("applying finite
     difference on the depth map"; reading S22 = SPEC:309-316): back-project the pixel centre

@@ -648,3 +648,52 @@ def test_normal_consistency_flat_splat_is_zero(O):
     v2 = np.any(nt2 != 0, 0)
     assert v2.sum() > 50
     assert (L2[v2] >= -1e-12).all() and (L2[v2] <= 2 * r2["alpha"][v2] + 1e-12).all()
+
+
+# ----------------------------------------------------------------------------- 3D filter (S23)
+
+def test_filter3d_covariance_and_mass(O):
+    """Reading S23 (Mip-Splatting 3D filter): the filtered Gaussian's Σ' equals Σ + f²I
+    (checked through the oracle's own Σ of both scenes), and o·√det Σ — the integral of
+    o·exp(−½xᵀΣ⁻¹x) up to (2π)^{3/2} — is preserved."""
+    sc = dense_scene(21, 20)
+    f = np.random.default_rng(2).uniform(0.01, 0.2, sc.n)
+    fs, _ = O.apply_filter3d(sc, f)
+    cam = sg.camera_identity(64, 64, 64)
+    A, B = O.project(sc, cam, OPT), O.project(fs, cam, OPT)
+    both = (A[:, 0] == 1) & (B[:, 0] == 1)
+    assert both.sum() > 10
+    Sa = A[both][:, 9:18].reshape(-1, 3, 3)
+    Sb = B[both][:, 9:18].reshape(-1, 3, 3)
+    np.testing.assert_allclose(Sb, Sa + (f[both] ** 2)[:, None, None] * np.eye(3), rtol=1e-12, atol=1e-14)
+    mass_a = sc.opacities[both].astype(np.float64) * np.sqrt(np.linalg.det(Sa))
+    mass_b = fs.opacities[both] * np.sqrt(np.linalg.det(Sb))
+    np.testing.assert_allclose(mass_b, mass_a, rtol=1e-9)
+
+
+def test_filter3d_gradient_vjp_vs_finite_differences(O):
+    """The raw-parameter gradient (dual-number gradient of the filtered scene mapped through
+    apply_filter3d's vjp) vs central differences of the filtered render in the raw scales
+    and opacity."""
+    sc = dense_scene(22, 30)
+    cam = sg.camera_identity(32, 32, 32)
+    f = np.random.default_rng(4).uniform(0.02, 0.1, sc.n)
+    cot = sg.cotangents(5, 32, 32)
+    fs, vjp = O.apply_filter3d(sc, f)
+    pg = O.project(fs, cam, OPT)
+    gid = int(np.nonzero(pg[:, 0] == 1)[0][3])
+    G = vjp(O.grad(fs, cam, OPT, cot, [gid]), [gid])[0]
+
+    def loss(scene):
+        return O.loss(O.render(O.apply_filter3d(scene, f)[0], cam, OPT), cot)
+
+    for j, (arr, idx) in enumerate([("scales", (0, gid)), ("scales", (2, gid)), ("opacities", (gid,))]):
+        h = 1e-6
+        sp, sm = sc.copy(), sc.copy()
+        for s_, sgn in ((sp, 1), (sm, -1)):
+            a = getattr(s_, arr).astype(np.float64)
+            a[idx] += sgn * h
+            setattr(s_, arr, a)
+        fd = (loss(sp) - loss(sm)) / (2 * h)
+        col = {0: 3, 1: 5, 2: 10}[j]
+        assert G[col] == pytest.approx(fd, rel=2e-4, abs=1e-7), (arr, idx)
