@@ -102,6 +102,9 @@ typedef struct rd_gaussians {
   const float* rotations;
   const float* opacities;
   const float* sh;
+  const float* filter3d; /* NULL, or [n]: the Mip-Splatting 3D filter size f per Gaussian (NEXT-3,
+                            reading S23): rendered as Σ + f²I (scales √(s² + f²)) with opacity
+                            o·Π s/√(s² + f²); gradients are w.r.t. the raw scales/opacities */
 } rd_gaussians;
 
 /* Device gradient arrays, same layouts as rd_gaussians; accumulated (+=). */

@@ -36,7 +36,7 @@ class RdOptions(ctypes.Structure):
 class RdGaussians(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("sh_coeffs", ctypes.c_int32), ("means", ctypes.c_void_p),
                 ("scales", ctypes.c_void_p), ("rotations", ctypes.c_void_p), ("opacities", ctypes.c_void_p),
-                ("sh", ctypes.c_void_p)]
+                ("sh", ctypes.c_void_p), ("filter3d", ctypes.c_void_p)]
 
 
 class RdGrads(ctypes.Structure):

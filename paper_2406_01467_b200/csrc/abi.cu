@@ -305,7 +305,7 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   RD_ENSURE(v->nvis, 2 * sizeof(uint32_t), s);
   RD_ENSURE(v->g2d, n * sizeof(G2D), s);
 
-  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
   v->begin(s);  // K1 timing includes the zeroing of the list counters
   RD_CUDA(cudaMemsetAsync(v->nvis.ptr, 0, 2 * sizeof(uint32_t), s));
   launch_preprocess_fwd(dg, c, o, tiles_x, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
@@ -467,7 +467,7 @@ rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* g
   if ((g->sh_coeffs * 3) % 4 == 0 && (((uintptr_t)g->sh | (uintptr_t)grads->sh) & 15u) != 0)
     return fail(RD_ERR_INVALID_ARGUMENT, "sh / its gradient not 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh};
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
   DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
   v->begin(s);
   launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const uint32_t*)v->vis.ptr, v->n_vis,

@@ -104,6 +104,7 @@ __device__ __forceinline__ void sh_basis_grad(float x, float y, float z, int deg
 template <typename S>
 struct GF {
   float mu[3], s[3], qr[4], o;
+  float s_raw[3], o_raw;  // the inputs before the 3D filter (= s, o without it)
   float zkey;   // the fp32 sort key of reading S7 (also the stored z_c)
   S qinv, qn[4];
   S Rc[9];  // W R(q̂), row-major
@@ -166,12 +167,29 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   }
   f.zkey = z;
   f.o = g.opac[i];
-  if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;
+  if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;  // o' ≤ o: also culls the filtered one
   f.s[0] = g.scales[3 * i];
   f.s[1] = g.scales[3 * i + 1];
   f.s[2] = g.scales[3 * i + 2];
   if (!(f.s[0] > 0.f && f.s[1] > 0.f && f.s[2] > 0.f) || !(isfin(f.s[0]) && isfin(f.s[1]) && isfin(f.s[2])))
     return false;
+  f.s_raw[0] = f.s[0];
+  f.s_raw[1] = f.s[1];
+  f.s_raw[2] = f.s[2];
+  f.o_raw = f.o;
+  if (g.filter3d) {  // 3D filter (S23): Σ + f²I ⇔ s' = √(s² + f²); o' = o·Π s/s'
+    const float fl = g.filter3d[i];
+    if (!isfin(fl)) return false;
+    float ratio = 1.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float sp = sqrtf(fmaf(f.s[k], f.s[k], fl * fl));
+      ratio *= f.s[k] / sp;
+      f.s[k] = sp;
+    }
+    f.o *= ratio;
+    if (!(f.o >= opt.alpha_min)) return false;
+  }
   {
     const float4 q4 = reinterpret_cast<const float4*>(g.rot)[i];  // [n][4], 16-B aligned rows
     f.qr[0] = q4.x;
@@ -624,6 +642,14 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   float4* grot = reinterpret_cast<float4*>(gr.rot) + i;
   const float4 oq = *grot;
   const float oo = gr.opac[i];
+  float d_o_raw = d_o;
+  if (g.filter3d) {  // through s' = √(s² + f²), o' = o·Π s/s' back to the raw s, o (S23)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      ds[k] = ds[k] * (S)(f.s_raw[k] / f.s[k]) +
+              (S)d_o * (S)f.o * ((S)1 / (S)f.s_raw[k] - (S)f.s_raw[k] / ((S)f.s[k] * (S)f.s[k]));
+    d_o_raw = d_o * (f.o / f.o_raw);
+  }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     gr.means[3 * i + k] = om[k] + (float)dmu[k] + dmu_extra[k];
@@ -632,7 +658,7 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   *grot = make_float4(oq.x + (float)((dqn[0] - f.qn[0] * qd) * f.qinv), oq.y + (float)((dqn[1] - f.qn[1] * qd) * f.qinv),
                       oq.z + (float)((dqn[2] - f.qn[2] * qd) * f.qinv), oq.w + (float)((dqn[3] - f.qn[3] * qd) * f.qinv));
   // α = min(α_max, o·G): d_o already excludes the clamp (K4)
-  gr.opac[i] = oo + d_o;
+  gr.opac[i] = oo + d_o_raw;
 }
 
 // K5b, fp32, one thread per entry of the visible list (the ones that are not is_big)

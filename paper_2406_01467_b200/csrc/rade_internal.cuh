@@ -41,6 +41,7 @@ struct DevGauss {
   const float* __restrict__ rot;
   const float* __restrict__ opac;
   const float* __restrict__ sh;
+  const float* __restrict__ filter3d;  // NULL, or the 3D filter size per Gaussian (reading S23)
 };
 
 struct DevGrads {

@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
+from typing import Optional
 
 import torch
 
@@ -46,12 +47,14 @@ def _check_f32(name, t, shape=None):
 class Gaussians:
     """Device parameters, one row per Gaussian (include/rade.h rd_gaussians): means [N,3],
     scales [N,3] (activated), rotations [N,4] (raw w,x,y,z), opacities [N] (activated),
-    sh [N,K,3] — the tensor layout of a 3DGS trainer."""
+    sh [N,K,3] — the tensor layout of a 3DGS trainer; optional filter3d [N] (the Mip-Splatting
+    3D filter size, NEXT-3: a constant input, it has no gradient)."""
     means: torch.Tensor
     scales: torch.Tensor
     rotations: torch.Tensor
     opacities: torch.Tensor
     sh: torch.Tensor
+    filter3d: Optional[torch.Tensor] = None
 
     @property
     def n(self):
@@ -66,11 +69,14 @@ class Gaussians:
         _check_f32("sh", self.sh)
         if self.sh.dim() != 3 or self.sh.shape[0] != n or self.sh.shape[2] != 3:
             raise ValueError("sh must be [N, K, 3]")
+        if self.filter3d is not None:
+            _check_f32("filter3d", self.filter3d, (n,))
 
     def c_struct(self):
         self.validate()
         return N.RdGaussians(self.n, int(self.sh.shape[1]), self.means.data_ptr(), self.scales.data_ptr(),
-                             self.rotations.data_ptr(), self.opacities.data_ptr(), self.sh.data_ptr())
+                             self.rotations.data_ptr(), self.opacities.data_ptr(), self.sh.data_ptr(),
+                             None if self.filter3d is None else self.filter3d.data_ptr())
 
     @staticmethod
     def from_numpy(scene, device="cuda"):

@@ -393,3 +393,42 @@ def test_normal_consistency_backward_vs_finite_differences():
     got = gD.cpu().numpy()
     np.testing.assert_allclose(got, fd, rtol=1e-3, atol=1e-3 * np.abs(fd).max())
     assert np.abs(fd).max() > 1e-2
+
+
+# ----------------------------------------------------------------------------- NEXT-3: 3D filter
+
+def test_filter3d_forward_and_backward_parity():
+    """Mip-Splatting 3D filter (reading S23): the GPU with a per-Gaussian filter size equals
+    the oracle on the filtered scene (forward ≤ 1e-4), and its raw-parameter gradients equal
+    the oracle's gradients mapped through the filter's vjp (≤ 1e-3 per class)."""
+    scene, cam, opt = dense_scene(31, 300), sg.camera_identity(64, 64, 64), sg.Options()
+    f = np.random.default_rng(6).uniform(0.005, 0.08, scene.n).astype(np.float32)
+    fs, vjp = oracle.apply_filter3d(scene, f.astype(np.float64))
+    ref = oracle.render(fs, cam, opt)
+    g = P.Gaussians.from_numpy(scene)
+    g.filter3d = torch.as_tensor(f).cuda()
+    out, view = P.render(g, cam, opts_dict(opt))
+    torch.cuda.synchronize()
+    gpu = {k: v.double().cpu().numpy() for k, v in out.items()}
+    ok = (ref["flags"] & (F1 | F3)) == 0
+    assert ok.mean() > 0.95
+    for k in ("color", "normal"):
+        assert np.abs(gpu[k] - ref[k])[:, ok].max() <= TOL, k
+    assert np.abs(gpu["alpha"] - ref["alpha"])[ok].max() <= TOL
+    okd = (ref["flags"] & (F1 | F3 | F4 | F5)) == 0
+    assert np.abs(gpu["depth"] - ref["depth"])[okd].max() <= TOL
+    cot = sg.cotangents(7, 64, 64)
+    cot = {k: (v * (ref["flags"] == 0)).astype(np.float32) for k, v in cot.items()}
+    c = {k: torch.as_tensor(v).contiguous().cuda() for k, v in cot.items()}
+    grads = g.zeros_like()
+    P.rd_render_bwd(view, g, c["color"], c["depth"], c["normal"], c["alpha"], grads)
+    torch.cuda.synchronize()
+    G = grads_to_rows(grads, scene.n)
+    pg = oracle.project(fs, cam, opt)
+    vis = np.nonzero(pg[:, 0] == 1)[0]
+    R = vjp(oracle.grad(fs, cam, opt, cot, vis), vis)
+    for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
+                     "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
+        nb = np.linalg.norm(R[:, sl])
+        assert nb > 0
+        assert np.linalg.norm(G[vis, sl] - R[:, sl]) / nb <= 1e-3, name
