@@ -697,3 +697,61 @@ def test_filter3d_gradient_vjp_vs_finite_differences(O):
         fd = (loss(sp) - loss(sm)) / (2 * h)
         col = {0: 3, 1: 5, 2: 10}[j]
         assert G[col] == pytest.approx(fd, rel=2e-4, abs=1e-7), (arr, idx)
+
+
+# ----------------------------------------------------------------------------- TSDF (S24)
+
+def _tsdf_cam():
+    return sg.Camera(60.0, 60.0, 32.0, 24.0, 64, 48, np.eye(3, dtype=np.float32), np.zeros(3, np.float32), 0.2)
+
+
+def test_tsdf_plane_zero_crossing(O):
+    """Reading S24: fusing the depth map of a fronto-parallel plane at depth d
+    gives tsdf = (d − z)/τ exactly wherever |d − z| < τ, so each z-column's zero crossing
+    lies at d (within ½ voxel of the voxel centres)."""
+    cam = _tsdf_cam()
+    d, vs = 2.03, 0.02
+    tau = 4 * vs
+    dims = (40, 10, 12)  # Z, Y, X
+    tsdf, w = np.ones(dims), np.zeros(dims)
+    origin = (-0.12, -0.1, 1.6)
+    O.tsdf_integrate(tsdf, w, origin, vs, tau, 100.0, np.full((48, 64), d), cam)
+    zc = origin[2] + (np.arange(dims[0]) + 0.5) * vs
+    band = np.abs(d - zc) < tau
+    assert (w[band] == 1).all()
+    np.testing.assert_allclose(tsdf[band], np.broadcast_to(((d - zc[band]) / tau)[:, None, None],
+                                                           (band.sum(), 10, 12)), atol=1e-6)
+    col = tsdf[:, 5, 6]
+    k = np.nonzero((col[:-1] > 0) & (col[1:] <= 0))[0][0]
+    zero = zc[k] + col[k] / (col[k] - col[k + 1]) * vs
+    assert abs(zero - d) < 0.5 * vs
+    assert (w[zc < d - tau - 1e-6] == 1).all() and (w[zc > d + tau + 1e-6] == 0).all()
+
+
+def test_tsdf_holes_twice_and_order(O):
+    """Holes leave the volume unchanged; the same map twice gives the same tsdf and doubled
+    weights; the weighted average does not depend on the view order."""
+    cam = _tsdf_cam()
+    rng = np.random.default_rng(0)
+    dims, vs = (20, 12, 14), 0.05
+    origin = (-0.35, -0.3, 1.5)
+    t0, w0 = np.ones(dims), np.zeros(dims)
+    O.tsdf_integrate(t0, w0, origin, vs, 0.2, 100.0, np.zeros((48, 64)), cam)
+    assert (w0 == 0).all() and (t0 == 1).all()
+    D1 = 2.0 + 0.1 * rng.random((48, 64))
+    D2 = 2.1 + 0.1 * rng.random((48, 64))
+    a, wa = np.ones(dims), np.zeros(dims)
+    O.tsdf_integrate(a, wa, origin, vs, 0.2, 100.0, D1, cam)
+    b, wb = a.copy(), wa.copy()
+    O.tsdf_integrate(b, wb, origin, vs, 0.2, 100.0, D1, cam)
+    np.testing.assert_allclose(b, a, atol=1e-15)
+    np.testing.assert_array_equal(wb, 2 * wa)
+    c, wc = np.ones(dims), np.zeros(dims)
+    d, wd = np.ones(dims), np.zeros(dims)
+    for D in (D1, D2):
+        O.tsdf_integrate(c, wc, origin, vs, 0.2, 100.0, D, cam)
+    for D in (D2, D1):
+        O.tsdf_integrate(d, wd, origin, vs, 0.2, 100.0, D, cam)
+    np.testing.assert_allclose(c, d, atol=1e-12)
+    np.testing.assert_array_equal(wc, wd)
+    assert (wc == 2).sum() > 100
