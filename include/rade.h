@@ -235,6 +235,27 @@ rd_status rd_normal_consistency_bwd(const rd_camera* cam, const float* depth, co
                                     const float* dL_dconsistency, float* dL_ddepth, float* dL_dalpha,
                                     float* dL_dnormal, rd_stream stream);
 
+/* NEXT-4: TSDF fusion of rendered median depth maps (reading S24). The volume
+ * is a [Z][Y][X] grid of fp32 tsdf and weight (DEVICE, caller-owned, initialise weight = 0);
+ * voxel (i, j, k) has its centre at origin + (i+½, j+½, k+½)·voxel_size. Each view updates
+ * every voxel that is in front of the camera (z_c > znear), projects into the image and
+ * finds a depth sample 0 < D ≤ max_depth with sdf = D − z_c > −truncation:
+ * tsdf ← (w·tsdf + clamp(sdf/truncation, −1, 1))/(w + 1), w ← w + 1. Views are applied in
+ * order; up to 32 views per kernel launch are fused (one read and one write of the volume per
+ * 32 views). depths: DEVICE [n_views][H][W] (0 = hole), all cameras the same width/height;
+ * cams: HOST array of n_views cameras. Marching-cubes extraction is not part of the library. */
+typedef struct rd_tsdf {
+  float origin[3];
+  float voxel_size;
+  int32_t dims[3];  /* X, Y, Z */
+  float truncation; /* e.g. 4 voxel_size */
+  float max_depth;  /* samples farther than this are ignored */
+  float* tsdf;      /* [Z][Y][X] */
+  float* weight;    /* [Z][Y][X] */
+} rd_tsdf;
+rd_status rd_tsdf_integrate(const rd_tsdf* volume, const float* depths, const rd_camera* cams, int32_t n_views,
+                            rd_stream stream);
+
 /* Profiling: when enabled, every kernel launch of this view is bracketed by CUDA events on
  * its stream and K3/K4 count the pairs they evaluate (a few atomics per warp). Enabling
  * or disabling resets the accumulators. rd_get_timings synchronises on the recorded

@@ -251,7 +251,8 @@ def tsdf_integrate(tsdf, weight, origin, voxel, trunc, max_depth, depth, cam):
     sdf = D − z_c > −trunc: tsdf ← (w·tsdf + clamp(sdf/trunc, −1, 1))/(w + 1), w ← w + 1.
     The voxel centre, X_c and (u, v) are formed in fp32 in a fixed operation order (no fused
     multiply-add), so the pixel choice is the same decision on both sides; the update is
-    fp64. tsdf, weight: float64 [Z, Y, X] updated in place."""
+    fp64 (so is sdf = D − z_c and its truncation test, a decision). tsdf, weight: float64
+    [Z, Y, X] updated in place."""
     f = np.float32
     Z, Y, X = tsdf.shape
     o = np.asarray(origin, f)
@@ -274,11 +275,11 @@ def tsdf_integrate(tsdf, weight, origin, voxel, trunc, max_depth, depth, cam):
     ok &= (u >= 0) & (v >= 0) & (u < f(cam.width)) & (v < f(cam.height))
     px = np.where(ok, np.floor(u), 0).astype(np.int64)
     py = np.where(ok, np.floor(v), 0).astype(np.int64)
-    D = np.asarray(depth, np.float64)[py, px]
-    ok &= (D > 0) & (D <= max_depth)
-    sdf = D - zc.astype(np.float64)
-    ok &= sdf > -trunc
-    new = np.clip(sdf / trunc, -1.0, 1.0)
+    D = np.asarray(depth, f)[py, px]
+    ok &= (D > 0) & (D <= f(max_depth))
+    sdf = D - zc  # fp32, the one decision both sides take in the same precision
+    ok &= sdf > -f(trunc)
+    new = np.clip(sdf.astype(np.float64) / trunc, -1.0, 1.0)
     tsdf[ok] = (weight[ok] * tsdf[ok] + new[ok]) / (weight[ok] + 1.0)
     weight[ok] += 1.0
 

@@ -44,6 +44,12 @@ class RdGrads(ctypes.Structure):
                 ("opacities", ctypes.c_void_p), ("sh", ctypes.c_void_p)]
 
 
+class RdTsdf(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_float * 3), ("voxel_size", ctypes.c_float), ("dims", ctypes.c_int32 * 3),
+                ("truncation", ctypes.c_float), ("max_depth", ctypes.c_float), ("tsdf", ctypes.c_void_p),
+                ("weight", ctypes.c_void_p)]
+
+
 class RdFwdMaps(ctypes.Structure):
     _fields_ = [("color", ctypes.c_void_p), ("depth", ctypes.c_void_p), ("normal", ctypes.c_void_p),
                 ("alpha", ctypes.c_void_p), ("distortion", ctypes.c_void_p)]
@@ -90,6 +96,7 @@ SIGNATURES = {
     "rd_blend_bwd": ([_VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_render_fwd_ex": ([_VP, ctypes.POINTER(RdFwdMaps), _VP], ctypes.c_int),
     "rd_normal_consistency": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
+    "rd_tsdf_integrate": ([ctypes.POINTER(RdTsdf), _VP, ctypes.POINTER(RdCamera), ctypes.c_int32, _VP], ctypes.c_int),
     "rd_normal_consistency_bwd": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_blend_bwd_ex": ([_VP, ctypes.POINTER(RdBwdCotangents), _VP], ctypes.c_int),
     "rd_preprocess_bwd": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 using namespace rade;
@@ -517,6 +518,40 @@ rd_status rd_normal_consistency_bwd(const rd_camera* cam, const float* depth, co
   launch_normal_consistency_bwd(cam->fx, cam->fy, cam->cx, cam->cy, cam->width, cam->height, depth, normal,
                                 dL_dconsistency, dL_ddepth, dL_dalpha, dL_dnormal, (cudaStream_t)stream);
   RD_CHECK_LAUNCH("normal_consistency_bwd");
+  return RD_OK;
+}
+
+rd_status rd_tsdf_integrate(const rd_tsdf* vol, const float* depths, const rd_camera* cams, int32_t n_views,
+                            rd_stream stream) {
+  g_err.clear();
+  if (!vol || (n_views > 0 && (!depths || !cams))) return fail(RD_ERR_INVALID_ARGUMENT, "NULL volume/depths/cams");
+  if (n_views < 0) return fail(RD_ERR_INVALID_ARGUMENT, "n_views < 0");
+  if (vol->dims[0] < 0 || vol->dims[1] < 0 || vol->dims[2] < 0) return fail(RD_ERR_INVALID_ARGUMENT, "negative dims");
+  if ((int64_t)vol->dims[0] * vol->dims[1] * vol->dims[2] > 0 && (!vol->tsdf || !vol->weight))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL tsdf/weight");
+  if (!(vol->voxel_size > 0.f) || !(vol->truncation > 0.f))
+    return fail(RD_ERR_INVALID_ARGUMENT, "voxel_size and truncation must be > 0");
+  const int W = n_views > 0 ? cams[0].width : 0, H = n_views > 0 ? cams[0].height : 0;
+  for (int v = 0; v < n_views; ++v) {
+    if (cams[v].width != W || cams[v].height != H)
+      return fail(RD_ERR_INVALID_ARGUMENT, "all cameras must have the same width/height");
+    if (!(cams[v].fx > 0.f && cams[v].fy > 0.f)) return fail(RD_ERR_INVALID_ARGUMENT, "fx, fy must be > 0");
+  }
+  const int per = tsdf_views_per_launch();
+  std::vector<float> rows(17 * (size_t)per);
+  for (int v0 = 0; v0 < n_views; v0 += per) {
+    const int nv = std::min(per, n_views - v0);
+    for (int k = 0; k < nv; ++k) {
+      const rd_camera& c = cams[v0 + k];
+      float* r = rows.data() + 17 * k;
+      for (int j = 0; j < 9; ++j) r[j] = c.R[j];
+      for (int j = 0; j < 3; ++j) r[9 + j] = c.t[j];
+      r[12] = c.fx; r[13] = c.fy; r[14] = c.cx; r[15] = c.cy; r[16] = c.znear;
+    }
+    launch_tsdf_integrate(rows.data(), nv, depths + (size_t)v0 * W * H, W, H, vol->origin, vol->voxel_size,
+                          vol->truncation, vol->max_depth, vol->dims, vol->tsdf, vol->weight, (cudaStream_t)stream);
+    RD_CHECK_LAUNCH("tsdf_integrate");
+  }
   return RD_OK;
 }
 

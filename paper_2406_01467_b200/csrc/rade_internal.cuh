@@ -203,6 +203,12 @@ void launch_normal_consistency(float fx, float fy, float cx, float cy, int W, in
 void launch_normal_consistency_bwd(float fx, float fy, float cx, float cy, int W, int H, const float* depth,
                                    const float* normal, const float* gL, float* gD, float* gA, float* gN,
                                    cudaStream_t s);
+// NEXT-4 (tsdf.cu): fuse n_views ≤ tsdf_views_per_launch() depth maps [n_views][H][W]; cam_rows
+// = n_views × 17 floats (R[9], t[3], fx, fy, cx, cy, znear); dims = X, Y, Z; tsdf/weight [Z][Y][X].
+int tsdf_views_per_launch();
+void launch_tsdf_integrate(const float* cam_rows, int n_views, const float* depths, int W, int H, const float origin[3],
+                           float voxel, float trunc, float max_depth, const int dims[3], float* tsdf, float* weight,
+                           cudaStream_t s);
 // debug: 64-bit keys (tile << 32 | float_bits(z_c)) of the sorted list
 void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,
                    cudaStream_t s);

@@ -273,6 +273,45 @@ def rd_normal_consistency_bwd(camera, depth, normal, dL_dconsistency, dL_ddepth=
                                                _stream_ptr(stream)), "rd_normal_consistency_bwd")
 
 
+class TsdfVolume:
+    """NEXT-4: a TSDF volume on the device ([Z][Y][X] fp32 tsdf and weight; reading S24)."""
+
+    def __init__(self, origin, voxel_size, dims_xyz, truncation=None, max_depth=1e30, device="cuda"):
+        self.origin = tuple(float(v) for v in origin)
+        self.voxel_size = float(voxel_size)
+        self.dims = tuple(int(v) for v in dims_xyz)
+        self.truncation = float(truncation if truncation is not None else 4 * voxel_size)
+        self.max_depth = float(max_depth)
+        X, Y, Z = self.dims
+        self.tsdf = torch.ones((Z, Y, X), dtype=torch.float32, device=device)
+        self.weight = torch.zeros((Z, Y, X), dtype=torch.float32, device=device)
+
+    def c_struct(self):
+        s = N.RdTsdf()
+        for k in range(3):
+            s.origin[k] = self.origin[k]
+            s.dims[k] = self.dims[k]
+        s.voxel_size, s.truncation, s.max_depth = self.voxel_size, self.truncation, self.max_depth
+        s.tsdf, s.weight = self.tsdf.data_ptr(), self.weight.data_ptr()
+        return s
+
+
+def rd_tsdf_integrate(volume: TsdfVolume, depths, cameras, stream=None):
+    """Fuses depth maps [V, H, W] (device fp32, 0 = hole) rendered from `cameras` (V)."""
+    depths = depths.contiguous()
+    if depths.dim() == 2:
+        depths = depths[None]
+    _check_f32("depths", depths)
+    V = depths.shape[0]
+    if len(cameras) != V:
+        raise ValueError("one camera per depth map")
+    cams = (N.RdCamera * max(V, 1))(*[camera_struct(c) for c in cameras])
+    s = volume.c_struct()
+    N.check(N.load().rd_tsdf_integrate(ctypes.byref(s), _ptr(depths), cams, V, _stream_ptr(stream)),
+            "rd_tsdf_integrate")
+    return volume
+
+
 def _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha):
     H, W = view.camera.height, view.camera.width
     for name, t, shp in (("dL_dcolor", dL_dcolor, (3, H, W)), ("dL_ddepth", dL_ddepth, (H, W)),

@@ -432,3 +432,33 @@ def test_filter3d_forward_and_backward_parity():
         nb = np.linalg.norm(R[:, sl])
         assert nb > 0
         assert np.linalg.norm(G[vis, sl] - R[:, sl]) / nb <= 1e-3, name
+
+
+# ----------------------------------------------------------------------------- NEXT-4: TSDF
+
+def _fuse_both(depths, cams, origin, vs, dims, trunc, max_depth=1e30):
+    vol = P.TsdfVolume(origin, vs, dims, trunc, max_depth)
+    D = torch.as_tensor(np.asarray(depths, np.float32)).contiguous().cuda()
+    P.rd_tsdf_integrate(vol, D, cams)
+    torch.cuda.synchronize()
+    X, Y, Z = dims
+    t, w = np.ones((Z, Y, X)), np.zeros((Z, Y, X))
+    for k, cam in enumerate(cams):
+        oracle.tsdf_integrate(t, w, origin, vs, trunc, max_depth, np.asarray(depths[k], np.float32), cam)
+    return vol.tsdf.double().cpu().numpy(), vol.weight.double().cpu().numpy(), t, w
+
+
+def test_tsdf_fusion_parity():
+    """TSDF fusion (reading S24) of the GPU's median depth maps of a scene seen from 40 views
+    (two kernel launches of up to 32 fused views): weights bit-exact, tsdf ≤ 1e-5."""
+    scene = dense_scene(41, 300)
+    cams = []
+    for k in range(40):
+        a = 2 * np.pi * k / 40
+        R, t = sg.look_at([0.8 * np.cos(a), 0.8 * np.sin(a), -0.5], [0.0, 0.0, 4.0], up=(0, -1, 0))
+        cams.append(sg.Camera(64.0, 64.0, 32.0, 32.0, 64, 64, R, t, 0.2))
+    depths = [gpu_forward(scene, c, sg.Options())[0]["depth"] for c in cams]
+    g, wg, t, w = _fuse_both(depths, cams, (-2.0, -2.0, 2.0), 0.05, (80, 80, 80), 0.2, 50.0)
+    np.testing.assert_array_equal(wg, w)
+    assert (w > 0).sum() > 5000 and w.max() > 20
+    np.testing.assert_allclose(g[w > 0], t[w > 0], atol=1e-5)
