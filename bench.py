@@ -532,7 +532,7 @@ def main():
     ap.add_argument("--distortion", action="store_true", help="NEXT-1: also render L_d and back-propagate it")
     ap.add_argument("--normal-consistency", action="store_true",
                     help="NEXT-2: also compute L_n on the maps and back-propagate it")
-    ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the views are pipelined over")
+    ap.add_argument("--pipeline", type=int, default=3, help="CUDA streams the views are pipelined over")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
