@@ -21,9 +21,13 @@ F1, F3, F4, F5 = 1, 4, 8, 16
 TOL = 1e-4
 
 
+BENCH_TILE = 8  # bench.py's default blend tile
+
+
 @pytest.fixture(scope="module")
 def c3():
     scene, cams, opt = sg.config_scene_and_cameras("C3")
+    opt.tile = BENCH_TILE
     cam = cams[0]
     g = P.Gaussians.from_numpy(scene)
     out, view = P.render(g, cam, opts_dict(opt))
@@ -202,3 +206,28 @@ def test_c3_distortion_sampled_pixels(c3):
     assert ok.mean() > 0.8 and ref["distortion"].max() > 1e-3
     err = np.abs(L[ys, xs] - ref["distortion"])[ok]
     assert err.max() <= TOL * max(1.0, np.abs(ref["distortion"][ok]).max()), err.max()
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4"])
+def test_other_configs_forward_sampled_pixels(cfg):
+    """The other BASELINE.json configurations at full size (C1 800×800 300k with a white
+    background, C2 1600×1200 400k, C4 1237×822 3M): 32 random pixels of view 0 vs the
+    oracle."""
+    scene, cams, opt = sg.config_scene_and_cameras(cfg)
+    opt.tile = BENCH_TILE
+    cam = cams[0]
+    g = P.Gaussians.from_numpy(scene)
+    out, _ = P.render(g, cam, opts_dict(opt))
+    torch.cuda.synchronize()
+    gpu = {k: v.double().cpu().numpy() for k, v in out.items()}
+    rng = np.random.default_rng(13)
+    pix = rng.choice(cam.width * cam.height, 32, replace=False)
+    ref = oracle.render(scene, cam, opt, pixels=pix)
+    ys, xs = pix // cam.width, pix % cam.width
+    ok = (ref["flags"] & (F1 | F3)) == 0
+    assert ok.mean() > 0.8
+    for k in ("color", "normal"):
+        assert np.abs(gpu[k][:, ys, xs] - ref[k])[:, ok].max() <= TOL, (cfg, k)
+    assert np.abs(gpu["alpha"][ys, xs] - ref["alpha"])[ok].max() <= TOL
+    okd = (ref["flags"] & (F1 | F3 | F4 | F5)) == 0
+    assert np.abs(gpu["depth"][ys, xs] - ref["depth"])[okd].max() <= TOL
