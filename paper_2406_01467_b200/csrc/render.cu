@@ -46,15 +46,14 @@ __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool insi
   s.done = !inside;
 }
 
-// One (pixel, splat) step of Eq.3 with the median-depth selection of reading S9, and with
-// DIST the depth-distortion sums of reading S21 (centred on the first blended depth d0, so
-// L_d = 2(A·D2 − D1²) loses no digits to cancellation: it is shift invariant).
+// The blend part of one (pixel, splat) step of Eq.3 (pair_power established α ≥ α_min, S8)
+// with the median-depth selection of reading S9, and with DIST the depth-distortion sums of
+// reading S21 (centred on the first blended depth d0, so L_d = 2(A·D2 − D1²) loses no digits
+// to cancellation: it is shift invariant). a3 = the record's r3 (z_c, p0, p1, ·) when DIST,
+// else read from shared memory (a3addr) only at the median splat.
 template <bool PROF, bool DIST>
-__device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4& a1, const float4& a2,
-                                         const float4& a3, float2 ulo, int pos, const DevOpt& opt) {
-  const PairAlpha pa = pair_power(a0, a1.x, a1.y, ulo, s.px, s.py, opt.log2_alpha_min);
-  if (PROF) ++s.n_eval;
-  if (!pa.pass) return;  // α < α_min: skipped (S8)
+__device__ __forceinline__ void fwd_blend(PixF& s, const PairAlpha& pa, const float4& a1, const float4& a2,
+                                          const float4& a3in, unsigned a3addr, int pos, const DevOpt& opt) {
   const float alpha = fminf(opt.alpha_max, ex2_approx(pa.e));
   const float Tn = __fmul_rn(s.T, __fsub_rn(1.f, alpha));
   if (Tn < opt.T_min) {  // stop before blending this splat (S8)
@@ -68,12 +67,13 @@ __device__ __forceinline__ void fwd_step(PixF& s, const float4& a0, const float4
   s.N0 = __fmaf_rn(w, a2.y, s.N0);
   s.N1 = __fmaf_rn(w, a2.z, s.N1);
   s.N2 = __fmaf_rn(w, a2.w, s.N2);
-  if (s.T > opt.median_T && Tn <= opt.median_T) {  // a3 = (z_c, p0, p1, ·)
+  if (s.T > opt.median_T && Tn <= opt.median_T) {
+    const float4 a3 = DIST ? a3in : lds128(a3addr);  // (z_c, p0, p1, ·)
     s.D = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
     s.med = pos;
   }
   if (DIST) {  // d of Eq.15 for this splat (the median channel's depth)
-    const float d = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
+    const float d = __fmaf_rn(a3in.y, pa.dx, __fmaf_rn(a3in.z, pa.dy, a3in.x));
     if (s.last == 0) s.d0 = d;
     const float e = d - s.d0;
     s.D1 = fmaf(w, e, s.D1);
@@ -231,15 +231,24 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                            opt.log2_alpha_min, wlist[warp])
                              : cnt;
     const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
-    for (int i = 0; i < nsel; ++i) {
-      if (A.done && B.done) break;
+    for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
+      if (__all_sync(0xffffffffu, A.done && B.done)) break;
       const int j = kFilter ? (int)wlist[warp][i] : i;
       const unsigned a = a_s0 + 16u * j;
-      const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH), a2 = lds128(a + 32u * BATCH),
-                   a3 = lds128(a + 48u * BATCH);
-      const float2 ulo = uv_lo(a3.w);
-      if (!A.done) fwd_step<PROF, DIST>(A, a0, a1, a2, a3, ulo, base + j, opt);
-      if (!B.done) fwd_step<PROF, DIST>(B, a0, a1, a2, a3, ulo, base + j, opt);
+      const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
+      const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
+      const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, A.px, A.py, opt.log2_alpha_min);
+      const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, B.px, B.py, opt.log2_alpha_min);
+      if (PROF) {
+        A.n_eval += A.done ? 0u : 1u;
+        B.n_eval += B.done ? 0u : 1u;
+      }
+      const bool okA = !A.done && pA.pass, okB = !B.done && pB.pass;  // α ≥ α_min (S8)
+      if (!__any_sync(0xffffffffu, okA || okB)) continue;  // no pixel of the warp blends it
+      const float4 a2 = lds128(a + 32u * BATCH);
+      const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;
+      if (okA) fwd_blend<PROF, DIST>(A, pA, a1, a2, a3, a + 48u * BATCH, base + j, opt);
+      if (okB) fwd_blend<PROF, DIST>(B, pB, a1, a2, a3, a + 48u * BATCH, base + j, opt);
     }
   }
   if (PROF) {
