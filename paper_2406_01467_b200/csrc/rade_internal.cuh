@@ -136,12 +136,23 @@ struct PairAlpha {
 __device__ __forceinline__ float2 uv_lo(float w) { return __half22float2(*reinterpret_cast<const __half2*>(&w)); }
 // dx = (u_hi − px) + u_lo: the first difference is exact or carries |dx|-relative rounding
 // only, so Δ is accurate to ~1e-7·|Δ| + the half rounding of u_lo (< 3e-8 px).
-__device__ __forceinline__ PairAlpha pair_power(const float4& r0, float g22, float lo, float2 ulo, float px, float py,
-                                                float log2_alpha_min) {
+// A thread's pixels share their column: the column terms dx and g11·dx come from
+// pair_column once per splat, pair_power adds the row terms per pixel.
+struct PairColumn {
+  float dx, g11dx;
+};
+__device__ __forceinline__ PairColumn pair_column(const float4& r0, float2 ulo, float px) {
+  PairColumn c;
+  c.dx = __fadd_rn(__fsub_rn(r0.x, px), ulo.x);
+  c.g11dx = __fmul_rn(r0.z, c.dx);
+  return c;
+}
+__device__ __forceinline__ PairAlpha pair_power(const float4& r0, float g22, float lo, float2 ulo,
+                                                const PairColumn& col, float py, float log2_alpha_min) {
   PairAlpha pa;
-  pa.dx = __fadd_rn(__fsub_rn(r0.x, px), ulo.x);
+  pa.dx = col.dx;
   pa.dy = __fadd_rn(__fsub_rn(r0.y, py), ulo.y);
-  const float t1 = __fmaf_rn(r0.z, pa.dx, __fmul_rn(r0.w, pa.dy));  // g11 dx + g21 dy
+  const float t1 = __fmaf_rn(r0.w, pa.dy, col.g11dx);  // g11 dx + g21 dy
   const float t2 = __fmul_rn(g22, pa.dy);
   const float pw = __fmaf_rn(t1, t1, __fmul_rn(t2, t2));
   pa.e = __fsub_rn(lo, pw);

@@ -237,8 +237,9 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
-      const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, A.px, A.py, opt.log2_alpha_min);
-      const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, B.px, B.py, opt.log2_alpha_min);
+      const PairColumn col = pair_column(a0, ulo, A.px);  // A and B share the column
+      const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, col, A.py, opt.log2_alpha_min);
+      const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, col, B.py, opt.log2_alpha_min);
       if (PROF) {
         A.n_eval += A.done ? 0u : 1u;
         B.n_eval += B.done ? 0u : 1u;
@@ -493,12 +494,13 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
+      const PairColumn col = pair_column(a0, ulo, s[0].px);  // the thread's pixels share the column
       PairAlpha pa[PPT];
       bool act[PPT];
       bool any = false;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        pa[k] = pair_power(a0, a1.x, a1.y, ulo, s[k].px, s[k].py, opt.log2_alpha_min);
+        pa[k] = pair_power(a0, a1.x, a1.y, ulo, col, s[k].py, opt.log2_alpha_min);
         act[k] = pos < s[k].last && pa[k].pass;
         any = any || act[k];
       }
