@@ -284,6 +284,113 @@ def tsdf_integrate(tsdf, weight, origin, voxel, trunc, max_depth, depth, cam):
     weight[ok] += 1.0
 
 
+# Marching cubes ("with the Marching Cube algorithm"; reading S25). The cube's corner
+# c ∈ 0..7 sits at (c & 1, c >> 1 & 1, c >> 2 & 1); inside = value < iso.
+_MC_EDGES = [(0, 1), (2, 3), (4, 5), (6, 7), (0, 2), (1, 3), (4, 6), (5, 7), (0, 4), (1, 5), (2, 6), (3, 7)]
+# faces as corner cycles, counter-clockwise seen from outside the cube
+_MC_FACES = [(0, 4, 6, 2), (1, 3, 7, 5), (0, 1, 5, 4), (2, 6, 7, 3), (0, 2, 3, 1), (4, 5, 7, 6)]
+_mc_cache = None
+
+
+def mc_table():
+    """Triangles (as edge triples) of every corner configuration, built by walking the cube
+    faces: on each face, every maximal run of inside corners is cut off by one segment from
+    the crossing entering the run to the crossing leaving it (so diagonal inside corners are
+    separated, a choice that depends on the face alone and so agrees between the two cubes
+    sharing it — watertight); the segments chain into loops through the crossing edges;
+    each loop is fanned into triangles, oriented so their normal points from the inside
+    corners to the outside ones. Returns a list of 256 lists of (e0, e1, e2)."""
+    global _mc_cache
+    if _mc_cache is not None:
+        return _mc_cache
+    pos = np.array([[c & 1, (c >> 1) & 1, (c >> 2) & 1] for c in range(8)], np.float64)
+    eid = {}
+    for k, (a, b) in enumerate(_MC_EDGES):
+        eid[(a, b)] = eid[(b, a)] = k
+    mid = np.array([(pos[a] + pos[b]) / 2 for a, b in _MC_EDGES])
+    table = []
+    for cfg in range(256):
+        ins = [(cfg >> c) & 1 == 1 for c in range(8)]
+        nxt = {}
+        for f in _MC_FACES:
+            for i in range(4):
+                if ins[f[i]] and not ins[f[i - 1]]:  # a run of inside corners starts at f[i]
+                    enter = eid[(f[i - 1], f[i])]
+                    j = i
+                    while ins[f[(j + 1) % 4]]:
+                        j += 1
+                    leave = eid[(f[j % 4], f[(j + 1) % 4])]
+                    nxt[enter] = leave
+        tris = []
+        seen = set()
+        inside_c = pos[[c for c in range(8) if ins[c]]].mean(0) if any(ins) else None
+        outside_c = pos[[c for c in range(8) if not ins[c]]].mean(0) if not all(ins) else None
+        for start in sorted(nxt):
+            if start in seen:
+                continue
+            loop = [start]
+            seen.add(start)
+            e = nxt[start]
+            while e != start:
+                loop.append(e)
+                seen.add(e)
+                e = nxt[e]
+            pts = mid[loop]
+            nrm = np.zeros(3)  # Newell normal of the loop
+            for k in range(len(loop)):
+                p, q = pts[k], pts[(k + 1) % len(loop)]
+                nrm += np.array([(p[1] - q[1]) * (p[2] + q[2]), (p[2] - q[2]) * (p[0] + q[0]),
+                                 (p[0] - q[0]) * (p[1] + q[1])])
+            if nrm @ (outside_c - inside_c) < 0:
+                loop = loop[::-1]
+            for k in range(1, len(loop) - 1):
+                tris.append((loop[0], loop[k], loop[k + 1]))
+        table.append(tris)
+    _mc_cache = table
+    return table
+
+
+def marching_cubes(tsdf, weight, origin, voxel, iso=0.0):
+    """Triangle soup of the iso-surface of a [Z][Y][X] volume (reading S25): cells between
+    voxel centres (origin + (i+½)·voxel), skipped when a corner has weight 0; per cell the
+    table's triangles, each vertex linearly interpolated on its edge,
+    p = p_a + (iso − v_a)/(v_b − v_a)·(p_b − p_a). Order: cells with x fastest, then y, z;
+    triangles in table order. Returns float64 [T, 3, 3] (vertex positions)."""
+    table = mc_table()
+    t = np.asarray(tsdf, np.float32)
+    w = np.asarray(weight)
+    Z, Y, X = t.shape
+    out = []
+    cx = lambda i: origin[0] + (i + 0.5) * voxel
+    cy = lambda j: origin[1] + (j + 0.5) * voxel
+    cz = lambda k: origin[2] + (k + 0.5) * voxel
+    corners = [(c & 1, (c >> 1) & 1, (c >> 2) & 1) for c in range(8)]
+    for k in range(Z - 1):
+        for j in range(Y - 1):
+            for i in range(X - 1):
+                vals, ok, cfg = [], True, 0
+                for c, (dx, dy, dz) in enumerate(corners):
+                    if w[k + dz, j + dy, i + dx] == 0:
+                        ok = False
+                        break
+                    v = float(t[k + dz, j + dy, i + dx])
+                    vals.append(v)
+                    if v < iso:
+                        cfg |= 1 << c
+                if not ok or cfg == 0 or cfg == 255:
+                    continue
+                for tri in table[cfg]:
+                    tv = []
+                    for e in tri:
+                        a, b = _MC_EDGES[e]
+                        pa = np.array([cx(i + corners[a][0]), cy(j + corners[a][1]), cz(k + corners[a][2])])
+                        pb = np.array([cx(i + corners[b][0]), cy(j + corners[b][1]), cz(k + corners[b][2])])
+                        s = (iso - vals[a]) / (vals[b] - vals[a])
+                        tv.append(pa + s * (pb - pa))
+                    out.append(tv)
+    return np.array(out, np.float64).reshape(-1, 3, 3)
+
+
 def depth_normal(depth, cam):
     """Normal from the depth map by finite differences ("applying finite
     difference on the depth map"; reading S22 = SPEC:309-316): back-project the pixel centre

@@ -755,3 +755,57 @@ def test_tsdf_holes_twice_and_order(O):
     np.testing.assert_allclose(c, d, atol=1e-12)
     np.testing.assert_array_equal(wc, wd)
     assert (wc == 2).sum() > 100
+
+
+# ----------------------------------------------------------------------------- marching cubes (S25)
+
+def _sphere_volume(n=28, vs=0.1, R=0.9, center=(0.03, -0.02, 0.05)):
+    origin = (-1.4, -1.4, -1.4)
+    c = origin[0] + (np.arange(n) + 0.5) * vs
+    Zc, Yc, Xc = np.meshgrid(c, c, c, indexing="ij")
+    sdf = np.sqrt((Xc - center[0]) ** 2 + (Yc - center[1]) ** 2 + (Zc - center[2]) ** 2) - R
+    tau = 4 * vs
+    return np.clip(sdf / tau, -1, 1).astype(np.float32), np.ones((n, n, n), np.float32), origin, vs, R, center
+
+
+def test_mc_sphere_accuracy_and_watertight(O):
+    """Reading S25: the iso-surface of an analytic sphere's truncated SDF lies on
+    the sphere (mean |d| < 0.05 voxel, max < 0.25 voxel; SPEC's bars are 0.5 / 1.5), and the
+    triangle soup is a closed, consistently oriented surface: after merging equal vertices
+    every directed edge occurs exactly once and its reverse exactly once; normals point out."""
+    ts, w, origin, vs, R, ctr = _sphere_volume()
+    m = O.marching_cubes(ts, w, origin, vs)
+    assert len(m) > 1000
+    d = np.linalg.norm(m.reshape(-1, 3) - np.array(ctr), axis=1) - R
+    assert np.abs(d).mean() < 0.05 * vs and np.abs(d).max() < 0.25 * vs
+    key = {tuple(np.round(p, 9)) for p in m.reshape(-1, 3)}
+    idx = {p: k for k, p in enumerate(sorted(key))}
+    tri = np.array([[idx[tuple(np.round(p, 9))] for p in t] for t in m])
+    directed = {}
+    for a, b, c in tri:
+        for e in ((a, b), (b, c), (c, a)):
+            directed[e] = directed.get(e, 0) + 1
+    assert all(v == 1 for v in directed.values())
+    assert all(directed.get((b, a), 0) == 1 for (a, b) in directed)
+    nrm = np.cross(m[:, 1] - m[:, 0], m[:, 2] - m[:, 0])
+    outward = np.einsum("ij,ij->i", nrm, m.mean(1) - np.array(ctr))
+    assert (outward > 0).all()
+
+
+def test_mc_plane_and_degenerate(O):
+    """A planar SDF gives triangles whose normals are parallel to the plane normal; an
+    all-positive volume and zero-weight corners give nothing."""
+    n, vs = 12, 0.1
+    origin = (0.0, 0.0, 0.0)
+    c = origin[0] + (np.arange(n) + 0.5) * vs
+    Zc, Yc, Xc = np.meshgrid(c, c, c, indexing="ij")
+    nrm = np.array([0.2, -0.3, 0.93])
+    nrm /= np.linalg.norm(nrm)
+    sdf = (Xc * nrm[0] + Yc * nrm[1] + Zc * nrm[2] - 0.55).astype(np.float32)
+    m = O.marching_cubes(sdf, np.ones_like(sdf), origin, vs)
+    assert len(m) > 50
+    tn = np.cross(m[:, 1] - m[:, 0], m[:, 2] - m[:, 0])
+    tn /= np.linalg.norm(tn, axis=1, keepdims=True)
+    np.testing.assert_allclose(tn, np.broadcast_to(nrm, tn.shape), atol=1e-6)
+    assert len(O.marching_cubes(np.ones_like(sdf), np.ones_like(sdf), origin, vs)) == 0
+    assert len(O.marching_cubes(sdf, np.zeros_like(sdf), origin, vs)) == 0
