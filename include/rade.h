@@ -243,7 +243,7 @@ rd_status rd_normal_consistency_bwd(const rd_camera* cam, const float* depth, co
  * tsdf ← (w·tsdf + clamp(sdf/truncation, −1, 1))/(w + 1), w ← w + 1. Views are applied in
  * order; up to 32 views per kernel launch are fused (one read and one write of the volume per
  * 32 views). depths: DEVICE [n_views][H][W] (0 = hole), all cameras the same width/height;
- * cams: HOST array of n_views cameras. Marching-cubes extraction is not part of the library. */
+ * cams: HOST array of n_views cameras. rd_marching_cubes extracts the mesh afterwards. */
 typedef struct rd_tsdf {
   float origin[3];
   float voxel_size;
@@ -255,6 +255,21 @@ typedef struct rd_tsdf {
 } rd_tsdf;
 rd_status rd_tsdf_integrate(const rd_tsdf* volume, const float* depths, const rd_camera* cams, int32_t n_views,
                             rd_stream stream);
+
+/* NEXT-4: marching cubes on the fused volume ("with the Marching Cube algorithm",
+ * reading S25). Cells join 2×2×2 voxel centres; a cell with a corner of weight 0 is skipped;
+ * corner c (x = c & 1, y = c >> 1 & 1, z = c >> 2 & 1) is inside when tsdf < iso. Each cell's
+ * triangles come from the face-walking table of reading S25 (watertight, normals pointing from
+ * inside to outside, ≤ 5 per cell); a vertex on the edge a→b is
+ * p_a + (iso − v_a)/(v_b − v_a)·(p_b − p_a), in fp32. The output is a triangle soup in cell
+ * order (x fastest, then y, z), triangles in table order: triangles = DEVICE f32
+ * [capacity][3 vertices][xyz], caller-owned. *n_triangles (HOST) receives the count; the
+ * triangles are written only when triangles != NULL and capacity ≥ the count (call once with
+ * NULL to size the buffer). Synchronises `stream` once (to read the count back); uses
+ * stream-ordered temporaries of 8 B per cell. Only volume->{origin, voxel_size, dims, tsdf,
+ * weight} are read. */
+rd_status rd_marching_cubes(const rd_tsdf* volume, float iso, float* triangles, int64_t capacity,
+                            int64_t* n_triangles, rd_stream stream);
 
 /* Profiling: when enabled, every kernel launch of this view is bracketed by CUDA events on
  * its stream and K3/K4 count the pairs they evaluate (a few atomics per warp). Enabling

@@ -97,6 +97,8 @@ SIGNATURES = {
     "rd_render_fwd_ex": ([_VP, ctypes.POINTER(RdFwdMaps), _VP], ctypes.c_int),
     "rd_normal_consistency": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_tsdf_integrate": ([ctypes.POINTER(RdTsdf), _VP, ctypes.POINTER(RdCamera), ctypes.c_int32, _VP], ctypes.c_int),
+    "rd_marching_cubes": ([ctypes.POINTER(RdTsdf), ctypes.c_float, _VP, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                           _VP], ctypes.c_int),
     "rd_normal_consistency_bwd": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_blend_bwd_ex": ([_VP, ctypes.POINTER(RdBwdCotangents), _VP], ctypes.c_int),
     "rd_preprocess_bwd": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librade.so")
 OBJDIR = os.path.join(ROOT, "build", "rade")
-SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu", "regularize.cu", "tsdf.cu"]
+SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu", "regularize.cu", "tsdf.cu", "mcubes.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]

@@ -555,6 +555,23 @@ rd_status rd_tsdf_integrate(const rd_tsdf* vol, const float* depths, const rd_ca
   return RD_OK;
 }
 
+rd_status rd_marching_cubes(const rd_tsdf* vol, float iso, float* triangles, int64_t capacity, int64_t* n_triangles,
+                            rd_stream stream) {
+  g_err.clear();
+  if (!vol || !n_triangles) return fail(RD_ERR_INVALID_ARGUMENT, "NULL volume/n_triangles");
+  if (vol->dims[0] < 0 || vol->dims[1] < 0 || vol->dims[2] < 0) return fail(RD_ERR_INVALID_ARGUMENT, "negative dims");
+  if ((int64_t)vol->dims[0] * vol->dims[1] * vol->dims[2] > 0 && (!vol->tsdf || !vol->weight))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL tsdf/weight");
+  if (!(vol->voxel_size > 0.f)) return fail(RD_ERR_INVALID_ARGUMENT, "voxel_size must be > 0");
+  if (capacity < 0) return fail(RD_ERR_INVALID_ARGUMENT, "capacity < 0");
+  const cudaError_t e = launch_marching_cubes(vol->origin, vol->voxel_size, vol->dims, vol->tsdf, vol->weight, iso,
+                                              triangles, capacity, n_triangles, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue) return fail(RD_ERR_INVALID_ARGUMENT, "volume has more than 2^31 cells");
+  if (e == cudaErrorMemoryAllocation) return fail(RD_ERR_ALLOC, "marching_cubes temporaries");
+  if (e != cudaSuccess) return fail(RD_ERR_CUDA, "marching_cubes: %s", cudaGetErrorString(e));
+  return RD_OK;
+}
+
 rd_status rd_set_profiling(rd_view* v, int32_t enabled) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   if (enabled) {

@@ -220,6 +220,11 @@ int tsdf_views_per_launch();
 void launch_tsdf_integrate(const float* cam_rows, int n_views, const float* depths, int W, int H, const float origin[3],
                            float voxel, float trunc, float max_depth, const int dims[3], float* tsdf, float* weight,
                            cudaStream_t s);
+// NEXT-4 (mcubes.cu): count, scan, emit; synchronises s once. cudaErrorInvalidValue when the
+// volume has ≥ 2^31 cells. triangles: f32 [capacity][3][3], written iff capacity ≥ count.
+cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int dims[3], const float* tsdf,
+                                  const float* weight, float iso, float* triangles, int64_t capacity,
+                                  int64_t* n_triangles, cudaStream_t s);
 // debug: 64-bit keys (tile << 32 | float_bits(z_c)) of the sorted list
 void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,
                    cudaStream_t s);

@@ -312,6 +312,21 @@ def rd_tsdf_integrate(volume: TsdfVolume, depths, cameras, stream=None):
     return volume
 
 
+def rd_marching_cubes(volume: TsdfVolume, iso=0.0, stream=None):
+    """NEXT-4: the iso-surface of the fused volume as a triangle soup [T, 3, 3] (device fp32),
+    cells in x-fastest order (reading S25). Two calls through the C-ABI: count, then emit."""
+    s = volume.c_struct()
+    n = ctypes.c_int64(0)
+    lib = N.load()
+    N.check(lib.rd_marching_cubes(ctypes.byref(s), float(iso), None, 0, ctypes.byref(n), _stream_ptr(stream)),
+            "rd_marching_cubes")
+    tris = torch.empty((n.value, 3, 3), dtype=torch.float32, device=volume.tsdf.device)
+    if n.value:
+        N.check(lib.rd_marching_cubes(ctypes.byref(s), float(iso), _ptr(tris), n.value, ctypes.byref(n),
+                                      _stream_ptr(stream)), "rd_marching_cubes")
+    return tris
+
+
 def _check_cot(view, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha):
     H, W = view.camera.height, view.camera.width
     for name, t, shp in (("dL_dcolor", dL_dcolor, (3, H, W)), ("dL_ddepth", dL_ddepth, (H, W)),

@@ -2,6 +2,7 @@
 
   normal_consistency  L_n forward + backward per view (image-space, HBM-bound)
   tsdf_integrate      fusion of 32 C3 median depth maps into a 256³ volume (HBM-bound)
+  marching_cubes      mesh extraction from that volume (count, scan, emit)
   filter3d            the bench step with the Mip-Splatting 3D filter on (frames/s)
 
     python tools/bench_next.py [--steps K]
@@ -93,6 +94,22 @@ def main():
                       "frac": byts / (ms * 1e-3) / 1e9 / peak,
                       "bytes": "16 B per voxel per launch (tsdf + weight in and out); the depth gathers hit L2",
                       "fused_voxels": int((vol.weight > 0).sum().item())}), flush=True)
+
+    # ---- marching cubes on the fused 256^3 volume (count + scan + emit, one sync)
+    ntri = P.rd_marching_cubes(vol).shape[0]
+
+    def mc():
+        P.rd_marching_cubes(vol)
+
+    ms = timed(mc, max(3, steps // 4))
+    ncell = 255 ** 3
+    byts = ncell * 8 * 2 + ncell * 8 + ntri * 36  # 2 passes × (tsdf, weight) ≈ 8 B/cell (x-neighbours cached), count+offset, out
+    print(json.dumps({"row": "NEXT-4 marching_cubes", "workload": "fused 256^3 volume of 32 C3 views",
+                      "ms": ms, "triangles": ntri, "cells_per_s": ncell / (ms * 1e-3),
+                      "achieved_GBps": byts / (ms * 1e-3) / 1e9, "peak_GBps": peak,
+                      "frac": byts / (ms * 1e-3) / 1e9 / peak,
+                      "bytes": "per cell: tsdf+weight read by count and emit passes, 4-B count + 4-B offset, "
+                               "36 B per triangle out (includes the host round trip of the count)"}), flush=True)
 
     # ---- the step with the 3D filter (forward + backward per view, serial)
     g.filter3d = torch.full((g.n,), 0.004, device="cuda")
