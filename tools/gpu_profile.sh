@@ -4,7 +4,7 @@
 #   usage (under gpurun): bash tools/gpu_profile.sh <tag> [kernel-regex] [extra bench args]
 TAG=${1:-r1}
 KREGEX=${2:-"k_render_bwd|k_render_fwd|k_preprocess_bwd"}
-shift 2 || true
+if [ $# -ge 2 ]; then shift 2; else shift $#; fi
 mkdir -p gpurun_out
 set -x
 timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu_$TAG.log 2>&1
