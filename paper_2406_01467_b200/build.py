@@ -22,6 +22,8 @@ SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu", "regularize.cu"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+# development only: extra -D switches for A/B experiments (tools/gpu_ab.sh)
+FLAGS += os.environ.get("RADE_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _deps_mtime():

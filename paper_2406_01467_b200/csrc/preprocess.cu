@@ -372,8 +372,14 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
 // K1 kernel: per-Gaussian forward (plus the depth-sort input dkey[i], didx[i] = i), then
 // the warp-aggregated append of the visible ids to the visible list (one atomic per warp;
 // list order is arbitrary — K5a, its only user, is order-independent).
+#ifndef RD_K1_MINB
+#define RD_K1_MINB 1
+#endif
+#ifndef RD_K5_MINB
+#define RD_K5_MINB 6  // ≤ 80 registers: more warps in flight for the gathers (K5b 0.206 -> 0.192 ms)
+#endif
 template <int DEG>
-__global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
+__global__ void __launch_bounds__(256, RD_K1_MINB) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
                                                          Record* __restrict__ rec, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
                                                          uint32_t* __restrict__ didx,
@@ -663,7 +669,7 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
 
 // K5b, fp32, one thread per entry of the visible list (the ones that are not is_big)
 // tiles (the others are K5b64's).
-__global__ void __launch_bounds__(128) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
+__global__ void __launch_bounds__(128, RD_K5_MINB) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
                                                         const uint32_t* __restrict__ touched,
                                                         const uint32_t* __restrict__ vis, int64_t n_vis,
                                                         const G2D* __restrict__ g2d, DevGrads gr) {

@@ -17,9 +17,10 @@
 // Epilogue: C += T·bg, A = 1 − T; per pixel state (T_final, n_contrib, median_pos) for K4.
 //
 // K4 replays each pixel's list backwards from n_contrib, reconstructing T_i = T_{i+1}/(1−α_i)
-// and one scalar suffix sum, and produces the 15 per-splat 2-D gradients, which are summed
-// over the thread's two pixels and then warp-reduced (butterfly reduce-scatter) before one
-// L2 atomic per value per (warp, splat).
+// and one scalar suffix sum, and produces the 12 per-splat sums of the 2-D gradients, which
+// are summed over the thread's two pixels and then warp-reduced (through shared memory)
+// before one L2 atomic per value per (warp, splat). At 8×8 tiles K3 leaves a per-tile bit
+// mask of the list positions some pixel blends; K4 stages and visits only those.
 #include "rade_internal.cuh"
 
 namespace rade {
@@ -170,6 +171,17 @@ __device__ __forceinline__ int warp_filter(const float4* s0, const float4* s1, c
   return nsel;
 }
 
+// Blend mask (TILE 8, K3 → K4): bit p of tile t says that some pixel of the tile passes the α
+// test at list position p while still blending (K4's active set is a subset of it: a pixel is
+// active at p iff p < n_contrib and α ≥ α_min, decided bit-identically by both kernels). Tile
+// t's words start at (range.x >> 5) + t, which is past the previous tile's last word
+// ((y >> 5) − (x >> 5) ≥ ⌊(y − x)/32⌋), so K3 writes whole words with plain stores, two per
+// staged batch of 64: word(p) = (range.x >> 5) + t + p / 32, bit p % 32. Batches past K3's
+// early exit are never read (K4 stops at max n_contrib ≤ K3's last position + 1).
+__device__ __forceinline__ unsigned blend_mask_word(unsigned rx, int pos, int tile) {
+  return (rx >> 5) + (unsigned)tile + ((unsigned)pos >> 5);
+}
+
 // K3: one CTA per TILE×TILE tile, TILE²/2 threads; warp w owns the 8×8 quadrant w of the
 // tile (lane l: column l % 8, rows l / 8 and l / 8 + 4). Per staged batch each warp first
 // filters the batch down to the splats that reach its quadrant, then blends those.
@@ -184,11 +196,13 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                                                 float* __restrict__ T_final,
                                                                 int32_t* __restrict__ n_contrib,
                                                                 int32_t* __restrict__ median_pos,
-                                                                DistIO dio, Counter* __restrict__ counters) {
+                                                                DistIO dio, uint32_t* __restrict__ bmask,
+                                                                Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / 2;  // threads
   constexpr int NW = NT / 32;          // warps = 8×8 quadrants
   constexpr int BATCH = TILE * TILE;   // splats staged per round
   constexpr bool kFilter = TILE > 8;
+  constexpr bool kMask = TILE == 8;    // one warp per tile: it records the blend mask for K4
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
@@ -231,6 +245,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                            opt.log2_alpha_min, wlist[warp])
                              : cnt;
     const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
+    unsigned long long bm = 0ull;  // kMask: blend-mask bits of this batch (bit j: position base + j)
     for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
       if (__all_sync(0xffffffffu, A.done && B.done)) break;
       const int j = kFilter ? (int)wlist[warp][i] : i;
@@ -246,10 +261,16 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       }
       const bool okA = !A.done && pA.pass, okB = !B.done && pB.pass;  // α ≥ α_min (S8)
       if (!__any_sync(0xffffffffu, okA || okB)) continue;  // no pixel of the warp blends it
+      if (kMask) bm |= 1ull << j;  // some pixel of the tile blends (or stops at) position base + j
       const float4 a2 = lds128(a + 32u * BATCH);
       const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;
       if (okA) fwd_blend<PROF, DIST>(A, pA, a1, a2, a3, a + 48u * BATCH, base + j, opt);
       if (okB) fwd_blend<PROF, DIST>(B, pB, a1, a2, a3, a + 48u * BATCH, base + j, opt);
+    }
+    if (kMask && lane == 0) {  // the batch's two words (positions past the last step: zero bits)
+      uint32_t* w = bmask + blend_mask_word(range.x, base, tile);
+      w[0] = (uint32_t)bm;
+      w[1] = (uint32_t)(bm >> 32);
     }
   }
   if (PROF) {
@@ -263,42 +284,28 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                   median_pos, dio);
 }
 
-// One butterfly level: lanes with bit `off` set keep the upper `half` of v[0..2·half) and
-// send the lower, the others the reverse; the kept half gets the partner's copy added.
-template <int HALF>
-__device__ __forceinline__ void butterfly(float* v, int lane, int off) {
-  const bool up = (lane & off) != 0;
+// Warp sum of v[0..NV) through shared memory (NV ≤ 16; red = this warp's [16][36] floats):
+// every lane stores its NV values in column `lane` of row k, lane pair (2k, 2k+1) then reads
+// row k's two halves as four float4 each, and one xor-1 shuffle completes the sum. Lanes 2k
+// and 2k+1 return Σ_lanes v[k]; ≈ NV + 22 instructions against ≈ 5·NV for a shuffle butterfly.
+constexpr int kRedPitch = 36;  // floats per row: 16-B aligned rows, conflict-free column stores
+template <int NV>
+__device__ __forceinline__ float smem_reduce(const float (&v)[NV], unsigned red, int lane) {
 #pragma unroll
-  for (int k = 0; k < HALF; ++k) {
-    const float send = up ? v[k] : v[k + HALF];
-    const float keep = up ? v[k + HALF] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+  for (int k = 0; k < NV; ++k)
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(red + 4u * (unsigned)(k * kRedPitch + lane)), "f"(v[k]) : "memory");
+  __syncwarp();
+  const int k = lane >> 1, q = lane & 1;
+  float s = 0.f;
+  if (k < NV) {
+    const unsigned a = red + 4u * (unsigned)(k * kRedPitch + 16 * q);
+    const float4 x0 = lds128(a), x1 = lds128(a + 16u), x2 = lds128(a + 32u), x3 = lds128(a + 48u);
+    s = ((x0.x + x0.y) + (x0.z + x0.w)) + ((x1.x + x1.y) + (x1.z + x1.w)) +
+        (((x2.x + x2.y) + (x2.z + x2.w)) + ((x3.x + x3.y) + (x3.z + x3.w)));
   }
-}
-
-// Reduce-scatter of v[0..11] across the warp (13 shuffles instead of 60 for a plain
-// all-reduce of 12 values): levels off = 16 (12 → 6), 8 (6 → 3), 4 (3 + a zero pad → 2),
-// 2 (→ 1), then an xor-1 exchange completes the sum. Lanes l and l^1 then hold the sum of
-// value slot12(l) (≥ 12: the pad, nothing).
-__device__ __forceinline__ int slot12(int lane) {
-  const int t = 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
-  return t == 3 ? 12 : ((lane & 16) ? 6 : 0) + ((lane & 8) ? 3 : 0) + t;
-}
-// Reduce-scatter of v[0..15] (16 shuffles): lanes l, l^1 end with Σ_lanes v[l >> 1].
-__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
-  butterfly<8>(v, lane, 16);
-  butterfly<4>(v, lane, 8);
-  butterfly<2>(v, lane, 4);
-  butterfly<1>(v, lane, 2);
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-__device__ __forceinline__ float reduce_scatter12(float (&v)[12], int lane) {
-  butterfly<6>(v, lane, 16);
-  butterfly<3>(v, lane, 8);
-  v[3] = 0.f;
-  butterfly<2>(v, lane, 4);
-  butterfly<1>(v, lane, 2);
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  __syncwarp();  // the rows are rewritten by the next splat
+  return s;
 }
 
 struct PixB {  // backward state of one pixel
@@ -422,14 +429,17 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
     const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
-    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, DistIO dio, G2D* __restrict__ g2d,
-    Counter* __restrict__ counters) {
+    const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, DistIO dio,
+    const uint32_t* __restrict__ bmask, G2D* __restrict__ g2d, Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / PPT;
   constexpr int NW = NT / 32;
   constexpr int BATCH = TILE * TILE;
   constexpr int SH = 4 * PPT;  // each warp: an 8-wide, SH-tall pixel rectangle
   constexpr bool kFilter = TILE > 8;
+  constexpr bool kMask = TILE == 8;  // one warp per tile: K3's blend mask selects the splats
+  constexpr int NV = DIST ? 15 : 12;  // per-splat sums (G2D order; + Σ gd, Σ gd·dx, Σ gd·dy)
   static_assert(NT % 32 == 0 && TILE % SH == 0, "whole warps tiling the tile");
+  static_assert(!kMask || NW == 1, "the blend mask is per tile = per warp");
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
@@ -442,7 +452,8 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   __shared__ uint32_t sid[BATCH];
-  __shared__ uint16_t wlist[kFilter ? NW : 1][kFilter ? BATCH : 1];
+  __shared__ uint16_t wlist[NW][BATCH];  // per warp: batch slots (kFilter) / list offsets (kMask)
+  __shared__ __align__(16) float sred[NW][16 * kRedPitch];
   __shared__ int s_maxlast;
 
   PixB s[PPT];
@@ -463,15 +474,39 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
   if (mylast > 0) atomicMax(&s_maxlast, mylast);
   __syncthreads();
   const int maxlast = s_maxlast;
+  const unsigned a_red = smem_addr(sred[warp]);
 
   for (int end = maxlast; end > 0; end -= BATCH) {
     const int start = max(0, end - BATCH);
     const int cnt = end - start;
+    int nsel = cnt;
+    unsigned long long bm = 0ull;
+    if (kMask) {  // the batch's 64 mask bits (relative positions 0..cnt-1)
+      const unsigned sh = (unsigned)start & 31u;
+      const uint32_t* w = bmask + blend_mask_word(range.x, start, tile);
+      const unsigned long long lo = (unsigned long long)w[0] | ((unsigned long long)w[1] << 32);
+      bm = lo >> sh;
+      if (sh + (unsigned)cnt > 64u) bm |= (unsigned long long)w[2] << (64u - sh);
+      if (cnt < 64) bm &= (1ull << cnt) - 1ull;
+      nsel = __popcll(bm);
+    }
     __syncthreads();
 #pragma unroll
     for (int h = 0; h < BATCH / NT; ++h) {
       const int t = (int)threadIdx.x + h * NT;
-      if (t < cnt) {
+      if (kMask) {  // stage only the splats some pixel of the tile blends, in list order
+        if ((bm >> t) & 1ull) {
+          const int slot = __popcll(bm & ((1ull << t) - 1ull));
+          const uint32_t id = ids[range.x + start + t];
+          const Record* r = rec + id;
+          sid[slot] = id;
+          wlist[0][slot] = (uint16_t)t;
+          sbuf[0][slot] = r->r0;
+          sbuf[1][slot] = r->r1;
+          sbuf[2][slot] = r->r2;
+          sbuf[3][slot] = r->r3;
+        }
+      } else if (t < cnt) {
         const uint32_t id = ids[range.x + start + t];
         const Record* r = rec + id;
         sid[t] = id;
@@ -483,13 +518,23 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     }
     __syncthreads();
     if (!__any_sync(0xffffffffu, start < mylast)) continue;  // the whole warp is past its pixels' lists
-    const int nsel = kFilter ? warp_filter(sbuf[0], sbuf[1], sbuf[3], cnt, lane, fx0, fx0 + 7.f, fy0,
-                                           fy0 + (float)(SH - 1), opt.log2_alpha_min, wlist[warp])
-                             : cnt;
-    const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid);
+    if (kFilter)
+      nsel = warp_filter(sbuf[0], sbuf[1], sbuf[3], cnt, lane, fx0, fx0 + 7.f, fy0, fy0 + (float)(SH - 1),
+                         opt.log2_alpha_min, wlist[warp]);
+    const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid), a_wl = smem_addr(wlist[warp]);
     for (int i = nsel - 1; i >= 0; --i) {
-      const int j = kFilter ? (int)wlist[warp][i] : i;
-      const int pos = start + j;
+      // slot j of the staged batch, at list position pos
+      int j, pos;
+      if (kMask) {
+        j = i;
+        pos = start + (int)(lds32(a_wl + 2u * (unsigned)(i & ~1)) >> (16 * (i & 1)) & 0xffffu);
+      } else if (kFilter) {
+        j = (int)wlist[warp][i];
+        pos = start + j;
+      } else {
+        j = i;
+        pos = start + j;
+      }
       if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
@@ -508,7 +553,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       if (am == 0u) continue;  // warp-uniform: no pixel of this warp uses the splat
       const float4 a2 = lds128(a + 32u * BATCH);
       const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;  // (z_c, p0, p1, ·) for d of Eq.15
-      constexpr int NG = DIST ? 16 : 12;  // + Σ gd, Σ gd·dx, Σ gd·dy of the distortion
+      constexpr int NG = DIST ? 16 : 12;
       float g[NG];
 #pragma unroll
       for (int k = 0; k < NG; ++k) g[k] = 0.f;
@@ -522,16 +567,15 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       if (__popc(am) == 1) {  // one contributing thread in this warp: no reduction needed
         if (any) {
 #pragma unroll
-          for (int k = 0; k < (DIST ? 15 : 12); ++k) g2d_add(dst, k, g[k]);
+          for (int k = 0; k < NV; ++k) g2d_add(dst, k, g[k]);
         }
-      } else if constexpr (DIST) {
-        const float v = reduce_scatter16(g, lane);
-        const int k = lane >> 1;
-        if ((lane & 1) == 0 && k < 15) g2d_add(dst, k, v);  // 12..14 → f[7..9] (Eq.15 sums)
       } else {
-        const float v = reduce_scatter12(g, lane);
-        const int k = slot12(lane);
-        if ((lane & 1) == 0 && k < 12) g2d_add(dst, k, v);
+        float gv[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) gv[k] = g[k];
+        const float v = smem_reduce<NV>(gv, a_red, lane);
+        const int k = lane >> 1;
+        if ((lane & 1) == 0 && k < NV) g2d_add(dst, k, v);  // DIST: 12..14 → f[7..9] (Eq.15 sums)
       }
     }
   }
@@ -542,11 +586,11 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal, float* alpha,
                        float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
-                       Counter* counters, cudaStream_t s) {
+                       uint32_t* bmask, Counter* counters, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
 #define RD_K3(T, P, D)                                                                                            \
   k_render_fwd<T, P, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal,   \
-                                                   alpha, T_final, n_contrib, median_pos, dio, counters)
+                                                   alpha, T_final, n_contrib, median_pos, dio, bmask, counters)
 #define RD_K3T(T)                                     \
   if (dio.d0) {                                       \
     if (counters) RD_K3(T, true, true); else RD_K3(T, false, true);   \
@@ -565,13 +609,13 @@ void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
-                       const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio, G2D* g2d,
-                       Counter* counters, cudaStream_t s) {
+                       const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio,
+                       const uint32_t* bmask, G2D* g2d, Counter* counters, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
 #define RD_K4(T, D)                                                                                        \
   k_render_bwd<T, 2, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, \
                                                    median_pos, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,  \
-                                                   dio, g2d, counters)
+                                                   dio, bmask, g2d, counters)
   if (opt.tile == 16) {
     if (dio.dL_ddist) RD_K4(16, true); else RD_K4(16, false);
   } else {
