@@ -467,13 +467,15 @@ def run_gpu(args, cfg_name, config):
         kernels[name]["share"] = tim["ms"][name] / tot_ms
     dom = max(kernels, key=lambda k: tim["ms"][k])
     dk = kernels[dom]
-    traffic = None
+    traffic, issue, capture = None, None, None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
-        traffic = json.load(open(tr_path)).get(dom)
+        tr = json.load(open(tr_path)).get(dom)
+        if isinstance(tr, dict):
+            traffic, issue, capture = tr.get("dram_bytes_per_launch"), tr.get("issue_active_pct"), tr.get("capture")
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
                 "peak": hbm if dk["bound"] == "hbm" else fp32, "unit": dk["unit"], "frac": dk["frac"],
-                "traffic": traffic,
+                "traffic": traffic, "issue_active_pct": issue, "ncu_capture": capture,
                 "peak_source": (f"{hbm_src} HBM copy (MEASURED_PEAKS.json)" if dk["bound"] == "hbm" else
                                 f"FP32 FFMA {n_sm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (DESIGN.md)")}
 

@@ -53,6 +53,7 @@ if os.path.exists(rp):
     lines.append("| kernel | " + " | ".join(f"{w} [{units[col[w]]}]" for w in col) + " |")
     lines.append("|---" * (len(col) + 1) + "|")
     per = defaultdict(list)
+    issue = defaultdict(list)
     for r in data:
         name = r[ki].split("(")[0].replace("void ", "").replace("rade::<unnamed>::", "")[:60]
         lines.append(f"| {name} | " + " | ".join(r[col[w]] for w in col) + " |")
@@ -63,17 +64,36 @@ if os.path.exists(rp):
             return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         if "dram__bytes_read.sum" in col:
             per[name].append(val("dram__bytes_read.sum") + val("dram__bytes_write.sum"))
+        if "smsp__issue_active.avg.pct_of_peak_sustained_active" in col:
+            issue[name].append(val("smsp__issue_active.avg.pct_of_peak_sustained_active"))
+
+    def bench_name(name):
+        """ncu kernel name -> the bench's kernel name (ms_per_view_by_kernel keys); K5 = 3 kernels"""
+        n = name.split("::")[-1]
+        for pre, b in (("k_render_bwd", "render_bwd"), ("k_render_fwd", "render_fwd"),
+                       ("k_preprocess_fwd", "preprocess_fwd"), ("k_preprocess_bwd", "preprocess_bwd"),
+                       ("k_duplicate", "duplicate"), ("k_ranges", "ranges")):
+            if n.startswith(pre):
+                return b
+        return None
+    agg_t, agg_i = defaultdict(float), defaultdict(list)
     for name, v in per.items():
-        key = {"k_render_bwd<16>": "render_bwd", "k_render_fwd<16>": "render_fwd", "k_preprocess_bwd<3>": "preprocess_bwd",
-               "k_preprocess_fwd<3>": "preprocess_fwd", "k_duplicate": "duplicate", "k_ranges": "ranges"}.get(name, name)
-        traffic[key] = sum(v) / len(v)
+        b = bench_name(name)
+        if b:  # K5's three kernels add up to one rd_preprocess_bwd call
+            agg_t[b] += sum(v) / len(v)
+            agg_i[b] += issue.get(name, [])
+    traffic = dict(agg_t)
+    issue_pct = {b: sum(v) / len(v) for b, v in agg_i.items() if v}
     lines.append("")
 open(os.path.join(out_dir, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
 if traffic:
     tp = os.path.join(out_dir, "traffic.json")
     old = json.load(open(tp)) if os.path.exists(tp) else {}
-    old.update(traffic)
-    old["_about"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes) from the latest "
-                     "`ncu --set full` capture of each kernel (profiles/ncu_<tag>.md)")
+    old = {k: v for k, v in old.items() if isinstance(v, dict)}  # drop the pre-r1w flat layout
+    for b, t in traffic.items():
+        old[b] = {"dram_bytes_per_launch": t, "issue_active_pct": issue_pct.get(b), "capture": tag}
+    old["_about"] = {"what": "per bench kernel (one C-ABI launch; K5 = its 3 kernels summed): dram__bytes_read.sum + "
+                             "dram__bytes_write.sum per launch and smsp__issue_active (% of peak, active cycles) "
+                             "from the latest `ncu --set full` capture that contains it (profiles/ncu_<capture>.md)"}
     json.dump(old, open(tp, "w"), indent=1)
 print("\n".join(lines))
