@@ -267,10 +267,10 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       if (okA) fwd_blend<PROF, DIST>(A, pA, a1, a2, a3, a + 48u * BATCH, base + j, opt);
       if (okB) fwd_blend<PROF, DIST>(B, pB, a1, a2, a3, a + 48u * BATCH, base + j, opt);
     }
-    if (kMask && lane == 0) {  // the batch's two words (positions past the last step: zero bits)
-      uint32_t* w = bmask + blend_mask_word(range.x, base, tile);
-      w[0] = (uint32_t)bm;
-      w[1] = (uint32_t)(bm >> 32);
+    if (kMask && lane == 0) {  // the batch's words (positions past the last step: zero bits);
+      uint32_t* w = bmask + blend_mask_word(range.x, base, tile);  // a word past the list's end
+      w[0] = (uint32_t)bm;                                         // may be the next tile's first
+      if (base + 32 < total) w[1] = (uint32_t)(bm >> 32);
     }
   }
   if (PROF) {
