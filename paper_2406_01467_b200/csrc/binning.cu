@@ -57,7 +57,8 @@ __device__ __forceinline__ uint32_t warp_upper_bound(const uint32_t* __restrict_
 }
 
 constexpr int kDupThreads = 256;
-constexpr int kDupOut = 2048;  // outputs per block
+constexpr int kDupPer = 8;     // consecutive outputs per thread
+constexpr int kDupOut = kDupThreads * kDupPer;  // outputs per block (2048)
 
 // Load-balanced emission over OUTPUTS: block b writes duplicates [b·2048, (b+1)·2048). In
 // depth order every visible Gaussian touches ≥ 1 tile, so the block's outputs come from at
@@ -97,19 +98,57 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, int64_t m,
     s_rect[k] = rect[id];
   }
   __syncthreads();
-  for (uint32_t o = o0 + threadIdx.x; o < o1; o += kDupThreads) {
-    // owner k: s_end[k] <= o < s_end[k + 1]
-    int lo = 0, hi = ng - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_end[mid] <= o) lo = mid; else hi = mid - 1;
+  // thread t writes the kDupPer consecutive outputs o0 + kDupPer·t ..: one binary search for
+  // the first one's owner, then a walk (every staged Gaussian has ≥ 1 tile, so the owner
+  // advances by at most one per output) with the tile stepped row-major over the rect, and
+  // two 16-B stores per array (a warp writes 1 KB contiguous per array)
+  const uint32_t o = o0 + (uint32_t)threadIdx.x * kDupPer;
+  if (o >= o1) return;
+  int lo = 0, hi = ng - 1;  // owner k: s_end[k] <= o < s_end[k + 1]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_end[mid] <= o) lo = mid; else hi = mid - 1;
+  }
+  int k = lo;
+  uint2 r = s_rect[k];
+  uint32_t x0 = r.x & 0xffffu, x1 = r.y & 0xffffu;
+  const uint32_t li = o - s_end[k], w = x1 - x0;
+  uint32_t ty = (r.x >> 16) + li / w, tx = x0 + li % w;
+  uint32_t key[kDupPer], val[kDupPer];
+#pragma unroll
+  for (int j = 0; j < kDupPer; ++j) {
+    const uint32_t oj = o + (uint32_t)j;
+    if (oj < o1) {
+      if (oj >= s_end[k + 1]) {  // the next Gaussian starts here, at its rect's first tile
+        ++k;
+        r = s_rect[k];
+        x0 = r.x & 0xffffu;
+        x1 = r.y & 0xffffu;
+        tx = x0;
+        ty = r.x >> 16;
+      }
+      key[j] = ty * (uint32_t)tiles_x + tx;
+      val[j] = s_id[k];
+      if (++tx == x1) {
+        tx = x0;
+        ++ty;
+      }
     }
-    const uint32_t li = o - s_end[lo];
-    const uint2 r = s_rect[lo];
-    const uint32_t x0 = r.x & 0xffffu, y0 = r.x >> 16, w = (r.y & 0xffffu) - x0;
-    const uint32_t ty = y0 + li / w, tx = x0 + li % w;
-    tile_keys[o] = ty * (uint32_t)tiles_x + tx;
-    vals[o] = s_id[lo];
+  }
+  if (o + kDupPer <= o1) {
+    uint4* kk = reinterpret_cast<uint4*>(tile_keys + o);
+    uint4* vv = reinterpret_cast<uint4*>(vals + o);
+    kk[0] = make_uint4(key[0], key[1], key[2], key[3]);
+    kk[1] = make_uint4(key[4], key[5], key[6], key[7]);
+    vv[0] = make_uint4(val[0], val[1], val[2], val[3]);
+    vv[1] = make_uint4(val[4], val[5], val[6], val[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kDupPer; ++j)
+      if (o + (uint32_t)j < o1) {
+        tile_keys[o + j] = key[j];
+        vals[o + j] = val[j];
+      }
   }
 }
 
