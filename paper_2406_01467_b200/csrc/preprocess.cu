@@ -150,35 +150,42 @@ __device__ __forceinline__ double sq_root(double v) { return sqrt(v); }
 template <typename S>
 __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
                                                  GF<S>& f) {
+  // every parameter load is issued before the cull tests, which are combined into one exit:
+  // K1 is latency-bound, and loads behind early exits would be four dependent HBM round trips
   f.mu[0] = g.means[3 * i];
   f.mu[1] = g.means[3 * i + 1];
   f.mu[2] = g.means[3 * i + 2];
-  if (!(isfin(f.mu[0]) && isfin(f.mu[1]) && isfin(f.mu[2]))) return false;
+  f.o = g.opac[i];
+  f.s[0] = g.scales[3 * i];
+  f.s[1] = g.scales[3 * i + 1];
+  f.s[2] = g.scales[3 * i + 2];
+  const float4 q4 = reinterpret_cast<const float4*>(g.rot)[i];  // [n][4], 16-B aligned rows
+  const float fl = g.filter3d ? g.filter3d[i] : 0.f;
+  bool ok = isfin(f.mu[0]) & isfin(f.mu[1]) & isfin(f.mu[2]);
   // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
   const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
-  if (!(z > cam.znear)) return false;
+  ok &= z > cam.znear;
   {  // guard band (reading S6b), decided in fp32 with the same op order as the oracle
     const float xk = __fmaf_rn(cam.R[0], f.mu[0], __fmaf_rn(cam.R[1], f.mu[1], __fmaf_rn(cam.R[2], f.mu[2], cam.t[0])));
     const float yk = __fmaf_rn(cam.R[3], f.mu[0], __fmaf_rn(cam.R[4], f.mu[1], __fmaf_rn(cam.R[5], f.mu[2], cam.t[1])));
     const float fu = __fmul_rn(cam.fx, xk), fv = __fmul_rn(cam.fy, yk);
-    if (!(fu >= __fmul_rn(cam.gu0, z) && fu <= __fmul_rn(cam.gu1, z) && fv >= __fmul_rn(cam.gv0, z) &&
-          fv <= __fmul_rn(cam.gv1, z)))
-      return false;
+    ok &= (fu >= __fmul_rn(cam.gu0, z)) & (fu <= __fmul_rn(cam.gu1, z)) & (fv >= __fmul_rn(cam.gv0, z)) &
+          (fv <= __fmul_rn(cam.gv1, z));
   }
   f.zkey = z;
-  f.o = g.opac[i];
-  if (!(f.o >= opt.alpha_min) || !isfin(f.o)) return false;  // o' ≤ o: also culls the filtered one
-  f.s[0] = g.scales[3 * i];
-  f.s[1] = g.scales[3 * i + 1];
-  f.s[2] = g.scales[3 * i + 2];
-  if (!(f.s[0] > 0.f && f.s[1] > 0.f && f.s[2] > 0.f) || !(isfin(f.s[0]) && isfin(f.s[1]) && isfin(f.s[2])))
-    return false;
+  ok &= (f.o >= opt.alpha_min) & isfin(f.o);  // o' ≤ o: also culls the filtered one
+  ok &= (f.s[0] > 0.f) & (f.s[1] > 0.f) & (f.s[2] > 0.f) & isfin(f.s[0]) & isfin(f.s[1]) & isfin(f.s[2]);
+  f.qr[0] = q4.x;
+  f.qr[1] = q4.y;
+  f.qr[2] = q4.z;
+  f.qr[3] = q4.w;
+  ok &= isfin(f.qr[0]) & isfin(f.qr[1]) & isfin(f.qr[2]) & isfin(f.qr[3]);
+  if (!ok) return false;
   f.s_raw[0] = f.s[0];
   f.s_raw[1] = f.s[1];
   f.s_raw[2] = f.s[2];
   f.o_raw = f.o;
   if (g.filter3d) {  // 3D filter (S23): Σ + f²I ⇔ s' = √(s² + f²); o' = o·Π s/s'
-    const float fl = g.filter3d[i];
     if (!isfin(fl)) return false;
     float ratio = 1.f;
 #pragma unroll
@@ -190,14 +197,6 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
     f.o *= ratio;
     if (!(f.o >= opt.alpha_min)) return false;
   }
-  {
-    const float4 q4 = reinterpret_cast<const float4*>(g.rot)[i];  // [n][4], 16-B aligned rows
-    f.qr[0] = q4.x;
-    f.qr[1] = q4.y;
-    f.qr[2] = q4.z;
-    f.qr[3] = q4.w;
-  }
-  if (!(isfin(f.qr[0]) && isfin(f.qr[1]) && isfin(f.qr[2]) && isfin(f.qr[3]))) return false;
   const S ql2 = (S)f.qr[0] * f.qr[0] + (S)f.qr[1] * f.qr[1] + (S)f.qr[2] * f.qr[2] + (S)f.qr[3] * f.qr[3];
   if (!(ql2 > S(0))) return false;
 
