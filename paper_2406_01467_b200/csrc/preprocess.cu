@@ -147,9 +147,13 @@ __device__ __forceinline__ float sq_root(float v) { return sqrtf(v); }
 __device__ __forceinline__ double sq_root(double v) { return sqrt(v); }
 
 // Loads one Gaussian and runs stage 1 up to the conic (no plane, no SH). False if culled.
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// pf_sh (K1): once the cheap culls pass, prefetch the Gaussian's SH row into L2 so its fetch
+// overlaps the covariance math instead of following it.
 template <typename S>
 __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
-                                                 GF<S>& f) {
+                                                 GF<S>& f, bool pf_sh = false) {
   // every parameter load is issued before the cull tests, which are combined into one exit:
   // K1 is latency-bound, and loads behind early exits would be four dependent HBM round trips
   f.mu[0] = g.means[3 * i];
@@ -181,6 +185,11 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   f.qr[3] = q4.w;
   ok &= isfin(f.qr[0]) & isfin(f.qr[1]) & isfin(f.qr[2]) & isfin(f.qr[3]);
   if (!ok) return false;
+  if (pf_sh) {  // the row's first and last byte: its (at most two) 128-B lines
+    const float* row = g.sh + i * g.sh_coeffs * 3;
+    prefetch_l2(row);
+    prefetch_l2(row + g.sh_coeffs * 3 - 1);
+  }
   f.s_raw[0] = f.s[0];
   f.s_raw[1] = f.s[1];
   f.s_raw[2] = f.s[2];
@@ -294,7 +303,7 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
                                                    uint32_t* __restrict__ dkey, uint32_t& rx0, uint32_t& ry0,
                                                    uint32_t& rw) {
   GF<double> f;
-  if (!gaussian_project<double>(g, i, cam, opt, f)) {
+  if (!gaussian_project<double>(g, i, cam, opt, f, true)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
     return 0u;
@@ -496,6 +505,14 @@ template <typename S>
 __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
                                                   const G2D* __restrict__ g2d, DevGrads& gr,
                                                   const float (&dmu_extra)[3]) {
+  // the G2D row and the gradient rows are needed only after the forward recompute: have
+  // them on their way to L2 now (no registers held)
+  prefetch_l2(g2d + i);
+  prefetch_l2(reinterpret_cast<const char*>(g2d + i) + sizeof(G2D) - 1);
+  prefetch_l2(gr.means + 3 * i);
+  prefetch_l2(gr.scales + 3 * i);
+  prefetch_l2(gr.rot + 4 * i);
+  prefetch_l2(gr.opac + i);
   GF<S> f;
   if (!gaussian_forward<S>(g, i, cam, opt, f)) return;
   // the G2D sums of K4 → 2-D gradients (log2 e · ln 2 = 1 cancels between the stored
