@@ -20,10 +20,38 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/dispatch/dispatch_radix_sort.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
 namespace rade {
 namespace {
+
+// CUB's onesweep radix sort with 512-thread × 12-key tiles (tools/sort_bench.cu on B200: 96 vs
+// 107 µs for the 1.5 M depth keys, 129 vs 141 µs for 5.6 M 12-bit tile keys against CUB's
+// default 384 × 23), 8-bit digits.
+struct SortHub {
+  using Base = cub::detail::radix::policy_hub<uint32_t, uint32_t, uint32_t>;
+  struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, Policy1000> {
+    using B = typename Base::Policy1000;
+    static constexpr bool ONESWEEP = true;
+    static constexpr int ONESWEEP_RADIX_BITS = 8;
+    using HistogramPolicy = typename B::HistogramPolicy;
+    using ExclusiveSumPolicy = typename B::ExclusiveSumPolicy;
+    using OnesweepPolicy =
+        cub::AgentRadixSortOnesweepPolicy<512, 12, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
+                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+    using ScanPolicy = typename B::ScanPolicy;
+    using DownsweepPolicy = typename B::DownsweepPolicy;
+    using AltDownsweepPolicy = typename B::AltDownsweepPolicy;
+    using UpsweepPolicy = typename B::UpsweepPolicy;
+    using AltUpsweepPolicy = typename B::AltUpsweepPolicy;
+    using SingleTilePolicy = typename B::SingleTilePolicy;
+    using SegmentedPolicy = typename B::SegmentedPolicy;
+    using AltSegmentedPolicy = typename B::AltSegmentedPolicy;
+  };
+  using MaxPolicy = Policy1000;
+};
+using Sort = cub::DispatchRadixSort<false, uint32_t, uint32_t, uint32_t, SortHub>;
 
 struct CountOf {
   const uint32_t* __restrict__ touched;
@@ -193,10 +221,10 @@ __global__ void __launch_bounds__(256) k_keys64(const uint32_t* __restrict__ til
 size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits) {
   size_t a = 0, b = 0, c = 0;
   cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, a, k, v, (int)n, 0, 32);
+  Sort::Dispatch(nullptr, a, k, v, (uint32_t)n, 0, 32, true, 0);
   cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it(nullptr, CountOf{nullptr});
   cub::DeviceScan::InclusiveSum(nullptr, b, it, (uint32_t*)nullptr, (int)n);
-  if (m > 0) cub::DeviceRadixSort::SortPairs(nullptr, c, k, v, (int)m, 0, tile_bits);
+  if (m > 0) Sort::Dispatch(nullptr, c, k, v, (uint32_t)m, 0, tile_bits, true, 0);
   size_t r = a > b ? a : b;
   return r > c ? r : c;
 }
@@ -205,7 +233,7 @@ int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t
                       size_t temp_bytes, cudaStream_t s) {
   if (n == 0) return 0;
   cub::DoubleBuffer<uint32_t> k(dkey0, dkey1), v(idx0, idx1);
-  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, 32, s);
+  Sort::Dispatch(temp, temp_bytes, k, v, (uint32_t)n, 0, 32, true, s);
   return k.selector;
 }
 
@@ -227,7 +255,7 @@ int launch_tile_sort(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t
                      void* temp, size_t temp_bytes, cudaStream_t s) {
   if (m == 0) return 0;
   cub::DoubleBuffer<uint32_t> k(keys0, keys1), v(vals0, vals1);
-  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)m, 0, tile_bits, s);
+  Sort::Dispatch(temp, temp_bytes, k, v, (uint32_t)m, 0, tile_bits, true, s);
   return k.selector;
 }
 
