@@ -78,7 +78,7 @@ int main() {
     memcpy(&b, &z, 4);
     hk[i] = (i % 2 == 0 && i < N) ? 0xffffffffu : b;  // half of the depth keys culled
     hv[i] = i;
-    ht[i] = rand() % 4056;
+    ht[i] = rand() % 15965;  // 8x8 tiles at 1237x822
   }
   uint32_t *kin, *vin, *tin, *k0, *k1, *v0, *v1;
   cudaMalloc(&kin, M * 4); cudaMalloc(&vin, M * 4); cudaMalloc(&tin, M * 4);
@@ -89,7 +89,7 @@ int main() {
   {  // CUB default
     for (int which = 0; which < 3; ++which) {
       const uint32_t n = which == 0 ? N : which == 1 ? N / 2 : M;
-      const int bits = which == 2 ? 12 : 32;
+      const int bits = which == 2 ? 14 : 32;
       const uint32_t* ki = which == 2 ? tin : kin;
       size_t tb = 0;
       cub::DoubleBuffer<uint32_t> K(k0, k1), V(v0, v1);
@@ -105,15 +105,16 @@ int main() {
 #define CFG(T, I)                                          \
   one<T, I>("depth", k0, k1, v0, v1, kin, vin, N, 32);      \
   one<T, I>("depth/2", k0, k1, v0, v1, kin, vin, N / 2, 32); \
-  one<T, I>("tile", k0, k1, v0, v1, tin, vin, M, 12);
-  CFG(384, 23)
-  CFG(256, 16)
-  CFG(256, 12)
-  CFG(256, 8)
-  CFG(512, 8)
+  one<T, I>("tile", k0, k1, v0, v1, tin, vin, M, 14);
   CFG(512, 12)
-  CFG(128, 16)
-  CFG(384, 12)
+  CFG(512, 16)
+  CFG(512, 20)
+  CFG(640, 12)
+  CFG(768, 12)
+  CFG(768, 8)
+  CFG(1024, 8)
+  CFG(1024, 6)
+  CFG(512, 10)
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
