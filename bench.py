@@ -420,7 +420,7 @@ def run_gpu(args, cfg_name, config):
         def step_e2e():
             run_views(per_view_e2e)
 
-        steps_e2e = max(1, args.steps // 2)
+        steps_e2e = max(1, args.steps)
         step_e2e()
         torch.cuda.synchronize()
         h2d = d2h = 0
