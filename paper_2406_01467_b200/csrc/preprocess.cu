@@ -690,17 +690,23 @@ __global__ void __launch_bounds__(128, RD_K5_MINB) k_preprocess_bwd(DevGauss g, 
                                                         const uint32_t* __restrict__ vis, int64_t n_vis,
                                                         const G2D* __restrict__ g2d, DevGrads gr) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_vis) return;
-  const uint32_t i = vis[p];  // over K1's visible list: every thread has work
-  if (is_big(touched[i], opt.tile)) return;  // K5b64's
-  const float zero[3] = {0.f, 0.f, 0.f};
-  geometry_backward<float>(g, i, cam, opt, g2d, gr, zero);
+  if (p < n_vis) {
+    const uint32_t i = vis[p];  // over K1's visible list: every thread has work
+    if (!is_big(touched[i], opt.tile)) {  // else K5b64's
+      const float zero[3] = {0.f, 0.f, 0.f};
+      geometry_backward<float>(g, i, cam, opt, g2d, gr, zero);
+    }
+  }
+  // launched as K5b64's programmatic dependent (the two write disjoint rows and overlap):
+  // do not complete before K5b64 has, so stream order after K5b still covers both
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // K5b64: the same chain rule in fp64 for the Gaussians of K1's big list.
 __global__ void __launch_bounds__(128) k_preprocess_bwd64(DevGauss g, DevCam cam, DevOpt opt,
                                                           const uint32_t* __restrict__ big, int64_t n_big,
                                                           const G2D* __restrict__ g2d, DevGrads gr) {
+  asm volatile("griddepcontrol.launch_dependents;");  // K5b may start now (disjoint rows)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_big) return;
   const float zero[3] = {0.f, 0.f, 0.f};
@@ -864,11 +870,22 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
     }
 #undef RD_K5A
   }
-  if (n_vis > 0)
-    k_preprocess_bwd<<<(unsigned)((n_vis + threads - 1) / threads), threads, 0, s>>>(g, cam, opt, tiles_touched,
-                                                                                     vis, n_vis, g2d, grads);
+  // K5b64 (few, fp64, latency-bound) first; K5b as its programmatic dependent, so the two
+  // run side by side instead of K5b64's ~11 µs trailing K5b
   if (n_big > 0)
     k_preprocess_bwd64<<<(unsigned)((n_big + 127) / 128), 128, 0, s>>>(g, cam, opt, big, n_big, g2d, grads);
+  if (n_vis > 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((n_vis + threads - 1) / threads));
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = n_big > 0 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_preprocess_bwd, g, cam, opt, tiles_touched, vis, n_vis, g2d, grads);
+  }
 }
 
 void launch_g2d_to_f32(const G2D* g2d, int64_t n, float* out, cudaStream_t s) {
