@@ -23,6 +23,7 @@ import os
 import subprocess
 import sys
 import threading
+from concurrent.futures import ThreadPoolExecutor
 import time
 
 import numpy as np
@@ -270,6 +271,8 @@ def run_gpu(args, cfg_name, config):
     # output maps: view v+1's preprocess/binning/blending overlap view v's. The gradient
     # accumulation (K5's read-modify-write of the shared gradient rows, rd_preprocess_bwd)
     # stays in view order: each waits for the previous view's (event chain).
+    if args.pipeline <= 0:  # every view of a step on its own stream: they all start at once
+        args.pipeline = min(max(1, B), 8)
     P_ = max(1, args.pipeline)
     slots = []
     for _ in range(P_):
@@ -290,10 +293,13 @@ def run_gpu(args, cfg_name, config):
     counter = {"v": 0}
     main_stream = torch.cuda.current_stream(device)
 
-    def one_view(slot, cam, cot, after, io=None):
+    def one_view(slot, cam, cot, after, io=None, after_enq=None, done_ev=None, done_enq=None):
         """io (end-to-end pass): events that order the view's forward after the D2H of the
         slot's previous maps, publish the forward for its D2H, hold K4 until the H2D of the
-        cotangents landed, and publish K4 (the cotangent buffer is free again)."""
+        cotangents landed, and publish K4 (the cotangent buffer is free again).
+        after: the previous view's K5 event (gradient rows are read-modify-written in view
+        order); with host threads, after_enq is set once that event has been recorded, and
+        done_enq is set once this view's (done_ev, or a fresh event) is. Returns that event."""
         st, vw, o = slot["stream"], slot["view"], slot["outs"]
         with torch.cuda.stream(st):
             P.rd_preprocess(vw, g, cam, opts, stream=st)
@@ -320,29 +326,64 @@ def run_gpu(args, cfg_name, config):
                 P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)  # K4: view-private output
             if io:
                 io["k4_done"].record(st)
+            if after_enq is not None:
+                after_enq.wait()  # host side: the previous view's K5 event is recorded
             st.wait_event(after)  # gradient rows: the previous view's K5 first
             P.rd_preprocess_bwd(vw, g, grads, stream=st)
-            slot["done"].record(st)
-        return slot["done"]
+            done = done_ev if done_ev is not None else torch.cuda.Event()
+            done.record(st)
+            slot["done"] = done
+            if done_enq is not None:
+                done_enq.set()
+        return done
+
+    pool = ThreadPoolExecutor(max_workers=max(1, args.pipeline)) if args.host_threads else None
 
     def run_views(per_view):
-        """Zero the gradients, run B views through the slots, join, all-reduce."""
+        """Zero the gradients, run B views through the slots, join, all-reduce.
+        With host threads (default) each slot's views are issued by their own host thread, so
+        one view's rd_bin (which waits for its count of duplicates) does not hold
+        back the issue of the other slots' views; the K5 order across views is kept by
+        per-view events (host-side flags make sure an event is recorded before it is awaited)."""
         fg.zero_()
         start = torch.cuda.Event()
         start.record(main_stream)
         for sl in slots:
             sl["stream"].wait_event(start)
-        prev = start
+        ks = []
         for b in range(B):
-            k = counter["v"]
+            ks.append(counter["v"])
             counter["v"] += 1
-            prev = per_view(slots[k % P_], k, prev)
+        if pool is None:
+            prev = start
+            for k in ks:
+                prev = per_view(slots[k % P_], k, prev, None, None, None)
+        else:
+            enq = [threading.Event() for _ in ks]
+            evs = [torch.cuda.Event() for _ in ks]
+
+            def worker(js):
+                try:
+                    torch.cuda.set_device(device)  # per thread
+                    for j in js:
+                        per_view(slots[ks[j] % P_], ks[j], start if j == 0 else evs[j - 1],
+                                 None if j == 0 else enq[j - 1], evs[j], enq[j])
+                except BaseException:
+                    for e in enq:  # never leave another thread waiting on this one
+                        e.set()
+                    raise
+
+            # one task per slot: its views in order
+            futs = [pool.submit(worker, [j for j in range(len(ks)) if ks[j] % P_ == si]) for si in range(P_)]
+            for f in futs:
+                f.result()
         for sl in slots:
             main_stream.wait_event(sl["done"])
         fg.allreduce()  # NCCL sum over ranks (no-op at N = 1)
 
     def step():
-        run_views(lambda sl, k, prev: one_view(sl, my_views[k % len(my_views)], cots[k % n_ring], prev))
+        run_views(lambda sl, k, prev, prev_enq, ev, enq: one_view(sl, my_views[k % len(my_views)], cots[k % n_ring],
+                                                                   prev, None, prev_enq, ev, enq))
 
     # ---------------- device-resident timed region (no per-kernel events: pipelined streams)
     for _ in range(args.warmup):
@@ -395,26 +436,55 @@ def run_gpu(args, cfg_name, config):
         # transfers on their own copy streams, overlapped with the compute of other views:
         # the H2D of a view's cotangents is only awaited by its K4, the D2H of its maps only
         # by the next forward of the same slot
-        cin, cout = torch.cuda.Stream(device), torch.cuda.Stream(device)
+        cins = [torch.cuda.Stream(device) for _ in slots]   # per slot: its host thread owns them
+        couts = [torch.cuda.Stream(device) for _ in slots]
+        io_lock = threading.Lock()
         ios = [{k: torch.cuda.Event() for k in ("cot_ready", "k4_done", "fwd_done", "outs_free")} for _ in slots]
 
-        def per_view_e2e(sl, k, prev):
+        tl_path = os.environ.get("RADE_E2E_TIMELINE")  # diagnostics: per-view event timeline
+        tl = []
+
+        def tev(stream):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
+
+        def per_view_e2e(sl, k, prev, prev_enq, ev, enq):
             nonlocal h2d, d2h
             i = slots.index(sl)
             io = ios[i]
+            cin, cout = cins[i], couts[i]
+            rec = {"host": time.perf_counter()} if tl_path else None
             with torch.cuda.stream(cin):
                 cin.wait_event(io["k4_done"])  # the slot's previous K4 has read the buffer
+                if rec is not None:
+                    rec["h2d0"] = tev(cin)
                 dev_cots[i].copy_(host_cots[k % n_ring], non_blocking=True)
                 io["cot_ready"].record(cin)
-            h2d += dev_cots[i].numel() * 4
-            done = one_view(sl, my_views[k % len(my_views)], dev_cots[i], prev, io)
+                if rec is not None:
+                    rec["h2d1"] = tev(cin)
+            with io_lock:
+                h2d += dev_cots[i].numel() * 4
+            if rec is not None:
+                rec["v0"] = tev(sl["stream"])
+            done = one_view(sl, my_views[k % len(my_views)], dev_cots[i], prev, io, prev_enq, ev, enq)
+            if rec is not None:
+                rec["v1"] = tev(sl["stream"])
+                rec["host_end"] = time.perf_counter()
             with torch.cuda.stream(cout):
                 cout.wait_event(io["fwd_done"])
+                if rec is not None:
+                    rec["d2h0"] = tev(cout)
                 for key in out_keys:
                     t = sl["outs"][key]
                     host_outs[i][key].copy_(t, non_blocking=True)
-                    d2h += t.numel() * 4
+                    with io_lock:
+                        d2h += t.numel() * 4
                 io["outs_free"].record(cout)
+                if rec is not None:
+                    rec["d2h1"] = tev(cout)
+            if rec is not None:
+                tl.append(rec)
             return done
 
         def step_e2e():
@@ -430,6 +500,11 @@ def run_gpu(args, cfg_name, config):
             step_e2e()
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(time.perf_counter() - t0, dist_on, device)
+        if tl_path and tl:
+            base_e, base_h = tl[0]["h2d0"], tl[0]["host"]
+            rows = [{k: (base_e.elapsed_time(v) if isinstance(v, torch.cuda.Event) else (v - base_h) * 1e3)
+                     for k, v in r.items()} for r in tl]
+            json.dump(rows, open(tl_path, "w"), indent=0)
         e2e = {"value": steps_e2e * B * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // steps_e2e,
                "d2h_bytes_per_step": d2h // steps_e2e,
                "what": "per view: H2D of the view's cotangent image (8 channels, 9 with --distortion) from "
@@ -495,6 +570,7 @@ def run_gpu(args, cfg_name, config):
         "pairs_blended_per_px": tim["pairs_blended_fwd"] / max(views_timed, 1) / (H * W),
         "ms_per_view_by_kernel": {k: tim["ms"][k] / max(views_timed, 1) for k in tim["ms"]},
         "parallelism": f"view-parallel dp{ws}",
+        "streams": P_, "host_threads": bool(args.host_threads),
     })
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -534,7 +610,10 @@ def main():
     ap.add_argument("--distortion", action="store_true", help="NEXT-1: also render L_d and back-propagate it")
     ap.add_argument("--normal-consistency", action="store_true",
                     help="NEXT-2: also compute L_n on the maps and back-propagate it")
-    ap.add_argument("--pipeline", type=int, default=3, help="CUDA streams the views are pipelined over")
+    ap.add_argument("--pipeline", type=int, default=0,
+                    help="CUDA streams (and host threads) the views are pipelined over; 0 = views per step (max 8)")
+    ap.add_argument("--single-host-thread", dest="host_threads", action="store_false",
+                    help="issue every view from the main thread (default: one host thread per stream)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -1,6 +1,6 @@
 """GPU parity at BASELINE.json's full size, in the launch configuration bench.py times
-(C3: 1.5M Gaussians, 1237x822, tile 16, views pipelined over two CUDA streams with the
-gradient accumulation chained by events).
+(C3: 1.5M Gaussians, 1237x822, 8x8 tiles, the views of a step pipelined over one CUDA
+stream and one host thread each, with the gradient accumulation chained by events).
 
 The oracle cannot render 1M pixels x 1.5M Gaussians in a test, so it is compared on
 sampled outputs it computes one by one (random pixels; the gradients of sampled visible
@@ -95,47 +95,82 @@ def test_c3_binning_bit_exact(c3):
     np.testing.assert_array_equal(ranges.astype(np.int64), exp)
 
 
-def _pipelined_grads(g, cams, opt, cots, n_streams):
-    """bench.py's launch configuration: views over n_streams streams, K4 free to overlap, K5
-    chained in view order by events."""
-    dev = torch.device("cuda")
+def _pipelined_grads(g, cams, opt, cots, n_streams, host_threads=False):
+    """bench.py's launch configuration: views over n_streams streams (each issued by its own
+    host thread when host_threads), K4 free to overlap, K5 chained in view order by per-view
+    events (a host flag makes sure an event is recorded before another thread awaits it)."""
+    import threading
+    dev = torch.device("cuda", torch.cuda.current_device())
     grads = g.zeros_like()
     slots = []
     for _ in range(n_streams):
         st = torch.cuda.Stream(dev)
         with torch.cuda.stream(st):
-            slots.append((st, P.View(dev), torch.cuda.Event()))
+            slots.append((st, P.View(dev)))
     start = torch.cuda.Event()
     start.record()
-    for st, _, _ in slots:
+    for st, _ in slots:
         st.wait_event(start)
-    prev = start
-    for k, (cam, cot) in enumerate(zip(cams, cots)):
-        st, vw, done = slots[k % n_streams]
+    evs = [torch.cuda.Event() for _ in cams]
+    enq = [threading.Event() for _ in cams]
+
+    def one(k):
+        st, vw = slots[k % n_streams]
+        cam, cot = cams[k], cots[k]
         with torch.cuda.stream(st):
             P.rd_preprocess(vw, g, cam, opts_dict(opt), stream=st)
             P.rd_bin(vw, stream=st)
             P.rd_render_fwd(vw, stream=st)
             P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)
-            st.wait_event(prev)
+            if k > 0:
+                enq[k - 1].wait()
+            st.wait_event(start if k == 0 else evs[k - 1])
             P.rd_preprocess_bwd(vw, g, grads, stream=st)
-            done.record(st)
-        prev = done
-    for st, _, _ in slots:
+            evs[k].record(st)
+            enq[k].set()
+
+    def worker(si):
+        torch.cuda.set_device(dev)
+        for k in range(si, len(cams), n_streams):
+            one(k)
+
+    if host_threads:
+        errs = []
+
+        def guarded(si):
+            try:
+                worker(si)
+            except BaseException as e:  # surfaced below: a dead thread must fail the test
+                errs.append(e)
+                for e_ in enq:
+                    e_.set()
+
+        ths = [threading.Thread(target=guarded, args=(si,)) for si in range(n_streams)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        assert not errs, errs
+    else:
+        for k in range(len(cams)):
+            one(k)
+    for st, _ in slots:
         torch.cuda.current_stream().wait_stream(st)
     torch.cuda.synchronize()
     return grads_to_rows(grads, g.n)
 
 
-def test_c3_pipelined_accumulation_matches_sequential(c3):
-    """Four views accumulated through two pipelined streams equal the sequential sum (float
-    atomics in K4: equal to rounding)."""
+@pytest.mark.parametrize("n_streams,host_threads", [(2, False), (4, True)])
+def test_c3_pipelined_accumulation_matches_sequential(c3, n_streams, host_threads):
+    """Four views accumulated through pipelined streams (bench.py's default: one stream and
+    one host thread per view of the step) equal the sequential sum (float atomics in K4:
+    equal to rounding)."""
     H, W = c3["cam"].height, c3["cam"].width
     gen = torch.Generator(device="cuda")
     gen.manual_seed(5)
     cots = [torch.randn((8, H, W), generator=gen, device="cuda") for _ in range(4)]
     cams = c3["cams"][:4]
-    a = _pipelined_grads(c3["g"], cams, c3["opt"], cots, 2)
+    a = _pipelined_grads(c3["g"], cams, c3["opt"], cots, n_streams, host_threads)
     b = _pipelined_grads(c3["g"], cams, c3["opt"], cots, 1)
     for sl in (slice(0, 3), slice(3, 6), slice(6, 10), slice(10, 11), slice(11, 59)):
         nb = np.linalg.norm(b[:, sl])
