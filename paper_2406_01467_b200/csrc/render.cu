@@ -367,7 +367,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // (the 3DGS derivation collapsed to one scalar, since g_C, g_N are per-pixel constants).
 // Branch-free: an inactive pair (past the pixel's list, or α < α_min) contributes exact
 // zeros (α masked to 0 ⇒ rinv = rcp(1) = 1, w = 0, dA = 0).
-template <bool DIST, int NG>
+template <bool DIST, int NG, bool FIRST>
 __device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[NG], const PairAlpha& pa, bool act, const float4& a1,
                                           const float4& a2, const float4& a3, const DevOpt& opt) {
   const float a_raw = ex2_approx(pa.e);                  // o·exp(−½ΔᵀCΔ)
@@ -380,24 +380,27 @@ __device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[NG], const PairAlp
   s.Dsuf = fmaf(w, dot, s.Dsuf);
   const float dA = a_raw * dL_dal;
   const float hx = dA * pa.dx, hy = dA * pa.dy;
-  g[0] += hx;
-  g[1] += hy;
-  g[2] = fmaf(hx, pa.dx, g[2]);
-  g[3] = fmaf(hx, pa.dy, g[3]);
-  g[4] = fmaf(hy, pa.dy, g[4]);
-  g[5] += dA;
-  g[6] = fmaf(w, s.gC0, g[6]);
-  g[7] = fmaf(w, s.gC1, g[7]);
-  g[8] = fmaf(w, s.gC2, g[8]);
-  g[9] = fmaf(w, s.gN0, g[9]);
-  g[10] = fmaf(w, s.gN1, g[10]);
-  g[11] = fmaf(w, s.gN2, g[11]);
+  // FIRST: the first pixel row of the step writes the sums instead of adding to zeros
+  auto add = [&](int k, float v) { g[k] = FIRST ? v : g[k] + v; };
+  auto fma_ = [&](int k, float a, float b) { g[k] = FIRST ? a * b : fmaf(a, b, g[k]); };
+  add(0, hx);
+  add(1, hy);
+  fma_(2, hx, pa.dx);
+  fma_(3, hx, pa.dy);
+  fma_(4, hy, pa.dy);
+  add(5, dA);
+  fma_(6, w, s.gC0);
+  fma_(7, w, s.gC1);
+  fma_(8, w, s.gC2);
+  fma_(9, w, s.gN0);
+  fma_(10, w, s.gN1);
+  fma_(11, w, s.gN2);
   if constexpr (DIST) {  // ∂L_d/∂d = 4 ω (A (d − d0) − D1), ω detached (S21); into the Eq.15 sums
     const float d = __fmaf_rn(a3.y, pa.dx, __fmaf_rn(a3.z, pa.dy, a3.x));
     const float gd = s.gL * w * fmaf(s.A, d - s.d0, -s.D1);
-    g[12] += gd;
-    g[13] = fmaf(gd, pa.dx, g[13]);
-    g[14] = fmaf(gd, pa.dy, g[14]);
+    add(12, gd);
+    fma_(13, gd, pa.dx);
+    fma_(14, gd, pa.dy);
   }
 }
 
@@ -555,11 +558,16 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;  // (z_c, p0, p1, ·) for d of Eq.15
       constexpr int NG = DIST ? 16 : 12;
       float g[NG];
+      // a pixel row no lane uses contributes exact zeros: skip it (the first row writes g)
+      if (__any_sync(0xffffffffu, act[0])) {
+        bwd_accum<DIST, NG, true>(s[0], g, pa[0], act[0], a1, a2, a3, opt);
+      } else {
 #pragma unroll
-      for (int k = 0; k < NG; ++k) g[k] = 0.f;
+        for (int k = 0; k < NG; ++k) g[k] = 0.f;
+      }
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)  // a pixel row no lane uses contributes exact zeros: skip it
-        if (__any_sync(0xffffffffu, act[k])) bwd_accum<DIST>(s[k], g, pa[k], act[k], a1, a2, a3, opt);
+      for (int k = 1; k < PPT; ++k)
+        if (__any_sync(0xffffffffu, act[k])) bwd_accum<DIST, NG, false>(s[k], g, pa[k], act[k], a1, a2, a3, opt);
       G2D* dst = g2d + lds32(a_id + 4u * j);
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
