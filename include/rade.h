@@ -52,6 +52,12 @@
  *
  * Synchronisation: every call is asynchronous on the given stream except rd_bin, which
  * reads the duplicate count M back to the host once (one D2H copy + stream sync).
+ *
+ * Threads: the library keeps no shared mutable state (the error message is thread-local);
+ * calls on DISTINCT rd_view handles may run concurrently from different host threads, which
+ * is how a multi-view caller keeps one view's rd_bin wait from holding back the issue of the
+ * others (bench.py: one stream and one host thread per view of a step). One rd_view must not
+ * be used by two threads at once.
  */
 #ifndef RADE_H_
 #define RADE_H_
