@@ -268,9 +268,9 @@ def run_gpu(args, cfg_name, config):
     opts = dict(tile=args.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
                 median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
     # Views are pipelined over `args.pipeline` CUDA streams, each with its own rd_view and
-    # output maps: view v+1's preprocess/binning/blending overlap view v's. The gradient
-    # accumulation (K5's read-modify-write of the shared gradient rows, rd_preprocess_bwd)
-    # stays in view order: each waits for the previous view's (event chain).
+    # output maps (and its own host thread): the views of a step run concurrently. Their
+    # gradient accumulations (K5, rd_preprocess_bwd) add into the one flat buffer with L2
+    # reductions, so they need no mutual order.
     if args.pipeline <= 0:  # every view of a step on its own stream: they all start at once
         args.pipeline = min(max(1, B), 8)
     P_ = max(1, args.pipeline)
@@ -293,13 +293,11 @@ def run_gpu(args, cfg_name, config):
     counter = {"v": 0}
     main_stream = torch.cuda.current_stream(device)
 
-    def one_view(slot, cam, cot, after, io=None, after_enq=None, done_ev=None, done_enq=None):
+    def one_view(slot, cam, cot, io=None):
         """io (end-to-end pass): events that order the view's forward after the D2H of the
         slot's previous maps, publish the forward for its D2H, hold K4 until the H2D of the
-        cotangents landed, and publish K4 (the cotangent buffer is free again).
-        after: the previous view's K5 event (gradient rows are read-modify-written in view
-        order); with host threads, after_enq is set once that event has been recorded, and
-        done_enq is set once this view's (done_ev, or a fresh event) is. Returns that event."""
+        cotangents landed, and publish K4 (the cotangent buffer is free again). K5 adds the
+        view's gradients with L2 reductions, so the views' K5 calls need no mutual order."""
         st, vw, o = slot["stream"], slot["view"], slot["outs"]
         with torch.cuda.stream(st):
             P.rd_preprocess(vw, g, cam, opts, stream=st)
@@ -326,16 +324,8 @@ def run_gpu(args, cfg_name, config):
                 P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)  # K4: view-private output
             if io:
                 io["k4_done"].record(st)
-            if after_enq is not None:
-                after_enq.wait()  # host side: the previous view's K5 event is recorded
-            st.wait_event(after)  # gradient rows: the previous view's K5 first
-            P.rd_preprocess_bwd(vw, g, grads, stream=st)
-            done = done_ev if done_ev is not None else torch.cuda.Event()
-            done.record(st)
-            slot["done"] = done
-            if done_enq is not None:
-                done_enq.set()
-        return done
+            P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
+            slot["done"].record(st)
 
     pool = ThreadPoolExecutor(max_workers=max(1, args.pipeline)) if args.host_threads else None
 
@@ -343,8 +333,7 @@ def run_gpu(args, cfg_name, config):
         """Zero the gradients, run B views through the slots, join, all-reduce.
         With host threads (default) each slot's views are issued by their own host thread, so
         one view's rd_bin (which waits for its count of duplicates) does not hold
-        back the issue of the other slots' views; the K5 order across views is kept by
-        per-view events (host-side flags make sure an event is recorded before it is awaited)."""
+        back the issue of the other slots' views."""
         fg.zero_()
         start = torch.cuda.Event()
         start.record(main_stream)
@@ -355,23 +344,13 @@ def run_gpu(args, cfg_name, config):
             ks.append(counter["v"])
             counter["v"] += 1
         if pool is None:
-            prev = start
             for k in ks:
-                prev = per_view(slots[k % P_], k, prev, None, None, None)
+                per_view(slots[k % P_], k)
         else:
-            enq = [threading.Event() for _ in ks]
-            evs = [torch.cuda.Event() for _ in ks]
-
             def worker(js):
-                try:
-                    torch.cuda.set_device(device)  # per thread
-                    for j in js:
-                        per_view(slots[ks[j] % P_], ks[j], start if j == 0 else evs[j - 1],
-                                 None if j == 0 else enq[j - 1], evs[j], enq[j])
-                except BaseException:
-                    for e in enq:  # never leave another thread waiting on this one
-                        e.set()
-                    raise
+                torch.cuda.set_device(device)  # per thread
+                for j in js:
+                    per_view(slots[ks[j] % P_], ks[j])
 
             # one task per slot: its views in order
             futs = [pool.submit(worker, [j for j in range(len(ks)) if ks[j] % P_ == si]) for si in range(P_)]
@@ -382,8 +361,7 @@ def run_gpu(args, cfg_name, config):
         fg.allreduce()  # NCCL sum over ranks (no-op at N = 1)
 
     def step():
-        run_views(lambda sl, k, prev, prev_enq, ev, enq: one_view(sl, my_views[k % len(my_views)], cots[k % n_ring],
-                                                                   prev, None, prev_enq, ev, enq))
+        run_views(lambda sl, k: one_view(sl, my_views[k % len(my_views)], cots[k % n_ring]))
 
     # ---------------- device-resident timed region (no per-kernel events: pipelined streams)
     for _ in range(args.warmup):
@@ -449,7 +427,7 @@ def run_gpu(args, cfg_name, config):
             e.record(stream)
             return e
 
-        def per_view_e2e(sl, k, prev, prev_enq, ev, enq):
+        def per_view_e2e(sl, k):
             nonlocal h2d, d2h
             i = slots.index(sl)
             io = ios[i]
@@ -467,7 +445,7 @@ def run_gpu(args, cfg_name, config):
                 h2d += dev_cots[i].numel() * 4
             if rec is not None:
                 rec["v0"] = tev(sl["stream"])
-            done = one_view(sl, my_views[k % len(my_views)], dev_cots[i], prev, io, prev_enq, ev, enq)
+            one_view(sl, my_views[k % len(my_views)], dev_cots[i], io)
             if rec is not None:
                 rec["v1"] = tev(sl["stream"])
                 rec["host_end"] = time.perf_counter()
@@ -485,7 +463,6 @@ def run_gpu(args, cfg_name, config):
                     rec["d2h1"] = tev(cout)
             if rec is not None:
                 tl.append(rec)
-            return done
 
         def step_e2e():
             run_views(per_view_e2e)

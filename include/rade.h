@@ -219,10 +219,11 @@ rd_status rd_blend_bwd(rd_view* view, const float* dL_dcolor, const float* dL_dd
                        const float* dL_dalpha, rd_stream stream);
 
 /* Stage 4, second half (K5): the per-Gaussian chain rule from the 2-D gradients of the last
- * rd_blend_bwd to means, scales, rotations, opacities and SH, ACCUMULATED (+=, plain
- * read-modify-write of each visible Gaussian's rows) into `grads`. Two calls that target
- * the same `grads` must not run concurrently (order them on one stream or with events);
- * rd_blend_bwd of another view may overlap this call. */
+ * rd_blend_bwd to means, scales, rotations, opacities and SH, ACCUMULATED (+=) into `grads`
+ * with L2 reductions (red.global.add): calls of different views into the same `grads` may
+ * run concurrently on different streams (the floating-point summation order, hence the
+ * rounding of the sum, then depends on timing). `grads` must be 16-byte aligned where
+ * rotations are. */
 rd_status rd_preprocess_bwd(rd_view* view, const rd_gaussians* g, const rd_grads* grads, rd_stream stream);
 
 /* NEXT-2: normal consistency (reading S22) on rendered maps (device, fp32,

@@ -149,6 +149,18 @@ __device__ __forceinline__ double sq_root(double v) { return sqrt(v); }
 // Loads one Gaussian and runs stage 1 up to the conic (no plane, no SH). False if culled.
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// Gradient accumulation into the caller's arrays is by L2 reductions (red.global.add, fire
+// and forget): no read round trip, and rd_preprocess_bwd calls of different views into the
+// same gradient arrays may run concurrently (the summation order, hence the rounding, then
+// depends on timing).
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add4(float4* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 // pf_sh (K1): once the cheap culls pass, prefetch the Gaussian's SH row into L2 so its fetch
 // overlaps the covariance math instead of following it.
 template <typename S>
@@ -461,27 +473,21 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam ca
     float drgb[3];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) drgb[ch] = rgb[ch] < 0.f ? 0.f : d_rgb[ch];
-    // += into this Gaussian's contiguous SH gradient row (16-B vector RMW when aligned;
-    // entries past the active degree are rewritten unchanged)
+    // += into this Gaussian's contiguous SH gradient row (16-B vector reductions when aligned;
+    // entries past the active degree get + 0)
     float* gsh = gr.sh + (int64_t)i * g.sh_coeffs * 3;
     if (vec) {
       float4* g4 = reinterpret_cast<float4*>(gsh);
-      float4 old[NV4];
-#pragma unroll
-      for (int q = 0; q < NV4; ++q) old[q] = g4[q];
 #pragma unroll
       for (int q = 0; q < NV4; ++q) {
         float d[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) d[e] = (4 * q + e) < NV ? Y[(4 * q + e) / 3] * drgb[(4 * q + e) % 3] : 0.f;
-        g4[q] = make_float4(old[q].x + d[0], old[q].y + d[1], old[q].z + d[2], old[q].w + d[3]);
+        red_add4(g4 + q, make_float4(d[0], d[1], d[2], d[3]));
       }
     } else {
-      float old[NV];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) old[j] = gsh[j];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) gsh[j] = old[j] + Y[j / 3] * drgb[j % 3];
+      for (int j = 0; j < NV; ++j) red_add(gsh + j, Y[j / 3] * drgb[j % 3]);
     }
     float c16[16];
 #pragma unroll
@@ -496,7 +502,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam ca
     dmu[2] += (gz - hz * dot) * idl;
   }
 #pragma unroll
-  for (int k = 0; k < 3; ++k) gr.means[3 * i + k] += dmu[k];
+  for (int k = 0; k < 3; ++k) red_add(gr.means + 3 * i + k, dmu[k]);
 }
 
 // K5b: geometry — centre, conic, depth plane and normal back to μ, s, q, o (dmu_extra: the
@@ -505,14 +511,10 @@ template <typename S>
 __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
                                                   const G2D* __restrict__ g2d, DevGrads& gr,
                                                   const float (&dmu_extra)[3]) {
-  // the G2D row and the gradient rows are needed only after the forward recompute: have
-  // them on their way to L2 now (no registers held)
+  // the G2D row is needed only after the forward recompute: have it on its way to L2 now
+  // (no registers held)
   prefetch_l2(g2d + i);
   prefetch_l2(reinterpret_cast<const char*>(g2d + i) + sizeof(G2D) - 1);
-  prefetch_l2(gr.means + 3 * i);
-  prefetch_l2(gr.scales + 3 * i);
-  prefetch_l2(gr.rot + 4 * i);
-  prefetch_l2(gr.opac + i);
   GF<S> f;
   if (!gaussian_forward<S>(g, i, cam, opt, f)) return;
   // the G2D sums of K4 → 2-D gradients (log2 e · ln 2 = 1 cancels between the stored
@@ -654,16 +656,6 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
                   a * dRq[6] + b * dRq[7]);
   const S qd = dqn[0] * w + dqn[1] * a + dqn[2] * b + dqn[3] * c;
 
-  // read-modify-write of the non-SH gradient rows, loads batched first
-  float om[3], os[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    om[k] = gr.means[3 * i + k];
-    os[k] = gr.scales[3 * i + k];
-  }
-  float4* grot = reinterpret_cast<float4*>(gr.rot) + i;
-  const float4 oq = *grot;
-  const float oo = gr.opac[i];
   float d_o_raw = d_o;
   if (g.filter3d) {  // through s' = √(s² + f²), o' = o·Π s/s' back to the raw s, o (S23)
 #pragma unroll
@@ -674,13 +666,14 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    gr.means[3 * i + k] = om[k] + (float)dmu[k] + dmu_extra[k];
-    gr.scales[3 * i + k] = os[k] + (float)ds[k];
+    red_add(gr.means + 3 * i + k, (float)dmu[k] + dmu_extra[k]);
+    red_add(gr.scales + 3 * i + k, (float)ds[k]);
   }
-  *grot = make_float4(oq.x + (float)((dqn[0] - f.qn[0] * qd) * f.qinv), oq.y + (float)((dqn[1] - f.qn[1] * qd) * f.qinv),
-                      oq.z + (float)((dqn[2] - f.qn[2] * qd) * f.qinv), oq.w + (float)((dqn[3] - f.qn[3] * qd) * f.qinv));
+  red_add4(reinterpret_cast<float4*>(gr.rot) + i,
+           make_float4((float)((dqn[0] - f.qn[0] * qd) * f.qinv), (float)((dqn[1] - f.qn[1] * qd) * f.qinv),
+                       (float)((dqn[2] - f.qn[2] * qd) * f.qinv), (float)((dqn[3] - f.qn[3] * qd) * f.qinv)));
   // α = min(α_max, o·G): d_o already excludes the clamp (K4)
-  gr.opac[i] = oo + d_o_raw;
+  red_add(gr.opac + i, d_o_raw);
 }
 
 // K5b, fp32, one thread per entry of the visible list (the ones that are not is_big)
@@ -763,10 +756,7 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
   for (int it = 0; it < NV4; ++it) {  // all 2·NV4 copies per lane in flight at once
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
     const uint32_t rid = __shfl_sync(0xffffffffu, id, row);
-    if ((vmask >> row) & 1u) {
-      cp_async16(&sc[row * P + c], &sh4[(int64_t)rid * L4 + c]);
-      cp_async16(&sg[row * P + c], &gsh4[(int64_t)rid * L4 + c]);
-    }
+    if ((vmask >> row) & 1u) cp_async16(&sc[row * P + c], &sh4[(int64_t)rid * L4 + c]);
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -799,8 +789,7 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
       float d[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) d[e] = (4 * q + e) < NV ? Y[(4 * q + e) / 3] * drgb[(4 * q + e) % 3] : 0.f;
-      const float4 o = sg[lane * P + q];
-      sg[lane * P + q] = make_float4(o.x + d[0], o.y + d[1], o.z + d[2], o.w + d[3]);
+      sg[lane * P + q] = make_float4(d[0], d[1], d[2], d[3]);
     }
     float c16[16];
 #pragma unroll
@@ -809,16 +798,16 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
     float gx, gy, gz;
     sh_basis_grad(hx, hy, hz, DEG, c16, gx, gy, gz);
     const float dot = gx * hx + gy * hy + gz * hz;  // through the normalisation of dir
-    gr.means[3 * (size_t)id] += (gx - hx * dot) * idl;
-    gr.means[3 * (size_t)id + 1] += (gy - hy * dot) * idl;
-    gr.means[3 * (size_t)id + 2] += (gz - hz * dot) * idl;
+    red_add(gr.means + 3 * (size_t)id, (gx - hx * dot) * idl);
+    red_add(gr.means + 3 * (size_t)id + 1, (gy - hy * dot) * idl);
+    red_add(gr.means + 3 * (size_t)id + 2, (gz - hz * dot) * idl);
   }
   __syncwarp();
 #pragma unroll
   for (int it = 0; it < NV4; ++it) {
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
     const uint32_t rid = __shfl_sync(0xffffffffu, id, row);
-    if ((vmask >> row) & 1u) gsh4[(int64_t)rid * L4 + c] = sg[row * P + c];
+    if ((vmask >> row) & 1u) red_add4(&gsh4[(int64_t)rid * L4 + c], sg[row * P + c]);
   }
 }
 
