@@ -392,14 +392,11 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
 // K1 kernel: per-Gaussian forward (plus the depth-sort input dkey[i], didx[i] = i), then
 // the warp-aggregated append of the visible ids to the visible list (one atomic per warp;
 // list order is arbitrary — K5a, its only user, is order-independent).
-#ifndef RD_K1_MINB
-#define RD_K1_MINB 1
-#endif
 #ifndef RD_K5_MINB
-#define RD_K5_MINB 6  // ≤ 80 registers: more warps in flight for the gathers (K5b 0.206 -> 0.192 ms)
+#define RD_K5_MINB 6  // K5b at ≤ 80 registers: more warps in flight for its gathers (0.096 -> 0.082 ms)
 #endif
 template <int DEG>
-__global__ void __launch_bounds__(256, RD_K1_MINB) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
+__global__ void __launch_bounds__(256) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
                                                          Record* __restrict__ rec, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
                                                          uint32_t* __restrict__ didx,
