@@ -272,9 +272,10 @@ rd_status rd_tsdf_integrate(const rd_tsdf* volume, const float* depths, const rd
  * order (x fastest, then y, z), triangles in table order: triangles = DEVICE f32
  * [capacity][3 vertices][xyz], caller-owned. *n_triangles (HOST) receives the count; the
  * triangles are written only when triangles != NULL and capacity ≥ the count (call once with
- * NULL to size the buffer). Synchronises `stream` once (to read the count back); uses
- * stream-ordered temporaries of 8 B per cell. Only volume->{origin, voxel_size, dims, tsdf,
- * weight} are read. */
+ * NULL to size the buffer, or pass a capacity guess and repeat only if it was short).
+ * Synchronises `stream` once (to read the count back); its temporaries (8 B per cell + the
+ * scan's) are a per-host-thread, grow-only cache kept across calls. Only volume->{origin,
+ * voxel_size, dims, tsdf, weight} are read. */
 rd_status rd_marching_cubes(const rd_tsdf* volume, float iso, float* triangles, int64_t capacity,
                             int64_t* n_triangles, rd_stream stream);
 

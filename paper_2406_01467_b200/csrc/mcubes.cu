@@ -167,15 +167,22 @@ __global__ void __launch_bounds__(256) k_mc_emit(Vol v, float iso, const uint32_
 
 }  // namespace
 
+namespace {
+// Per host thread, grow-only scratch reused across calls (count, offset, scan temp) and a
+// pinned slot for the count read-back: a fresh cudaMallocAsync / cudaMallocHost per call cost
+// milliseconds (and cudaFreeHost synchronises the device).
+struct McScratch {
+  uint32_t *count = nullptr, *offset = nullptr, *host = nullptr;
+  void* temp = nullptr;
+  size_t cells = 0, temp_bytes = 0;
+};
+thread_local McScratch t_mc;
+}  // namespace
+
 cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int dims[3], const float* tsdf,
                                   const float* weight, float iso, float* triangles, int64_t capacity,
                                   int64_t* n_triangles, cudaStream_t s) {
-  static McTable table;
-  static bool built = false;
-  if (!built) {
-    table = build_table();
-    built = true;
-  }
+  static const McTable table = build_table();  // thread-safe one-time construction
   cudaError_t e = cudaMemcpyToSymbolAsync(c_tri, table.tri, sizeof(table.tri), 0, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(c_ntri, table.ntri, sizeof(table.ntri), 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
@@ -186,30 +193,41 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
   if (ncell > 0x7fffffffLL) return cudaErrorInvalidValue;
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)ncell);
-  uint32_t *count = nullptr, *offset = nullptr, *host = nullptr;
-  void* temp = nullptr;
-  e = cudaMallocAsync(&count, ncell * 4, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&offset, ncell * 4, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&temp, scan_bytes, s);
-  if (e == cudaSuccess) e = cudaMallocHost(&host, 8);
-  if (e == cudaSuccess) {
-    const unsigned grid = (unsigned)((ncell + 255) / 256);
-    k_mc_count<<<grid, 256, 0, s>>>(v, iso, count);
-    cub::DeviceScan::ExclusiveSum(temp, scan_bytes, count, offset, (int)ncell, s);
-    cudaMemcpyAsync(host, offset + (ncell - 1), 4, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(host + 1, count + (ncell - 1), 4, cudaMemcpyDeviceToHost, s);
-    e = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) {
-      *n_triangles = (int64_t)host[0] + host[1];
-      if (triangles && capacity >= *n_triangles) k_mc_emit<<<grid, 256, 0, s>>>(v, iso, offset, triangles);
-      e = cudaGetLastError();
-    }
+  McScratch& m = t_mc;
+  if (!m.host) {
+    e = cudaMallocHost(&m.host, 8);
+    if (e != cudaSuccess) return e;
   }
-  if (count) cudaFreeAsync(count, s);
-  if (offset) cudaFreeAsync(offset, s);
-  if (temp) cudaFreeAsync(temp, s);
-  if (host) cudaFreeHost(host);
-  return e;
+  if (m.cells < (size_t)ncell) {
+    e = cudaStreamSynchronize(s);  // the old buffers may still be in use on s
+    if (m.count) cudaFree(m.count);
+    if (m.offset) cudaFree(m.offset);
+    m.count = m.offset = nullptr;
+    m.cells = 0;
+    if (e == cudaSuccess) e = cudaMalloc(&m.count, (size_t)ncell * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&m.offset, (size_t)ncell * 4);
+    if (e != cudaSuccess) return e;
+    m.cells = (size_t)ncell;
+  }
+  if (m.temp_bytes < scan_bytes) {
+    e = cudaStreamSynchronize(s);
+    if (m.temp) cudaFree(m.temp);
+    m.temp = nullptr;
+    m.temp_bytes = 0;
+    if (e == cudaSuccess) e = cudaMalloc(&m.temp, scan_bytes);
+    if (e != cudaSuccess) return e;
+    m.temp_bytes = scan_bytes;
+  }
+  const unsigned grid = (unsigned)((ncell + 255) / 256);
+  k_mc_count<<<grid, 256, 0, s>>>(v, iso, m.count);
+  cub::DeviceScan::ExclusiveSum(m.temp, scan_bytes, m.count, m.offset, (int)ncell, s);
+  cudaMemcpyAsync(m.host, m.offset + (ncell - 1), 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(m.host + 1, m.count + (ncell - 1), 4, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *n_triangles = (int64_t)m.host[0] + m.host[1];
+  if (triangles && capacity >= *n_triangles) k_mc_emit<<<grid, 256, 0, s>>>(v, iso, m.offset, triangles);
+  return cudaGetLastError();
 }
 
 }  // namespace rade

@@ -285,6 +285,7 @@ class TsdfVolume:
         X, Y, Z = self.dims
         self.tsdf = torch.ones((Z, Y, X), dtype=torch.float32, device=device)
         self.weight = torch.zeros((Z, Y, X), dtype=torch.float32, device=device)
+        self._mc_capacity = 0  # triangle buffer size guess for rd_marching_cubes (last count + 25%)
 
     def c_struct(self):
         s = N.RdTsdf()
@@ -318,8 +319,14 @@ def rd_marching_cubes(volume: TsdfVolume, iso=0.0, stream=None):
     s = volume.c_struct()
     n = ctypes.c_int64(0)
     lib = N.load()
-    N.check(lib.rd_marching_cubes(ctypes.byref(s), float(iso), None, 0, ctypes.byref(n), _stream_ptr(stream)),
-            "rd_marching_cubes")
+    # one call when the buffer of the volume's previous extraction (+25%) is large enough
+    cap = getattr(volume, "_mc_capacity", 0)
+    buf = torch.empty((cap, 3, 3), dtype=torch.float32, device=volume.tsdf.device) if cap else None
+    N.check(lib.rd_marching_cubes(ctypes.byref(s), float(iso), _ptr(buf) if cap else None, cap, ctypes.byref(n),
+                                  _stream_ptr(stream)), "rd_marching_cubes")
+    if cap and n.value <= cap:
+        return buf[:n.value]
+    volume._mc_capacity = int(n.value * 1.25) + 1024
     tris = torch.empty((n.value, 3, 3), dtype=torch.float32, device=volume.tsdf.device)
     if n.value:
         N.check(lib.rd_marching_cubes(ctypes.byref(s), float(iso), _ptr(tris), n.value, ctypes.byref(n),
