@@ -1,13 +1,13 @@
 // render.cu — stage 3 (K3, blend forward) and the first half of stage 4 (K4, blend
 // backward) of the RaDe-GS rasterizer, sm_100a.
 //
-// One CTA per TILE×TILE tile, TILE²/2 threads, each owning two pixels; each warp owns a
-// compact band of rows (16×4 pixels at TILE 16), which keeps its ballot-based skipping
-// tight (pixels sampled at (i+½, j+½), reading S4). Each CTA walks its
-// tile's depth-sorted list (ranges from K2) in batches of TILE² splats staged in shared
-// memory (two coalesced 64-B record gathers per thread); every shared-memory broadcast,
-// loop step and — in K4 — every warp reduction then serves two pixels. The block leaves
-// as soon as every pixel is saturated (__syncthreads_count).
+// One CTA per TILE×TILE tile, TILE²/2 threads, each owning two pixels of the same column;
+// each warp owns an 8×8 pixel quadrant (lane l: column l % 8, rows l / 8 and l / 8 + 4), so
+// at the default 8×8 tiles a CTA is one warp (pixels sampled at (i+½, j+½), reading S4).
+// Each CTA walks its tile's depth-sorted list (ranges from K2) in batches of TILE² splats
+// staged in shared memory (one coalesced 64-B record gather per splat); every shared-memory
+// broadcast, loop step and — in K4 — every warp reduction then serves two pixels per thread.
+// The block leaves as soon as every pixel is saturated (__syncthreads_count).
 //
 // Per (pixel, splat), front to back (Eq.3; readings S1, S8, S9, S10):
 //   α = min(α_max, o·exp(−½ Δᵀ conic Δ)), Δ = (u_c − u, v_c − v)  (skip if α < α_min)
