@@ -490,6 +490,24 @@ def test_marching_cubes_random_volume_every_configuration():
     np.testing.assert_allclose(gpu, ref, atol=1e-5)
 
 
+def test_marching_cubes_capacity_guess_paths():
+    """The binding's one-call path (a capacity guess kept from the volume's last extraction)
+    and its fallback (guess too small: count, allocate, emit) give the oracle's soup."""
+    rng = np.random.default_rng(8)
+    t = rng.uniform(-1, 1, (12, 12, 12)).astype(np.float32)
+    w = np.ones_like(t)
+    ref = oracle.marching_cubes(t, w, (0.0, 0.0, 0.0), 0.5, 0.0)
+    vol = P.TsdfVolume((0.0, 0.0, 0.0), 0.5, (12, 12, 12))
+    vol.tsdf.copy_(torch.as_tensor(t))
+    vol.weight.copy_(torch.as_tensor(w))
+    for cap in (0, 7, None):  # no guess, too small, the binding's own guess
+        if cap is not None:
+            vol._mc_capacity = cap
+        gpu = P.rd_marching_cubes(vol).double().cpu().numpy()
+        assert gpu.shape == ref.shape, cap
+        np.testing.assert_allclose(gpu, ref, atol=1e-5)
+
+
 def test_marching_cubes_degenerate_volumes():
     """Empty (< 2 voxels along an axis), unobserved (weight 0), all-inside / all-outside:
     no triangles; a too-small capacity returns the count and writes nothing."""
