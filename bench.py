@@ -293,21 +293,35 @@ def run_gpu(args, cfg_name, config):
     counter = {"v": 0}
     main_stream = torch.cuda.current_stream(device)
 
+    phase_log = [] if os.environ.get("RADE_PHASES") else None
+
     def one_view(slot, cam, cot, io=None):
         """io (end-to-end pass): events that order the view's forward after the D2H of the
         slot's previous maps, publish the forward for its D2H, hold K4 until the H2D of the
         cotangents landed, and publish K4 (the cotangent buffer is free again). K5 adds the
         view's gradients with L2 reductions, so the views' K5 calls need no mutual order."""
         st, vw, o = slot["stream"], slot["view"], slot["outs"]
+        ph = [] if phase_log is not None else None  # diagnostics: per-view phase events
+
+        def mark():
+            if ph is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                ph.append(e)
         with torch.cuda.stream(st):
+            mark()
             P.rd_preprocess(vw, g, cam, opts, stream=st)
             P.rd_bin(vw, stream=st)
+            mark()
             if io:
                 st.wait_event(io["outs_free"])
             if args.distortion:  # NEXT-1: + the depth-distortion map and its gradient
+                mark()
                 P.rd_render_fwd_ex(vw, o["color"], o["depth"], o["normal"], o["alpha"], o["distortion"], stream=st)
             else:
+                mark()
                 P.rd_render_fwd(vw, o["color"], o["depth"], o["normal"], o["alpha"], stream=st)
+            mark()
             if io:
                 io["fwd_done"].record(st)
                 st.wait_event(io["cot_ready"])
@@ -324,8 +338,12 @@ def run_gpu(args, cfg_name, config):
                 P.rd_blend_bwd(vw, cot[0:3], cot[3], cot[4:7], cot[7], stream=st)  # K4: view-private output
             if io:
                 io["k4_done"].record(st)
+            mark()
             P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
             slot["done"].record(st)
+            mark()
+        if ph is not None:
+            phase_log.append(ph)
 
     pool = ThreadPoolExecutor(max_workers=max(1, args.pipeline)) if args.host_threads else None
 
@@ -382,6 +400,26 @@ def run_gpu(args, cfg_name, config):
     elapsed_ms = max_over_ranks(e0.elapsed_time(e1), dist_on, device)
     total_views = args.steps * B * ws
     value = total_views / (elapsed_ms / 1e3)
+
+    if os.environ.get("RADE_PROF_CONC"):  # diagnostics: per-kernel times under the concurrent schedule
+        for sl in slots:
+            P.rd_set_profiling(sl["view"], True)
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        acc = {}
+        for sl in slots:
+            t = P.rd_get_timings(sl["view"], reset=True)
+            P.rd_set_profiling(sl["view"], False)
+            for k, v in t["ms"].items():
+                acc[k] = acc.get(k, 0.0) + v / max(t["views"], 1) / len(slots)
+        print("concurrent per-kernel ms per view:", {k: round(v, 4) for k, v in acc.items()}, flush=True)
+    if phase_log:  # diagnostics: [start, binned, fwd start, fwd end, K5 start, K5 end] per view, ms
+        t0e = phase_log[-4 * 5][0] if len(phase_log) >= 20 else phase_log[0][0]
+        rows = [[t0e.elapsed_time(e) for e in ph] for ph in phase_log[-20:]]
+        json.dump(rows, open(os.environ["RADE_PHASES"], "w"))
+        phase_log.clear()
 
     # ---------------- per-kernel timings: the same steps again, serialised on one stream with
     # the ABI's CUDA-event hooks around every kernel (rd_set_profiling)

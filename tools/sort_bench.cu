@@ -8,18 +8,18 @@
 #include <cstdlib>
 #include <vector>
 
-template <int THREADS, int ITEMS>
+template <int THREADS, int ITEMS, int RB = 8>
 struct Hub {
   using Base = cub::detail::radix::policy_hub<uint32_t, uint32_t, uint32_t>;
   struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, Policy1000> {
     using B = typename Base::Policy1000;
     static constexpr bool ONESWEEP = true;
-    static constexpr int ONESWEEP_RADIX_BITS = 8;
+    static constexpr int ONESWEEP_RADIX_BITS = RB;
     using HistogramPolicy = typename B::HistogramPolicy;
     using ExclusiveSumPolicy = typename B::ExclusiveSumPolicy;
     using OnesweepPolicy =
         cub::AgentRadixSortOnesweepPolicy<THREADS, ITEMS, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
-                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, RB>;
     using ScanPolicy = typename B::ScanPolicy;
     using DownsweepPolicy = typename B::DownsweepPolicy;
     using AltDownsweepPolicy = typename B::AltDownsweepPolicy;
@@ -54,17 +54,17 @@ float run(uint32_t* k0, uint32_t* k1, uint32_t* v0, uint32_t* v1, const uint32_t
   return best;
 }
 
-template <int T, int I>
+template <int T, int I, int RB = 8>
 void one(const char* name, uint32_t* k0, uint32_t* k1, uint32_t* v0, uint32_t* v1, const uint32_t* kin,
          const uint32_t* vin, uint32_t n, int bits) {
   size_t tb = 0;
   cub::DoubleBuffer<uint32_t> K(k0, k1), V(v0, v1);
-  cub::DispatchRadixSort<false, uint32_t, uint32_t, uint32_t, Hub<T, I>>::Dispatch(nullptr, tb, K, V, n, 0, bits, true,
-                                                                                 0);
+  cub::DispatchRadixSort<false, uint32_t, uint32_t, uint32_t, Hub<T, I, RB>>::Dispatch(nullptr, tb, K, V, n, 0, bits,
+                                                                                     true, 0);
   void* tmp;
   cudaMalloc(&tmp, tb);
-  float ms = run<Hub<T, I>>(k0, k1, v0, v1, kin, vin, n, bits, tmp, tb, 20);
-  printf("%-10s n=%u bits=%d  %d x %d : %.1f us\n", name, n, bits, T, I, ms * 1e3);
+  float ms = run<Hub<T, I, RB>>(k0, k1, v0, v1, kin, vin, n, bits, tmp, tb, 20);
+  printf("%-10s n=%u bits=%d  %d x %d rb=%d : %.1f us\n", name, n, bits, T, I, RB, ms * 1e3);
   cudaFree(tmp);
 }
 
@@ -107,14 +107,10 @@ int main() {
   one<T, I>("depth/2", k0, k1, v0, v1, kin, vin, N / 2, 32); \
   one<T, I>("tile", k0, k1, v0, v1, tin, vin, M, 14);
   CFG(512, 12)
-  CFG(512, 16)
-  CFG(512, 20)
-  CFG(640, 12)
-  CFG(768, 12)
-  CFG(768, 8)
-  CFG(1024, 8)
-  CFG(1024, 6)
-  CFG(512, 10)
+  one<512, 12, 7>("tile", k0, k1, v0, v1, tin, vin, M, 14);
+  one<512, 12, 6>("tile", k0, k1, v0, v1, tin, vin, M, 14);
+  one<256, 16, 7>("tile", k0, k1, v0, v1, tin, vin, M, 14);
+  one<512, 12, 8>("depth", k0, k1, v0, v1, kin, vin, N, 24);
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
