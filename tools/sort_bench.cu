@@ -107,9 +107,9 @@ int main() {
   one<T, I>("depth/2", k0, k1, v0, v1, kin, vin, N / 2, 32); \
   one<T, I>("tile", k0, k1, v0, v1, tin, vin, M, 14);
   CFG(512, 12)
+  // digit widths other than 8 time fine but sort wrongly with this ranking policy (the
+  // binning parity tests failed with 7-bit digits): timing only, do not adopt
   one<512, 12, 7>("tile", k0, k1, v0, v1, tin, vin, M, 14);
-  one<512, 12, 6>("tile", k0, k1, v0, v1, tin, vin, M, 14);
-  one<256, 16, 7>("tile", k0, k1, v0, v1, tin, vin, M, 14);
   one<512, 12, 8>("depth", k0, k1, v0, v1, kin, vin, N, 24);
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
