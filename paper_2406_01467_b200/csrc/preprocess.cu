@@ -392,9 +392,11 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
 // K1 kernel: per-Gaussian forward (plus the depth-sort input dkey[i], didx[i] = i), then
 // the warp-aggregated append of the visible ids to the visible list (one atomic per warp;
 // list order is arbitrary — K5a, its only user, is order-independent).
-#ifndef RD_K5_MINB
-#define RD_K5_MINB 6  // K5b at ≤ 80 registers: more warps in flight for its gathers (0.096 -> 0.082 ms)
+#ifndef RD_K5_THREADS
+#define RD_K5_THREADS 128
 #endif
+// K5b at ≤ 80 registers (768 threads per SM): more warps in flight for its gathers (0.096 -> 0.082 ms)
+#define RD_K5_MINB (768 / RD_K5_THREADS)
 template <int DEG>
 #ifndef RD_K1_THREADS
 #define RD_K1_THREADS 64  // finer blocks fill the SMs more evenly: 0.107 -> 0.101 ms
@@ -678,7 +680,7 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
 
 // K5b, fp32, one thread per entry of the visible list (the ones that are not is_big)
 // tiles (the others are K5b64's).
-__global__ void __launch_bounds__(128, RD_K5_MINB) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
+__global__ void __launch_bounds__(RD_K5_THREADS, RD_K5_MINB) k_preprocess_bwd(DevGauss g, DevCam cam, DevOpt opt,
                                                         const uint32_t* __restrict__ touched,
                                                         const uint32_t* __restrict__ vis, int64_t n_vis,
                                                         const G2D* __restrict__ g2d, DevGrads gr) {
@@ -865,8 +867,8 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
     k_preprocess_bwd64<<<(unsigned)((n_big + 127) / 128), 128, 0, s>>>(g, cam, opt, big, n_big, g2d, grads);
   if (n_vis > 0) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((n_vis + threads - 1) / threads));
-    cfg.blockDim = dim3(threads);
+    cfg.gridDim = dim3((unsigned)((n_vis + RD_K5_THREADS - 1) / RD_K5_THREADS));
+    cfg.blockDim = dim3(RD_K5_THREADS);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
