@@ -32,8 +32,10 @@ struct PixF {  // forward state of one pixel
   float d0, D1, D2;  // depth distortion (S21): Σω(d − d0), Σω(d − d0)², d0 = first blended depth
   int last, med;
   unsigned n_eval, n_blend;
-  bool done;
 };
+// A saturated (or outside) pixel is marked by py = +inf: pair_power then yields e = −inf or
+// NaN, whose α test fails, so the blend loop needs no separate "done" test per pair.
+__device__ __forceinline__ bool pix_done(const PixF& s) { return s.py == __int_as_float(0x7f800000); }
 
 __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool inside) {
   s.px = px;
@@ -44,7 +46,7 @@ __device__ __forceinline__ void pixf_init(PixF& s, float px, float py, bool insi
   s.last = 0;
   s.med = -1;
   s.n_eval = s.n_blend = 0;
-  s.done = !inside;
+  if (!inside) s.py = __int_as_float(0x7f800000);
 }
 
 // The blend part of one (pixel, splat) step of Eq.3 (pair_power established α ≥ α_min, S8)
@@ -58,7 +60,7 @@ __device__ __forceinline__ void fwd_blend(PixF& s, const PairAlpha& pa, const fl
   const float alpha = fminf(opt.alpha_max, ex2_approx(pa.e));
   const float Tn = __fmul_rn(s.T, __fsub_rn(1.f, alpha));
   if (Tn < opt.T_min) {  // stop before blending this splat (S8)
-    s.done = true;
+    s.py = __int_as_float(0x7f800000);  // done
     return;
   }
   const float w = __fmul_rn(alpha, s.T);
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   pixf_init(A, (float)px + 0.5f, (float)pyA + 0.5f, inA);
   pixf_init(B, (float)px + 0.5f, (float)pyB + 0.5f, inB);
   for (int base = 0; base < total; base += BATCH) {
-    if (__syncthreads_count(A.done && B.done) == NT) break;
+    if (__syncthreads_count(pix_done(A) && pix_done(B)) == NT) break;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int t = (int)threadIdx.x + h * NT;
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       }
     }
     __syncthreads();
-    if (__all_sync(0xffffffffu, A.done && B.done)) continue;  // this warp is saturated
+    if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) continue;  // this warp is saturated
     const int cnt = min(BATCH, total - base);
     // 8×8 tiles: the binning rect is already tight, filtering costs more than it saves
     const int nsel = kFilter ? warp_filter(s0, s1, s3, cnt, lane, fx0, fx0 + 7.f, fy0, fy0 + 7.f,
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
     const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
     unsigned long long bm = 0ull;  // kMask: blend-mask bits of this batch (bit j: position base + j)
     for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
-      if (__all_sync(0xffffffffu, A.done && B.done)) break;
+      if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) break;
       const int j = kFilter ? (int)wlist[warp][i] : i;
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
@@ -256,10 +258,10 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, col, A.py, opt.log2_alpha_min);
       const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, col, B.py, opt.log2_alpha_min);
       if (PROF) {
-        A.n_eval += A.done ? 0u : 1u;
-        B.n_eval += B.done ? 0u : 1u;
+        A.n_eval += pix_done(A) ? 0u : 1u;
+        B.n_eval += pix_done(B) ? 0u : 1u;
       }
-      const bool okA = !A.done && pA.pass, okB = !B.done && pB.pass;  // α ≥ α_min (S8)
+      const bool okA = pA.pass, okB = pB.pass;  // α ≥ α_min (S8); false for saturated pixels
       if (!__any_sync(0xffffffffu, okA || okB)) continue;  // no pixel of the warp blends it
       if (kMask) bm |= 1ull << j;  // some pixel of the tile blends (or stops at) position base + j
       const float4 a2 = lds128(a + 32u * BATCH);
