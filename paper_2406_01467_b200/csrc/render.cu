@@ -33,6 +33,14 @@ struct PixF {  // forward state of one pixel
   int last, med;
   unsigned n_eval, n_blend;
 };
+// Pins a loop-invariant value in a register (ptxas otherwise rematerialises it every
+// iteration, e.g. (float)px + 0.5 or a constant-bank load).
+__device__ __forceinline__ float opaque(float x) {
+  float r;
+  asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // A saturated (or outside) pixel is marked by py = +inf: pair_power then yields e = −inf or
 // NaN, whose α test fails, so the blend loop needs no separate "done" test per pair.
 __device__ __forceinline__ bool pix_done(const PixF& s) { return s.py == __int_as_float(0x7f800000); }
@@ -247,6 +255,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                            opt.log2_alpha_min, wlist[warp])
                              : cnt;
     const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
+    const float cpx = opaque(A.px), la_min = opaque(opt.log2_alpha_min);
     unsigned long long bm = 0ull;  // kMask: blend-mask bits of this batch (bit j: position base + j)
     for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
       if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) break;
@@ -254,9 +263,9 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
-      const PairColumn col = pair_column(a0, ulo, A.px);  // A and B share the column
-      const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, col, A.py, opt.log2_alpha_min);
-      const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, col, B.py, opt.log2_alpha_min);
+      const PairColumn col = pair_column(a0, ulo, cpx);  // A and B share the column
+      const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, col, A.py, la_min);
+      const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, col, B.py, la_min);
       if (PROF) {
         A.n_eval += pix_done(A) ? 0u : 1u;
         B.n_eval += pix_done(B) ? 0u : 1u;
