@@ -349,6 +349,7 @@ __device__ __forceinline__ void pixb_init(PixB& s, float px, float py, bool insi
     if (dL_dcolor) { s.gC0 = dL_dcolor[pix]; s.gC1 = dL_dcolor[HW + pix]; s.gC2 = dL_dcolor[2 * HW + pix]; }
     if (dL_dnormal) { s.gN0 = dL_dnormal[pix]; s.gN1 = dL_dnormal[HW + pix]; s.gN2 = dL_dnormal[2 * HW + pix]; }
     if (dL_ddepth) s.gD = dL_ddepth[pix];
+    if (s.gD == 0.f) s.med = -1;  // no median-depth gradient from this pixel: never a hit
     if (dL_dalpha) gA = dL_dalpha[pix];
     if (dio.dL_ddist) {
       s.gL = 4.f * dio.dL_ddist[pix];
@@ -418,7 +419,6 @@ __device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[NG], const PairAlp
 // Median-depth sums Σ g_D, Σ g_D·dx, Σ g_D·dy (G2D f[7..9]) for D = z_c + p·Δ (Eq.4,
 // PAPER:443-450): one pixel per splat at most, so added directly (no warp reduction).
 __device__ __forceinline__ void bwd_median(const PixB& s, G2D* row, const PairAlpha& pa) {
-  if (s.gD == 0.f) return;
   atomicAdd(&row->f[7], s.gD);
   atomicAdd(&row->f[8], s.gD * pa.dx);
   atomicAdd(&row->f[9], s.gD * pa.dy);
@@ -580,9 +580,17 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
       for (int k = 1; k < PPT; ++k)
         if (__any_sync(0xffffffffu, act[k])) bwd_accum<DIST, NG, false>(s[k], g, pa[k], act[k], a1, a2, a3, opt);
       G2D* dst = g2d + lds32(a_id + 4u * j);
+      bool hit[PPT], any_hit = false;  // the splat is this pixel's median one (med = -1 if g_D = 0)
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (act[k] && pos == s[k].med) bwd_median(s[k], dst, pa[k]);
+      for (int k = 0; k < PPT; ++k) {
+        hit[k] = act[k] && pos == s[k].med;
+        any_hit = any_hit || hit[k];
+      }
+      if (__any_sync(0xffffffffu, any_hit)) {  // warp-uniform: most steps have no median hit
+#pragma unroll
+        for (int k = 0; k < PPT; ++k)
+          if (hit[k]) bwd_median(s[k], dst, pa[k]);
+      }
       if (__popc(am) == 1) {  // one contributing thread in this warp: no reduction needed
         if (any) {
 #pragma unroll
