@@ -552,7 +552,9 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
         j = i;
         pos = start + j;
       }
-      if (!__any_sync(0xffffffffu, pos < mylast)) continue;  // the whole warp is past its pixels' lists
+      // the whole warp is past its pixels' lists (never at 8×8 tiles: the warp is the tile, and
+      // the walk starts at the tile's largest n_contrib)
+      if (!kMask && !__any_sync(0xffffffffu, pos < mylast)) continue;
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
