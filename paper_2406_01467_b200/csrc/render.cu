@@ -469,7 +469,8 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   __shared__ uint32_t sid[BATCH];
-  __shared__ uint16_t wlist[NW][BATCH];  // per warp: batch slots (kFilter) / list offsets (kMask)
+  __shared__ uint16_t wlist[kFilter ? NW : 1][kFilter ? BATCH : 1];  // per warp: batch slots (kFilter)
+  __shared__ int spos[kMask ? BATCH : 1];                            // list position per slot (kMask)
   __shared__ __align__(16) float sred[NW][16 * kRedPitch];
   __shared__ int s_maxlast;
 
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
           const uint32_t id = ids[range.x + start + t];
           const Record* r = rec + id;
           sid[slot] = id;
-          wlist[0][slot] = (uint16_t)t;
+          spos[slot] = start + t;
           sbuf[0][slot] = r->r0;
           sbuf[1][slot] = r->r1;
           sbuf[2][slot] = r->r2;
@@ -538,13 +539,13 @@ __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     if (kFilter)
       nsel = warp_filter(sbuf[0], sbuf[1], sbuf[3], cnt, lane, fx0, fx0 + 7.f, fy0, fy0 + (float)(SH - 1),
                          opt.log2_alpha_min, wlist[warp]);
-    const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid), a_wl = smem_addr(wlist[warp]);
+    const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid), a_pos = smem_addr(spos);
     for (int i = nsel - 1; i >= 0; --i) {
       // slot j of the staged batch, at list position pos
       int j, pos;
       if (kMask) {
         j = i;
-        pos = start + (int)(lds32(a_wl + 2u * (unsigned)(i & ~1)) >> (16 * (i & 1)) & 0xffffu);
+        pos = (int)lds32(a_pos + 4u * (unsigned)i);
       } else if (kFilter) {
         j = (int)wlist[warp][i];
         pos = start + j;
