@@ -255,8 +255,9 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                            opt.log2_alpha_min, wlist[warp])
                              : cnt;
     const unsigned a_s0 = smem_addr(s0);  // s0..s3 are contiguous
-    const float cpx = opaque(A.px), la_min = opaque(opt.log2_alpha_min);
-    unsigned long long bm = 0ull;  // kMask: blend-mask bits of this batch (bit j: position base + j)
+    const float cpx = opaque(A.px);
+    const float la_min = __shfl_sync(0xffffffffu, opt.log2_alpha_min, 0);  // a register, not a per-step LDC
+    unsigned mine = 0u;  // kMask: bit 0 / 1 = this batch's step lane / lane + 32 was blended
     for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
       if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) break;
       const int j = kFilter ? (int)wlist[warp][i] : i;
@@ -272,16 +273,20 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       }
       const bool okA = pA.pass, okB = pB.pass;  // α ≥ α_min (S8); false for saturated pixels
       if (!__any_sync(0xffffffffu, okA || okB)) continue;  // no pixel of the warp blends it
-      if (kMask) bm |= 1ull << j;  // some pixel of the tile blends (or stops at) position base + j
+      if (kMask && (j & 31) == lane) mine |= 1u + (unsigned)(j >> 5);  // some pixel blends (or stops at) base + j
       const float4 a2 = lds128(a + 32u * BATCH);
       const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;
       if (okA) fwd_blend<PROF, DIST>(A, pA, a1, a2, a3, a + 48u * BATCH, base + j, opt);
       if (okB) fwd_blend<PROF, DIST>(B, pB, a1, a2, a3, a + 48u * BATCH, base + j, opt);
     }
-    if (kMask && lane == 0) {  // the batch's words (positions past the last step: zero bits);
-      uint32_t* w = bmask + blend_mask_word(range.x, base, tile);  // a word past the list's end
-      w[0] = (uint32_t)bm;                                         // may be the next tile's first
-      if (base + 32 < total) w[1] = (uint32_t)(bm >> 32);
+    if (kMask) {  // the batch's words (positions past the last step: zero bits); a word past
+      const unsigned lo = __ballot_sync(0xffffffffu, mine & 1u);  // the list's end may be the
+      const unsigned hi = __ballot_sync(0xffffffffu, mine & 2u);  // next tile's first
+      if (lane == 0) {
+        uint32_t* w = bmask + blend_mask_word(range.x, base, tile);
+        w[0] = lo;
+        if (base + 32 < total) w[1] = hi;
+      }
     }
   }
   if (PROF) {
