@@ -442,10 +442,15 @@ __device__ __forceinline__ void g2d_add(G2D* row, int k, float v) {
 
 // K4: one CTA per tile, TILE²/PPT threads, PPT pixels per thread. Warp w owns an 8-wide,
 // 4·PPT-tall pixel rectangle of the tile (lane l: column l % 8, rows l / 8 + 4k, k < PPT).
-// Per staged batch the warp filters the splats that can reach its rectangle (warp_filter),
-// then, per such splat in reverse order, evaluates α for its pixels, skips the splat if none
-// uses it (ballot), otherwise accumulates the 15 sums over the thread's PPT pixels, reduces
-// them across the warp and issues one L2 atomic per value.
+// The list is walked backwards from the tile's largest n_contrib in batches of TILE² list
+// positions. At 8×8 tiles (kMask) only the positions K3's blend mask marks are staged
+// (compacted, with their 32-bit positions); at 16×16 each warp filters the staged batch down
+// to the splats that can reach its rectangle (warp_filter). Per splat the warp evaluates α
+// for its pixels, skips the splat if none uses it (ballot), otherwise accumulates the 12
+// sums (15 with L_d) over the thread's PPT pixels, adds the median-depth terms of the pixels
+// whose median splat it is (warp-uniform hit test), and either lets up to kDirectLanes
+// contributing lanes add their sums with atomics or reduces the sums across the warp
+// (smem_reduce) and issues one L2 atomic per value.
 template <int TILE, int PPT, bool DIST>
 __global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
