@@ -279,14 +279,14 @@ def run_gpu(args, cfg_name, config):
         st = torch.cuda.Stream(device)
         with torch.cuda.stream(st):  # the view's scratch is allocated on its own stream
             slot = {"stream": st, "view": P.View(device),
-                    "outs": {"color": torch.empty((3, H, W), device=device),
-                             "depth": torch.empty((H, W), device=device),
-                             "normal": torch.empty((3, H, W), device=device),
-                             "alpha": torch.empty((H, W), device=device),
-                             "distortion": torch.empty((H, W), device=device),
-                             "consistency": torch.empty((H, W), device=device)},
+                    # the maps are planes of one [10, H, W] buffer: one D2H copy per view (e2e)
+                    "outbuf": torch.empty((10, H, W), device=device),
+
                     "cot": torch.empty((10, H, W), device=device),
                     "done": torch.cuda.Event()}
+            ob = slot["outbuf"]
+            slot["outs"] = {"color": ob[0:3], "depth": ob[3], "normal": ob[4:7], "alpha": ob[7],
+                            "distortion": ob[8], "consistency": ob[9]}
         slots.append(slot)
     view = slots[0]["view"]
     outs = slots[0]["outs"]
@@ -443,10 +443,8 @@ def run_gpu(args, cfg_name, config):
         host_cots = [c[:nch].cpu().pin_memory() for c in cots]
         h2d = 0
         d2h = 0
-        out_keys = [k for k in outs if (k != "distortion" or args.distortion)
-                    and (k != "consistency" or args.normal_consistency)]
-        host_outs = [{k: torch.empty(outs[k].shape, dtype=torch.float32).pin_memory() for k in out_keys}
-                     for _ in slots]
+        n_out = 10 if args.normal_consistency else 9 if args.distortion else 8  # map planes read back
+        host_outs = [torch.empty((n_out, H, W), dtype=torch.float32).pin_memory() for _ in slots]
         dev_cots = [torch.empty((nch, H, W), device=device) for _ in slots]
 
         # transfers on their own copy streams, overlapped with the compute of other views:
@@ -491,11 +489,10 @@ def run_gpu(args, cfg_name, config):
                 cout.wait_event(io["fwd_done"])
                 if rec is not None:
                     rec["d2h0"] = tev(cout)
-                for key in out_keys:
-                    t = sl["outs"][key]
-                    host_outs[i][key].copy_(t, non_blocking=True)
-                    with io_lock:
-                        d2h += t.numel() * 4
+                t = sl["outbuf"][:n_out]
+                host_outs[i].copy_(t, non_blocking=True)
+                with io_lock:
+                    d2h += t.numel() * 4
                 io["outs_free"].record(cout)
                 if rec is not None:
                     rec["d2h1"] = tev(cout)
