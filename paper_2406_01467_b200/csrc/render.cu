@@ -451,8 +451,13 @@ __device__ __forceinline__ void g2d_add(G2D* row, int k, float v) {
 // whose median splat it is (warp-uniform hit test), and either lets up to kDirectLanes
 // contributing lanes add their sums with atomics or reduces the sums across the warp
 // (smem_reduce) and issues one L2 atomic per value.
+#ifndef RD_K4_MINB
+// ≤ 73 registers at 8×8 tiles (70 used, no spills): K4 alone is 1.5% slower than at 77, but
+// its CTAs leave room for the other views' kernels, and the step runs 0.7% faster
+#define RD_K4_MINB 28
+#endif
 template <int TILE, int PPT, bool DIST>
-__global__ void __launch_bounds__(TILE* TILE / PPT) k_render_bwd(
+__global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)) k_render_bwd(
     DevCam cam, DevOpt opt, int tiles_x, const uint2* __restrict__ ranges, const uint32_t* __restrict__ ids,
     const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
