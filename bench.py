@@ -519,10 +519,10 @@ def run_gpu(args, cfg_name, config):
             json.dump(rows, open(tl_path, "w"), indent=0)
         e2e = {"value": steps_e2e * B * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // steps_e2e,
                "d2h_bytes_per_step": d2h // steps_e2e,
-               "what": "per view: H2D of the view's cotangent image (8 channels, 9 with --distortion) from "
-                       "pinned host memory, the five C-ABI calls, D2H of the rendered maps, on two copy streams "
-                       "overlapped with the compute of other views; Gaussians and gradients stay resident "
-                       "(model state); host wall clock, max over ranks"}
+               "what": "per view: H2D of the view's cotangent image (8 channels, 9 with --distortion, 10 with "
+                       "--normal-consistency) from pinned host memory, the five C-ABI calls, one D2H of the rendered "
+                       "map planes, on the view's own copy streams overlapped with the other views' compute; "
+                       "Gaussians and gradients stay resident (model state); host wall clock, max over ranks"}
 
     # ---------------- roofline of the dominant kernel + per-kernel breakdown
     hbm, hbm_src, sm_max = peaks()
