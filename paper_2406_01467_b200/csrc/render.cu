@@ -259,7 +259,6 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
     const float la_min = __shfl_sync(0xffffffffu, opt.log2_alpha_min, 0);  // a register, not a per-step LDC
     unsigned mine = 0u;  // kMask: bit 0 / 1 = this batch's step lane / lane + 32 was blended
     for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
-      if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) break;
       const int j = kFilter ? (int)wlist[warp][i] : i;
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
@@ -278,6 +277,8 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;
       if (okA) fwd_blend<PROF, DIST>(A, pA, a1, a2, a3, a + 48u * BATCH, base + j, opt);
       if (okB) fwd_blend<PROF, DIST>(B, pB, a1, a2, a3, a + 48u * BATCH, base + j, opt);
+      // a pixel can only saturate in a step that blends: test for the whole warp only then
+      if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) break;
     }
     if (kMask) {  // the batch's words (positions past the last step: zero bits); a word past
       const unsigned lo = __ballot_sync(0xffffffffu, mine & 1u);  // the list's end may be the
@@ -304,10 +305,13 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
 // every lane stores its NV values in column `lane` of row k, lane pair (2k, 2k+1) then reads
 // row k's two halves as four float4 each, and one xor-1 shuffle completes the sum. Lanes 2k
 // and 2k+1 return Σ_lanes v[k]; ≈ NV + 22 instructions against ≈ 5·NV for a shuffle butterfly.
-constexpr int kRedPitch = 36;
 // K4: when at most this many lanes hold contributions for a splat, each adds its own sums with
 // atomics instead of the warp reduction (measured 1 → 5: K4 −2.5%; 8+: L2 contention)
-constexpr int kDirectLanes = 5;  // floats per row: 16-B aligned rows, conflict-free column stores
+#ifndef RD_K4_DIRECT
+#define RD_K4_DIRECT 5
+#endif
+constexpr int kDirectLanes = RD_K4_DIRECT;
+constexpr int kRedPitch = 36;  // floats per row: 16-B aligned rows, conflict-free column stores
 template <int NV>
 __device__ __forceinline__ float smem_reduce(const float (&v)[NV], unsigned red, int lane) {
 #pragma unroll
