@@ -88,6 +88,7 @@ struct rd_view {
   Buf T_final, n_contrib, median_pos;
   Buf g2d;
   Buf bmask;  // K3 → K4 blend mask (tile 8)
+  Buf tile_order;  // K3/K4 launch order (longest lists first)
   // profiling
   bool prof = false;
   cudaStream_t last_stream = nullptr;
@@ -218,7 +219,7 @@ rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
                 &v->didx1,  &v->tmp,    &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->bmask, &v->vis, &v->big, &v->nvis, &v->dist_d0, &v->dist_D1};
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->bmask, &v->tile_order, &v->vis, &v->big, &v->nvis, &v->dist_d0, &v->dist_D1};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
@@ -396,6 +397,7 @@ rd_status rd_render_fwd_ex(rd_view* v, const rd_fwd_maps* maps, rd_stream stream
   RD_ENSURE(v->n_contrib, HW * sizeof(int32_t), s);
   RD_ENSURE(v->median_pos, HW * sizeof(int32_t), s);
   RD_ENSURE(v->bmask, blend_mask_words(v->M, v->tiles_x * v->tiles_y) * sizeof(uint32_t), s);
+  RD_ENSURE(v->tile_order, (size_t)v->tiles_x * v->tiles_y * sizeof(uint32_t), s);
   DistIO dio{nullptr, nullptr, nullptr, nullptr};
   v->dist_fwd = maps->distortion != nullptr;
   if (v->dist_fwd) {
@@ -408,7 +410,7 @@ rd_status rd_render_fwd_ex(rd_view* v, const rd_fwd_maps* maps, rd_stream stream
   launch_render_fwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, maps->color, maps->depth, maps->normal, maps->alpha,
                     (float*)v->T_final.ptr, (int32_t*)v->n_contrib.ptr, (int32_t*)v->median_pos.ptr, dio,
-                    (uint32_t*)v->bmask.ptr, v->ctr(), s);
+                    (uint32_t*)v->bmask.ptr, (uint32_t*)v->tile_order.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("render_fwd");
   v->end(K_FWD, s);
   v->acc_views += 1;
@@ -448,7 +450,7 @@ rd_status rd_blend_bwd_ex(rd_view* v, const rd_bwd_cotangents* cot, rd_stream st
   launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
                     (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, dio,
-                    (const uint32_t*)v->bmask.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
+                    (const uint32_t*)v->bmask.ptr, (const uint32_t*)v->tile_order.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("render_bwd");
   v->end(K_BWD, s);
   v->stage = 4;

@@ -228,16 +228,19 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
 // debug: 64-bit keys (tile << 32 | float_bits(z_c)) of the sorted list
 void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec, int64_t m, uint64_t* out,
                    cudaStream_t s);
+// order: tiles_x·tiles_y u32, the K3/K4 launch order written by launch_render_fwd (read by the
+// backward of the same forward).
 // K3/K4 blend mask (tile 8): ≥ blend_mask_words(M, n_tiles) u32, written by K3, read by K4.
 inline size_t blend_mask_words(int64_t m, int n_tiles) { return (size_t)(m / 32) + (size_t)n_tiles + 8; }
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal,
                        float* alpha, float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
-                       uint32_t* bmask, Counter* counters, cudaStream_t s);
+                       uint32_t* bmask, uint32_t* order, Counter* counters, cudaStream_t s);
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
                        const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio,
-                       const uint32_t* bmask, G2D* g2d, Counter* counters, cudaStream_t s);
+                       const uint32_t* bmask, const uint32_t* order, G2D* g2d, Counter* counters,
+                       cudaStream_t s);
 
 }  // namespace rade

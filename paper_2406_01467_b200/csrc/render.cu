@@ -192,6 +192,31 @@ __device__ __forceinline__ unsigned blend_mask_word(unsigned rx, int pos, int ti
   return (rx >> 5) + (unsigned)tile + ((unsigned)pos >> 5);
 }
 
+// Launch order of the tiles for K3/K4: longest lists first (log2 buckets), so the heavy tiles
+// — clustered where the scene is — do not start last and leave a tail. One block; the order
+// within a bucket is arbitrary (a tile's outputs do not depend on when it runs).
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int n_tiles,
+                                                     uint32_t* __restrict__ order) {
+  __shared__ uint32_t cnt[32], off[32];
+  if (threadIdx.x < 32) cnt[threadIdx.x] = 0u;
+  __syncthreads();
+  auto bucket = [&](int t) {
+    const uint2 r = ranges[t];
+    return 31 - min(31, 32 - __clz((int)(r.y - r.x)));  // longer list → smaller bucket
+  };
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&cnt[bucket(t)], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t a = 0u;
+    for (int b = 0; b < 32; ++b) {
+      off[b] = a;
+      a += cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&off[bucket(t)], 1u)] = (uint32_t)t;
+}
+
 // K3: one CTA per TILE×TILE tile, TILE²/2 threads; warp w owns the 8×8 quadrant w of the
 // tile (lane l: column l % 8, rows l / 8 and l / 8 + 4). Per staged batch each warp first
 // filters the batch down to the splats that reach its quadrant, then blends those.
@@ -207,13 +232,14 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                                                 int32_t* __restrict__ n_contrib,
                                                                 int32_t* __restrict__ median_pos,
                                                                 DistIO dio, uint32_t* __restrict__ bmask,
+                                                                const uint32_t* __restrict__ order,
                                                                 Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / 2;  // threads
   constexpr int NW = NT / 32;          // warps = 8×8 quadrants
   constexpr int BATCH = TILE * TILE;   // splats staged per round
   constexpr bool kFilter = TILE > 8;
   constexpr bool kMask = TILE == 8;    // one warp per tile: it records the blend mask for K4
-  const int tile = blockIdx.x;
+  const int tile = (int)order[blockIdx.x];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
   const int qx = tx * TILE + (warp % (TILE / 8)) * 8, qy = ty * TILE + (warp / (TILE / 8)) * 8;
@@ -466,7 +492,8 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
     const Record* __restrict__ rec, const float* __restrict__ T_final, const int32_t* __restrict__ n_contrib,
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
     const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, DistIO dio,
-    const uint32_t* __restrict__ bmask, G2D* __restrict__ g2d, Counter* __restrict__ counters) {
+    const uint32_t* __restrict__ bmask, const uint32_t* __restrict__ order, G2D* __restrict__ g2d,
+    Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / PPT;
   constexpr int NW = NT / 32;
   constexpr int BATCH = TILE * TILE;
@@ -476,7 +503,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
   constexpr int NV = DIST ? 15 : 12;  // per-splat sums (G2D order; + Σ gd, Σ gd·dx, Σ gd·dy)
   static_assert(NT % 32 == 0 && TILE % SH == 0, "whole warps tiling the tile");
   static_assert(!kMask || NW == 1, "the blend mask is per tile = per warp");
-  const int tile = blockIdx.x;
+  const int tile = (int)order[blockIdx.x];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
   const int qx = tx * TILE + (warp % (TILE / 8)) * 8, qy = ty * TILE + (warp / (TILE / 8)) * SH;
@@ -638,11 +665,12 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal, float* alpha,
                        float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
-                       uint32_t* bmask, Counter* counters, cudaStream_t s) {
+                       uint32_t* bmask, uint32_t* order, Counter* counters, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
+  k_tile_order<<<1, 1024, 0, s>>>(ranges, (int)grid, order);
 #define RD_K3(T, P, D)                                                                                            \
   k_render_fwd<T, P, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal,   \
-                                                   alpha, T_final, n_contrib, median_pos, dio, bmask, counters)
+                                                   alpha, T_final, n_contrib, median_pos, dio, bmask, order, counters)
 #define RD_K3T(T)                                     \
   if (dio.d0) {                                       \
     if (counters) RD_K3(T, true, true); else RD_K3(T, false, true);   \
@@ -662,12 +690,13 @@ void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
                        const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio,
-                       const uint32_t* bmask, G2D* g2d, Counter* counters, cudaStream_t s) {
+                       const uint32_t* bmask, const uint32_t* order, G2D* g2d, Counter* counters,
+                       cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
 #define RD_K4(T, D)                                                                                        \
   k_render_bwd<T, 2, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, \
                                                    median_pos, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,  \
-                                                   dio, bmask, g2d, counters)
+                                                   dio, bmask, order, g2d, counters)
   if (opt.tile == 16) {
     if (dio.dL_ddist) RD_K4(16, true); else RD_K4(16, false);
   } else {
