@@ -200,11 +200,20 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
   __shared__ uint32_t cnt[32], off[32];
   if (threadIdx.x < 32) cnt[threadIdx.x] = 0u;
   __syncthreads();
+  const unsigned lane = threadIdx.x & 31u, below = (1u << lane) - 1u;
   auto bucket = [&](int t) {
     const uint2 r = ranges[t];
     return 31 - min(31, 32 - __clz((int)(r.y - r.x)));  // longer list → smaller bucket
   };
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&cnt[bucket(t)], 1u);
+  // most tiles share a few buckets: one shared atomic per (warp, bucket) group (__match_any)
+  // instead of one per tile, which would serialise thousands of updates of one address
+  const int rounds = (n_tiles + (int)blockDim.x - 1) / (int)blockDim.x;
+  for (int k = 0; k < rounds; ++k) {
+    const int t = k * (int)blockDim.x + (int)threadIdx.x;
+    const int b = t < n_tiles ? bucket(t) : 32;  // 32: no tile
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    if (b < 32 && (peers & below) == 0u) atomicAdd(&cnt[b], (unsigned)__popc(peers));
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t a = 0u;
@@ -214,7 +223,16 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&off[bucket(t)], 1u)] = (uint32_t)t;
+  for (int k = 0; k < rounds; ++k) {
+    const int t = k * (int)blockDim.x + (int)threadIdx.x;
+    const int b = t < n_tiles ? bucket(t) : 32;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0u;
+    if (b < 32 && (int)lane == leader) base = atomicAdd(&off[b], (unsigned)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (b < 32) order[base + (uint32_t)__popc(peers & below)] = (uint32_t)t;
+  }
 }
 
 // K3: one CTA per TILE×TILE tile, TILE²/2 threads; warp w owns the 8×8 quadrant w of the
