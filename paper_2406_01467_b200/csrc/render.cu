@@ -7,7 +7,8 @@
 // Each CTA walks its tile's depth-sorted list (ranges from K2) in batches of TILE² splats
 // staged in shared memory (one coalesced 64-B record gather per splat); every shared-memory
 // broadcast, loop step and — in K4 — every warp reduction then serves two pixels per thread.
-// The block leaves as soon as every pixel is saturated (__syncthreads_count).
+// The block leaves as soon as every pixel is saturated (__syncthreads_count). The CTAs are
+// launched longest tile list first (k_tile_order, computed before K3 and reused by K4).
 //
 // Per (pixel, splat), front to back (Eq.3; readings S1, S8, S9, S10):
 //   α = min(α_max, o·exp(−½ Δᵀ conic Δ)), Δ = (u_c − u, v_c − v)  (skip if α < α_min)
