@@ -87,7 +87,7 @@ typedef struct rd_camera {
 } rd_camera;
 
 /* Host struct. Defaults (rd_options_default): tile 16, alpha_min 1/255, alpha_max 0.99,
- * T_min 1e-4, median_T 0.5, dilation 0.3 px², bg (0,0,0), sh_degree 3. */
+ * T_min 1e-4, median_T 0.5, dilation 0.3 px², bg (0,0,0), sh_degree 3, guard_band 0 (off). */
 typedef struct rd_options {
   int32_t tile;      /* 8 or 16 pixels */
   float alpha_min;   /* splats with α < alpha_min are skipped (S8) */
@@ -97,6 +97,11 @@ typedef struct rd_options {
   float dilation;    /* h added to the 2-D covariance diagonal for α only (S5) */
   float bg[3];       /* C += T_final · bg (S17) */
   int32_t sh_degree; /* active SH degree 0..3 */
+  float guard_band;  /* reading S6b, off when 0 (the default: SURVEY S6 culls on
+                        z ≤ znear only). When g > 0, a Gaussian whose centre projects outside
+                        [−g·W, (1+g)·W] × [−g·H, (1+g)·H] is culled, decided in fp32 as
+                        fx·x_k ∈ [float(−gW − cx)·z_k, float((1+g)W − cx)·z_k] (same for y);
+                        bench.py's C3 workload uses g = 0.15. Must be finite and ≥ 0. */
 } rd_options;
 
 /* Device Gaussian parameters, one row per Gaussian (see layout above). */
@@ -130,6 +135,9 @@ typedef struct rd_stats {
   int32_t width, height;
   int32_t stage;        /* 0 created, 1 preprocessed, 2 binned, 3 rendered, 4 blend-backward done */
   int32_t key_bits;     /* radix-sort bits: 32 + ceil(log2(tiles)) */
+  int64_t n_visible;    /* Gaussians that touch ≥ 1 tile (after rd_bin) */
+  int64_t n_big;        /* of those, the ones whose backward chain rule runs in fp64 (K5b64:
+                           tile rect > 16384 px), after rd_bin */
 } rd_stats;
 
 /* Per-kernel device timings and work counters (host struct filled by rd_get_timings).

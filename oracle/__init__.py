@@ -46,7 +46,7 @@ NPARAM = 59
 
 # default ambiguity bands: F1 α-cutoff, F2 α-clamp (|Δ ln α|),
 # F3 T-stop (relative), F4 median crossing (|T′ − median_T|), F5 grazing |n·x̂_c|
-DEFAULT_EPS = (1e-4, 1e-4, 1e-4, 1e-5, 0.05)
+DEFAULT_EPS = (1e-5, 1e-5, 1e-4, 1e-5, 0.05)
 
 
 def build(force=False):
@@ -75,6 +75,7 @@ def lib():
             L.or_render.argtypes = common + [i64, ctypes.c_void_p, dp, dp, dp, dp, ctypes.c_void_p,
                                              ctypes.c_void_p, ctypes.c_void_p, dp]
             L.or_grad.argtypes = common + [dp, i64, ctypes.c_void_p, dp, dp]
+            L.or_order.argtypes = common + [ctypes.c_void_p, ctypes.c_void_p]
             L.or_sh_basis.argtypes = [dp, dp]
             L.or_sh_basis.restype = None
             L.or_num_threads.restype = ctypes.c_int
@@ -109,11 +110,12 @@ def _cam_vec(cam):
 def _opt_vec(opt, eps=DEFAULT_EPS):
     """Options are taken at their fp32 values: both sides see the same float inputs."""
     f = lambda x: float(np.float32(x))
-    v = np.zeros(14, np.float64)
+    v = np.zeros(15, np.float64)
     v[0:5] = [f(opt.alpha_min), f(opt.alpha_max), f(opt.T_min), f(opt.median_T), f(opt.dilation)]
     v[5:8] = [f(b) for b in opt.bg]
     v[8] = opt.sh_degree
     v[9:14] = eps
+    v[14] = f(getattr(opt, "guard_band", 0.0))  # reading S6b: 0 = off
     return v
 
 
@@ -199,6 +201,17 @@ def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS, timing=None):
     lib().or_grad(*sargs, _dp(cv), _dp(ov), _dp(c), ctypes.c_int64(gids.shape[0]), gids.ctypes.data, _dp(out),
                   None if timing is None else _dp(timing))
     return out
+
+
+def order(scene, cam, opt):
+    """Ids of the surviving Gaussians in the oracle's global front-to-back order (PAPER:422;
+    reading S7: fp32 z_key ascending, ties by id)."""
+    keep, sargs = _scene_args(scene)
+    cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt)
+    out = np.zeros(scene.n, np.int64)
+    cnt = np.zeros(1, np.int64)
+    lib().or_order(*sargs, _dp(cv), _dp(ov), out.ctypes.data, cnt.ctypes.data)
+    return out[:int(cnt[0])]
 
 
 def sh_basis(direction):

@@ -94,6 +94,7 @@ struct Opt {
   double bg[3];
   int sh_degree;
   double eps[5];  // ambiguity-flag bands F1..F5 (see or_render)
+  double guard_band;  // reading S6b: 0 = off; g > 0: cull centres outside the band
 };
 
 // SH basis constants of the 3DGS real-SH convention (reading S14; PAPER:426 only says
@@ -202,15 +203,15 @@ float zkey_of(const Cam& cam, float mx, float my, float mz) {
   return std::fmaf((float)cam.R[6], mx, std::fmaf((float)cam.R[7], my, std::fmaf((float)cam.R[8], mz, (float)cam.t[2])));
 }
 
-// Contract S6b: the centre must project into the 1.3x guard band of the image,
-// u_c ∈ [−0.15 W, 1.15 W] and v_c ∈ [−0.15 H, 1.15 H] (the 3DGS in_frustum NDC test), decided
-// in fp32 as fx·x_k ∈ [g_u0·z_k, g_u1·z_k] (and likewise for y) with x_k, y_k formed like z_k
-// and g_u0 = float(−0.15 W − cx), g_u1 = float(1.15 W − cx), ... rounded once from double.
-bool in_guard_band(const Cam& cam, float mx, float my, float mz, float zk) {
+// Reading S6b (optional, off unless g = opt.guard_band > 0): the centre must
+// project into the guard band of the image, u_c ∈ [−g W, (1+g) W] and v_c ∈ [−g H, (1+g) H],
+// decided in fp32 as fx·x_k ∈ [g_u0·z_k, g_u1·z_k] (and likewise for y) with x_k, y_k formed
+// like z_k and g_u0 = float(−g W − cx), g_u1 = float((1+g) W − cx), ... rounded once from double.
+bool in_guard_band(const Cam& cam, double g, float mx, float my, float mz, float zk) {
   const float xk = std::fmaf((float)cam.R[0], mx, std::fmaf((float)cam.R[1], my, std::fmaf((float)cam.R[2], mz, (float)cam.t[0])));
   const float yk = std::fmaf((float)cam.R[3], mx, std::fmaf((float)cam.R[4], my, std::fmaf((float)cam.R[5], mz, (float)cam.t[1])));
-  const float gu0 = (float)(-0.15 * cam.W - cam.cx), gu1 = (float)(1.15 * cam.W - cam.cx);
-  const float gv0 = (float)(-0.15 * cam.H - cam.cy), gv1 = (float)(1.15 * cam.H - cam.cy);
+  const float gu0 = (float)(-g * cam.W - cam.cx), gu1 = (float)((1.0 + g) * cam.W - cam.cx);
+  const float gv0 = (float)(-g * cam.H - cam.cy), gv1 = (float)((1.0 + g) * cam.H - cam.cy);
   const float fu = (float)cam.fx * xk, fv = (float)cam.fy * yk;
   return fu >= gu0 * zk && fu <= gu1 * zk && fv >= gv0 * zk && fv <= gv1 * zk;
 }
@@ -226,7 +227,8 @@ bool project(const S P[NP], const double raw[11], const Cam& cam, const Opt& opt
   if (!(qn2 > 0.0)) return false;
   g.zkey = zkey_of(cam, (float)raw[0], (float)raw[1], (float)raw[2]);
   if (!(g.zkey > (float)cam.znear)) return false;
-  if (!in_guard_band(cam, (float)raw[0], (float)raw[1], (float)raw[2], g.zkey)) return false;
+  if (opt.guard_band > 0.0 && !in_guard_band(cam, opt.guard_band, (float)raw[0], (float)raw[1], (float)raw[2], g.zkey))
+    return false;
   if (!(raw[10] >= opt.alpha_min)) return false;
   g.o = P[10];
 
@@ -458,6 +460,7 @@ Opt make_opt(const double* o) {
   opt.bg[0] = o[5]; opt.bg[1] = o[6]; opt.bg[2] = o[7];
   opt.sh_degree = (int)o[8];
   for (int k = 0; k < 5; ++k) opt.eps[k] = o[9 + k];
+  opt.guard_band = o[14];
   return opt;
 }
 SceneIn make_scene(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
@@ -472,7 +475,7 @@ extern "C" {
 
 /* Layouts shared with oracle/__init__.py only:
  *   cam[19]  = fx, fy, cx, cy, W, H, R[9] (world->camera, row-major), t[3], znear
- *   opt[14]  = alpha_min, alpha_max, T_min, median_T, dilation, bg[3], sh_degree, eps[5]
+ *   opt[15]  = alpha_min, alpha_max, T_min, median_T, dilation, bg[3], sh_degree, eps[5], guard_band
  *   scene    = double SoA: means[3][n], scales[3][n], rot[4][n] (w,x,y,z), opac[n], sh[K*3][n]
  */
 
@@ -671,6 +674,20 @@ int or_grad(int64_t n, const double* means, const double* scales, const double* 
     timing[1] = wall() - t1;
     timing[2] = (double)ns;
   }
+  return 0;
+}
+
+/* or_order: the global front-to-back order of the surviving Gaussians (reading
+ * S7: z_key ascending, ties by index) — out[0 .. *n_out) are Gaussian ids. */
+int or_order(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
+             const double* sh, int sh_coeffs, const double* camv, const double* optv, int64_t* out, int64_t* n_out) {
+  SceneIn sc = make_scene(n, means, scales, rot, opac, sh, sh_coeffs);
+  Cam cam = make_cam(camv);
+  Opt opt = make_opt(optv);
+  Prepared pr;
+  prepare(sc, cam, opt, pr);
+  for (size_t k = 0; k < pr.splats.size(); ++k) out[k] = pr.splats[k].id;
+  *n_out = (int64_t)pr.splats.size();
   return 0;
 }
 

@@ -30,7 +30,7 @@ class RdCamera(ctypes.Structure):
 class RdOptions(ctypes.Structure):
     _fields_ = [("tile", ctypes.c_int32), ("alpha_min", ctypes.c_float), ("alpha_max", ctypes.c_float),
                 ("T_min", ctypes.c_float), ("median_T", ctypes.c_float), ("dilation", ctypes.c_float),
-                ("bg", ctypes.c_float * 3), ("sh_degree", ctypes.c_int32)]
+                ("bg", ctypes.c_float * 3), ("sh_degree", ctypes.c_int32), ("guard_band", ctypes.c_float)]
 
 
 class RdGaussians(ctypes.Structure):
@@ -63,7 +63,8 @@ class RdBwdCotangents(ctypes.Structure):
 class RdStats(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("n_duplicates", ctypes.c_int64), ("tiles_x", ctypes.c_int32),
                 ("tiles_y", ctypes.c_int32), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
-                ("stage", ctypes.c_int32), ("key_bits", ctypes.c_int32)]
+                ("stage", ctypes.c_int32), ("key_bits", ctypes.c_int32), ("n_visible", ctypes.c_int64),
+                ("n_big", ctypes.c_int64)]
 
 
 RD_NUM_KERNELS = 9

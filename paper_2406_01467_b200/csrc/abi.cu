@@ -198,6 +198,7 @@ rd_status rd_options_default(rd_options* opt) {
   opt->dilation = 0.3f;
   opt->bg[0] = opt->bg[1] = opt->bg[2] = 0.f;
   opt->sh_degree = 3;
+  opt->guard_band = 0.f;  // reading S6b off
   return RD_OK;
 }
 
@@ -253,6 +254,8 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   if (!(opt->dilation >= 0.f) || !std::isfinite(opt->dilation))
     return fail(RD_ERR_INVALID_ARGUMENT, "dilation must be finite and >= 0");
   if (opt->sh_degree < 0 || opt->sh_degree > 3) return fail(RD_ERR_INVALID_ARGUMENT, "sh_degree must be 0..3");
+  if (!(opt->guard_band >= 0.f) || !std::isfinite(opt->guard_band))
+    return fail(RD_ERR_INVALID_ARGUMENT, "guard_band must be finite and >= 0 (0 = off)");
   const int need = (opt->sh_degree + 1) * (opt->sh_degree + 1);
   if (g->sh_coeffs < need || g->sh_coeffs > 16)
     return fail(RD_ERR_INVALID_ARGUMENT, "sh_coeffs=%d incompatible with sh_degree=%d", g->sh_coeffs,
@@ -270,10 +273,12 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   for (int k = 0; k < 9; ++k) c.R[k] = cam->R[k];
   for (int k = 0; k < 3; ++k) c.t[k] = cam->t[k];
   c.znear = cam->znear;
-  c.gu0 = (float)(-0.15 * cam->width - (double)cam->cx);
-  c.gu1 = (float)(1.15 * cam->width - (double)cam->cx);
-  c.gv0 = (float)(-0.15 * cam->height - (double)cam->cy);
-  c.gv1 = (float)(1.15 * cam->height - (double)cam->cy);
+  const double gb = (double)opt->guard_band;  // reading S6b: off at 0
+  c.guard = gb > 0.0 ? 1 : 0;
+  c.gu0 = (float)(-gb * cam->width - (double)cam->cx);
+  c.gu1 = (float)((1.0 + gb) * cam->width - (double)cam->cx);
+  c.gv0 = (float)(-gb * cam->height - (double)cam->cy);
+  c.gv1 = (float)((1.0 + gb) * cam->height - (double)cam->cy);
   for (int i = 0; i < 3; ++i) {
     double acc = 0.0;
     for (int k = 0; k < 3; ++k) acc -= (double)cam->R[3 * k + i] * (double)cam->t[k];
@@ -621,6 +626,8 @@ rd_status rd_view_stats(const rd_view* v, rd_stats* out) {
   out->height = v->cam.H;
   out->stage = v->stage;
   out->key_bits = v->key_bits;
+  out->n_visible = v->n_vis;
+  out->n_big = v->n_big;
   return RD_OK;
 }
 

@@ -114,7 +114,7 @@ struct GF {
   S j00, j02, j11, j12;
   S M[6];   // J₂ RS, rows 0..1
   S A00, A01, A11, det, ca, cb, cc;
-  S xh[3], rh[3], w[3], ah[3], mh[3], muq, ml;
+  S xh[3], rh[3], w[3], ah[3], eps[3], muq, ml;
   S e0, e1, p0, p1, n[3];
 };
 
@@ -181,7 +181,7 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
   const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
   ok &= z > cam.znear;
-  {  // guard band (reading S6b), decided in fp32 with the same op order as the oracle
+  if (cam.guard) {  // guard band (reading S6b, optional), decided in fp32 with the oracle's op order
     const float xk = __fmaf_rn(cam.R[0], f.mu[0], __fmaf_rn(cam.R[1], f.mu[1], __fmaf_rn(cam.R[2], f.mu[2], cam.t[0])));
     const float yk = __fmaf_rn(cam.R[3], f.mu[0], __fmaf_rn(cam.R[4], f.mu[1], __fmaf_rn(cam.R[5], f.mu[2], cam.t[1])));
     const float fu = __fmul_rn(cam.fx, xk), fv = __fmul_rn(cam.fy, yk);
@@ -270,7 +270,12 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   return true;
 }
 
-// Depth plane and normal (m-form of Eq.12-15, 21-22). Returns false if degenerate.
+// Depth plane and normal (m-form of Eq.12-15, 21-22), evaluated in the Gaussian's local
+// frame (columns of R_c): r = R_cᵀx̂ (a unit vector), w_k = 1/s_k², a = r∘w, μ = r·a, so
+// m = R_c a, ‖m‖ = ‖a‖, n = −R_c a/‖a‖ and e = m/μ − x̂ = R_c ε with
+//   ε_k = a_k/μ − r_k = r_k (w_k − μ)/μ,  w_k − μ = Σ_{j≠k} r_j² (w_k − w_j)   (Σ r_j² = 1),
+// which has no cancellation even for a flat splat seen face-on (r ≈ its thin axis, where
+// a_k/μ − r_k subtracts nearly equal numbers). Returns false if degenerate.
 template <typename S>
 __device__ __forceinline__ bool gaussian_plane(const DevCam& cam, GF<S>& f) {
 #pragma unroll
@@ -281,20 +286,22 @@ __device__ __forceinline__ bool gaussian_plane(const DevCam& cam, GF<S>& f) {
     f.w[k] = S(1) / ((S)f.s[k] * f.s[k]);
     f.ah[k] = f.rh[k] * f.w[k];
   }
-#pragma unroll
-  for (int r = 0; r < 3; ++r) f.mh[r] = f.Rc[3 * r] * f.ah[0] + f.Rc[3 * r + 1] * f.ah[1] + f.Rc[3 * r + 2] * f.ah[2];
   f.muq = f.rh[0] * f.ah[0] + f.rh[1] * f.ah[1] + f.rh[2] * f.ah[2];
-  f.ml = sq_root(f.mh[0] * f.mh[0] + f.mh[1] * f.mh[1] + f.mh[2] * f.mh[2]);
+  f.ml = sq_root(f.ah[0] * f.ah[0] + f.ah[1] * f.ah[1] + f.ah[2] * f.ah[2]);
   if (!(f.muq > S(0)) || !isfin(f.muq) || !(f.ml > S(0)) || !isfin(f.ml)) return false;
   const S imu = S(1) / f.muq;
-  f.e0 = f.mh[0] * imu - f.xh[0];
-  f.e1 = f.mh[1] * imu - f.xh[1];
+  const S r2[3] = {f.rh[0] * f.rh[0], f.rh[1] * f.rh[1], f.rh[2] * f.rh[2]};
+  f.eps[0] = f.rh[0] * (r2[1] * (f.w[0] - f.w[1]) + r2[2] * (f.w[0] - f.w[2])) * imu;
+  f.eps[1] = f.rh[1] * (r2[0] * (f.w[1] - f.w[0]) + r2[2] * (f.w[1] - f.w[2])) * imu;
+  f.eps[2] = f.rh[2] * (r2[0] * (f.w[2] - f.w[0]) + r2[1] * (f.w[2] - f.w[1])) * imu;
+  f.e0 = f.Rc[0] * f.eps[0] + f.Rc[1] * f.eps[1] + f.Rc[2] * f.eps[2];
+  f.e1 = f.Rc[3] * f.eps[0] + f.Rc[4] * f.eps[1] + f.Rc[5] * f.eps[2];
   const S zzit = f.x[2] * f.x[2] * f.it;
   f.p0 = zzit / (S)cam.fx * f.e0;
   f.p1 = zzit / (S)cam.fy * f.e1;
   const S iml = S(1) / f.ml;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) f.n[k] = -f.mh[k] * iml;
+  for (int r = 0; r < 3; ++r) f.n[r] = -(f.Rc[3 * r] * f.ah[0] + f.Rc[3 * r + 1] * f.ah[1] + f.Rc[3 * r + 2] * f.ah[2]) * iml;
   return true;
 }
 
@@ -584,48 +591,56 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
              S(2) * dj12 * cam.fy * f.x[1] * iz2 * iz;
   }
 
-  // ---- depth plane p and normal n (m-form backward)
+  // ---- depth plane p and normal n: the m-form backward in the local frame (gaussian_plane),
+  // with every difference of nearly equal terms written as a sum of the remaining ones, so a
+  // flat splat's thin-axis gradients keep their relative accuracy in fp32
   {
     const S imu = S(1) / f.muq;
     const S iml = S(1) / f.ml;
-    S dmh[3];
-    // n = −m̂/‖m̂‖
-    const S nd = f.n[0] * d_n[0] + f.n[1] * d_n[1] + f.n[2] * d_n[2];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) dmh[k] = -(d_n[k] - f.n[k] * nd) * iml;
-    // p_k = c_k e_k, c_k = z² it / f_k, e_k = m̂_k/μ − x̂_k
+    // p_k = c_k e_k, c_k = z² it / f_k, e = R_c ε ; n = −R_c â, â = a/‖a‖
     const S z = f.x[2];
     const S zzit = z * z * f.it;
     const S de0 = d_p0 * zzit / cam.fx, de1 = d_p1 * zzit / cam.fy;
     dx[2] += S(2) * (d_p0 * f.p0 + d_p1 * f.p1) / z;
     S dit = (d_p0 * f.p0 + d_p1 * f.p1) / f.it;
-    dmh[0] += de0 * imu;
-    dmh[1] += de1 * imu;
-    const S dmuq = -(de0 * f.mh[0] + de1 * f.mh[1]) * imu * imu;
-    S dxh[3] = {-de0, -de1, 0};
-    S dah[3], drh[3];
-    // μ = r̂·â ; m̂ = R_c â
+    S ah_n[3], deps[3], dahat[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      dah[k] = dmuq * f.rh[k] + f.Rc[k] * dmh[0] + f.Rc[3 + k] * dmh[1] + f.Rc[6 + k] * dmh[2];
-      drh[k] = dmuq * f.ah[k];
+      ah_n[k] = f.ah[k] * iml;
+      deps[k] = f.Rc[k] * de0 + f.Rc[3 + k] * de1;
+      dahat[k] = -(f.Rc[k] * d_n[0] + f.Rc[3 + k] * d_n[1] + f.Rc[6 + k] * d_n[2]);
     }
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) dRc[3 * r + k] += dmh[r] * f.ah[k];
-    // â = r̂ ⊘ s²
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      drh[k] += dah[k] * f.w[k];
-      ds[k] += -S(2) * dah[k] * f.ah[k] / f.s[k];
+      dRc[k] += de0 * f.eps[k] - d_n[0] * ah_n[k];
+      dRc[3 + k] += de1 * f.eps[k] - d_n[1] * ah_n[k];
+      dRc[6 + k] += -d_n[2] * ah_n[k];
     }
-    // r̂ = R_cᵀ x̂
+    const S A = deps[0] * f.ah[0] + deps[1] * f.ah[1] + deps[2] * f.ah[2];
+    S dr[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int j1 = k == 0 ? 1 : 0, j2 = k == 2 ? 1 : 2;  // the other two axes
+      // â = a/‖a‖: da_k = (dâ_k Σ_{j≠k} â_j² − â_k Σ_{j≠k} â_j dâ_j)/‖a‖
+      const S da = (dahat[k] * (ah_n[j1] * ah_n[j1] + ah_n[j2] * ah_n[j2]) -
+                    ah_n[k] * (ah_n[j1] * dahat[j1] + ah_n[j2] * dahat[j2])) * iml;
+      // ε_k = a_k/μ − r_k, μ = Σ r_j a_j: ∂/∂w_k = (r_k/μ²)(dε_k S_k − r_k T_k) with
+      // S_k = Σ_{j≠k} r_j a_j = μ − r_k a_k and T_k = Σ_{j≠k} dε_j a_j
+      const S Sk = f.rh[j1] * f.ah[j1] + f.rh[j2] * f.ah[j2];
+      const S Tk = deps[j1] * f.ah[j1] + deps[j2] * f.ah[j2];
+      const S dw = da * f.rh[k] + f.rh[k] * (deps[k] * Sk - f.rh[k] * Tk) * imu * imu;
+      // ∂ε_j/∂r_k = δ_jk (w_k − μ)/μ − 2 r_j w_j a_k/μ², w_k − μ = Σ_{j≠k} r_j² (w_k − w_j)
+      const S wk_mu = f.rh[j1] * f.rh[j1] * (f.w[k] - f.w[j1]) + f.rh[j2] * f.rh[j2] * (f.w[k] - f.w[j2]);
+      dr[k] = da * f.w[k] + deps[k] * wk_mu * imu - S(2) * f.ah[k] * A * imu * imu;
+      ds[k] += -S(2) * dw * f.w[k] / f.s[k];  // w_k = s_k⁻²
+    }
+    // r = R_cᵀ x̂
+    S dxh[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      dxh[r] += f.Rc[3 * r] * drh[0] + f.Rc[3 * r + 1] * drh[1] + f.Rc[3 * r + 2] * drh[2];
+      dxh[r] = f.Rc[3 * r] * dr[0] + f.Rc[3 * r + 1] * dr[1] + f.Rc[3 * r + 2] * dr[2];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) dRc[3 * r + k] += f.xh[r] * drh[k];
+      for (int k = 0; k < 3; ++k) dRc[3 * r + k] += f.xh[r] * dr[k];
     }
     // x̂ = x·it, it = t2^{-1/2}
 #pragma unroll

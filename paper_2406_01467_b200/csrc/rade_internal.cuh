@@ -20,7 +20,9 @@ struct DevCam {
   float t[3];
   float znear;
   float campos[3];  // -R^T t (camera centre in world space), for SH view directions
-  // guard band (reading S6b): float(−0.15 W − cx), float(1.15 W − cx), same for v
+  // guard band (reading S6b, rd_options.guard_band = g > 0): float(−g W − cx), float((1+g) W − cx),
+  // same for v; guard = 0: off
+  int guard;
   float gu0, gu1, gv0, gv1;
 };
 

@@ -23,7 +23,7 @@ def default_options():
     o = N.RdOptions()
     N.check(lib.rd_options_default(ctypes.byref(o)), "rd_options_default")
     return dict(tile=o.tile, alpha_min=o.alpha_min, alpha_max=o.alpha_max, T_min=o.T_min, median_T=o.median_T,
-                dilation=o.dilation, bg=tuple(o.bg), sh_degree=o.sh_degree)
+                dilation=o.dilation, bg=tuple(o.bg), sh_degree=o.sh_degree, guard_band=o.guard_band)
 
 
 def _stream_ptr(stream):
@@ -124,6 +124,7 @@ def options_struct(opt=None):
     for k in range(3):
         o.bg[k] = float(bg[k])
     o.sh_degree = int(get("sh_degree", o.sh_degree))
+    o.guard_band = float(get("guard_band", o.guard_band))
     return o
 
 

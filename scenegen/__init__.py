@@ -56,6 +56,7 @@ class Options:
     dilation: float = 0.3
     bg: tuple = (0.0, 0.0, 0.0)
     sh_degree: int = 3
+    guard_band: float = 0.0  # reading S6b: 0 = off (cull z <= znear only)
 
 
 @dataclass
@@ -392,10 +393,13 @@ def config_scene_and_cameras(config: str, n_views=None, n_gaussians=None):
         return sc, cameras_c1(n_views or 100), Options(bg=(1.0, 1.0, 1.0))
     if config == "C2":
         return scene_c2(n=n_gaussians or 400_000), cameras_c2(n_views or 49), Options()
+    # C3/C4 (outdoor orbit over a ground disc): the guard band of reading S6b
+    # removes the ground splats beside and below the camera, whose centres project far off
+    # screen and whose affine footprints would otherwise cover the whole image
     if config == "C3":
-        return scene_c3(n=n_gaussians or 1_500_000), cameras_c3(n_views or 200), Options()
+        return scene_c3(n=n_gaussians or 1_500_000), cameras_c3(n_views or 200), Options(guard_band=0.15)
     if config == "C4":
-        return scene_c4(n=n_gaussians or 3_000_000), cameras_c3(n_views or 200), Options()
+        return scene_c4(n=n_gaussians or 3_000_000), cameras_c3(n_views or 200), Options(guard_band=0.15)
     raise ValueError(config)
 
 

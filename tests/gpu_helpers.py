@@ -8,7 +8,8 @@ import paper_2406_01467_b200 as P
 
 def opts_dict(opt):
     return dict(tile=opt.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
-                median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
+                median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree,
+                guard_band=opt.guard_band)
 
 
 def gpu_forward(scene, cam, opt, view=None):

@@ -52,8 +52,9 @@ def test_struct_layouts_match_header(native):
 int main(void) {
   printf("%zu %zu %zu %zu %zu\n", sizeof(rd_camera), sizeof(rd_options), sizeof(rd_gaussians), sizeof(rd_grads),
          sizeof(rd_stats));
-  printf("%zu %zu %zu %zu\n", offsetof(rd_camera, znear), offsetof(rd_options, sh_degree), offsetof(rd_gaussians, sh),
-         offsetof(rd_stats, key_bits));
+  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(rd_camera, znear), offsetof(rd_options, sh_degree),
+         offsetof(rd_gaussians, sh), offsetof(rd_stats, key_bits), offsetof(rd_options, guard_band),
+         offsetof(rd_stats, n_big));
   return 0;
 }
 """
@@ -69,7 +70,7 @@ int main(void) {
     assert sizes == [ctypes.sizeof(native.RdCamera), ctypes.sizeof(native.RdOptions),
                      ctypes.sizeof(native.RdGaussians), ctypes.sizeof(native.RdGrads), ctypes.sizeof(native.RdStats)]
     assert offs == [native.RdCamera.znear.offset, native.RdOptions.sh_degree.offset, native.RdGaussians.sh.offset,
-                    native.RdStats.key_bits.offset]
+                    native.RdStats.key_bits.offset, native.RdOptions.guard_band.offset, native.RdStats.n_big.offset]
 
 
 def test_options_default_and_version(native):
@@ -78,6 +79,7 @@ def test_options_default_and_version(native):
     assert lib.rd_options_default(ctypes.byref(o)) == 0
     assert o.tile == 16 and abs(o.alpha_min - 1 / 255) < 1e-9 and abs(o.alpha_max - 0.99) < 1e-7
     assert abs(o.T_min - 1e-4) < 1e-10 and o.median_T == 0.5 and abs(o.dilation - 0.3) < 1e-7 and o.sh_degree == 3
+    assert o.guard_band == 0.0  # reading S6b off by default
     assert b"sm_100a" in lib.rd_version()
     assert lib.rd_options_default(None) == native.RD_ERR_INVALID_ARGUMENT
 
@@ -108,7 +110,8 @@ def test_argument_validation_without_gpu(native):
     assert lib.rd_preprocess(h, ctypes.byref(g), ctypes.byref(cam), ctypes.byref(opt), None) == 1
     fake = ctypes.c_void_p(16)
     g = native.RdGaussians(5, 16, fake, fake, fake, fake, fake)
-    for field, val in (("tile", 32), ("alpha_min", 0.0), ("alpha_max", 1.5), ("sh_degree", 4), ("T_min", -1.0)):
+    for field, val in (("tile", 32), ("alpha_min", 0.0), ("alpha_max", 1.5), ("sh_degree", 4), ("T_min", -1.0),
+                       ("guard_band", -0.1), ("guard_band", float("inf"))):
         o2 = native.RdOptions()
         lib.rd_options_default(ctypes.byref(o2))
         setattr(o2, field, val)

@@ -45,7 +45,7 @@ def test_c3_forward_sampled_pixels(c3):
     gpu = c3["gpu"]
     fl = ref["flags"]
     ok = (fl & (F1 | F3)) == 0
-    assert ok.mean() > 0.8, ok.mean()
+    assert (~ok).sum() <= max(1, 0.01 * len(pix)), (~ok).sum()  # flagged ≤ 1%
     assert (ref["alpha"] > 0.5).mean() > 0.3  # the sample hits the scene
     for k in ("color", "normal"):
         err = np.abs(gpu[k][:, ys, xs] - ref[k])[:, ok]
@@ -76,6 +76,18 @@ def _binning_reference(rect, touched, zkey, tiles_x):
     keys = ((ty * tiles_x + tx).astype(np.uint64) << np.uint64(32)) | zb[ids[rep]]
     order = np.argsort(keys, kind="stable")
     return keys[order], ids[rep][order].astype(np.uint32)
+
+
+def test_c3_zkey_bits_match_oracle(c3):
+    """The sort key (reading S7) of every visible Gaussian at C3, bit for bit against the
+    oracle's fp32 z_key; and every Gaussian the GPU keeps is one the oracle keeps."""
+    rec, rect, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(c3["view"]))
+    pg = oracle.project(c3["scene"], c3["cam"], c3["opt"])
+    vis = touched > 0
+    assert vis.sum() > 500_000 and np.all(pg[vis, 0] == 1)
+    zg = np.ascontiguousarray(rec[vis][:, 12]).view(np.uint32)
+    zo = pg[vis, oracle.PG["zkey"]].astype(np.float32).view(np.uint32)
+    np.testing.assert_array_equal(zg, zo)
 
 
 def test_c3_binning_bit_exact(c3):
@@ -200,19 +212,27 @@ def test_c3_sampled_gradients(c3):
     torch.cuda.synchronize()
     G = grads_to_rows(grads, g.n)
     _, _, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(view))
-    # contributing Gaussians (largest opacity gradient) with a small footprint (the
-    # oracle's cost is per covered pixel)
-    small = np.nonzero((touched > 0) & (touched <= 4))[0]
-    cand = small[np.argsort(-np.abs(G[small, 10]))[:200]]
-    gids = rng.choice(cand, 6, replace=False)
-    R = oracle.grad(scene, cam, opt, {k: v.astype(np.float64) for k, v in cot.items()}, gids)
-    A = G[gids]
-    for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
-                     "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
-        nb = np.linalg.norm(R[:, sl])
-        assert nb > 0, name
-        rel = np.linalg.norm(A[:, sl] - R[:, sl]) / nb
-        assert rel <= 1e-3, (name, rel)
+    # contributing Gaussians (largest opacity gradient) of three footprint classes (the
+    # oracle's cost is per covered pixel): small (≤ 4 tiles), medium (16–64 tiles) and big
+    # (tile rect > 16 384 px: the fp64 chain rule K5b64)
+    t64 = touched.astype(np.int64)
+    groups = {"small": ((t64 > 0) & (t64 <= 4), 6), "medium": ((t64 >= 16) & (t64 <= 64), 4),
+              "big": (t64 * opt.tile ** 2 > 16384, 2)}
+    assert P.rd_view_stats(view)["n_big"] == int(groups["big"][0].sum()) > 0
+    for gname, (sel, k) in groups.items():
+        ids = np.nonzero(sel)[0]
+        if gname == "big":  # the smallest big ones (the oracle walks every covered pixel)
+            ids = ids[np.argsort(t64[ids])[:40]]
+        cand = ids[np.argsort(-np.abs(G[ids, 10]))[:200]]
+        gids = rng.choice(cand, k, replace=False)
+        R = oracle.grad(scene, cam, opt, {k_: v.astype(np.float64) for k_, v in cot.items()}, gids)
+        A = G[gids]
+        for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
+                         "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
+            nb = np.linalg.norm(R[:, sl])
+            assert nb > 0, (gname, name)
+            rel = np.linalg.norm(A[:, sl] - R[:, sl]) / nb
+            assert rel <= 1e-3, (gname, name, rel)
 
 
 def test_c3_distortion_sampled_pixels(c3):
@@ -229,7 +249,7 @@ def test_c3_distortion_sampled_pixels(c3):
     ref = oracle.render(c3["scene"], cam, c3["opt"], pixels=pix)
     ys, xs = pix // cam.width, pix % cam.width
     ok = (ref["flags"] & (F1 | F3)) == 0
-    assert ok.mean() > 0.8 and ref["distortion"].max() > 1e-3
+    assert (~ok).sum() <= max(1, 0.01 * len(pix)) and ref["distortion"].max() > 1e-3
     err = np.abs(L[ys, xs] - ref["distortion"])[ok]
     assert err.max() <= TOL * max(1.0, np.abs(ref["distortion"][ok]).max()), err.max()
 
@@ -251,9 +271,33 @@ def test_other_configs_forward_sampled_pixels(cfg):
     ref = oracle.render(scene, cam, opt, pixels=pix)
     ys, xs = pix // cam.width, pix % cam.width
     ok = (ref["flags"] & (F1 | F3)) == 0
-    assert ok.mean() > 0.8
+    assert (~ok).sum() <= max(1, 0.01 * len(pix))
     for k in ("color", "normal"):
         assert np.abs(gpu[k][:, ys, xs] - ref[k])[:, ok].max() <= TOL, (cfg, k)
     assert np.abs(gpu["alpha"][ys, xs] - ref["alpha"])[ok].max() <= TOL
     okd = (ref["flags"] & (F1 | F3 | F4 | F5)) == 0
     assert np.abs(gpu["depth"][ys, xs] - ref["depth"])[okd].max() <= TOL
+
+
+def test_c3_guard_band_off_sampled_pixels(c3):
+    """C3 with the guard band of reading S6b off (the ABI default): 48 random
+    pixels vs the oracle with the same option; the near-camera ground splats then reach
+    into the image (the band changes the image: checked, not assumed)."""
+    cam = c3["cam"]
+    opt = sg.Options(tile=BENCH_TILE, guard_band=0.0)
+    out, view = P.render(c3["g"], cam, opts_dict(opt))
+    torch.cuda.synchronize()
+    gpu = {k: v.double().cpu().numpy() for k, v in out.items()}
+    assert P.rd_view_stats(view)["n_visible"] > P.rd_view_stats(c3["view"])["n_visible"]
+    rng = np.random.default_rng(14)
+    pix = rng.choice(cam.width * cam.height, 48, replace=False)
+    ref = oracle.render(c3["scene"], cam, opt, pixels=pix)
+    ys, xs = pix // cam.width, pix % cam.width
+    ok = (ref["flags"] & (F1 | F3)) == 0
+    assert (~ok).sum() <= max(1, 0.01 * len(pix))
+    for k in ("color", "normal"):
+        assert np.abs(gpu[k][:, ys, xs] - ref[k])[:, ok].max() <= TOL, k
+    assert np.abs(gpu["alpha"][ys, xs] - ref["alpha"])[ok].max() <= TOL
+    okd = (ref["flags"] & (F1 | F3 | F4 | F5)) == 0
+    assert np.abs(gpu["depth"][ys, xs] - ref["depth"])[okd].max() <= TOL
+    assert np.abs(gpu["color"] - c3["gpu"]["color"]).max() > 1e-2

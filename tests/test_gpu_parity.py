@@ -30,7 +30,36 @@ def _scenes():
              ("deg0", dense_scene(4, 200), sg.camera_identity(64, 64, 64), sg.Options(sh_degree=0))]
     sc = dense_scene(5, 500, zr=(1.5, 4.0))
     cases.append(("lookat", sc, _lookat_cam(rng, 96, 72), sg.Options()))
+    # ties (reading S7): with the identity camera z_key = z exactly, and z takes 3 values, so
+    # most pairs of overlapping splats tie on depth and are ordered by id
+    tie = dense_scene(6, 300)
+    z_new = np.random.default_rng(6).choice([2.5, 3.0, 4.0], tie.n).astype(np.float32)
+    tie.means[:2] *= z_new / tie.means[2]
+    tie.means[2] = z_new
+    cases.append(("ties_t8", tie, sg.camera_identity(64, 64, 64), sg.Options(tile=8)))
+    # centres off screen beside the camera (reading S6b): band off (default) and on
+    off = _offscreen_scene(7)
+    cases.append(("offscreen", off, sg.camera_identity(64, 64, 64), sg.Options()))
+    cases.append(("offscreen_gb", off, sg.camera_identity(64, 64, 64), sg.Options(guard_band=0.15)))
     return cases
+
+
+def _offscreen_scene(seed, n_side=16):
+    """dense_scene plus wide splats whose centres project 0.2–0.6 image widths outside the
+    image at small depth (z ∈ [0.5, 1.2]): with the guard band off their affine footprints
+    reach into the image, with it on (g = 0.15) they are culled."""
+    rng = np.random.default_rng(seed)
+    base = dense_scene(seed, 200)
+    z = rng.uniform(0.5, 1.2, n_side)
+    u = np.where(rng.random(n_side) < 0.5, rng.uniform(-0.6, -0.2, n_side), rng.uniform(1.2, 1.6, n_side)) * 64
+    v = rng.uniform(0.1, 0.9, n_side) * 64
+    swap = rng.random(n_side) < 0.3
+    u[swap], v[swap] = v[swap], u[swap]
+    x, y = (u - 32) * z / 64, (v - 32) * z / 64
+    s = np.exp(rng.uniform(np.log(0.05), np.log(0.2), (3, n_side)))
+    side = sg.make_scene(np.stack([x, y, z]), s, sg.random_quaternions(rng, n_side),
+                         rng.uniform(0.05, 0.5, n_side), sg.sh_coeffs(rng, n_side))
+    return concat(base, side)
 
 
 def _lookat_cam(rng, W, H):
@@ -53,7 +82,7 @@ def test_forward_parity(case):
     ref, gpu = case["ref"], case["gpu"]
     fl = ref["flags"]
     ok = (fl & (F1 | F3)) == 0
-    assert ok.mean() > 0.95, ok.mean()
+    assert ok.mean() >= 0.99, ok.mean()  # flagged pixels ≤ 1%
     for k in ("color", "normal"):
         err = np.abs(gpu[k] - ref[k])[:, ok]
         assert err.max() <= TOL, (k, err.max())
@@ -104,6 +133,10 @@ def test_preprocess_parity(case):
     np.testing.assert_allclose(r[:, 1] + lo[:, 1], o[:, oracle.PG["v"]], rtol=0, atol=2e-6)
     np.testing.assert_allclose(r[:, 6:9], o[:, oracle.PG["rgb"]], atol=1e-5)
     np.testing.assert_allclose(r[:, 12], o[:, oracle.PG["z"]], rtol=1e-6)
+    # the sort key (reading S7) bit for bit: the GPU's fp32 z_key = the oracle's fp32 z_key
+    zg = np.ascontiguousarray(rec[vis][:, 12]).view(np.uint32)
+    zo = o[:, oracle.PG["zkey"]].astype(np.float32).view(np.uint32)
+    np.testing.assert_array_equal(zg, zo)
     ng = np.abs(o[:, oracle.PG["ndotx"]]) >= 0.05
     np.testing.assert_allclose(r[ng, 9:12], o[ng, 67:70], atol=2e-6)
     np.testing.assert_allclose(r[ng, 13:15], o[ng][:, oracle.PG["p"]], rtol=1e-3, atol=1e-7)
@@ -126,6 +159,37 @@ def test_binning_bit_exact(case):
         if len(w):
             exp[t] = (w[0], w[-1] + 1)
     np.testing.assert_array_equal(ranges.astype(np.int64), exp)
+
+
+def test_binning_order_matches_oracle(case):
+    """Per tile, the GPU's id list is the ORACLE's global front-to-back order (PAPER:422;
+    reading S7: z_key, ties by id — oracle.order) restricted to the Gaussians whose rect
+    covers the tile; the 64-bit keys carry the oracle's z_key bits; ranges follow."""
+    view, scene, cam, opt = case["view"], case["scene"], case["cam"], case["opt"]
+    rec, rect, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(view))
+    keys, ids, ranges = (t.cpu().numpy() for t in P.rd_debug_binning(view))
+    st = P.rd_view_stats(view)
+    tx_n = st["tiles_x"]
+    order = oracle.order(scene, cam, opt)
+    zk = oracle.project(scene, cam, opt)[:, oracle.PG["zkey"]].astype(np.float32).view(np.uint32)
+    per_tile = [[] for _ in range(tx_n * st["tiles_y"])]
+    for i in order:
+        if touched[i] == 0:
+            continue
+        r0, r1 = int(rect[i, 0]) & 0xFFFFFFFF, int(rect[i, 1]) & 0xFFFFFFFF
+        for ty in range(r0 >> 16, r1 >> 16):
+            for tx in range(r0 & 0xFFFF, r1 & 0xFFFF):
+                per_tile[ty * tx_n + tx].append(i)
+    exp_ids = np.array([i for lst in per_tile for i in lst], np.uint32)
+    exp_keys = np.array([(t << 32) | int(zk[i]) for t, lst in enumerate(per_tile) for i in lst], np.uint64)
+    np.testing.assert_array_equal(ids.view(np.uint32), exp_ids)
+    np.testing.assert_array_equal(keys.view(np.uint64), exp_keys)
+    starts = np.cumsum([0] + [len(l) for l in per_tile])
+    exp_r = np.array([(starts[t], starts[t + 1]) if per_tile[t] else (0, 0) for t in range(len(per_tile))])
+    np.testing.assert_array_equal(ranges.astype(np.int64), exp_r)
+    if case["name"].startswith("ties"):  # the case must actually exercise the tie-break
+        zz = np.float32(zk.view(np.float32))
+        assert any(len(l) > 1 and len(set(zz[l])) < len(l) for l in per_tile)
 
 
 def test_rect_is_conservative(case):
@@ -175,11 +239,73 @@ def test_backward_parity(case):
         rel = np.linalg.norm(a - b) / nb
         assert rel <= 1e-3, (name, rel)
         med = np.median(np.abs(b[b != 0])) if (b != 0).any() else 0.0
-        bad = np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med
-        assert bad.mean() <= 0.002, (name, bad.mean(), np.abs(a - b).max())
+        bad = np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med  # every entry
+        assert not bad.any(), (name, int(bad.sum()), np.abs(a - b).max())
     # Gaussians the GPU did not draw get exactly zero gradient
     off = np.setdiff1d(np.arange(scene.n), vis)
     assert np.all(G[off] == 0)
+
+
+def _big_splat_scene(seed=12, W=256):
+    """A 256×256 view: 160 small Gaussians (dense_scene) plus 10 screen-sized splats whose
+    tile rects exceed 16 384 px (so K1 puts them on the big list and their chain rule runs in
+    fp64, K5b64): z ∈ [1.2, 3], scales 0.15–0.5 (σ ≈ 20–100 px), half of them flat (s_min =
+    1e-3·s), three of those tilted to 70–80° from the view ray (near-grazing); opacities low
+    enough that the splats behind them still receive gradient."""
+    rng = np.random.default_rng(seed)
+    base = dense_scene(seed, 160, width=W, height=W, f=float(W))
+    nb = 10
+    z = rng.uniform(1.2, 3.0, nb)
+    uv = rng.uniform(0.25, 0.75, (2, nb)) * W
+    x, y = (uv[0] - W / 2) * z / W, (uv[1] - W / 2) * z / W
+    s = np.exp(rng.uniform(np.log(0.15), np.log(0.5), (3, nb)))
+    flat = np.arange(nb) < 5
+    s[2, flat] = s[0, flat] * 1e-3
+    nrm = np.stack([np.zeros(nb), np.zeros(nb), -np.ones(nb)], 0)
+    ang = np.deg2rad(rng.uniform(70, 80, nb))
+    tilt = np.arange(nb) < 3  # flat and near-grazing: normal 70–80° away from the view axis
+    nrm[:, tilt] = np.stack([np.sin(ang[tilt]), np.zeros(3), -np.cos(ang[tilt])], 0)
+    q = sg.quaternion_with_axis3(nrm, rng)
+    q[:, ~flat] = sg.random_quaternions(rng, (~flat).sum())
+    big = sg.make_scene(np.stack([x, y, z]), s, q, rng.uniform(0.15, 0.45, nb), sg.sh_coeffs(rng, nb))
+    return concat(base, big), sg.camera_identity(W, W, float(W))
+
+
+@pytest.mark.parametrize("tile", [8, 16])
+def test_big_splats_fp64_backward_parity(tile):
+    """K5b64 (the fp64 chain rule of the screen-sized splats, rade_internal.cuh is_big)
+    against the oracle's exact dual-number gradients: every parameter class, ≤ 1e-3 relative
+    in norm and elementwise (|Δg| ≤ 1e-3|g| + 1e-3·median|g|) on every entry, for the big
+    splats alone and for all visible Gaussians; flagged pixels (≤ 1%) get zero cotangent."""
+    scene, cam = _big_splat_scene()
+    opt = sg.Options(tile=tile)
+    ref = oracle.render(scene, cam, opt)
+    mask = ref["flags"] == 0
+    assert mask.mean() >= 0.99, mask.mean()
+    cot = sg.cotangents(13, cam.width, cam.height)
+    cot = {k: (v * mask).astype(np.float32) for k, v in cot.items()}
+    out, G, view = gpu_grads(scene, cam, opt, cot)
+    st = P.rd_view_stats(view)
+    _, _, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(view))
+    big = np.nonzero(touched.astype(np.int64) * tile * tile > 16384)[0]
+    assert st["n_big"] == len(big) >= 8, (st["n_big"], len(big))
+    assert (big >= 160).sum() >= 8  # most of the added screen-sized splats
+    ok = (ref["flags"] & (F1 | F3)) == 0
+    for k in ("color", "normal"):
+        assert np.abs(out[k] - ref[k])[:, ok].max() <= TOL, k
+    vis = np.nonzero(touched > 0)[0]
+    R = oracle.grad(scene, cam, opt, cot, vis)
+    Gv = G[vis]
+    for rows, label in ((np.isin(vis, big), "big"), (np.ones(len(vis), bool), "all")):
+        for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
+                         "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
+            a, b = Gv[rows, sl], R[rows, sl]
+            nb = np.linalg.norm(b)
+            assert nb > 0, (label, name)
+            assert np.linalg.norm(a - b) / nb <= 1e-3, (label, name, np.linalg.norm(a - b) / nb)
+            med = np.median(np.abs(b[b != 0]))
+            bad = np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med
+            assert not bad.any(), (label, name, int(bad.sum()))
 
 
 def test_tile_size_independence():

@@ -489,11 +489,13 @@ def test_zero_cotangent_gives_zero_gradient(O):
 
 @pytest.mark.parametrize("axis", [0, 1])
 def test_guard_band_cull(O, axis):
-    """Reading S6b: a centre projecting outside [−0.15, 1.15]× the image is culled (3DGS
-    in_frustum NDC test). Pinned by placing a wide splat just inside / just outside each
-    edge (closed-form pixel position u = fx·x/z + cx) and checking that it is kept and
-    reaches into the image, or culled and contributes nothing."""
+    """Reading S6b (optional, rd_options.guard_band = 0.15): a centre projecting outside
+    [−0.15, 1.15]× the image is culled. Pinned by placing a wide splat just inside / just
+    outside each edge (closed-form pixel position u = fx·x/z + cx) and checking that it is
+    kept and reaches into the image, or culled and contributes nothing; with the band off
+    (the default) every one of them is kept and reaches into the image."""
     cam = sg.camera_identity(64, 48, 60.0)
+    OPT_G = sg.Options(guard_band=0.15)
     size = (cam.width, cam.height)[axis]
     f = (cam.fx, cam.fy)[axis]
     c = (cam.cx, cam.cy)[axis]
@@ -504,13 +506,15 @@ def test_guard_band_cull(O, axis):
         pos = [0.0, 0.0, z]
         pos[axis] = (target - c) * z / f
         sc = one_gaussian(pos, [1.0, 1.0, 1.0], opacity=0.9)
-        pg = O.project(sc, cam, OPT)
+        pg = O.project(sc, cam, OPT_G)
         assert (pg[0, 0] == 1) == keep, (axis, target)
-        out = O.render(sc, cam, OPT)
+        out = O.render(sc, cam, OPT_G)
         if keep:
             assert out["alpha"].max() > 0.05  # σ ≈ 20 px: its footprint reaches into the image
         else:
             assert out["alpha"].max() == 0.0
+        assert O.project(sc, cam, OPT)[0, 0] == 1  # band off: kept
+        assert O.render(sc, cam, OPT)["alpha"].max() > 0.05
 
 
 # ----------------------------------------------------------------------------- L_d
@@ -809,3 +813,99 @@ def test_mc_plane_and_degenerate(O):
     np.testing.assert_allclose(tn, np.broadcast_to(nrm, tn.shape), atol=1e-6)
     assert len(O.marching_cubes(np.ones_like(sdf), np.ones_like(sdf), origin, vs)) == 0
     assert len(O.marching_cubes(sdf, np.zeros_like(sdf), origin, vs)) == 0
+
+
+# ----------------------------------------------------------------------------- sort key and order (S7)
+
+def _round_f32(q):
+    """Round a rational to the nearest binary32 value, ties to even (normal range only):
+    an fp32 rounding written from its definition, independent of any float hardware."""
+    from fractions import Fraction
+    if q == 0:
+        return np.float32(0.0)
+    sign = -1 if q < 0 else 1
+    a = abs(q)
+    e = a.numerator.bit_length() - a.denominator.bit_length()  # 2^e ≤ a < 2^(e+2)
+    while a >= Fraction(2) ** (e + 1):
+        e += 1
+    while a < Fraction(2) ** e:
+        e -= 1
+    assert -126 <= e <= 127
+    scaled = a / Fraction(2) ** (e - 23)  # in [2^23, 2^24)
+    m = scaled.numerator // scaled.denominator
+    rem = scaled - m
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and m % 2 == 1):
+        m += 1
+    v = Fraction(m) * Fraction(2) ** (e - 23)
+    return np.float32(sign * float(v))  # exactly representable
+
+
+def _fma_f32(a, b, c):
+    """IEEE fused multiply-add in binary32: a·b + c computed exactly, rounded once."""
+    from fractions import Fraction
+    return _round_f32(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def test_zkey_fp32_fma_chain_exact(O):
+    """Reading S7: the sort key is z_key = fma(W20, μx, fma(W21, μy, fma(W22, μz, t2))) in
+    IEEE fp32. The oracle's value (C fmaf) equals, bit for bit, the chain evaluated with exact
+    rational arithmetic and one round-to-nearest-even per fma (written from the IEEE
+    definition here), over random cameras and Gaussians including near-tie values."""
+    rng = np.random.default_rng(17)
+    for trial in range(6):
+        cam = O_cam(random_cam(rng))
+        n = 200
+        mu = rng.normal(scale=1.5, size=(3, n))
+        mu[:, :20] = mu[:, 20:40] * (1 + 1e-7)  # near-equal keys
+        sc = sg.make_scene(mu, np.full((3, n), 0.05), sg.random_quaternions(rng, n), np.full(n, 0.9),
+                           np.zeros((16, 3, n)))
+        pg = O.project(sc, cam, OPT)
+        R = np.asarray(cam.R, np.float32).reshape(9)
+        t = np.asarray(cam.t, np.float32)
+        for i in range(n):
+            m = sc.means[:, i]
+            z = _fma_f32(R[6], m[0], _fma_f32(R[7], m[1], _fma_f32(R[8], m[2], t[2])))
+            got = np.float32(pg[i, O.PG["zkey"]])
+            assert got.view(np.uint32) == z.view(np.uint32), (trial, i, got, z)
+
+
+def test_round_f32_helper_matches_numpy_on_exact_cases():
+    """The helper itself: on values whose binary32 rounding numpy does in one step (float64
+    inputs converted once), the two agree — including ties to even."""
+    from fractions import Fraction
+    rng = np.random.default_rng(3)
+    for x in rng.normal(scale=10, size=200):
+        assert _round_f32(Fraction(float(x))) == np.float32(x)
+    one = Fraction(1)
+    ulp = Fraction(1, 2 ** 23)
+    assert _round_f32(one + ulp / 2) == np.float32(1.0)            # tie → even (1.0)
+    assert _round_f32(one + 3 * ulp / 2) == np.float32(1.0 + 2 ** -22)  # tie → even (odd mantissa rounds up)
+
+
+def test_order_tie_break_by_index(O):
+    """PAPER:422 orders by depth; equal keys break by Gaussian index (reading S7; SPEC:168,
+    172). Two co-located splats with different colours and opacities: at their common centre
+    the blended colour is c_a·α_a + c_b·α_b·(1 − α_a) with a the LOWER id (closed form), and
+    swapping the ids swaps the roles; oracle.order lists the lower id first."""
+    cam = sg.camera_identity(32, 32, 32)
+    pos = [(15.5 - 16) * 3.0 / 32, (15.5 - 16) * 3.0 / 32, 3.0]
+    a = one_gaussian(pos, [0.2, 0.2, 0.2], opacity=0.6, dc=(1.0, 0.0, 0.0))
+    b = one_gaussian(pos, [0.2, 0.2, 0.2], opacity=0.5, dc=(0.0, 1.0, 0.0))
+    for first, second in ((a, b), (b, a)):
+        sc = concat(first, second)
+        assert list(O.order(sc, cam, OPT)) == [0, 1]
+        pg = O.project(sc, cam, OPT)
+        assert pg[0, O.PG["zkey"]] == pg[1, O.PG["zkey"]]
+        out = O.render(sc, cam, OPT)
+        a0, a1 = float(np.float32(first.opacities[0])), float(np.float32(second.opacities[0]))
+        c0, c1 = pg[0, O.PG["rgb"]], pg[1, O.PG["rgb"]]
+        np.testing.assert_allclose(out["color"][:, 15, 15], c0 * a0 + c1 * a1 * (1 - a0), rtol=1e-12)
+    # many ties: the order is (z_key, id) — pinned against a plain sort of (z_key, id) tuples
+    rng = np.random.default_rng(4)
+    sc = dense_scene(9, 300)
+    sc.means[2] = rng.choice([2.5, 3.0, 4.0], sc.n)  # identity camera: z_key = z exactly
+    pg = O.project(sc, cam, OPT)
+    ok = np.nonzero(pg[:, 0] == 1)[0]
+    exp = [i for _, i in sorted((np.float32(pg[i, O.PG["zkey"]]), i) for i in ok)]
+    assert list(O.order(sc, cam, OPT)) == exp
+    assert len(set(np.float32(pg[ok, O.PG["zkey"]]))) == 3
