@@ -152,6 +152,37 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(args):
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment re-launches itself
+    as N ranks under torch.distributed.run on this node (127.0.0.1 rendezvous) and returns
+    the launcher's exit code; None when this process is already a rank (or N = 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def views_per_step(args, n_views, ws):
+    """--views-per-step B (views per rank per step), or 'epoch': B = ceil(V/P), one all-reduce
+    per pass over the config's views."""
+    if str(args.views_per_step) == "epoch":
+        return max(1, math.ceil(n_views / ws))
+    b = int(args.views_per_step)
+    if b < 1:
+        raise SystemExit("--views-per-step must be >= 1 or 'epoch'")
+    return b
+
+
 def barrier(dist_on):
     if dist_on:
         import torch.distributed as dist
@@ -224,13 +255,94 @@ def run_reference(args, cfg_name, config):
     frame_s = float(np.mean(times))
     value = 1.0 / frame_s
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": frame_s * 1e3 * args.views_per_step, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": frame_s * 1e3 * views_per_step(args, len(cams), 1),
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"each step: {desc}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- gloo dry run
+
+
+def run_dry_gloo(args, cfg_name, config):
+    """The GPU arm's distributed skeleton on CPU: the same rank layout (torchrun env), view
+    partition, views per step (incl. 'epoch'), flat-buffer accumulation, bucketed all-reduce,
+    barrier + max-over-ranks timing and rank-0 JSON line — with each view's fwd+bwd replaced by
+    a deterministic fake gradient (the CUDA path needs a GPU). Checks after every step that
+    the all-reduced buffer equals the sum of the fake gradients of ALL ranks' views of the
+    step and that the replicas agree bitwise."""
+    import torch
+    import torch.distributed as dist
+    import scenegen as sg
+    from paper_2406_01467_b200.parallel import FlatGrads, views_for_rank
+
+    ws, rank, _ = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    dist_on = ws > 1
+    if dist_on:
+        dist.init_process_group("gloo")
+    n_views = sg.CONFIGS[cfg_name]["views"]
+    n = 257  # fake Gaussians (the buffer layout of FlatGrads, small)
+    fg = FlatGrads.allocate(n, 16, "cpu")
+    B = views_per_step(args, n_views, ws)
+    mine = views_for_rank(n_views, ws, rank) or [rank % n_views]  # more ranks than views: repeat one
+
+    def fake(v):
+        return torch.full((fg.flat.numel(),), float(v % 7 + 1)) * (torch.arange(fg.flat.numel()) % 5 + 1)
+
+    counter = {"v": 0}
+
+    def step():
+        fg.zero_()
+        ks = []
+        for _ in range(B):
+            ks.append(counter["v"])
+            counter["v"] += 1
+        for k in ks:
+            fg.flat += fake(mine[k % len(mine)])
+        fg.allreduce(bucket_bytes=args.bucket_mb << 20)
+        # every rank's views of this step: rank r ran views_for_rank(...)[k % len] for the same ks
+        exp = torch.zeros_like(fg.flat)
+        for r in range(ws):
+            vr = views_for_rank(n_views, ws, r) or [r % n_views]
+            for k in ks:
+                exp += fake(vr[k % len(vr)])
+        assert torch.equal(fg.flat, exp), "all-reduced buffer != sum over ranks"
+        if dist_on:
+            cs = torch.tensor([float(fg.flat.double().sum())], dtype=torch.float64)
+            lo, hi = cs.clone(), cs.clone()
+            dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+            dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+            assert lo.item() == hi.item(), "replicas differ"
+
+    for _ in range(args.warmup):
+        step()
+    barrier(dist_on)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    barrier(dist_on)
+    elapsed = time.perf_counter() - t0
+    if dist_on:
+        t = torch.tensor([elapsed], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    total = args.steps * B * ws
+    config.update({"views_per_step_per_rank": B, "parallelism": f"view-parallel dp{ws} (gloo dry run)"})
+    line = {"metric": METRIC, "value": total / elapsed, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+            "dry_run": "gloo: fake per-view gradients, all-reduce checked against the sum over ranks", "gpu_launches": 0}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist_on:
+        dist.destroy_process_group()
     return 0
 
 
@@ -243,6 +355,9 @@ def run_gpu(args, cfg_name, config):
     import scenegen as sg
 
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} (launch with torchrun, or let "
+                         f"bench.py re-launch itself by leaving WORLD_SIZE unset)")
     dist_on = ws > 1
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -254,8 +369,9 @@ def run_gpu(args, cfg_name, config):
 
     scene, cams, opt = sg.config_scene_and_cameras(cfg_name, n_gaussians=args.n_gaussians)
     n = scene.n
-    my_views = [cams[v] for v in views_for_rank(len(cams), ws, rank)]
-    B = args.views_per_step
+    my_views = [cams[v] for v in (views_for_rank(len(cams), ws, rank) or [rank % len(cams)])]
+    B = views_per_step(args, len(cams), ws)
+    comm_stream = torch.cuda.Stream(device) if dist_on else None  # the all-reduce's side stream
     g = P.Gaussians.from_numpy(scene, device)
     K = g.sh.shape[1]
     fg = FlatGrads.allocate(n, K, device)  # one flat buffer: the all-reduce operand
@@ -266,7 +382,9 @@ def run_gpu(args, cfg_name, config):
     gen.manual_seed(SEED_COT + rank)
     cots = [torch.randn((10, H, W), generator=gen, device=device, dtype=torch.float32) for _ in range(n_ring)]
     opts = dict(tile=args.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
-                median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
+                median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree,
+                guard_band=opt.guard_band if args.guard_band is None else args.guard_band)
+    config["guard_band"] = opts["guard_band"]
     # Views are pipelined over `args.pipeline` CUDA streams, each with its own rd_view and
     # output maps (and its own host thread): the views of a step run concurrently. Their
     # gradient accumulations (K5, rd_preprocess_bwd) add into the one flat buffer with L2
@@ -322,14 +440,15 @@ def run_gpu(args, cfg_name, config):
                 mark()
                 P.rd_render_fwd(vw, o["color"], o["depth"], o["normal"], o["alpha"], stream=st)
             mark()
-            if io:
-                io["fwd_done"].record(st)
-                st.wait_event(io["cot_ready"])
-            if args.normal_consistency:  # NEXT-2: L_n on the maps; its cotangents join the maps'
-                ct = slot["cot"]
-                ct.copy_(cot)
+            if args.normal_consistency:  # NEXT-2: L_n on the maps (its plane is read back with them)
                 P.rd_normal_consistency(cam, o["depth"], o["alpha"], o["normal"], consistency=o["consistency"],
                                         stream=st)
+            if io:
+                io["fwd_done"].record(st)  # every map plane of the view is written
+                st.wait_event(io["cot_ready"])
+            if args.normal_consistency:  # its cotangents join the maps'
+                ct = slot["cot"]
+                ct.copy_(cot)
                 P.rd_normal_consistency_bwd(cam, o["depth"], o["normal"], ct[9], ct[3], ct[7], ct[4:7], stream=st)
                 cot = ct
             if args.distortion:
@@ -374,9 +493,15 @@ def run_gpu(args, cfg_name, config):
             futs = [pool.submit(worker, [j for j in range(len(ks)) if ks[j] % P_ == si]) for si in range(P_)]
             for f in futs:
                 f.result()
-        for sl in slots:
-            main_stream.wait_event(sl["done"])
-        fg.allreduce()  # NCCL sum over ranks (no-op at N = 1)
+        if comm_stream is None:
+            for sl in slots:
+                main_stream.wait_event(sl["done"])
+        else:  # NCCL sum over ranks on a side stream once every view's K5 has added its rows
+            for sl in slots:
+                comm_stream.wait_event(sl["done"])
+            with torch.cuda.stream(comm_stream):
+                fg.allreduce(bucket_bytes=args.bucket_mb << 20)
+            main_stream.wait_stream(comm_stream)
 
     def step():
         run_views(lambda sl, k: one_view(sl, my_views[k % len(my_views)], cots[k % n_ring]))
@@ -583,6 +708,8 @@ def run_gpu(args, cfg_name, config):
         "ms_per_view_by_kernel": {k: tim["ms"][k] / max(views_timed, 1) for k in tim["ms"]},
         "parallelism": f"view-parallel dp{ws}",
         "streams": P_, "host_threads": bool(args.host_threads),
+        "allreduce": (f"NCCL sum of the {4 * fg.flat.numel() / 2**20:.0f} MB flat gradient buffer once per step, "
+                      f"{args.bucket_mb} MB buckets on a side stream" if dist_on else "none (N = 1)"),
     })
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -612,7 +739,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="rade", choices=["rade", "reference"])
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
-    ap.add_argument("--views-per-step", type=int, default=4)
+    ap.add_argument("--views-per-step", default="4",
+                    help="views per rank per step, or 'epoch' (ceil(views / ranks): one all-reduce per epoch)")
+    ap.add_argument("--bucket-mb", type=int, default=64, help="all-reduce bucket size (N > 1)")
+    ap.add_argument("--guard-band", type=float, default=None,
+                    help="reading S6b guard band (0 = off); default: the config's (C3/C4 0.15, others off)")
+    ap.add_argument("--dry-run-gloo", action="store_true",
+                    help="CPU-only rehearsal of the distributed step (gloo, fake per-view work): plumbing test")
     ap.add_argument("--n-gaussians", type=int, default=None)
     ap.add_argument("--ref-pixels", type=int, default=32, help="oracle arm: forward pixels sampled per step")
     ap.add_argument("--ref-grads", type=int, default=2, help="oracle arm: Gaussians differentiated per step")
@@ -631,6 +764,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 does not meet the timing rules", file=sys.stderr)
+    rc = relaunch_if_needed(args)
+    if rc is not None:
+        return rc
     import scenegen as sg
     info = sg.CONFIGS[args.config]
     config = {"workload": f"{args.config}: {info['name']}", "width": info["width"], "height": info["height"],
@@ -640,6 +776,8 @@ def main():
               "scene_recipe": "scenegen (DESIGN.md §Input recipe), seed 0 + config index"}
     if args.impl == "reference":
         return run_reference(args, args.config, config)
+    if args.dry_run_gloo:
+        return run_dry_gloo(args, args.config, config)
     return run_gpu(args, args.config, config)
 
 
