@@ -107,15 +107,20 @@ def peaks():
 
 
 def fp32_peak_tflops(n_sm, sm_mhz):
-    """FFMA peak: SMs × 128 FP32 lanes × 2 flop × clock."""
-    return n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12
+    """FP32 FFMA peak: the measured one (profiles/fp32_peak.json, tools/ffma_peak.cu on this
+    pool's B200s); else the formula SMs × 128 FP32 lanes × 2 flop × clock. Returns (TFLOP/s,
+    source)."""
+    p = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["fp32_ffma_tflops"]), "measured FFMA (profiles/fp32_peak.json)"
+    return n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12, f"formula: {n_sm} SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz"
 
 
-# algorithmic work per unit (DESIGN.md §Roofline, SURVEY.md §8(d))
-FWD_FLOP_EVAL, FWD_FLOP_BLEND = 12, 15     # K3: per evaluated pair / extra per blended pair
-BWD_FLOP_EVAL, BWD_FLOP_BLEND = 12, 80     # K4: per evaluated pair / extra per blended pair
-K1_B_ALL, K1_B_VIS = 20, 296               # K1: cull read (means + opacity + touched) / visible
-K5_B_ALL, K5_B_VIS = 4, 772                # K5: touched / params 236 + g2d 64 + grads RMW 472
+# algorithmic work per unit: SURVEY.md §8(d)'s units (DESIGN.md §7)
+FWD_FLOP_PASS = 46     # K3: flop per α-passing (blended) pair: 23 FP32-pipe instructions, FFMA = 2
+BWD_FLOP_PASS = 120    # K4: flop per α-passing pair
+K1_B_ALL, K1_B_VIS = 12, 300               # K1: cull read per Gaussian / 224 B in + 76 B out per visible
+K5_B_VIS = 600                             # K5: params 236 + 2-D grads 60 + record 64 + grads 236 per visible
 
 
 def kernel_work(name, t, views, tile_bits):
@@ -134,11 +139,11 @@ def kernel_work(name, t, views, tile_bits):
     if name == "ranges":
         return 4 * M, "hbm"
     if name == "render_fwd":
-        return FWD_FLOP_EVAL * t["pairs_evaluated_fwd"] + FWD_FLOP_BLEND * t["pairs_blended_fwd"], "alu"
+        return FWD_FLOP_PASS * t["pairs_blended_fwd"], "alu"
     if name == "render_bwd":
-        return BWD_FLOP_EVAL * t["pairs_evaluated_bwd"] + BWD_FLOP_BLEND * t["pairs_blended_fwd"], "alu"
+        return BWD_FLOP_PASS * t["pairs_blended_fwd"], "alu"
     if name == "preprocess_bwd":
-        return K5_B_ALL * n * views + K5_B_VIS * nvis, "hbm"
+        return K5_B_VIS * nvis, "hbm"
     raise KeyError(name)
 
 
@@ -652,7 +657,7 @@ def run_gpu(args, cfg_name, config):
     # ---------------- roofline of the dominant kernel + per-kernel breakdown
     hbm, hbm_src, sm_max = peaks()
     n_sm = torch.cuda.get_device_properties(device).multi_processor_count
-    fp32 = fp32_peak_tflops(n_sm, sm_max)
+    fp32, fp32_src = fp32_peak_tflops(n_sm, sm_max)
     views_timed = tim["views"]
     tim_ext = dict(tim)
     tim_ext["n"] = n
@@ -688,8 +693,9 @@ def run_gpu(args, cfg_name, config):
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
                 "peak": hbm if dk["bound"] == "hbm" else fp32, "unit": dk["unit"], "frac": dk["frac"],
                 "traffic": traffic, "issue_active_pct": issue, "ncu_capture": capture,
-                "peak_source": (f"{hbm_src} HBM copy (MEASURED_PEAKS.json)" if dk["bound"] == "hbm" else
-                                f"FP32 FFMA {n_sm} SMs x 128 lanes x 2 flop x {sm_max:.0f} MHz (DESIGN.md)")}
+                "peak_source": (f"{hbm_src} HBM copy (MEASURED_PEAKS.json)" if dk["bound"] == "hbm" else fp32_src),
+                "unit_of_work": ("SURVEY.md §8(d): K3 46 flop / K4 120 flop per alpha-passing (blended) pair, "
+                                 "K1 12 B per Gaussian + 300 B per visible, K5 600 B per visible")}
 
     # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so):
     # K1, depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan),

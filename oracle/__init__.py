@@ -368,7 +368,9 @@ def marching_cubes(tsdf, weight, origin, voxel, iso=0.0):
     voxel centres (origin + (i+½)·voxel), skipped when a corner has weight 0; per cell the
     table's triangles, each vertex linearly interpolated on its edge,
     p = p_a + (iso − v_a)/(v_b − v_a)·(p_b − p_a). Order: cells with x fastest, then y, z;
-    triangles in table order. Returns float64 [T, 3, 3] (vertex positions)."""
+    triangles in table order; a triangle with two vertices on the same cube corner (a corner
+    value equal to iso makes s exactly 0 or 1) has zero area and is dropped. Returns float64
+    [T, 3, 3] (vertex positions)."""
     table = mc_table()
     t = np.asarray(tsdf, np.float32)
     w = np.asarray(weight)
@@ -393,13 +395,16 @@ def marching_cubes(tsdf, weight, origin, voxel, iso=0.0):
                 if not ok or cfg == 0 or cfg == 255:
                     continue
                 for tri in table[cfg]:
-                    tv = []
+                    tv, at = [], []
                     for e in tri:
                         a, b = _MC_EDGES[e]
                         pa = np.array([cx(i + corners[a][0]), cy(j + corners[a][1]), cz(k + corners[a][2])])
                         pb = np.array([cx(i + corners[b][0]), cy(j + corners[b][1]), cz(k + corners[b][2])])
                         s = (iso - vals[a]) / (vals[b] - vals[a])
                         tv.append(pa + s * (pb - pa))
+                        at.append(a if s == 0.0 else b if s == 1.0 else -1 - len(at))  # corner it sits on
+                    if len(set(at)) < 3:  # two vertices on one corner: zero area, dropped (S25)
+                        continue
                     out.append(tv)
     return np.array(out, np.float64).reshape(-1, 3, 3)
 

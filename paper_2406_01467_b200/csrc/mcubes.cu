@@ -13,6 +13,10 @@
 // Extraction is three passes over the (X−1)(Y−1)(Z−1) cells: count triangles per cell (0 if
 // a corner has weight 0), exclusive scan (CUB), emit each cell's triangles at its offset —
 // a deterministic triangle soup in cell order (x fastest), triangles in table order.
+// Degenerate triangles are dropped (reading S25): a vertex lands exactly on a cube corner only
+// when that corner's value equals iso (then s = (iso − v_a)/(v_b − v_a) is exactly 0 or 1),
+// and a triangle is degenerate exactly when two of its vertices land on the same corner
+// (three distinct corner / edge-interior points of a cube cannot be collinear here).
 #include "rade_internal.cuh"
 
 #include <cub/device/device_scan.cuh>
@@ -126,6 +130,19 @@ __device__ __forceinline__ int cell_config(const Vol& v, int i, int j, int k, fl
   return cfg;
 }
 
+// The cube corner a vertex on edge e sits on (s = 0: its first corner, s = 1: its second), −1
+// for an edge-interior vertex.
+__device__ __forceinline__ int vertex_corner(int e, const float (&val)[8], float iso) {
+  const int a = c_edge[e][0], b = c_edge[e][1];
+  const float s = (iso - val[a]) / (val[b] - val[a]);
+  return s == 0.f ? a : (s == 1.f ? b : -1);
+}
+__device__ __forceinline__ bool tri_degenerate(int cfg, int t, const float (&val)[8], float iso) {
+  const int c0 = vertex_corner(c_tri[cfg][3 * t], val, iso), c1 = vertex_corner(c_tri[cfg][3 * t + 1], val, iso),
+            c2 = vertex_corner(c_tri[cfg][3 * t + 2], val, iso);
+  return (c0 >= 0 && (c0 == c1 || c0 == c2)) || (c1 >= 0 && c1 == c2);
+}
+
 __global__ void __launch_bounds__(256) k_mc_count(Vol v, float iso, uint32_t* __restrict__ count) {
   const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int CX = v.X - 1, CY = v.Y - 1;
@@ -134,7 +151,10 @@ __global__ void __launch_bounds__(256) k_mc_count(Vol v, float iso, uint32_t* __
   const int i = (int)(cell % CX), j = (int)((cell / CX) % CY), k = (int)(cell / ((int64_t)CX * CY));
   float val[8];
   const int cfg = cell_config(v, i, j, k, iso, val);
-  count[cell] = cfg < 0 ? 0u : (uint32_t)c_ntri[cfg];
+  uint32_t n = 0;
+  if (cfg >= 0)
+    for (int t = 0; t < c_ntri[cfg]; ++t) n += tri_degenerate(cfg, t, val, iso) ? 0u : 1u;
+  count[cell] = n;
 }
 
 __global__ void __launch_bounds__(256) k_mc_emit(Vol v, float iso, const uint32_t* __restrict__ offset,
@@ -149,7 +169,8 @@ __global__ void __launch_bounds__(256) k_mc_emit(Vol v, float iso, const uint32_
   if (cfg < 0) return;
   const int n = c_ntri[cfg];
   float* o = out + (int64_t)offset[cell] * 9;
-  for (int t = 0; t < n; ++t)
+  for (int t = 0, w = 0; t < n; ++t) {
+    if (tri_degenerate(cfg, t, val, iso)) continue;
     for (int q = 0; q < 3; ++q) {
       const int e = c_tri[cfg][3 * t + q], a = c_edge[e][0], b = c_edge[e][1];
       const float s = (iso - val[a]) / (val[b] - val[a]);
@@ -160,9 +181,11 @@ __global__ void __launch_bounds__(256) k_mc_emit(Vol v, float iso, const uint32_
       for (int d = 0; d < 3; ++d) {
         const float pa = __fadd_rn(__fmul_rn((float)ia[d] + 0.5f, v.vs), org[d]);
         const float pb = __fadd_rn(__fmul_rn((float)ib[d] + 0.5f, v.vs), org[d]);
-        o[9 * t + 3 * q + d] = pa + s * (pb - pa);
+        o[9 * w + 3 * q + d] = pa + s * (pb - pa);
       }
     }
+    ++w;
+  }
 }
 
 }  // namespace
@@ -170,21 +193,34 @@ __global__ void __launch_bounds__(256) k_mc_emit(Vol v, float iso, const uint32_
 namespace {
 // Per host thread, grow-only scratch reused across calls (count, offset, scan temp) and a
 // pinned slot for the count read-back: a fresh cudaMallocAsync / cudaMallocHost per call cost
-// milliseconds (and cudaFreeHost synchronises the device).
+// milliseconds (and cudaFreeHost synchronises the device). `done` is recorded after the last
+// use of the scratch (the emit reads offset asynchronously); the next call — possibly on
+// another stream — waits for it before rewriting count / offset, and before freeing them.
 struct McScratch {
   uint32_t *count = nullptr, *offset = nullptr, *host = nullptr;
   void* temp = nullptr;
   size_t cells = 0, temp_bytes = 0;
+  cudaEvent_t done = nullptr;
 };
 thread_local McScratch t_mc;
+
+// The triangulation table goes to constant memory once per process (every call used to
+// rewrite it asynchronously while an earlier emit on another stream could be reading it).
+cudaError_t upload_table() {
+  static cudaError_t status = [] {
+    const McTable table = build_table();
+    cudaError_t e = cudaMemcpyToSymbol(c_tri, table.tri, sizeof(table.tri));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_ntri, table.ntri, sizeof(table.ntri));
+    return e;
+  }();
+  return status;
+}
 }  // namespace
 
 cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int dims[3], const float* tsdf,
                                   const float* weight, float iso, float* triangles, int64_t capacity,
                                   int64_t* n_triangles, cudaStream_t s) {
-  static const McTable table = build_table();  // thread-safe one-time construction
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_tri, table.tri, sizeof(table.tri), 0, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(c_ntri, table.ntri, sizeof(table.ntri), 0, cudaMemcpyHostToDevice, s);
+  cudaError_t e = upload_table();  // thread-safe one-time construction and upload
   if (e != cudaSuccess) return e;
   *n_triangles = 0;
   if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2) return cudaSuccess;
@@ -196,10 +232,15 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
   McScratch& m = t_mc;
   if (!m.host) {
     e = cudaMallocHost(&m.host, 8);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  } else {
+    e = cudaStreamWaitEvent(s, m.done, 0);  // the previous call's emit has read offset
     if (e != cudaSuccess) return e;
   }
   if (m.cells < (size_t)ncell) {
-    e = cudaStreamSynchronize(s);  // the old buffers may still be in use on s
+    e = cudaEventSynchronize(m.done);  // the old buffers may still be in use
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (m.count) cudaFree(m.count);
     if (m.offset) cudaFree(m.offset);
     m.count = m.offset = nullptr;
@@ -210,7 +251,8 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
     m.cells = (size_t)ncell;
   }
   if (m.temp_bytes < scan_bytes) {
-    e = cudaStreamSynchronize(s);
+    e = cudaEventSynchronize(m.done);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (m.temp) cudaFree(m.temp);
     m.temp = nullptr;
     m.temp_bytes = 0;
@@ -227,7 +269,9 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
   if (e != cudaSuccess) return e;
   *n_triangles = (int64_t)m.host[0] + m.host[1];
   if (triangles && capacity >= *n_triangles) k_mc_emit<<<grid, 256, 0, s>>>(v, iso, m.offset, triangles);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventRecord(m.done, s);
+  return e;
 }
 
 }  // namespace rade

@@ -408,7 +408,10 @@ template <int DEG>
 #ifndef RD_K1_THREADS
 #define RD_K1_THREADS 64  // finer blocks fill the SMs more evenly: 0.107 -> 0.101 ms
 #endif
-__global__ void __launch_bounds__(RD_K1_THREADS) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
+#ifndef RD_K1_MINB
+#define RD_K1_MINB 8  // ≤ 128 registers: 16 warps per SM for the latency-bound loads
+#endif
+__global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
                                                          Record* __restrict__ rec, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
                                                          uint32_t* __restrict__ didx,

@@ -634,6 +634,42 @@ def test_marching_cubes_capacity_guess_paths():
         np.testing.assert_allclose(gpu, ref, atol=1e-5)
 
 
+def test_marching_cubes_exact_iso_corners():
+    """Corner values equal to iso (integer volume, iso 0): the zero-area triangles with two
+    vertices on one corner are dropped on both sides (reading S25); same soup, same order."""
+    rng = np.random.default_rng(21)
+    t = rng.integers(-1, 2, (17, 17, 17)).astype(np.float32)
+    gpu, ref = _mc_both(t, np.ones_like(t), (0.5, -1.0, 2.0), 0.25, 0.0)
+    assert ref.shape[0] > 1000 and gpu.shape == ref.shape
+    np.testing.assert_allclose(gpu, ref, atol=1e-6)
+    area = np.linalg.norm(np.cross(gpu[:, 1] - gpu[:, 0], gpu[:, 2] - gpu[:, 0]), axis=1)
+    assert area.min() > 0
+
+
+def test_marching_cubes_scratch_across_streams():
+    """Two extractions issued back to back from one host thread on two different streams
+    (the per-thread scratch is shared): both return the oracle's soup."""
+    rng = np.random.default_rng(22)
+    vols, refs = [], []
+    for n in (20, 14):
+        t = rng.uniform(-1, 1, (n, n, n)).astype(np.float32)
+        vol = P.TsdfVolume((0.0, 0.0, 0.0), 0.5, (n, n, n))
+        vol.tsdf.copy_(torch.as_tensor(t))
+        vol.weight.fill_(1.0)
+        vols.append(vol)
+        refs.append(oracle.marching_cubes(t, np.ones_like(t), (0.0, 0.0, 0.0), 0.5, 0.0))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        a = P.rd_marching_cubes(vols[0])
+    with torch.cuda.stream(s2):
+        b = P.rd_marching_cubes(vols[1])
+    torch.cuda.synchronize()
+    for got, ref in ((a, refs[0]), (b, refs[1])):
+        got = got.double().cpu().numpy()
+        assert got.shape == ref.shape
+        np.testing.assert_allclose(got, ref, atol=1e-5)
+
+
 def test_marching_cubes_degenerate_volumes():
     """Empty (< 2 voxels along an axis), unobserved (weight 0), all-inside / all-outside:
     no triangles; a too-small capacity returns the count and writes nothing."""

@@ -909,3 +909,24 @@ def test_order_tie_break_by_index(O):
     exp = [i for _, i in sorted((np.float32(pg[i, O.PG["zkey"]]), i) for i in ok)]
     assert list(O.order(sc, cam, OPT)) == exp
     assert len(set(np.float32(pg[ok, O.PG["zkey"]]))) == 3
+
+
+def test_mc_exact_iso_corners_no_degenerate_triangles(O):
+    """Reading S25: corner values equal to iso put vertices exactly on cube corners; every
+    triangle that would have two vertices on one corner (zero area) is dropped, and all the
+    others keep a positive area. Integer-valued volume with iso = 0 hits this everywhere."""
+    rng = np.random.default_rng(21)
+    t = rng.integers(-1, 2, (9, 9, 9)).astype(np.float32)
+    tri = O.marching_cubes(t, np.ones_like(t), (0.0, 0.0, 0.0), 1.0, 0.0)
+    assert tri.shape[0] > 100
+    area = 0.5 * np.linalg.norm(np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]), axis=1)
+    assert area.min() > 1e-6
+    # the table alone (no drop) would emit more: some were degenerate
+    table = O.mc_table()
+    n_all = 0
+    for k in range(8):
+        for j in range(8):
+            for i in range(8):
+                cfg = sum(1 << c for c in range(8) if t[k + (c >> 2 & 1), j + (c >> 1 & 1), i + (c & 1)] < 0)
+                n_all += len(table[cfg]) if 0 < cfg < 255 else 0
+    assert n_all > tri.shape[0]
