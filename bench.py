@@ -121,6 +121,12 @@ FWD_FLOP_PASS = 46     # K3: flop per α-passing (blended) pair: 23 FP32-pipe in
 BWD_FLOP_PASS = 120    # K4: flop per α-passing pair
 K1_B_ALL, K1_B_VIS = 12, 300               # K1: cull read per Gaussian / 224 B in + 76 B out per visible
 K5_B_VIS = 600                             # K5: params 236 + 2-D grads 60 + record 64 + grads 236 per visible
+# batched K5 (rd_preprocess_bwd_views): per Gaussian visible in any view of the batch its SH row
+# once (192 B) and its SH gradient row reduced once (read + write, 384 B); per (visible Gaussian,
+# view) the geometry pass: parameters 56 B (means, scales, rotation, opacity), the 80-B 2-D
+# gradient row and the geometry gradient rows reduced (read + write, 88 B); the views'
+# tiles_touched (4 B per Gaussian per view)
+K5V_B_UNION, K5V_B_VIS, K5V_B_ALL = 576, 224, 4
 
 
 def kernel_work(name, t, views, tile_bits):
@@ -143,6 +149,8 @@ def kernel_work(name, t, views, tile_bits):
     if name == "render_bwd":
         return BWD_FLOP_PASS * t["pairs_blended_fwd"], "alu"
     if name == "preprocess_bwd":
+        if t.get("n_visible_union"):  # batched K5
+            return K5V_B_UNION * t["n_visible_union"] + K5V_B_VIS * nvis + K5V_B_ALL * n * views, "hbm"
         return K5_B_VIS * nvis, "hbm"
     raise KeyError(name)
 
@@ -413,6 +421,8 @@ def run_gpu(args, cfg_name, config):
         slots.append(slot)
     view = slots[0]["view"]
     outs = slots[0]["outs"]
+    streams = {"k5": torch.cuda.Stream(device)}  # the batched K5 of each round of views
+    k5_done = torch.cuda.Event()
     counter = {"v": 0}
     main_stream = torch.cuda.current_stream(device)
 
@@ -463,8 +473,9 @@ def run_gpu(args, cfg_name, config):
             if io:
                 io["k4_done"].record(st)
             mark()
-            P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
-            slot["done"].record(st)
+            if args.k5 == "per-view":
+                P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
+            slot["done"].record(st)  # batched K5: the round's rd_preprocess_bwd_views waits for this
             mark()
         if ph is not None:
             phase_log.append(ph)
@@ -485,25 +496,39 @@ def run_gpu(args, cfg_name, config):
         for b in range(B):
             ks.append(counter["v"])
             counter["v"] += 1
-        if pool is None:
-            for k in ks:
-                per_view(slots[k % P_], k)
-        else:
-            def worker(js):
-                torch.cuda.set_device(device)  # per thread
-                for j in js:
-                    per_view(slots[ks[j] % P_], ks[j])
+        # rounds of one view per slot; with the batched K5 (default) each round ends with ONE
+        # rd_preprocess_bwd_views over its views on k5_stream (after every view's K4), and a
+        # slot's next view waits for it (its K1 rewrites the view's 2-D gradient rows)
+        last = []
+        for r0 in range(0, len(ks), P_):
+            rnd = ks[r0:r0 + P_]
+            used = [slots[i] for i in range(len(rnd))]
+            if pool is None:
+                for sl, k in zip(used, rnd):
+                    per_view(sl, k)
+            else:
+                def worker(sl, k):
+                    torch.cuda.set_device(device)  # per thread
+                    per_view(sl, k)
 
-            # one task per slot: its views in order
-            futs = [pool.submit(worker, [j for j in range(len(ks)) if ks[j] % P_ == si]) for si in range(P_)]
-            for f in futs:
-                f.result()
-        if comm_stream is None:
-            for sl in slots:
-                main_stream.wait_event(sl["done"])
-        else:  # NCCL sum over ranks on a side stream once every view's K5 has added its rows
-            for sl in slots:
-                comm_stream.wait_event(sl["done"])
+                futs = [pool.submit(worker, sl, k) for sl, k in zip(used, rnd)]
+                for f in futs:
+                    f.result()
+            if args.k5 == "batched":
+                k5s = streams["k5"]
+                for sl in used:
+                    k5s.wait_event(sl["done"])
+                P.rd_preprocess_bwd_views([sl["view"] for sl in used], g, grads, stream=k5s)
+                k5_done.record(k5s)
+                for sl in used:
+                    sl["stream"].wait_event(k5_done)
+                last = [k5_done]
+            else:
+                last = [sl["done"] for sl in used]
+        waiter = main_stream if comm_stream is None else comm_stream
+        for ev in last:
+            waiter.wait_event(ev)
+        if comm_stream is not None:  # NCCL sum over ranks on a side stream once every view's K5 has added its rows
             with torch.cuda.stream(comm_stream):
                 fg.allreduce(bucket_bytes=args.bucket_mb << 20)
             main_stream.wait_stream(comm_stream)
@@ -553,18 +578,35 @@ def run_gpu(args, cfg_name, config):
 
     # ---------------- per-kernel timings: the same steps again, serialised on one stream with
     # the ABI's CUDA-event hooks around every kernel (rd_set_profiling)
-    slots_all = slots
-    slots = slots_all[:1]
-    P_ = 1
-    P.rd_set_profiling(view, True)
+    # every slot keeps its view and buffers, but all of them (and the batched K5) run on one
+    # stream from one host thread, so the kernels are serialised and each one's CUDA-event time
+    # is its own; timings are summed over the slots' views
+    prof_stream = torch.cuda.Stream(device)
+    saved = [sl["stream"] for sl in slots], streams["k5"], pool
+    for sl in slots:
+        sl["stream"] = prof_stream
+        P.rd_set_profiling(sl["view"], True)
+    streams["k5"], pool = prof_stream, None
     torch.cuda.synchronize()
     for _ in range(args.steps):
         step()
     torch.cuda.synchronize()
-    tim = P.rd_get_timings(view, reset=True)
-    P.rd_set_profiling(view, False)
-    slots = slots_all
-    P_ = len(slots_all)
+    tim = None
+    for sl in slots:
+        t = P.rd_get_timings(sl["view"], reset=True)
+        P.rd_set_profiling(sl["view"], False)
+        if tim is None:
+            tim = t
+            continue
+        for key in ("ms", "launches"):
+            for kname, val in t[key].items():
+                tim[key][kname] = tim[key].get(kname, 0) + val
+        for key in ("n_duplicates", "views", "pairs_evaluated_fwd", "pairs_blended_fwd", "pairs_evaluated_bwd",
+                    "n_visible", "n_visible_union"):
+            tim[key] += t[key]
+    for sl, st_ in zip(slots, saved[0]):
+        sl["stream"] = st_
+    streams["k5"], pool = saved[1], saved[2]
 
     # ---------------- end-to-end: host cotangents in (pinned), rendered maps out, per step
     e2e = None
@@ -748,6 +790,8 @@ def main():
     ap.add_argument("--views-per-step", default="4",
                     help="views per rank per step, or 'epoch' (ceil(views / ranks): one all-reduce per epoch)")
     ap.add_argument("--bucket-mb", type=int, default=64, help="all-reduce bucket size (N > 1)")
+    ap.add_argument("--k5", default="batched", choices=["batched", "per-view"],
+                    help="K5 of a round of views in one rd_preprocess_bwd_views call, or per view")
     ap.add_argument("--guard-band", type=float, default=None,
                     help="reading S6b guard band (0 = off); default: the config's (C3/C4 0.15, others off)")
     ap.add_argument("--dry-run-gloo", action="store_true",

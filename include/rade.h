@@ -154,6 +154,8 @@ typedef struct rd_timings {
   int64_t n_visible;               /* Σ over views of Gaussians with tiles_touched > 0 */
   int64_t n_duplicates;            /* Σ over views of M */
   int64_t views;                   /* rd_render_fwd calls since the last reset */
+  int64_t n_visible_union;         /* Σ over rd_preprocess_bwd_views calls timed on this view of the
+                                      Gaussians visible in at least one of their views */
 } rd_timings;
 
 typedef void* (*rd_alloc_fn)(size_t bytes, void* ctx);
@@ -233,6 +235,19 @@ rd_status rd_blend_bwd(rd_view* view, const float* dL_dcolor, const float* dL_dd
  * rounding of the sum, then depends on timing). `grads` must be 16-byte aligned where
  * rotations are. */
 rd_status rd_preprocess_bwd(rd_view* view, const rd_gaussians* g, const rd_grads* grads, rd_stream stream);
+
+/* Stage 4 second half (K5) for n_views ≤ 8 views of the SAME Gaussians at once (the views of
+ * a training step): equivalent to rd_preprocess_bwd on each view in turn (up to
+ * the fp32 summation order), but each Gaussian's parameter and SH rows are read once, the
+ * chain rules of every view in which it is visible are summed on chip, and its gradient rows
+ * are updated with ONE reduction (per-view K5 re-reads and re-reduces the rows once per view;
+ * PAPER:43-46 is the training use). Every view must have completed rd_blend_bwd with the
+ * same options; the caller orders `stream` after the views' streams (e.g. events) and
+ * before any later use of the views' scratch. Errors: n_views ∉ [1, 8], NULL or repeated
+ * views, differing Gaussians / options → RD_ERR_INVALID_ARGUMENT; a view before
+ * rd_blend_bwd → RD_ERR_STATE. Timed (rd_get_timings) on views[0] as one K5 launch. */
+rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
+                                  const rd_grads* grads, rd_stream stream);
 
 /* NEXT-2: normal consistency (reading S22) on rendered maps (device, fp32,
  * the layouts of rd_render_fwd): ñ = the finite-difference normal of the median depth map

@@ -76,7 +76,7 @@ class RdTimings(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * RD_NUM_KERNELS), ("launches", ctypes.c_int64 * RD_NUM_KERNELS),
                 ("pairs_evaluated_fwd", ctypes.c_int64), ("pairs_blended_fwd", ctypes.c_int64),
                 ("pairs_evaluated_bwd", ctypes.c_int64), ("n_visible", ctypes.c_int64),
-                ("n_duplicates", ctypes.c_int64), ("views", ctypes.c_int64)]
+                ("n_duplicates", ctypes.c_int64), ("views", ctypes.c_int64), ("n_visible_union", ctypes.c_int64)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -103,6 +103,8 @@ SIGNATURES = {
     "rd_normal_consistency_bwd": ([ctypes.POINTER(RdCamera), _VP, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "rd_blend_bwd_ex": ([_VP, ctypes.POINTER(RdBwdCotangents), _VP], ctypes.c_int),
     "rd_preprocess_bwd": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
+    "rd_preprocess_bwd_views": ([ctypes.POINTER(_VP), ctypes.c_int32, ctypes.POINTER(RdGaussians),
+                                 ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
     "rd_view_stats": ([_VP, ctypes.POINTER(RdStats)], ctypes.c_int),
     "rd_set_profiling": ([_VP, ctypes.c_int32], ctypes.c_int),
     "rd_get_timings": ([_VP, ctypes.POINTER(RdTimings), ctypes.c_int32], ctypes.c_int),

@@ -487,6 +487,56 @@ rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* g
   return RD_OK;
 }
 
+rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g, const rd_grads* grads,
+                                  rd_stream stream) {
+  g_err.clear();
+  if (!views || !g || !grads) return fail(RD_ERR_INVALID_ARGUMENT, "NULL views/gaussians/grads");
+  if (n_views < 1 || n_views > kMaxBatchViews)
+    return fail(RD_ERR_INVALID_ARGUMENT, "n_views must be 1..%d", kMaxBatchViews);
+  if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities || !g->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL Gaussian array");
+  if (g->n > 0 && (!grads->means || !grads->scales || !grads->rotations || !grads->opacities || !grads->sh))
+    return fail(RD_ERR_INVALID_ARGUMENT, "NULL gradient array");
+  if ((((uintptr_t)g->rotations | (uintptr_t)grads->rotations) & 15u) != 0)
+    return fail(RD_ERR_INVALID_ARGUMENT, "rotations / their gradients not 16-byte aligned");
+  if ((g->sh_coeffs * 3) % 4 == 0 && (((uintptr_t)g->sh | (uintptr_t)grads->sh) & 15u) != 0)
+    return fail(RD_ERR_INVALID_ARGUMENT, "sh / its gradient not 16-byte aligned");
+  DevCam cams[kMaxBatchViews];
+  const uint32_t* touched[kMaxBatchViews];
+  const G2D* g2d[kMaxBatchViews];
+  const uint32_t* big[kMaxBatchViews];
+  int64_t n_big[kMaxBatchViews];
+  const uint32_t* vis[kMaxBatchViews];
+  int64_t n_vis[kMaxBatchViews];
+  for (int k = 0; k < n_views; ++k) {
+    const rd_view* v = views[k];
+    if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "views[%d] is NULL", k);
+    if (v->stage < 4) return fail(RD_ERR_STATE, "views[%d]: rd_preprocess_bwd_views before rd_blend_bwd", k);
+    if (g->n != v->n || g->sh_coeffs != v->sh_coeffs)
+      return fail(RD_ERR_INVALID_ARGUMENT, "views[%d]: Gaussians differ from those given to rd_preprocess", k);
+    if (std::memcmp(&v->opt, &views[0]->opt, sizeof(DevOpt)) != 0)
+      return fail(RD_ERR_INVALID_ARGUMENT, "views[%d]: options differ from views[0]'s", k);
+    for (int j = 0; j < k; ++j)
+      if (views[j] == v) return fail(RD_ERR_INVALID_ARGUMENT, "views[%d] repeats views[%d]", k, j);
+    cams[k] = v->cam;
+    touched[k] = (const uint32_t*)v->touched.ptr;
+    g2d[k] = (const G2D*)v->g2d.ptr;
+    big[k] = (const uint32_t*)v->big.ptr;
+    n_big[k] = v->n_big;
+    vis[k] = (const uint32_t*)v->vis.ptr;
+    n_vis[k] = v->n_vis;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
+  DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
+  rd_view* v0 = views[0];
+  v0->begin(s);  // timed on views[0] (K_PREBWD, one launch for the batch)
+  launch_preprocess_bwd_views(dg, v0->opt, n_views, cams, touched, g2d, vis, n_vis, big, n_big, dgr, v0->ctr(), s);
+  RD_CHECK_LAUNCH("preprocess_bwd_views");
+  v0->end(K_PREBWD, s);
+  return RD_OK;
+}
+
 rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
                         const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream) {
   g_err.clear();
@@ -611,6 +661,7 @@ rd_status rd_get_timings(rd_view* v, rd_timings* out, int32_t reset) {
     out->pairs_blended_fwd = (int64_t)h[1];
     out->pairs_evaluated_bwd = (int64_t)h[2];
     out->n_visible = (int64_t)h[3];
+    out->n_visible_union = (int64_t)h[4];
   }
   if (reset) v->reset_acc();
   return RD_OK;

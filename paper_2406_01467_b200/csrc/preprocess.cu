@@ -517,18 +517,39 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam ca
   for (int k = 0; k < 3; ++k) red_add(gr.means + 3 * i + k, dmu[k]);
 }
 
-// K5b: geometry — centre, conic, depth plane and normal back to μ, s, q, o (dmu_extra: the
-// view-direction part of dL/dμ from K5a when fused).
+// One Gaussian's gradient rows (μ, s, raw q, o) summed over the views a K5b launch handles,
+// added to the caller's arrays once by grad_flush.
+struct GradAcc {
+  float dmu[3], ds[3], dq[4], dop;
+};
+__device__ __forceinline__ void grad_zero(GradAcc& a) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) a.dmu[k] = a.ds[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a.dq[k] = 0.f;
+  a.dop = 0.f;
+}
+__device__ __forceinline__ void grad_flush(const GradAcc& a, DevGrads& gr, int64_t i) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    red_add(gr.means + 3 * i + k, a.dmu[k]);
+    red_add(gr.scales + 3 * i + k, a.ds[k]);
+  }
+  red_add4(reinterpret_cast<float4*>(gr.rot) + i, make_float4(a.dq[0], a.dq[1], a.dq[2], a.dq[3]));
+  red_add(gr.opac + i, a.dop);
+}
+
+// K5b: geometry — centre, conic, depth plane and normal of one view back to μ, s, q, o,
+// added to acc; false if the Gaussian is culled in this view.
 template <typename S>
-__device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
-                                                  const G2D* __restrict__ g2d, DevGrads& gr,
-                                                  const float (&dmu_extra)[3]) {
+__device__ __forceinline__ bool geometry_backward(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
+                                                  const G2D* __restrict__ g2d, GradAcc& acc) {
   // the G2D row is needed only after the forward recompute: have it on its way to L2 now
   // (no registers held)
   prefetch_l2(g2d + i);
   prefetch_l2(reinterpret_cast<const char*>(g2d + i) + sizeof(G2D) - 1);
   GF<S> f;
-  if (!gaussian_forward<S>(g, i, cam, opt, f)) return;
+  if (!gaussian_forward<S>(g, i, cam, opt, f)) return false;
   // the G2D sums of K4 → 2-D gradients (log2 e · ln 2 = 1 cancels between the stored
   // (A2, B2, C2) = log2e·(−a/2, −b, −c/2) and α = 2^e):
   //   dL/du = −(a S0 + b S1) + p0 S12, dL/dv = −(b S0 + c S1) + p1 S12,
@@ -686,14 +707,14 @@ __device__ __forceinline__ void geometry_backward(const DevGauss& g, int64_t i, 
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    red_add(gr.means + 3 * i + k, (float)dmu[k] + dmu_extra[k]);
-    red_add(gr.scales + 3 * i + k, (float)ds[k]);
+    acc.dmu[k] += (float)dmu[k];
+    acc.ds[k] += (float)ds[k];
   }
-  red_add4(reinterpret_cast<float4*>(gr.rot) + i,
-           make_float4((float)((dqn[0] - f.qn[0] * qd) * f.qinv), (float)((dqn[1] - f.qn[1] * qd) * f.qinv),
-                       (float)((dqn[2] - f.qn[2] * qd) * f.qinv), (float)((dqn[3] - f.qn[3] * qd) * f.qinv)));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc.dq[k] += (float)((dqn[k] - f.qn[k] * qd) * f.qinv);
   // α = min(α_max, o·G): d_o already excludes the clamp (K4)
-  red_add(gr.opac + i, d_o_raw);
+  acc.dop += d_o_raw;
+  return true;
 }
 
 // K5b, fp32, one thread per entry of the visible list (the ones that are not is_big)
@@ -706,8 +727,9 @@ __global__ void __launch_bounds__(RD_K5_THREADS, RD_K5_MINB) k_preprocess_bwd(De
   if (p < n_vis) {
     const uint32_t i = vis[p];  // over K1's visible list: every thread has work
     if (!is_big(touched[i], opt.tile)) {  // else K5b64's
-      const float zero[3] = {0.f, 0.f, 0.f};
-      geometry_backward<float>(g, i, cam, opt, g2d, gr, zero);
+      GradAcc acc;
+      grad_zero(acc);
+      if (geometry_backward<float>(g, i, cam, opt, g2d, acc)) grad_flush(acc, gr, i);
     }
   }
   // launched as K5b64's programmatic dependent (the two write disjoint rows and overlap):
@@ -722,8 +744,128 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd64(DevGauss g, DevCam cam
   asm volatile("griddepcontrol.launch_dependents;");  // K5b may start now (disjoint rows)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_big) return;
-  const float zero[3] = {0.f, 0.f, 0.f};
-  geometry_backward<double>(g, big[p], cam, opt, g2d, gr, zero);
+  GradAcc acc;
+  grad_zero(acc);
+  if (geometry_backward<double>(g, big[p], cam, opt, g2d, acc)) grad_flush(acc, gr, big[p]);
+}
+
+// ---------------------------------------------------------------------------- K5, B views
+// rd_preprocess_bwd_views: the views of a step share the Gaussians. The SH part of K5 — the
+// HBM-bound one (per view it read each visible Gaussian's 192-B coefficient row and reduced
+// into its 192-B gradient row: ~0.55 GB per C3 view) — runs ONCE for all the views: each
+// Gaussian's row is read once, every view's colour gradient is accumulated on chip, and the
+// gradient row gets one reduction. The geometry part (K5b / K5b64) stays per view: it is
+// latency-bound on its gathers, and its per-(Gaussian, view) thread parallelism beats fusing
+// (measured: a fused geometry pass, one thread looping over the views or lane groups with a
+// shuffle reduction, was 1.5x slower than the per-view kernels).
+struct ViewsBwd {
+  int nv;
+  DevCam cam[kMaxBatchViews];
+  const uint32_t* touched[kMaxBatchViews];
+  const G2D* g2d[kMaxBatchViews];
+};
+
+#ifndef RD_K5AV_MINB
+#define RD_K5AV_MINB 8  // ≤ 128 registers (16 warps per SM): 12 and 10 spilled and measured slower
+#endif
+// K5a over B views: as k_preprocess_bwd_sh_coop, but each warp owns 32 consecutive ids (the
+// SH rows of a warp are one contiguous 6-KB block), copies the rows of the ids visible in any
+// view once, and accumulates every view's SH and view-direction gradients before one
+// reduction per row.
+template <int DEG>
+__global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(DevGauss g, DevOpt opt,
+                                                                const __grid_constant__ ViewsBwd vb, DevGrads gr,
+                                                                Counter* __restrict__ counters) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int NV = 3 * K, NV4 = (NV + 3) / 4, P = NV4 + 1;
+  __shared__ float4 s_coef[2][32 * P];
+  __shared__ float4 s_grad[2][32 * P];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned mask = 0u;
+  if (id < g.n) {
+#pragma unroll 1
+    for (int v = 0; v < vb.nv; ++v) mask |= (vb.touched[v][id] > 0u ? 1u : 0u) << v;
+  }
+  const unsigned vmask = __ballot_sync(0xffffffffu, mask != 0u);
+  if (vmask == 0u) return;  // warp-uniform
+  if (counters && lane == 0) atomicAdd(counters + 4, (Counter)__popc(vmask));
+  const int64_t base = id - lane;
+  const int64_t L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
+  float4* sc = s_coef[warp];
+  float4* sg = s_grad[warp];
+  const float4* sh4 = reinterpret_cast<const float4*>(g.sh);
+  float4* gsh4 = reinterpret_cast<float4*>(gr.sh);
+#pragma unroll
+  for (int it = 0; it < NV4; ++it) {
+    const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
+    if ((vmask >> row) & 1u) cp_async16(&sc[row * P + c], &sh4[(base + row) * L4 + c]);
+  }
+  cp_async_commit();
+#pragma unroll
+  for (int q = 0; q < NV4; ++q) sg[lane * P + q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mu0 = 0.f, mu1 = 0.f, mu2 = 0.f;
+  if (mask) {
+    mu0 = g.means[3 * id];
+    mu1 = g.means[3 * id + 1];
+    mu2 = g.means[3 * id + 2];
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  if (mask) {
+    const float* coef = reinterpret_cast<const float*>(sc + lane * P);  // the row, read from shared memory
+    float dmu[3] = {0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int v = 0; v < vb.nv; ++v) {
+      if (!((mask >> v) & 1u)) continue;
+      const DevCam& cam = vb.cam[v];
+      const G2D* row = vb.g2d[v] + id;
+      const float d_rgb[3] = {row->f[1], row->f[2], row->f[3]};
+      const float ex = mu0 - cam.campos[0], ey = mu1 - cam.campos[1], ez = mu2 - cam.campos[2];
+      const float idl = rsqrtf(ex * ex + ey * ey + ez * ez);
+      const float hx = ex * idl, hy = ey * idl, hz = ez * idl;
+      float Y[16];
+      sh_basis(hx, hy, hz, DEG, Y);
+      float rgb[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) rgb[ch] += Y[k] * coef[k * 3 + ch];
+      float drgb[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) drgb[ch] = rgb[ch] < 0.f ? 0.f : d_rgb[ch];  // clamp: zero grad
+#pragma unroll
+      for (int q = 0; q < NV4; ++q) {
+        float d[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) d[e] = (4 * q + e) < NV ? Y[(4 * q + e) / 3] * drgb[(4 * q + e) % 3] : 0.f;
+        float4 a = sg[lane * P + q];
+        a.x += d[0];
+        a.y += d[1];
+        a.z += d[2];
+        a.w += d[3];
+        sg[lane * P + q] = a;
+      }
+      float c16[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        c16[k] = k < K ? drgb[0] * coef[3 * k] + drgb[1] * coef[3 * k + 1] + drgb[2] * coef[3 * k + 2] : 0.f;
+      float gx, gy, gz;
+      sh_basis_grad(hx, hy, hz, DEG, c16, gx, gy, gz);
+      const float dot = gx * hx + gy * hy + gz * hz;  // through the normalisation of dir
+      dmu[0] += (gx - hx * dot) * idl;
+      dmu[1] += (gy - hy * dot) * idl;
+      dmu[2] += (gz - hz * dot) * idl;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) red_add(gr.means + 3 * id + k, dmu[k]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < NV4; ++it) {
+    const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
+    if ((vmask >> row) & 1u) red_add4(&gsh4[(base + row) * L4 + c], sg[row * P + c]);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_g2d_to_f32(const G2D* __restrict__ g2d, int64_t n, float* __restrict__ out) {
@@ -894,6 +1036,62 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_preprocess_bwd, g, cam, opt, tiles_touched, vis, n_vis, g2d, grads);
+  }
+}
+
+void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, const DevCam* cams,
+                                 const uint32_t* const* touched, const G2D* const* g2d, const uint32_t* const* vis,
+                                 const int64_t* n_vis, const uint32_t* const* big, const int64_t* n_big,
+                                 DevGrads grads, Counter* counters, cudaStream_t s) {
+  if (g.n == 0 || nv <= 0) return;
+  ViewsBwd vb{};
+  vb.nv = nv;
+  for (int v = 0; v < nv; ++v) {
+    vb.cam[v] = cams[v];
+    vb.touched[v] = touched[v];
+    vb.g2d[v] = g2d[v];
+  }
+  if ((g.sh_coeffs * 3) % 4 == 0) {
+    const unsigned cblocks = (unsigned)((g.n + 63) / 64);
+#define RD_K5AV(D) k_preprocess_bwd_sh_views<D><<<cblocks, 64, 0, s>>>(g, opt, vb, grads, counters)
+    switch (opt.sh_degree) {
+      case 0: RD_K5AV(0); break;
+      case 1: RD_K5AV(1); break;
+      case 2: RD_K5AV(2); break;
+      default: RD_K5AV(3); break;
+    }
+#undef RD_K5AV
+  } else {  // rows not 16-B multiples: the per-view SH kernel, once per view
+    const unsigned blocks = (unsigned)((g.n + 127) / 128);
+    for (int v = 0; v < nv; ++v) {
+#define RD_K5A(D) k_preprocess_bwd_sh<D><<<blocks, 128, 0, s>>>(g, cams[v], opt, touched[v], g2d[v], grads)
+      switch (opt.sh_degree) {
+        case 0: RD_K5A(0); break;
+        case 1: RD_K5A(1); break;
+        case 2: RD_K5A(2); break;
+        default: RD_K5A(3); break;
+      }
+#undef RD_K5A
+    }
+  }
+  // geometry per view: its fp64 big list, then the fp32 pass over its visible list as the big
+  // list's programmatic dependent (rows are only ever added by reductions)
+  for (int v = 0; v < nv; ++v) {
+    if (n_big[v] > 0)
+      k_preprocess_bwd64<<<(unsigned)((n_big[v] + 127) / 128), 128, 0, s>>>(g, cams[v], opt, big[v], n_big[v], g2d[v],
+                                                                          grads);
+    if (n_vis[v] > 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)((n_vis[v] + RD_K5_THREADS - 1) / RD_K5_THREADS));
+      cfg.blockDim = dim3(RD_K5_THREADS);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = n_big[v] > 0 ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_preprocess_bwd, g, cams[v], opt, touched[v], vis[v], n_vis[v], g2d[v], grads);
+    }
   }
 }
 

@@ -174,9 +174,10 @@ struct DistIO {
 
 // ------------------------------------------------------------------ launchers (host)
 // Profiling counters (nullable): [0] pairs evaluated by K3, [1] pairs blended by K3,
-// [2] pairs evaluated by K4, [3] visible Gaussians (K1).
+// [2] pairs evaluated by K4, [3] visible Gaussians (K1), [4] Gaussians visible in at least
+// one view of a batched K5 (rd_preprocess_bwd_views).
 typedef unsigned long long Counter;
-constexpr int kNumCounters = 4;
+constexpr int kNumCounters = 5;
 
 __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
   // all 32 lanes must call this (converged)
@@ -196,6 +197,14 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
                            DevGrads grads, cudaStream_t s);
+// K5 for nv ≤ kMaxBatchViews views of the same Gaussians at once (rd_preprocess_bwd_views):
+// per-view cameras, tiles_touched, G2D rows, visible and big lists; gradients += the sum over
+// the views (the SH part fused over the views, the geometry part per view).
+constexpr int kMaxBatchViews = 8;
+void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, const DevCam* cams,
+                                 const uint32_t* const* touched, const G2D* const* g2d, const uint32_t* const* vis,
+                                 const int64_t* n_vis, const uint32_t* const* big, const int64_t* n_big,
+                                 DevGrads grads, Counter* counters, cudaStream_t s);
 // debug: G2D rows → f32 [n][16] (m[0..4], f[0..9], 0)
 void launch_g2d_to_f32(const G2D* g2d, int64_t n, float* out, cudaStream_t s);
 // K2 (binning.cu). Sorts return the CUB DoubleBuffer selector (1: result in the *1 buffers).

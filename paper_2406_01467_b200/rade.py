@@ -369,6 +369,21 @@ def rd_blend_bwd(view: View, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None, dL
                                   _stream_ptr(stream)), "rd_blend_bwd")
 
 
+def rd_preprocess_bwd_views(views, gaussians: Gaussians, grads: Gaussians, stream=None):
+    """K5 of up to 8 views of the same Gaussians in one pass (rows read and reduced once).
+    The caller orders `stream` after every view's rd_blend_bwd."""
+    views = list(views)
+    arr = (_VP_T * len(views))(*[v.handle for v in views])
+    g = gaussians.c_struct()
+    gr = _grads_struct(grads)
+    N.check(N.load().rd_preprocess_bwd_views(arr, len(views), ctypes.byref(g), ctypes.byref(gr), _stream_ptr(stream)),
+            "rd_preprocess_bwd_views")
+    return grads
+
+
+_VP_T = ctypes.c_void_p
+
+
 def rd_preprocess_bwd(view: View, gaussians: Gaussians, grads: Gaussians, stream=None):
     """K5 only: accumulates (+=) parameter gradients from the last rd_blend_bwd of the view."""
     g = gaussians.c_struct()

@@ -301,3 +301,32 @@ def test_c3_guard_band_off_sampled_pixels(c3):
     okd = (ref["flags"] & (F1 | F3 | F4 | F5)) == 0
     assert np.abs(gpu["depth"][ys, xs] - ref["depth"])[okd].max() <= TOL
     assert np.abs(gpu["color"] - c3["gpu"]["color"]).max() > 1e-2
+
+
+def test_c3_batched_k5_equals_per_view_sum(c3):
+    """bench.py's default K5 (rd_preprocess_bwd_views over the 4 views of a step) equals the
+    per-view rd_preprocess_bwd sum at C3 to fp32 rounding, every parameter class."""
+    g, opt = c3["g"], c3["opt"]
+    H, W = c3["cam"].height, c3["cam"].width
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    views = []
+    for cam in c3["cams"][:4]:
+        cot = torch.randn((8, H, W), generator=gen, device="cuda")
+        v = P.View()
+        P.rd_preprocess(v, g, cam, opts_dict(opt))
+        P.rd_bin(v)
+        P.rd_render_fwd(v)
+        P.rd_blend_bwd(v, cot[0:3], cot[3], cot[4:7], cot[7])
+        views.append(v)
+    assert sum(P.rd_view_stats(v)["n_big"] for v in views) > 0
+    ga, gb = g.zeros_like(), g.zeros_like()
+    P.rd_preprocess_bwd_views(views, g, ga)
+    for v in views:
+        P.rd_preprocess_bwd(v, g, gb)
+    torch.cuda.synchronize()
+    a, b = grads_to_rows(ga, g.n), grads_to_rows(gb, g.n)
+    for sl in (slice(0, 3), slice(3, 6), slice(6, 10), slice(10, 11), slice(11, 59)):
+        nb = np.linalg.norm(b[:, sl])
+        assert nb > 0
+        assert np.linalg.norm(a[:, sl] - b[:, sl]) <= 1e-5 * nb, sl

@@ -727,3 +727,86 @@ def test_marching_cubes_of_fused_depth_maps():
     a, b = e2e.reshape(-1, 3), ref.reshape(-1, 3)
     assert cKDTree(b).query(a)[0].max() <= 0.1 * vs
     assert cKDTree(a).query(b)[0].max() <= 0.1 * vs
+
+
+# ----------------------------------------------------------------------------- batched K5
+
+def _views_of(scene, cams, opt, cots):
+    g = P.Gaussians.from_numpy(scene)
+    views = []
+    for cam, cot in zip(cams, cots):
+        view = P.View()
+        P.rd_preprocess(view, g, cam, opts_dict(opt))
+        P.rd_bin(view)
+        P.rd_render_fwd(view)
+        c = {k: torch.as_tensor(v).contiguous().cuda() for k, v in cot.items()}
+        P.rd_blend_bwd(view, c["color"], c["depth"], c["normal"], c["alpha"])
+        views.append(view)
+    return g, views
+
+
+def _orbit_cams(n, W=64, H=64, f=64.0, r=0.8, z=-0.5):
+    cams = []
+    for k in range(n):
+        a = 2 * np.pi * k / n
+        R, t = sg.look_at([r * np.cos(a), r * np.sin(a), z], [0.0, 0.0, 4.0], up=(0, -1, 0))
+        cams.append(sg.Camera(f, f, W / 2, H / 2, W, H, R, t, 0.2))
+    return cams
+
+
+@pytest.mark.parametrize("which", ["dense", "big"])
+def test_batched_k5_matches_oracle_sum_over_views(which):
+    """rd_preprocess_bwd_views over 3 views (each Gaussian's rows read once, the views' chain
+    rules summed on chip) = Σ over views of the oracle's exact gradients (≤ 1e-3 per class,
+    elementwise on every entry) and = the per-view rd_preprocess_bwd sum to fp32 rounding;
+    'big' adds screen-sized splats (their fp64 K5b64 pass runs per view inside the batch)."""
+    if which == "dense":
+        scene, cams = dense_scene(33, 300, zr=(3.0, 6.0)), _orbit_cams(3)
+    else:
+        scene, cam0 = _big_splat_scene(seed=14, W=256)
+        cams = _orbit_cams(3, W=256, H=256, f=256.0, r=0.3, z=0.0)
+    opt = sg.Options(tile=8)
+    cots, R = [], 0.0
+    for k, cam in enumerate(cams):
+        ref = oracle.render(scene, cam, opt)
+        mask = ref["flags"] == 0
+        assert mask.mean() >= 0.99
+        cot = {k_: (v * mask).astype(np.float32) for k_, v in sg.cotangents(40 + k, cam.width, cam.height).items()}
+        cots.append(cot)
+        R = R + oracle.grad(scene, cam, opt, cot, np.arange(scene.n))
+    g, views = _views_of(scene, cams, opt, cots)
+    if which == "big":
+        assert sum(P.rd_view_stats(v)["n_big"] for v in views) > 0
+    gb = g.zeros_like()
+    P.rd_preprocess_bwd_views(views, g, gb)
+    gs = g.zeros_like()
+    for v in views:
+        P.rd_preprocess_bwd(v, g, gs)
+    torch.cuda.synchronize()
+    B, S = grads_to_rows(gb, scene.n), grads_to_rows(gs, scene.n)
+    for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
+                     "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
+        a, b = B[:, sl], R[:, sl]
+        nb = np.linalg.norm(b)
+        assert nb > 0, name
+        assert np.linalg.norm(a - b) / nb <= 1e-3, (name, np.linalg.norm(a - b) / nb)
+        med = np.median(np.abs(b[b != 0]))
+        assert not (np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med).any(), name
+        assert np.linalg.norm(a - S[:, sl]) <= 1e-5 * np.linalg.norm(S[:, sl]), name
+
+
+def test_batched_k5_argument_errors():
+    scene, cams = dense_scene(34, 50), _orbit_cams(2)
+    opt = sg.Options(tile=8)
+    cots = [sg.cotangents(k, 64, 64) for k in range(2)]
+    g, views = _views_of(scene, cams, opt, cots)
+    gr = g.zeros_like()
+    for bad, status in (([views[0], views[0]], 1), ([views[0]] * 9, 1), ([], 1)):
+        with pytest.raises(P.rade.N.RadeError) as e:
+            P.rd_preprocess_bwd_views(bad, g, gr)
+        assert e.value.status == status
+    fresh = P.View()
+    P.rd_preprocess(fresh, g, cams[0], opts_dict(opt))
+    with pytest.raises(P.rade.N.RadeError) as e:
+        P.rd_preprocess_bwd_views([views[0], fresh], g, gr)
+    assert e.value.status == 2
