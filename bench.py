@@ -737,13 +737,17 @@ def run_gpu(args, cfg_name, config):
                 "traffic": traffic, "issue_active_pct": issue, "ncu_capture": capture,
                 "peak_source": (f"{hbm_src} HBM copy (MEASURED_PEAKS.json)" if dk["bound"] == "hbm" else fp32_src),
                 "unit_of_work": ("SURVEY.md §8(d): K3 46 flop / K4 120 flop per alpha-passing (blended) pair, "
-                                 "K1 12 B per Gaussian + 300 B per visible, K5 600 B per visible")}
+                                 "K1 12 B per Gaussian + 300 B per visible, K5 600 B per visible (batched K5: "
+                                 "DESIGN.md §7)")}
 
-    # kernel launches per view (ours + the CUB sort/scan kernels compiled into librade.so):
-    # K1, depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan),
-    # duplicate, tile sort (histogram + exclusive-sum + passes), ranges, K3, K4, K5a + K5b + K5b64
-    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 3
+    # kernel launches (ours + the CUB sort/scan kernels compiled into librade.so): per view K1,
+    # depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan), duplicate,
+    # tile sort (histogram + exclusive-sum + passes), ranges, tile order, K3, K4, K5b + K5b64;
+    # per round of views the batched SH kernel (or K5a per view)
+    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 1 + 2
     views_per_rank = args.steps * B
+    rounds = args.steps * math.ceil(B / P_)
+    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 == "batched" else views_per_rank)
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)
     config.update({
@@ -762,7 +766,7 @@ def run_gpu(args, cfg_name, config):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
-            "roofline": roofline, "kernels": kernels, "gpu_launches": launches_per_view * views_per_rank,
+            "roofline": roofline, "kernels": kernels, "gpu_launches": launches_total,
             "clocks": clk, "e2e": e2e}
 
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -810,3 +810,36 @@ def test_batched_k5_argument_errors():
     with pytest.raises(P.rade.N.RadeError) as e:
         P.rd_preprocess_bwd_views([views[0], fresh], g, gr)
     assert e.value.status == 2
+
+
+def test_view_reuse_depth_sort_capacity():
+    """One rd_view reused across views whose visible counts differ (the visible-only depth sort
+    sizes itself from the view's history): few → many visible (the capacity guess is too
+    small: redone at full size) → few (padding beyond the visible ones). Every render equals a
+    fresh view's bit for bit, binning included."""
+    rng = np.random.default_rng(35)
+    n = 24000
+    z = rng.uniform(2.0, 6.0, n)
+    x = rng.uniform(-0.5, 0.5, n) * z
+    y = rng.uniform(-0.5, 0.5, n) * z
+    sc = sg.make_scene(np.stack([x, y, z]), np.exp(rng.uniform(np.log(0.005), np.log(0.03), (3, n))),
+                       sg.random_quaternions(rng, n), sg.opacity_mixture(rng, n), sg.sh_coeffs(rng, n))
+    g = P.Gaussians.from_numpy(sc)
+    # a camera seeing a corner of the cloud, one seeing all of it, then the corner again
+    near = sg.Camera(64.0, 64.0, 32.0 + 200.0, 32.0 + 200.0, 64, 64, np.eye(3, dtype=np.float32),
+                     np.zeros(3, np.float32), 0.2)
+    full = sg.camera_identity(64, 64, 64.0)
+    opt = opts_dict(sg.Options(tile=8))
+    reused = P.View()
+    counts = []
+    for cam in (near, full, near, full):
+        out_r, _ = P.render(g, cam, opt, view=reused)
+        out_f, fresh = P.render(g, cam, opt)
+        torch.cuda.synchronize()
+        for k in out_r:
+            assert torch.equal(out_r[k], out_f[k]), k
+        kr, ir, rr = P.rd_debug_binning(reused)
+        kf, i_f, rf = P.rd_debug_binning(fresh)
+        assert torch.equal(kr, kf) and torch.equal(ir, i_f) and torch.equal(rr, rf)
+        counts.append(P.rd_view_stats(reused)["n_visible"])
+    assert counts[0] < 4000 < 16000 < counts[1], counts
