@@ -545,9 +545,11 @@ def run_gpu(args, cfg_name, config):
     torch.cuda.synchronize()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record()
-    for _ in range(args.steps):
+    for j in range(args.steps):
         step()
+        marks[j].record()  # step boundary on the main stream (it waited for the step's last K5)
     e1.record()
     torch.cuda.synchronize()
     barrier(dist_on)
@@ -555,6 +557,8 @@ def run_gpu(args, cfg_name, config):
     elapsed_ms = max_over_ranks(e0.elapsed_time(e1), dist_on, device)
     total_views = args.steps * B * ws
     value = total_views / (elapsed_ms / 1e3)
+    step_ms = np.array([e0.elapsed_time(marks[0])] + [marks[j - 1].elapsed_time(marks[j]) for j in range(1, args.steps)])
+    views_covered = len(set((k % len(my_views)) for k in range(args.warmup * B, (args.warmup + args.steps) * B)))
 
     if os.environ.get("RADE_PROF_CONC"):  # diagnostics: per-kernel times under the concurrent schedule
         for sl in slots:
@@ -758,6 +762,11 @@ def run_gpu(args, cfg_name, config):
         "pairs_evaluated_per_px_fwd": tim["pairs_evaluated_fwd"] / max(views_timed, 1) / (H * W),
         "pairs_blended_per_px": tim["pairs_blended_fwd"] / max(views_timed, 1) / (H * W),
         "ms_per_view_by_kernel": {k: tim["ms"][k] / max(views_timed, 1) for k in tim["ms"]},
+        "step_ms": {"median": float(np.median(step_ms)), "mean": float(step_ms.mean()),
+                    "p10": float(np.percentile(step_ms, 10)), "p90": float(np.percentile(step_ms, 90)),
+                    "per_view_median": float(np.median(step_ms)) / B, "per_view_mean": float(step_ms.mean()) / B,
+                    "what": "device time per step (CUDA events on the main stream, this rank), and per view = / B"},
+        "views_covered_per_rank": f"{views_covered} of the rank's {len(my_views)} views in the timed steps",
         "parallelism": f"view-parallel dp{ws}",
         "streams": P_, "host_threads": bool(args.host_threads),
         "allreduce": (f"NCCL sum of the {4 * fg.flat.numel() / 2**20:.0f} MB flat gradient buffer once per step, "
@@ -787,7 +796,7 @@ def run_gpu(args, cfg_name, config):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50, help="timed steps (50 × 4 views = one pass over C3's 200 views)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="rade", choices=["rade", "reference"])
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
