@@ -47,7 +47,7 @@ def main():
     scene, cams, opt = sg.config_scene_and_cameras("C3")
     g = P.Gaussians.from_numpy(scene)
     opts = dict(tile=8, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min, median_T=opt.median_T,
-                dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
+                dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree, guard_band=opt.guard_band)
     view = P.View()
     maps = []
     for cam in cams[:32]:

@@ -20,7 +20,7 @@ def main():
         scene, cams, opt = sg.config_scene_and_cameras(name)
         g = P.Gaussians.from_numpy(scene)
         opts = dict(tile=opt.tile, alpha_min=opt.alpha_min, alpha_max=opt.alpha_max, T_min=opt.T_min,
-                    median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree)
+                    median_T=opt.median_T, dilation=opt.dilation, bg=opt.bg, sh_degree=opt.sh_degree, guard_band=opt.guard_band)
         view = P.View()
         lens = []
         for cam in cams[:: max(1, len(cams) // 8)][:8]:
