@@ -125,6 +125,10 @@ typedef struct rd_grads {
   float* rotations;
   float* opacities;
   float* sh;
+  float* means2d; /* optional (NULL: not produced), [n][2]: dL/d(u_c, v_c), the gradient w.r.t. the
+                     projected centre in pixels with every other per-splat quantity held fixed
+                     (the screen-space gradient 3DGS densification accumulates; PAPER:44 trains
+                     with the 3DGS schedule); += per view, 0 for Gaussians culled in a view */
 } rd_grads;
 
 /* Per-view statistics (host struct filled by rd_view_stats). */

@@ -43,6 +43,7 @@ PG = dict(valid=0, zkey=1, x=slice(2, 5), z=5, tc=6, u=7, v=8, Sigma=slice(9, 18
           qhat=slice(60, 63), q=slice(63, 65), p=slice(65, 67), n=slice(67, 70), rgb=slice(70, 73),
           rgb_clamped=slice(73, 76), o=76, ndotx=77)
 NPARAM = 59
+NDUAL = 61  # + dL/d(u_c, v_c) (or_grad columns 59, 60)
 
 # default ambiguity bands: F1 α-cutoff, F2 α-clamp (|Δ ln α|),
 # F3 T-stop (relative), F4 median crossing (|T′ − median_T|), F5 grazing |n·x̂_c|
@@ -181,10 +182,11 @@ def render(scene, cam, opt, pixels=None, eps=DEFAULT_EPS, timing=None):
                 median_id=mid.reshape(shape), distortion=dist.reshape(shape))
 
 
-def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS, timing=None):
+def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS, timing=None, means2d=False):
     """Exact dL/dθ for the listed Gaussians, L = Σ_px cot·(C, D, N, A[, L_d]) (cot["distortion"]
     optional; ω detached in L_d, S21). Returns [len(gids), 59] (μ 0..2, s 3..5, q 6..9, o 10,
-    sh 11 + coeff*3 + ch)."""
+    sh 11 + coeff*3 + ch); with means2d=True [len(gids), 61], columns 59..60 = dL/d(u_c, v_c)
+    (the projected centre, every other per-splat quantity fixed)."""
     keep, sargs = _scene_args(scene)
     cv, ov = _cam_vec(_cam_f32(cam)), _opt_vec(opt, eps)
     W, H = cam.width, cam.height
@@ -197,10 +199,10 @@ def grad(scene, cam, opt, cot, gids, eps=DEFAULT_EPS, timing=None):
         c[8] = cot["distortion"]
     c = np.ascontiguousarray(c)
     gids = np.ascontiguousarray(gids, np.int64)
-    out = np.zeros((gids.shape[0], NPARAM), np.float64)
+    out = np.zeros((gids.shape[0], NDUAL), np.float64)
     lib().or_grad(*sargs, _dp(cv), _dp(ov), _dp(c), ctypes.c_int64(gids.shape[0]), gids.ctypes.data, _dp(out),
                   None if timing is None else _dp(timing))
-    return out
+    return out if means2d else np.ascontiguousarray(out[:, :NPARAM])
 
 
 def order(scene, cam, opt):

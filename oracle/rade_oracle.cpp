@@ -48,7 +48,10 @@
 
 namespace {
 
-constexpr int NP = 59;  // parameters per Gaussian: μ 3, s 3, q 4, o 1, sh 16*3
+// dual slots per Gaussian: μ 3, s 3, q 4, o 1, sh 16*3 (the 59 parameters), then 2 for an
+// offset of the projected centre (u_c, v_c) — zero-valued inputs whose derivative is the
+// screen-space ("means2d") gradient, the other per-splat quantities held fixed
+constexpr int NP = 61;
 
 // ------------------------------------------------------------------ dual numbers
 struct Dual {
@@ -196,6 +199,8 @@ void load_params(const SceneIn& sc, int64_t i, S P[NP]) {
   P[10] = S(sc.opac[i]);
   for (int k = 0; k < 48; ++k) P[11 + k] = S(0.0);
   for (int k = 0; k < sc.sh_coeffs * 3; ++k) P[11 + k] = S(sc.sh[k * n + i]);
+  P[59] = S(0.0);  // centre offsets (means2d slots)
+  P[60] = S(0.0);
 }
 
 // Contract S7: z_key = fmaf(W20, μx, fmaf(W21, μy, fmaf(W22, μz, t2))) in IEEE fp32.
@@ -248,8 +253,8 @@ bool project(const S P[NP], const double raw[11], const Cam& cam, const Opt& opt
   for (int i = 0; i < 3; ++i) g.x[i] = cam.R[3 * i] * P[0] + cam.R[3 * i + 1] * P[1] + cam.R[3 * i + 2] * P[2] + cam.t[i];
   g.z = g.x[2];
   g.tc = sqrt(g.x[0] * g.x[0] + g.x[1] * g.x[1] + g.x[2] * g.x[2]);
-  g.u = cam.fx * g.x[0] / g.z + cam.cx;
-  g.v = cam.fy * g.x[1] / g.z + cam.cy;
+  g.u = cam.fx * g.x[0] / g.z + cam.cx + P[59];  // + 0: carries d/du_c (means2d)
+  g.v = cam.fy * g.x[1] / g.z + cam.cy + P[60];
 
   // J = ∂(u, v, t)/∂x  (reading S2: t = ‖x‖)
   S z2 = g.z * g.z;
@@ -608,9 +613,11 @@ int or_render(int64_t n, const double* means, const double* scales, const double
 
 /* or_grad: exact gradient of L = Σ_px g·(C, D, N, A, L_d) w.r.t. the 59 parameters of each
  * listed Gaussian, by forward-mode dual numbers through or_render's definition (ω detached
- * in L_d, S21).
+ * in L_d, S21), and w.r.t. its projected centre (u_c, v_c) with every other per-splat
+ * quantity held fixed (the screen-space gradient of 3DGS's densification).
  *   cot[9][H][W] planar: dL/dC (3), dL/dD, dL/dN (3), dL/dA, dL/dL_d.
- *   out[k*59 + j]: j = μ 0..2, s 3..5, q(w,x,y,z) 6..9, o 10, sh 11 + coeff*3 + channel.
+ *   out[k*61 + j]: j = μ 0..2, s 3..5, q(w,x,y,z) 6..9, o 10, sh 11 + coeff*3 + channel,
+ *   59..60 = dL/d(u_c, v_c).
  *   culled Gaussians get zero. */
 int or_grad(int64_t n, const double* means, const double* scales, const double* rot, const double* opac,
             const double* sh, int sh_coeffs, const double* camv, const double* optv, const double* cot,

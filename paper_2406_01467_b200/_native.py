@@ -41,7 +41,7 @@ class RdGaussians(ctypes.Structure):
 
 class RdGrads(ctypes.Structure):
     _fields_ = [("means", ctypes.c_void_p), ("scales", ctypes.c_void_p), ("rotations", ctypes.c_void_p),
-                ("opacities", ctypes.c_void_p), ("sh", ctypes.c_void_p)]
+                ("opacities", ctypes.c_void_p), ("sh", ctypes.c_void_p), ("means2d", ctypes.c_void_p)]
 
 
 class RdTsdf(ctypes.Structure):

@@ -478,7 +478,7 @@ rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* g
     return fail(RD_ERR_INVALID_ARGUMENT, "sh / its gradient not 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
-  DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
+  DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh, grads->means2d};
   v->begin(s);
   launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const uint32_t*)v->vis.ptr, v->n_vis,
                         (const uint32_t*)v->big.ptr, v->n_big, (const G2D*)v->g2d.ptr, dgr, s);
@@ -528,7 +528,7 @@ rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const 
   }
   cudaStream_t s = (cudaStream_t)stream;
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
-  DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh};
+  DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh, grads->means2d};
   rd_view* v0 = views[0];
   v0->begin(s);  // timed on views[0] (K_PREBWD, one launch for the batch)
   launch_preprocess_bwd_views(dg, v0->opt, n_views, cams, touched, g2d, vis, n_vis, big, n_big, dgr, v0->ctr(), s);

@@ -520,14 +520,14 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd_sh(DevGauss g, DevCam ca
 // One Gaussian's gradient rows (μ, s, raw q, o) summed over the views a K5b launch handles,
 // added to the caller's arrays once by grad_flush.
 struct GradAcc {
-  float dmu[3], ds[3], dq[4], dop;
+  float dmu[3], ds[3], dq[4], dop, duv[2];
 };
 __device__ __forceinline__ void grad_zero(GradAcc& a) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) a.dmu[k] = a.ds[k] = 0.f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) a.dq[k] = 0.f;
-  a.dop = 0.f;
+  a.dop = a.duv[0] = a.duv[1] = 0.f;
 }
 __device__ __forceinline__ void grad_flush(const GradAcc& a, DevGrads& gr, int64_t i) {
 #pragma unroll
@@ -537,6 +537,10 @@ __device__ __forceinline__ void grad_flush(const GradAcc& a, DevGrads& gr, int64
   }
   red_add4(reinterpret_cast<float4*>(gr.rot) + i, make_float4(a.dq[0], a.dq[1], a.dq[2], a.dq[3]));
   red_add(gr.opac + i, a.dop);
+  if (gr.means2d) {  // optional screen-space gradient
+    red_add(gr.means2d + 2 * i, a.duv[0]);
+    red_add(gr.means2d + 2 * i + 1, a.duv[1]);
+  }
 }
 
 // K5b: geometry — centre, conic, depth plane and normal of one view back to μ, s, q, o,
@@ -559,6 +563,8 @@ __device__ __forceinline__ bool geometry_backward(const DevGauss& g, int64_t i, 
   const S S12 = q.f[7];
   const S d_u = -(f.ca * S0 + f.cb * S1) + f.p0 * S12;
   const S d_v = -(f.cb * S0 + f.cc * S1) + f.p1 * S12;
+  acc.duv[0] += (float)d_u;  // dL/d(u_c, v_c): the screen-space gradient (rd_grads.means2d)
+  acc.duv[1] += (float)d_v;
   const float d_o = q.f[0] / f.o;
   const S d_n[3] = {q.f[4], q.f[5], q.f[6]};
   const S d_z = S12, d_p0 = q.f[8], d_p1 = q.f[9];

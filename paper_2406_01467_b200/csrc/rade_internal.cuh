@@ -52,6 +52,7 @@ struct DevGrads {
   float* __restrict__ rot;
   float* __restrict__ opac;
   float* __restrict__ sh;
+  float* __restrict__ means2d;  // optional [n][2]: dL/d(u_c, v_c)
 };
 
 // Per-visible-Gaussian record written by K1 and gathered by K3/K4 (64 B, 4 x float4):

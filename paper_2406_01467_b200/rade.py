@@ -55,6 +55,7 @@ class Gaussians:
     opacities: torch.Tensor
     sh: torch.Tensor
     filter3d: Optional[torch.Tensor] = None
+    means2d: Optional[torch.Tensor] = None  # as a gradient holder only: dL/d(u_c, v_c) [N, 2] (optional)
 
     @property
     def n(self):
@@ -85,9 +86,13 @@ class Gaussians:
         return Gaussians(f(scene.means.T), f(scene.scales.T), f(scene.rotations.T), f(scene.opacities),
                          f(scene.sh.transpose(2, 0, 1)))
 
-    def zeros_like(self):
-        return Gaussians(*(torch.zeros_like(t) for t in (self.means, self.scales, self.rotations, self.opacities,
-                                                             self.sh)))
+    def zeros_like(self, means2d: bool = False):
+        """A zeroed gradient holder; means2d=True adds the [N, 2] screen-space gradient."""
+        g = Gaussians(*(torch.zeros_like(t) for t in (self.means, self.scales, self.rotations, self.opacities,
+                                                          self.sh)))
+        if means2d:
+            g.means2d = torch.zeros((self.n, 2), dtype=torch.float32, device=self.means.device)
+        return g
 
     def tensors(self):
         return (self.means, self.scales, self.rotations, self.opacities, self.sh)
@@ -347,8 +352,11 @@ def _grads_struct(grads):
     if grads is None:
         raise ValueError("grads is required")
     grads.validate()
+    if grads.means2d is not None:
+        _check_f32("means2d", grads.means2d, (grads.n, 2))
     return N.RdGrads(grads.means.data_ptr(), grads.scales.data_ptr(), grads.rotations.data_ptr(),
-                     grads.opacities.data_ptr(), grads.sh.data_ptr())
+                     grads.opacities.data_ptr(), grads.sh.data_ptr(),
+                     None if grads.means2d is None else grads.means2d.data_ptr())
 
 
 def rd_render_bwd(view: View, gaussians: Gaussians, dL_dcolor=None, dL_ddepth=None, dL_dnormal=None,

@@ -843,3 +843,31 @@ def test_view_reuse_depth_sort_capacity():
         assert torch.equal(kr, kf) and torch.equal(ir, i_f) and torch.equal(rr, rf)
         counts.append(P.rd_view_stats(reused)["n_visible"])
     assert counts[0] < 4000 < 16000 < counts[1], counts
+
+
+def test_means2d_gradient_parity(case):
+    """rd_grads.means2d (dL/d(u_c, v_c), the screen-space gradient) against the oracle's dual
+    numbers on the projected centre (oracle.grad(..., means2d=True) columns 59..60): ≤ 1e-3
+    relative in norm and elementwise on every entry; the other classes are unchanged by
+    requesting it."""
+    scene, cam, opt, view, g = case["scene"], case["cam"], case["opt"], case["view"], case["g"]
+    ref = case["ref"]
+    mask = ref["flags"] == 0
+    cot = {k: (v * mask).astype(np.float32) for k, v in sg.cotangents(17, cam.width, cam.height).items()}
+    c = {k: torch.as_tensor(v).contiguous().cuda() for k, v in cot.items()}
+    ga, gb = g.zeros_like(means2d=True), g.zeros_like()
+    P.rd_render_bwd(view, g, c["color"], c["depth"], c["normal"], c["alpha"], ga)
+    P.rd_render_bwd(view, g, c["color"], c["depth"], c["normal"], c["alpha"], gb)
+    torch.cuda.synchronize()
+    vis = np.nonzero(oracle.project(scene, cam, opt)[:, 0] == 1)[0]
+    R = oracle.grad(scene, cam, opt, cot, vis, means2d=True)
+    a, b = ga.means2d.double().cpu().numpy()[vis], R[:, 59:61]
+    nb = np.linalg.norm(b)
+    assert nb > 0
+    assert np.linalg.norm(a - b) / nb <= 1e-3, np.linalg.norm(a - b) / nb
+    med = np.median(np.abs(b[b != 0]))
+    assert not (np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med).any()
+    off = np.setdiff1d(np.arange(scene.n), vis)
+    assert np.all(ga.means2d.cpu().numpy()[off] == 0)
+    A, B = grads_to_rows(ga, scene.n), grads_to_rows(gb, scene.n)
+    assert np.linalg.norm(A - B) <= 1e-5 * np.linalg.norm(B)

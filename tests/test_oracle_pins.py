@@ -930,3 +930,33 @@ def test_mc_exact_iso_corners_no_degenerate_triangles(O):
                 cfg = sum(1 << c for c in range(8) if t[k + (c >> 2 & 1), j + (c >> 1 & 1), i + (c & 1)] < 0)
                 n_all += len(table[cfg]) if 0 < cfg < 255 else 0
     assert n_all > tri.shape[0]
+
+
+def test_means2d_gradient_single_splat_closed_form(O):
+    """The oracle's dL/d(u_c, v_c) (dual slots 59..60: the projected centre moved with every
+    other per-splat quantity fixed) for ONE splat and colour + alpha cotangents equals the
+    closed form Σ_px g(px)·∂α/∂u_c with α = o·exp(−½ΔᵀCΔ), Δ = centre − pixel, so
+    ∂α/∂(u_c, v_c) = −α·CΔ (S1, S4) — C and α from the oracle's projection,
+    pixels near the α_min / α_max kinks excluded."""
+    cam = sg.camera_identity(48, 40, 50.0)
+    sc = one_gaussian([0.13, -0.07, 2.5], [0.12, 0.07, 0.2], quat=(0.9, 0.2, -0.3, 0.1), opacity=0.7,
+                      dc=(0.4, -0.1, 0.25))
+    rng = np.random.default_rng(5)
+    cot = {"color": rng.normal(size=(3, 40, 48)), "depth": np.zeros((40, 48)), "normal": np.zeros((3, 40, 48)),
+           "alpha": rng.normal(size=(40, 48))}
+    pg = O.project(sc, cam, OPT)[0]
+    conic = pg[O.PG["conic"]]
+    C = np.array([[conic[0], conic[1]], [conic[1], conic[2]]])
+    rgb = pg[O.PG["rgb"]]
+    uu, vv = np.meshgrid(np.arange(48) + 0.5, np.arange(40) + 0.5)
+    d = np.stack([pg[O.PG["u"]] - uu, pg[O.PG["v"]] - vv], -1)
+    a = float(np.float32(0.7)) * np.exp(-0.5 * np.einsum("hwi,ij,hwj->hw", d, C, d))
+    amin, amax = float(np.float32(1 / 255)), float(np.float32(0.99))
+    ok = (a >= amin * (1 + 1e-4)) & (a < amax)
+    assert (a >= amax).sum() == 0 and ok.sum() > 100
+    g = cot["alpha"] + np.einsum("c,chw->hw", rgb, cot["color"])  # dL/dα per pixel (single splat)
+    dadu = -a[..., None] * np.einsum("ij,hwj->hwi", C, d)
+    exp = np.einsum("hw,hwi->i", np.where(ok, g, 0.0), dadu)
+    cot_m = {k: (v * ok if v.ndim == 2 else v * ok[None]) for k, v in cot.items()}
+    got = O.grad(sc, cam, OPT, cot_m, [0], means2d=True)[0, 59:61]
+    np.testing.assert_allclose(got, exp, rtol=1e-10, atol=1e-12)
