@@ -608,6 +608,8 @@ def run_gpu(args, cfg_name, config):
         for key in ("n_duplicates", "views", "pairs_evaluated_fwd", "pairs_blended_fwd", "pairs_evaluated_bwd",
                     "n_visible", "n_visible_union"):
             tim[key] += t[key]
+        for kname, val in t["n_culled"].items():
+            tim["n_culled"][kname] += val
     for sl, st_ in zip(slots, saved[0]):
         sl["stream"] = st_
     streams["k5"], pool = saved[1], saved[2]
@@ -759,6 +761,7 @@ def run_gpu(args, cfg_name, config):
         "l2": "inputs larger than L2: 354 MB of Gaussian parameters streamed per view (126 MB L2)"
         if n >= 1_000_000 else "small config",
         "M_per_view": M_avg, "visible_per_view": vis_avg, "tiles_per_visible": M_avg / max(vis_avg, 1),
+        "culled_per_view": {k: v / max(views_timed, 1) for k, v in tim["n_culled"].items()},
         "pairs_evaluated_per_px_fwd": tim["pairs_evaluated_fwd"] / max(views_timed, 1) / (H * W),
         "pairs_blended_per_px": tim["pairs_blended_fwd"] / max(views_timed, 1) / (H * W),
         "ms_per_view_by_kernel": {k: tim["ms"][k] / max(views_timed, 1) for k in tim["ms"]},

@@ -160,6 +160,12 @@ typedef struct rd_timings {
   int64_t views;                   /* rd_render_fwd calls since the last reset */
   int64_t n_visible_union;         /* Σ over rd_preprocess_bwd_views calls timed on this view of the
                                       Gaussians visible in at least one of their views */
+  int64_t n_culled[6];             /* Σ over rd_preprocess calls of the Gaussians culled (not an error,
+                                      SPEC:49, 58, 76, 85), by the first reason that applies:
+                                      [0] invalid input (non-finite, scale ≤ 0, zero quaternion),
+                                      [1] centre depth ≤ znear, [2] outside the guard band (S6b),
+                                      [3] opacity < alpha_min, [4] degenerate 2-D covariance or plane,
+                                      [5] footprint entirely off screen */
 } rd_timings;
 
 typedef void* (*rd_alloc_fn)(size_t bytes, void* ctx);

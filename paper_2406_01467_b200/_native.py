@@ -76,7 +76,8 @@ class RdTimings(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * RD_NUM_KERNELS), ("launches", ctypes.c_int64 * RD_NUM_KERNELS),
                 ("pairs_evaluated_fwd", ctypes.c_int64), ("pairs_blended_fwd", ctypes.c_int64),
                 ("pairs_evaluated_bwd", ctypes.c_int64), ("n_visible", ctypes.c_int64),
-                ("n_duplicates", ctypes.c_int64), ("views", ctypes.c_int64), ("n_visible_union", ctypes.c_int64)]
+                ("n_duplicates", ctypes.c_int64), ("views", ctypes.c_int64), ("n_visible_union", ctypes.c_int64),
+                ("n_culled", ctypes.c_int64 * 6)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)

@@ -163,9 +163,14 @@ __device__ __forceinline__ void red_add4(float4* p, float4 v) {
 
 // pf_sh (K1): once the cheap culls pass, prefetch the Gaussian's SH row into L2 so its fetch
 // overlaps the covariance math instead of following it.
+// Cull reasons (rd_timings.n_culled; SPEC:49, 58, 76, 85 — a degenerate primitive is culled,
+// not an error): the first that applies, in this order.
+enum CullWhy { kVisible = 0, kCullInvalid = 1, kCullNear = 2, kCullGuard = 3, kCullOpacity = 4, kCullDegenerate = 5,
+               kCullOffscreen = 6 };
+
 template <typename S>
 __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
-                                                 GF<S>& f, bool pf_sh = false) {
+                                                 GF<S>& f, bool pf_sh = false, int* why = nullptr) {
   // every parameter load is issued before the cull tests, which are combined into one exit:
   // K1 is latency-bound, and loads behind early exits would be four dependent HBM round trips
   f.mu[0] = g.means[3 * i];
@@ -177,26 +182,31 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   f.s[2] = g.scales[3 * i + 2];
   const float4 q4 = reinterpret_cast<const float4*>(g.rot)[i];  // [n][4], 16-B aligned rows
   const float fl = g.filter3d ? g.filter3d[i] : 0.f;
-  bool ok = isfin(f.mu[0]) & isfin(f.mu[1]) & isfin(f.mu[2]);
+  const bool finite_mu = isfin(f.mu[0]) & isfin(f.mu[1]) & isfin(f.mu[2]);
   // centre depth in the fixed fp32 op order of reading S7 (it is also the sort key)
   const float z = __fmaf_rn(cam.R[6], f.mu[0], __fmaf_rn(cam.R[7], f.mu[1], __fmaf_rn(cam.R[8], f.mu[2], cam.t[2])));
-  ok &= z > cam.znear;
+  const bool near_ok = z > cam.znear;
+  bool guard_ok = true;
   if (cam.guard) {  // guard band (reading S6b, optional), decided in fp32 with the oracle's op order
     const float xk = __fmaf_rn(cam.R[0], f.mu[0], __fmaf_rn(cam.R[1], f.mu[1], __fmaf_rn(cam.R[2], f.mu[2], cam.t[0])));
     const float yk = __fmaf_rn(cam.R[3], f.mu[0], __fmaf_rn(cam.R[4], f.mu[1], __fmaf_rn(cam.R[5], f.mu[2], cam.t[1])));
     const float fu = __fmul_rn(cam.fx, xk), fv = __fmul_rn(cam.fy, yk);
-    ok &= (fu >= __fmul_rn(cam.gu0, z)) & (fu <= __fmul_rn(cam.gu1, z)) & (fv >= __fmul_rn(cam.gv0, z)) &
-          (fv <= __fmul_rn(cam.gv1, z));
+    guard_ok = (fu >= __fmul_rn(cam.gu0, z)) & (fu <= __fmul_rn(cam.gu1, z)) & (fv >= __fmul_rn(cam.gv0, z)) &
+               (fv <= __fmul_rn(cam.gv1, z));
   }
   f.zkey = z;
-  ok &= (f.o >= opt.alpha_min) & isfin(f.o);  // o' ≤ o: also culls the filtered one
-  ok &= (f.s[0] > 0.f) & (f.s[1] > 0.f) & (f.s[2] > 0.f) & isfin(f.s[0]) & isfin(f.s[1]) & isfin(f.s[2]);
+  const bool opac_ok = f.o >= opt.alpha_min;  // o' ≤ o: also culls the filtered one
   f.qr[0] = q4.x;
   f.qr[1] = q4.y;
   f.qr[2] = q4.z;
   f.qr[3] = q4.w;
-  ok &= isfin(f.qr[0]) & isfin(f.qr[1]) & isfin(f.qr[2]) & isfin(f.qr[3]);
-  if (!ok) return false;
+  const bool valid = finite_mu & isfin(f.o) & (f.s[0] > 0.f) & (f.s[1] > 0.f) & (f.s[2] > 0.f) & isfin(f.s[0]) &
+                     isfin(f.s[1]) & isfin(f.s[2]) & isfin(f.qr[0]) & isfin(f.qr[1]) & isfin(f.qr[2]) &
+                     isfin(f.qr[3]);
+  if (!(valid & near_ok & guard_ok & opac_ok)) {
+    if (why) *why = !valid ? kCullInvalid : !near_ok ? kCullNear : !guard_ok ? kCullGuard : kCullOpacity;
+    return false;
+  }
   if (pf_sh) {  // the row's first and last byte: its (at most two) 128-B lines
     const float* row = g.sh + i * g.sh_coeffs * 3;
     prefetch_l2(row);
@@ -207,7 +217,10 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   f.s_raw[2] = f.s[2];
   f.o_raw = f.o;
   if (g.filter3d) {  // 3D filter (S23): Σ + f²I ⇔ s' = √(s² + f²); o' = o·Π s/s'
-    if (!isfin(fl)) return false;
+    if (!isfin(fl)) {
+      if (why) *why = kCullInvalid;
+      return false;
+    }
     float ratio = 1.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -216,10 +229,16 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
       f.s[k] = sp;
     }
     f.o *= ratio;
-    if (!(f.o >= opt.alpha_min)) return false;
+    if (!(f.o >= opt.alpha_min)) {
+      if (why) *why = kCullOpacity;
+      return false;
+    }
   }
   const S ql2 = (S)f.qr[0] * f.qr[0] + (S)f.qr[1] * f.qr[1] + (S)f.qr[2] * f.qr[2] + (S)f.qr[3] * f.qr[3];
-  if (!(ql2 > S(0))) return false;
+  if (!(ql2 > S(0))) {
+    if (why) *why = kCullInvalid;  // zero quaternion
+    return false;
+  }
 
   const S R[9] = {cam.R[0], cam.R[1], cam.R[2], cam.R[3], cam.R[4], cam.R[5], cam.R[6], cam.R[7], cam.R[8]};
 #pragma unroll
@@ -262,7 +281,10 @@ __device__ __forceinline__ bool gaussian_project(const DevGauss& g, int64_t i, c
   f.A01 = f.M[0] * f.M[3] + f.M[1] * f.M[4] + f.M[2] * f.M[5];
   f.A11 = f.M[3] * f.M[3] + f.M[4] * f.M[4] + f.M[5] * f.M[5] + (S)opt.dilation;
   f.det = f.A00 * f.A11 - f.A01 * f.A01;
-  if (!(f.det > S(0)) || !isfin(f.det)) return false;
+  if (!(f.det > S(0)) || !isfin(f.det)) {
+    if (why) *why = kCullDegenerate;
+    return false;
+  }
   const S idet = S(1) / f.det;
   f.ca = f.A11 * idet;
   f.cb = -f.A01 * idet;
@@ -320,9 +342,10 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
                                                    const DevOpt& opt, Record* __restrict__ rec,
                                                    uint2* __restrict__ rect, uint32_t* __restrict__ touched,
                                                    uint32_t* __restrict__ dkey, uint32_t& rx0, uint32_t& ry0,
-                                                   uint32_t& rw) {
+                                                   uint32_t& rw, int& why) {
   GF<double> f;
-  if (!gaussian_project<double>(g, i, cam, opt, f, true)) {
+  why = kVisible;
+  if (!gaussian_project<double>(g, i, cam, opt, f, true, &why)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
     return 0u;
@@ -341,6 +364,7 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
   if (!(fx0 <= fx1 && fy0 <= fy1)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
+    why = kCullOffscreen;
     return 0u;
   }
   const int T = opt.tile;
@@ -354,6 +378,7 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
   if (!gaussian_plane<double>(cam, f)) {
     touched[i] = 0u;
     dkey[i] = 0xffffffffu;
+    why = kCullDegenerate;
     return 0u;
   }
 
@@ -421,9 +446,18 @@ __global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(De
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(threadIdx.x & 31);
   uint32_t x0 = 0, y0 = 0, w = 1, nt = 0;
+  int why = kVisible;
   if (i < g.n) {
     didx[i] = (uint32_t)i;
-    nt = preprocess_one<DEG>(g, i, cam, opt, rec, rect, touched, dkey, x0, y0, w);
+    nt = preprocess_one<DEG>(g, i, cam, opt, rec, rect, touched, dkey, x0, y0, w, why);
+  }
+  if (counters) {  // profiling: culls by reason (warp-aggregated)
+#pragma unroll
+    for (int r = kCullInvalid; r <= kCullOffscreen; ++r) {
+      const unsigned m = __ballot_sync(0xffffffffu, i < g.n && why == r);
+      if (lane == 0 && m)
+        atomicAdd(counters + kCullCounter0 + (r - 1) * kCullSlots + (blockIdx.x & (kCullSlots - 1)), (Counter)__popc(m));
+    }
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, nt > 0u);
   if (vmask == 0u) return;  // warp-uniform

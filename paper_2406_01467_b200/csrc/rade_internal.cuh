@@ -176,9 +176,13 @@ struct DistIO {
 // ------------------------------------------------------------------ launchers (host)
 // Profiling counters (nullable): [0] pairs evaluated by K3, [1] pairs blended by K3,
 // [2] pairs evaluated by K4, [3] visible Gaussians (K1), [4] Gaussians visible in at least
-// one view of a batched K5 (rd_preprocess_bwd_views).
+// one view of a batched K5 (rd_preprocess_bwd_views), [5 + 64 r + b] K1's culls by reason r
+// (invalid input, near plane, guard band, opacity < alpha_min, degenerate, off screen),
+// spread over 64 slots b so the atomics of 23 k warps do not all hit one address.
 typedef unsigned long long Counter;
-constexpr int kNumCounters = 5;
+constexpr int kCullCounter0 = 5;
+constexpr int kCullSlots = 64;  // each reason's count spread over 64 addresses (block index mod 64)
+constexpr int kNumCounters = kCullCounter0 + 6 * kCullSlots;
 
 __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
   // all 32 lanes must call this (converged)

@@ -414,7 +414,8 @@ def rd_set_profiling(view: View, enabled: bool = True):
 def rd_get_timings(view: View, reset: bool = False) -> dict:
     t = N.RdTimings()
     N.check(view.lib.rd_get_timings(view.handle, ctypes.byref(t), 1 if reset else 0), "rd_get_timings")
-    d = {k: getattr(t, k) for k, _ in N.RdTimings._fields_ if k not in ("ms", "launches")}
+    d = {k: getattr(t, k) for k, _ in N.RdTimings._fields_ if k not in ("ms", "launches", "n_culled")}
+    d["n_culled"] = dict(zip(("invalid", "near", "guard_band", "opacity", "degenerate", "off_screen"), t.n_culled))
     d["ms"] = {name: t.ms[i] for i, name in enumerate(N.KERNEL_NAMES)}
     d["launches"] = {name: t.launches[i] for i, name in enumerate(N.KERNEL_NAMES)}
     return d

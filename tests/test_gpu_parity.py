@@ -871,3 +871,29 @@ def test_means2d_gradient_parity(case):
     assert np.all(ga.means2d.cpu().numpy()[off] == 0)
     A, B = grads_to_rows(ga, scene.n), grads_to_rows(gb, scene.n)
     assert np.linalg.norm(A - B) <= 1e-5 * np.linalg.norm(B)
+
+
+def test_cull_counters_by_reason():
+    """Per-primitive invalidity is a cull, not an error; the profiling
+    counters (rd_timings.n_culled) attribute each culled Gaussian to the first reason that
+    applies: invalid input, near plane, guard band (S6b), opacity, degenerate, off screen."""
+    cam = sg.camera_identity(40, 24, 40)
+    scene = concat(one_gaussian([0, 0, 3], [0.1, -0.1, 0.1]),                  # invalid: scale ≤ 0
+                   one_gaussian([0, 0, 3], [0.1] * 3, quat=(0, 0, 0, 0)),      # invalid: zero quaternion
+                   one_gaussian([np.nan, 0, 3], [0.1] * 3),                    # invalid: NaN mean
+                   one_gaussian([0, 0, -3], [0.1] * 3),                        # near: behind the camera
+                   one_gaussian([0, 0, 0.1], [0.1] * 3),                       # near: z < znear
+                   one_gaussian([12.0, 0, 3], [0.01] * 3),                     # guard band (u ≈ 180 px)
+                   one_gaussian([0, 0, 3], [0.1] * 3, opacity=1e-3),           # opacity < alpha_min
+                   one_gaussian([0.2, 0.1, 3], [0.1] * 3))                     # visible
+    reasons = ("invalid", "near", "guard_band", "opacity", "degenerate", "off_screen")
+    for gb, exp in ((0.15, (3, 2, 1, 1, 0, 0)), (0.0, (3, 2, 0, 1, 0, 1))):  # band off: off screen instead
+        g = P.Gaussians.from_numpy(scene)
+        view = P.View()
+        P.rd_set_profiling(view, True)
+        P.rd_preprocess(view, g, cam, opts_dict(sg.Options(guard_band=gb)))
+        P.rd_bin(view)
+        P.rd_render_fwd(view)
+        t = P.rd_get_timings(view, reset=True)
+        assert tuple(t["n_culled"][r] for r in reasons) == exp, (gb, t["n_culled"])
+        assert t["n_visible"] == 1
