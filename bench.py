@@ -817,7 +817,7 @@ def main():
     ap.add_argument("--ref-grads", type=int, default=2, help="oracle arm: Gaussians differentiated per step")
     ap.add_argument("--cpu-pixels", type=int, default=2048, help="cpu_baseline: forward pixels sampled")
     ap.add_argument("--cpu-grads", type=int, default=64, help="cpu_baseline: Gaussians differentiated")
-    ap.add_argument("--tile", type=int, default=8, choices=[8, 16], help="blend tile edge (outputs are tile-size independent)")
+    ap.add_argument("--tile", type=int, default=8, choices=[8, 16, 32], help="blend tile edge (outputs are tile-size independent)")
     ap.add_argument("--distortion", action="store_true", help="NEXT-1: also render L_d and back-propagate it")
     ap.add_argument("--normal-consistency", action="store_true",
                     help="NEXT-2: also compute L_n on the maps and back-propagate it")

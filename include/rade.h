@@ -42,7 +42,7 @@
  *
  * Errors: functions never throw; they return an rd_status and set a thread-local message
  * readable with rd_last_error(). Invalid arguments (null pointers, n < 0, width/height ≤ 0,
- * rotations not 16-byte aligned, tile ∉ {8, 16}, thresholds outside (0, 1),
+ * rotations not 16-byte aligned, tile ∉ {8, 16, 32}, thresholds outside (0, 1),
  * alpha_min ≥ alpha_max, sh_degree > 3 or
  * (sh_degree+1)^2 > sh_coeffs) return RD_ERR_INVALID_ARGUMENT; out-of-order calls return
  * RD_ERR_STATE; allocation failure RD_ERR_ALLOC; CUDA launch/runtime errors RD_ERR_CUDA.
@@ -89,7 +89,7 @@ typedef struct rd_camera {
 /* Host struct. Defaults (rd_options_default): tile 16, alpha_min 1/255, alpha_max 0.99,
  * T_min 1e-4, median_T 0.5, dilation 0.3 px², bg (0,0,0), sh_degree 3, guard_band 0 (off). */
 typedef struct rd_options {
-  int32_t tile;      /* 8 or 16 pixels */
+  int32_t tile;      /* 8, 16 or 32 pixels (outputs do not depend on it, reading S8) */
   float alpha_min;   /* splats with α < alpha_min are skipped (S8) */
   float alpha_max;   /* α = min(alpha_max, o·G) (S8) */
   float T_min;       /* stop before blending a splat that would make T < T_min (S8) */

@@ -247,7 +247,8 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   if (!(cam->fx > 0.f && cam->fy > 0.f) || !std::isfinite(cam->fx) || !std::isfinite(cam->fy))
     return fail(RD_ERR_INVALID_ARGUMENT, "fx, fy must be finite and > 0");
   if (!(cam->znear > 0.f)) return fail(RD_ERR_INVALID_ARGUMENT, "znear must be > 0");
-  if (opt->tile != 8 && opt->tile != 16) return fail(RD_ERR_INVALID_ARGUMENT, "tile must be 8 or 16");
+  if (opt->tile != 8 && opt->tile != 16 && opt->tile != 32)
+    return fail(RD_ERR_INVALID_ARGUMENT, "tile must be 8, 16 or 32");
   if (!in01(opt->alpha_min) || !in01(opt->alpha_max) || !in01(opt->T_min) || !in01(opt->median_T))
     return fail(RD_ERR_INVALID_ARGUMENT, "alpha_min, alpha_max, T_min, median_T must lie in (0, 1)");
   if (!(opt->alpha_min < opt->alpha_max)) return fail(RD_ERR_INVALID_ARGUMENT, "alpha_min must be < alpha_max");

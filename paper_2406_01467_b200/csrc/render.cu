@@ -27,6 +27,10 @@
 namespace rade {
 namespace {
 
+// Splats staged per batch: TILE² (one per pixel), capped at 256 for 32×32 tiles so the
+// staged records, warp lists and reduction rows fit the 48-KB static shared memory.
+__host__ __device__ constexpr int batch_of(int tile) { return tile * tile < 256 ? tile * tile : 256; }
+
 struct PixF {  // forward state of one pixel
   float px, py;
   float T, C0, C1, C2, N0, N1, N2, D;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                                                 Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / 2;  // threads
   constexpr int NW = NT / 32;          // warps = 8×8 quadrants
-  constexpr int BATCH = TILE * TILE;   // splats staged per round
+  constexpr int BATCH = batch_of(TILE);  // splats staged per round
   constexpr bool kFilter = TILE > 8;
   constexpr bool kMask = TILE == 8;    // one warp per tile: it records the blend mask for K4
   const int tile = (int)order[blockIdx.x];
@@ -281,10 +285,10 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   for (int base = 0; base < total; base += BATCH) {
     if (__syncthreads_count(pix_done(A) && pix_done(B)) == NT) break;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < (BATCH + NT - 1) / NT; ++h) {
       const int t = (int)threadIdx.x + h * NT;
       const int k = base + t;
-      if (k < total) {
+      if (t < BATCH && k < total) {
         const Record* r = rec + ids[range.x + k];
         s0[t] = r->r0;
         s1[t] = r->r1;
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
     Counter* __restrict__ counters) {
   constexpr int NT = TILE * TILE / PPT;
   constexpr int NW = NT / 32;
-  constexpr int BATCH = TILE * TILE;
+  constexpr int BATCH = batch_of(TILE);
   constexpr int SH = 4 * PPT;  // each warp: an 8-wide, SH-tall pixel rectangle
   constexpr bool kFilter = TILE > 8;
   constexpr bool kMask = TILE == 8;  // one warp per tile: K3's blend mask selects the splats
@@ -575,8 +579,9 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
     }
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < BATCH / NT; ++h) {
+    for (int h = 0; h < (BATCH + NT - 1) / NT; ++h) {
       const int t = (int)threadIdx.x + h * NT;
+      if (t >= BATCH) break;
       if (kMask) {  // stage only the splats some pixel of the tile blends, in list order
         if ((bm >> t) & 1ull) {
           const int slot = __popcll(bm & ((1ull << t) - 1ull));
@@ -696,7 +701,9 @@ void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
   } else {                                            \
     if (counters) RD_K3(T, true, false); else RD_K3(T, false, false); \
   }
-  if (opt.tile == 16) {
+  if (opt.tile == 32) {
+    RD_K3T(32)
+  } else if (opt.tile == 16) {
     RD_K3T(16)
   } else {
     RD_K3T(8)
@@ -712,14 +719,16 @@ void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
                        const uint32_t* bmask, const uint32_t* order, G2D* g2d, Counter* counters,
                        cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
-#define RD_K4(T, D)                                                                                        \
-  k_render_bwd<T, 2, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, \
-                                                   median_pos, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,  \
-                                                   dio, bmask, order, g2d, counters)
-  if (opt.tile == 16) {
-    if (dio.dL_ddist) RD_K4(16, true); else RD_K4(16, false);
+#define RD_K4(T, PPT, D)                                                                                       \
+  k_render_bwd<T, PPT, D><<<grid, T * T / PPT, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, \
+                                                       median_pos, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,  \
+                                                       dio, bmask, order, g2d, counters)
+  if (opt.tile == 32) {  // 4 pixels per thread: 8 warps of 8×16 pixels (the reduction rows fit)
+    if (dio.dL_ddist) RD_K4(32, 4, true); else RD_K4(32, 4, false);
+  } else if (opt.tile == 16) {
+    if (dio.dL_ddist) RD_K4(16, 2, true); else RD_K4(16, 2, false);
   } else {
-    if (dio.dL_ddist) RD_K4(8, true); else RD_K4(8, false);
+    if (dio.dL_ddist) RD_K4(8, 2, true); else RD_K4(8, 2, false);
   }
 #undef RD_K4
 }

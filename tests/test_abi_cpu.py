@@ -110,7 +110,7 @@ def test_argument_validation_without_gpu(native):
     assert lib.rd_preprocess(h, ctypes.byref(g), ctypes.byref(cam), ctypes.byref(opt), None) == 1
     fake = ctypes.c_void_p(16)
     g = native.RdGaussians(5, 16, fake, fake, fake, fake, fake)
-    for field, val in (("tile", 32), ("alpha_min", 0.0), ("alpha_max", 1.5), ("sh_degree", 4), ("T_min", -1.0),
+    for field, val in (("tile", 64), ("tile", 12), ("alpha_min", 0.0), ("alpha_max", 1.5), ("sh_degree", 4), ("T_min", -1.0),
                        ("guard_band", -0.1), ("guard_band", float("inf"))):
         o2 = native.RdOptions()
         lib.rd_options_default(ctypes.byref(o2))

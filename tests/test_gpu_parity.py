@@ -24,6 +24,8 @@ def _scenes():
     cases = [("C0", sg.scene_c0(), sg.camera_c0(), sg.Options()),
              ("dense400", dense_scene(1, 400), sg.camera_identity(64, 64, 64), sg.Options()),
              ("dense400_t8", dense_scene(1, 400), sg.camera_identity(64, 64, 64), sg.Options(tile=8)),
+             ("ragged_t32", dense_scene(2, 300, width=83, height=61, f=70.0), sg.camera_identity(83, 61, 70.0),
+              sg.Options(tile=32, bg=(0.2, 0.5, 1.0))),
              ("ragged", dense_scene(2, 300, width=83, height=61, f=70.0), sg.camera_identity(83, 61, 70.0),
               sg.Options(bg=(0.2, 0.5, 1.0))),
              ("deg1", dense_scene(3, 200), sg.camera_identity(64, 64, 64), sg.Options(sh_degree=1)),
@@ -309,13 +311,18 @@ def test_big_splats_fp64_backward_parity(tile):
 
 
 def test_tile_size_independence():
-    """Outputs are bit-identical for tile 8 and 16 (the per-pixel op sequence does not depend
-    on the tile; reading S8)."""
-    scene, cam = dense_scene(21, 400), sg.camera_identity(64, 64, 64)
-    a, _, _ = gpu_forward(scene, cam, sg.Options(tile=16))
-    b, _, _ = gpu_forward(scene, cam, sg.Options(tile=8))
-    for k in a:
-        np.testing.assert_array_equal(a[k], b[k])
+    """Outputs are bit-identical for tile 8, 16 and 32 (the per-pixel op sequence does not
+    depend on the tile; reading S8), on a ragged image; gradients agree to float-atomic
+    rounding."""
+    scene, cam = dense_scene(21, 400, width=83, height=61, f=70.0), sg.camera_identity(83, 61, 70.0)
+    cot = sg.cotangents(4, 83, 61)
+    outs = {t: gpu_grads(scene, cam, sg.Options(tile=t), cot) for t in (8, 16, 32)}
+    for t in (16, 32):
+        for k in outs[8][0]:
+            np.testing.assert_array_equal(outs[t][0][k], outs[8][0][k], err_msg=f"tile {t} {k}")
+        G, G8 = outs[t][1], outs[8][1]
+        for sl in (slice(0, 3), slice(3, 6), slice(6, 10), slice(10, 11), slice(11, 59)):
+            assert np.linalg.norm(G[:, sl] - G8[:, sl]) <= 1e-5 * np.linalg.norm(G8[:, sl]), (t, sl)
 
 
 def test_forward_determinism_and_backward_close():
