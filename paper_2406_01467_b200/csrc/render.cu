@@ -46,6 +46,36 @@ __device__ __forceinline__ float opaque(float x) {
   return r;
 }
 
+// Blackwell packed FP32 (FFMA2 / FADD2 / FMUL2): a thread's two pixels — rows A and B of one
+// column — as the lo / hi halves of a 64-bit register pair, so their per-pair arithmetic is one
+// instruction per operation instead of two (each half is rounded exactly as the scalar IEEE op:
+// the decisions stay bit-identical to the scalar code and to K4). A scalar operand of a packed
+// op is broadcast by ptxas (`R.F32` operand), so bc() costs nothing.
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2 bc(float x) { return pk(x, x); }
+__device__ __forceinline__ float lo_of(f2 v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float hi_of(f2 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // A saturated (or outside) pixel is marked by py = +inf: pair_power then yields e = −inf or
 // NaN, whose α test fails, so the blend loop needs no separate "done" test per pair.
 __device__ __forceinline__ bool pix_done(const PixF& s) { return s.py == __int_as_float(0x7f800000); }
@@ -260,7 +290,10 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   constexpr int NT = TILE * TILE / 2;  // threads
   constexpr int NW = NT / 32;          // warps = 8×8 quadrants
   constexpr int BATCH = batch_of(TILE);  // splats staged per round
-  constexpr bool kFilter = TILE > 8;
+#ifndef RD_K3_FILTER8
+#define RD_K3_FILTER8 0
+#endif
+  constexpr bool kFilter = TILE > 8 || RD_K3_FILTER8;
   constexpr bool kMask = TILE == 8;    // one warp per tile: it records the blend mask for K4
   const int tile = (int)order[blockIdx.x];
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -282,8 +315,19 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   PixF A, B;
   pixf_init(A, (float)px + 0.5f, (float)pyA + 0.5f, inA);
   pixf_init(B, (float)px + 0.5f, (float)pyB + 0.5f, inB);
+#ifndef RD_K3_PACKED
+#define RD_K3_PACKED 1
+#endif
+  constexpr bool kPacked = RD_K3_PACKED != 0;
+  const float kInf = __int_as_float(0x7f800000);
+  // packed state (rows A | B): −py (−inf once the pixel is done), T, colour, normal, and with
+  // DIST the distortion sums; the scalar PixF keeps px, D, last, med and the counters
+  f2 NPY = pk(-A.py, -B.py), T2 = bc(1.f), C0 = bc(0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0;
+  f2 DD0 = C0, DD1 = C0, DD2 = C0;
+  auto done_A = [&]() { return kPacked ? lo_of(NPY) == -kInf : pix_done(A); };
+  auto done_B = [&]() { return kPacked ? hi_of(NPY) == -kInf : pix_done(B); };
   for (int base = 0; base < total; base += BATCH) {
-    if (__syncthreads_count(pix_done(A) && pix_done(B)) == NT) break;
+    if (__syncthreads_count(done_A() && done_B()) == NT) break;
 #pragma unroll
     for (int h = 0; h < (BATCH + NT - 1) / NT; ++h) {
       const int t = (int)threadIdx.x + h * NT;
@@ -297,7 +341,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       }
     }
     __syncthreads();
-    if (__all_sync(0xffffffffu, pix_done(A) && pix_done(B))) continue;  // this warp is saturated
+    if (__all_sync(0xffffffffu, done_A() && done_B())) continue;  // this warp is saturated
     const int cnt = min(BATCH, total - base);
     // 8×8 tiles: the binning rect is already tight, filtering costs more than it saves
     const int nsel = kFilter ? warp_filter(s0, s1, s3, cnt, lane, fx0, fx0 + 7.f, fy0, fy0 + 7.f,
@@ -313,6 +357,64 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
       const PairColumn col = pair_column(a0, ulo, cpx);  // A and B share the column
+      if constexpr (kPacked) {
+        // pair_power for both rows at once: dy = (v_hi − py) + v_lo, t1 = g21 dy + g11 dx,
+        // t2 = g22 dy, e = log2 o − (t1² + t2²) — the same IEEE ops, per half
+        const f2 DY = add2(add2(bc(a0.y), NPY), bc(ulo.y));
+        const f2 T1 = fma2(bc(a0.w), DY, bc(col.g11dx));
+        const f2 T2s = mul2(bc(a1.x), DY);
+        const f2 E = fma2(fma2(T1, T1, mul2(T2s, T2s)), bc(-1.f), bc(a1.y));
+        const float eA = lo_of(E), eB = hi_of(E);
+        if (PROF) {
+          A.n_eval += done_A() ? 0u : 1u;
+          B.n_eval += done_B() ? 0u : 1u;
+        }
+        const bool okA = eA >= la_min, okB = eB >= la_min;  // α ≥ α_min (S8); false when done
+        if (!__any_sync(0xffffffffu, okA || okB)) continue;  // no pixel of the warp blends it
+        if (kMask && (j & 31) == lane) mine |= 1u + (unsigned)(j >> 5);
+        const float4 a2 = lds128(a + 32u * BATCH);
+        // both rows branch-free: an inactive row gets α = 0 (T, colour, normal unchanged exactly)
+        const float alA = okA ? fminf(opt.alpha_max, ex2_approx(eA)) : 0.f;
+        const float alB = okB ? fminf(opt.alpha_max, ex2_approx(eB)) : 0.f;
+        const f2 TN = mul2(T2, fma2(pk(alA, alB), bc(-1.f), bc(1.f)));  // T·(1 − α)
+        const float TnA = lo_of(TN), TnB = hi_of(TN), TA = lo_of(T2), TB = hi_of(T2);
+        const bool stA = okA && TnA < opt.T_min, stB = okB && TnB < opt.T_min;  // stop before it (S8)
+        const bool bA = okA && !stA, bB = okB && !stB;
+        const f2 W = mul2(pk(bA ? alA : 0.f, bB ? alB : 0.f), T2);  // w = α T
+        C0 = fma2(W, bc(a1.z), C0);
+        C1 = fma2(W, bc(a1.w), C1);
+        C2 = fma2(W, bc(a2.x), C2);
+        N0 = fma2(W, bc(a2.y), N0);
+        N1 = fma2(W, bc(a2.z), N1);
+        N2 = fma2(W, bc(a2.w), N2);
+        const int pos = base + j;
+        const bool mA = bA && TA > opt.median_T && TnA <= opt.median_T;  // the median splat (S9)
+        const bool mB = bB && TB > opt.median_T && TnB <= opt.median_T;
+        if (DIST || __any_sync(0xffffffffu, mA || mB)) {
+          const float4 a3 = lds128(a + 48u * BATCH);  // (z_c, p0, p1, ·)
+          const float dA = __fmaf_rn(a3.y, col.dx, __fmaf_rn(a3.z, lo_of(DY), a3.x));
+          const float dB = __fmaf_rn(a3.y, col.dx, __fmaf_rn(a3.z, hi_of(DY), a3.x));
+          if (mA) { A.D = dA; A.med = pos; }
+          if (mB) { B.D = dB; B.med = pos; }
+          if (DIST) {  // Σω(d − d0), Σω(d − d0)², d0 = the first blended depth (S21)
+            DD0 = pk(bA && A.last == 0 ? dA : lo_of(DD0), bB && B.last == 0 ? dB : hi_of(DD0));
+            const f2 Ed = pk(bA ? dA - lo_of(DD0) : 0.f, bB ? dB - hi_of(DD0) : 0.f);
+            DD1 = fma2(W, Ed, DD1);
+            DD2 = fma2(mul2(W, Ed), Ed, DD2);
+          }
+        }
+        T2 = pk(bA ? TnA : TA, bB ? TnB : TB);
+        NPY = pk(stA ? -kInf : lo_of(NPY), stB ? -kInf : hi_of(NPY));
+        if (bA) A.last = pos + 1;
+        if (bB) B.last = pos + 1;
+        if (PROF) {
+          A.n_blend += bA ? 1u : 0u;
+          B.n_blend += bB ? 1u : 0u;
+        }
+        // a pixel can only saturate in a step that blends: test for the whole warp only then
+        if (__all_sync(0xffffffffu, done_A() && done_B())) break;
+        continue;
+      }
       const PairAlpha pA = pair_power(a0, a1.x, a1.y, ulo, col, A.py, la_min);
       const PairAlpha pB = pair_power(a0, a1.x, a1.y, ulo, col, B.py, la_min);
       if (PROF) {
@@ -342,6 +444,12 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   if (PROF) {
     warp_count(counters + 0, A.n_eval + B.n_eval);
     warp_count(counters + 1, A.n_blend + B.n_blend);
+  }
+  if constexpr (kPacked) {  // back to the per-pixel records for the store
+    A.T = lo_of(T2); B.T = hi_of(T2);
+    A.C0 = lo_of(C0); B.C0 = hi_of(C0); A.C1 = lo_of(C1); B.C1 = hi_of(C1); A.C2 = lo_of(C2); B.C2 = hi_of(C2);
+    A.N0 = lo_of(N0); B.N0 = hi_of(N0); A.N1 = lo_of(N1); B.N1 = hi_of(N1); A.N2 = lo_of(N2); B.N2 = hi_of(N2);
+    A.d0 = lo_of(DD0); B.d0 = hi_of(DD0); A.D1 = lo_of(DD1); B.D1 = hi_of(DD1); A.D2 = lo_of(DD2); B.D2 = hi_of(DD2);
   }
   const int HW = cam.W * cam.H;
   fwd_store<DIST>(A, inA, pyA * cam.W + px, HW, opt, color, depth, normal, alpha_out, T_final, n_contrib,
