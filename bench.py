@@ -461,6 +461,8 @@ def run_gpu(args, cfg_name, config):
             if io:
                 io["fwd_done"].record(st)  # every map plane of the view is written
                 st.wait_event(io["cot_ready"])
+                if io.get("loss_fn") is not None:  # e2e loss mode: cotangents from the loss on device
+                    cot = io["loss_fn"](o)
             if args.normal_consistency:  # its cotangents join the maps'
                 ct = slot["cot"]
                 ct.copy_(cot)
@@ -614,9 +616,83 @@ def run_gpu(args, cfg_name, config):
         sl["stream"] = st_
     streams["k5"], pool = saved[1], saved[2]
 
-    # ---------------- end-to-end: host cotangents in (pinned), rendered maps out, per step
+    # ---------------- end-to-end: per step, inputs from pinned host memory in, result out.
+    # loss mode (default): a view's input is its ground-truth RGB image (uint8, the training
+    # data), the user-side loss (L1 colour, plus the regularisers' weights when enabled) and its
+    # cotangents are computed on the device with torch ops, and the step's result read back is
+    # the loss (4 B per view). maps mode: 8-channel fp32 cotangent images in, the rendered map
+    # planes out (a loss computed on the host; PCIe-bound).
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.e2e_mode == "loss":
+        gen_gt = torch.Generator()
+        gen_gt.manual_seed(SEED_COT + 7 + rank)
+        host_gts = [torch.randint(0, 256, (3, H, W), generator=gen_gt, dtype=torch.uint8).pin_memory()
+                    for _ in range(n_ring)]
+        dev_gts = [torch.empty((3, H, W), dtype=torch.uint8, device=device) for _ in slots]
+        host_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in slots]
+        dev_loss = [torch.zeros(1, dtype=torch.float32, device=device) for _ in slots]
+        cot_bufs = [torch.zeros((10, H, W), device=device) for _ in slots]
+        cins = [torch.cuda.Stream(device) for _ in slots]
+        couts = [torch.cuda.Stream(device) for _ in slots]
+        ios = [{k: torch.cuda.Event() for k in ("cot_ready", "k4_done", "fwd_done", "outs_free", "loss_done")}
+               for _ in slots]
+        lam_d, lam_n = 100.0 / (H * W), 0.05 / (H * W)  # regulariser weights (RaDe-GS-like magnitudes)
+        h2d = d2h = 0
+        io_lock = threading.Lock()
+
+        def make_loss_fn(i):
+            def loss_fn(o):
+                cb = cot_bufs[i]
+                diff = o["color"] - dev_gts[i].float() * (1.0 / 255.0)
+                dev_loss[i].copy_(diff.abs().mean().reshape(1))
+                torch.sign(diff, out=cb[0:3])
+                cb[0:3].mul_(1.0 / (3 * H * W))
+                if args.distortion:
+                    cb[8].fill_(lam_d)
+                if args.normal_consistency:
+                    cb[9].fill_(lam_n)
+                ios[i]["loss_done"].record(torch.cuda.current_stream(device))
+                return cb
+            return loss_fn
+
+        for i in range(len(slots)):
+            ios[i]["loss_fn"] = make_loss_fn(i)
+
+        def per_view_loss(sl, k):
+            nonlocal h2d, d2h
+            i = slots.index(sl)
+            io = ios[i]
+            with torch.cuda.stream(cins[i]):
+                cins[i].wait_event(io["k4_done"])  # the slot's previous loss has read the image
+                dev_gts[i].copy_(host_gts[k % n_ring], non_blocking=True)
+                io["cot_ready"].record(cins[i])
+            one_view(sl, my_views[k % len(my_views)], None, io)
+            with torch.cuda.stream(couts[i]):
+                couts[i].wait_event(io["loss_done"])
+                host_loss[i].copy_(dev_loss[i], non_blocking=True)
+                io["outs_free"].record(couts[i])
+            with io_lock:
+                h2d += dev_gts[i].numel()
+                d2h += 4
+
+        steps_e2e = max(1, args.steps)
+        run_views(per_view_loss)
+        torch.cuda.synchronize()
+        h2d = d2h = 0
+        barrier(dist_on)
+        t0 = time.perf_counter()
+        for _ in range(steps_e2e):
+            run_views(per_view_loss)
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, dist_on, device)
+        e2e = {"value": steps_e2e * B * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // steps_e2e,
+               "d2h_bytes_per_step": d2h // steps_e2e, "mode": "loss",
+               "what": "per view: H2D of the view's ground-truth RGB image (uint8) from pinned host memory, the "
+                       "ABI calls, the user-side L1 colour loss and its cotangent on the device (torch), D2H of the "
+                       "loss; batched K5 per round; Gaussians and gradients stay resident (model state); host wall "
+                       "clock, max over ranks",
+               "last_loss": float(host_loss[0].item())}
+    if not args.no_e2e and args.e2e_mode == "maps":
         nch = 10 if args.normal_consistency else 9 if args.distortion else 8  # cotangent channels consumed
         host_cots = [c[:nch].cpu().pin_memory() for c in cots]
         h2d = 0
@@ -696,7 +772,7 @@ def run_gpu(args, cfg_name, config):
                      for k, v in r.items()} for r in tl]
             json.dump(rows, open(tl_path, "w"), indent=0)
         e2e = {"value": steps_e2e * B * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // steps_e2e,
-               "d2h_bytes_per_step": d2h // steps_e2e,
+               "d2h_bytes_per_step": d2h // steps_e2e, "mode": "maps",
                "what": "per view: H2D of the view's cotangent image (8 channels, 9 with --distortion, 10 with "
                        "--normal-consistency) from pinned host memory, the five C-ABI calls, one D2H of the rendered "
                        "map planes, on the view's own copy streams overlapped with the other views' compute; "
@@ -826,6 +902,8 @@ def main():
     ap.add_argument("--single-host-thread", dest="host_threads", action="store_false",
                     help="issue every view from the main thread (default: one host thread per stream)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-mode", default="loss", choices=["loss", "maps"],
+                    help="e2e inputs/outputs: GT images in + loss out (default), or cotangent images in + maps out")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
