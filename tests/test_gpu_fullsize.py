@@ -330,3 +330,93 @@ def test_c3_batched_k5_equals_per_view_sum(c3):
         nb = np.linalg.norm(b[:, sl])
         assert nb > 0
         assert np.linalg.norm(a[:, sl] - b[:, sl]) <= 1e-5 * nb, sl
+
+
+def _sampled_grad_check(scene, cam, opt, g, view, cot, rng, groups, label):
+    """GPU gradients of the sampled Gaussians (per footprint group) vs the oracle's exact dual
+    numbers over the full frame; ≤ 1e-3 relative per parameter class."""
+    c = {k: torch.as_tensor(v).cuda().contiguous() for k, v in cot.items() if k != "distortion"}
+    grads = g.zeros_like()
+    if "distortion" in cot:
+        P.rd_blend_bwd_ex(view, c["color"], c["depth"], c["normal"], c["alpha"],
+                          torch.as_tensor(cot["distortion"]).cuda().contiguous())
+        P.rd_preprocess_bwd(view, g, grads)
+    else:
+        P.rd_render_bwd(view, g, c["color"], c["depth"], c["normal"], c["alpha"], grads)
+    torch.cuda.synchronize()
+    G = grads_to_rows(grads, g.n)
+    _, _, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(view))
+    t64 = touched.astype(np.int64)
+    for gname, (lo, hi, k) in groups.items():
+        ids = np.nonzero((t64 >= lo) & (t64 <= hi))[0]
+        cand = ids[np.argsort(-np.abs(G[ids, 10]))[:200]]
+        gids = rng.choice(cand, k, replace=False)
+        R = oracle.grad(scene, cam, opt, {k_: v.astype(np.float64) for k_, v in cot.items()}, gids)
+        for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
+                         "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
+            nb = np.linalg.norm(R[:, sl])
+            assert nb > 0, (label, gname, name)
+            rel = np.linalg.norm(G[gids, sl] - R[:, sl]) / nb
+            assert rel <= 1e-3, (label, gname, name, rel)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4"])
+def test_other_configs_sampled_gradients(cfg):
+    """Gradients at the other BASELINE.json configurations (full size, bench tile): small
+    and medium Gaussians sampled among the contributing ones vs the oracle."""
+    scene, cams, opt = sg.config_scene_and_cameras(cfg)
+    opt.tile = BENCH_TILE
+    cam = cams[0]
+    g = P.Gaussians.from_numpy(scene)
+    _, view = P.render(g, cam, opts_dict(opt))
+    rng = np.random.default_rng(31)
+    H, W = cam.height, cam.width
+    cot = {"color": rng.normal(size=(3, H, W)).astype(np.float32), "depth": rng.normal(size=(H, W)).astype(np.float32),
+           "normal": rng.normal(size=(3, H, W)).astype(np.float32), "alpha": rng.normal(size=(H, W)).astype(np.float32)}
+    _sampled_grad_check(scene, cam, opt, g, view, cot, rng, {"small": (1, 4, 3), "medium": (16, 64, 2)}, cfg)
+
+
+def test_c3_distortion_sampled_gradients(c3):
+    """NEXT-1 at full size: gradients of Σ g·(C, D, N, A, L_d) (ω detached in L_d, S21) of
+    sampled C3 Gaussians vs the oracle."""
+    scene, cam, opt, g = c3["scene"], c3["cam"], c3["opt"], c3["g"]
+    view = P.View()
+    P.rd_preprocess(view, g, cam, opts_dict(opt))
+    P.rd_bin(view)
+    P.rd_render_fwd_ex(view, distortion=True)
+    rng = np.random.default_rng(32)
+    H, W = cam.height, cam.width
+    cot = {"color": rng.normal(size=(3, H, W)).astype(np.float32), "depth": rng.normal(size=(H, W)).astype(np.float32),
+           "normal": rng.normal(size=(3, H, W)).astype(np.float32), "alpha": rng.normal(size=(H, W)).astype(np.float32),
+           "distortion": (10.0 * rng.normal(size=(H, W))).astype(np.float32)}
+    _sampled_grad_check(scene, cam, opt, g, view, cot, rng, {"small": (1, 4, 3), "medium": (16, 64, 2)}, "C3+L_d")
+
+
+def test_c3_normal_consistency_crop(c3):
+    """NEXT-2 at full size: L_n and ñ of the C3 maps (GPU kernel on the full 1237×822 maps) vs
+    the oracle's numpy definition on a 96×96 crop of the same maps (interior pixels; stencils
+    of ambiguous orientation excluded as in the small-case test)."""
+    gpu = c3["gpu"]
+    cam = c3["cam"]
+    dev = torch.device("cuda")
+    t = {k: torch.as_tensor(np.asarray(gpu[k], np.float32)).contiguous().to(dev) for k in ("depth", "alpha", "normal")}
+    L, nt = P.rd_normal_consistency(cam, t["depth"], t["alpha"], t["normal"], consistency=True, depth_normal=True)
+    torch.cuda.synchronize()
+    y0, x0, S = 360, 560, 96
+    crop = lambda a: a[..., y0:y0 + S + 1, x0:x0 + S + 1].astype(np.float32).astype(np.float64)
+    import copy
+    cc = copy.copy(cam)
+    cc.cx, cc.cy, cc.width, cc.height = cam.cx - x0, cam.cy - y0, S + 1, S + 1
+    Lr, ntr = oracle.normal_consistency(crop(gpu["depth"]), crop(gpu["alpha"]), crop(gpu["normal"]), cc)
+    Lg = L.cpu().numpy()[y0:y0 + S, x0:x0 + S]
+    ng = nt.cpu().numpy()[:, y0:y0 + S, x0:x0 + S]
+    Lr, ntr = Lr[:S, :S], ntr[:, :S, :S]
+    xs = (np.arange(S) + 0.5 - cc.cx) / cam.fx
+    ys = (np.arange(S) + 0.5 - cc.cy) / cam.fy
+    ray = np.stack([np.broadcast_to(xs[None, :], (S, S)), np.broadcast_to(ys[:, None], (S, S)), np.ones((S, S))], 0)
+    cosang = np.abs(np.sum(ntr * ray, 0)) / np.linalg.norm(ray, axis=0)
+    valid = np.any(ntr != 0, 0)
+    ok = ~valid | (cosang > 1e-3)
+    assert valid.sum() > 1000
+    np.testing.assert_allclose(ng[:, ok], ntr[:, ok], atol=1e-4)
+    np.testing.assert_allclose(Lg[ok], Lr[ok], atol=1e-4)
