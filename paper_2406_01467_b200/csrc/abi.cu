@@ -76,13 +76,16 @@ struct rd_view {
   int key_bits = 0;   // 32 + tile_bits: the equivalent one-pass 64-bit key width
   int tile_bits = 0;
   int64_t M = 0;
-  int dsel = 0, tsel = 0;  // CUB DoubleBuffer selectors of the depth and tile sorts
+  int tsel = 0;  // buffer (0/1) holding the sorted tile keys and ids
   int64_t n_vis = 0, n_big = 0;
   bool g2d_dirty = false;  // the G2D rows hold a previous rd_blend_bwd's sums (K1 zeroes them)
   bool dist_fwd = false;   // the last forward produced the distortion map and its K4 state
   Buf dist_d0, dist_D1;
-  uint32_t* host_M = nullptr;  // pinned: [0] M, [1] visible Gaussians, [2] big ones
-  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, tmp, vis, big, nvis;
+  uint32_t* host_M = nullptr;  // mapped pinned: [0] visible, [1] big, [2] M, written by K2h
+  uint32_t* host_M_dev = nullptr;  // its device alias
+  cudaEvent_t m_ready = nullptr;  // recorded after K2h, waited on by rd_bin (the path's one sync)
+  BinSort bs{nullptr, 0u};  // K2's look-back state (binning.cu)
+  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, vis, big, bincnt, status, bstart;
   Buf tkeys0, tkeys1, vals0, vals1;
   Buf ranges;
   Buf T_final, n_contrib, median_pos;
@@ -182,6 +185,18 @@ struct rd_view {
     if (st_ != RD_OK) return st_;             \
   } while (0)
 
+// K2's look-back status words for up to n_items per pass; zeroed when (re)allocated (every
+// later pass tags its words with a fresh epoch, so they are never cleared again)
+#define RD_ENSURE_STATUS(v, n_items, s)                                                   \
+  do {                                                                                   \
+    const size_t bytes_ = bin_status_words(n_items) * sizeof(unsigned long long);        \
+    if ((v)->status.cap < bytes_) {                                                       \
+      RD_ENSURE((v)->status, bytes_, s);                                                  \
+      RD_CUDA(cudaMemsetAsync((v)->status.ptr, 0, (v)->status.cap, s));                   \
+      (v)->bs.status = (unsigned long long*)(v)->status.ptr;                              \
+    }                                                                                    \
+  } while (0)
+
 extern "C" {
 
 const char* rd_last_error(void) { return g_err.c_str(); }
@@ -219,13 +234,14 @@ rd_status rd_view_create(rd_view** view, rd_alloc_fn alloc, rd_free_fn free_fn, 
 rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
-                &v->didx1,  &v->tmp,    &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->bmask, &v->tile_order, &v->vis, &v->big, &v->nvis, &v->dist_d0, &v->dist_D1};
+                &v->didx1,  &v->status, &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->bmask, &v->tile_order, &v->vis, &v->big, &v->bincnt, &v->bstart, &v->dist_d0, &v->dist_D1};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
   for (Buf* b : all) v->release(*b, v->last_stream);
   if (v->host_M) cudaFreeHost(v->host_M);
+  if (v->m_ready) cudaEventDestroy(v->m_ready);
   delete v;
   return RD_OK;
 }
@@ -263,7 +279,8 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
                 opt->sh_degree);
   const int tiles_x = (cam->width + opt->tile - 1) / opt->tile;
   const int tiles_y = (cam->height + opt->tile - 1) / opt->tile;
-  if (tiles_x > 65535 || tiles_y > 65535) return fail(RD_ERR_INVALID_ARGUMENT, "image too large");
+  if (tiles_x > bin_max_tiles_per_axis() || tiles_y > bin_max_tiles_per_axis())
+    return fail(RD_ERR_INVALID_ARGUMENT, "image too large: more than %d tiles per axis", bin_max_tiles_per_axis());
 
   cudaStream_t s = (cudaStream_t)stream;
   v->n = g->n;
@@ -311,15 +328,21 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   RD_ENSURE(v->didx1, n * sizeof(uint32_t), s);
   RD_ENSURE(v->vis, n * sizeof(uint32_t), s);
   RD_ENSURE(v->big, n * sizeof(uint32_t), s);
-  RD_ENSURE(v->nvis, 2 * sizeof(uint32_t), s);
+  const size_t cnt_words = (size_t)kBinCntDiff + (size_t)(tiles_x + 1) + (size_t)(tiles_y + 1) + (size_t)bin_bases_words();
+  RD_ENSURE(v->bincnt, cnt_words * sizeof(uint32_t), s);
   RD_ENSURE(v->g2d, n * sizeof(G2D), s);
+  if (!v->host_M) {
+    RD_CUDA(cudaHostAlloc((void**)&v->host_M, 4 * sizeof(uint32_t), cudaHostAllocMapped));
+    RD_CUDA(cudaHostGetDevicePointer((void**)&v->host_M_dev, v->host_M, 0));
+  }
+  if (!v->m_ready) RD_CUDA(cudaEventCreateWithFlags(&v->m_ready, cudaEventDisableTiming));
 
   DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
-  v->begin(s);  // K1 timing includes the zeroing of the list counters
-  RD_CUDA(cudaMemsetAsync(v->nvis.ptr, 0, 2 * sizeof(uint32_t), s));
+  v->begin(s);  // K1 timing includes the zeroing of its counters
+  RD_CUDA(cudaMemsetAsync(v->bincnt.ptr, 0, kBinCntHist * sizeof(uint32_t), s));
   launch_preprocess_fwd(dg, c, o, tiles_x, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
-                        (uint32_t*)v->dkey0.ptr, (uint32_t*)v->didx0.ptr, (uint32_t*)v->nvis.ptr,
-                        (uint32_t*)v->vis.ptr, (uint32_t*)v->big.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
+                        (uint32_t*)v->dkey0.ptr, (uint32_t*)v->bincnt.ptr, (uint32_t*)v->vis.ptr,
+                        (uint32_t*)v->big.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
   RD_CHECK_LAUNCH("preprocess_fwd");
   v->end(K_PRE, s);
   v->stage = 1;
@@ -336,50 +359,64 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = v->n;
   const int n_tiles = v->tiles_x * v->tiles_y;
+  uint32_t* cnt = (uint32_t*)v->bincnt.ptr;
+  uint32_t* hist = cnt + kBinCntHist;
+  int* diff_x = (int*)(cnt + kBinCntDiff);
+  int* diff_y = diff_x + (v->tiles_x + 1);
+  uint32_t* bases = (uint32_t*)(diff_y + (v->tiles_y + 1));
+  uint32_t* const dk[2] = {(uint32_t*)v->dkey0.ptr, (uint32_t*)v->dkey1.ptr};
+  uint32_t* const di[2] = {(uint32_t*)v->didx0.ptr, (uint32_t*)v->didx1.ptr};
+  const uint32_t* sorted_ids = di[0];  // depth pass 3 writes buffer 0
   int64_t M = 0;
-  v->dsel = v->tsel = 0;
-  const uint32_t* sorted_ids = (const uint32_t*)v->didx0.ptr;
   if (n > 0) {
-    const size_t tb = binning_temp_bytes(n, 0, v->tile_bits);
-    RD_ENSURE(v->tmp, tb, s);
-    if (!v->host_M) RD_CUDA(cudaMallocHost(&v->host_M, 3 * sizeof(uint32_t)));
-    v->begin(s);
-    v->dsel = launch_depth_sort((uint32_t*)v->dkey0.ptr, (uint32_t*)v->dkey1.ptr, (uint32_t*)v->didx0.ptr,
-                                (uint32_t*)v->didx1.ptr, n, v->tmp.ptr, v->tmp.cap, s);
-    RD_CHECK_LAUNCH("depth_sort");
+    // K2h and the depth passes are sized on the device (K1's visible count), so they are queued
+    // before the host waits for the counts K2h writes (the one sync of the path)
+    RD_ENSURE_STATUS(v, n, s);
+    v->begin(s);  // the depth sort's time includes K2h and the zeroing of its histograms
+    RD_CUDA(cudaMemsetAsync(hist, 0, (kBinCntDiff - kBinCntHist + v->tiles_x + v->tiles_y + 2) * sizeof(uint32_t), s));
+    launch_bin_hist(n, dk[0], (const uint2*)v->rect.ptr, v->tiles_x, v->tiles_y, cnt, bases, v->host_M_dev, s);
+    RD_CHECK_LAUNCH("bin_hist");
+    RD_CUDA(cudaEventRecord(v->m_ready, s));  // K2h has written the counts to host_M
+    for (int p = 0; p < 4; ++p) {
+      launch_depth_pass(p, dk[0], n, cnt, bases, dk, di, v->bs, s);
+      RD_CHECK_LAUNCH("depth_sort");
+    }
     v->end(K_DSORT, s);
-    sorted_ids = (const uint32_t*)(v->dsel ? v->didx1.ptr : v->didx0.ptr);
+    RD_CUDA(cudaEventSynchronize(v->m_ready));
+    v->n_vis = (int64_t)v->host_M[0];
+    v->n_big = (int64_t)v->host_M[1];
+    M = (int64_t)v->host_M[2];
+    if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
+    RD_ENSURE(v->bstart, bin_bstart_words(M) * sizeof(uint32_t), s);
     v->begin(s);
-    launch_scan(sorted_ids, (const uint32_t*)v->touched.ptr, (uint32_t*)v->offsets.ptr, n, v->tmp.ptr, v->tmp.cap, s);
+    launch_scan(sorted_ids, (const uint32_t*)v->touched.ptr, (uint32_t*)v->offsets.ptr, n, cnt,
+                (uint32_t*)v->bstart.ptr, M, v->bs, s);
     RD_CHECK_LAUNCH("scan");
     v->end(K_SCAN, s);
-    RD_CUDA(cudaMemcpyAsync(v->host_M, (const uint32_t*)v->offsets.ptr + (n - 1), sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, s));
-    RD_CUDA(cudaMemcpyAsync(v->host_M + 1, v->nvis.ptr, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    RD_CUDA(cudaStreamSynchronize(s));
-    M = (int64_t)v->host_M[0];
-    v->n_vis = (int64_t)v->host_M[1];
-    v->n_big = (int64_t)v->host_M[2];
   }
-  if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
   RD_ENSURE(v->tkeys0, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->tkeys1, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->vals0, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->vals1, (size_t)M * sizeof(uint32_t), s);
   RD_ENSURE(v->ranges, (size_t)n_tiles * sizeof(uint2), s);
+  v->tsel = 0;
   if (M > 0) {
-    v->begin(s);
-    launch_duplicate(n, M, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect.ptr, v->tiles_x,
-                     (uint32_t*)v->tkeys0.ptr, (uint32_t*)v->vals0.ptr, s);
-    RD_CHECK_LAUNCH("duplicate");
-    v->end(K_DUP, s);
-    const size_t tb = binning_temp_bytes(0, M, v->tile_bits);
-    RD_ENSURE(v->tmp, tb, s);
-    v->begin(s);
-    v->tsel = launch_tile_sort((uint32_t*)v->tkeys0.ptr, (uint32_t*)v->tkeys1.ptr, (uint32_t*)v->vals0.ptr,
-                               (uint32_t*)v->vals1.ptr, M, v->tile_bits, v->tmp.ptr, v->tmp.cap, s);
-    RD_CHECK_LAUNCH("tile_sort");
-    v->end(K_TSORT, s);
+    RD_ENSURE_STATUS(v, M, s);
+    uint32_t* const tk[2] = {(uint32_t*)v->tkeys0.ptr, (uint32_t*)v->tkeys1.ptr};
+    uint32_t* const tv[2] = {(uint32_t*)v->vals0.ptr, (uint32_t*)v->vals1.ptr};
+    const int np = tile_sort_passes(v->tiles_x, v->tiles_y);
+    for (int p = 0; p < np; ++p) {
+      v->begin(s);
+      launch_tile_pass(p, M, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect.ptr,
+                       (const uint32_t*)v->bstart.ptr, v->tiles_x, v->tiles_y, bases, tk, tv, v->bs, s);
+      RD_CHECK_LAUNCH(p == 0 ? "duplicate" : "tile_sort");
+      if (p == 0) {
+        v->end(K_DUP, s);  // K2c: the duplicates generated and ranked by their first tile digit
+      } else {
+        v->end(K_TSORT, s);
+      }
+    }
+    v->tsel = (np - 1) % 2;
   }
   const uint32_t* keys = (const uint32_t*)(v->tsel ? v->tkeys1.ptr : v->tkeys0.ptr);
   v->begin(s);

@@ -1,185 +1,585 @@
-// binning.cu — stage 2 (K2) of the RaDe-GS rasterizer, sm_100a.
+// binning.cu — stage 2 (K2) of the RaDe-GS rasterizer, sm_100a, hand-written (no library sort).
 //
-// The depth sort of PAPER:422 per tile, as a two-stage stable sort whose result is
-// bit-identical to one LSD radix sort of 64-bit keys (tile << 32 | float_bits(z_c)) over
+// The depth sort of PAPER:422 per tile, as a two-stage stable LSD radix sort whose result is
+// bit-identical to one stable sort of 64-bit keys (tile << 32 | float_bits(z_c)) over the
 // (Gaussian, tile) pairs emitted in id order (reading S7):
 //
-//   K2a  depth sort: stable radix sort of the N pairs (float_bits(z_c), id) — culled or
-//        off-screen Gaussians carry key 0xFFFFFFFF and sink to the end. Order (z_c, id).
-//   K2b  inclusive scan of tiles_touched gathered in that order → offsets; M = offsets[N−1]
-//   K2c  duplicate: each Gaussian, in depth order, emits (tile, id) for every tile of its
-//        rect (warp-cooperative, coalesced stores)
-//   K2d  stable radix sort of the M pairs by tile on ceil(log2 T) bits (2 passes at 4096
-//        tiles instead of 6 passes over 12-byte pairs): within a tile the (z_c, id) order
-//        of K2a is preserved
+//   K2h  histograms: one pass over the N depth keys (id order) builds the four 8-bit digit
+//        histograms of the visible keys and two difference arrays over the tile columns and
+//        rows — a rect [x0, x1) × [y0, y1) adds h = y1 − y0 at x0 and −h at x1 (and w = x1 − x0
+//        at y0, −w at y1), so their prefix sums are the number of duplicates per tile column
+//        and per tile row: the digit histograms of every tile pass, without the duplicates
+//   K2a  depth sort: 4 onesweep passes (8-bit digits) of (float_bits(z_c), id). The first pass
+//        reads the N keys in id order and keeps only the visible ones (culled keys are
+//        0xFFFFFFFF and are never read downstream), so passes 2-4 move n_vis pairs. Order
+//        (z_c, id): z_c > znear > 0, so the IEEE bit pattern orders like the value
+//   K2b  inclusive scan of tiles_touched gathered in that order → offsets (single pass,
+//        decoupled look-back)
+//   K2c  duplicate + first tile pass, fused: each 2048-output block emits (tile, id) for its
+//        outputs (load-balanced over outputs, as K2's generator) and ranks them by the first
+//        tile digit right away, so the unsorted duplicates never reach HBM
+//   K2d  remaining tile passes: the tile key is packed as (ty << 16 | tx) and sorted tx digits
+//        first, then ty digits — the same order as ty·tiles_x + tx, so within a tile the
+//        (z_c, id) order of K2a is preserved; the last pass writes ty·tiles_x + tx. At 8×8
+//        tiles up to 2048×2048 px this is 2 passes (tx, ty ≤ 256)
 //   K2e  ranges[tile] = [first, last) in the sorted list
 //
-// z_c > znear > 0, so the IEEE bit pattern orders like the value. Integer work: checked
-// bit-exactly against a CPU std::stable_sort of the 64-bit keys.
+// Every onesweep pass: 256 threads × 8 items per block (2048), items warp-striped so a
+// warp-wide __match_any_sync ranks them stably; per-warp digit counters → warp offsets →
+// block-local sorted layout in shared memory; the block's per-digit counts published to and
+// prefixed by a decoupled look-back over the blocks (one thread per digit, a window of
+// predecessors per round trip; status words carry an epoch tag, so no zeroing between
+// passes); then coalesced runs per digit to HBM. A pass is a chain of dependent L2/HBM round
+// trips per block (items, look-back, scatter), so everything a block can know beforehand is
+// precomputed: the digit bases of every pass (the last K2h block scans the histograms) and,
+// for K2c, the first Gaussian of every output block (written by K2b). Integer work: checked
+// bit-exactly against the oracle's global (z_key, id) order restricted per tile and a CPU
+// stable sort.
 #include "rade_internal.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/dispatch/dispatch_radix_sort.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
+#include <atomic>
+#include <mutex>
 
 namespace rade {
 namespace {
 
-// CUB's onesweep radix sort with 512-thread × 12-key tiles (tools/sort_bench.cu on B200: 96 vs
-// 107 µs for the 1.5 M depth keys, 129 vs 141 µs for 5.6 M 12-bit tile keys against CUB's
-// default 384 × 23), 8-bit digits.
-struct SortHub {
-  using Base = cub::detail::radix::policy_hub<uint32_t, uint32_t, uint32_t>;
-  struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, Policy1000> {
-    using B = typename Base::Policy1000;
-    static constexpr bool ONESWEEP = true;
-    static constexpr int ONESWEEP_RADIX_BITS = 8;
-    using HistogramPolicy = typename B::HistogramPolicy;
-    using ExclusiveSumPolicy = typename B::ExclusiveSumPolicy;
-    using OnesweepPolicy =
-        cub::AgentRadixSortOnesweepPolicy<512, 12, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
-                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
-    using ScanPolicy = typename B::ScanPolicy;
-    using DownsweepPolicy = typename B::DownsweepPolicy;
-    using AltDownsweepPolicy = typename B::AltDownsweepPolicy;
-    using UpsweepPolicy = typename B::UpsweepPolicy;
-    using AltUpsweepPolicy = typename B::AltUpsweepPolicy;
-    using SingleTilePolicy = typename B::SingleTilePolicy;
-    using SegmentedPolicy = typename B::SegmentedPolicy;
-    using AltSegmentedPolicy = typename B::AltSegmentedPolicy;
-  };
-  using MaxPolicy = Policy1000;
-};
-using Sort = cub::DispatchRadixSort<false, uint32_t, uint32_t, uint32_t, SortHub>;
+#ifndef RD_SORT_THREADS
+#define RD_SORT_THREADS 512
+#endif
+constexpr int kST = RD_SORT_THREADS;  // threads per sort block
+constexpr int kSI = 8;            // items per thread
+constexpr int kSTile = kST * kSI; // items per block
+constexpr int kRadix = 256;
+constexpr int kMaxTileAxis = 2048;  // difference-array entries per axis (tiles per axis ≤ 2047)
+#ifndef RD_LOOKWIN
+#define RD_LOOKWIN 8
+#endif
+constexpr int kLookWin = RD_LOOKWIN;  // look-back predecessors read per round trip
+#ifndef RD_SORT_MINB
+#define RD_SORT_MINB (1024 / RD_SORT_THREADS)  // ≤ 64 registers: 32 warps per SM
+#endif
+#ifndef RD_HIST_BPS
+#define RD_HIST_BPS 2   // K2h blocks per SM (each flushes its histograms with global atomics)
+#endif
 
-struct CountOf {
-  const uint32_t* __restrict__ touched;
-  __host__ __device__ __forceinline__ uint32_t operator()(const uint32_t id) const { return touched[id]; }
-};
-
-// First index p in [0, n) with a[p] > target (n if none), searched by a whole warp: each
-// round probes 32 evenly spaced positions and keeps the bracket (4 rounds for n = 1.5M).
-__device__ __forceinline__ uint32_t warp_upper_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t target,
-                                                     int lane) {
-  uint32_t lo = 0, hi = n;  // answer in [lo, hi]
-  while (hi - lo > 32) {
-    const uint32_t step = (hi - lo + 31) / 32;
-    const uint32_t probe = lo + (uint32_t)lane * step;
-    const bool gt = probe < hi ? (a[probe] > target) : true;
-    const unsigned m = __ballot_sync(0xffffffffu, gt);
-    if (m == 0) {
-      lo = lo + 31 * step + 1;
-    } else {
-      const int f = __ffs(m) - 1;
-      if (f == 0) return lo;
-      const uint32_t nlo = lo + (uint32_t)(f - 1) * step + 1;
-      hi = min(hi, lo + (uint32_t)f * step);
-      lo = nlo;
-    }
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// status word: (tag << 32) | value, tag = 4·epoch + 1 (block aggregate) or + 2 (inclusive
+// prefix); any tag from an earlier epoch is < 4·epoch, i.e. "not yet published"
+__device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32_t flag, uint32_t v) {
+  return ((unsigned long long)(4u * epoch + flag) << 32) | v;
+}
+// Exclusive prefix of `mine` over the blocks before b for one counter: publishes the
+// aggregate, walks back summing aggregates until an inclusive prefix, publishes the inclusive.
+__device__ __forceinline__ uint32_t lookback(unsigned long long* status, int stride, int b, uint32_t epoch,
+                                             uint32_t mine) {
+  if (b == 0) {
+    st_status(status, pack_status(epoch, 2u, mine));
+    return 0u;
   }
-  const uint32_t probe = lo + (uint32_t)lane;
-  const bool gt = probe < hi ? (a[probe] > target) : true;
-  const unsigned m = __ballot_sync(0xffffffffu, gt);
-  return m ? min(hi, lo + (uint32_t)(__ffs(m) - 1)) : hi;
+  st_status(status + (size_t)b * stride, pack_status(epoch, 1u, mine));
+  const uint32_t agg = 4u * epoch + 1u, inc = 4u * epoch + 2u;
+  uint32_t excl = 0u;
+  // a window of kLookWin predecessors per round trip (independent loads; across the block's
+  // digit threads each row is one contiguous 2-KB read): blocks that start together walk back
+  // ~b/2 predecessors before they meet an inclusive prefix, so one load per step would make
+  // the first wave's latency hundreds of L2 round trips
+  int p = b - 1;
+  for (;;) {
+    unsigned long long s[kLookWin];
+#pragma unroll
+    for (int k = 0; k < kLookWin; ++k) s[k] = p - k >= 0 ? ld_status(status + (size_t)(p - k) * stride) : 0ull;
+    int used = 0;
+    bool done = false;
+#pragma unroll
+    for (int k = 0; k < kLookWin; ++k) {
+      if (!done && used == k) {
+        const uint32_t tag = (uint32_t)(s[k] >> 32);
+        if (tag >= agg) {  // published (block 0 always publishes an inclusive prefix)
+          excl += (uint32_t)s[k];
+          done = tag == inc;
+          ++used;
+        }
+      }
+    }
+    if (done) break;
+    p -= used;  // a not-yet-published entry: reload the window from it
+  }
+  st_status(status + (size_t)b * stride, pack_status(epoch, 2u, excl + mine));
+  return excl;
 }
 
-constexpr int kDupThreads = 256;
-constexpr int kDupPer = 8;     // consecutive outputs per thread
-constexpr int kDupOut = kDupThreads * kDupPer;  // outputs per block (2048)
+// Exclusive scan over the block's NT threads (one value each); *total = the sum.
+template <int NT = kST>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp, uint32_t* total) {
+  const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  uint32_t wpre = 0u, tot = 0u;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    const uint32_t v = s_warp[w];
+    wpre += w < warp ? v : 0u;
+    tot += v;
+  }
+  *total = tot;
+  __syncthreads();  // s_warp reusable
+  return wpre + inc - x;
+}
 
-// Load-balanced emission over OUTPUTS: block b writes duplicates [b·2048, (b+1)·2048). In
-// depth order every visible Gaussian touches ≥ 1 tile, so the block's outputs come from at
-// most 2048 consecutive positions [g0, g1], found by one warp-wide search of the inclusive
-// offsets. Their offsets, ids and rects are staged in shared memory; each output finds its
-// owner by binary search there. Stores are coalesced and a huge near-camera splat is spread
-// over as many blocks as its tiles need (no per-thread or per-warp serialisation). Per
-// Gaussian the tiles are emitted row-major over its rect.
-__global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, int64_t m, const uint32_t* __restrict__ offsets,
-                                                            const uint32_t* __restrict__ sorted_ids,
-                                                            const uint2* __restrict__ rect, int tiles_x,
-                                                            uint32_t* __restrict__ tile_keys,
-                                                            uint32_t* __restrict__ vals) {
-  __shared__ uint32_t s_end[kDupOut + 1];
-  __shared__ uint32_t s_id[kDupOut];
-  __shared__ uint2 s_rect[kDupOut];
-  __shared__ uint32_t s_g[2];
-  const uint32_t o0 = blockIdx.x * (uint32_t)kDupOut;
-  const uint32_t o1 = min((uint32_t)m, o0 + (uint32_t)kDupOut);
-  if (threadIdx.x < 32) {
-    const uint32_t g0 = warp_upper_bound(offsets, (uint32_t)n, o0, (int)threadIdx.x);
-    const uint32_t g1 = warp_upper_bound(offsets, (uint32_t)n, o1 - 1, (int)threadIdx.x);
-    if (threadIdx.x == 0) {
-      s_g[0] = g0;
-      s_g[1] = g1;
+// The tile passes on the packed key (ty << 16 | tx): tx low digit [, tx high digit], ty low
+// digit [, ty high digit] — 8-bit digits of one axis each, so their histograms follow from the
+// axis difference arrays.
+struct TilePass {
+  int axis;    // 0: tx, 1: ty
+  int dshift;  // digit = (coordinate >> dshift) & 255
+};
+__host__ __device__ __forceinline__ int tile_pass_list(int tiles_x, int tiles_y, TilePass* tp) {
+  int np = 0;
+  tp[np++] = TilePass{0, 0};
+  if (tiles_x > 256) tp[np++] = TilePass{0, 8};
+  tp[np++] = TilePass{1, 0};
+  if (tiles_y > 256) tp[np++] = TilePass{1, 8};
+  return np;
+}
+constexpr int kBaseStride = kRadix + 1;  // bases of one pass: 256 exclusive digit starts + the total
+
+// ------------------------------------------------------------------------------- K2h
+// Depth digit histograms of the visible keys (digits aggregated per warp with
+// __match_any_sync: the high digits of nearby depths coincide) and the tile difference arrays;
+// the last block to finish turns them into the digit bases of every pass (bases[pass][257]:
+// depth passes 0-3, then the tile passes).
+constexpr int kHistThreads = 512;
+__global__ void __launch_bounds__(kHistThreads) k_bin_hist(int64_t n, const uint32_t* __restrict__ dkey,
+                                                           const uint2* __restrict__ rect, int tiles_x, int tiles_y,
+                                                           uint32_t* __restrict__ hist, int* __restrict__ diff_x,
+                                                           int* __restrict__ diff_y, uint32_t* __restrict__ cnt,
+                                                           uint32_t* __restrict__ bases,
+                                                           volatile uint32_t* __restrict__ host_counts) {
+  uint32_t* done = cnt + 3;
+  __shared__ uint32_t sh[4][kRadix];
+  __shared__ int sx[kMaxTileAxis], sy[kMaxTileAxis];
+  __shared__ uint32_t s_warp[kHistThreads / 32];
+  __shared__ uint32_t s_bins[kRadix];
+  __shared__ bool s_last;
+  __shared__ uint32_t s_m;
+  const int tid = (int)threadIdx.x;
+  if (tid == 0) s_m = 0u;
+  for (int k = tid; k < 4 * kRadix; k += kHistThreads) (&sh[0][0])[k] = 0u;
+  for (int k = tid; k < kMaxTileAxis; k += kHistThreads) sx[k] = sy[k] = 0;
+  __syncthreads();
+  const int lane = tid & 31;
+  uint32_t mdup = 0u;  // this thread's duplicates (tiles touched)
+  const int64_t stride = (int64_t)gridDim.x * kHistThreads;
+  const int64_t rounds = (n + stride - 1) / stride;  // warp-uniform trip count (match_any below)
+  for (int64_t r = 0; r < rounds; ++r) {
+    const int64_t i = r * stride + (int64_t)blockIdx.x * kHistThreads + tid;
+    const uint32_t k = i < n ? dkey[i] : 0xffffffffu;
+    const bool vis = k != 0xffffffffu;
+    uint2 q = make_uint2(0u, 0u);
+    if (vis) q = rect[i];
+    if (vis) {  // the low digits of nearby depths differ: plain shared atomics
+      atomicAdd(&sh[0][k & 255u], 1u);
+      atomicAdd(&sh[1][(k >> 8) & 255u], 1u);
+    }
+#pragma unroll
+    for (int p = 2; p < 4; ++p) {  // the high ones mostly coincide: one atomic per distinct digit
+      const uint32_t d = vis ? (k >> (8 * p)) & 255u : 256u;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (vis && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
+    }
+    if (vis) {
+      const int x0 = (int)(q.x & 0xffffu), y0 = (int)(q.x >> 16), x1 = (int)(q.y & 0xffffu), y1 = (int)(q.y >> 16);
+      atomicAdd(&sx[x0], y1 - y0);
+      atomicSub(&sx[x1], y1 - y0);
+      atomicAdd(&sy[y0], x1 - x0);
+      atomicSub(&sy[y1], x1 - x0);
+      mdup += (uint32_t)((x1 - x0) * (y1 - y0));
+    }
+  }
+  mdup = __reduce_add_sync(0xffffffffu, mdup);
+  if (lane == 0 && mdup) atomicAdd(&s_m, mdup);
+  __syncthreads();
+  if (tid == 0 && s_m) atomicAdd(cnt + 2, s_m);  // M
+  for (int k = tid; k < 4 * kRadix; k += kHistThreads) {
+    const uint32_t v = (&sh[0][0])[k];
+    if (v) atomicAdd(hist + k, v);
+  }
+  for (int k = tid; k <= tiles_x; k += kHistThreads)
+    if (sx[k]) atomicAdd(diff_x + k, sx[k]);
+  for (int k = tid; k <= tiles_y; k += kHistThreads)
+    if (sy[k]) atomicAdd(diff_y + k, sy[k]);
+
+  // the last block: digit bases of every pass
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {  // K1's visible / big counts and M, to mapped pinned host memory (the host
+    host_counts[0] = __ldcg(cnt);  // reads them once this kernel's completion event fires)
+    host_counts[1] = __ldcg(cnt + 1);
+    host_counts[2] = __ldcg(cnt + 2);
+  }
+  uint32_t tot;
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t c = tid < kRadix ? __ldcg(hist + kRadix * p + tid) : 0u;
+    const uint32_t e = block_excl_scan<kHistThreads>(c, s_warp, &tot);
+    if (tid < kRadix) bases[kBaseStride * p + tid] = e;
+    if (tid == 0) bases[kBaseStride * p + kRadix] = tot;
+  }
+  // per-axis duplicate counts (prefix sums of the difference arrays) into sx / sy: thread t owns
+  // entries [4t, 4t + 4) of the ≤ 2048
+  for (int axis = 0; axis < 2; ++axis) {
+    const int len = axis == 0 ? tiles_x : tiles_y;
+    const int* diff = axis == 0 ? diff_x : diff_y;
+    int* h = axis == 0 ? sx : sy;
+    int v[4], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = 4 * tid + j;
+      v[j] = e < len ? __ldcg(diff + e) : 0;
+      sum += v[j];
+    }
+    int run = (int)block_excl_scan<kHistThreads>((uint32_t)sum, s_warp, &tot);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      run += v[j];
+      h[4 * tid + j] = 4 * tid + j < len ? run : 0;
     }
   }
   __syncthreads();
-  const uint32_t g0 = s_g[0];
-  const int ng = (int)(s_g[1] - g0) + 1;  // ≤ kDupOut
-  // s_end[0] = start of g0; s_end[k + 1] = end of g0 + k
-  if (threadIdx.x == 0) s_end[0] = g0 == 0 ? 0u : offsets[g0 - 1];
-  for (int k = threadIdx.x; k < ng; k += kDupThreads) {
-    s_end[k + 1] = offsets[g0 + k];
-    const uint32_t id = sorted_ids[g0 + k];
-    s_id[k] = id;
-    s_rect[k] = rect[id];
+  TilePass tp[4];
+  const int np = tile_pass_list(tiles_x, tiles_y, tp);
+  for (int p = 0; p < np; ++p) {
+    if (tid < kRadix) s_bins[tid] = 0u;
+    __syncthreads();
+    const int* h = tp[p].axis == 0 ? sx : sy;
+    const int len = tp[p].axis == 0 ? tiles_x : tiles_y;
+    for (int e = tid; e < len; e += kHistThreads)
+      if (h[e] > 0) atomicAdd(&s_bins[(e >> tp[p].dshift) & 255], (uint32_t)h[e]);
+    __syncthreads();
+    const uint32_t c = tid < kRadix ? s_bins[tid] : 0u;
+    const uint32_t e = block_excl_scan<kHistThreads>(c, s_warp, &tot);
+    if (tid < kRadix) bases[kBaseStride * (4 + p) + tid] = e;
+    if (tid == 0) bases[kBaseStride * (4 + p) + kRadix] = tot;
+  }
+  if (tid == 0) *done = 0u;  // for the next view
+}
+
+// ------------------------------------------------------------------------------- onesweep
+enum PassMode { kDepthFirst = 0, kDepth = 1, kTileGen = 2, kTile = 3 };
+
+struct PassArgs {
+  const uint32_t* __restrict__ keys_in;  // kDepthFirst: the N keys in id order; kDepth/kTile: pass input
+  const uint32_t* __restrict__ vals_in;
+  uint32_t* __restrict__ keys_out;
+  uint32_t* __restrict__ vals_out;
+  int64_t n;   // items: kDepthFirst N Gaussians, kDepth n_vis, kTileGen/kTile M
+  const uint32_t* n_dev;  // if set, the item count is read here (kDepth: K1's visible count)
+  int shift;   // digit = (key >> shift) & 255
+  const uint32_t* __restrict__ bases;  // this pass's 256 digit bases + total (K2h)
+  int last, tiles_x;                   // kTile: the last pass writes ty·tiles_x + tx
+  // kTileGen: the generator's inputs (K2b offsets over the depth-sorted visible ids, K2b's
+  // first Gaussian of each output block)
+  const uint32_t* __restrict__ offsets;
+  const uint32_t* __restrict__ sorted_ids;
+  const uint2* __restrict__ rect;
+  const uint32_t* __restrict__ bstart;
+  unsigned long long* status;
+  uint32_t epoch;
+};
+
+struct GenSmem {  // kTileGen: the block's Gaussians (≤ 2049: every visible one touches ≥ 1 tile)
+  uint32_t end[kSTile + 2];
+  uint32_t id[kSTile + 1];
+  uint2 rect[kSTile + 1];
+};
+struct PassSmem {
+  uint32_t key[kSTile];
+  uint32_t val[kSTile];
+  uint32_t cnt[kST / 32][kRadix];  // per-warp digit counts → warp offsets within the block's digit run
+};
+union SortSmem {
+  GenSmem gen;
+  PassSmem pass;
+};
+
+// K2c generator: the block's Gaussians are [bstart[b], bstart[b + 1]] (K2b: the owners of its
+// first output and of the next block's first output). Thread t produces outputs o0 + 8t ..
+// o0 + 8t + 7 (one binary search for the first one's owner in the staged Gaussians, then a
+// walk: the owner advances by at most one per output, the tile steps row-major over its
+// rect) as packed (ty << 16 | tx) keys.
+__device__ __forceinline__ void generate_dups(const PassArgs& a, GenSmem& g, int b, uint32_t o0, uint32_t o1,
+                                              uint32_t (&key)[kSI], uint32_t (&val)[kSI]) {
+  const uint32_t g0 = a.bstart[b];
+  const int ng = (int)(a.bstart[b + 1] - g0) + 1;
+  if (threadIdx.x == 0) g.end[0] = g0 == 0 ? 0u : a.offsets[g0 - 1];
+  for (int k = threadIdx.x; k < ng; k += kST) {
+    g.end[k + 1] = a.offsets[g0 + k];
+    const uint32_t id = a.sorted_ids[g0 + k];
+    g.id[k] = id;
+    g.rect[k] = a.rect[id];
   }
   __syncthreads();
-  // thread t writes the kDupPer consecutive outputs o0 + kDupPer·t ..: one binary search for
-  // the first one's owner, then a walk (every staged Gaussian has ≥ 1 tile, so the owner
-  // advances by at most one per output) with the tile stepped row-major over the rect, and
-  // two 16-B stores per array (a warp writes 1 KB contiguous per array)
-  const uint32_t o = o0 + (uint32_t)threadIdx.x * kDupPer;
+  const uint32_t o = o0 + (uint32_t)threadIdx.x * kSI;
+#pragma unroll
+  for (int j = 0; j < kSI; ++j) key[j] = val[j] = 0u;
   if (o >= o1) return;
-  int lo = 0, hi = ng - 1;  // owner k: s_end[k] <= o < s_end[k + 1]
+  int lo = 0, hi = ng - 1;  // owner k: end[k] <= o < end[k + 1]
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (s_end[mid] <= o) lo = mid; else hi = mid - 1;
+    if (g.end[mid] <= o) lo = mid; else hi = mid - 1;
   }
   int k = lo;
-  uint2 r = s_rect[k];
+  uint2 r = g.rect[k];
   uint32_t x0 = r.x & 0xffffu, x1 = r.y & 0xffffu;
-  const uint32_t li = o - s_end[k], w = x1 - x0;
+  const uint32_t li = o - g.end[k], w = x1 - x0;
   uint32_t ty = (r.x >> 16) + li / w, tx = x0 + li % w;
-  uint32_t key[kDupPer], val[kDupPer];
 #pragma unroll
-  for (int j = 0; j < kDupPer; ++j) {
+  for (int j = 0; j < kSI; ++j) {
     const uint32_t oj = o + (uint32_t)j;
     if (oj < o1) {
-      if (oj >= s_end[k + 1]) {  // the next Gaussian starts here, at its rect's first tile
+      if (oj >= g.end[k + 1]) {  // the next Gaussian starts here, at its rect's first tile
         ++k;
-        r = s_rect[k];
+        r = g.rect[k];
         x0 = r.x & 0xffffu;
         x1 = r.y & 0xffffu;
         tx = x0;
         ty = r.x >> 16;
       }
-      key[j] = ty * (uint32_t)tiles_x + tx;
-      val[j] = s_id[k];
+      key[j] = (ty << 16) | tx;
+      val[j] = g.id[k];
       if (++tx == x1) {
         tx = x0;
         ++ty;
       }
     }
   }
-  if (o + kDupPer <= o1) {
-    uint4* kk = reinterpret_cast<uint4*>(tile_keys + o);
-    uint4* vv = reinterpret_cast<uint4*>(vals + o);
-    kk[0] = make_uint4(key[0], key[1], key[2], key[3]);
-    kk[1] = make_uint4(key[4], key[5], key[6], key[7]);
-    vv[0] = make_uint4(val[0], val[1], val[2], val[3]);
-    vv[1] = make_uint4(val[4], val[5], val[6], val[7]);
+}
+
+// One LSD pass. Blocks are processed in blockIdx order (the dispatch order of a 1-D grid, as
+// every single-pass look-back scan assumes), so a block's predecessors are resident or done.
+#ifdef RD_BIN_TRACE  // development: per-block phase timestamps of the last tile pass
+__device__ unsigned long long g_bin_trace[8192][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RD_TRACE(k) if (MODE == kTile && threadIdx.x == 0 && blockIdx.x < 8192) g_bin_trace[blockIdx.x][k] = gtimer();
+#else
+#define RD_TRACE(k)
+#endif
+
+template <int MODE>
+__global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
+  extern __shared__ __align__(16) unsigned char dsmem[];  // SortSmem (> 48 KB at 512 threads)
+  SortSmem& sm = *reinterpret_cast<SortSmem*>(dsmem);
+  __shared__ uint32_t s_gbase[kRadix + 1];  // the pass's digit bases (K2h) + total
+  __shared__ uint32_t s_lstart[kRadix];     // start of digit d in the block's sorted layout
+  __shared__ uint32_t s_dst[kRadix];        // global position of the block's first item of digit d − lstart
+  __shared__ uint32_t s_warp[kST / 32];
+  __shared__ uint32_t s_cnt;
+  const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = (int)blockIdx.x;
+  const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
+  const int64_t base = (int64_t)b * kSTile;
+  if (base >= n) return;  // the grid is sized for an upper bound; later blocks are empty too
+  RD_TRACE(0)
+
+  // this block's items, warp-striped: warp w, lane l, item j ↔ position base + 256w + 32j + l
+  uint32_t key[kSI], val[kSI];
+  bool ok[kSI];
+  if constexpr (MODE != kTileGen) {  // loads first: their latency overlaps the set-up below
+#pragma unroll
+    for (int j = 0; j < kSI; ++j) {
+      const int64_t p = base + warp * 256 + j * 32 + lane;
+      ok[j] = p < n;
+      key[j] = ok[j] ? a.keys_in[p] : 0u;
+      if constexpr (MODE == kDepthFirst) {
+        val[j] = (uint32_t)p;
+      } else {
+        val[j] = ok[j] ? a.vals_in[p] : 0u;
+      }
+    }
+  }
+  if (tid <= kRadix) s_gbase[tid] = a.bases[tid];
+  if constexpr (MODE == kTileGen) {
+    const uint32_t o0 = (uint32_t)base, o1 = (uint32_t)(n < base + kSTile ? n : base + kSTile);
+    uint32_t gk[kSI], gv[kSI];
+    generate_dups(a, sm.gen, b, o0, o1, gk, gv);
+    __syncthreads();  // the staged Gaussians are dead: the same shared memory takes the transpose
+    uint4* kk = reinterpret_cast<uint4*>(sm.pass.key + tid * kSI);
+    uint4* vv = reinterpret_cast<uint4*>(sm.pass.val + tid * kSI);
+    kk[0] = make_uint4(gk[0], gk[1], gk[2], gk[3]);
+    kk[1] = make_uint4(gk[4], gk[5], gk[6], gk[7]);
+    vv[0] = make_uint4(gv[0], gv[1], gv[2], gv[3]);
+    vv[1] = make_uint4(gv[4], gv[5], gv[6], gv[7]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSI; ++j) {
+      const int p = warp * 256 + j * 32 + lane;
+      ok[j] = base + p < n;
+      key[j] = sm.pass.key[p];
+      val[j] = sm.pass.val[p];
+    }
+    __syncthreads();  // every lane has read its transposed items
+  }
+  if constexpr (MODE == kDepthFirst) {
+#pragma unroll
+    for (int j = 0; j < kSI; ++j) ok[j] = ok[j] && key[j] != 0xffffffffu;  // culled / off screen: dropped
+  }
+  for (int k = tid; k < (kST / 32) * kRadix; k += kST) (&sm.pass.cnt[0][0])[k] = 0u;
+  __syncthreads();
+  RD_TRACE(1)
+
+  // stable rank within the warp: items in (j, lane) order = position order; the lanes holding
+  // the same digit found by 8 ballots (constant cost, unlike __match_any_sync, whose cost grows
+  // with the number of distinct digits in the warp — the tile digits of consecutive duplicates
+  // are mostly distinct)
+  uint32_t rank[kSI];
+  const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < kSI; ++j) {
+    const uint32_t d = (key[j] >> a.shift) & 255u;
+    unsigned peers = __ballot_sync(0xffffffffu, ok[j]);
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      const bool on = (d >> bit) & 1u;
+      const unsigned bb = __ballot_sync(0xffffffffu, on);
+      peers &= on ? bb : ~bb;
+    }
+    uint32_t c = 0u;
+    if (ok[j]) c = sm.pass.cnt[warp][d];
+    __syncwarp();
+    rank[j] = c + (uint32_t)__popc(peers & below);
+    if (ok[j] && (peers & below) == 0u) sm.pass.cnt[warp][d] = c + (uint32_t)__popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  RD_TRACE(2)
+  // per digit (thread d < 256): warp offsets, the block's count, its sorted-layout start,
+  // look-back
+  {
+    const int d = tid;
+    uint32_t run = 0u;
+    if (d < kRadix) {
+#pragma unroll
+      for (int w = 0; w < kST / 32; ++w) {
+        const uint32_t c = sm.pass.cnt[w][d];
+        sm.pass.cnt[w][d] = run;
+        run += c;
+      }
+    }
+    uint32_t btot;
+    const uint32_t ls = block_excl_scan(run, s_warp, &btot);
+    if (d == 0) s_cnt = btot;
+    if (d < kRadix) {
+      s_lstart[d] = ls;
+      uint32_t excl = 0u;
+      if (s_gbase[d + 1] != s_gbase[d])  // digits no item of the pass has are never looked up
+        excl = lookback(a.status + d, kRadix, b, a.epoch, run);
+      s_dst[d] = s_gbase[d] + excl - ls;
+    }
+  }
+  __syncthreads();
+  RD_TRACE(3)
+  // block-local sorted layout, then coalesced runs per digit
+#pragma unroll
+  for (int j = 0; j < kSI; ++j) {
+    if (ok[j]) {
+      const uint32_t d = (key[j] >> a.shift) & 255u;
+      const uint32_t p = s_lstart[d] + sm.pass.cnt[warp][d] + rank[j];
+      sm.pass.key[p] = key[j];
+      sm.pass.val[p] = val[j];
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)s_cnt;
+  for (int i = tid; i < cnt; i += kST) {
+    const uint32_t k = sm.pass.key[i];
+    const uint32_t dst = s_dst[(k >> a.shift) & 255u] + (uint32_t)i;
+    uint32_t out = k;
+    if constexpr (MODE == kTile || MODE == kTileGen)
+      if (a.last) out = (k >> 16) * (uint32_t)a.tiles_x + (k & 0xffffu);
+    a.keys_out[dst] = out;
+    a.vals_out[dst] = sm.pass.val[i];
+  }
+  RD_TRACE(4)
+}
+
+// ------------------------------------------------------------------------------- K2b
+// offsets[p] = Σ_{q ≤ p} tiles_touched[ids[q]]: thread t sums items 8t..8t+7 of its block,
+// block scan, one look-back word per block. Each Gaussian also records itself as the first
+// Gaussian of the K2c output blocks whose first output it owns: bstart[ob] = p for every
+// ob·2048 in [offset_before, offset), and bstart[out_blocks] = n − 1.
+__global__ void __launch_bounds__(kST) k_scan(const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ ids,
+                                              const uint32_t* __restrict__ touched, uint32_t* __restrict__ offsets,
+                                              uint32_t* __restrict__ bstart, uint32_t out_blocks,
+                                              unsigned long long* status, uint32_t epoch) {
+  __shared__ uint32_t s_warp[kST / 32];
+  __shared__ uint32_t s_excl;
+  const int b = (int)blockIdx.x;
+  const int64_t n = (int64_t)*n_dev;
+  if ((int64_t)b * kSTile >= n) return;  // grid sized for N
+  const int64_t p0 = (int64_t)b * kSTile + (int64_t)threadIdx.x * kSI;
+  uint32_t v[kSI], t[kSI];
+  if (p0 + kSI <= n) {
+    const uint4 q0 = *reinterpret_cast<const uint4*>(ids + p0);
+    const uint4 q1 = *reinterpret_cast<const uint4*>(ids + p0 + 4);
+    v[0] = touched[q0.x]; v[1] = touched[q0.y]; v[2] = touched[q0.z]; v[3] = touched[q0.w];
+    v[4] = touched[q1.x]; v[5] = touched[q1.y]; v[6] = touched[q1.z]; v[7] = touched[q1.w];
   } else {
 #pragma unroll
-    for (int j = 0; j < kDupPer; ++j)
-      if (o + (uint32_t)j < o1) {
-        tile_keys[o + j] = key[j];
-        vals[o + j] = val[j];
-      }
+    for (int j = 0; j < kSI; ++j) v[j] = p0 + j < n ? touched[ids[p0 + j]] : 0u;
+  }
+  uint32_t s = 0u;
+#pragma unroll
+  for (int j = 0; j < kSI; ++j) {
+    t[j] = v[j];
+    s += v[j];
+    v[j] = s;
+  }
+  uint32_t btot;
+  const uint32_t te = block_excl_scan(s, s_warp, &btot);
+  if (threadIdx.x == 0) s_excl = lookback(status, 1, b, epoch, btot);
+  __syncthreads();
+  const uint32_t e = s_excl + te;
+  if (p0 + kSI <= n) {
+    uint4* o = reinterpret_cast<uint4*>(offsets + p0);
+    o[0] = make_uint4(e + v[0], e + v[1], e + v[2], e + v[3]);
+    o[1] = make_uint4(e + v[4], e + v[5], e + v[6], e + v[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSI; ++j)
+      if (p0 + j < n) offsets[p0 + j] = e + v[j];
+  }
+#pragma unroll
+  for (int j = 0; j < kSI; ++j) {
+    if (p0 + j < n) {
+      const uint32_t hi = e + v[j], lo = hi - t[j];  // this Gaussian's outputs [lo, hi)
+      for (uint32_t ob = (lo + kSTile - 1) / kSTile; ob * (uint32_t)kSTile < hi; ++ob) bstart[ob] = (uint32_t)(p0 + j);
+      if (p0 + j == n - 1) bstart[out_blocks] = (uint32_t)(p0 + j);
+    }
   }
 }
 
+// ------------------------------------------------------------------------------- K2e
 // 8 consecutive sorted keys per thread (two 16-B loads) + the next one; a boundary between
 // positions k and k+1 closes tile keys[k] and opens tile keys[k+1].
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int64_t m,
@@ -216,47 +616,119 @@ __global__ void __launch_bounds__(256) k_keys64(const uint32_t* __restrict__ til
   out[k] = ((uint64_t)tiles[k] << 32) | (uint64_t)__float_as_uint(rec[ids[k]].r3.x);
 }
 
+unsigned blocks_of(int64_t n) { return (unsigned)((n + kSTile - 1) / kSTile); }
+
 }  // namespace
 
-size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits) {
-  size_t a = 0, b = 0, c = 0;
-  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
-  Sort::Dispatch(nullptr, a, k, v, (uint32_t)n, 0, 32, true, 0);
-  cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it(nullptr, CountOf{nullptr});
-  cub::DeviceScan::InclusiveSum(nullptr, b, it, (uint32_t*)nullptr, (int)n);
-  if (m > 0) Sort::Dispatch(nullptr, c, k, v, (uint32_t)m, 0, tile_bits, true, 0);
-  size_t r = a > b ? a : b;
-  return r > c ? r : c;
+size_t bin_status_words(int64_t n_items) { return (size_t)(blocks_of(n_items) + 1) * kRadix; }
+size_t bin_bstart_words(int64_t m) { return (size_t)blocks_of(m) + 2; }
+int bin_max_tiles_per_axis() { return kMaxTileAxis - 1; }
+int bin_bases_words() { return 8 * kBaseStride; }
+
+constexpr int kSortSmem = (int)sizeof(SortSmem);
+template <int MODE>
+static void sort_attrs() {
+  cudaFuncSetAttribute(k_onesweep<MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_onesweep<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+}
+static void set_carveout_once() {  // views are binned from several host threads at once
+  static std::once_flag once;
+  std::call_once(once, [] {
+    sort_attrs<kDepthFirst>();
+    sort_attrs<kDepth>();
+    sort_attrs<kTileGen>();
+    sort_attrs<kTile>();
+  });
 }
 
-int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t* idx1, int64_t n, void* temp,
-                      size_t temp_bytes, cudaStream_t s) {
-  if (n == 0) return 0;
-  cub::DoubleBuffer<uint32_t> k(dkey0, dkey1), v(idx0, idx1);
-  Sort::Dispatch(temp, temp_bytes, k, v, (uint32_t)n, 0, 32, true, s);
-  return k.selector;
-}
-
-void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp,
-                 size_t temp_bytes, cudaStream_t s) {
+void launch_bin_hist(int64_t n, const uint32_t* dkey, const uint2* rect, int tiles_x, int tiles_y, uint32_t* cnt,
+                     uint32_t* bases, uint32_t* host_counts, cudaStream_t s) {
+  uint32_t* hist = cnt + kBinCntHist;
+  int* diff_x = (int*)(cnt + kBinCntDiff);
+  int* diff_y = diff_x + (tiles_x + 1);
   if (n == 0) return;
-  cub::TransformInputIterator<uint32_t, CountOf, const uint32_t*> it(sorted_ids, CountOf{tiles_touched});
-  cub::DeviceScan::InclusiveSum(temp, temp_bytes, it, offsets, (int)n, s);
+  static std::atomic<int> sms_cache{0};
+  int sms = sms_cache.load();
+  if (sms == 0) {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms_cache.store(v);
+    sms = v;
+  }
+  const int64_t want = (n + kHistThreads - 1) / kHistThreads;
+  const unsigned grid = (unsigned)(want < RD_HIST_BPS * sms ? want : RD_HIST_BPS * sms);
+  k_bin_hist<<<grid, kHistThreads, 0, s>>>(n, dkey, rect, tiles_x, tiles_y, hist, diff_x, diff_y, cnt, bases,
+                                           host_counts);
 }
 
-void launch_duplicate(int64_t n, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
-                      int tiles_x, uint32_t* tile_keys, uint32_t* vals, cudaStream_t s) {
-  if (n == 0 || m == 0) return;
-  k_duplicate<<<(unsigned)((m + kDupOut - 1) / kDupOut), kDupThreads, 0, s>>>(n, m, offsets, sorted_ids, rect, tiles_x,
-                                                                            tile_keys, vals);
+// Pass p (0..3) of the depth sort: pass 0 reads the N keys in id order (ids implicit) and
+// writes buffer 1, then 1 → 0 → 1 → 0, so the result is in buffer 0. Passes 1-3 read the
+// visible count from n_vis_dev (grid sized for N: no host sync before them).
+void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const uint32_t* n_vis_dev,
+                       const uint32_t* bases, uint32_t* const kb[2], uint32_t* const vb[2], BinSort& bs,
+                       cudaStream_t s) {
+  if (n == 0) return;
+  set_carveout_once();
+  const int out = p % 2 == 0 ? 1 : 0;
+  PassArgs a{};
+  a.keys_in = p == 0 ? dkey_id_order : kb[out ^ 1];
+  a.vals_in = p == 0 ? nullptr : vb[out ^ 1];
+  a.keys_out = kb[out];
+  a.vals_out = vb[out];
+  a.n = n;
+  a.n_dev = p == 0 ? nullptr : n_vis_dev;
+  a.shift = 8 * p;
+  a.bases = bases + kBaseStride * p;
+  a.status = bs.status;
+  a.epoch = ++bs.epoch;
+  if (p == 0)
+    k_onesweep<kDepthFirst><<<blocks_of(n), kST, kSortSmem, s>>>(a);
+  else
+    k_onesweep<kDepth><<<blocks_of(n), kST, kSortSmem, s>>>(a);
 }
 
-int launch_tile_sort(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int tile_bits,
-                     void* temp, size_t temp_bytes, cudaStream_t s) {
-  if (m == 0) return 0;
-  cub::DoubleBuffer<uint32_t> k(keys0, keys1), v(vals0, vals1);
-  Sort::Dispatch(temp, temp_bytes, k, v, (uint32_t)m, 0, tile_bits, true, s);
-  return k.selector;
+void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n_max,
+                 const uint32_t* n_dev, uint32_t* bstart, int64_t m, BinSort& bs, cudaStream_t s) {
+  if (n_max == 0) return;
+  k_scan<<<blocks_of(n_max), kST, 0, s>>>(n_dev, sorted_ids, tiles_touched, offsets, bstart, blocks_of(m), bs.status,
+                                          ++bs.epoch);
+}
+
+int tile_sort_passes(int tiles_x, int tiles_y) {
+  TilePass tp[4];
+  return tile_pass_list(tiles_x, tiles_y, tp);
+}
+
+// Tile pass p writes buffer p % 2; pass 0 generates the duplicates (K2c) from the scan.
+void launch_tile_pass(int p, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
+                      const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases, uint32_t* const kb[2],
+                      uint32_t* const vb[2], BinSort& bs, cudaStream_t s) {
+  if (m == 0) return;
+  set_carveout_once();
+  TilePass tp[4];
+  const int np = tile_pass_list(tiles_x, tiles_y, tp);
+  const int out = p % 2;
+  PassArgs a{};
+  a.keys_in = p == 0 ? nullptr : kb[out ^ 1];
+  a.vals_in = p == 0 ? nullptr : vb[out ^ 1];
+  a.keys_out = kb[out];
+  a.vals_out = vb[out];
+  a.n = m;
+  a.shift = 16 * tp[p].axis + tp[p].dshift;
+  a.bases = bases + kBaseStride * (4 + p);
+  a.last = p == np - 1 ? 1 : 0;
+  a.tiles_x = tiles_x;
+  a.offsets = offsets;
+  a.sorted_ids = sorted_ids;
+  a.rect = rect;
+  a.bstart = bstart;
+  a.status = bs.status;
+  a.epoch = ++bs.epoch;
+  if (p == 0)
+    k_onesweep<kTileGen><<<blocks_of(m), kST, kSortSmem, s>>>(a);
+  else
+    k_onesweep<kTile><<<blocks_of(m), kST, kSortSmem, s>>>(a);
 }
 
 void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s) {
@@ -275,3 +747,9 @@ void launch_keys64(const uint32_t* tiles, const uint32_t* ids, const Record* rec
 }
 
 }  // namespace rade
+
+#ifdef RD_BIN_TRACE
+extern "C" int rd_debug_bin_trace(unsigned long long* host, int nblocks) {
+  return (int)cudaMemcpyFromSymbol(host, rade::g_bin_trace, sizeof(unsigned long long) * 6 * (size_t)nblocks);
+}
+#endif

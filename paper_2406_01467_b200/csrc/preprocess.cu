@@ -421,7 +421,7 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
   return nt;
 }
 
-// K1 kernel: per-Gaussian forward (plus the depth-sort input dkey[i], didx[i] = i), then
+// K1 kernel: per-Gaussian forward (plus the depth-sort input dkey[i] in id order), then
 // the warp-aggregated append of the visible ids to the visible list (one atomic per warp;
 // list order is arbitrary — K5a, its only user, is order-independent).
 #ifndef RD_K5_THREADS
@@ -439,7 +439,6 @@ template <int DEG>
 __global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
                                                          Record* __restrict__ rec, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
-                                                         uint32_t* __restrict__ didx,
                                                          uint32_t* __restrict__ count, uint32_t* __restrict__ vis,
                                                          uint32_t* __restrict__ big, G2D* __restrict__ g2d,
                                                          Counter* __restrict__ counters) {
@@ -448,7 +447,6 @@ __global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(De
   uint32_t x0 = 0, y0 = 0, w = 1, nt = 0;
   int why = kVisible;
   if (i < g.n) {
-    didx[i] = (uint32_t)i;
     nt = preprocess_one<DEG>(g, i, cam, opt, rec, rect, touched, dkey, x0, y0, w, why);
   }
   if (counters) {  // profiling: culls by reason (warp-aggregated)
@@ -1017,13 +1015,13 @@ __global__ void __launch_bounds__(64) k_preprocess_bwd_sh_coop(DevGauss g, DevCa
 }  // namespace
 
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
-                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* count,
+                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* count,
                            uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s) {
   if (g.n == 0) return;
   const int threads = RD_K1_THREADS;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
 #define RD_K1(D)                                                                                                 \
-  k_preprocess_fwd<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, rec, rect, tiles_touched, dkey, didx, \
+  k_preprocess_fwd<D><<<blocks, threads, 0, s>>>(g, cam, opt, tiles_x, rec, rect, tiles_touched, dkey, \
                                                  count, vis, big, g2d, counters)
   switch (opt.sh_degree) {
     case 0: RD_K1(0); break;

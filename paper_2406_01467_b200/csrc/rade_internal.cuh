@@ -190,12 +190,12 @@ __device__ __forceinline__ void warp_count(Counter* ctr, unsigned v) {
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, (Counter)v);
 }
 
-// K1 also writes the depth-sort input: dkey[i] = float_bits(z_c) (0xFFFFFFFF if the
-// Gaussian touches no tile) and didx[i] = i, zeroes the G2D row of every visible Gaussian,
-// and appends the visible ids to vis (count[0]) and the big ones (is_big)
-// tiles to big (count[1]); count is zeroed beforehand.
+// K1 also writes the depth-sort input dkey[i] = float_bits(z_c) in id order (0xFFFFFFFF if
+// the Gaussian touches no tile), zeroes the G2D row of every visible Gaussian, appends the
+// visible ids to vis (count[0]) and the big ones (is_big) to big (count[1]); count is zeroed
+// beforehand.
 void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, int tiles_x, Record* rec,
-                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* didx, uint32_t* count,
+                           uint2* rect, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* count,
                            uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s);
 // K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry: fp32 in id
 // order for the visible Gaussians that are not is_big, fp64 over the big list).
@@ -213,15 +213,35 @@ void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, c
 // debug: G2D rows → f32 [n][16] (m[0..4], f[0..9], 0)
 void launch_g2d_to_f32(const G2D* g2d, int64_t n, float* out, cudaStream_t s);
 // K2 (binning.cu). Sorts return the CUB DoubleBuffer selector (1: result in the *1 buffers).
-size_t binning_temp_bytes(int64_t n, int64_t m, int tile_bits);
-int launch_depth_sort(uint32_t* dkey0, uint32_t* dkey1, uint32_t* idx0, uint32_t* idx1, int64_t n, void* temp,
-                      size_t temp_bytes, cudaStream_t s);
-void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n, void* temp,
-                 size_t temp_bytes, cudaStream_t s);
-void launch_duplicate(int64_t n, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
-                      int tiles_x, uint32_t* tile_keys, uint32_t* vals, cudaStream_t s);
-int launch_tile_sort(uint32_t* keys0, uint32_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t m, int tile_bits,
-                     void* temp, size_t temp_bytes, cudaStream_t s);
+// K2 (binning.cu): hand-written onesweep radix passes with decoupled look-back. BinSort is the
+// view's look-back state: status words (zeroed when allocated, epoch-tagged after that) and
+// the host-side epoch counter.
+struct BinSort {
+  unsigned long long* status;
+  uint32_t epoch;
+};
+size_t bin_status_words(int64_t n_items);
+size_t bin_bstart_words(int64_t m);
+int bin_max_tiles_per_axis();
+int bin_bases_words();
+// bincnt layout (u32): [0] visible, [1] big (K1), [2] M (K2h) (zeroed before K1), [3] K2h's
+// done-counter (zeroed before K1, reset by K2h), [4, 4 + 1024) the four depth digit
+// histograms, then diff_x[tiles_x + 1], diff_y[tiles_y + 1] (zeroed before K2h), then the
+// digit bases of every pass (bin_bases_words(), written by K2h)
+constexpr int kBinCntHist = 4;
+constexpr int kBinCntDiff = 4 + 1024;
+// K2h: also adds M to cnt[2] and writes cnt[0..2] to host_counts (mapped pinned memory)
+void launch_bin_hist(int64_t n, const uint32_t* dkey, const uint2* rect, int tiles_x, int tiles_y, uint32_t* cnt,
+                     uint32_t* bases, uint32_t* host_counts, cudaStream_t s);
+void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const uint32_t* n_vis_dev,
+                       const uint32_t* bases, uint32_t* const kb[2], uint32_t* const vb[2], BinSort& bs,
+                       cudaStream_t s);
+void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n_max,
+                 const uint32_t* n_dev, uint32_t* bstart, int64_t m, BinSort& bs, cudaStream_t s);
+int tile_sort_passes(int tiles_x, int tiles_y);
+void launch_tile_pass(int p, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
+                      const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases, uint32_t* const kb[2],
+                      uint32_t* const vb[2], BinSort& bs, cudaStream_t s);
 void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s);
 // NEXT-2 (regularize.cu): L_n = A − Nᵀñ per pixel and ñ (either may be NULL); backward adds
 // into the map cotangents gD (atomics), gA, gN (any may be NULL).
