@@ -585,6 +585,71 @@ __device__ __forceinline__ void bwd_accum(PixB& s, float (&g)[NG], const PairAlp
   }
 }
 
+
+// K4 with Blackwell packed FP32 (PPT = 2): the thread's two pixels — rows A and B of one column —
+// as the halves of 64-bit register pairs (see k_render_fwd). Per step the α evaluation is the
+// same IEEE ops per half as pair_power (decisions bit-identical to K3), and the per-splat sums
+// use that the two pixels share dx: of the six moment sums only Σ dA, Σ dA·dy, Σ dA·dy² need
+// both rows; Σ dA·dx = dx Σ dA, Σ dA·dx² = dx² Σ dA, Σ dA·dx·dy = dx Σ dA·dy (likewise for
+// the distortion sums).
+#ifndef RD_K4_PACKED
+#define RD_K4_PACKED 1
+#endif
+struct PixB2 {  // backward state of the thread's two pixels (lo = row A, hi = row B)
+  f2 NPY, T, TFa, Dsuf, gC0, gC1, gC2, gN0, gN1, gN2;
+  f2 gL, d0, D1, A;  // depth distortion (S21)
+};
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { return fma2(b, bc(-1.f), a); }
+
+template <bool DIST, int NG>
+__device__ __forceinline__ void bwd_accum2(PixB2& s, float (&g)[NG], f2 DY, float dx, float eA, float eB, bool actA,
+                                           bool actB, const float4& a1, const float4& a2, const float4& a3,
+                                           const DevOpt& opt) {
+  const float rA = ex2_approx(eA), rB = ex2_approx(eB);  // α_raw = o·exp(−½ΔᵀCΔ)
+  const f2 AL = pk(actA ? fminf(opt.alpha_max, rA) : 0.f, actB ? fminf(opt.alpha_max, rB) : 0.f);
+  const f2 OMA = fma2(AL, bc(-1.f), bc(1.f));  // 1 − α (exact 1 when masked)
+  const f2 RINV = pk(rcp_approx(lo_of(OMA)), rcp_approx(hi_of(OMA)));
+  s.T = mul2(s.T, RINV);  // T_i = T_{i+1} / (1 − α_i)
+  const f2 W = mul2(AL, s.T);
+  f2 DOT = mul2(bc(a1.z), s.gC0);
+  DOT = fma2(bc(a1.w), s.gC1, DOT);
+  DOT = fma2(bc(a2.x), s.gC2, DOT);
+  DOT = fma2(bc(a2.y), s.gN0, DOT);
+  DOT = fma2(bc(a2.z), s.gN1, DOT);
+  DOT = fma2(bc(a2.w), s.gN2, DOT);
+  // ∂L/∂α = T·dot − (D_suf − T_final·(g_A − bg·g_C))/(1 − α)
+  const f2 X = fma2(s.T, DOT, mul2(RINV, sub2(s.TFa, s.Dsuf)));
+  s.Dsuf = fma2(W, DOT, s.Dsuf);
+  const float dlA = actA && rA <= opt.alpha_max ? lo_of(X) : 0.f;  // clamped α: no gradient (S8)
+  const float dlB = actB && rB <= opt.alpha_max ? hi_of(X) : 0.f;
+  const f2 DA = mul2(pk(rA, rB), pk(dlA, dlB));  // dA = α_raw·∂L/∂α
+  const f2 PY = mul2(DA, DY), PYY = mul2(PY, DY);
+  const float S0 = lo_of(DA) + hi_of(DA), S1 = lo_of(PY) + hi_of(PY);
+  g[5] = S0;
+  g[0] = dx * S0;
+  g[2] = dx * g[0];
+  g[1] = S1;
+  g[3] = dx * S1;
+  g[4] = lo_of(PYY) + hi_of(PYY);
+  const f2 C0 = mul2(W, s.gC0), C1 = mul2(W, s.gC1), C2 = mul2(W, s.gC2);
+  const f2 N0 = mul2(W, s.gN0), N1 = mul2(W, s.gN1), N2 = mul2(W, s.gN2);
+  g[6] = lo_of(C0) + hi_of(C0);
+  g[7] = lo_of(C1) + hi_of(C1);
+  g[8] = lo_of(C2) + hi_of(C2);
+  g[9] = lo_of(N0) + hi_of(N0);
+  g[10] = lo_of(N1) + hi_of(N1);
+  g[11] = lo_of(N2) + hi_of(N2);
+  if constexpr (DIST) {  // ∂L_d/∂d = 4 ω (A (d − d0) − D1), ω detached (S21); d of Eq.15 per row
+    const f2 D = fma2(bc(a3.y), bc(dx), fma2(bc(a3.z), DY, bc(a3.x)));
+    const f2 GD = mul2(mul2(s.gL, W), fma2(s.A, sub2(D, s.d0), mul2(s.D1, bc(-1.f))));
+    const f2 GDY = mul2(GD, DY);
+    const float S3 = lo_of(GD) + hi_of(GD);
+    g[12] = S3;
+    g[13] = dx * S3;
+    g[14] = lo_of(GDY) + hi_of(GDY);
+  }
+}
+
 // Median-depth sums Σ g_D, Σ g_D·dx, Σ g_D·dy (G2D f[7..9]) for D = z_c + p·Δ (Eq.4,
 // PAPER:443-450): one pixel per splat at most, so added directly (no warp reduction).
 __device__ __forceinline__ void bwd_median(const PixB& s, G2D* row, const PairAlpha& pa) {
@@ -670,6 +735,20 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
   __syncthreads();
   const int maxlast = s_maxlast;
   const unsigned a_red = smem_addr(sred[warp]);
+  constexpr bool kPk = PPT == 2 && RD_K4_PACKED != 0;
+  const float la_min = __shfl_sync(0xffffffffu, opt.log2_alpha_min, 0);  // a register, not a per-step LDC
+  PixB2 P2;  // kPk: the two pixels' state as packed pairs (s[k] keeps last, med, gD, px)
+  if constexpr (kPk) {
+    const PixB& A = s[0];
+    const PixB& B = s[PPT - 1];
+    P2.NPY = pk(-A.py, -B.py);
+    P2.T = pk(A.T, B.T);
+    P2.TFa = pk(A.TFa, B.TFa);
+    P2.Dsuf = pk(0.f, 0.f);
+    P2.gC0 = pk(A.gC0, B.gC0); P2.gC1 = pk(A.gC1, B.gC1); P2.gC2 = pk(A.gC2, B.gC2);
+    P2.gN0 = pk(A.gN0, B.gN0); P2.gN1 = pk(A.gN1, B.gN1); P2.gN2 = pk(A.gN2, B.gN2);
+    P2.gL = pk(A.gL, B.gL); P2.d0 = pk(A.d0, B.d0); P2.D1 = pk(A.D1, B.D1); P2.A = pk(A.A, B.A);
+  }
 
   for (int end = maxlast; end > 0; end -= BATCH) {
     const int start = max(0, end - BATCH);
@@ -738,6 +817,43 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
       const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
       const PairColumn col = pair_column(a0, ulo, s[0].px);  // the thread's pixels share the column
+      if constexpr (kPk) {
+        // pair_power for both rows at once (the same IEEE ops per half)
+        const f2 DY = add2(add2(bc(a0.y), P2.NPY), bc(ulo.y));
+        const f2 T1 = fma2(bc(a0.w), DY, bc(col.g11dx));
+        const f2 T2s = mul2(bc(a1.x), DY);
+        const f2 E = fma2(fma2(T1, T1, mul2(T2s, T2s)), bc(-1.f), bc(a1.y));
+        const float eA = lo_of(E), eB = hi_of(E);
+        const bool actA = pos < s[0].last && eA >= la_min, actB = pos < s[1].last && eB >= la_min;
+        const bool any = actA || actB;
+        const unsigned am = __ballot_sync(0xffffffffu, any);
+        if (am == 0u) continue;  // warp-uniform: no pixel of this warp uses the splat
+        const float4 a2 = lds128(a + 32u * BATCH);
+        const float4 a3 = DIST ? lds128(a + 48u * BATCH) : a2;
+        constexpr int NG = DIST ? 16 : 12;
+        float g[NG];
+        bwd_accum2<DIST, NG>(P2, g, DY, col.dx, eA, eB, actA, actB, a1, a2, a3, opt);
+        G2D* dst = g2d + lds32(a_id + 4u * j);
+        const bool hA = actA && pos == s[0].med, hB = actB && pos == s[1].med;  // median splat (med = -1 if g_D = 0)
+        if (__any_sync(0xffffffffu, hA || hB)) {
+          if (hA) bwd_median(s[0], dst, PairAlpha{col.dx, lo_of(DY), eA, true});
+          if (hB) bwd_median(s[1], dst, PairAlpha{col.dx, hi_of(DY), eB, true});
+        }
+        if (__popc(am) <= kDirectLanes) {  // few contributing threads: their own atomics, no reduction
+          if (any) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) g2d_add(dst, k, g[k]);
+          }
+        } else {
+          float gv[NV];
+#pragma unroll
+          for (int k = 0; k < NV; ++k) gv[k] = g[k];
+          const float v = smem_reduce<NV>(gv, a_red, lane);
+          const int k = lane >> 1;
+          if ((lane & 1) == 0 && k < NV) g2d_add(dst, k, v);
+        }
+        continue;
+      }
       PairAlpha pa[PPT];
       bool act[PPT];
       bool any = false;
