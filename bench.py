@@ -129,19 +129,20 @@ K5_B_VIS = 600                             # K5: params 236 + 2-D grads 60 + rec
 K5V_B_UNION, K5V_B_VIS, K5V_B_ALL = 576, 224, 4
 
 
-def kernel_work(name, t, views, tile_bits):
+def kernel_work(name, t, views, tile_passes):
     """Algorithmic (bytes or flops, bound) summed over the timed views for one kernel."""
     n, nvis, M = t["n"], t["n_visible"], t["n_duplicates"]
     if name == "preprocess_fwd":
         return K1_B_ALL * n * views + K1_B_VIS * nvis, "hbm"
-    if name == "depth_sort":   # (key, id) 8 B read + 8 B write per radix pass, 4 passes
-        return 16 * 4 * n * views, "hbm"
-    if name == "scan":         # sorted id + gathered count read, offset write
-        return 12 * n * views, "hbm"
-    if name == "duplicate":    # offsets + sorted ids + rects of visible, 8 B (tile, id) per duplicate
-        return 8 * n * views + 8 * nvis + 8 * M, "hbm"
-    if name == "tile_sort":    # (tile, id) 8 B read + 8 B write per pass
-        return 16 * M * math.ceil(tile_bits / 8), "hbm"
+    if name == "depth_sort":   # K2h: key per Gaussian + rect per visible; pass 0: key per Gaussian
+        # read, (key, id) per visible written; passes 1-3: (key, id) read + written per visible
+        return 8 * n * views + (8 + 8 + 3 * 16) * nvis, "hbm"
+    if name == "scan":         # sorted id + gathered count read, offset written, per visible
+        return 12 * nvis, "hbm"
+    if name == "duplicate":    # K2c + first tile pass: offsets, sorted ids, rects of the visible,
+        return 16 * nvis + 8 * M, "hbm"  # (tile, id) 8 B written per duplicate
+    if name == "tile_sort":    # the remaining tile passes: (tile, id) 8 B read + 8 B written
+        return 16 * M * (tile_passes - 1), "hbm"
     if name == "ranges":
         return 4 * M, "hbm"
     if name == "render_fwd":
@@ -477,6 +478,8 @@ def run_gpu(args, cfg_name, config):
             mark()
             if args.k5 == "per-view":
                 P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
+            elif args.k5 == "split":  # K5 geometry now, overlapping the other views' K3/K4
+                P.rd_preprocess_bwd_geometry(vw, g, grads, stream=st)
             slot["done"].record(st)  # batched K5: the round's rd_preprocess_bwd_views waits for this
             mark()
         if ph is not None:
@@ -516,11 +519,14 @@ def run_gpu(args, cfg_name, config):
                 futs = [pool.submit(worker, sl, k) for sl, k in zip(used, rnd)]
                 for f in futs:
                     f.result()
-            if args.k5 == "batched":
+            if args.k5 in ("batched", "split"):
                 k5s = streams["k5"]
                 for sl in used:
                     k5s.wait_event(sl["done"])
-                P.rd_preprocess_bwd_views([sl["view"] for sl in used], g, grads, stream=k5s)
+                if args.k5 == "split":  # the round's SH part (its geometry parts ran per view)
+                    P.rd_preprocess_bwd_views_sh([sl["view"] for sl in used], g, grads, stream=k5s)
+                else:
+                    P.rd_preprocess_bwd_views([sl["view"] for sl in used], g, grads, stream=k5s)
                 k5_done.record(k5s)
                 for sl in used:
                     sl["stream"].wait_event(k5_done)
@@ -786,13 +792,13 @@ def run_gpu(args, cfg_name, config):
     tim_ext = dict(tim)
     tim_ext["n"] = n
     st = P.rd_view_stats(view)
-    tile_bits = st["key_bits"] - 32
+    tile_passes = (2 if st["tiles_x"] > 256 else 1) + (2 if st["tiles_y"] > 256 else 1)
     kernels = {}
     for name, ms in tim["ms"].items():
         launches = tim["launches"][name]
         if launches == 0:
             continue
-        work, bound = kernel_work(name, tim_ext, views_timed, tile_bits)
+        work, bound = kernel_work(name, tim_ext, views_timed, tile_passes)
         avg_ms = ms / launches
         per_launch = work / launches
         if bound == "hbm":
@@ -822,14 +828,13 @@ def run_gpu(args, cfg_name, config):
                                  "K1 12 B per Gaussian + 300 B per visible, K5 600 B per visible (batched K5: "
                                  "DESIGN.md §7)")}
 
-    # kernel launches (ours + the CUB sort/scan kernels compiled into librade.so): per view K1,
-    # depth sort (histogram + exclusive-sum + 4 onesweep passes), scan (init + scan), duplicate,
-    # tile sort (histogram + exclusive-sum + passes), ranges, tile order, K3, K4, K5b + K5b64;
-    # per round of views the batched SH kernel (or K5a per view)
-    launches_per_view = 1 + (2 + 4) + 2 + 1 + (2 + math.ceil(tile_bits / 8)) + 1 + 1 + 1 + 1 + 2
+    # kernel launches (all ours, librade.so): per view K1, K2h, 4 depth passes, scan, the tile
+    # passes (the first fused with the duplicate generation), ranges, tile order, K3, K4,
+    # K5b + K5b64; per round of views the batched SH kernel (or K5a per view)
+    launches_per_view = 1 + 1 + 4 + 1 + tile_passes + 1 + 1 + 1 + 1 + 2
     views_per_rank = args.steps * B
     rounds = args.steps * math.ceil(B / P_)
-    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 == "batched" else views_per_rank)
+    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split") else views_per_rank)
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)
     config.update({
@@ -882,7 +887,7 @@ def main():
     ap.add_argument("--views-per-step", default="4",
                     help="views per rank per step, or 'epoch' (ceil(views / ranks): one all-reduce per epoch)")
     ap.add_argument("--bucket-mb", type=int, default=64, help="all-reduce bucket size (N > 1)")
-    ap.add_argument("--k5", default="batched", choices=["batched", "per-view"],
+    ap.add_argument("--k5", default="batched", choices=["batched", "split", "per-view"],
                     help="K5 of a round of views in one rd_preprocess_bwd_views call, or per view")
     ap.add_argument("--guard-band", type=float, default=None,
                     help="reading S6b guard band (0 = off); default: the config's (C3/C4 0.15, others off)")

@@ -259,6 +259,20 @@ rd_status rd_preprocess_bwd(rd_view* view, const rd_gaussians* g, const rd_grads
 rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
                                   const rd_grads* grads, rd_stream stream);
 
+/* K5 in two parts, for a caller that pipelines the views of a step: the GEOMETRY part of one
+ * view (K5b64 + K5b: the chain rule of its 2-D gradients through the projection, conic, depth
+ * plane and normal into means, scales, rotations, opacities — and means2d — plus the
+ * 3D-filter mapping) may run on the view's stream right after its
+ * rd_blend_bwd, while other views still blend; the SH part of a round of views (the colour
+ * gradient into the SH rows and its view-direction term of dL/dμ) runs once all
+ * of them are done. rd_preprocess_bwd_geometry on each view + rd_preprocess_bwd_views_sh on
+ * the round = rd_preprocess_bwd_views on the round (up to the fp32 summation order: every
+ * part adds with reductions). Same arguments, ordering rules and errors as
+ * rd_preprocess_bwd / rd_preprocess_bwd_views; each is timed as a K5 launch. */
+rd_status rd_preprocess_bwd_geometry(rd_view* view, const rd_gaussians* g, const rd_grads* grads, rd_stream stream);
+rd_status rd_preprocess_bwd_views_sh(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
+                                     const rd_grads* grads, rd_stream stream);
+
 /* NEXT-2: normal consistency (reading S22) on rendered maps (device, fp32,
  * the layouts of rd_render_fwd): ñ = the finite-difference normal of the median depth map
  * (back-project the pixel and its right / lower neighbours with the camera intrinsics,

@@ -500,7 +500,8 @@ rd_status rd_blend_bwd_ex(rd_view* v, const rd_bwd_cotangents* cot, rd_stream st
   return RD_OK;
 }
 
-rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* grads, rd_stream stream) {
+static rd_status preprocess_bwd_parts(rd_view* v, const rd_gaussians* g, const rd_grads* grads, rd_stream stream,
+                                      int parts) {
   g_err.clear();
   if (!v || !g || !grads) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/gaussians/grads");
   if (v->stage < 4) return fail(RD_ERR_STATE, "rd_preprocess_bwd before rd_blend_bwd");
@@ -519,14 +520,22 @@ rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* g
   DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh, grads->means2d};
   v->begin(s);
   launch_preprocess_bwd(dg, v->cam, v->opt, (const uint32_t*)v->touched.ptr, (const uint32_t*)v->vis.ptr, v->n_vis,
-                        (const uint32_t*)v->big.ptr, v->n_big, (const G2D*)v->g2d.ptr, dgr, s);
+                        (const uint32_t*)v->big.ptr, v->n_big, (const G2D*)v->g2d.ptr, dgr, s, parts);
   RD_CHECK_LAUNCH("preprocess_bwd");
   v->end(K_PREBWD, s);
   return RD_OK;
 }
 
-rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g, const rd_grads* grads,
-                                  rd_stream stream) {
+rd_status rd_preprocess_bwd(rd_view* v, const rd_gaussians* g, const rd_grads* grads, rd_stream stream) {
+  return preprocess_bwd_parts(v, g, grads, stream, kK5All);
+}
+
+rd_status rd_preprocess_bwd_geometry(rd_view* v, const rd_gaussians* g, const rd_grads* grads, rd_stream stream) {
+  return preprocess_bwd_parts(v, g, grads, stream, kK5Geometry);
+}
+
+static rd_status preprocess_bwd_views_parts(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
+                                            const rd_grads* grads, rd_stream stream, int parts) {
   g_err.clear();
   if (!views || !g || !grads) return fail(RD_ERR_INVALID_ARGUMENT, "NULL views/gaussians/grads");
   if (n_views < 1 || n_views > kMaxBatchViews)
@@ -569,10 +578,21 @@ rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const 
   DevGrads dgr{grads->means, grads->scales, grads->rotations, grads->opacities, grads->sh, grads->means2d};
   rd_view* v0 = views[0];
   v0->begin(s);  // timed on views[0] (K_PREBWD, one launch for the batch)
-  launch_preprocess_bwd_views(dg, v0->opt, n_views, cams, touched, g2d, vis, n_vis, big, n_big, dgr, v0->ctr(), s);
+  launch_preprocess_bwd_views(dg, v0->opt, n_views, cams, touched, g2d, vis, n_vis, big, n_big, dgr, v0->ctr(), s,
+                              parts);
   RD_CHECK_LAUNCH("preprocess_bwd_views");
   v0->end(K_PREBWD, s);
   return RD_OK;
+}
+
+rd_status rd_preprocess_bwd_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g, const rd_grads* grads,
+                                  rd_stream stream) {
+  return preprocess_bwd_views_parts(views, n_views, g, grads, stream, kK5All);
+}
+
+rd_status rd_preprocess_bwd_views_sh(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
+                                     const rd_grads* grads, rd_stream stream) {
+  return preprocess_bwd_views_parts(views, n_views, g, grads, stream, kK5Sh);
 }
 
 rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,

@@ -1034,11 +1034,12 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
-                           DevGrads grads, cudaStream_t s) {
+                           DevGrads grads, cudaStream_t s, int parts) {
   if (g.n == 0) return;
   const int threads = 128;
   const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
-  if ((g.sh_coeffs * 3) % 4 == 0) {
+  if (!(parts & kK5Sh)) {
+  } else if ((g.sh_coeffs * 3) % 4 == 0) {
     const unsigned cblocks = (unsigned)((n_vis + 63) / 64);
 #define RD_K5A(D) \
   if (cblocks) k_preprocess_bwd_sh_coop<D><<<cblocks, 64, 0, s>>>(g, cam, opt, vis, n_vis, g2d, grads)
@@ -1061,6 +1062,7 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
   }
   // K5b64 (few, fp64, latency-bound) first; K5b as its programmatic dependent, so the two
   // run side by side instead of K5b64's ~11 µs trailing K5b
+  if (!(parts & kK5Geometry)) return;
   if (n_big > 0)
     k_preprocess_bwd64<<<(unsigned)((n_big + 127) / 128), 128, 0, s>>>(g, cam, opt, big, n_big, g2d, grads);
   if (n_vis > 0) {
@@ -1080,7 +1082,7 @@ void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, const DevCam* cams,
                                  const uint32_t* const* touched, const G2D* const* g2d, const uint32_t* const* vis,
                                  const int64_t* n_vis, const uint32_t* const* big, const int64_t* n_big,
-                                 DevGrads grads, Counter* counters, cudaStream_t s) {
+                                 DevGrads grads, Counter* counters, cudaStream_t s, int parts) {
   if (g.n == 0 || nv <= 0) return;
   ViewsBwd vb{};
   vb.nv = nv;
@@ -1089,7 +1091,8 @@ void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, c
     vb.touched[v] = touched[v];
     vb.g2d[v] = g2d[v];
   }
-  if ((g.sh_coeffs * 3) % 4 == 0) {
+  if (!(parts & kK5Sh)) {
+  } else if ((g.sh_coeffs * 3) % 4 == 0) {
     const unsigned cblocks = (unsigned)((g.n + 63) / 64);
 #define RD_K5AV(D) k_preprocess_bwd_sh_views<D><<<cblocks, 64, 0, s>>>(g, opt, vb, grads, counters)
     switch (opt.sh_degree) {
@@ -1114,6 +1117,7 @@ void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, c
   }
   // geometry per view: its fp64 big list, then the fp32 pass over its visible list as the big
   // list's programmatic dependent (rows are only ever added by reductions)
+  if (!(parts & kK5Geometry)) return;
   for (int v = 0; v < nv; ++v) {
     if (n_big[v] > 0)
       k_preprocess_bwd64<<<(unsigned)((n_big[v] + 127) / 128), 128, 0, s>>>(g, cams[v], opt, big[v], n_big[v], g2d[v],

@@ -199,9 +199,12 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
                            uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s);
 // K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry: fp32 in id
 // order for the visible Gaussians that are not is_big, fp64 over the big list).
+// K5 parts: the SH colour (+ view-direction) part and the geometry part (K5b64 + K5b); both
+// add into the gradients with reductions, so they may run in any order
+constexpr int kK5Sh = 1, kK5Geometry = 2, kK5All = 3;
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
-                           DevGrads grads, cudaStream_t s);
+                           DevGrads grads, cudaStream_t s, int parts = kK5All);
 // K5 for nv ≤ kMaxBatchViews views of the same Gaussians at once (rd_preprocess_bwd_views):
 // per-view cameras, tiles_touched, G2D rows, visible and big lists; gradients += the sum over
 // the views (the SH part fused over the views, the geometry part per view).
@@ -209,7 +212,7 @@ constexpr int kMaxBatchViews = 8;
 void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, const DevCam* cams,
                                  const uint32_t* const* touched, const G2D* const* g2d, const uint32_t* const* vis,
                                  const int64_t* n_vis, const uint32_t* const* big, const int64_t* n_big,
-                                 DevGrads grads, Counter* counters, cudaStream_t s);
+                                 DevGrads grads, Counter* counters, cudaStream_t s, int parts = kK5All);
 // debug: G2D rows → f32 [n][16] (m[0..4], f[0..9], 0)
 void launch_g2d_to_f32(const G2D* g2d, int64_t n, float* out, cudaStream_t s);
 // K2 (binning.cu). Sorts return the CUB DoubleBuffer selector (1: result in the *1 buffers).

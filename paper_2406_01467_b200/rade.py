@@ -392,6 +392,28 @@ def rd_preprocess_bwd_views(views, gaussians: Gaussians, grads: Gaussians, strea
 _VP_T = ctypes.c_void_p
 
 
+def rd_preprocess_bwd_geometry(view: View, gaussians: Gaussians, grads: Gaussians, stream=None):
+    """K5 geometry part of one view (K5b64 + K5b), right after its rd_blend_bwd; the SH part of
+    the round follows with rd_preprocess_bwd_views_sh."""
+    g = gaussians.c_struct()
+    gr = _grads_struct(grads)
+    N.check(view.lib.rd_preprocess_bwd_geometry(view.handle, ctypes.byref(g), ctypes.byref(gr), _stream_ptr(stream)),
+            "rd_preprocess_bwd_geometry")
+    return grads
+
+
+def rd_preprocess_bwd_views_sh(views, gaussians: Gaussians, grads: Gaussians, stream=None):
+    """K5 SH part of a round of views (rows read and reduced once), after their geometry parts
+    may already have run."""
+    views = list(views)
+    arr = (_VP_T * len(views))(*[v.handle for v in views])
+    g = gaussians.c_struct()
+    gr = _grads_struct(grads)
+    N.check(N.load().rd_preprocess_bwd_views_sh(arr, len(views), ctypes.byref(g), ctypes.byref(gr),
+                                                _stream_ptr(stream)), "rd_preprocess_bwd_views_sh")
+    return grads
+
+
 def rd_preprocess_bwd(view: View, gaussians: Gaussians, grads: Gaussians, stream=None):
     """K5 only: accumulates (+=) parameter gradients from the last rd_blend_bwd of the view."""
     g = gaussians.c_struct()

@@ -320,16 +320,20 @@ def test_c3_batched_k5_equals_per_view_sum(c3):
         P.rd_blend_bwd(v, cot[0:3], cot[3], cot[4:7], cot[7])
         views.append(v)
     assert sum(P.rd_view_stats(v)["n_big"] for v in views) > 0
-    ga, gb = g.zeros_like(), g.zeros_like()
+    ga, gb, gc = g.zeros_like(), g.zeros_like(), g.zeros_like()
     P.rd_preprocess_bwd_views(views, g, ga)
     for v in views:
         P.rd_preprocess_bwd(v, g, gb)
+    for v in views:  # bench --k5 split: geometry per view, then the round's SH part
+        P.rd_preprocess_bwd_geometry(v, g, gc)
+    P.rd_preprocess_bwd_views_sh(views, g, gc)
     torch.cuda.synchronize()
-    a, b = grads_to_rows(ga, g.n), grads_to_rows(gb, g.n)
+    a, b, c = grads_to_rows(ga, g.n), grads_to_rows(gb, g.n), grads_to_rows(gc, g.n)
     for sl in (slice(0, 3), slice(3, 6), slice(6, 10), slice(10, 11), slice(11, 59)):
         nb = np.linalg.norm(b[:, sl])
         assert nb > 0
         assert np.linalg.norm(a[:, sl] - b[:, sl]) <= 1e-5 * nb, sl
+        assert np.linalg.norm(c[:, sl] - b[:, sl]) <= 1e-5 * nb, sl
 
 
 def _sampled_grad_check(scene, cam, opt, g, view, cot, rng, groups, label):

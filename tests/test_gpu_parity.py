@@ -789,8 +789,13 @@ def test_batched_k5_matches_oracle_sum_over_views(which):
     gs = g.zeros_like()
     for v in views:
         P.rd_preprocess_bwd(v, g, gs)
+    gp = g.zeros_like()  # split: geometry per view, then the round's SH part
+    for v in views:
+        P.rd_preprocess_bwd_geometry(v, g, gp)
+    P.rd_preprocess_bwd_views_sh(views, g, gp)
     torch.cuda.synchronize()
     B, S = grads_to_rows(gb, scene.n), grads_to_rows(gs, scene.n)
+    Sp = grads_to_rows(gp, scene.n)
     for name, sl in {"means": slice(0, 3), "scales": slice(3, 6), "rotations": slice(6, 10),
                      "opacities": slice(10, 11), "sh": slice(11, 59)}.items():
         a, b = B[:, sl], R[:, sl]
@@ -800,6 +805,7 @@ def test_batched_k5_matches_oracle_sum_over_views(which):
         med = np.median(np.abs(b[b != 0]))
         assert not (np.abs(a - b) > 1e-3 * np.abs(b) + 1e-3 * med).any(), name
         assert np.linalg.norm(a - S[:, sl]) <= 1e-5 * np.linalg.norm(S[:, sl]), name
+        assert np.linalg.norm(Sp[:, sl] - a) <= 1e-5 * np.linalg.norm(a), name
 
 
 def test_batched_k5_argument_errors():
@@ -809,13 +815,17 @@ def test_batched_k5_argument_errors():
     g, views = _views_of(scene, cams, opt, cots)
     gr = g.zeros_like()
     for bad, status in (([views[0], views[0]], 1), ([views[0]] * 9, 1), ([], 1)):
-        with pytest.raises(P.rade.N.RadeError) as e:
-            P.rd_preprocess_bwd_views(bad, g, gr)
-        assert e.value.status == status
+        for fn in (P.rd_preprocess_bwd_views, P.rd_preprocess_bwd_views_sh):
+            with pytest.raises(P.rade.N.RadeError) as e:
+                fn(bad, g, gr)
+            assert e.value.status == status
     fresh = P.View()
     P.rd_preprocess(fresh, g, cams[0], opts_dict(opt))
     with pytest.raises(P.rade.N.RadeError) as e:
         P.rd_preprocess_bwd_views([views[0], fresh], g, gr)
+    assert e.value.status == 2
+    with pytest.raises(P.rade.N.RadeError) as e:
+        P.rd_preprocess_bwd_geometry(fresh, g, gr)
     assert e.value.status == 2
 
 
