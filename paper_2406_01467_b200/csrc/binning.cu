@@ -46,6 +46,9 @@ namespace {
 #ifndef RD_SORT_THREADS
 #define RD_SORT_THREADS 512
 #endif
+#ifndef RD_RANK_MATCH
+#define RD_RANK_MATCH 0  // 1: __match_any_sync ranking instead of the 8 ballots
+#endif
 constexpr int kST = RD_SORT_THREADS;  // threads per sort block
 constexpr int kSI = 8;            // items per thread
 constexpr int kSTile = kST * kSI; // items per block
@@ -405,13 +408,14 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
   uint32_t key[kSI], val[kSI];
   bool ok[kSI];
   if constexpr (MODE != kTileGen) {  // loads first: their latency overlaps the set-up below
+    const uint32_t p0 = (uint32_t)base + (uint32_t)(warp * 256 + lane), nn = (uint32_t)n;  // < 2^31
 #pragma unroll
     for (int j = 0; j < kSI; ++j) {
-      const int64_t p = base + warp * 256 + j * 32 + lane;
-      ok[j] = p < n;
+      const uint32_t p = p0 + (uint32_t)(j * 32);
+      ok[j] = p < nn;
       key[j] = ok[j] ? a.keys_in[p] : 0u;
       if constexpr (MODE == kDepthFirst) {
-        val[j] = (uint32_t)p;
+        val[j] = p;
       } else {
         val[j] = ok[j] ? a.vals_in[p] : 0u;
       }
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
 #pragma unroll
     for (int j = 0; j < kSI; ++j) {
       const int p = warp * 256 + j * 32 + lane;
-      ok[j] = base + p < n;
+      ok[j] = (uint32_t)base + (uint32_t)p < (uint32_t)n;
       key[j] = sm.pass.key[p];
       val[j] = sm.pass.val[p];
     }
@@ -456,13 +460,16 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
 #pragma unroll
   for (int j = 0; j < kSI; ++j) {
     const uint32_t d = (key[j] >> a.shift) & 255u;
+#if RD_RANK_MATCH
+    const unsigned peers = __match_any_sync(0xffffffffu, ok[j] ? d : 256u);
+#else
     unsigned peers = __ballot_sync(0xffffffffu, ok[j]);
 #pragma unroll
-    for (int bit = 0; bit < 8; ++bit) {
-      const bool on = (d >> bit) & 1u;
-      const unsigned bb = __ballot_sync(0xffffffffu, on);
-      peers &= on ? bb : ~bb;
+    for (int bit = 0; bit < 8; ++bit) {  // m = all ones where this lane's digit has the bit
+      const unsigned m = (unsigned)((int)(d << (31 - bit)) >> 31);
+      peers &= ~(__ballot_sync(0xffffffffu, (int)m < 0) ^ m);
     }
+#endif
     uint32_t c = 0u;
     if (ok[j]) c = sm.pass.cnt[warp][d];
     __syncwarp();
