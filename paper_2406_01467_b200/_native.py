@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librade.so")
+# RADE_LIB selects another build of the same ABI (e.g. librade_checks.so, the RD_CHECKS build)
+LIB_PATH = os.environ.get("RADE_LIB") or os.path.join(HERE, "librade.so")
 
 RD_OK, RD_ERR_INVALID_ARGUMENT, RD_ERR_STATE, RD_ERR_ALLOC, RD_ERR_CUDA = range(5)
 STATUS_NAMES = {0: "RD_OK", 1: "RD_ERR_INVALID_ARGUMENT", 2: "RD_ERR_STATE", 3: "RD_ERR_ALLOC", 4: "RD_ERR_CUDA"}

@@ -156,6 +156,9 @@ struct rd_view {
     pending.push_back(Ev{cur_a, b, k});
   }
   Counter* ctr() { return prof ? (Counter*)counters.ptr : nullptr; }
+  DevBounds bounds() const {
+    return DevBounds{n, M, (int64_t)(bmask.cap / sizeof(uint32_t)), (int64_t)tiles_x * tiles_y};
+  }
   void resolve() {
     for (const Ev& e : pending) {
       float ms = 0.f;
@@ -407,7 +410,7 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
     const int np = tile_sort_passes(v->tiles_x, v->tiles_y);
     for (int p = 0; p < np; ++p) {
       v->begin(s);
-      launch_tile_pass(p, M, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect.ptr,
+      launch_tile_pass(p, M, v->n_vis, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect.ptr,
                        (const uint32_t*)v->bstart.ptr, v->tiles_x, v->tiles_y, bases, tk, tv, v->bs, s);
       RD_CHECK_LAUNCH(p == 0 ? "duplicate" : "tile_sort");
       if (p == 0) {
@@ -453,7 +456,7 @@ rd_status rd_render_fwd_ex(rd_view* v, const rd_fwd_maps* maps, rd_stream stream
   launch_render_fwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, maps->color, maps->depth, maps->normal, maps->alpha,
                     (float*)v->T_final.ptr, (int32_t*)v->n_contrib.ptr, (int32_t*)v->median_pos.ptr, dio,
-                    (uint32_t*)v->bmask.ptr, (uint32_t*)v->tile_order.ptr, v->ctr(), s);
+                    (uint32_t*)v->bmask.ptr, (uint32_t*)v->tile_order.ptr, v->ctr(), v->bounds(), s);
   RD_CHECK_LAUNCH("render_fwd");
   v->end(K_FWD, s);
   v->acc_views += 1;
@@ -493,7 +496,8 @@ rd_status rd_blend_bwd_ex(rd_view* v, const rd_bwd_cotangents* cot, rd_stream st
   launch_render_bwd(v->cam, v->opt, v->tiles_x, v->tiles_y, (const uint2*)v->ranges.ptr, ids,
                     (const Record*)v->rec.ptr, (const float*)v->T_final.ptr, (const int32_t*)v->n_contrib.ptr,
                     (const int32_t*)v->median_pos.ptr, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha, dio,
-                    (const uint32_t*)v->bmask.ptr, (const uint32_t*)v->tile_order.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
+                    (const uint32_t*)v->bmask.ptr, (const uint32_t*)v->tile_order.ptr, (G2D*)v->g2d.ptr, v->ctr(),
+                    v->bounds(), s);
   RD_CHECK_LAUNCH("render_bwd");
   v->end(K_BWD, s);
   v->stage = 4;

@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kHistThreads) k_bin_hist(int64_t n, const uint
     }
     if (vis) {
       const int x0 = (int)(q.x & 0xffffu), y0 = (int)(q.x >> 16), x1 = (int)(q.y & 0xffffu), y1 = (int)(q.y >> 16);
+      RD_CHECK(x0 < x1 && x1 <= tiles_x && y0 < y1 && y1 <= tiles_y);
       atomicAdd(&sx[x0], y1 - y0);
       atomicSub(&sx[x1], y1 - y0);
       atomicAdd(&sy[y0], x1 - x0);
@@ -302,6 +303,7 @@ struct PassArgs {
   const uint32_t* __restrict__ sorted_ids;
   const uint2* __restrict__ rect;
   const uint32_t* __restrict__ bstart;
+  int64_t n_gauss;  // entries of offsets / sorted_ids (RD_CHECKS)
   unsigned long long* status;
   uint32_t epoch;
 };
@@ -330,6 +332,7 @@ __device__ __forceinline__ void generate_dups(const PassArgs& a, GenSmem& g, int
                                               uint32_t (&key)[kSI], uint32_t (&val)[kSI]) {
   const uint32_t g0 = a.bstart[b];
   const int ng = (int)(a.bstart[b + 1] - g0) + 1;
+  RD_CHECK(ng >= 1 && ng <= kSTile + 1 && (int64_t)g0 + ng <= a.n_gauss);
   if (threadIdx.x == 0) g.end[0] = g0 == 0 ? 0u : a.offsets[g0 - 1];
   for (int k = threadIdx.x; k < ng; k += kST) {
     g.end[k + 1] = a.offsets[g0 + k];
@@ -512,6 +515,7 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
     if (ok[j]) {
       const uint32_t d = (key[j] >> a.shift) & 255u;
       const uint32_t p = s_lstart[d] + sm.pass.cnt[warp][d] + rank[j];
+      RD_CHECK(p < (uint32_t)kSTile);
       sm.pass.key[p] = key[j];
       sm.pass.val[p] = val[j];
     }
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
   for (int i = tid; i < cnt; i += kST) {
     const uint32_t k = sm.pass.key[i];
     const uint32_t dst = s_dst[(k >> a.shift) & 255u] + (uint32_t)i;
+    RD_CHECK(dst < s_gbase[kRadix]);
     uint32_t out = k;
     if constexpr (MODE == kTile || MODE == kTileGen)
       if (a.last) out = (k >> 16) * (uint32_t)a.tiles_x + (k & 0xffffu);
@@ -580,7 +585,10 @@ __global__ void __launch_bounds__(kST) k_scan(const uint32_t* __restrict__ n_dev
   for (int j = 0; j < kSI; ++j) {
     if (p0 + j < n) {
       const uint32_t hi = e + v[j], lo = hi - t[j];  // this Gaussian's outputs [lo, hi)
-      for (uint32_t ob = (lo + kSTile - 1) / kSTile; ob * (uint32_t)kSTile < hi; ++ob) bstart[ob] = (uint32_t)(p0 + j);
+      for (uint32_t ob = (lo + kSTile - 1) / kSTile; ob * (uint32_t)kSTile < hi; ++ob) {
+        RD_CHECK(ob < out_blocks);
+        bstart[ob] = (uint32_t)(p0 + j);
+      }
       if (p0 + j == n - 1) bstart[out_blocks] = (uint32_t)(p0 + j);
     }
   }
@@ -708,9 +716,9 @@ int tile_sort_passes(int tiles_x, int tiles_y) {
 }
 
 // Tile pass p writes buffer p % 2; pass 0 generates the duplicates (K2c) from the scan.
-void launch_tile_pass(int p, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
-                      const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases, uint32_t* const kb[2],
-                      uint32_t* const vb[2], BinSort& bs, cudaStream_t s) {
+void launch_tile_pass(int p, int64_t m, int64_t n_gauss, const uint32_t* offsets, const uint32_t* sorted_ids,
+                      const uint2* rect, const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases,
+                      uint32_t* const kb[2], uint32_t* const vb[2], BinSort& bs, cudaStream_t s) {
   if (m == 0) return;
   set_carveout_once();
   TilePass tp[4];
@@ -730,6 +738,7 @@ void launch_tile_pass(int p, int64_t m, const uint32_t* offsets, const uint32_t*
   a.sorted_ids = sorted_ids;
   a.rect = rect;
   a.bstart = bstart;
+  a.n_gauss = n_gauss;
   a.status = bs.status;
   a.epoch = ++bs.epoch;
   if (p == 0)

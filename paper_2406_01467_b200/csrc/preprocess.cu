@@ -471,12 +471,16 @@ __global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(De
   bbase = __shfl_sync(0xffffffffu, bbase, 0);
   const unsigned below = (1u << lane) - 1u;
   if (nt > 0u) {
+    RD_CHECK((int64_t)(base + __popc(vmask & below)) < g.n);
     vis[base + __popc(vmask & below)] = (uint32_t)i;
     float4* row = reinterpret_cast<float4*>(g2d + i);
 #pragma unroll
     for (int q = 0; q < 5; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  if (bigg) big[bbase + __popc(bmask & below)] = (uint32_t)i;
+  if (bigg) {
+    RD_CHECK((int64_t)(bbase + __popc(bmask & below)) < g.n);
+    big[bbase + __popc(bmask & below)] = (uint32_t)i;
+  }
 }
 
 // ---------------------------------------------------------------------------- K5

@@ -6,6 +6,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef RD_CHECKS
+#include <cstdio>
+#endif
 
 namespace rade {
 
@@ -166,6 +169,34 @@ __device__ __forceinline__ PairAlpha pair_power(const float4& r0, float g22, flo
 // Depth distortion (reading S21) plumbing: K3 writes the L_d map (dist, may be NULL) and the
 // per-pixel state d0 (first blended depth) and D1 = Σω(d − d0) when d0 != NULL; K4 adds the
 // L_d gradient when dL_ddist != NULL (then d0/D1 must hold K3's values).
+// Debug build (-DRD_CHECKS, `python -m paper_2406_01467_b200.build --checks` → librade_checks.so,
+// selected with RADE_LIB): device-side bounds assertions on the index math of the binning
+// passes, K1's list appends and K3/K4's staging, blend-mask words and record gathers — a
+// failed check prints its condition and traps (the launch fails with an error). compute-
+// sanitizer is not available on the GPU pool, so this build plus the bit-exact / rerun
+// determinism tests stand in for memcheck / racecheck.
+#ifdef RD_CHECKS
+#define RD_CHECK(cond)                                                                                         \
+  do {                                                                                                         \
+    if (!(cond)) {                                                                                             \
+      printf("RD_CHECK failed %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #cond, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                                \
+      __trap();                                                                                                \
+    }                                                                                                          \
+  } while (0)
+#else
+#define RD_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+// Capacities the RD_CHECKS build checks K3/K4's indices against (unused otherwise).
+struct DevBounds {
+  int64_t n;           // Gaussians (records)
+  int64_t m;           // duplicates (sorted ids)
+  int64_t mask_words;  // blend-mask words
+  int64_t n_tiles;
+};
+
 struct DistIO {
   float* dist;
   float* d0;
@@ -242,9 +273,9 @@ void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const ui
 void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n_max,
                  const uint32_t* n_dev, uint32_t* bstart, int64_t m, BinSort& bs, cudaStream_t s);
 int tile_sort_passes(int tiles_x, int tiles_y);
-void launch_tile_pass(int p, int64_t m, const uint32_t* offsets, const uint32_t* sorted_ids, const uint2* rect,
-                      const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases, uint32_t* const kb[2],
-                      uint32_t* const vb[2], BinSort& bs, cudaStream_t s);
+void launch_tile_pass(int p, int64_t m, int64_t n_gauss, const uint32_t* offsets, const uint32_t* sorted_ids,
+                      const uint2* rect, const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases,
+                      uint32_t* const kb[2], uint32_t* const vb[2], BinSort& bs, cudaStream_t s);
 void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s);
 // NEXT-2 (regularize.cu): L_n = A − Nᵀñ per pixel and ñ (either may be NULL); backward adds
 // into the map cotangents gD (atomics), gA, gN (any may be NULL).
@@ -274,12 +305,12 @@ inline size_t blend_mask_words(int64_t m, int n_tiles) { return (size_t)(m / 32)
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal,
                        float* alpha, float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
-                       uint32_t* bmask, uint32_t* order, Counter* counters, cudaStream_t s);
+                       uint32_t* bmask, uint32_t* order, Counter* counters, const DevBounds& bd, cudaStream_t s);
 void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, const float* T_final, const int32_t* n_contrib,
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
                        const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio,
                        const uint32_t* bmask, const uint32_t* order, G2D* g2d, Counter* counters,
-                       cudaStream_t s);
+                       const DevBounds& bd, cudaStream_t s);
 
 }  // namespace rade

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
                                                                 int32_t* __restrict__ median_pos,
                                                                 DistIO dio, uint32_t* __restrict__ bmask,
                                                                 const uint32_t* __restrict__ order,
-                                                                Counter* __restrict__ counters) {
+                                                                Counter* __restrict__ counters, DevBounds bd) {
   constexpr int NT = TILE * TILE / 2;  // threads
   constexpr int NW = NT / 32;          // warps = 8×8 quadrants
   constexpr int BATCH = batch_of(TILE);  // splats staged per round
@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   constexpr bool kFilter = TILE > 8 || RD_K3_FILTER8;
   constexpr bool kMask = TILE == 8;    // one warp per tile: it records the blend mask for K4
   const int tile = (int)order[blockIdx.x];
+  RD_CHECK(tile >= 0 && tile < bd.n_tiles);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
   const int qx = tx * TILE + (warp % (TILE / 8)) * 8, qy = ty * TILE + (warp / (TILE / 8)) * 8;
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   const float fx0 = (float)qx + 0.5f, fy0 = (float)qy + 0.5f;  // pixel-centre rectangle of the quadrant
   const uint2 range = ranges[tile];
   const int total = (int)(range.y - range.x);
+  RD_CHECK(range.x <= range.y && (int64_t)range.y <= bd.m);
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   __shared__ uint16_t wlist[kFilter ? NW : 1][kFilter ? BATCH : 1];
@@ -333,6 +335,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const int t = (int)threadIdx.x + h * NT;
       const int k = base + t;
       if (t < BATCH && k < total) {
+        RD_CHECK((int64_t)ids[range.x + k] < bd.n);
         const Record* r = rec + ids[range.x + k];
         s0[t] = r->r0;
         s1[t] = r->r1;
@@ -435,6 +438,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
       const unsigned lo = __ballot_sync(0xffffffffu, mine & 1u);  // the list's end may be the
       const unsigned hi = __ballot_sync(0xffffffffu, mine & 2u);  // next tile's first
       if (lane == 0) {
+        RD_CHECK((int64_t)blend_mask_word(range.x, base, tile) + (base + 32 < total ? 1 : 0) < bd.mask_words);
         uint32_t* w = bmask + blend_mask_word(range.x, base, tile);
         w[0] = lo;
         if (base + 32 < total) w[1] = hi;
@@ -689,7 +693,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
     const int32_t* __restrict__ median_pos, const float* __restrict__ dL_dcolor, const float* __restrict__ dL_ddepth,
     const float* __restrict__ dL_dnormal, const float* __restrict__ dL_dalpha, DistIO dio,
     const uint32_t* __restrict__ bmask, const uint32_t* __restrict__ order, G2D* __restrict__ g2d,
-    Counter* __restrict__ counters) {
+    Counter* __restrict__ counters, DevBounds bd) {
   constexpr int NT = TILE * TILE / PPT;
   constexpr int NW = NT / 32;
   constexpr int BATCH = batch_of(TILE);
@@ -700,6 +704,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
   static_assert(NT % 32 == 0 && TILE % SH == 0, "whole warps tiling the tile");
   static_assert(!kMask || NW == 1, "the blend mask is per tile = per warp");
   const int tile = (int)order[blockIdx.x];
+  RD_CHECK(tile >= 0 && tile < bd.n_tiles);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
   const int qx = tx * TILE + (warp % (TILE / 8)) * 8, qy = ty * TILE + (warp / (TILE / 8)) * SH;
@@ -708,6 +713,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
   const float fx0 = (float)qx + 0.5f, fy0 = (float)qy + 0.5f;
   const uint2 range = ranges[tile];
   const int HW = cam.W * cam.H;
+  RD_CHECK(range.x <= range.y && (int64_t)range.y <= bd.m);
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
   __shared__ uint32_t sid[BATCH];
@@ -734,6 +740,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
   if (mylast > 0) atomicMax(&s_maxlast, mylast);
   __syncthreads();
   const int maxlast = s_maxlast;
+  RD_CHECK(maxlast <= (int)(range.y - range.x));
   const unsigned a_red = smem_addr(sred[warp]);
   constexpr bool kPk = PPT == 2 && RD_K4_PACKED != 0;
   const float la_min = __shfl_sync(0xffffffffu, opt.log2_alpha_min, 0);  // a register, not a per-step LDC
@@ -757,6 +764,8 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
     unsigned long long bm = 0ull;
     if (kMask) {  // the batch's 64 mask bits (relative positions 0..cnt-1)
       const unsigned sh = (unsigned)start & 31u;
+      RD_CHECK((int64_t)blend_mask_word(range.x, start, tile) + ((unsigned)start % 32u + (unsigned)cnt > 64u ? 2 : 1) <
+               bd.mask_words);
       const uint32_t* w = bmask + blend_mask_word(range.x, start, tile);
       const unsigned long long lo = (unsigned long long)w[0] | ((unsigned long long)w[1] << 32);
       bm = lo >> sh;
@@ -773,6 +782,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
         if ((bm >> t) & 1ull) {
           const int slot = __popcll(bm & ((1ull << t) - 1ull));
           const uint32_t id = ids[range.x + start + t];
+          RD_CHECK(slot < BATCH && (int64_t)id < bd.n);
           const Record* r = rec + id;
           sid[slot] = id;
           spos[slot] = start + t;
@@ -783,6 +793,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
         }
       } else if (t < cnt) {
         const uint32_t id = ids[range.x + start + t];
+        RD_CHECK((int64_t)id < bd.n);
         const Record* r = rec + id;
         sid[t] = id;
         sbuf[0][t] = r->r0;
@@ -913,12 +924,12 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
 void launch_render_fwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int tiles_y, const uint2* ranges,
                        const uint32_t* ids, const Record* rec, float* color, float* depth, float* normal, float* alpha,
                        float* T_final, int32_t* n_contrib, int32_t* median_pos, const DistIO& dio,
-                       uint32_t* bmask, uint32_t* order, Counter* counters, cudaStream_t s) {
+                       uint32_t* bmask, uint32_t* order, Counter* counters, const DevBounds& bd, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
   k_tile_order<<<1, 1024, 0, s>>>(ranges, (int)grid, order);
 #define RD_K3(T, P, D)                                                                                            \
   k_render_fwd<T, P, D><<<grid, T * T / 2, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, color, depth, normal,   \
-                                                   alpha, T_final, n_contrib, median_pos, dio, bmask, order, counters)
+                                                   alpha, T_final, n_contrib, median_pos, dio, bmask, order, counters, bd)
 #define RD_K3T(T)                                     \
   if (dio.d0) {                                       \
     if (counters) RD_K3(T, true, true); else RD_K3(T, false, true);   \
@@ -941,12 +952,12 @@ void launch_render_bwd(const DevCam& cam, const DevOpt& opt, int tiles_x, int ti
                        const int32_t* median_pos, const float* dL_dcolor, const float* dL_ddepth,
                        const float* dL_dnormal, const float* dL_dalpha, const DistIO& dio,
                        const uint32_t* bmask, const uint32_t* order, G2D* g2d, Counter* counters,
-                       cudaStream_t s) {
+                       const DevBounds& bd, cudaStream_t s) {
   const unsigned grid = (unsigned)(tiles_x * tiles_y);
 #define RD_K4(T, PPT, D)                                                                                       \
   k_render_bwd<T, PPT, D><<<grid, T * T / PPT, 0, s>>>(cam, opt, tiles_x, ranges, ids, rec, T_final, n_contrib, \
                                                        median_pos, dL_dcolor, dL_ddepth, dL_dnormal, dL_dalpha,  \
-                                                       dio, bmask, order, g2d, counters)
+                                                       dio, bmask, order, g2d, counters, bd)
   if (opt.tile == 32) {  // 4 pixels per thread: 8 warps of 8×16 pixels (the reduction rows fit)
     if (dio.dL_ddist) RD_K4(32, 4, true); else RD_K4(32, 4, false);
   } else if (opt.tile == 16) {
