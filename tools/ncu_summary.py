@@ -68,19 +68,26 @@ if os.path.exists(rp):
             issue[name].append(val("smsp__issue_active.avg.pct_of_peak_sustained_active"))
 
     def bench_name(name):
-        """ncu kernel name -> the bench's kernel name (ms_per_view_by_kernel keys); K5 = 3 kernels"""
-        n = name.split("::")[-1]
-        for pre, b in (("k_render_bwd", "render_bwd"), ("k_render_fwd", "render_fwd"),
-                       ("k_preprocess_fwd", "preprocess_fwd"), ("k_preprocess_bwd", "preprocess_bwd"),
-                       ("k_duplicate", "duplicate"), ("k_ranges", "ranges")):
+        """ncu kernel name -> (the bench's kernel name, launches per bench launch): K2's depth sort is
+        K2h + 4 onesweep passes (pass 0 and 3 x pass 1-3), K5 = its kernels summed"""
+        n = name.split("::")[-1].replace("(int)", "")
+        for pre, b, k in (("k_render_bwd", "render_bwd", 1), ("k_render_fwd", "render_fwd", 1),
+                          ("k_preprocess_fwd", "preprocess_fwd", 1),
+                          # bench's K5 launch = one rd_preprocess_bwd_views per round of 4 views:
+                          # the batched SH kernel once, K5b64 + K5b per view
+                          ("k_preprocess_bwd_sh", "preprocess_bwd", 1), ("k_preprocess_bwd", "preprocess_bwd", 4),
+                          ("k_bin_hist", "depth_sort", 1), ("k_onesweep<0>", "depth_sort", 1),
+                          ("k_onesweep<1>", "depth_sort", 3), ("k_scan", "scan", 1),
+                          ("k_onesweep<2>", "duplicate", 1), ("k_onesweep<3>", "tile_sort", 1),
+                          ("k_ranges", "ranges", 1)):
             if n.startswith(pre):
-                return b
-        return None
+                return b, k
+        return None, 0
     agg_t, agg_i = defaultdict(float), defaultdict(list)
     for name, v in per.items():
-        b = bench_name(name)
-        if b:  # K5's three kernels add up to one rd_preprocess_bwd call
-            agg_t[b] += sum(v) / len(v)
+        b, k = bench_name(name)
+        if b:  # a bench launch = its kernels summed
+            agg_t[b] += k * sum(v) / len(v)
             agg_i[b] += issue.get(name, [])
     traffic = dict(agg_t)
     issue_pct = {b: sum(v) / len(v) for b, v in agg_i.items() if v}
