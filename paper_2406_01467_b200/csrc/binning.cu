@@ -314,8 +314,7 @@ struct GenSmem {  // kTileGen: the block's Gaussians (≤ 2049: every visible on
   uint2 rect[kSTile + 1];
 };
 struct PassSmem {
-  uint32_t key[kSTile];
-  uint32_t val[kSTile];
+  uint2 kv[kSTile];  // (key, value) pairs: one 8-B access per item
   uint32_t cnt[kST / 32][kRadix];  // per-warp digit counts → warp offsets within the block's digit run
 };
 union SortSmem {
@@ -396,7 +395,6 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
   extern __shared__ __align__(16) unsigned char dsmem[];  // SortSmem (> 48 KB at 512 threads)
   SortSmem& sm = *reinterpret_cast<SortSmem*>(dsmem);
   __shared__ uint32_t s_gbase[kRadix + 1];  // the pass's digit bases (K2h) + total
-  __shared__ uint32_t s_lstart[kRadix];     // start of digit d in the block's sorted layout
   __shared__ uint32_t s_dst[kRadix];        // global position of the block's first item of digit d − lstart
   __shared__ uint32_t s_warp[kST / 32];
   __shared__ uint32_t s_cnt;
@@ -430,19 +428,19 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
     uint32_t gk[kSI], gv[kSI];
     generate_dups(a, sm.gen, b, o0, o1, gk, gv);
     __syncthreads();  // the staged Gaussians are dead: the same shared memory takes the transpose
-    uint4* kk = reinterpret_cast<uint4*>(sm.pass.key + tid * kSI);
-    uint4* vv = reinterpret_cast<uint4*>(sm.pass.val + tid * kSI);
-    kk[0] = make_uint4(gk[0], gk[1], gk[2], gk[3]);
-    kk[1] = make_uint4(gk[4], gk[5], gk[6], gk[7]);
-    vv[0] = make_uint4(gv[0], gv[1], gv[2], gv[3]);
-    vv[1] = make_uint4(gv[4], gv[5], gv[6], gv[7]);
+    uint4* kk = reinterpret_cast<uint4*>(sm.pass.kv + tid * kSI);
+    kk[0] = make_uint4(gk[0], gv[0], gk[1], gv[1]);
+    kk[1] = make_uint4(gk[2], gv[2], gk[3], gv[3]);
+    kk[2] = make_uint4(gk[4], gv[4], gk[5], gv[5]);
+    kk[3] = make_uint4(gk[6], gv[6], gk[7], gv[7]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kSI; ++j) {
       const int p = warp * 256 + j * 32 + lane;
       ok[j] = (uint32_t)base + (uint32_t)p < (uint32_t)n;
-      key[j] = sm.pass.key[p];
-      val[j] = sm.pass.val[p];
+      const uint2 q = sm.pass.kv[p];
+      key[j] = q.x;
+      val[j] = q.y;
     }
     __syncthreads();  // every lane has read its transposed items
   }
@@ -500,7 +498,8 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
     const uint32_t ls = block_excl_scan(run, s_warp, &btot);
     if (d == 0) s_cnt = btot;
     if (d < kRadix) {
-      s_lstart[d] = ls;
+#pragma unroll
+      for (int w = 0; w < kST / 32; ++w) sm.pass.cnt[w][d] += ls;  // warp offsets → block positions
       uint32_t excl = 0u;
       if (s_gbase[d + 1] != s_gbase[d])  // digits no item of the pass has are never looked up
         excl = lookback(a.status + d, kRadix, b, a.epoch, run);
@@ -514,23 +513,23 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
   for (int j = 0; j < kSI; ++j) {
     if (ok[j]) {
       const uint32_t d = (key[j] >> a.shift) & 255u;
-      const uint32_t p = s_lstart[d] + sm.pass.cnt[warp][d] + rank[j];
+      const uint32_t p = sm.pass.cnt[warp][d] + rank[j];  // (the digit's block start included)
       RD_CHECK(p < (uint32_t)kSTile);
-      sm.pass.key[p] = key[j];
-      sm.pass.val[p] = val[j];
+      sm.pass.kv[p] = make_uint2(key[j], val[j]);
     }
   }
   __syncthreads();
   const int cnt = (int)s_cnt;
   for (int i = tid; i < cnt; i += kST) {
-    const uint32_t k = sm.pass.key[i];
+    const uint2 q = sm.pass.kv[i];
+    const uint32_t k = q.x;
     const uint32_t dst = s_dst[(k >> a.shift) & 255u] + (uint32_t)i;
     RD_CHECK(dst < s_gbase[kRadix]);
     uint32_t out = k;
     if constexpr (MODE == kTile || MODE == kTileGen)
       if (a.last) out = (k >> 16) * (uint32_t)a.tiles_x + (k & 0xffffu);
     a.keys_out[dst] = out;
-    a.vals_out[dst] = sm.pass.val[i];
+    a.vals_out[dst] = q.y;
   }
   RD_TRACE(4)
 }
