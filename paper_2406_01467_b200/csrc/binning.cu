@@ -593,6 +593,47 @@ __global__ void __launch_bounds__(kST) k_scan(const uint32_t* __restrict__ n_dev
   }
 }
 
+// Plain exclusive scan of a u32 array (marching cubes' per-cell triangle counts, NEXT-4):
+// thread t scans items 8t..8t+7 of its block, block scan, one look-back word per block.
+__global__ void __launch_bounds__(kST) k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                   int64_t n, unsigned long long* status, uint32_t epoch) {
+  __shared__ uint32_t s_warp[kST / 32];
+  __shared__ uint32_t s_excl;
+  const int b = (int)blockIdx.x;
+  const int64_t p0 = (int64_t)b * kSTile + (int64_t)threadIdx.x * kSI;
+  uint32_t v[kSI];
+  if (p0 + kSI <= n) {
+    const uint4 q0 = *reinterpret_cast<const uint4*>(in + p0);
+    const uint4 q1 = *reinterpret_cast<const uint4*>(in + p0 + 4);
+    v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
+    v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSI; ++j) v[j] = p0 + j < n ? in[p0 + j] : 0u;
+  }
+  uint32_t s = 0u;
+#pragma unroll
+  for (int j = 0; j < kSI; ++j) {
+    const uint32_t x = v[j];
+    v[j] = s;  // exclusive
+    s += x;
+  }
+  uint32_t btot;
+  const uint32_t te = block_excl_scan(s, s_warp, &btot);
+  if (threadIdx.x == 0) s_excl = lookback(status, 1, b, epoch, btot);
+  __syncthreads();
+  const uint32_t e = s_excl + te;
+  if (p0 + kSI <= n) {
+    uint4* o = reinterpret_cast<uint4*>(out + p0);
+    o[0] = make_uint4(e + v[0], e + v[1], e + v[2], e + v[3]);
+    o[1] = make_uint4(e + v[4], e + v[5], e + v[6], e + v[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSI; ++j)
+      if (p0 + j < n) out[p0 + j] = e + v[j];
+  }
+}
+
 // ------------------------------------------------------------------------------- K2e
 // 8 consecutive sorted keys per thread (two 16-B loads) + the next one; a boundary between
 // positions k and k+1 closes tile keys[k] and opens tile keys[k+1].
@@ -635,6 +676,7 @@ unsigned blocks_of(int64_t n) { return (unsigned)((n + kSTile - 1) / kSTile); }
 }  // namespace
 
 size_t bin_status_words(int64_t n_items) { return (size_t)(blocks_of(n_items) + 1) * kRadix; }
+size_t scan_status_words(int64_t n) { return (size_t)blocks_of(n) + 1; }
 size_t bin_bstart_words(int64_t m) { return (size_t)blocks_of(m) + 2; }
 int bin_max_tiles_per_axis() { return kMaxTileAxis - 1; }
 int bin_bases_words() { return 8 * kBaseStride; }
@@ -744,6 +786,11 @@ void launch_tile_pass(int p, int64_t m, int64_t n_gauss, const uint32_t* offsets
     k_onesweep<kTileGen><<<blocks_of(m), kST, kSortSmem, s>>>(a);
   else
     k_onesweep<kTile><<<blocks_of(m), kST, kSortSmem, s>>>(a);
+}
+
+void launch_scan_excl_u32(const uint32_t* in, uint32_t* out, int64_t n, BinSort& bs, cudaStream_t s) {
+  if (n == 0) return;
+  k_scan_excl<<<blocks_of(n), kST, 0, s>>>(in, out, n, bs.status, ++bs.epoch);
 }
 
 void launch_ranges(const uint32_t* keys, int64_t m, int n_tiles, uint2* ranges, cudaStream_t s) {

@@ -11,15 +11,14 @@
 // from the inside corners to the outside ones.
 //
 // Extraction is three passes over the (X−1)(Y−1)(Z−1) cells: count triangles per cell (0 if
-// a corner has weight 0), exclusive scan (CUB), emit each cell's triangles at its offset —
+// a corner has weight 0), exclusive scan (binning.cu's single-pass look-back scan), emit each
+// cell's triangles at its offset —
 // a deterministic triangle soup in cell order (x fastest), triangles in table order.
 // Degenerate triangles are dropped (reading S25): a vertex lands exactly on a cube corner only
 // when that corner's value equals iso (then s = (iso − v_a)/(v_b − v_a) is exactly 0 or 1),
 // and a triangle is degenerate exactly when two of its vertices land on the same corner
 // (three distinct corner / edge-interior points of a cube cannot be collinear here).
 #include "rade_internal.cuh"
-
-#include <cub/device/device_scan.cuh>
 
 #include <cmath>
 #include <vector>
@@ -198,8 +197,9 @@ namespace {
 // another stream — waits for it before rewriting count / offset, and before freeing them.
 struct McScratch {
   uint32_t *count = nullptr, *offset = nullptr, *host = nullptr;
-  void* temp = nullptr;
-  size_t cells = 0, temp_bytes = 0;
+  unsigned long long* status = nullptr;  // the scan's look-back words (zeroed when allocated)
+  size_t cells = 0, status_words = 0;
+  uint32_t epoch = 0;
   cudaEvent_t done = nullptr;
 };
 thread_local McScratch t_mc;
@@ -227,8 +227,6 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
   const Vol v{origin[0], origin[1], origin[2], voxel, dims[0], dims[1], dims[2], tsdf, weight};
   const int64_t ncell = (int64_t)(dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1);
   if (ncell > 0x7fffffffLL) return cudaErrorInvalidValue;
-  size_t scan_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)ncell);
   McScratch& m = t_mc;
   if (!m.host) {
     e = cudaMallocHost(&m.host, 8);
@@ -250,19 +248,23 @@ cudaError_t launch_marching_cubes(const float origin[3], float voxel, const int 
     if (e != cudaSuccess) return e;
     m.cells = (size_t)ncell;
   }
-  if (m.temp_bytes < scan_bytes) {
+  const size_t words = scan_status_words(ncell);
+  if (m.status_words < words) {
     e = cudaEventSynchronize(m.done);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (m.temp) cudaFree(m.temp);
-    m.temp = nullptr;
-    m.temp_bytes = 0;
-    if (e == cudaSuccess) e = cudaMalloc(&m.temp, scan_bytes);
+    if (m.status) cudaFree(m.status);
+    m.status = nullptr;
+    m.status_words = 0;
+    if (e == cudaSuccess) e = cudaMalloc(&m.status, words * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(m.status, 0, words * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
-    m.temp_bytes = scan_bytes;
+    m.status_words = words;
   }
   const unsigned grid = (unsigned)((ncell + 255) / 256);
   k_mc_count<<<grid, 256, 0, s>>>(v, iso, m.count);
-  cub::DeviceScan::ExclusiveSum(m.temp, scan_bytes, m.count, m.offset, (int)ncell, s);
+  BinSort bs{m.status, m.epoch};
+  launch_scan_excl_u32(m.count, m.offset, ncell, bs, s);
+  m.epoch = bs.epoch;
   cudaMemcpyAsync(m.host, m.offset + (ncell - 1), 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(m.host + 1, m.count + (ncell - 1), 4, cudaMemcpyDeviceToHost, s);
   e = cudaStreamSynchronize(s);

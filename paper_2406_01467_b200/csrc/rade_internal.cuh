@@ -273,6 +273,9 @@ void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const ui
 void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n_max,
                  const uint32_t* n_dev, uint32_t* bstart, int64_t m, BinSort& bs, cudaStream_t s);
 int tile_sort_passes(int tiles_x, int tiles_y);
+// exclusive scan of n u32 (look-back state bs: scan_status_words(n) words, zeroed when allocated)
+size_t scan_status_words(int64_t n);
+void launch_scan_excl_u32(const uint32_t* in, uint32_t* out, int64_t n, BinSort& bs, cudaStream_t s);
 void launch_tile_pass(int p, int64_t m, int64_t n_gauss, const uint32_t* offsets, const uint32_t* sorted_ids,
                       const uint2* rect, const uint32_t* bstart, int tiles_x, int tiles_y, const uint32_t* bases,
                       uint32_t* const kb[2], uint32_t* const vb[2], BinSort& bs, cudaStream_t s);
