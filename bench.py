@@ -415,7 +415,9 @@ def run_gpu(args, cfg_name, config):
                     "outbuf": torch.empty((10, H, W), device=device),
 
                     "cot": torch.empty((10, H, W), device=device),
-                    "done": torch.cuda.Event()}
+                    "done": torch.cuda.Event(),
+                    # --stagger: recorded after the view's rd_bin; set on the host once recorded
+                    "binned": torch.cuda.Event(), "binned_host": threading.Event()}
             ob = slot["outbuf"]
             slot["outs"] = {"color": ob[0:3], "depth": ob[3], "normal": ob[4:7], "alpha": ob[7],
                             "distortion": ob[8], "consistency": ob[9]}
@@ -443,9 +445,16 @@ def run_gpu(args, cfg_name, config):
                 e.record(st)
                 ph.append(e)
         with torch.cuda.stream(st):
+            prev = slot.get("stagger_after")
+            if prev is not None:  # --stagger S: start once the view S slots earlier is binned
+                prev["binned_host"].wait()
+                st.wait_event(prev["binned"])
             mark()
             P.rd_preprocess(vw, g, cam, opts, stream=st)
             P.rd_bin(vw, stream=st)
+            if args.stagger:
+                slot["binned"].record(st)
+                slot["binned_host"].set()
             mark()
             if io:
                 st.wait_event(io["outs_free"])
@@ -508,6 +517,9 @@ def run_gpu(args, cfg_name, config):
         for r0 in range(0, len(ks), P_):
             rnd = ks[r0:r0 + P_]
             used = [slots[i] for i in range(len(rnd))]
+            for i, sl in enumerate(used):
+                sl["binned_host"].clear()
+                sl["stagger_after"] = used[i - args.stagger] if args.stagger and i >= args.stagger else None
             if pool is None:
                 for sl, k in zip(used, rnd):
                     per_view(sl, k)
@@ -907,6 +919,8 @@ def main():
     ap.add_argument("--single-host-thread", dest="host_threads", action="store_false",
                     help="issue every view from the main thread (default: one host thread per stream)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stagger", type=int, default=0,
+                    help="view k of a round starts once view k - S is binned (0: all views at once)")
     ap.add_argument("--e2e-mode", default="loss", choices=["loss", "maps"],
                     help="e2e inputs/outputs: GT images in + loss out (default), or cotangent images in + maps out")
     ap.add_argument("--no-cpu-baseline", action="store_true")
