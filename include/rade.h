@@ -13,8 +13,8 @@
  * Calls, in order, per view:
  *   rd_preprocess  stage 1 (K1): per-Gaussian EWA projection, conic, α-bounded tile rect,
  *                  SH colour, depth-plane coefficients p and normal n
- *   rd_bin         stage 2 (K2): tile-count scan, duplicate (tile | depth) keys, device
- *                  radix sort, per-tile ranges
+ *   rd_bin         stage 2 (K2): depth radix sort, tile-count scan, duplicate (tile | depth)
+ *                  keys, tile radix sort (hand-written onesweep passes), per-tile ranges
  *   rd_render_fwd  stage 3 (K3): per-tile front-to-back blend of C, A, N, median D
  *   rd_render_bwd  stage 4 (K4, K5): reverse replay per pixel, per-Gaussian chain rule
  *                  (also as its two halves rd_blend_bwd (K4) and rd_preprocess_bwd (K5))
@@ -51,7 +51,9 @@
  * contributes nothing and receives zero gradient.
  *
  * Synchronisation: every call is asynchronous on the given stream except rd_bin, which
- * reads the duplicate count M back to the host once (one D2H copy + stream sync).
+ * reads the duplicate count M back to the host once: its histogram kernel writes the counts
+ * to mapped pinned memory and rd_bin waits for that kernel's completion event (not for the
+ * stream), with the depth sort already queued behind it.
  *
  * Threads: the library keeps no shared mutable state (the error message is thread-local);
  * calls on DISTINCT rd_view handles may run concurrently from different host threads, which
@@ -138,15 +140,16 @@ typedef struct rd_stats {
   int32_t tiles_x, tiles_y;
   int32_t width, height;
   int32_t stage;        /* 0 created, 1 preprocessed, 2 binned, 3 rendered, 4 blend-backward done */
-  int32_t key_bits;     /* radix-sort bits: 32 + ceil(log2(tiles)) */
+  int32_t key_bits;     /* width of the equivalent one-pass sort key: 32 + ceil(log2(tiles)) */
   int64_t n_visible;    /* Gaussians that touch ≥ 1 tile (after rd_bin) */
   int64_t n_big;        /* of those, the ones whose backward chain rule runs in fp64 (K5b64:
                            tile rect > 16384 px), after rd_bin */
 } rd_stats;
 
 /* Per-kernel device timings and work counters (host struct filled by rd_get_timings).
- * Kernel index: 0 K1 preprocess_fwd, 1 K2a depth_sort, 2 K2b scan, 3 K2c duplicate,
- * 4 K2d tile_sort, 5 K2e ranges, 6 K3 render_fwd, 7 K4 render_bwd (including the zeroing of
+ * Kernel index: 0 K1 preprocess_fwd, 1 K2a depth_sort (incl. the K2h histogram kernel), 2 K2b
+ * scan, 3 K2c duplicate (fused with the first tile pass), 4 K2d tile_sort (remaining tile
+ * passes), 5 K2e ranges, 6 K3 render_fwd, 7 K4 render_bwd (including the zeroing of
  * the 2-D gradient scratch), 8 K5 preprocess_bwd. */
 #define RD_NUM_KERNELS 9
 typedef struct rd_timings {
@@ -190,10 +193,15 @@ rd_status rd_view_destroy(rd_view* view);
 rd_status rd_preprocess(rd_view* view, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
                         rd_stream stream);
 
-/* Stage 2 (K2). Exclusive scan of tiles touched; reads M to the host (writes it to
- * *n_duplicates_out if non-NULL); emits M keys (tile << 32 | float_bits(z_c)) with the
- * Gaussian id as value in id order; stable LSD radix sort on bits [0, 32 + ceil(log2 T));
- * per-tile [first, last) ranges. Order = (tile, z_c, id): the depth sort of PAPER:422. */
+/* Stage 2 (K2). Result: the M (tile, Gaussian id) pairs in the order of ONE stable sort of
+ * the 64-bit keys (tile << 32 | float_bits(z_c)) emitted in id order — per tile the
+ * Gaussians front to back by z_c, ties by id (the depth sort of PAPER:422, reading S7) — and
+ * per-tile [first, last) ranges; M is read to the host (written to *n_duplicates_out if
+ * non-NULL). Computed as a stable depth sort of the visible Gaussians (4 radix passes), the
+ * scan of their tile counts, and a stable sort of the duplicates by tile (tx, then ty digits;
+ * the first pass fused with the duplicate generation), all single-pass radix passes with
+ * decoupled look-back (binning.cu). Images of more than 2047 tiles per axis are rejected by
+ * rd_preprocess (RD_ERR_INVALID_ARGUMENT). */
 rd_status rd_bin(rd_view* view, int64_t* n_duplicates_out, rd_stream stream);
 
 /* Stage 3 (K3). One CTA per tile. Any output pointer may be NULL to skip that map.

@@ -37,14 +37,25 @@ def main():
     out, view = P.render(g, cam, opts)
     torch.cuda.synchronize()
     gpu = {k: v.double().cpu().numpy() for k, v in out.items()}
+    # bench.py's cpu_baseline extrapolates the oracle's forward from a random-pixel sample
+    # (project+sort time + per-pixel time × W·H / n): the full frame below validates it
+    rng = np.random.default_rng(0)
+    n_s = 2048
+    ts = np.zeros(3)
+    oracle.render(scene, cam, opt, pixels=rng.choice(cam.width * cam.height, n_s, replace=False), timing=ts)
+    extrap = ts[0] + ts[1] * (cam.width * cam.height / n_s)
+    tf = np.zeros(3)
     t0 = time.time()
-    ref = oracle.render(scene, cam, opt)
+    ref = oracle.render(scene, cam, opt, timing=tf)
     t_or = time.time() - t0
     fl = ref["flags"]
     ok = (fl & (F1 | F3)) == 0
     okd = (fl & (F1 | F3 | F4 | F5)) == 0
     res = {"config": cfg, "view": vi, "width": cam.width, "height": cam.height, "gaussians": int(scene.n),
            "oracle_threads": oracle.num_threads(), "oracle_s": t_or,
+           "cpu_baseline_check": {"sample_pixels": n_s, "extrapolated_full_frame_s": extrap,
+                                  "full_frame_s": float(tf[0] + tf[1]),
+                                  "ratio_extrapolated_over_full": extrap / float(tf[0] + tf[1])},
            "flagged_share_F1_F3": float(1 - ok.mean()), "flagged_share_depth": float(1 - okd.mean()),
            "alpha_mean": float(ref["alpha"].mean()), "tolerance": TOL}
     worst = {}
