@@ -122,6 +122,13 @@ def test_argument_validation_without_gpu(native):
     assert lib.rd_preprocess(h, ctypes.byref(g4), ctypes.byref(cam), ctypes.byref(o2), None) == 1
     cam0 = native.RdCamera(fx=10, fy=10, cx=5, cy=5, width=0, height=10, znear=0.2)
     assert lib.rd_preprocess(h, ctypes.byref(g), ctypes.byref(cam0), ctypes.byref(opt), None) == 1
+    # the binning's per-axis tile histograms cap an image at 2047 tiles per axis (rade.h rd_bin)
+    o8 = native.RdOptions()
+    lib.rd_options_default(ctypes.byref(o8))
+    o8.tile = 8
+    big = native.RdCamera(fx=10, fy=10, cx=5, cy=5, width=8 * 2048, height=10, znear=0.2)
+    assert lib.rd_preprocess(h, ctypes.byref(g), ctypes.byref(big), ctypes.byref(o8), None) == 1
+    assert b"too large" in lib.rd_last_error()
     # out-of-order calls are state errors
     assert lib.rd_bin(h, None, None) == native.RD_ERR_STATE
     assert lib.rd_render_fwd(h, None, None, None, None, None) == native.RD_ERR_STATE
