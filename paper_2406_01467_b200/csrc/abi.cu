@@ -85,7 +85,7 @@ struct rd_view {
   uint32_t* host_M_dev = nullptr;  // its device alias
   cudaEvent_t m_ready = nullptr;  // recorded after K2h, waited on by rd_bin (the path's one sync)
   BinSort bs{nullptr, 0u};  // K2's look-back state (binning.cu)
-  Buf rec, rect, touched, offsets, dkey0, dkey1, didx0, didx1, vis, big, bincnt, status, bstart;
+  Buf rec, rect, rect_s, touched, offsets, dkey0, dkey1, didx0, didx1, vis, big, bincnt, status, bstart;
   Buf tkeys0, tkeys1, vals0, vals1;
   Buf ranges;
   Buf T_final, n_contrib, median_pos;
@@ -238,7 +238,7 @@ rd_status rd_view_destroy(rd_view* v) {
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   Buf* all[] = {&v->rec,    &v->rect,   &v->touched, &v->offsets, &v->dkey0,   &v->dkey1,     &v->didx0,
                 &v->didx1,  &v->status, &v->tkeys0,  &v->tkeys1,  &v->vals0,   &v->vals1,     &v->ranges,
-                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->bmask, &v->tile_order, &v->vis, &v->big, &v->bincnt, &v->bstart, &v->dist_d0, &v->dist_D1};
+                &v->T_final, &v->n_contrib, &v->median_pos, &v->g2d, &v->counters, &v->bmask, &v->tile_order, &v->vis, &v->big, &v->bincnt, &v->bstart, &v->rect_s, &v->dist_d0, &v->dist_D1};
   if (v->stage > 0 || v->prof) cudaStreamSynchronize(v->last_stream);
   v->resolve();
   for (cudaEvent_t e : v->pool) cudaEventDestroy(e);
@@ -323,6 +323,7 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   const size_t n = (size_t)g->n;
   RD_ENSURE(v->rec, n * sizeof(Record), s);
   RD_ENSURE(v->rect, n * sizeof(uint2), s);
+  RD_ENSURE(v->rect_s, n * sizeof(uint2), s);
   RD_ENSURE(v->touched, n * sizeof(uint32_t), s);
   RD_ENSURE(v->offsets, n * sizeof(uint32_t), s);
   RD_ENSURE(v->dkey0, n * sizeof(uint32_t), s);
@@ -392,7 +393,7 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
     if (M > 0x7fffffffLL) return fail(RD_ERR_INVALID_ARGUMENT, "M = %lld duplicates >= 2^31", (long long)M);
     RD_ENSURE(v->bstart, bin_bstart_words(M) * sizeof(uint32_t), s);
     v->begin(s);
-    launch_scan(sorted_ids, (const uint32_t*)v->touched.ptr, (uint32_t*)v->offsets.ptr, n, cnt,
+    launch_scan(sorted_ids, (const uint2*)v->rect.ptr, (uint2*)v->rect_s.ptr, (uint32_t*)v->offsets.ptr, n, cnt,
                 (uint32_t*)v->bstart.ptr, M, v->bs, s);
     RD_CHECK_LAUNCH("scan");
     v->end(K_SCAN, s);
@@ -410,7 +411,7 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
     const int np = tile_sort_passes(v->tiles_x, v->tiles_y);
     for (int p = 0; p < np; ++p) {
       v->begin(s);
-      launch_tile_pass(p, M, v->n_vis, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect.ptr,
+      launch_tile_pass(p, M, v->n_vis, (const uint32_t*)v->offsets.ptr, sorted_ids, (const uint2*)v->rect_s.ptr,
                        (const uint32_t*)v->bstart.ptr, v->tiles_x, v->tiles_y, bases, tk, tv, v->bs, s);
       RD_CHECK_LAUNCH(p == 0 ? "duplicate" : "tile_sort");
       if (p == 0) {

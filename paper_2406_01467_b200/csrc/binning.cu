@@ -301,7 +301,7 @@ struct PassArgs {
   // first Gaussian of each output block)
   const uint32_t* __restrict__ offsets;
   const uint32_t* __restrict__ sorted_ids;
-  const uint2* __restrict__ rect;
+  const uint2* __restrict__ rect;  // in depth order (K2b's rect_s)
   const uint32_t* __restrict__ bstart;
   int64_t n_gauss;  // entries of offsets / sorted_ids (RD_CHECKS)
   unsigned long long* status;
@@ -337,7 +337,7 @@ __device__ __forceinline__ void generate_dups(const PassArgs& a, GenSmem& g, int
     g.end[k + 1] = a.offsets[g0 + k];
     const uint32_t id = a.sorted_ids[g0 + k];
     g.id[k] = id;
-    g.rect[k] = a.rect[id];
+    g.rect[k] = a.rect[g0 + k];  // K2b's depth-ordered copy
   }
   __syncthreads();
   const uint32_t o = o0 + (uint32_t)threadIdx.x * kSI;
@@ -536,13 +536,16 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
 
 // ------------------------------------------------------------------------------- K2b
 // offsets[p] = Σ_{q ≤ p} tiles_touched[ids[q]]: thread t sums items 8t..8t+7 of its block,
-// block scan, one look-back word per block. Each Gaussian also records itself as the first
-// Gaussian of the K2c output blocks whose first output it owns: bstart[ob] = p for every
-// ob·2048 in [offset_before, offset), and bstart[out_blocks] = n − 1.
+// block scan, one look-back word per block. The count of a Gaussian is its rect's area, so the
+// scan gathers the rect (8 B) and also writes it in depth order (rect_s), which K2c then reads
+// coalesced alongside the offsets instead of gathering it by id behind them. Each Gaussian
+// also records itself as the first Gaussian of the K2c output blocks whose first output it
+// owns: bstart[ob] = p for every ob·4096 in [offset_before, offset), and bstart[out_blocks] =
+// n − 1.
 __global__ void __launch_bounds__(kST) k_scan(const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ ids,
-                                              const uint32_t* __restrict__ touched, uint32_t* __restrict__ offsets,
-                                              uint32_t* __restrict__ bstart, uint32_t out_blocks,
-                                              unsigned long long* status, uint32_t epoch) {
+                                              const uint2* __restrict__ rect, uint2* __restrict__ rect_s,
+                                              uint32_t* __restrict__ offsets, uint32_t* __restrict__ bstart,
+                                              uint32_t out_blocks, unsigned long long* status, uint32_t epoch) {
   __shared__ uint32_t s_warp[kST / 32];
   __shared__ uint32_t s_excl;
   const int b = (int)blockIdx.x;
@@ -550,15 +553,25 @@ __global__ void __launch_bounds__(kST) k_scan(const uint32_t* __restrict__ n_dev
   if ((int64_t)b * kSTile >= n) return;  // grid sized for N
   const int64_t p0 = (int64_t)b * kSTile + (int64_t)threadIdx.x * kSI;
   uint32_t v[kSI], t[kSI];
+  uint2 r[kSI];
   if (p0 + kSI <= n) {
     const uint4 q0 = *reinterpret_cast<const uint4*>(ids + p0);
     const uint4 q1 = *reinterpret_cast<const uint4*>(ids + p0 + 4);
-    v[0] = touched[q0.x]; v[1] = touched[q0.y]; v[2] = touched[q0.z]; v[3] = touched[q0.w];
-    v[4] = touched[q1.x]; v[5] = touched[q1.y]; v[6] = touched[q1.z]; v[7] = touched[q1.w];
+    r[0] = rect[q0.x]; r[1] = rect[q0.y]; r[2] = rect[q0.z]; r[3] = rect[q0.w];
+    r[4] = rect[q1.x]; r[5] = rect[q1.y]; r[6] = rect[q1.z]; r[7] = rect[q1.w];
+    uint4* o = reinterpret_cast<uint4*>(rect_s + p0);
+#pragma unroll
+    for (int j = 0; j < kSI; j += 2) o[j / 2] = make_uint4(r[j].x, r[j].y, r[j + 1].x, r[j + 1].y);
   } else {
 #pragma unroll
-    for (int j = 0; j < kSI; ++j) v[j] = p0 + j < n ? touched[ids[p0 + j]] : 0u;
+    for (int j = 0; j < kSI; ++j) {
+      r[j] = p0 + j < n ? rect[ids[p0 + j]] : make_uint2(0u, 0u);
+      if (p0 + j < n) rect_s[p0 + j] = r[j];
+    }
   }
+#pragma unroll
+  for (int j = 0; j < kSI; ++j)  // tiles touched = rect area (0 past the end)
+    v[j] = ((r[j].y & 0xffffu) - (r[j].x & 0xffffu)) * ((r[j].y >> 16) - (r[j].x >> 16));
   uint32_t s = 0u;
 #pragma unroll
   for (int j = 0; j < kSI; ++j) {
@@ -744,10 +757,10 @@ void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const ui
     k_onesweep<kDepth><<<blocks_of(n), kST, kSortSmem, s>>>(a);
 }
 
-void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n_max,
+void launch_scan(const uint32_t* sorted_ids, const uint2* rect, uint2* rect_s, uint32_t* offsets, int64_t n_max,
                  const uint32_t* n_dev, uint32_t* bstart, int64_t m, BinSort& bs, cudaStream_t s) {
   if (n_max == 0) return;
-  k_scan<<<blocks_of(n_max), kST, 0, s>>>(n_dev, sorted_ids, tiles_touched, offsets, bstart, blocks_of(m), bs.status,
+  k_scan<<<blocks_of(n_max), kST, 0, s>>>(n_dev, sorted_ids, rect, rect_s, offsets, bstart, blocks_of(m), bs.status,
                                           ++bs.epoch);
 }
 

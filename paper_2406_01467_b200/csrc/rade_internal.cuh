@@ -270,7 +270,7 @@ void launch_bin_hist(int64_t n, const uint32_t* dkey, const uint2* rect, int til
 void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const uint32_t* n_vis_dev,
                        const uint32_t* bases, uint32_t* const kb[2], uint32_t* const vb[2], BinSort& bs,
                        cudaStream_t s);
-void launch_scan(const uint32_t* sorted_ids, const uint32_t* tiles_touched, uint32_t* offsets, int64_t n_max,
+void launch_scan(const uint32_t* sorted_ids, const uint2* rect, uint2* rect_s, uint32_t* offsets, int64_t n_max,
                  const uint32_t* n_dev, uint32_t* bstart, int64_t m, BinSort& bs, cudaStream_t s);
 int tile_sort_passes(int tiles_x, int tiles_y);
 // exclusive scan of n u32 (look-back state bs: scan_status_words(n) words, zeroed when allocated)
