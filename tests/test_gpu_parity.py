@@ -194,6 +194,41 @@ def test_binning_order_matches_oracle(case):
         assert any(len(l) > 1 and len(set(zz[l])) < len(l) for l in per_tile)
 
 
+@pytest.mark.parametrize("W,H", [(2120, 40), (40, 2120), (2072, 2072)])
+def test_binning_more_than_256_tiles_per_axis(W, H):
+    """Beyond 256 tiles per axis at 8×8 tiles the tile sort takes a second digit per axis
+    (tx low / tx high / ty low / ty high passes, binning.cu): keys, ids and ranges still equal
+    the stable sort of the 64-bit keys, and the forward still matches the oracle (sampled)."""
+    n = 3000 if W * H < 10 ** 6 else 6000
+    scene = dense_scene(61, n, width=W, height=H, f=64.0, smin=0.01, smax=0.12)
+    cam, opt = sg.camera_identity(W, H, 64.0), sg.Options(tile=8)
+    res, view, _ = gpu_forward(scene, cam, opt)
+    st = P.rd_view_stats(view)
+    assert max(st["tiles_x"], st["tiles_y"]) > 256
+    rec, rect, touched = (t.cpu().numpy() for t in P.rd_debug_preprocess(view))
+    keys, ids, ranges = (t.cpu().numpy() for t in P.rd_debug_binning(view))
+    rk, ri = cpu_binning_reference(rect, touched, rec[:, 12], st["tiles_x"])
+    assert st["n_duplicates"] == len(rk) > 0
+    np.testing.assert_array_equal(keys.view(np.uint64), rk)
+    np.testing.assert_array_equal(ids.view(np.uint32), ri)
+    tiles = (rk >> np.uint64(32)).astype(np.int64)
+    T = st["tiles_x"] * st["tiles_y"]
+    first = np.full(T, -1, np.int64)
+    last = np.full(T, -1, np.int64)
+    pos = np.arange(len(tiles))
+    first[tiles[::-1]] = pos[::-1]
+    last[tiles] = pos
+    exp = np.where(first[:, None] >= 0, np.stack([first, last + 1], 1), 0)
+    np.testing.assert_array_equal(ranges.reshape(-1, 2).astype(np.int64), exp)
+    rng = np.random.default_rng(62)
+    pix = rng.choice(W * H, 256, replace=False)
+    ref = oracle.render(scene, cam, opt, pixels=pix)
+    ys, xs = pix // W, pix % W
+    ok = (ref["flags"] & 5) == 0
+    assert np.abs(res["color"][:, ys, xs] - ref["color"])[:, ok].max() <= 1e-4
+    assert np.abs(res["alpha"][ys, xs] - ref["alpha"])[ok].max() <= 1e-4
+
+
 def test_rect_is_conservative(case):
     """Every pixel where the oracle's α clears α_min (outside the F1 band) lies in a tile of
     the GPU's rect."""
