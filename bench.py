@@ -424,7 +424,9 @@ def run_gpu(args, cfg_name, config):
         slots.append(slot)
     view = slots[0]["view"]
     outs = slots[0]["outs"]
-    streams = {"k5": torch.cuda.Stream(device)}  # the batched K5 of each round of views
+    streams = {"k5": torch.cuda.Stream(device),  # the batched K5 of each round of views
+               "zero": torch.cuda.Stream(device)}  # the step's gradient zeroing
+    zeroed = {"ev": torch.cuda.Event()}
     k5_done = torch.cuda.Event()
     counter = {"v": 0}
     main_stream = torch.cuda.current_stream(device)
@@ -485,6 +487,8 @@ def run_gpu(args, cfg_name, config):
             if io:
                 io["k4_done"].record(st)
             mark()
+            if args.k5 in ("per-view", "split"):
+                st.wait_event(zeroed["ev"])  # the step's gradients are zeroed
             if args.k5 == "per-view":
                 P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
             elif args.k5 == "split":  # K5 geometry now, overlapping the other views' K3/K4
@@ -501,11 +505,17 @@ def run_gpu(args, cfg_name, config):
         With host threads (default) each slot's views are issued by their own host thread, so
         one view's rd_bin (which waits for its count of duplicates) does not hold
         back the issue of the other slots' views."""
-        fg.zero_()
         start = torch.cuda.Event()
-        start.record(main_stream)
+        start.record(main_stream)  # the previous step is complete (its K5 / all-reduce)
         for sl in slots:
             sl["stream"].wait_event(start)
+        # the gradients are written by K5 only, so their zeroing (a 354-MB memset at C3) runs on
+        # its own stream beside the views' K1..K4; every K5 waits for it
+        zs = streams["zero"]
+        zs.wait_event(start)
+        with torch.cuda.stream(zs):
+            fg.zero_()
+        zeroed["ev"].record(zs)
         ks = []
         for b in range(B):
             ks.append(counter["v"])
@@ -533,6 +543,7 @@ def run_gpu(args, cfg_name, config):
                     f.result()
             if args.k5 in ("batched", "split"):
                 k5s = streams["k5"]
+                k5s.wait_event(zeroed["ev"])
                 for sl in used:
                     k5s.wait_event(sl["done"])
                 if args.k5 == "split":  # the round's SH part (its geometry parts ran per view)
@@ -606,11 +617,11 @@ def run_gpu(args, cfg_name, config):
     # stream from one host thread, so the kernels are serialised and each one's CUDA-event time
     # is its own; timings are summed over the slots' views
     prof_stream = torch.cuda.Stream(device)
-    saved = [sl["stream"] for sl in slots], streams["k5"], pool
+    saved = [sl["stream"] for sl in slots], streams["k5"], pool, streams["zero"]
     for sl in slots:
         sl["stream"] = prof_stream
         P.rd_set_profiling(sl["view"], True)
-    streams["k5"], pool = prof_stream, None
+    streams["k5"], streams["zero"], pool = prof_stream, prof_stream, None
     torch.cuda.synchronize()
     for _ in range(args.steps):
         step()
@@ -632,7 +643,7 @@ def run_gpu(args, cfg_name, config):
             tim["n_culled"][kname] += val
     for sl, st_ in zip(slots, saved[0]):
         sl["stream"] = st_
-    streams["k5"], pool = saved[1], saved[2]
+    streams["k5"], pool, streams["zero"] = saved[1], saved[2], saved[3]
 
     # ---------------- end-to-end: per step, inputs from pinned host memory in, result out.
     # loss mode (default): a view's input is its ground-truth RGB image (uint8, the training
