@@ -472,6 +472,9 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
 #define RD_K4_DIRECT 5
 #endif
 constexpr int kDirectLanes = RD_K4_DIRECT;
+#ifndef RD_REDUCE_PACKED
+#define RD_REDUCE_PACKED 1
+#endif
 constexpr int kRedPitch = 36;  // floats per row: 16-B aligned rows, conflict-free column stores
 template <int NV>
 __device__ __forceinline__ float smem_reduce(const float (&v)[NV], unsigned red, int lane) {
@@ -484,8 +487,16 @@ __device__ __forceinline__ float smem_reduce(const float (&v)[NV], unsigned red,
   if (k < NV) {
     const unsigned a = red + 4u * (unsigned)(k * kRedPitch + 16 * q);
     const float4 x0 = lds128(a), x1 = lds128(a + 16u), x2 = lds128(a + 32u), x3 = lds128(a + 48u);
+#if RD_REDUCE_PACKED
+    // the 16 values as 8 register pairs summed with packed adds: 7 FADD2 + 1 FADD instead of 15
+    const f2 t0 = add2(pk(x0.x, x0.y), pk(x0.z, x0.w)), t1 = add2(pk(x1.x, x1.y), pk(x1.z, x1.w));
+    const f2 t2 = add2(pk(x2.x, x2.y), pk(x2.z, x2.w)), t3 = add2(pk(x3.x, x3.y), pk(x3.z, x3.w));
+    const f2 t = add2(add2(t0, t1), add2(t2, t3));
+    s = lo_of(t) + hi_of(t);
+#else
     s = ((x0.x + x0.y) + (x0.z + x0.w)) + ((x1.x + x1.y) + (x1.z + x1.w)) +
         (((x2.x + x2.y) + (x2.z + x2.w)) + ((x3.x + x3.y) + (x3.z + x3.w)));
+#endif
   }
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   __syncwarp();  // the rows are rewritten by the next splat
