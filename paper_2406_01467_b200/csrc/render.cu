@@ -76,6 +76,12 @@ __device__ __forceinline__ f2 add2(f2 a, f2 b) {
   return r;
 }
 
+__device__ __forceinline__ float2 lds64f(unsigned a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
 // A saturated (or outside) pixel is marked by py = +inf: pair_power then yields e = −inf or
 // NaN, whose α test fails, so the blend loop needs no separate "done" test per pair.
 __device__ __forceinline__ bool pix_done(const PixF& s) { return s.py == __int_as_float(0x7f800000); }
@@ -727,6 +733,12 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
   RD_CHECK(range.x <= range.y && (int64_t)range.y <= bd.m);
 
   __shared__ float4 sbuf[4][BATCH];  // record quarters r0..r3 of the batch
+#ifndef RD_K4_ULO
+#define RD_K4_ULO 1
+#endif
+  // the centre's fp16 remainder (r3.w) as floats, converted once per staged splat (K4 stages
+  // only the splats the blend mask selects, so the conversion is cheaper than per step)
+  __shared__ float2 sulo[RD_K4_ULO ? BATCH : 1];
   __shared__ uint32_t sid[BATCH];
   __shared__ uint16_t wlist[kFilter ? NW : 1][kFilter ? BATCH : 1];  // per warp: batch slots (kFilter)
   __shared__ int spos[kMask ? BATCH : 1];                            // list position per slot (kMask)
@@ -800,7 +812,9 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
           sbuf[0][slot] = r->r0;
           sbuf[1][slot] = r->r1;
           sbuf[2][slot] = r->r2;
-          sbuf[3][slot] = r->r3;
+          const float4 q3 = r->r3;
+          sbuf[3][slot] = q3;
+          if (RD_K4_ULO) sulo[slot] = uv_lo(q3.w);
         }
       } else if (t < cnt) {
         const uint32_t id = ids[range.x + start + t];
@@ -810,7 +824,9 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
         sbuf[0][t] = r->r0;
         sbuf[1][t] = r->r1;
         sbuf[2][t] = r->r2;
-        sbuf[3][t] = r->r3;
+        const float4 q3 = r->r3;
+        sbuf[3][t] = q3;
+        if (RD_K4_ULO) sulo[t] = uv_lo(q3.w);
       }
     }
     __syncthreads();
@@ -819,6 +835,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
       nsel = warp_filter(sbuf[0], sbuf[1], sbuf[3], cnt, lane, fx0, fx0 + 7.f, fy0, fy0 + (float)(SH - 1),
                          opt.log2_alpha_min, wlist[warp]);
     const unsigned a_s0 = smem_addr(sbuf[0]), a_id = smem_addr(sid), a_pos = smem_addr(spos);
+    const unsigned a_ulo = smem_addr(sulo);
     for (int i = nsel - 1; i >= 0; --i) {
       // slot j of the staged batch, at list position pos
       int j, pos;
@@ -837,7 +854,7 @@ __global__ void __launch_bounds__(TILE* TILE / PPT, (TILE == 8 ? RD_K4_MINB : 1)
       if (!kMask && !__any_sync(0xffffffffu, pos < mylast)) continue;
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
-      const float2 ulo = uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));  // r3.w
+      const float2 ulo = RD_K4_ULO ? lds64f(a_ulo + 8u * j) : uv_lo(__uint_as_float(lds32(a + 48u * BATCH + 12u)));
       const PairColumn col = pair_column(a0, ulo, s[0].px);  // the thread's pixels share the column
       if constexpr (kPk) {
         // pair_power for both rows at once (the same IEEE ops per half)
