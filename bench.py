@@ -372,11 +372,16 @@ def run_gpu(args, cfg_name, config):
     if ws != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} (launch with torchrun, or let "
                          f"bench.py re-launch itself by leaving WORLD_SIZE unset)")
-    dist_on = ws > 1
+    dist_on = ws > 1 or args.nccl_single
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if dist_on:
         import torch.distributed as dist
+        if ws == 1:  # --nccl-single: the N > 1 code path (NCCL group, side-stream bucketed
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")  # all-reduce, barriers, max over
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))  # ranks) as one rank
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=device)
 
     from paper_2406_01467_b200.parallel import FlatGrads, views_for_rank
@@ -930,6 +935,8 @@ def main():
     ap.add_argument("--single-host-thread", dest="host_threads", action="store_false",
                     help="issue every view from the main thread (default: one host thread per stream)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--nccl-single", action="store_true",
+                    help="at N = 1, run the multi-GPU code path anyway (an NCCL group of one rank)")
     ap.add_argument("--stagger", type=int, default=0,
                     help="view k of a round starts once view k - S is binned (0: all views at once)")
     ap.add_argument("--e2e-mode", default="loss", choices=["loss", "maps"],
