@@ -642,7 +642,7 @@ def run_gpu(args, cfg_name, config):
             for kname, val in t[key].items():
                 tim[key][kname] = tim[key].get(kname, 0) + val
         for key in ("n_duplicates", "views", "pairs_evaluated_fwd", "pairs_blended_fwd", "pairs_evaluated_bwd",
-                    "n_visible", "n_visible_union"):
+                    "n_visible", "n_visible_union", "pairs_issued_fwd"):
             tim[key] += t[key]
         for kname, val in t["n_culled"].items():
             tim["n_culled"][kname] += val
@@ -873,6 +873,9 @@ def run_gpu(args, cfg_name, config):
         "culled_per_view": {k: v / max(views_timed, 1) for k, v in tim["n_culled"].items()},
         "pairs_evaluated_per_px_fwd": tim["pairs_evaluated_fwd"] / max(views_timed, 1) / (H * W),
         "pairs_blended_per_px": tim["pairs_blended_fwd"] / max(views_timed, 1) / (H * W),
+        # E_issued = K3 warp steps × 64 pixels; E_px / E_issued = the SIMT efficiency
+        "pairs_issued_per_px_fwd": tim.get("pairs_issued_fwd", 0) / max(views_timed, 1) / (H * W),
+        "simt_efficiency_fwd": tim["pairs_evaluated_fwd"] / max(tim.get("pairs_issued_fwd", 0), 1),
         "ms_per_view_by_kernel": {k: tim["ms"][k] / max(views_timed, 1) for k in tim["ms"]},
         "step_ms": {"median": float(np.median(step_ms)), "mean": float(step_ms.mean()),
                     "p10": float(np.percentile(step_ms, 10)), "p90": float(np.percentile(step_ms, 90)),

@@ -169,6 +169,9 @@ typedef struct rd_timings {
                                       [1] centre depth ≤ znear, [2] outside the guard band (S6b),
                                       [3] opacity < alpha_min, [4] degenerate 2-D covariance or plane,
                                       [5] footprint entirely off screen */
+  int64_t pairs_issued_fwd;        /* (pixel, splat) slots K3's warps stepped through: steps × the 64
+                                      pixels of a warp (E_issued); pairs_evaluated_fwd /
+                                      this = the SIMT efficiency of the walk */
 } rd_timings;
 
 typedef void* (*rd_alloc_fn)(size_t bytes, void* ctx);

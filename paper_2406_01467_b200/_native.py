@@ -78,7 +78,7 @@ class RdTimings(ctypes.Structure):
                 ("pairs_evaluated_fwd", ctypes.c_int64), ("pairs_blended_fwd", ctypes.c_int64),
                 ("pairs_evaluated_bwd", ctypes.c_int64), ("n_visible", ctypes.c_int64),
                 ("n_duplicates", ctypes.c_int64), ("views", ctypes.c_int64), ("n_visible_union", ctypes.c_int64),
-                ("n_culled", ctypes.c_int64 * 6)]
+                ("n_culled", ctypes.c_int64 * 6), ("pairs_issued_fwd", ctypes.c_int64)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)

@@ -725,6 +725,7 @@ rd_status rd_get_timings(rd_view* v, rd_timings* out, int32_t reset) {
     out->pairs_evaluated_bwd = (int64_t)h[2];
     out->n_visible = (int64_t)h[3];
     out->n_visible_union = (int64_t)h[4];
+    out->pairs_issued_fwd = (int64_t)h[kIssuedCounter];
     for (int k = 0; k < 6; ++k)
       for (int b = 0; b < kCullSlots; ++b) out->n_culled[k] += (int64_t)h[kCullCounter0 + k * kCullSlots + b];
   }

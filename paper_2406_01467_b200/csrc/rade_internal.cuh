@@ -211,7 +211,8 @@ struct DistIO {
 // (invalid input, near plane, guard band, opacity < alpha_min, degenerate, off screen),
 // spread over 64 slots b so the atomics of 23 k warps do not all hit one address.
 typedef unsigned long long Counter;
-constexpr int kCullCounter0 = 5;
+constexpr int kIssuedCounter = 5;  // K3: warp steps × 64 pixels
+constexpr int kCullCounter0 = 6;
 constexpr int kCullSlots = 64;  // each reason's count spread over 64 addresses (block index mod 64)
 constexpr int kNumCounters = kCullCounter0 + 6 * kCullSlots;
 

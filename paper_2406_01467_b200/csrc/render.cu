@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   // DIST the distortion sums; the scalar PixF keeps px, D, last, med and the counters
   f2 NPY = pk(-A.py, -B.py), T2 = bc(1.f), C0 = bc(0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0;
   f2 DD0 = C0, DD1 = C0, DD2 = C0;
+  unsigned steps = 0;  // PROF: this warp's splat steps (E_issued)
   auto done_A = [&]() { return kPacked ? lo_of(NPY) == -kInf : pix_done(A); };
   auto done_B = [&]() { return kPacked ? hi_of(NPY) == -kInf : pix_done(B); };
   for (int base = 0; base < total; base += BATCH) {
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
     const float la_min = __shfl_sync(0xffffffffu, opt.log2_alpha_min, 0);  // a register, not a per-step LDC
     unsigned mine = 0u;  // kMask: bit 0 / 1 = this batch's step lane / lane + 32 was blended
     for (int i = 0; i < nsel; ++i) {  // the warp stays converged: uniform exits and skips only
+      if (PROF) ++steps;
       const int j = kFilter ? (int)wlist[warp][i] : i;
       const unsigned a = a_s0 + 16u * j;
       const float4 a0 = lds128(a), a1 = lds128(a + 16u * BATCH);
@@ -454,6 +456,7 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
   if (PROF) {
     warp_count(counters + 0, A.n_eval + B.n_eval);
     warp_count(counters + 1, A.n_blend + B.n_blend);
+    if (lane == 0 && steps) atomicAdd(counters + kIssuedCounter, (Counter)steps * 64u);  // 64 pixels per warp
   }
   if constexpr (kPacked) {  // back to the per-pixel records for the store
     A.T = lo_of(T2); B.T = hi_of(T2);
