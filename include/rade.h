@@ -204,7 +204,8 @@ rd_status rd_preprocess(rd_view* view, const rd_gaussians* g, const rd_camera* c
  * scan of their tile counts, and a stable sort of the duplicates by tile (tx, then ty digits;
  * the first pass fused with the duplicate generation), all single-pass radix passes with
  * decoupled look-back (binning.cu). Images of more than 2047 tiles per axis are rejected by
- * rd_preprocess (RD_ERR_INVALID_ARGUMENT). */
+ * rd_preprocess (RD_ERR_INVALID_ARGUMENT). A second rd_bin before the next rd_preprocess
+ * returns the same M and leaves the lists as they are. */
 rd_status rd_bin(rd_view* view, int64_t* n_duplicates_out, rd_stream stream);
 
 /* Stage 3 (K3). One CTA per tile. Any output pointer may be NULL to skip that map.

@@ -77,6 +77,7 @@ struct rd_view {
   int tile_bits = 0;
   int64_t M = 0;
   int tsel = 0;  // buffer (0/1) holding the sorted tile keys and ids
+  bool binned = false;  // rd_bin ran since the last rd_preprocess
   int64_t n_vis = 0, n_big = 0;
   bool g2d_dirty = false;  // the G2D rows hold a previous rd_blend_bwd's sums (K1 zeroes them)
   bool dist_fwd = false;   // the last forward produced the distortion map and its K4 state
@@ -350,6 +351,7 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   RD_CHECK_LAUNCH("preprocess_fwd");
   v->end(K_PRE, s);
   v->stage = 1;
+  v->binned = false;
   v->M = 0;
   v->n_vis = v->n_big = 0;
   v->g2d_dirty = false;
@@ -360,6 +362,10 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   g_err.clear();
   if (!v) return fail(RD_ERR_INVALID_ARGUMENT, "view is NULL");
   if (v->stage < 1) return fail(RD_ERR_STATE, "rd_bin before rd_preprocess");
+  if (v->binned) {  // already binned since the last rd_preprocess: the sorted lists stand (the depth
+    if (n_duplicates_out) *n_duplicates_out = v->M;  // passes consumed K1's id-order keys)
+    return RD_OK;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = v->n;
   const int n_tiles = v->tiles_x * v->tiles_y;
@@ -430,6 +436,7 @@ rd_status rd_bin(rd_view* v, int64_t* n_duplicates_out, rd_stream stream) {
   v->M = M;
   v->acc_M += M;
   v->stage = 2;
+  v->binned = true;
   if (n_duplicates_out) *n_duplicates_out = M;
   return RD_OK;
 }

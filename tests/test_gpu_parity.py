@@ -864,6 +864,29 @@ def test_batched_k5_argument_errors():
     assert e.value.status == 2
 
 
+def test_bin_twice_keeps_the_lists():
+    """A second rd_bin before the next rd_preprocess returns the same M and leaves keys, ids and
+    ranges bit-identical (the depth passes consume K1's id-order keys, so it must not re-sort);
+    the render after it equals a fresh view's."""
+    scene = dense_scene(71, 400)
+    cam, opt = sg.camera_identity(64, 64, 64.0), sg.Options(tile=8)
+    g = P.Gaussians.from_numpy(scene)
+    view = P.View()
+    P.rd_preprocess(view, g, cam, opts_dict(opt))
+    m1 = P.rd_bin(view)
+    k1, i1, r1 = (t.clone() for t in P.rd_debug_binning(view))
+    m2 = P.rd_bin(view)
+    k2, i2, r2 = P.rd_debug_binning(view)
+    torch.cuda.synchronize()
+    assert m1 == m2 > 0
+    assert torch.equal(k1, k2) and torch.equal(i1, i2) and torch.equal(r1, r2)
+    out = P.rd_render_fwd(view)
+    ref, _ = P.render(g, cam, opts_dict(opt))
+    torch.cuda.synchronize()
+    for k in ref:
+        assert torch.equal(out[k], ref[k]), k
+
+
 def test_view_reuse_depth_sort_capacity():
     """One rd_view reused across views whose visible counts differ (the visible-only depth sort
     sizes itself from the view's history): few → many visible (the capacity guess is too
