@@ -519,7 +519,10 @@ def run_gpu(args, cfg_name, config):
         zs = streams["zero"]
         zs.wait_event(start)
         with torch.cuda.stream(zs):
-            fg.zero_()
+            if args.k5 == "set":  # the first round's K5 sets the SH rows (RD_K5_SET_SH)
+                fg.zero_geometry_()
+            else:
+                fg.zero_()
         zeroed["ev"].record(zs)
         ks = []
         for b in range(B):
@@ -546,13 +549,16 @@ def run_gpu(args, cfg_name, config):
                 futs = [pool.submit(worker, sl, k) for sl, k in zip(used, rnd)]
                 for f in futs:
                     f.result()
-            if args.k5 in ("batched", "split"):
+            if args.k5 in ("batched", "split", "set"):
                 k5s = streams["k5"]
                 k5s.wait_event(zeroed["ev"])
                 for sl in used:
                     k5s.wait_event(sl["done"])
                 if args.k5 == "split":  # the round's SH part (its geometry parts ran per view)
                     P.rd_preprocess_bwd_views_sh([sl["view"] for sl in used], g, grads, stream=k5s)
+                elif args.k5 == "set":  # the step's first round SETS the SH gradient rows
+                    P.rd_preprocess_bwd_views_ex([sl["view"] for sl in used], g, grads,
+                                                 flags=P.rade.RD_K5_SET_SH if r0 == 0 else 0, stream=k5s)
                 else:
                     P.rd_preprocess_bwd_views([sl["view"] for sl in used], g, grads, stream=k5s)
                 k5_done.record(k5s)
@@ -862,7 +868,7 @@ def run_gpu(args, cfg_name, config):
     launches_per_view = 1 + 1 + 4 + 1 + tile_passes + 1 + 1 + 1 + 1 + 2
     views_per_rank = args.steps * B
     rounds = args.steps * math.ceil(B / P_)
-    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split") else views_per_rank)
+    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split", "set") else views_per_rank)
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)
     config.update({
@@ -918,8 +924,10 @@ def main():
     ap.add_argument("--views-per-step", default="4",
                     help="views per rank per step, or 'epoch' (ceil(views / ranks): one all-reduce per epoch)")
     ap.add_argument("--bucket-mb", type=int, default=64, help="all-reduce bucket size (N > 1)")
-    ap.add_argument("--k5", default="batched", choices=["batched", "split", "per-view"],
-                    help="K5 of a round of views in one rd_preprocess_bwd_views call, or per view")
+    ap.add_argument("--k5", default="set", choices=["set", "batched", "split", "per-view"],
+                    help="K5 of a round of views in one call: 'set' (default) sets the SH gradient rows in the "
+                         "step's first round (RD_K5_SET_SH; only the other gradients are zeroed), 'batched' "
+                         "accumulates all; 'split' runs the geometry parts per view; or 'per-view'")
     ap.add_argument("--guard-band", type=float, default=None,
                     help="reading S6b guard band (0 = off); default: the config's (C3/C4 0.15, others off)")
     ap.add_argument("--dry-run-gloo", action="store_true",

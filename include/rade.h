@@ -285,6 +285,19 @@ rd_status rd_preprocess_bwd_geometry(rd_view* view, const rd_gaussians* g, const
 rd_status rd_preprocess_bwd_views_sh(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
                                      const rd_grads* grads, rd_stream stream);
 
+/* rd_preprocess_bwd_views with flags: RD_K5_SH_ONLY (= rd_preprocess_bwd_views_sh),
+ * RD_K5_GEOMETRY_ONLY (the geometry parts of the views), RD_K5_SET_SH — the SH gradient rows
+ * are SET instead of accumulated: every Gaussian's row is written, with 0 where it is visible
+ * in none of the views, and the old values are never read (a caller whose step has one round
+ * of views and who zeroes only the non-SH gradients saves the SH rows' zeroing and the read of
+ * the reduction; needs sh_coeffs·3 a multiple of 4). Errors: unknown or contradictory flags →
+ * RD_ERR_INVALID_ARGUMENT; otherwise as rd_preprocess_bwd_views. */
+#define RD_K5_SH_ONLY 1u
+#define RD_K5_GEOMETRY_ONLY 2u
+#define RD_K5_SET_SH 4u
+rd_status rd_preprocess_bwd_views_ex(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
+                                     const rd_grads* grads, uint32_t flags, rd_stream stream);
+
 /* NEXT-2: normal consistency (reading S22) on rendered maps (device, fp32,
  * the layouts of rd_render_fwd): ñ = the finite-difference normal of the median depth map
  * (back-project the pixel and its right / lower neighbours with the camera intrinsics,

@@ -607,6 +607,22 @@ rd_status rd_preprocess_bwd_views_sh(rd_view* const* views, int32_t n_views, con
   return preprocess_bwd_views_parts(views, n_views, g, grads, stream, kK5Sh);
 }
 
+rd_status rd_preprocess_bwd_views_ex(rd_view* const* views, int32_t n_views, const rd_gaussians* g,
+                                     const rd_grads* grads, uint32_t flags, rd_stream stream) {
+  g_err.clear();
+  if (flags & ~(uint32_t)(RD_K5_SH_ONLY | RD_K5_GEOMETRY_ONLY | RD_K5_SET_SH))
+    return fail(RD_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if ((flags & RD_K5_SH_ONLY) && (flags & RD_K5_GEOMETRY_ONLY))
+    return fail(RD_ERR_INVALID_ARGUMENT, "RD_K5_SH_ONLY and RD_K5_GEOMETRY_ONLY exclude each other");
+  if ((flags & RD_K5_SET_SH) && (flags & RD_K5_GEOMETRY_ONLY))
+    return fail(RD_ERR_INVALID_ARGUMENT, "RD_K5_SET_SH needs the SH part");
+  if ((flags & RD_K5_SET_SH) && g && (g->sh_coeffs * 3) % 4 != 0)
+    return fail(RD_ERR_INVALID_ARGUMENT, "RD_K5_SET_SH needs SH rows of a multiple of 4 floats");
+  int parts = (flags & RD_K5_SH_ONLY) ? kK5Sh : (flags & RD_K5_GEOMETRY_ONLY) ? kK5Geometry : kK5All;
+  if (flags & RD_K5_SET_SH) parts |= kK5ShSet;
+  return preprocess_bwd_views_parts(views, n_views, g, grads, stream, parts);
+}
+
 rd_status rd_render_bwd(rd_view* v, const rd_gaussians* g, const float* dL_dcolor, const float* dL_ddepth,
                         const float* dL_dnormal, const float* dL_dalpha, const rd_grads* grads, rd_stream stream) {
   g_err.clear();

@@ -817,7 +817,7 @@ struct ViewsBwd {
 template <int DEG>
 __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(DevGauss g, DevOpt opt,
                                                                 const __grid_constant__ ViewsBwd vb, DevGrads gr,
-                                                                Counter* __restrict__ counters) {
+                                                                Counter* __restrict__ counters, bool set_sh) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int NV = 3 * K, NV4 = (NV + 3) / 4, P = NV4 + 1;
   __shared__ float4 s_coef[2][32 * P];
@@ -830,14 +830,20 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
     for (int v = 0; v < vb.nv; ++v) mask |= (vb.touched[v][id] > 0u ? 1u : 0u) << v;
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, mask != 0u);
-  if (vmask == 0u) return;  // warp-uniform
-  if (counters && lane == 0) atomicAdd(counters + 4, (Counter)__popc(vmask));
   const int64_t base = id - lane;
   const int64_t L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
+  float4* gsh4 = reinterpret_cast<float4*>(gr.sh);
+  if (vmask == 0u) {  // warp-uniform: none of the 32 Gaussians is visible in any view
+    if (set_sh) {  // set mode: their SH gradient rows are 0
+      for (int f = lane; f < 32 * (int)L4; f += 32)
+        if (base + f / L4 < g.n) gsh4[base * L4 + f] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
+  if (counters && lane == 0) atomicAdd(counters + 4, (Counter)__popc(vmask));
   float4* sc = s_coef[warp];
   float4* sg = s_grad[warp];
   const float4* sh4 = reinterpret_cast<const float4*>(g.sh);
-  float4* gsh4 = reinterpret_cast<float4*>(gr.sh);
 #pragma unroll
   for (int it = 0; it < NV4; ++it) {
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
@@ -903,6 +909,20 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
     for (int k = 0; k < 3; ++k) red_add(gr.means + 3 * id + k, dmu[k]);
   }
   __syncwarp();
+  if (set_sh) {  // set mode: every row of the warp is written (0 where visible in no view), the
+    // old values never read (the rows' 192-B read of the reduction disappears)
+#pragma unroll
+    for (int it = 0; it < NV4; ++it) {
+      const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
+      if (base + row < g.n) gsh4[(base + row) * L4 + c] = sg[row * P + c];
+    }
+    // coefficients above the active degree get no gradient: 0
+    for (int f = lane; f < 32 * (int)(L4 - NV4); f += 32) {
+      const int row = f / (int)(L4 - NV4), c = NV4 + f % (int)(L4 - NV4);
+      if (base + row < g.n) gsh4[(base + row) * L4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
 #pragma unroll
   for (int it = 0; it < NV4; ++it) {
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
@@ -1098,7 +1118,7 @@ void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, c
   if (!(parts & kK5Sh)) {
   } else if ((g.sh_coeffs * 3) % 4 == 0) {
     const unsigned cblocks = (unsigned)((g.n + 63) / 64);
-#define RD_K5AV(D) k_preprocess_bwd_sh_views<D><<<cblocks, 64, 0, s>>>(g, opt, vb, grads, counters)
+#define RD_K5AV(D) k_preprocess_bwd_sh_views<D><<<cblocks, 64, 0, s>>>(g, opt, vb, grads, counters, (parts & kK5ShSet) != 0)
     switch (opt.sh_degree) {
       case 0: RD_K5AV(0); break;
       case 1: RD_K5AV(1); break;

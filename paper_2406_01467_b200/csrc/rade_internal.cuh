@@ -234,6 +234,9 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
 // K5 parts: the SH colour (+ view-direction) part and the geometry part (K5b64 + K5b); both
 // add into the gradients with reductions, so they may run in any order
 constexpr int kK5Sh = 1, kK5Geometry = 2, kK5All = 3;
+// with kK5Sh: SET the SH gradient rows instead of adding (every row written, 0 for Gaussians
+// visible in none of the views; only by the batched views kernel, rows of 4k floats)
+constexpr int kK5ShSet = 4;
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,
                            const uint32_t* vis, int64_t n_vis, const uint32_t* big, int64_t n_big, const G2D* g2d,
                            DevGrads grads, cudaStream_t s, int parts = kK5All);

@@ -50,6 +50,12 @@ class FlatGrads:
         self.flat.zero_()
         return self
 
+    def zero_geometry_(self):
+        """Zeroes all but the SH gradients (the segments before them): the step's SH rows are then
+        SET by rd_preprocess_bwd_views_ex(..., RD_K5_SET_SH)."""
+        self.flat[: self.flat.numel() - self.sh.numel()].zero_()
+        return self
+
     def as_gaussians(self):
         from .rade import Gaussians
         return Gaussians(self.means, self.scales, self.rotations, self.opacities, self.sh)

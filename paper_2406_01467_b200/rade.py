@@ -402,6 +402,21 @@ def rd_preprocess_bwd_geometry(view: View, gaussians: Gaussians, grads: Gaussian
     return grads
 
 
+RD_K5_SH_ONLY, RD_K5_GEOMETRY_ONLY, RD_K5_SET_SH = 1, 2, 4
+
+
+def rd_preprocess_bwd_views_ex(views, gaussians: Gaussians, grads: Gaussians, flags: int = 0, stream=None):
+    """rd_preprocess_bwd_views with flags (RD_K5_SH_ONLY, RD_K5_GEOMETRY_ONLY, RD_K5_SET_SH: the SH
+    gradient rows are set, 0 where visible in none of the views, instead of accumulated)."""
+    views = list(views)
+    arr = (_VP_T * len(views))(*[v.handle for v in views])
+    g = gaussians.c_struct()
+    gr = _grads_struct(grads)
+    N.check(N.load().rd_preprocess_bwd_views_ex(arr, len(views), ctypes.byref(g), ctypes.byref(gr), int(flags),
+                                                _stream_ptr(stream)), "rd_preprocess_bwd_views_ex")
+    return grads
+
+
 def rd_preprocess_bwd_views_sh(views, gaussians: Gaussians, grads: Gaussians, stream=None):
     """K5 SH part of a round of views (rows read and reduced once), after their geometry parts
     may already have run."""

@@ -327,7 +327,11 @@ def test_c3_batched_k5_equals_per_view_sum(c3):
     for v in views:  # bench --k5 split: geometry per view, then the round's SH part
         P.rd_preprocess_bwd_geometry(v, g, gc)
     P.rd_preprocess_bwd_views_sh(views, g, gc)
+    gs = g.zeros_like()  # bench --k5 set: SH rows set (garbage before), the rest accumulated
+    gs.sh.fill_(-7.0)
+    P.rd_preprocess_bwd_views_ex(views, g, gs, flags=P.rade.RD_K5_SET_SH)
     torch.cuda.synchronize()
+    assert torch.equal(gs.sh, ga.sh)
     a, b, c = grads_to_rows(ga, g.n), grads_to_rows(gb, g.n), grads_to_rows(gc, g.n)
     for sl in (slice(0, 3), slice(3, 6), slice(6, 10), slice(10, 11), slice(11, 59)):
         nb = np.linalg.norm(b[:, sl])

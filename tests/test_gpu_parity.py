@@ -843,6 +843,44 @@ def test_batched_k5_matches_oracle_sum_over_views(which):
         assert np.linalg.norm(Sp[:, sl] - a) <= 1e-5 * np.linalg.norm(a), name
 
 
+@pytest.mark.parametrize("sh_degree", [3, 1])
+def test_batched_k5_set_sh_rows(sh_degree):
+    """rd_preprocess_bwd_views_ex(RD_K5_SET_SH) writes every SH gradient row — the batched
+    gradient where a Gaussian is visible in some view, 0 elsewhere and above the active degree —
+    without reading the old values: on a buffer whose SH part holds garbage it equals the
+    accumulating call on a zeroed buffer (same summation order, bit for bit), and the other
+    classes are accumulated as usual."""
+    behind = dense_scene(37, 40, zr=(3.0, 6.0))  # mirrored behind the cameras: culled in every view
+    behind.means[2] *= -1.0
+    scene, cams = concat(dense_scene(36, 300, zr=(3.0, 6.0)), behind), _orbit_cams(3)
+    scene.sh_degree = sh_degree
+    opt = sg.Options(tile=8, sh_degree=sh_degree)
+    cots = [sg.cotangents(50 + k, 64, 64) for k in range(3)]
+    g, views = _views_of(scene, cams, opt, cots)
+    ref = g.zeros_like()
+    P.rd_preprocess_bwd_views(views, g, ref)
+    got = g.zeros_like()
+    got.sh.fill_(123.0)  # garbage: every SH row must be overwritten
+    P.rd_preprocess_bwd_views_ex(views, g, got, flags=P.rade.RD_K5_SET_SH)
+    torch.cuda.synchronize()
+    assert torch.equal(got.sh, ref.sh)  # one store vs one reduction onto 0: the same values
+    for name in ("means", "scales", "rotations", "opacities"):  # float atomics: order-dependent rounding
+        a, b = getattr(got, name).cpu().numpy(), getattr(ref, name).cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-6 * max(np.abs(b).max(), 1e-30), name
+    vis = np.zeros(scene.n, bool)
+    for v in views:
+        vis |= P.rd_debug_preprocess(v)[2].cpu().numpy() > 0
+    assert (~vis).any() and vis.any()
+    sh = got.sh.cpu().numpy().reshape(scene.n, -1)
+    assert not sh[~vis].any()  # rows of Gaussians visible in no view: 0
+    K = (sh_degree + 1) ** 2
+    assert not sh[:, 3 * K:].any()  # coefficients above the active degree: 0
+    with pytest.raises(P.rade.N.RadeError):
+        P.rd_preprocess_bwd_views_ex(views, g, got, flags=8)
+    with pytest.raises(P.rade.N.RadeError):
+        P.rd_preprocess_bwd_views_ex(views, g, got, flags=P.rade.RD_K5_SET_SH | P.rade.RD_K5_GEOMETRY_ONLY)
+
+
 def test_batched_k5_argument_errors():
     scene, cams = dense_scene(34, 50), _orbit_cams(2)
     opt = sg.Options(tile=8)
