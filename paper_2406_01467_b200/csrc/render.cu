@@ -240,20 +240,30 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
                                                      uint32_t* __restrict__ order) {
   __shared__ uint32_t cnt[32], off[32];
   if (threadIdx.x < 32) cnt[threadIdx.x] = 0u;
-  __syncthreads();
   const unsigned lane = threadIdx.x & 31u, below = (1u << lane) - 1u;
-  auto bucket = [&](int t) {
-    const uint2 r = ranges[t];
-    return 31 - min(31, 32 - __clz((int)(r.y - r.x)));  // longer list → smaller bucket
-  };
-  // most tiles share a few buckets: one shared atomic per (warp, bucket) group (__match_any)
-  // instead of one per tile, which would serialise thousands of updates of one address
+  // thread t owns tiles t, t + 1024, ...: their buckets are computed once, up to kPer of them
+  // with all range loads in flight together (one block: the kernel is a chain of dependent
+  // rounds, so the loads must not be one round trip per round)
+  constexpr int kPer = 16;  // 16 × 1024 tiles (C3 at 8×8: 15 965; more: further chunks)
   const int rounds = (n_tiles + (int)blockDim.x - 1) / (int)blockDim.x;
-  for (int k = 0; k < rounds; ++k) {
-    const int t = k * (int)blockDim.x + (int)threadIdx.x;
-    const int b = t < n_tiles ? bucket(t) : 32;  // 32: no tile
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
-    if (b < 32 && (peers & below) == 0u) atomicAdd(&cnt[b], (unsigned)__popc(peers));
+  __syncthreads();
+  for (int r0 = 0; r0 < rounds; r0 += kPer) {
+    uint2 rg[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
+      rg[k] = (r0 + k < rounds && t < n_tiles) ? ranges[t] : make_uint2(0u, 0u);
+    }
+    // most tiles share a few buckets: one shared atomic per (warp, bucket) group (__match_any)
+    // instead of one per tile, which would serialise thousands of updates of one address
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
+      if (r0 + k >= rounds) break;  // block-uniform
+      const int b = t < n_tiles ? 31 - min(31, 32 - __clz((int)(rg[k].y - rg[k].x))) : 32;  // longer → smaller
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      if (b < 32 && (peers & below) == 0u) atomicAdd(&cnt[b], (unsigned)__popc(peers));
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -264,15 +274,25 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
     }
   }
   __syncthreads();
-  for (int k = 0; k < rounds; ++k) {
-    const int t = k * (int)blockDim.x + (int)threadIdx.x;
-    const int b = t < n_tiles ? bucket(t) : 32;
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0u;
-    if (b < 32 && (int)lane == leader) base = atomicAdd(&off[b], (unsigned)__popc(peers));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (b < 32) order[base + (uint32_t)__popc(peers & below)] = (uint32_t)t;
+  for (int r0 = 0; r0 < rounds; r0 += kPer) {
+    uint2 rg[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
+      rg[k] = (r0 + k < rounds && t < n_tiles) ? ranges[t] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
+      if (r0 + k >= rounds) break;
+      const int b = t < n_tiles ? 31 - min(31, 32 - __clz((int)(rg[k].y - rg[k].x))) : 32;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0u;
+      if (b < 32 && (int)lane == leader) base = atomicAdd(&off[b], (unsigned)__popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (b < 32) order[base + (uint32_t)__popc(peers & below)] = (uint32_t)t;
+    }
   }
 }
 
