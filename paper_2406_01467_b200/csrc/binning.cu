@@ -118,6 +118,39 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* status, int str
   return excl;
 }
 
+// The same for a single counter, walked by a whole warp (all 32 lanes call it): lane i reads
+// predecessor b − 1 − i, so one round trip covers 32 blocks (a single-word scan's blocks are
+// all resident at once and would otherwise walk ~b/2 predecessors 8 per round trip). Returns
+// the exclusive prefix on every lane.
+__device__ __forceinline__ uint32_t lookback_warp(unsigned long long* status, int b, uint32_t epoch,
+                                                  uint32_t mine) {
+  const int lane = (int)(threadIdx.x & 31);
+  if (b == 0) {
+    if (lane == 0) st_status(status, pack_status(epoch, 2u, mine));
+    return 0u;
+  }
+  if (lane == 0) st_status(status + b, pack_status(epoch, 1u, mine));
+  const uint32_t agg = 4u * epoch + 1u, inc = 4u * epoch + 2u;
+  uint32_t excl = 0u;
+  int p = b - 1;
+  for (;;) {
+    const int q = p - lane;
+    const unsigned long long st = q >= 0 ? ld_status(status + q) : 0ull;
+    const uint32_t tag = (uint32_t)(st >> 32);
+    const bool ready = q < 0 || tag >= agg, is_inc = q >= 0 && tag == inc;
+    const unsigned nr = __ballot_sync(0xffffffffu, !ready), ic = __ballot_sync(0xffffffffu, is_inc);
+    const int first_nr = nr ? __ffs(nr) - 1 : 32, first_inc = ic ? __ffs(ic) - 1 : 32;
+    if (first_inc < first_nr) {  // lanes 0..first_inc: aggregates then an inclusive prefix
+      excl += __reduce_add_sync(0xffffffffu, lane <= first_inc ? (uint32_t)st : 0u);
+      break;
+    }
+    excl += __reduce_add_sync(0xffffffffu, lane < first_nr ? (uint32_t)st : 0u);  // the ready aggregates
+    p -= first_nr;  // restart at the first one not yet published
+  }
+  if (lane == 0) st_status(status + b, pack_status(epoch, 2u, excl + mine));
+  return excl;
+}
+
 // Exclusive scan over the block's NT threads (one value each); *total = the sum.
 template <int NT = kST>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp, uint32_t* total) {
@@ -581,7 +614,10 @@ __global__ void __launch_bounds__(kST) k_scan(const uint32_t* __restrict__ n_dev
   }
   uint32_t btot;
   const uint32_t te = block_excl_scan(s, s_warp, &btot);
-  if (threadIdx.x == 0) s_excl = lookback(status, 1, b, epoch, btot);
+  if (threadIdx.x < 32) {
+    const uint32_t x = lookback_warp(status, b, epoch, btot);
+    if (threadIdx.x == 0) s_excl = x;
+  }
   __syncthreads();
   const uint32_t e = s_excl + te;
   if (p0 + kSI <= n) {
@@ -633,7 +669,10 @@ __global__ void __launch_bounds__(kST) k_scan_excl(const uint32_t* __restrict__ 
   }
   uint32_t btot;
   const uint32_t te = block_excl_scan(s, s_warp, &btot);
-  if (threadIdx.x == 0) s_excl = lookback(status, 1, b, epoch, btot);
+  if (threadIdx.x < 32) {
+    const uint32_t x = lookback_warp(status, b, epoch, btot);
+    if (threadIdx.x == 0) s_excl = x;
+  }
   __syncthreads();
   const uint32_t e = s_excl + te;
   if (p0 + kSI <= n) {
