@@ -56,7 +56,7 @@ if hasattr(lib, "rd_debug_bin_trace"):  # built with -DRD_BIN_TRACE: phases of t
     import ctypes
     import numpy as np
     M = P.rd_view_stats(view)["n_duplicates"]
-    nb = min(8192, (M + 2047) // 2048)
+    nb = min(8192, (M + 4095) // 4096)
     buf = np.zeros((nb, 6), np.uint64)
     lib.rd_debug_bin_trace(buf.ctypes.data_as(ctypes.c_void_p), nb)
     t = buf[:, :5].astype(np.float64)
