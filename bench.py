@@ -430,7 +430,9 @@ def run_gpu(args, cfg_name, config):
     view = slots[0]["view"]
     outs = slots[0]["outs"]
     streams = {"k5": torch.cuda.Stream(device),  # the batched K5 of each round of views
-               "zero": torch.cuda.Stream(device)}  # the step's gradient zeroing
+               "zero": torch.cuda.Stream(device),  # the step's gradient zeroing
+               "k1": torch.cuda.Stream(device)}  # --k1 batched: the round's K1
+    k1_ev = torch.cuda.Event()
     zeroed = {"ev": torch.cuda.Event()}
     k5_done = torch.cuda.Event()
     counter = {"v": 0}
@@ -457,7 +459,11 @@ def run_gpu(args, cfg_name, config):
                 prev["binned_host"].wait()
                 st.wait_event(prev["binned"])
             mark()
-            P.rd_preprocess(vw, g, cam, opts, stream=st)
+            if slot.get("k1_done") is not None:  # --k1 batched: the round's K1 ran in one launch
+                st.wait_event(slot["k1_done"])
+            else:
+                P.rd_preprocess(vw, g, cam, opts, stream=st)
+            mark()  # K1 done
             P.rd_bin(vw, stream=st)
             if args.stagger:
                 slot["binned"].record(st)
@@ -505,6 +511,9 @@ def run_gpu(args, cfg_name, config):
 
     pool = ThreadPoolExecutor(max_workers=max(1, args.pipeline)) if args.host_threads else None
 
+    def cam_of(k):
+        return my_views[k % len(my_views)]
+
     def run_views(per_view):
         """Zero the gradients, run B views through the slots, join, all-reduce.
         With host threads (default) each slot's views are issued by their own host thread, so
@@ -535,6 +544,18 @@ def run_gpu(args, cfg_name, config):
         for r0 in range(0, len(ks), P_):
             rnd = ks[r0:r0 + P_]
             used = [slots[i] for i in range(len(rnd))]
+            if args.k1 == "batched":  # one K1 launch for the round's views (rd_preprocess_views)
+                k1s = streams["k1"]
+                k1s.wait_event(start)
+                if r0 > 0:
+                    k1s.wait_event(k5_done)  # the previous round's K5 has read the views' 2-D gradients
+                P.rd_preprocess_views([sl["view"] for sl in used], g, [cam_of(k) for k in rnd], opts, stream=k1s)
+                k1_ev.record(k1s)
+                for sl in used:
+                    sl["k1_done"] = k1_ev
+            else:
+                for sl in used:
+                    sl["k1_done"] = None
             for i, sl in enumerate(used):
                 sl["binned_host"].clear()
                 sl["stagger_after"] = used[i - args.stagger] if args.stagger and i >= args.stagger else None
@@ -616,7 +637,7 @@ def run_gpu(args, cfg_name, config):
             for k, v in t["ms"].items():
                 acc[k] = acc.get(k, 0.0) + v / max(t["views"], 1) / len(slots)
         print("concurrent per-kernel ms per view:", {k: round(v, 4) for k, v in acc.items()}, flush=True)
-    if phase_log:  # diagnostics: [start, binned, fwd start, fwd end, K5 start, K5 end] per view, ms
+    if phase_log:  # diagnostics: [start, K1 done, binned, fwd start, fwd end, K4 end, K5 end] per view, ms
         t0e = phase_log[-4 * 5][0] if len(phase_log) >= 20 else phase_log[0][0]
         rows = [[t0e.elapsed_time(e) for e in ph] for ph in phase_log[-20:]]
         json.dump(rows, open(os.environ["RADE_PHASES"], "w"))
@@ -628,11 +649,11 @@ def run_gpu(args, cfg_name, config):
     # stream from one host thread, so the kernels are serialised and each one's CUDA-event time
     # is its own; timings are summed over the slots' views
     prof_stream = torch.cuda.Stream(device)
-    saved = [sl["stream"] for sl in slots], streams["k5"], pool, streams["zero"]
+    saved = [sl["stream"] for sl in slots], streams["k5"], pool, streams["zero"], streams["k1"]
     for sl in slots:
         sl["stream"] = prof_stream
         P.rd_set_profiling(sl["view"], True)
-    streams["k5"], streams["zero"], pool = prof_stream, prof_stream, None
+    streams["k5"], streams["zero"], streams["k1"], pool = prof_stream, prof_stream, prof_stream, None
     torch.cuda.synchronize()
     for _ in range(args.steps):
         step()
@@ -654,7 +675,7 @@ def run_gpu(args, cfg_name, config):
             tim["n_culled"][kname] += val
     for sl, st_ in zip(slots, saved[0]):
         sl["stream"] = st_
-    streams["k5"], pool, streams["zero"] = saved[1], saved[2], saved[3]
+    streams["k5"], pool, streams["zero"], streams["k1"] = saved[1], saved[2], saved[3], saved[4]
 
     # ---------------- end-to-end: per step, inputs from pinned host memory in, result out.
     # loss mode (default): a view's input is its ground-truth RGB image (uint8, the training
@@ -869,6 +890,8 @@ def run_gpu(args, cfg_name, config):
     views_per_rank = args.steps * B
     rounds = args.steps * math.ceil(B / P_)
     launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split", "set") else views_per_rank)
+    if args.k1 == "batched":  # one K1 per round instead of one per view
+        launches_total += rounds - views_per_rank
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
     vis_avg = tim["n_visible"] / max(views_timed, 1)
     config.update({
@@ -928,6 +951,8 @@ def main():
                     help="K5 of a round of views in one call: 'set' (default) sets the SH gradient rows in the "
                          "step's first round (RD_K5_SET_SH; only the other gradients are zeroed), 'batched' "
                          "accumulates all; 'split' runs the geometry parts per view; or 'per-view'")
+    ap.add_argument("--k1", default="batched", choices=["batched", "per-view"],
+                    help="K1 per view on its stream, or one rd_preprocess_views launch per round of views")
     ap.add_argument("--guard-band", type=float, default=None,
                     help="reading S6b guard band (0 = off); default: the config's (C3/C4 0.15, others off)")
     ap.add_argument("--dry-run-gloo", action="store_true",

@@ -196,6 +196,15 @@ rd_status rd_view_destroy(rd_view* view);
 rd_status rd_preprocess(rd_view* view, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
                         rd_stream stream);
 
+/* Stage 1 for n_views ≤ 8 views of the SAME Gaussians at once (a training step's round of
+ * views): equivalent to rd_preprocess on each (views[k], cams[k]) — bit for bit — but one K1
+ * launch on `stream` runs every Gaussian through all the views in turn, so its parameter and
+ * SH rows are read from DRAM once. cams: HOST array of n_views cameras; opt shared. The caller
+ * orders each view's later calls (on its own stream) after `stream`. Errors: n_views ∉ [1, 8],
+ * NULL / repeated views → RD_ERR_INVALID_ARGUMENT; otherwise as rd_preprocess. */
+rd_status rd_preprocess_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g, const rd_camera* cams,
+                              const rd_options* opt, rd_stream stream);
+
 /* Stage 2 (K2). Result: the M (tile, Gaussian id) pairs in the order of ONE stable sort of
  * the 64-bit keys (tile << 32 | float_bits(z_c)) emitted in id order — per tile the
  * Gaussians front to back by z_c, ties by id (the depth sort of PAPER:422, reading S7) — and

@@ -110,6 +110,8 @@ SIGNATURES = {
     "rd_preprocess_bwd_geometry": ([_VP, ctypes.POINTER(RdGaussians), ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
     "rd_preprocess_bwd_views_sh": ([ctypes.POINTER(_VP), ctypes.c_int32, ctypes.POINTER(RdGaussians),
                                     ctypes.POINTER(RdGrads), _VP], ctypes.c_int),
+    "rd_preprocess_views": ([ctypes.POINTER(_VP), ctypes.c_int32, ctypes.POINTER(RdGaussians),
+                             ctypes.POINTER(RdCamera), ctypes.POINTER(RdOptions), _VP], ctypes.c_int),
     "rd_preprocess_bwd_views_ex": ([ctypes.POINTER(_VP), ctypes.c_int32, ctypes.POINTER(RdGaussians),
                                     ctypes.POINTER(RdGrads), ctypes.c_uint32, _VP], ctypes.c_int),
     "rd_view_stats": ([_VP, ctypes.POINTER(RdStats)], ctypes.c_int),

@@ -252,8 +252,8 @@ rd_status rd_view_destroy(rd_view* v) {
 
 static bool in01(float x) { return x > 0.f && x < 1.f && std::isfinite(x); }
 
-rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
-                        rd_stream stream) {
+static rd_status preprocess_setup(rd_view* v, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
+                                 cudaStream_t s) {
   g_err.clear();
   if (!v || !g || !cam || !opt) return fail(RD_ERR_INVALID_ARGUMENT, "NULL view/gaussians/camera/options");
   if (g->n < 0) return fail(RD_ERR_INVALID_ARGUMENT, "n < 0");
@@ -286,7 +286,6 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   if (tiles_x > bin_max_tiles_per_axis() || tiles_y > bin_max_tiles_per_axis())
     return fail(RD_ERR_INVALID_ARGUMENT, "image too large: more than %d tiles per axis", bin_max_tiles_per_axis());
 
-  cudaStream_t s = (cudaStream_t)stream;
   v->n = g->n;
   v->sh_coeffs = g->sh_coeffs;
   DevCam& c = v->cam;
@@ -342,19 +341,70 @@ rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam,
   }
   if (!v->m_ready) RD_CUDA(cudaEventCreateWithFlags(&v->m_ready, cudaEventDisableTiming));
 
-  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
-  v->begin(s);  // K1 timing includes the zeroing of its counters
-  RD_CUDA(cudaMemsetAsync(v->bincnt.ptr, 0, kBinCntHist * sizeof(uint32_t), s));
-  launch_preprocess_fwd(dg, c, o, tiles_x, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
-                        (uint32_t*)v->dkey0.ptr, (uint32_t*)v->bincnt.ptr, (uint32_t*)v->vis.ptr,
-                        (uint32_t*)v->big.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
-  RD_CHECK_LAUNCH("preprocess_fwd");
-  v->end(K_PRE, s);
+  return RD_OK;
+}
+
+// After K1 (one view or a round): the view's state.
+static void preprocess_done(rd_view* v) {
   v->stage = 1;
   v->binned = false;
   v->M = 0;
   v->n_vis = v->n_big = 0;
   v->g2d_dirty = false;
+}
+
+rd_status rd_preprocess(rd_view* v, const rd_gaussians* g, const rd_camera* cam, const rd_options* opt,
+                        rd_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  rd_status st = preprocess_setup(v, g, cam, opt, s);
+  if (st != RD_OK) return st;
+  const DevCam& c = v->cam;
+  const DevOpt& o = v->opt;
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
+  v->begin(s);  // K1 timing includes the zeroing of its counters
+  RD_CUDA(cudaMemsetAsync(v->bincnt.ptr, 0, kBinCntHist * sizeof(uint32_t), s));
+  launch_preprocess_fwd(dg, c, o, v->tiles_x, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
+                        (uint32_t*)v->dkey0.ptr, (uint32_t*)v->bincnt.ptr, (uint32_t*)v->vis.ptr,
+                        (uint32_t*)v->big.ptr, (G2D*)v->g2d.ptr, v->ctr(), s);
+  RD_CHECK_LAUNCH("preprocess_fwd");
+  v->end(K_PRE, s);
+  preprocess_done(v);
+  return RD_OK;
+}
+
+rd_status rd_preprocess_views(rd_view* const* views, int32_t n_views, const rd_gaussians* g, const rd_camera* cams,
+                              const rd_options* opt, rd_stream stream) {
+  g_err.clear();
+  if (!views || !cams) return fail(RD_ERR_INVALID_ARGUMENT, "NULL views / cameras");
+  if (n_views < 1 || n_views > kMaxBatchViews)
+    return fail(RD_ERR_INVALID_ARGUMENT, "n_views must be 1..%d", kMaxBatchViews);
+  for (int k = 0; k < n_views; ++k) {
+    if (!views[k]) return fail(RD_ERR_INVALID_ARGUMENT, "views[%d] is NULL", k);
+    for (int j = 0; j < k; ++j)
+      if (views[j] == views[k]) return fail(RD_ERR_INVALID_ARGUMENT, "views[%d] repeats views[%d]", k, j);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  K1Views kv{};
+  kv.nv = n_views;
+  for (int k = 0; k < n_views; ++k) {
+    rd_view* v = views[k];
+    rd_status st = preprocess_setup(v, g, &cams[k], opt, s);
+    if (st != RD_OK) return st;
+    RD_CUDA(cudaMemsetAsync(v->bincnt.ptr, 0, kBinCntHist * sizeof(uint32_t), s));
+    kv.v[k] = K1Out{v->cam, (Record*)v->rec.ptr, (uint2*)v->rect.ptr, (uint32_t*)v->touched.ptr,
+                    (uint32_t*)v->dkey0.ptr, (uint32_t*)v->bincnt.ptr, (uint32_t*)v->vis.ptr, (uint32_t*)v->big.ptr,
+                    (G2D*)v->g2d.ptr, v->ctr()};
+  }
+  DevGauss dg{g->n, g->sh_coeffs, g->means, g->scales, g->rotations, g->opacities, g->sh, g->filter3d};
+  rd_view* v0 = views[0];
+  v0->begin(s);  // timed on views[0] (one K1 launch for the round)
+  launch_preprocess_fwd_views(dg, v0->opt, kv, s);
+  RD_CHECK_LAUNCH("preprocess_fwd_views");
+  v0->end(K_PRE, s);
+  for (int k = 0; k < n_views; ++k) {
+    views[k]->last_stream = s;
+    preprocess_done(views[k]);
+  }
   return RD_OK;
 }
 

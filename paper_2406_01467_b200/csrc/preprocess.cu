@@ -429,20 +429,20 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
 #endif
 // K5b at ≤ 80 registers (768 threads per SM): more warps in flight for its gathers (0.096 -> 0.082 ms)
 #define RD_K5_MINB (768 / RD_K5_THREADS)
-template <int DEG>
 #ifndef RD_K1_THREADS
 #define RD_K1_THREADS 64  // finer blocks fill the SMs more evenly: 0.107 -> 0.101 ms
 #endif
 #ifndef RD_K1_MINB
 #define RD_K1_MINB 8  // ≤ 128 registers: 16 warps per SM for the latency-bound loads
 #endif
-__global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
-                                                         Record* __restrict__ rec, uint2* __restrict__ rect,
-                                                         uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
-                                                         uint32_t* __restrict__ count, uint32_t* __restrict__ vis,
-                                                         uint32_t* __restrict__ big, G2D* __restrict__ g2d,
-                                                         Counter* __restrict__ counters) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// The per-Gaussian part of K1 for one view plus its warp-level appends (all 32 lanes call it).
+template <int DEG>
+__device__ __forceinline__ void k1_view(const DevGauss& g, int64_t i, const DevCam& cam, const DevOpt& opt,
+                                        Record* __restrict__ rec, uint2* __restrict__ rect,
+                                        uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
+                                        uint32_t* __restrict__ count, uint32_t* __restrict__ vis,
+                                        uint32_t* __restrict__ big, G2D* __restrict__ g2d,
+                                        Counter* __restrict__ counters) {
   const int lane = (int)(threadIdx.x & 31);
   uint32_t x0 = 0, y0 = 0, w = 1, nt = 0;
   int why = kVisible;
@@ -480,6 +480,31 @@ __global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(De
   if (bigg) {
     RD_CHECK((int64_t)(bbase + __popc(bmask & below)) < g.n);
     big[bbase + __popc(bmask & below)] = (uint32_t)i;
+  }
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd(DevGauss g, DevCam cam, DevOpt opt, int tiles_x,
+                                                         Record* __restrict__ rec, uint2* __restrict__ rect,
+                                                         uint32_t* __restrict__ touched, uint32_t* __restrict__ dkey,
+                                                         uint32_t* __restrict__ count, uint32_t* __restrict__ vis,
+                                                         uint32_t* __restrict__ big, G2D* __restrict__ g2d,
+                                                         Counter* __restrict__ counters) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  k1_view<DEG>(g, i, cam, opt, rec, rect, touched, dkey, count, vis, big, g2d, counters);
+}
+
+// K1 over a round of views of the same Gaussians: each thread runs its Gaussian through every
+// view in turn, so the parameter and SH rows come from DRAM once and from L1/L2 after that
+// (4 views read 84 MB of parameters and ~0.2 GB of SH rows once instead of 4×).
+template <int DEG>
+__global__ void __launch_bounds__(RD_K1_THREADS, RD_K1_MINB) k_preprocess_fwd_views(DevGauss g, DevOpt opt,
+                                                                              const __grid_constant__ K1Views kv) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 1
+  for (int v = 0; v < kv.nv; ++v) {
+    const K1Out& o = kv.v[v];
+    k1_view<DEG>(g, i, o.cam, opt, o.rec, o.rect, o.touched, o.dkey, o.count, o.vis, o.big, o.g2d, o.counters);
   }
 }
 
@@ -1054,6 +1079,18 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
     default: RD_K1(3); break;
   }
 #undef RD_K1
+}
+
+void launch_preprocess_fwd_views(const DevGauss& g, const DevOpt& opt, const K1Views& kv, cudaStream_t s) {
+  if (g.n == 0 || kv.nv <= 0) return;
+  const int threads = RD_K1_THREADS;
+  const unsigned blocks = (unsigned)((g.n + threads - 1) / threads);
+  switch (opt.sh_degree) {
+    case 0: k_preprocess_fwd_views<0><<<blocks, threads, 0, s>>>(g, opt, kv); break;
+    case 1: k_preprocess_fwd_views<1><<<blocks, threads, 0, s>>>(g, opt, kv); break;
+    case 2: k_preprocess_fwd_views<2><<<blocks, threads, 0, s>>>(g, opt, kv); break;
+    default: k_preprocess_fwd_views<3><<<blocks, threads, 0, s>>>(g, opt, kv); break;
+  }
 }
 
 void launch_preprocess_bwd(const DevGauss& g, const DevCam& cam, const DevOpt& opt, const uint32_t* tiles_touched,

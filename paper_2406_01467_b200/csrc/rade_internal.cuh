@@ -231,6 +231,24 @@ void launch_preprocess_fwd(const DevGauss& g, const DevCam& cam, const DevOpt& o
                            uint32_t* vis, uint32_t* big, G2D* g2d, Counter* counters, cudaStream_t s);
 // K5 = K5a (SH; over the n_vis visible ids of K1's list) then K5b (geometry: fp32 in id
 // order for the visible Gaussians that are not is_big, fp64 over the big list).
+// K1 over a round of views (rd_preprocess_views): per view its camera and output arrays
+struct K1Out {
+  DevCam cam;
+  Record* rec;
+  uint2* rect;
+  uint32_t* touched;
+  uint32_t* dkey;
+  uint32_t* count;
+  uint32_t* vis;
+  uint32_t* big;
+  G2D* g2d;
+  Counter* counters;
+};
+struct K1Views {
+  int nv;
+  K1Out v[8];
+};
+void launch_preprocess_fwd_views(const DevGauss& g, const DevOpt& opt, const K1Views& kv, cudaStream_t s);
 // K5 parts: the SH colour (+ view-direction) part and the geometry part (K5b64 + K5b); both
 // add into the gradients with reductions, so they may run in any order
 constexpr int kK5Sh = 1, kK5Geometry = 2, kK5All = 3;

@@ -191,6 +191,23 @@ def rd_preprocess(view: View, gaussians: Gaussians, camera, options=None, stream
     view.camera, view.options, view.n = c, o, gaussians.n
 
 
+def rd_preprocess_views(views, gaussians: Gaussians, cameras, options=None, stream=None):
+    """K1 for a round of views (≤ 8) of the same Gaussians in one launch on `stream`
+    (parameter and SH rows read once); = rd_preprocess on each view."""
+    views = list(views)
+    if len(cameras) != len(views):
+        raise ValueError("one camera per view")
+    arr = (ctypes.c_void_p * len(views))(*[v.handle for v in views])
+    g = gaussians.c_struct()
+    cs = [camera_struct(c) for c in cameras]
+    carr = (N.RdCamera * len(cs))(*cs)
+    o = options_struct(options)
+    N.check(N.load().rd_preprocess_views(arr, len(views), ctypes.byref(g), carr, ctypes.byref(o),
+                                         _stream_ptr(stream)), "rd_preprocess_views")
+    for v, c in zip(views, cs):
+        v.camera, v.options, v.n = c, o, gaussians.n
+
+
 def rd_bin(view: View, stream=None) -> int:
     m = ctypes.c_int64(0)
     N.check(view.lib.rd_bin(view.handle, ctypes.byref(m), _stream_ptr(stream)), "rd_bin")

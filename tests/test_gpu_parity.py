@@ -902,6 +902,34 @@ def test_batched_k5_argument_errors():
     assert e.value.status == 2
 
 
+def test_preprocess_views_equals_per_view():
+    """rd_preprocess_views (one K1 launch over a round of views) = rd_preprocess on each view,
+    bit for bit: records, rects, tile counts, and the binned lists and renders that follow."""
+    scene, cams = dense_scene(38, 400, zr=(3.0, 6.0)), _orbit_cams(3)
+    opt = sg.Options(tile=8)
+    g = P.Gaussians.from_numpy(scene)
+    batched = [P.View() for _ in cams]
+    P.rd_preprocess_views(batched, g, cams, opts_dict(opt))
+    for v, cam in zip(batched, cams):
+        single = P.View()
+        P.rd_preprocess(single, g, cam, opts_dict(opt))
+        (ra, ea, ta), (rb, eb, tb) = P.rd_debug_preprocess(v), P.rd_debug_preprocess(single)
+        assert torch.equal(ta, tb)
+        vis = tb > 0  # culled Gaussians get no record / rect
+        assert vis.any()
+        assert torch.equal(ra[vis], rb[vis]) and torch.equal(ea[vis], eb[vis])
+        P.rd_bin(v)
+        P.rd_bin(single)
+        for a, b in zip(P.rd_debug_binning(v), P.rd_debug_binning(single)):
+            assert torch.equal(a, b)
+        o1, o2 = P.rd_render_fwd(v), P.rd_render_fwd(single)
+        torch.cuda.synchronize()
+        for k in o1:
+            assert torch.equal(o1[k], o2[k]), k
+    with pytest.raises(P.rade.N.RadeError):
+        P.rd_preprocess_views([batched[0], batched[0]], g, cams[:2], opts_dict(opt))
+
+
 def test_bin_twice_keeps_the_lists():
     """A second rd_bin before the next rd_preprocess returns the same M and leaves keys, ids and
     ranges bit-identical (the depth passes consume K1's id-order keys, so it must not re-sort);
