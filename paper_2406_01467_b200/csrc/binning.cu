@@ -15,7 +15,7 @@
 //        (z_c, id): z_c > znear > 0, so the IEEE bit pattern orders like the value
 //   K2b  inclusive scan of tiles_touched gathered in that order → offsets (single pass,
 //        decoupled look-back)
-//   K2c  duplicate + first tile pass, fused: each 2048-output block emits (tile, id) for its
+//   K2c  duplicate + first tile pass, fused: each 4096-output block emits (tile, id) for its
 //        outputs (load-balanced over outputs, as K2's generator) and ranks them by the first
 //        tile digit right away, so the unsorted duplicates never reach HBM
 //   K2d  remaining tile passes: the tile key is packed as (ty << 16 | tx) and sorted tx digits
@@ -24,8 +24,8 @@
 //        tiles up to 2048×2048 px this is 2 passes (tx, ty ≤ 256)
 //   K2e  ranges[tile] = [first, last) in the sorted list
 //
-// Every onesweep pass: 256 threads × 8 items per block (2048), items warp-striped so a
-// warp-wide __match_any_sync ranks them stably; per-warp digit counters → warp offsets →
+// Every onesweep pass: 512 threads × 8 items per block (4096), items warp-striped so a
+// warp ranks them stably (8 ballots per item); per-warp digit counters → warp offsets →
 // block-local sorted layout in shared memory; the block's per-digit counts published to and
 // prefixed by a decoupled look-back over the blocks (one thread per digit, a window of
 // predecessors per round trip; status words carry an epoch tag, so no zeroing between
