@@ -847,6 +847,12 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
   constexpr int NV = 3 * K, NV4 = (NV + 3) / 4, P = NV4 + 1;
   __shared__ float4 s_coef[2][32 * P];
   __shared__ float4 s_grad[2][32 * P];
+#ifndef RD_K5AV_PRE
+#define RD_K5AV_PRE 2  // views whose colour gradients are prefetched into shared memory
+#endif
+  // the colour gradient (G2D f[1..3]) of the first RD_K5AV_PRE views, copied in with the SH rows
+  // (cp.async: no registers) instead of one dependent load per view inside the view loop
+  __shared__ float s_drgb[RD_K5AV_PRE > 0 ? 2 : 1][RD_K5AV_PRE > 0 ? RD_K5AV_PRE : 1][3][32];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned mask = 0u;
@@ -874,6 +880,15 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
     if ((vmask >> row) & 1u) cp_async16(&sc[row * P + c], &sh4[(base + row) * L4 + c]);
   }
+  if (RD_K5AV_PRE > 0) {
+#pragma unroll
+    for (int v = 0; v < (RD_K5AV_PRE > 0 ? RD_K5AV_PRE : 1); ++v)
+      if (v < vb.nv && ((mask >> v) & 1u)) {
+        const float* f = vb.g2d[v][id].f + 1;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async4(&s_drgb[warp][v][c][lane], f + c);
+      }
+  }
   cp_async_commit();
 #pragma unroll
   for (int q = 0; q < NV4; ++q) sg[lane * P + q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -892,8 +907,16 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
     for (int v = 0; v < vb.nv; ++v) {
       if (!((mask >> v) & 1u)) continue;
       const DevCam& cam = vb.cam[v];
-      const G2D* row = vb.g2d[v] + id;
-      const float d_rgb[3] = {row->f[1], row->f[2], row->f[3]};
+      float d_rgb[3];
+      if (v < RD_K5AV_PRE) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d_rgb[c] = s_drgb[warp][v < RD_K5AV_PRE ? v : 0][c][lane];
+      } else {
+        const G2D* row = vb.g2d[v] + id;
+        d_rgb[0] = row->f[1];
+        d_rgb[1] = row->f[2];
+        d_rgb[2] = row->f[3];
+      }
       const float ex = mu0 - cam.campos[0], ey = mu1 - cam.campos[1], ez = mu2 - cam.campos[2];
       const float idl = rsqrtf(ex * ex + ey * ey + ez * ez);
       const float hx = ex * idl, hy = ey * idl, hz = ez * idl;
