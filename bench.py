@@ -412,8 +412,11 @@ def run_gpu(args, cfg_name, config):
         args.pipeline = min(max(1, B), 8)
     P_ = max(1, args.pipeline)
     slots = []
-    for _ in range(P_):
-        st = torch.cuda.Stream(device)
+    lo_prio, hi_prio = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+    config["stream_priorities"] = args.prio
+    for i in range(P_):
+        # --prio views: slot i at priority hi + i (clamped to the device's range; lower = higher)
+        st = torch.cuda.Stream(device, priority=min(lo_prio, hi_prio + i) if args.prio != "none" else 0)
         with torch.cuda.stream(st):  # the view's scratch is allocated on its own stream
             slot = {"stream": st, "view": P.View(device),
                     # the maps are planes of one [10, H, W] buffer: one D2H copy per view (e2e)
@@ -429,7 +432,7 @@ def run_gpu(args, cfg_name, config):
         slots.append(slot)
     view = slots[0]["view"]
     outs = slots[0]["outs"]
-    streams = {"k5": torch.cuda.Stream(device),  # the batched K5 of each round of views
+    streams = {"k5": torch.cuda.Stream(device, priority=hi_prio if args.prio == "views-k5" else 0),  # the batched K5
                "zero": torch.cuda.Stream(device),  # the step's gradient zeroing
                "k1": torch.cuda.Stream(device)}  # --k1 batched: the round's K1
     k1_ev = torch.cuda.Event()
@@ -973,6 +976,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nccl-single", action="store_true",
                     help="at N = 1, run the multi-GPU code path anyway (an NCCL group of one rank)")
+    ap.add_argument("--prio", default="none", choices=["none", "views", "views-k5"],
+                    help="stream priorities: views = the round's earlier views on higher-priority streams "
+                         "(they finish binning first and their K3/K4 fill the others' latency gaps); "
+                         "views-k5 = also the K5 stream highest")
     ap.add_argument("--stagger", type=int, default=0,
                     help="view k of a round starts once view k - S is binned (0: all views at once)")
     ap.add_argument("--e2e-mode", default="loss", choices=["loss", "maps"],

@@ -832,6 +832,9 @@ struct ViewsBwd {
   const G2D* g2d[kMaxBatchViews];
 };
 
+#ifndef RD_K5AV_TOUCHED_UNROLL
+#define RD_K5AV_TOUCHED_UNROLL 1
+#endif
 #ifndef RD_K5AV_MINB
 #define RD_K5AV_MINB 8  // ≤ 128 registers (16 warps per SM): 12 and 10 spilled and measured slower
 #endif
@@ -857,8 +860,17 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned mask = 0u;
   if (id < g.n) {
+#if RD_K5AV_TOUCHED_UNROLL
+    // every view's load issued before the first use: one round trip, not one per view
+    uint32_t t[kMaxBatchViews];
+#pragma unroll
+    for (int v = 0; v < kMaxBatchViews; ++v) t[v] = v < vb.nv ? vb.touched[v][id] : 0u;
+#pragma unroll
+    for (int v = 0; v < kMaxBatchViews; ++v) mask |= (t[v] > 0u ? 1u : 0u) << v;
+#else
 #pragma unroll 1
     for (int v = 0; v < vb.nv; ++v) mask |= (vb.touched[v][id] > 0u ? 1u : 0u) << v;
+#endif
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, mask != 0u);
   const int64_t base = id - lane;
