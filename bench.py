@@ -501,11 +501,11 @@ def run_gpu(args, cfg_name, config):
             if io:
                 io["k4_done"].record(st)
             mark()
-            if args.k5 in ("per-view", "split"):
+            if args.k5 in ("per-view", "split", "split-set"):
                 st.wait_event(zeroed["ev"])  # the step's gradients are zeroed
             if args.k5 == "per-view":
                 P.rd_preprocess_bwd(vw, g, grads, stream=st)  # K5: += by L2 reductions
-            elif args.k5 == "split":  # K5 geometry now, overlapping the other views' K3/K4
+            elif args.k5 in ("split", "split-set"):  # K5 geometry now, overlapping the other views' K3/K4
                 P.rd_preprocess_bwd_geometry(vw, g, grads, stream=st)
             slot["done"].record(st)  # batched K5: the round's rd_preprocess_bwd_views waits for this
             mark()
@@ -531,7 +531,7 @@ def run_gpu(args, cfg_name, config):
         zs = streams["zero"]
         zs.wait_event(start)
         with torch.cuda.stream(zs):
-            if args.k5 == "set":  # the first round's K5 sets the SH rows (RD_K5_SET_SH)
+            if args.k5 in ("set", "split-set"):  # the first round's K5 sets the SH rows (RD_K5_SET_SH)
                 fg.zero_geometry_()
             else:
                 fg.zero_()
@@ -573,13 +573,17 @@ def run_gpu(args, cfg_name, config):
                 futs = [pool.submit(worker, sl, k) for sl, k in zip(used, rnd)]
                 for f in futs:
                     f.result()
-            if args.k5 in ("batched", "split", "set"):
+            if args.k5 in ("batched", "split", "set", "split-set"):
                 k5s = streams["k5"]
                 k5s.wait_event(zeroed["ev"])
                 for sl in used:
                     k5s.wait_event(sl["done"])
                 if args.k5 == "split":  # the round's SH part (its geometry parts ran per view)
                     P.rd_preprocess_bwd_views_sh([sl["view"] for sl in used], g, grads, stream=k5s)
+                elif args.k5 == "split-set":  # the round's SH part, setting the rows in the first round
+                    P.rd_preprocess_bwd_views_ex([sl["view"] for sl in used], g, grads,
+                                                 flags=P.rade.RD_K5_SH_ONLY | (P.rade.RD_K5_SET_SH if r0 == 0 else 0),
+                                                 stream=k5s)
                 elif args.k5 == "set":  # the step's first round SETS the SH gradient rows
                     P.rd_preprocess_bwd_views_ex([sl["view"] for sl in used], g, grads,
                                                  flags=P.rade.RD_K5_SET_SH if r0 == 0 else 0, stream=k5s)
@@ -892,7 +896,7 @@ def run_gpu(args, cfg_name, config):
     launches_per_view = 1 + 1 + 4 + 1 + tile_passes + 1 + 1 + 1 + 1 + 2
     views_per_rank = args.steps * B
     rounds = args.steps * math.ceil(B / P_)
-    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split", "set") else views_per_rank)
+    launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split", "set", "split-set") else views_per_rank)
     if args.k1 == "batched":  # one K1 per round instead of one per view
         launches_total += rounds - views_per_rank
     M_avg = tim["n_duplicates"] / max(views_timed, 1)
@@ -950,7 +954,7 @@ def main():
     ap.add_argument("--views-per-step", default="4",
                     help="views per rank per step, or 'epoch' (ceil(views / ranks): one all-reduce per epoch)")
     ap.add_argument("--bucket-mb", type=int, default=64, help="all-reduce bucket size (N > 1)")
-    ap.add_argument("--k5", default="set", choices=["set", "batched", "split", "per-view"],
+    ap.add_argument("--k5", default="set", choices=["set", "batched", "split", "split-set", "per-view"],
                     help="K5 of a round of views in one call: 'set' (default) sets the SH gradient rows in the "
                          "step's first round (RD_K5_SET_SH; only the other gradients are zeroed), 'batched' "
                          "accumulates all; 'split' runs the geometry parts per view; or 'per-view'")
