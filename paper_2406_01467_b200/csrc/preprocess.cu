@@ -793,7 +793,17 @@ __global__ void __launch_bounds__(RD_K5_THREADS, RD_K5_MINB) k_preprocess_bwd(De
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n_vis) {
     const uint32_t i = vis[p];  // over K1's visible list: every thread has work
-    if (!is_big(touched[i], opt.tile)) {  // else K5b64's
+#ifndef RD_K5B_EARLY
+#define RD_K5B_EARLY 1
+#endif
+    if (RD_K5B_EARLY) {
+      // tiles_touched loaded beside the parameters and the 2-D gradient row (one round trip after
+      // the id, not two); the few big Gaussians (K5b64's) compute and drop their result
+      const bool big = is_big(touched[i], opt.tile);
+      GradAcc acc;
+      grad_zero(acc);
+      if (geometry_backward<float>(g, i, cam, opt, g2d, acc) && !big) grad_flush(acc, gr, i);
+    } else if (!is_big(touched[i], opt.tile)) {  // else K5b64's
       GradAcc acc;
       grad_zero(acc);
       if (geometry_backward<float>(g, i, cam, opt, g2d, acc)) grad_flush(acc, gr, i);
