@@ -552,10 +552,17 @@ def run_gpu(args, cfg_name, config):
                 k1s.wait_event(start)
                 if r0 > 0:
                     k1s.wait_event(k5_done)  # the previous round's K5 has read the views' 2-D gradients
-                P.rd_preprocess_views([sl["view"] for sl in used], g, [cam_of(k) for k in rnd], opts, stream=k1s)
-                k1_ev.record(k1s)
-                for sl in used:
-                    sl["k1_done"] = k1_ev
+                # --k1-groups G: the round's views in G batched K1 launches, so the first group's
+                # views start binning while the next group's K1 runs
+                ng = max(1, min(args.k1_groups, len(used)))
+                per = (len(used) + ng - 1) // ng
+                for gi in range(0, len(used), per):
+                    grp, gk = used[gi:gi + per], rnd[gi:gi + per]
+                    P.rd_preprocess_views([sl["view"] for sl in grp], g, [cam_of(k) for k in gk], opts, stream=k1s)
+                    ev = k1_ev if gi == 0 else torch.cuda.Event()
+                    ev.record(k1s)
+                    for sl in grp:
+                        sl["k1_done"] = ev
             else:
                 for sl in used:
                     sl["k1_done"] = None
@@ -980,6 +987,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nccl-single", action="store_true",
                     help="at N = 1, run the multi-GPU code path anyway (an NCCL group of one rank)")
+    ap.add_argument("--k1-groups", type=int, default=1,
+                    help="--k1 batched: the round's views in this many batched K1 launches (1 = one launch)")
     ap.add_argument("--prio", default="none", choices=["none", "views", "views-k5"],
                     help="stream priorities: views = the round's earlier views on higher-priority streams "
                          "(they finish binning first and their K3/K4 fill the others' latency gaps); "
