@@ -884,23 +884,33 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
   }
   const unsigned vmask = __ballot_sync(0xffffffffu, mask != 0u);
   const int64_t base = id - lane;
-  const int64_t L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
-  float4* gsh4 = reinterpret_cast<float4*>(gr.sh);
+  const int L4 = g.sh_coeffs * 3 / 4;  // global row pitch in float4
+  // the warp's 32 rows: one block of 32·L4 float4 from here (32-bit offsets within it)
+  float4* gsh4 = reinterpret_cast<float4*>(gr.sh) + base * L4;
+  const int nrows = g.n - base < 32 ? (int)(g.n - base) : 32;  // rows of the warp that exist
   if (vmask == 0u) {  // warp-uniform: none of the 32 Gaussians is visible in any view
     if (set_sh) {  // set mode: their SH gradient rows are 0
-      for (int f = lane; f < 32 * (int)L4; f += 32)
-        if (base + f / L4 < g.n) gsh4[base * L4 + f] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int f = lane; f < nrows * L4; f += 32) gsh4[f] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     return;
   }
   if (counters && lane == 0) atomicAdd(counters + 4, (Counter)__popc(vmask));
   float4* sc = s_coef[warp];
   float4* sg = s_grad[warp];
-  const float4* sh4 = reinterpret_cast<const float4*>(g.sh);
+  const float4* sh4 = reinterpret_cast<const float4*>(g.sh) + base * L4;
+  if (L4 == NV4) {  // rows of exactly the active coefficients: the warp's block is contiguous
+    const float4* src = sh4 + lane;
 #pragma unroll
-  for (int it = 0; it < NV4; ++it) {
-    const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
-    if ((vmask >> row) & 1u) cp_async16(&sc[row * P + c], &sh4[(base + row) * L4 + c]);
+    for (int it = 0; it < NV4; ++it) {
+      const unsigned f = (unsigned)(it * 32 + lane), row = f / (unsigned)NV4;
+      if ((vmask >> row) & 1u) cp_async16(&sc[f + row], src + it * 32);
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < NV4; ++it) {
+      const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
+      if ((vmask >> row) & 1u) cp_async16(&sc[row * P + c], &sh4[row * L4 + c]);
+    }
   }
   if (RD_K5AV_PRE > 0) {
 #pragma unroll
@@ -981,22 +991,34 @@ __global__ void __launch_bounds__(64, RD_K5AV_MINB) k_preprocess_bwd_sh_views(De
   __syncwarp();
   if (set_sh) {  // set mode: every row of the warp is written (0 where visible in no view), the
     // old values never read (the rows' 192-B read of the reduction disappears)
+    if (nrows == 32 && L4 == NV4) {  // the usual case: the warp's rows are one contiguous block
+      float4* dst = gsh4 + lane;
+#pragma unroll
+      for (int it = 0; it < NV4; ++it) {
+        const unsigned f = (unsigned)(it * 32 + lane), row = f / (unsigned)NV4;
+        dst[it * 32] = sg[f + row];  // row·P + c = f + row (P = NV4 + 1)
+      }
+      return;
+    }
 #pragma unroll
     for (int it = 0; it < NV4; ++it) {
       const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
-      if (base + row < g.n) gsh4[(base + row) * L4 + c] = sg[row * P + c];
+      if (row < nrows) gsh4[row * L4 + c] = sg[row * P + c];
     }
     // coefficients above the active degree get no gradient: 0
-    for (int f = lane; f < 32 * (int)(L4 - NV4); f += 32) {
-      const int row = f / (int)(L4 - NV4), c = NV4 + f % (int)(L4 - NV4);
-      if (base + row < g.n) gsh4[(base + row) * L4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (L4 > NV4) {
+      const int W = L4 - NV4;
+      for (int f = lane; f < nrows * W; f += 32) {
+        const int row = f / W, c = NV4 + (f - row * W);
+        gsh4[row * L4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
     return;
   }
 #pragma unroll
   for (int it = 0; it < NV4; ++it) {
     const int f = it * 32 + lane, row = f / NV4, c = f - row * NV4;
-    if ((vmask >> row) & 1u) red_add4(&gsh4[(base + row) * L4 + c], sg[row * P + c]);
+    if ((vmask >> row) & 1u) red_add4(&gsh4[row * L4 + c], sg[row * P + c]);
   }
 }
 
