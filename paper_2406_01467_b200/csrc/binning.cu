@@ -220,12 +220,24 @@ __global__ void __launch_bounds__(kHistThreads) k_bin_hist(int64_t n, const uint
   uint32_t mdup = 0u;  // this thread's duplicates (tiles touched)
   const int64_t stride = (int64_t)gridDim.x * kHistThreads;
   const int64_t rounds = (n + stride - 1) / stride;  // warp-uniform trip count (match_any below)
-  for (int64_t r = 0; r < rounds; ++r) {
-    const int64_t i = r * stride + (int64_t)blockIdx.x * kHistThreads + tid;
-    const uint32_t k = i < n ? dkey[i] : 0xffffffffu;
+#ifndef RD_HIST_U
+#define RD_HIST_U 4  // rounds whose key and rect loads are issued together (one round trip per U)
+#endif
+  for (int64_t r0 = 0; r0 < rounds; r0 += RD_HIST_U) {
+    uint32_t kk[RD_HIST_U];
+    uint2 qq[RD_HIST_U];
+#pragma unroll
+    for (int u = 0; u < RD_HIST_U; ++u) {  // loads first (rect unconditionally: no key → rect chain)
+      const int64_t i = (r0 + u) * stride + (int64_t)blockIdx.x * kHistThreads + tid;
+      kk[u] = i < n ? dkey[i] : 0xffffffffu;
+      qq[u] = i < n ? rect[i] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < RD_HIST_U; ++u) {
+    if (r0 + u >= rounds) break;  // warp-uniform
+    const uint32_t k = kk[u];
     const bool vis = k != 0xffffffffu;
-    uint2 q = make_uint2(0u, 0u);
-    if (vis) q = rect[i];
+    const uint2 q = qq[u];
     if (vis) {  // the low digits of nearby depths differ: plain shared atomics
       atomicAdd(&sh[0][k & 255u], 1u);
       atomicAdd(&sh[1][(k >> 8) & 255u], 1u);
@@ -244,6 +256,7 @@ __global__ void __launch_bounds__(kHistThreads) k_bin_hist(int64_t n, const uint
       atomicAdd(&sy[y0], x1 - x0);
       atomicSub(&sy[y1], x1 - x0);
       mdup += (uint32_t)((x1 - x0) * (y1 - y0));
+    }
     }
   }
   mdup = __reduce_add_sync(0xffffffffu, mdup);

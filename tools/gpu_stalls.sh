@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $B > /dev/null 2>&1 || { echo "bench failed"; exit 1; }
 timeout 900 ncu --section WarpStateStats --section SchedulerStats --section Occupancy --section LaunchStats \
-  --clock-control none -k regex:"${KREGEX:-k_render_(fwd|bwd)}" -s 8 -c ${KCOUNT:-2} --csv --page raw \
+  --clock-control none -k regex:"${KREGEX:-k_render_(fwd|bwd)}" -s ${KSKIP:-8} -c ${KCOUNT:-2} --csv --page raw \
   --log-file gpurun_out/stalls_${TAG}.csv $B > /dev/null 2>&1
 python - gpurun_out/stalls_${TAG}.csv <<'PY'
 import csv, sys
