@@ -428,7 +428,9 @@ __device__ __forceinline__ uint32_t preprocess_one(const DevGauss& g, int64_t i,
 #define RD_K5_THREADS 128
 #endif
 // K5b at ≤ 80 registers (768 threads per SM): more warps in flight for its gathers (0.096 -> 0.082 ms)
-#define RD_K5_MINB (768 / RD_K5_THREADS)
+#ifndef RD_K5_MINB
+#define RD_K5_MINB (768 / RD_K5_THREADS)  // (measured: 5 → 96 registers, 7 → 72: both slower)
+#endif
 #ifndef RD_K1_THREADS
 #define RD_K1_THREADS 64  // finer blocks fill the SMs more evenly: 0.107 -> 0.101 ms
 #endif
