@@ -875,6 +875,18 @@ def test_batched_k5_set_sh_rows(sh_degree):
     assert not sh[~vis].any()  # rows of Gaussians visible in no view: 0
     K = (sh_degree + 1) ** 2
     assert not sh[:, 3 * K:].any()  # coefficients above the active degree: 0
+    # bench --k5 split-set: each view's geometry part on its own, then the round's SH part
+    # setting the rows (RD_K5_SH_ONLY | RD_K5_SET_SH) — the same gradients
+    spl = g.zeros_like()
+    spl.sh.fill_(-7.0)
+    for v in views:
+        P.rd_preprocess_bwd_geometry(v, g, spl)
+    P.rd_preprocess_bwd_views_ex(views, g, spl, flags=P.rade.RD_K5_SH_ONLY | P.rade.RD_K5_SET_SH)
+    torch.cuda.synchronize()
+    assert torch.equal(spl.sh, ref.sh)
+    for name in ("means", "scales", "rotations", "opacities"):
+        a, b = getattr(spl, name).cpu().numpy(), getattr(ref, name).cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-6 * max(np.abs(b).max(), 1e-30), name
     with pytest.raises(P.rade.N.RadeError):
         P.rd_preprocess_bwd_views_ex(views, g, got, flags=8)
     with pytest.raises(P.rade.N.RadeError):
