@@ -352,6 +352,7 @@ struct PassArgs {
   int64_t n_gauss;  // entries of offsets / sorted_ids (RD_CHECKS)
   unsigned long long* status;
   uint32_t epoch;
+  int match;  // rank with __match_any_sync (passes whose digits repeat within a warp)
 };
 
 struct GenSmem {  // kTileGen: the block's Gaussians (≤ 2049: every visible one touches ≥ 1 tile)
@@ -507,16 +508,17 @@ __global__ void __launch_bounds__(kST, RD_SORT_MINB) k_onesweep(PassArgs a) {
 #pragma unroll
   for (int j = 0; j < kSI; ++j) {
     const uint32_t d = (key[j] >> a.shift) & 255u;
-#if RD_RANK_MATCH
-    const unsigned peers = __match_any_sync(0xffffffffu, ok[j] ? d : 256u);
-#else
-    unsigned peers = __ballot_sync(0xffffffffu, ok[j]);
+    unsigned peers;
+    if (RD_RANK_MATCH || a.match) {  // warp-uniform
+      peers = __match_any_sync(0xffffffffu, ok[j] ? d : 256u);
+    } else {
+      peers = __ballot_sync(0xffffffffu, ok[j]);
 #pragma unroll
-    for (int bit = 0; bit < 8; ++bit) {  // m = all ones where this lane's digit has the bit
-      const unsigned m = (unsigned)((int)(d << (31 - bit)) >> 31);
-      peers &= ~(__ballot_sync(0xffffffffu, (int)m < 0) ^ m);
+      for (int bit = 0; bit < 8; ++bit) {  // m = all ones where this lane's digit has the bit
+        const unsigned m = (unsigned)((int)(d << (31 - bit)) >> 31);
+        peers &= ~(__ballot_sync(0xffffffffu, (int)m < 0) ^ m);
+      }
     }
-#endif
     uint32_t c = 0u;
     if (ok[j]) c = sm.pass.cnt[warp][d];
     __syncwarp();
@@ -803,6 +805,11 @@ void launch_depth_pass(int p, const uint32_t* dkey_id_order, int64_t n, const ui
   a.bases = bases + kBaseStride * p;
   a.status = bs.status;
   a.epoch = ++bs.epoch;
+#ifndef RD_MATCH_DEPTH
+#define RD_MATCH_DEPTH 8  // bit p: depth pass p ranks with __match_any_sync (pass 3: the top byte — sign and
+                           // 7 exponent bits — takes few values per warp; 2 and the tile passes: slower)
+#endif
+  a.match = (RD_MATCH_DEPTH >> p) & 1;
   if (p == 0)
     k_onesweep<kDepthFirst><<<blocks_of(n), kST, kSortSmem, s>>>(a);
   else
@@ -847,6 +854,10 @@ void launch_tile_pass(int p, int64_t m, int64_t n_gauss, const uint32_t* offsets
   a.n_gauss = n_gauss;
   a.status = bs.status;
   a.epoch = ++bs.epoch;
+#ifndef RD_MATCH_TILE
+#define RD_MATCH_TILE 0  // bit p: tile pass p ranks with __match_any_sync
+#endif
+  a.match = (RD_MATCH_TILE >> p) & 1;
   if (p == 0)
     k_onesweep<kTileGen><<<blocks_of(m), kST, kSortSmem, s>>>(a);
   else
