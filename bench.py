@@ -899,11 +899,14 @@ def run_gpu(args, cfg_name, config):
 
     # kernel launches (all ours, librade.so): per view K1, K2h, 4 depth passes, scan, the tile
     # passes (the first fused with the duplicate generation), ranges, tile order, K3, K4,
-    # K5b + K5b64; per round of views the batched SH kernel (or K5a per view)
+    # K5b + K5b64 (batched K5: one of each per round, blockIdx.y = view); per round of views
+    # the batched SH kernel (or K5a per view)
     launches_per_view = 1 + 1 + 4 + 1 + tile_passes + 1 + 1 + 1 + 1 + 2
     views_per_rank = args.steps * B
     rounds = args.steps * math.ceil(B / P_)
     launches_total = launches_per_view * views_per_rank + (rounds if args.k5 in ("batched", "split", "set", "split-set") else views_per_rank)
+    if args.k5 in ("batched", "set"):  # the round's geometry parts: one K5b64 + one K5b launch per round
+        launches_total += 2 * rounds - 2 * views_per_rank
     if args.k1 == "batched":  # one K1 per round instead of one per view
         launches_total += rounds - views_per_rank
     M_avg = tim["n_duplicates"] / max(views_timed, 1)

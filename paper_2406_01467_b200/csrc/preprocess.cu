@@ -828,6 +828,41 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd64(DevGauss g, DevCam cam
   if (geometry_backward<double>(g, big[p], cam, opt, g2d, acc)) grad_flush(acc, gr, big[p]);
 }
 
+// The geometry parts of a round of views in one launch each (blockIdx.y = view): no tail and
+// launch gap between the views' kernels. Same per-thread work as k_preprocess_bwd(64).
+struct ViewsGeo {
+  DevCam cam[kMaxBatchViews];
+  const uint32_t* touched[kMaxBatchViews];
+  const uint32_t* list[kMaxBatchViews];  // visible list (K5b) / big list (K5b64)
+  int64_t n[kMaxBatchViews];
+  const G2D* g2d[kMaxBatchViews];
+};
+__global__ void __launch_bounds__(RD_K5_THREADS, RD_K5_MINB) k_preprocess_bwd_geo_views(DevGauss g, DevOpt opt,
+                                                                             const __grid_constant__ ViewsGeo vg,
+                                                                             DevGrads gr) {
+  const int v = (int)blockIdx.y;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < vg.n[v]) {
+    const uint32_t i = vg.list[v][p];
+    const bool big = is_big(vg.touched[v][i], opt.tile);
+    GradAcc acc;
+    grad_zero(acc);
+    if (geometry_backward<float>(g, i, vg.cam[v], opt, vg.g2d[v], acc) && !big) grad_flush(acc, gr, i);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__global__ void __launch_bounds__(128) k_preprocess_bwd64_views(DevGauss g, DevOpt opt, const __grid_constant__ ViewsGeo vg,
+                                                                DevGrads gr) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int v = (int)blockIdx.y;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= vg.n[v]) return;
+  const uint32_t i = vg.list[v][p];
+  GradAcc acc;
+  grad_zero(acc);
+  if (geometry_backward<double>(g, i, vg.cam[v], opt, vg.g2d[v], acc)) grad_flush(acc, gr, i);
+}
+
 // ---------------------------------------------------------------------------- K5, B views
 // rd_preprocess_bwd_views: the views of a step share the Gaussians. The SH part of K5 — the
 // HBM-bound one (per view it read each visible Gaussian's 192-B coefficient row and reduced
@@ -1248,6 +1283,39 @@ void launch_preprocess_bwd_views(const DevGauss& g, const DevOpt& opt, int nv, c
   // geometry per view: its fp64 big list, then the fp32 pass over its visible list as the big
   // list's programmatic dependent (rows are only ever added by reductions)
   if (!(parts & kK5Geometry)) return;
+#ifndef RD_K5_GEO_BATCH
+#define RD_K5_GEO_BATCH 1
+#endif
+  if (RD_K5_GEO_BATCH) {
+    ViewsGeo vb64{}, vbv{};
+    int64_t max_big = 0, max_vis = 0;
+    for (int v = 0; v < nv; ++v) {
+      vb64.cam[v] = vbv.cam[v] = cams[v];
+      vb64.touched[v] = vbv.touched[v] = touched[v];
+      vb64.g2d[v] = vbv.g2d[v] = g2d[v];
+      vb64.list[v] = big[v];
+      vb64.n[v] = n_big[v];
+      vbv.list[v] = vis[v];
+      vbv.n[v] = n_vis[v];
+      max_big = n_big[v] > max_big ? n_big[v] : max_big;
+      max_vis = n_vis[v] > max_vis ? n_vis[v] : max_vis;
+    }
+    if (max_big > 0)
+      k_preprocess_bwd64_views<<<dim3((unsigned)((max_big + 127) / 128), (unsigned)nv), 128, 0, s>>>(g, opt, vb64, grads);
+    if (max_vis > 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)((max_vis + RD_K5_THREADS - 1) / RD_K5_THREADS), (unsigned)nv);
+      cfg.blockDim = dim3(RD_K5_THREADS);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = max_big > 0 ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_preprocess_bwd_geo_views, g, opt, vbv, grads);
+    }
+    return;
+  }
   for (int v = 0; v < nv; ++v) {
     if (n_big[v] > 0)
       k_preprocess_bwd64<<<(unsigned)((n_big[v] + 127) / 128), 128, 0, s>>>(g, cams[v], opt, big[v], n_big[v], g2d[v],
