@@ -74,8 +74,11 @@ if os.path.exists(rp):
         for pre, b, k in (("k_render_bwd", "render_bwd", 1), ("k_render_fwd", "render_fwd", 1),
                           ("k_preprocess_fwd", "preprocess_fwd", 1),
                           # bench's K5 launch = one rd_preprocess_bwd_views per round of 4 views:
-                          # the batched SH kernel once, K5b64 + K5b per view
-                          ("k_preprocess_bwd_sh", "preprocess_bwd", 1), ("k_preprocess_bwd", "preprocess_bwd", 4),
+                          # the batched SH kernel once, the batched K5b64 + K5b once (blockIdx.y =
+                          # view; per-view K5b64 + K5b four times in older captures)
+                          ("k_preprocess_bwd_sh", "preprocess_bwd", 1),
+                          ("k_preprocess_bwd_geo_views", "preprocess_bwd", 1),
+                          ("k_preprocess_bwd64_views", "preprocess_bwd", 1), ("k_preprocess_bwd", "preprocess_bwd", 4),
                           ("k_bin_hist", "depth_sort", 1), ("k_onesweep<0>", "depth_sort", 1),
                           ("k_onesweep<1>", "depth_sort", 3), ("k_scan", "scan", 1),
                           ("k_onesweep<2>", "duplicate", 1), ("k_onesweep<3>", "tile_sort", 1),
