@@ -502,9 +502,10 @@ __global__ void __launch_bounds__(TILE* TILE / 2) k_render_fwd(DevCam cam, DevOp
 // row k's two halves as four float4 each, and one xor-1 shuffle completes the sum. Lanes 2k
 // and 2k+1 return Σ_lanes v[k]; ≈ NV + 22 instructions against ≈ 5·NV for a shuffle butterfly.
 // K4: when at most this many lanes hold contributions for a splat, each adds its own sums with
-// atomics instead of the warp reduction (measured 1 → 5: K4 −2.5%; 8+: L2 contention)
+// atomics instead of the warp reduction (round 1: 1 → 5 K4 −2.5%, 8+: L2 contention; re-tuned
+// after the packed reduction made the reduction cheaper: 5 → 4 K4 0.379 → 0.377 ms, 6 slower)
 #ifndef RD_K4_DIRECT
-#define RD_K4_DIRECT 5
+#define RD_K4_DIRECT 4
 #endif
 constexpr int kDirectLanes = RD_K4_DIRECT;
 #ifndef RD_REDUCE_PACKED
