@@ -236,10 +236,20 @@ __device__ __forceinline__ unsigned blend_mask_word(unsigned rx, int pos, int ti
 // Launch order of the tiles for K3/K4: longest lists first (log2 buckets), so the heavy tiles
 // — clustered where the scene is — do not start last and leave a tail. One block; the order
 // within a bucket is arbitrary (a tile's outputs do not depend on when it runs).
+#ifndef RD_ORDER_SUB
+#define RD_ORDER_SUB 1  // buckets of 2^-SUB octave of list length (the SUB bits below the leading one)
+#endif
+constexpr int kNB = 32 << RD_ORDER_SUB;  // buckets (bucket 0 = the longest lists)
+__device__ __forceinline__ int tile_bucket(uint32_t len) {
+  const int lg = len ? 31 - __clz((int)len) : -1;  // floor(log2 len)
+  const int sub = lg >= RD_ORDER_SUB ? (int)((len >> (lg - RD_ORDER_SUB)) & ((1u << RD_ORDER_SUB) - 1u))
+                                     : (lg > 0 ? (int)((len << (RD_ORDER_SUB - lg)) & ((1u << RD_ORDER_SUB) - 1u)) : 0);
+  return (kNB - 1) - min(kNB - 1, ((lg + 1) << RD_ORDER_SUB) + sub);
+}
 __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int n_tiles,
                                                      uint32_t* __restrict__ order) {
-  __shared__ uint32_t cnt[32], off[32];
-  if (threadIdx.x < 32) cnt[threadIdx.x] = 0u;
+  __shared__ uint32_t cnt[kNB], off[kNB];
+  if (threadIdx.x < kNB) cnt[threadIdx.x] = 0u;
   const unsigned lane = threadIdx.x & 31u, below = (1u << lane) - 1u;
   // thread t owns tiles t, t + 1024, ...: their buckets are computed once, up to kPer of them
   // with all range loads in flight together (one block: the kernel is a chain of dependent
@@ -260,15 +270,15 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
     for (int k = 0; k < kPer; ++k) {
       const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
       if (r0 + k >= rounds) break;  // block-uniform
-      const int b = t < n_tiles ? 31 - min(31, 32 - __clz((int)(rg[k].y - rg[k].x))) : 32;  // longer → smaller
+      const int b = t < n_tiles ? tile_bucket(rg[k].y - rg[k].x) : kNB;  // longer → smaller
       const unsigned peers = __match_any_sync(0xffffffffu, b);
-      if (b < 32 && (peers & below) == 0u) atomicAdd(&cnt[b], (unsigned)__popc(peers));
+      if (b < kNB && (peers & below) == 0u) atomicAdd(&cnt[b], (unsigned)__popc(peers));
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t a = 0u;
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       off[b] = a;
       a += cnt[b];
     }
@@ -285,13 +295,13 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
     for (int k = 0; k < kPer; ++k) {
       const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
       if (r0 + k >= rounds) break;
-      const int b = t < n_tiles ? 31 - min(31, 32 - __clz((int)(rg[k].y - rg[k].x))) : 32;
+      const int b = t < n_tiles ? tile_bucket(rg[k].y - rg[k].x) : kNB;
       const unsigned peers = __match_any_sync(0xffffffffu, b);
       const int leader = __ffs(peers) - 1;
       uint32_t base = 0u;
-      if (b < 32 && (int)lane == leader) base = atomicAdd(&off[b], (unsigned)__popc(peers));
+      if (b < kNB && (int)lane == leader) base = atomicAdd(&off[b], (unsigned)__popc(peers));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (b < 32) order[base + (uint32_t)__popc(peers & below)] = (uint32_t)t;
+      if (b < kNB) order[base + (uint32_t)__popc(peers & below)] = (uint32_t)t;
     }
   }
 }
