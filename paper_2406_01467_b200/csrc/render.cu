@@ -237,7 +237,7 @@ __device__ __forceinline__ unsigned blend_mask_word(unsigned rx, int pos, int ti
 // — clustered where the scene is — do not start last and leave a tail. One block; the order
 // within a bucket is arbitrary (a tile's outputs do not depend on when it runs).
 #ifndef RD_ORDER_SUB
-#define RD_ORDER_SUB 1  // buckets of 2^-SUB octave of list length (the SUB bits below the leading one)
+#define RD_ORDER_SUB 2  // buckets of 2^-SUB octave of list length (the SUB bits below the leading one)
 #endif
 constexpr int kNB = 32 << RD_ORDER_SUB;  // buckets (bucket 0 = the longest lists)
 __device__ __forceinline__ int tile_bucket(uint32_t len) {
@@ -271,6 +271,14 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
       const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
       if (r0 + k >= rounds) break;  // block-uniform
       const int b = t < n_tiles ? tile_bucket(rg[k].y - rg[k].x) : kNB;  // longer → smaller
+#ifndef RD_ORDER_ATOMIC
+#define RD_ORDER_ATOMIC 1  // one plain shared atomic per tile (0: __match_any grouping; with 128 buckets
+                           // the contention is low and the plain atomics are cheaper)
+#endif
+      if (RD_ORDER_ATOMIC) {
+        if (b < kNB) atomicAdd(&cnt[b], 1u);
+        continue;
+      }
       const unsigned peers = __match_any_sync(0xffffffffu, b);
       if (b < kNB && (peers & below) == 0u) atomicAdd(&cnt[b], (unsigned)__popc(peers));
     }
@@ -296,6 +304,10 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
       const int t = (r0 + k) * (int)blockDim.x + (int)threadIdx.x;
       if (r0 + k >= rounds) break;
       const int b = t < n_tiles ? tile_bucket(rg[k].y - rg[k].x) : kNB;
+      if (RD_ORDER_ATOMIC) {
+        if (b < kNB) order[atomicAdd(&off[b], 1u)] = (uint32_t)t;
+        continue;
+      }
       const unsigned peers = __match_any_sync(0xffffffffu, b);
       const int leader = __ffs(peers) - 1;
       uint32_t base = 0u;
